@@ -1,0 +1,165 @@
+/* slq.h -- C-ABI of the B200-native SLQ / FD-HVP library (libslq.so).
+ *
+ * The one hot path of arXiv 2602.00816 ("Hessian Spectral Analysis at Foundation Model Scale"):
+ * stochastic Lanczos quadrature driven by shard-local central finite-difference Hessian-vector
+ * products, with theta and every P-vector partitioned FSDP-style.  Citations are PAPER.md line
+ * numbers (P:n) with their section / equation / algorithm; S:n are SPEC.md lines.
+ *
+ * Conventions (all entry points)
+ *   - Every call returns slq_status; SLQ_OK == 0.  On error, slq_last_error(ctx) (or
+ *     slq_last_error(NULL) for calls without a context) returns a NUL-terminated message that
+ *     stays valid until the next call on the same context/thread.
+ *   - "collective" calls must be made by every rank of the world, in the same order, with the
+ *     same scalar arguments.  With world_size == 1 no communicator is created.
+ *   - Shard pointers (v_shard, out_shard, g_shard) hold P_loc = slq_local_len(ctx) fp32 values in
+ *     the library's FSDP layout (below).  They may be DEVICE pointers on the context's device
+ *     (zero-copy, stream-ordered) or HOST pointers (copied in/out inside the call).  The caller
+ *     owns them; the library never retains a caller pointer after the call returns.
+ *   - Calls are synchronous on return (the library's stream is synchronised before returning).
+ *   - A context is bound to one process/GPU and is not thread-safe.
+ *
+ * FSDP layout ("perturbations ... applied to each rank's local DTensor shard";
+ * SURVEY.md §8(a) A0, §8(e)).  Parameters are in canonical order (layer-major; see DESIGN.md
+ * "Canonical parameter order").  They are grouped into FSDP units: MLP = 1 unit; GPT/Llama =
+ * [embedding], [block 0] ... [block L-1], [final norm (+ head)].  Unit u has numel_u real
+ * parameters, padded to padded_u = roundup(numel_u, 16*world_size); rank r owns the chunk
+ * [r*chunk_u, (r+1)*chunk_u) with chunk_u = padded_u / world_size.  The local shard is the
+ * concatenation of the rank's chunks of all units, P_loc = sum_u chunk_u.  Padding entries are
+ * zero on input and are returned as zero.  No full-length vector is ever gathered
+ * (P:112).
+ */
+#ifndef SLQ_H_
+#define SLQ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct slq_ctx slq_ctx; /* opaque; one per process/GPU */
+
+typedef enum {
+  SLQ_OK = 0,
+  SLQ_EINVAL = 2,       /* bad descriptor / shape / layout / argument (SPEC exit code 2) */
+  SLQ_ENUMERIC = 3,     /* non-finite loss or gradient; see slq_lanczos_info */
+  SLQ_ECUDA = 4,        /* CUDA runtime error, or the CUDA kernels are unavailable */
+  SLQ_ENCCL = 5,        /* NCCL error (including a peer abort) */
+  SLQ_ETIMEOUT = 6,     /* collective watchdog expired */
+  SLQ_ENOMEM = 7,       /* device allocation failed */
+  SLQ_EUNSUPPORTED = 8  /* valid request this build does not implement */
+} slq_status;
+
+enum { SLQ_ARCH_MLP = 0, SLQ_ARCH_GPT = 1, SLQ_ARCH_LLAMA = 2 };
+/* arithmetic of the two gradient passes.  FP64: fp64 activations/accumulation on the GPU
+ * (the parity mode of the fp32 models); FP32: fp32 passes (reported only). */
+enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1 };
+enum { SLQ_REORTH_NONE = 0, SLQ_REORTH_FULL = 1 };
+enum { SLQ_PARAM_FP32 = 0, SLQ_PARAM_BF16 = 1 };
+
+/* Model + numerics description.  Fields unused by an arch are ignored (set them to 0). */
+typedef struct {
+  int32_t arch;            /* SLQ_ARCH_* */
+  int32_t n_layers, d_model, n_heads, n_kv_heads, d_ff, vocab, seq_len; /* GPT / Llama */
+  int32_t d_in, d_hidden, n_classes;                                    /* MLP */
+  int32_t tie_embeddings;  /* 1: output head reuses the token embedding (GPT-2 style) */
+  double rope_theta;       /* Llama RoPE base */
+  double norm_eps;         /* LayerNorm / RMSNorm epsilon */
+  int32_t param_dtype;     /* SLQ_PARAM_*: storage dtype of theta (bf16 values are held in fp32) */
+  int32_t pass_numerics;   /* SLQ_PASS_* */
+  int32_t reorth;          /* SLQ_REORTH_*: Lanczos reorthogonalisation */
+  int32_t max_steps;       /* largest m slq_lanczos will be asked for (sizes the Krylov basis) */
+  double eps_default;      /* FD step used by slq_lanczos (the north-star signature has no eps) */
+} slq_model_desc;
+
+/* This rank's slice of the data (Alg. 1 "dataloader").  The loss is the mean token
+ * cross-entropy over the GLOBAL batch (sum of w_b = 1), so every rank passes the global
+ * count.  The library copies what it needs; pointers are host memory, not retained. */
+typedef struct {
+  const float* params_host;  /* FULL canonical-order theta_0, fp32, P values (every rank) */
+  const int32_t* tokens;     /* GPT/Llama: [n_seq_local][seq_len + 1] token ids */
+  int32_t n_seq_local, n_seq_global;
+  const float* x;            /* MLP: [n_rows_local][d_in] inputs */
+  const int32_t* y;          /* MLP: [n_rows_local] labels */
+  int32_t n_rows_local, n_rows_global;
+} slq_batch;
+
+typedef struct {
+  int32_t rank, world_size, device;
+  const void* nccl_unique_id; /* 128 bytes from slq_nccl_unique_id() on rank 0, broadcast by the
+                                 caller; ignored when world_size == 1 */
+  void* cuda_stream;          /* cudaStream_t to run on, or NULL for a library-owned stream */
+} slq_world;
+
+/* Create a context: validate, plan the FSDP layout, create the NCCL communicator (world > 1),
+ * allocate device state, upload this rank's chunks of theta_0 and its data slice.  Collective. */
+slq_status slq_init(const slq_model_desc* desc, const slq_batch* batch, const slq_world* world,
+                    slq_ctx** out);
+slq_status slq_destroy(slq_ctx* ctx);
+const char* slq_last_error(const slq_ctx* ctx);
+
+int64_t slq_local_len(const slq_ctx* ctx);   /* P_loc (padded, this rank) */
+int64_t slq_global_len(const slq_ctx* ctx);  /* P (real parameters) */
+int32_t slq_num_units(const slq_ctx* ctx);
+/* unit u: global canonical offset, real numel, this rank's local offset and chunk length */
+slq_status slq_unit_info(const slq_ctx* ctx, int32_t u, int64_t* global_offset, int64_t* numel,
+                         int64_t* local_offset, int64_t* chunk);
+
+/* Host-only layout planner (no GPU, no context): the same plan slq_init makes.  unit_table gets
+ * 4 int64 per unit {global_offset, numel, local_offset, chunk}; pass NULL to query n_units. */
+slq_status slq_plan_layout(const slq_model_desc* desc, int32_t world_size, int64_t* P,
+                           int64_t* P_loc, int32_t* n_units, int64_t* unit_table);
+
+/* 128-byte NCCL unique id for slq_world.nccl_unique_id (call on rank 0 only). */
+slq_status slq_nccl_unique_id(void* out128);
+
+/* Hv for a caller direction: out = ||v|| (grad L(theta + eps vhat) - grad L(theta - eps vhat))/(2 eps)
+ * (Eq. (1); Alg. 1).  Implemented as a step eta = fl32(eps/||v||) along v:
+ * theta+- = fmaf(+-eta, v, theta) out of place in fp32 (theta is never written, so it is
+ * bit-identical afterwards), two gradient passes, out = (g+ - g-)/(2 eta).  ||v|| costs the
+ * one scalar all-reduce P:197 allows.  v == 0 returns 0.  v_shard/out_shard must not alias.
+ * Collective. */
+slq_status slq_hvp(slq_ctx* ctx, const float* v_shard, float* out_shard, double eps);
+
+/* One gradient evaluation = the paper's T_grad (one forward + one backward with all
+ * FSDP collectives, no optimiser).  g_shard may be NULL (timing); loss may be NULL.  Collective. */
+slq_status slq_grad(slq_ctx* ctx, float* g_shard, double* loss);
+
+/* m steps of Lanczos (App. C) on the FD-HVP operator with step
+ * eps_default, from the Rademacher probe q_1[i] = s(probe_seed, gid(i))/sqrt(P) (integer
+ * splitmix64 hash).  alpha[m] and beta[m-1] (= beta_2..beta_m) are host
+ * arrays.  Breakdown (beta_{k+1} <= tol * max|T|) returns SLQ_OK with the unfilled entries NaN;
+ * see slq_lanczos_info.  Collective. */
+slq_status slq_lanczos(slq_ctx* ctx, uint64_t probe_seed, int32_t m, double* alpha, double* beta);
+slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_next,
+                            int32_t* nonfinite);
+
+/* Gauss quadrature of T_m (host only, no context, pure): nodes ascending (Ritz values) and
+ * weights = squared first components of the normalised eigenvectors (sum 1).
+ * beta may be NULL when m == 1.  Implicit-shift QL (Golub-Welsch). */
+slq_status slq_quadrature(const double* alpha, const double* beta, int32_t m, double* nodes,
+                          double* weights);
+
+/* Writes the Lanczos start vector q_1 (probe) for probe_seed into a caller shard (device or host).
+ * Exposed so the probe can be checked bit-exactly against an independent generator. */
+slq_status slq_probe(slq_ctx* ctx, uint64_t probe_seed, float* q_shard);
+
+/* Per-kernel-class timing with CUDA events recorded on the library stream around every launch
+ * (off by default).  classes: see slq_kernel_class_name.  Stats accumulate until reset. */
+slq_status slq_profile(slq_ctx* ctx, int32_t enable, int32_t reset);
+int32_t slq_num_kernel_classes(void);
+const char* slq_kernel_class_name(int32_t cls);
+slq_status slq_kernel_stats(const slq_ctx* ctx, int32_t cls, double* total_ms, int64_t* launches,
+                            double* flops, double* bytes);
+/* NCCL collectives issued since the context was created (collective audit):
+ * all-gathers, reduce-scatters, all-reduces.  All zero when world_size == 1. */
+slq_status slq_collective_counts(const slq_ctx* ctx, int64_t* allgather, int64_t* reduce_scatter,
+                                 int64_t* allreduce);
+/* total kernel launches issued by the library since the context was created */
+int64_t slq_launch_count(const slq_ctx* ctx);
+void* slq_stream(const slq_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLQ_H_ */

@@ -1,0 +1,395 @@
+// C-ABI of libslq.so (include/slq.h): argument checking, context lifetime, host/device buffer
+// marshalling, the per-kernel-class CUDA-event profiler.  No torch types cross this boundary.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "common.h"
+#include "engine.h"
+#include "kernels.h"
+#include "layout.h"
+
+namespace slq {
+void tridiag_gauss(const double* alpha, const double* beta, int m, double* nodes, double* weights);
+
+const char* kernel_class_name(int c) {
+  static const char* names[KC_COUNT] = {"gemm", "attention", "norm", "cross_entropy", "embedding",
+                                        "elementwise", "perturb", "fd_lanczos", "reorth", "vector"};
+  return (c >= 0 && c < KC_COUNT) ? names[c] : "?";
+}
+
+struct Profiler {
+  bool on = false;
+  struct Rec {
+    cudaEvent_t a, b;
+    int cls;
+    double flops, bytes;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t open = nullptr;
+  double ms[KC_COUNT] = {}, flops[KC_COUNT] = {}, bytes[KC_COUNT] = {};
+  int64_t count[KC_COUNT] = {};
+  cudaEvent_t take() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void flush() {
+    for (Rec& r : pending) {
+      cudaEventSynchronize(r.b);
+      float t = 0;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      ms[r.cls] += t;
+      flops[r.cls] += r.flops;
+      bytes[r.cls] += r.bytes;
+      count[r.cls]++;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+  void reset() {
+    flush();
+    for (int i = 0; i < KC_COUNT; ++i) ms[i] = flops[i] = bytes[i] = 0, count[i] = 0;
+  }
+  ~Profiler() {
+    flush();
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+void prof_begin(Profiler* p, int, cudaStream_t s) {
+  if (!p || !p->on) return;
+  p->open = p->take();
+  cudaEventRecord(p->open, s);
+}
+void prof_end(Profiler* p, int cls, cudaStream_t s, double flops, double bytes) {
+  if (!p || !p->on || !p->open) return;
+  cudaEvent_t e = p->take();
+  cudaEventRecord(e, s);
+  p->pending.push_back({p->open, e, cls, flops, bytes});
+  p->open = nullptr;
+  if (p->pending.size() > 200000) p->flush();
+}
+
+void* Workspace::get(size_t need, cudaStream_t s) {
+  if (need <= bytes) return ptr;
+  if (ptr) {
+    SLQ_CUDA(cudaStreamSynchronize(s));
+    SLQ_CUDA(cudaFree(ptr));
+    ptr = nullptr;
+    bytes = 0;
+  }
+  const size_t nb = need + need / 4 + 4096;
+  SLQ_CUDA(cudaMalloc(&ptr, nb));
+  bytes = nb;
+  return ptr;
+}
+Workspace::~Workspace() {
+  if (ptr) cudaFree(ptr);
+}
+
+}  // namespace slq
+
+using namespace slq;
+
+struct slq_ctx {
+  slq_model_desc desc;
+  slq_world world;
+  LayoutPlan plan;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::unique_ptr<Comm> comm;
+  Profiler prof;
+  Workspace ws;
+  int64_t launches = 0;
+  std::unique_ptr<Engine> engine;
+  std::string err;
+  float* stage_in = nullptr;  // device staging for host-pointer calls
+  float* stage_out = nullptr;
+  Launch launch() { return Launch{stream, &prof, &ws, &launches}; }
+  ~slq_ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    engine.reset();
+    if (stage_in) cudaFree(stage_in);
+    if (stage_out) cudaFree(stage_out);
+    comm.reset();
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+thread_local std::string g_err;
+
+slq_status fail(slq_ctx* ctx, slq_status s, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  g_err = msg;
+  return s;
+}
+
+template <class F>
+slq_status guarded(slq_ctx* ctx, F&& f) {
+  try {
+    f();
+    return SLQ_OK;
+  } catch (const Error& e) {
+    return fail(ctx, e.status, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, SLQ_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, SLQ_ECUDA, e.what());
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void check_device(slq_ctx* ctx) { SLQ_CUDA(cudaSetDevice(ctx->world.device)); }
+
+void ensure_stage(slq_ctx* ctx) {
+  if (!ctx->stage_in) {
+    SLQ_CUDA(cudaMalloc(&ctx->stage_in, sizeof(float) * (size_t)ctx->plan.P_loc));
+    SLQ_CUDA(cudaMalloc(&ctx->stage_out, sizeof(float) * (size_t)ctx->plan.P_loc));
+  }
+}
+
+// float4 paths need 16-byte aligned shards; stage misaligned device pointers
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+}  // namespace
+
+extern "C" {
+
+const char* slq_last_error(const slq_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+slq_status slq_plan_layout(const slq_model_desc* desc, int32_t world, int64_t* P, int64_t* P_loc, int32_t* n_units,
+                           int64_t* table) {
+  return guarded(nullptr, [&] {
+    SLQ_CHECK_ARG(desc != nullptr, "desc");
+    LayoutPlan p = plan_layout(*desc, world);
+    if (P) *P = p.P;
+    if (P_loc) *P_loc = p.P_loc;
+    if (n_units) *n_units = (int32_t)p.units.size();
+    if (table)
+      for (size_t u = 0; u < p.units.size(); ++u) {
+        table[4 * u + 0] = p.units[u].global_offset;
+        table[4 * u + 1] = p.units[u].numel;
+        table[4 * u + 2] = p.units[u].local_offset;
+        table[4 * u + 3] = p.units[u].chunk;
+      }
+  });
+}
+
+slq_status slq_nccl_unique_id(void* out128) {
+  return guarded(nullptr, [&] {
+    SLQ_CHECK_ARG(out128 != nullptr, "out");
+    nccl_unique_id(out128);
+  });
+}
+
+slq_status slq_init(const slq_model_desc* desc, const slq_batch* batch, const slq_world* world, slq_ctx** out) {
+  if (out) *out = nullptr;
+  std::unique_ptr<slq_ctx> ctx(new slq_ctx());
+  slq_status st = guarded(nullptr, [&] {
+    SLQ_CHECK_ARG(desc && batch && world && out, "null argument");
+    SLQ_CHECK_ARG(world->world_size >= 1 && world->rank >= 0 && world->rank < world->world_size, "rank/world");
+    ctx->desc = *desc;
+    ctx->world = *world;
+    ctx->plan = plan_layout(*desc, world->world_size);
+    SLQ_CHECK_ARG(batch->params_host != nullptr, "params_host");
+    HostBatch hb;
+    if (desc->arch == SLQ_ARCH_MLP) {
+      SLQ_CHECK_ARG(batch->n_rows_local >= 1 && batch->n_rows_global >= batch->n_rows_local, "n_rows");
+      SLQ_CHECK_ARG(batch->x && batch->y, "x / y");
+      hb.n_rows = batch->n_rows_local;
+      hb.n_rows_global = batch->n_rows_global;
+      hb.x.assign(batch->x, batch->x + (size_t)hb.n_rows * desc->d_in);
+      hb.y.assign(batch->y, batch->y + hb.n_rows);
+      for (int32_t v : hb.y) SLQ_CHECK_ARG(v >= 0 && v < desc->n_classes, "label out of range");
+    } else {
+      SLQ_CHECK_ARG(batch->n_seq_local >= 1 && batch->n_seq_global >= batch->n_seq_local, "n_seq");
+      SLQ_CHECK_ARG(batch->tokens, "tokens");
+      hb.n_seq = batch->n_seq_local;
+      hb.n_seq_global = batch->n_seq_global;
+      hb.tokens.assign(batch->tokens, batch->tokens + (size_t)hb.n_seq * (desc->seq_len + 1));
+      for (int32_t v : hb.tokens) SLQ_CHECK_ARG(v >= 0 && v < desc->vocab, "token id out of range");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(SLQ_ECUDA, "no CUDA device: the CUDA path is required (no CPU fallback exists)");
+    SLQ_CHECK_ARG(world->device >= 0 && world->device < ndev, "device");
+    check_device(ctx.get());
+    if (world->cuda_stream) {
+      ctx->stream = (cudaStream_t)world->cuda_stream;
+    } else {
+      SLQ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+    if (world->world_size > 1)
+      ctx->comm.reset(new Comm(world->nccl_unique_id, world->rank, world->world_size, world->device));
+    ctx->engine = make_engine(*desc, ctx->plan, hb, batch->params_host, world->rank, ctx->comm.get(),
+                              ctx->launch());
+  });
+  if (st == SLQ_OK) *out = ctx.release();
+  return st;
+}
+
+slq_status slq_destroy(slq_ctx* ctx) {
+  delete ctx;
+  return SLQ_OK;
+}
+
+int64_t slq_local_len(const slq_ctx* ctx) { return ctx ? ctx->plan.P_loc : -1; }
+int64_t slq_global_len(const slq_ctx* ctx) { return ctx ? ctx->plan.P : -1; }
+int32_t slq_num_units(const slq_ctx* ctx) { return ctx ? (int32_t)ctx->plan.units.size() : -1; }
+
+slq_status slq_unit_info(const slq_ctx* ctx, int32_t u, int64_t* g, int64_t* numel, int64_t* l, int64_t* chunk) {
+  if (!ctx || u < 0 || u >= (int32_t)ctx->plan.units.size()) return fail(nullptr, SLQ_EINVAL, "unit index");
+  const UnitPlan& p = ctx->plan.units[u];
+  if (g) *g = p.global_offset;
+  if (numel) *numel = p.numel;
+  if (l) *l = p.local_offset;
+  if (chunk) *chunk = p.chunk;
+  return SLQ_OK;
+}
+
+slq_status slq_hvp(slq_ctx* ctx, const float* v, float* out, double eps) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    SLQ_CHECK_ARG(v && out, "null v/out");
+    SLQ_CHECK_ARG(eps > 0, "eps > 0");
+    SLQ_CHECK_ARG(v != out, "v and out must not alias");
+    check_device(ctx);
+    const size_t bytes = sizeof(float) * (size_t)ctx->plan.P_loc;
+    const bool vdev = is_device_ptr(v), odev = is_device_ptr(out);
+    const float* vd = v;
+    float* od = out;
+    if (!vdev || !aligned16(v)) {
+      ensure_stage(ctx);
+      SLQ_CUDA(cudaMemcpyAsync(ctx->stage_in, v, bytes, vdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               ctx->stream));
+      vd = ctx->stage_in;
+    }
+    if (!odev) {
+      ensure_stage(ctx);
+      od = ctx->stage_out;
+    }
+    ctx->engine->hvp(vd, od, eps);
+    if (!odev) {
+      SLQ_CUDA(cudaMemcpyAsync(out, od, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      SLQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  });
+}
+
+slq_status slq_grad(slq_ctx* ctx, float* g, double* loss) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    check_device(ctx);
+    const size_t bytes = sizeof(float) * (size_t)ctx->plan.P_loc;
+    const bool gdev = g ? is_device_ptr(g) : true;
+    float* gd = g;
+    if (g && !gdev) {
+      ensure_stage(ctx);
+      gd = ctx->stage_out;
+    }
+    const double l = ctx->engine->grad(gd);
+    if (g && !gdev) {
+      SLQ_CUDA(cudaMemcpyAsync(g, gd, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      SLQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    if (loss) *loss = l;
+  });
+}
+
+slq_status slq_lanczos(slq_ctx* ctx, uint64_t seed, int32_t m, double* alpha, double* beta) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    SLQ_CHECK_ARG(alpha != nullptr && (m == 1 || beta != nullptr), "alpha / beta");
+    check_device(ctx);
+    std::vector<double> b(std::max(m - 1, 1));
+    ctx->engine->lanczos(seed, m, alpha, b.data());
+    for (int i = 0; i + 1 < m; ++i) beta[i] = b[i];
+  });
+}
+
+slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_next, int32_t* nonfinite) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  const LanczosInfo& i = ctx->engine->last_info;
+  if (m_done) *m_done = i.m_done;
+  if (beta_next) *beta_next = i.beta_next;
+  if (nonfinite) *nonfinite = i.nonfinite;
+  return SLQ_OK;
+}
+
+slq_status slq_quadrature(const double* alpha, const double* beta, int32_t m, double* nodes, double* weights) {
+  return guarded(nullptr, [&] { tridiag_gauss(alpha, beta, m, nodes, weights); });
+}
+
+slq_status slq_probe(slq_ctx* ctx, uint64_t seed, float* q) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    SLQ_CHECK_ARG(q != nullptr, "q");
+    check_device(ctx);
+    if (is_device_ptr(q)) {
+      ctx->engine->probe(seed, q);
+    } else {
+      ensure_stage(ctx);
+      ctx->engine->probe(seed, ctx->stage_out);
+      SLQ_CUDA(cudaMemcpy(q, ctx->stage_out, sizeof(float) * (size_t)ctx->plan.P_loc, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+slq_status slq_profile(slq_ctx* ctx, int32_t enable, int32_t reset) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    if (reset) ctx->prof.reset();
+    ctx->prof.on = enable != 0;
+  });
+}
+
+int32_t slq_num_kernel_classes(void) { return KC_COUNT; }
+const char* slq_kernel_class_name(int32_t c) { return kernel_class_name(c); }
+
+slq_status slq_kernel_stats(const slq_ctx* ctx, int32_t cls, double* ms, int64_t* launches, double* flops,
+                            double* bytes) {
+  if (!ctx || cls < 0 || cls >= KC_COUNT) return fail(nullptr, SLQ_EINVAL, "ctx / class");
+  slq_ctx* c = const_cast<slq_ctx*>(ctx);
+  c->prof.flush();
+  if (ms) *ms = c->prof.ms[cls];
+  if (launches) *launches = c->prof.count[cls];
+  if (flops) *flops = c->prof.flops[cls];
+  if (bytes) *bytes = c->prof.bytes[cls];
+  return SLQ_OK;
+}
+
+int64_t slq_launch_count(const slq_ctx* ctx) { return ctx ? ctx->launches : -1; }
+void* slq_stream(const slq_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+slq_status slq_collective_counts(const slq_ctx* ctx, int64_t* ag, int64_t* rs, int64_t* ar) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  CommCounts c;
+  if (ctx->comm) c = ctx->comm->counts;
+  if (ag) *ag = c.allgather;
+  if (rs) *rs = c.reduce_scatter;
+  if (ar) *ar = c.allreduce;
+  return SLQ_OK;
+}
+
+}  // extern "C"

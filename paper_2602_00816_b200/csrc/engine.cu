@@ -1,0 +1,296 @@
+// FD-HVP (Eq. (1), Alg. 1) and Lanczos (§4, App. C) orchestration on device-resident shards.
+//
+// Per HVP (done out of place):  theta+- = fmaf(+-eta, v, theta)  ->  pass(theta+) ->
+// g+ ; pass(theta-) -> g- ; out = (g+ - g-)/(2 eta).  theta is never written.
+// Per Lanczos step (P:307-311 in A(2,7) order; reading SURVEY §8(c2) #2, #5):
+//   w = H q_k - beta_k q_{k-1};  alpha_k = <w, q_k>;  w -= alpha_k q_k;
+//   [full: CGS over q_1..q_k, twice];  beta_{k+1} = ||w||;  q_{k+1} = w / beta_{k+1}
+// All dot products are fp64 partials reduced in a fixed order, then (R > 1) one small fp64
+// all-reduce.  Vectors are fp32 shards in the FSDP layout.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "engine.h"
+
+namespace slq {
+
+namespace {
+
+template <class T>
+struct LocalIO : PassIO<T> {
+  const LayoutPlan* plan;
+  const T* shard = nullptr;
+  T* gshard = nullptr;
+  const T* params(int u) override { return shard + plan->units[u].local_offset; }
+  T* grads(int u) override { return gshard + plan->units[u].local_offset; }
+  void grads_done(int) override {}
+};
+
+// ZeRO-3: gather a unit's parameters before its forward and again before its backward; reduce-
+// scatter its gradient after its backward.  Unit 0 (embedding) has its own
+// parameter and gradient buffers so it can stay live with any other unit (tied head).
+template <class T>
+struct FsdpIO : PassIO<T> {
+  const LayoutPlan* plan;
+  Comm* comm;
+  cudaStream_t s;
+  const T* shard = nullptr;
+  T* gshard = nullptr;
+  T *pbuf0, *pbuf1, *gbuf0, *gbuf1;
+  CommType ct() const { return sizeof(T) == 8 ? COMM_F64 : COMM_F32; }
+  const T* params(int u) override {
+    const UnitPlan& up = plan->units[u];
+    T* dst = u == 0 ? pbuf0 : pbuf1;
+    comm->allgather(shard + up.local_offset, dst, (size_t)up.chunk, ct(), s);
+    return dst;
+  }
+  T* grads(int u) override { return u == 0 ? gbuf0 : gbuf1; }
+  void grads_done(int u) override {
+    const UnitPlan& up = plan->units[u];
+    T* g = u == 0 ? gbuf0 : gbuf1;
+    if (up.padded > up.numel)
+      SLQ_CUDA(cudaMemsetAsync(g + up.numel, 0, sizeof(T) * (size_t)(up.padded - up.numel), s));
+    comm->reduce_scatter(g, gshard + up.local_offset, (size_t)up.chunk, ct(), s);
+  }
+};
+
+template <class T>
+struct EngineT : Engine {
+  slq_model_desc d;
+  const LayoutPlan& plan;
+  Launch L;
+  Comm* comm;
+  int rank;
+  int64_t n;  // P_loc
+  std::vector<void*> allocs;
+  float* theta;
+  T *thp, *thm, *gp, *gm;
+  float *basis = nullptr, *w = nullptr, *vq[3] = {nullptr, nullptr, nullptr};
+  double* dscal;      // [0] sumsq, [1] beta_k, [2] loss, [3..] alpha / reorth coefficients
+  double* partials;
+  int* dflag;
+  UnitDev* units_dev;
+  int max_steps;
+  std::unique_ptr<Runner<T>> runner;
+  LocalIO<T> lio;
+  FsdpIO<T> fio;
+  double* hstage;  // pinned host scalars
+
+  template <class U>
+  U* dalloc(int64_t cnt) {
+    void* p = nullptr;
+    SLQ_CUDA(cudaMalloc(&p, sizeof(U) * (size_t)std::max<int64_t>(cnt, 1)));
+    allocs.push_back(p);
+    return (U*)p;
+  }
+
+  EngineT(const slq_model_desc& d_, const LayoutPlan& plan_, const HostBatch& b, const float* theta_host, int rank_,
+          Comm* comm_, const Launch& L_)
+      : d(d_), plan(plan_), L(L_), comm(comm_), rank(rank_) {
+    n = plan.P_loc;
+    max_steps = d.max_steps;
+    theta = dalloc<float>(n);
+    {  // this rank's chunk of every unit; padding zero
+      std::vector<float> h((size_t)n, 0.0f);
+      for (const UnitPlan& u : plan.units) {
+        const int64_t start = (int64_t)rank * u.chunk;
+        for (int64_t j = 0; j < u.chunk; ++j) {
+          const int64_t p = start + j;
+          if (p < u.numel) h[(size_t)(u.local_offset + j)] = theta_host[u.global_offset + p];
+        }
+      }
+      SLQ_CUDA(cudaMemcpy(theta, h.data(), sizeof(float) * (size_t)n, cudaMemcpyHostToDevice));
+    }
+    thp = dalloc<T>(n); thm = dalloc<T>(n); gp = dalloc<T>(n); gm = dalloc<T>(n);
+    SLQ_CUDA(cudaMemset(gp, 0, sizeof(T) * (size_t)n));
+    SLQ_CUDA(cudaMemset(gm, 0, sizeof(T) * (size_t)n));
+    w = dalloc<float>(n);
+    if (d.reorth == SLQ_REORTH_FULL) {
+      basis = dalloc<float>((int64_t)(max_steps + 1) * n);
+    } else {
+      for (int i = 0; i < 3; ++i) vq[i] = dalloc<float>(n);
+    }
+    dscal = dalloc<double>(8 + 2 * (int64_t)(max_steps + 1));
+    const int64_t np = std::max<int64_t>(vec_nblocks(n), (int64_t)reorth_nblocks(n) * (max_steps + 1));
+    partials = dalloc<double>(np);
+    dflag = dalloc<int>(1);
+    {
+      std::vector<UnitDev> ud;
+      for (const UnitPlan& u : plan.units)
+        ud.push_back(UnitDev{u.local_offset, u.chunk, u.global_offset, u.numel, (int64_t)rank * u.chunk});
+      units_dev = dalloc<UnitDev>((int64_t)ud.size());
+      SLQ_CUDA(cudaMemcpy(units_dev, ud.data(), sizeof(UnitDev) * ud.size(), cudaMemcpyHostToDevice));
+    }
+    SLQ_CUDA(cudaMallocHost(&hstage, 64 * sizeof(double)));
+    runner = make_runner<T>(d, plan, b, L);
+    lio.plan = &plan;
+    fio.plan = &plan;
+    fio.comm = comm;
+    fio.s = L.stream;
+    if (comm) {
+      int64_t mx = 0;
+      for (const UnitPlan& u : plan.units) mx = std::max(mx, u.padded);
+      fio.pbuf0 = dalloc<T>(plan.units[0].padded);
+      fio.gbuf0 = dalloc<T>(plan.units[0].padded);
+      fio.pbuf1 = dalloc<T>(mx);
+      fio.gbuf1 = dalloc<T>(mx);
+    }
+    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+  }
+  ~EngineT() override {
+    cudaStreamSynchronize(L.stream);
+    for (void* p : allocs) cudaFree(p);
+    if (hstage) cudaFreeHost(hstage);
+  }
+
+  double pass_flops() const override { return runner->flops_per_pass(); }
+
+  void pass(const T* th, T* g, double* loss_dev) {
+    if (comm) {
+      fio.shard = th;
+      fio.gshard = g;
+      runner->fwd_bwd(fio, loss_dev);
+    } else {
+      lio.shard = th;
+      lio.gshard = g;
+      runner->fwd_bwd(lio, loss_dev);
+    }
+  }
+
+  // fixed-order reduction of `k` partial columns into out (device), then all-reduce
+  void finish_reduce(int nb, int k, double* out) {
+    reduce_partials(L, partials, nb, k, out);
+    if (comm) comm->allreduce_sum_f64(out, (size_t)k, L.stream);
+  }
+
+  // host copy of `cnt` device doubles (synchronises the stream)
+  void to_host(const double* dev, int cnt, double* host) {
+    SLQ_CUDA(cudaMemcpyAsync(hstage, dev, sizeof(double) * cnt, cudaMemcpyDeviceToHost, L.stream));
+    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    memcpy(host, hstage, sizeof(double) * cnt);
+  }
+
+  void hvp(const float* v, float* out, double eps) override {
+    sumsq_partials(L, v, n, partials);
+    finish_reduce(vec_nblocks(n), 1, dscal + 0);
+    double ss;
+    to_host(dscal, 1, &ss);
+    if (!std::isfinite(ss)) throw Error(SLQ_ENUMERIC, "non-finite direction v");
+    if (ss == 0.0) {
+      SLQ_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)n, L.stream));
+      SLQ_CUDA(cudaStreamSynchronize(L.stream));
+      return;
+    }
+    const float eta = (float)(eps / sqrt(ss));
+    SLQ_CHECK_ARG(eta > 0.0f && std::isfinite(eta), "eps / ||v|| not representable in fp32");
+    perturb<T>(L, theta, v, eta, thp, thm, n);
+    pass(thp, gp, dscal + 2);
+    pass(thm, gm, dscal + 2);
+    SLQ_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), L.stream));
+    fd_out<T>(L, gp, gm, 1.0 / (2.0 * (double)eta), out, n, dflag);
+    int flag = 0;
+    SLQ_CUDA(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, L.stream));
+    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    if (flag) throw Error(SLQ_ENUMERIC, "non-finite gradient in the FD-HVP");
+  }
+
+  double grad(float* g) override {
+    convert_f32<T>(L, theta, thp, n);
+    pass(thp, gp, dscal + 2);
+    if (comm) comm->allreduce_sum_f64(dscal + 2, 1, L.stream);
+    if (g) to_f32<T>(L, gp, g, n);
+    double loss;
+    to_host(dscal + 2, 1, &loss);
+    return loss / runner->tokens_global();
+  }
+
+  void probe(uint64_t seed, float* q) override {
+    probe_fill(L, q, n, units_dev, (int)plan.units.size(), seed, 1.0 / sqrt((double)plan.P));
+    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+  }
+
+  LanczosInfo lanczos(uint64_t seed, int m, double* alpha, double* beta) override {
+    last_info = LanczosInfo();
+    SLQ_CHECK_ARG(m >= 1 && m <= max_steps, "1 <= m <= max_steps");
+    const bool full = d.reorth == SLQ_REORTH_FULL;
+    const float eps_f = (float)d.eps_default;
+    const double inv2eps = 1.0 / (2.0 * (double)eps_f);
+    for (int i = 0; i < m; ++i) alpha[i] = NAN;
+    for (int i = 0; i + 1 < m; ++i) beta[i] = NAN;
+    LanczosInfo info;
+    auto qrow = [&](int k) -> float* { return full ? basis + (int64_t)k * n : vq[k % 3]; };
+    double* d_beta = dscal + 1;
+    double* d_coef = dscal + 8;                  // [max_steps + 1]
+    double* d_alpha = dscal + 8 + (max_steps + 1);  // [max_steps + 1]
+    probe_fill(L, qrow(0), n, units_dev, (int)plan.units.size(), seed, 1.0 / sqrt((double)plan.P));
+    double tmax = 0.0;
+    for (int k = 0; k < m; ++k) {
+      float* qk = qrow(k);
+      const float* qprev = k > 0 ? qrow(k - 1) : nullptr;
+      perturb<T>(L, theta, qk, eps_f, thp, thm, n);
+      pass(thp, gp, dscal + 2);
+      pass(thm, gm, dscal + 2);
+      if (full) {
+        fd_w<T>(L, gp, gm, inv2eps, k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
+        const int nb = reorth_nblocks(n);
+        // CGS pass 1 over q_1..q_k (its coefficient on q_k is alpha_k)
+        reorth_dots(L, basis, n, k + 1, w, n, partials);
+        finish_reduce(nb, k + 1, d_coef);
+        SLQ_CUDA(cudaMemcpyAsync(d_alpha + k, d_coef + k, sizeof(double), cudaMemcpyDeviceToDevice, L.stream));
+        reorth_update(L, basis, n, k + 1, d_coef, w, n, nullptr);
+        // CGS pass 2
+        reorth_dots(L, basis, n, k + 1, w, n, partials);
+        finish_reduce(nb, k + 1, d_coef);
+        reorth_update(L, basis, n, k + 1, d_coef, w, n, partials);
+        finish_reduce(vec_nblocks(n), 1, dscal + 0);
+      } else {
+        fd_w<T>(L, gp, gm, inv2eps, k > 0 ? d_beta : nullptr, qprev, w, qk, n, partials);
+        finish_reduce(vec_nblocks(n), 1, d_alpha + k);
+        axpy_dev(L, w, qk, d_alpha + k, -1.0, n, partials);
+        finish_reduce(vec_nblocks(n), 1, dscal + 0);
+      }
+      double h[2];
+      to_host(d_alpha + k, 1, &h[0]);
+      to_host(dscal + 0, 1, &h[1]);
+      const double a = h[0], bnext = sqrt(std::max(h[1], 0.0));
+      if (!std::isfinite(a) || !std::isfinite(h[1])) {
+        info.nonfinite = 1;
+        info.m_done = k;
+        last_info = info;
+        throw Error(SLQ_ENUMERIC, "non-finite Lanczos coefficient at step " + std::to_string(k + 1));
+      }
+      alpha[k] = a;
+      if (k + 1 < m) beta[k] = bnext;
+      tmax = std::max(tmax, fabs(a));
+      if (k > 0) tmax = std::max(tmax, beta[k - 1]);
+      info.m_done = k + 1;
+      info.beta_next = bnext;
+      if (k + 1 < m && bnext <= 1e-7 * tmax) {  // breakdown: invariant subspace (fp32 vectors)
+        beta[k] = NAN;
+        break;
+      }
+      if (k + 1 < m) {
+        scale_by_inv_sqrt(L, w, dscal + 0, qrow(k + 1), n);
+        SLQ_CUDA(cudaMemcpyAsync(d_beta, &bnext, sizeof(double), cudaMemcpyHostToDevice, L.stream));
+        SLQ_CUDA(cudaStreamSynchronize(L.stream));
+      }
+    }
+    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    last_info = info;
+    return info;
+  }
+};
+
+}  // namespace
+
+std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
+                                    const float* theta_host, int rank, Comm* comm, const Launch& L) {
+  if (d.pass_numerics == SLQ_PASS_FP64)
+    return std::unique_ptr<Engine>(new EngineT<double>(d, plan, b, theta_host, rank, comm, L));
+  return std::unique_ptr<Engine>(new EngineT<float>(d, plan, b, theta_host, rank, comm, L));
+}
+
+}  // namespace slq

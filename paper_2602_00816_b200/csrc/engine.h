@@ -1,0 +1,33 @@
+// The FD-HVP / Lanczos engine behind the C-ABI (one per context).
+#pragma once
+
+#include <memory>
+
+#include "comm.h"
+#include "kernels.h"
+#include "layout.h"
+#include "model.h"
+
+namespace slq {
+
+struct LanczosInfo {
+  int m_done = 0;
+  double beta_next = 0;
+  int nonfinite = 0;
+};
+
+struct Engine {
+  virtual ~Engine() {}
+  // v, out: device pointers, P_loc fp32 each
+  virtual void hvp(const float* v, float* out, double eps) = 0;
+  virtual double grad(float* g) = 0;  // returns the global mean loss
+  virtual LanczosInfo lanczos(uint64_t seed, int m, double* alpha, double* beta) = 0;
+  virtual void probe(uint64_t seed, float* q) = 0;
+  virtual double pass_flops() const = 0;  // algorithmic FLOPs of one fwd+bwd (this rank)
+  LanczosInfo last_info;
+};
+
+std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
+                                    const float* theta_host_full, int rank, Comm* comm, const Launch& L);
+
+}  // namespace slq

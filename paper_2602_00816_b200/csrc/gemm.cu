@@ -1,0 +1,245 @@
+// Dense contractions of the two gradient passes for the fp64 / fp32 pass
+// modes.  tcgen05 has no fp64 kind, so the fp64 parity passes run on the FP64 pipe: a
+// register-blocked SIMT GEMM, double-buffered through shared memory, with the layer epilogues
+// fused (bias, residual add, GELU / tanh and their derivatives) and a deterministic split-K for
+// the weight-gradient contractions over tokens (K = tokens >> M, N).
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace slq {
+
+namespace {
+
+__device__ __forceinline__ double dtanh_(double x) { return tanh(x); }
+__device__ __forceinline__ float dtanh_(float x) { return tanhf(x); }
+
+template <class T>
+__device__ __forceinline__ T gelu_tanh(T u) {
+  const T c = T(0.7978845608028654);  // sqrt(2/pi)
+  T t = dtanh_(c * (u + T(0.044715) * u * u * u));
+  return T(0.5) * u * (T(1) + t);
+}
+
+template <class T>
+__device__ __forceinline__ T gelu_tanh_grad(T u) {
+  const T c = T(0.7978845608028654);
+  T t = dtanh_(c * (u + T(0.044715) * u * u * u));
+  return T(0.5) * (T(1) + t) + T(0.5) * u * (T(1) - t * t) * c * (T(1) + T(3) * T(0.044715) * u * u);
+}
+
+__device__ __forceinline__ int64_t boff(const BatchOff& o, int z) {
+  return (int64_t)(z / o.div) * o.outer + (int64_t)((z % o.div) / o.rep) * o.inner;
+}
+
+template <class T>
+__device__ __forceinline__ void epilogue_store(const GemmArgs<T>& p, T* C, int m, int n, T acc) {
+  T v = p.alpha * acc;
+  if (p.bias) v += p.bias[n];
+  if (p.resid) v += p.resid[(int64_t)m * p.ldr + n];
+  T out;
+  switch (p.act) {
+    case ACT_GELU:
+      p.C2[(int64_t)m * p.ldc2 + n] = v;
+      out = gelu_tanh(v);
+      break;
+    case ACT_TANH:
+      out = dtanh_(v);
+      break;
+    case ACT_DGELU:
+      out = v * gelu_tanh_grad(p.aux[(int64_t)m * p.ldaux + n]);
+      break;
+    case ACT_DTANH: {
+      T h = p.aux[(int64_t)m * p.ldaux + n];
+      out = v * (T(1) - h * h);
+      break;
+    }
+    default:
+      out = v;
+  }
+  T* dst = C + (int64_t)m * p.ldc + n;
+  if (p.accumulate)
+    *dst += out;
+  else
+    *dst = out;
+}
+
+// BM x BN tile per CTA, BK-deep k-slices double-buffered in smem, TM x TN outputs per thread.
+// AK: A is K-contiguous (sAk == 1) else M-contiguous;  BKm: B is K-contiguous else N-contiguous.
+template <class T, int BM, int BN, int BK, int TM, int TN, bool AK, bool BKm>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    gemm_kernel(GemmArgs<T> p, int splits, int kchunk, T* __restrict__ ws) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr int ALD = BM * BK / NT;
+  constexpr int BLD = BN * BK / NT;
+  static_assert(ALD * NT == BM * BK && BLD * NT == BN * BK, "tile/threads");
+  __shared__ T As[2][BK][BM + 1];
+  __shared__ T Bs[2][BK][BN + 1];
+
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int z = blockIdx.z / splits, split = blockIdx.z % splits;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const T* __restrict__ A = p.A + boff(p.offA, z);
+  const T* __restrict__ B = p.B + boff(p.offB, z);
+  const int kb = split * kchunk;
+  const int ke = min(p.K, kb + kchunk);
+
+  T ra[ALD], rb[BLD];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < ALD; ++i) {
+      const int idx = tid + i * NT;
+      int m, k;
+      if (AK) { m = idx / BK; k = idx % BK; } else { m = idx % BM; k = idx / BM; }
+      const int gm = m0 + m, gk = k0 + k;
+      ra[i] = (gm < p.M && gk < ke) ? A[(int64_t)gm * p.sAm + (int64_t)gk * p.sAk] : T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < BLD; ++i) {
+      const int idx = tid + i * NT;
+      int n, k;
+      if (BKm) { n = idx / BK; k = idx % BK; } else { n = idx % BN; k = idx / BN; }
+      const int gn = n0 + n, gk = k0 + k;
+      rb[i] = (gn < p.N && gk < ke) ? B[(int64_t)gk * p.sBk + (int64_t)gn * p.sBn] : T(0);
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < ALD; ++i) {
+      const int idx = tid + i * NT;
+      int m, k;
+      if (AK) { m = idx / BK; k = idx % BK; } else { m = idx % BM; k = idx / BM; }
+      As[buf][k][m] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < BLD; ++i) {
+      const int idx = tid + i * NT;
+      int n, k;
+      if (BKm) { n = idx / BK; k = idx % BK; } else { n = idx % BN; k = idx / BN; }
+      Bs[buf][k][n] = rb[i];
+    }
+  };
+
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+  if (kb < ke) {
+    gload(kb);
+    sstore(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = kb; k0 < ke; k0 += BK) {
+      const bool more = k0 + BK < ke;
+      if (more) gload(k0 + BK);
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        T a[TM], b[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = As[buf][kk][ty * TM + i];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) b[j] = Bs[buf][kk][tx * TN + j];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
+      if (more) sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+  if (splits > 1) {
+    T* W = ws + (int64_t)split * p.M * p.N;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int m = m0 + ty * TM + i;
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int n = n0 + tx * TN + j;
+        if (n < p.N) W[(int64_t)m * p.N + n] = acc[i][j];
+      }
+    }
+    return;
+  }
+  T* C = p.C + boff(p.offC, z);
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int m = m0 + ty * TM + i;
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int n = n0 + tx * TN + j;
+      if (n < p.N) epilogue_store(p, C, m, n, acc[i][j]);
+    }
+  }
+}
+
+template <class T>
+__global__ void splitk_reduce(GemmArgs<T> p, int splits, const T* __restrict__ ws) {
+  const int64_t mn = (int64_t)p.M * p.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mn; i += (int64_t)gridDim.x * blockDim.x) {
+    T s = T(0);
+    for (int k = 0; k < splits; ++k) s += ws[k * mn + i];
+    epilogue_store(p, p.C, (int)(i / p.N), (int)(i % p.N), s);
+  }
+}
+
+template <class T, bool AK, bool BKm>
+void launch_cfg(const Launch& L, const GemmArgs<T>& a) {
+  constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+  const int tiles_m = (int)ceil_div(a.M, BM), tiles_n = (int)ceil_div(a.N, BN);
+  const int tiles = tiles_m * tiles_n * a.batch;
+  int splits = 1;
+  if (a.batch == 1 && tiles < 2 * 148 && a.K >= 512) {
+    splits = (int)ceil_div(2 * 148, tiles);
+    splits = std::min<int>(splits, (int)(a.K / 256));
+    splits = std::max(1, std::min(splits, 32));
+  }
+  int kchunk = (int)ceil_div(ceil_div(a.K, splits), BK) * BK;
+  splits = (int)ceil_div(a.K, kchunk);
+  T* ws = nullptr;
+  if (splits > 1) ws = (T*)L.ws->get(sizeof(T) * (size_t)splits * a.M * a.N, L.stream);
+  dim3 grid(tiles_n, tiles_m, a.batch * splits);
+  LaunchScope scope(L.prof, KC_GEMM, L.stream, 2.0 * a.M * a.N * (double)a.K * a.batch,
+                    sizeof(T) * ((double)a.M * a.K + (double)a.K * a.N + (double)a.M * a.N) * a.batch);
+  gemm_kernel<T, BM, BN, BK, TM, TN, AK, BKm><<<grid, (BM / TM) * (BN / TN), 0, L.stream>>>(a, splits, kchunk, ws);
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+  if (splits > 1) {
+    const int64_t mn = (int64_t)a.M * a.N;
+    int blocks = (int)std::min<int64_t>(ceil_div(mn, 256), 148 * 8);
+    splitk_reduce<T><<<blocks, 256, 0, L.stream>>>(a, splits, ws);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+}
+
+}  // namespace
+
+template <class T>
+void gemm(const Launch& L, const GemmArgs<T>& a) {
+  SLQ_CHECK_ARG(a.M >= 0 && a.N >= 0 && a.K >= 0 && a.batch >= 1, "gemm dims");
+  if (a.M == 0 || a.N == 0) return;
+  SLQ_CHECK_ARG(a.sAk == 1 || a.sAm == 1, "gemm A layout");
+  SLQ_CHECK_ARG(a.sBk == 1 || a.sBn == 1, "gemm B layout");
+  SLQ_CHECK_ARG(a.batch == 1 || (!a.resid && !a.aux && !a.C2), "batched gemm epilogue");
+  SLQ_CHECK_ARG(a.act != ACT_GELU || a.C2, "GELU epilogue needs C2");
+  SLQ_CHECK_ARG((a.act != ACT_DGELU && a.act != ACT_DTANH) || a.aux, "derivative epilogue needs aux");
+  const bool ak = a.sAk == 1 && !(a.sAm == 1 && a.K == 1);
+  const bool bk = a.sBk == 1 && !(a.sBn == 1 && a.K == 1);
+  if (ak && bk) launch_cfg<T, true, true>(L, a);
+  else if (ak && !bk) launch_cfg<T, true, false>(L, a);
+  else if (!ak && bk) launch_cfg<T, false, true>(L, a);
+  else launch_cfg<T, false, false>(L, a);
+}
+
+template void gemm<double>(const Launch&, const GemmArgs<double>&);
+template void gemm<float>(const Launch&, const GemmArgs<float>&);
+
+}  // namespace slq

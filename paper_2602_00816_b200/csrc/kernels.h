@@ -1,0 +1,123 @@
+// Kernel launchers (device code in *.cu).  All launches go to L.stream and are recorded by the
+// per-class profiler.  T is the pass arithmetic type (double for SLQ_PASS_FP64, float for FP32).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.h"
+
+namespace slq {
+
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need, cudaStream_t s);  // grows (stream-synchronised) when too small
+  ~Workspace();
+};
+
+struct Launch {
+  cudaStream_t stream;
+  Profiler* prof;
+  Workspace* ws;      // split-K / reduction scratch
+  int64_t* launches;  // launch counter
+};
+
+// batch addressing of one operand: offset(z) = (z / div) * outer + ((z % div) / rep) * inner
+struct BatchOff {
+  int64_t outer = 0, inner = 0;
+  int div = 1, rep = 1;
+};
+
+enum Act { ACT_NONE = 0, ACT_GELU = 1, ACT_TANH = 2, ACT_DGELU = 3, ACT_DTANH = 4 };
+
+template <class T>
+struct GemmArgs {
+  // C[z](m, n) (+)= epilogue( alpha * sum_k A[z](m, k) * B[z](k, n) )
+  int M = 0, N = 0, K = 0, batch = 1;
+  const T* A = nullptr;
+  int64_t sAm = 0, sAk = 0;  // one of them must be 1
+  BatchOff offA;
+  const T* B = nullptr;
+  int64_t sBk = 0, sBn = 0;  // one of them must be 1
+  BatchOff offB;
+  T* C = nullptr;
+  int64_t ldc = 0;
+  BatchOff offC;
+  T alpha = T(1);
+  const T* bias = nullptr;   // [N], added after scaling
+  const T* resid = nullptr;  // added: resid[m * ldr + n]
+  int64_t ldr = 0;
+  const T* aux = nullptr;  // DGELU: pre-activation u;  DTANH: tanh output h
+  int64_t ldaux = 0;
+  T* C2 = nullptr;  // GELU: also store the pre-activation here
+  int64_t ldc2 = 0;
+  int act = ACT_NONE;
+  bool accumulate = false;  // C += result instead of C = result
+};
+
+template <class T>
+void gemm(const Launch& L, const GemmArgs<T>& a);
+
+// ---- layers (layers.cu) ----
+template <class T> void convert_f32(const Launch& L, const float* x, T* y, int64_t n);
+template <class T> void embed_fwd(const Launch& L, const int32_t* tok, int tok_stride, int nseq, int T_,
+                                  const T* wte, const T* wpe, T* x, int D);
+template <class T> void embed_bwd_rows(const Launch& L, const int32_t* csr_off, const int32_t* csr_pos,
+                                       const T* dx, T* dW, int V, int D, bool accumulate);
+template <class T> void pos_bwd(const Launch& L, const T* dx, T* dwpe, int nseq, int T_, int D);
+template <class T> void layernorm_fwd(const Launch& L, const T* x, const T* g, const T* b, T* y, T* mean,
+                                      T* rstd, int rows, int D, double eps);
+template <class T> void layernorm_bwd(const Launch& L, const T* dy, const T* x, const T* mean, const T* rstd,
+                                      const T* g, const T* dres, T* dx, int rows, int D);
+template <class T> void rmsnorm_fwd(const Launch& L, const T* x, const T* g, T* y, T* rstd, int rows, int D,
+                                    double eps);
+template <class T> void rmsnorm_bwd(const Launch& L, const T* dy, const T* x, const T* rstd, const T* g,
+                                    const T* dres, T* dx, int rows, int D);
+// column reductions over rows (deterministic two-stage):
+//   mode 0: out0[c] = sum_r dy[r,c]                                  (bias grad)
+//   mode 1: out0[c] = sum_r dy*(x-mean)*rstd, out1[c] = sum_r dy     (LayerNorm g, b)
+//   mode 2: out0[c] = sum_r dy*x*rstd                                 (RMSNorm g)
+template <class T> void colreduce(const Launch& L, int mode, const T* dy, int64_t lddy, const T* x,
+                                  const T* mean, const T* rstd, T* out0, T* out1, int rows, int cols,
+                                  bool accumulate);
+template <class T> void softmax_causal_fwd(const Launch& L, T* S, int64_t rows, int T_);
+template <class T> void softmax_bwd(const Launch& L, const T* P, T* dP, int64_t rows, int T_);
+template <class T> void cross_entropy(const Launch& L, T* logits, const int32_t* tgt, int tgt_stride, int T_,
+                                      double* loss_rows, int rows, int V, double inv_ntok);
+void sum_rows_f64(const Launch& L, const double* x, int n, double* out);
+template <class T> void rope(const Launch& L, T* x, int64_t ld, int rows, int T_, int heads, int hd,
+                             const T* cos_t, const T* sin_t, bool inverse);
+// ab = [rows][2F] holding (a | b) per row (gate | up); f = silu(a) * b  [rows][F]
+template <class T> void swiglu_fwd(const Launch& L, const T* ab, T* f, int rows, int F);
+template <class T> void swiglu_bwd(const Launch& L, const T* df, const T* ab, T* dab, int rows, int F);
+template <class T> void add_inplace(const Launch& L, T* y, const T* x, int64_t n);
+
+// ---- vector ops of the Lanczos / FD path (vec.cu) ----
+struct UnitDev {  // per-unit layout for device kernels
+  int64_t local_offset, chunk, global_offset, numel, start_in_unit;
+};
+void probe_fill(const Launch& L, float* q, int64_t n_loc, const UnitDev* units, int n_units, uint64_t seed,
+                double inv_sqrt_P);
+template <class T> void perturb(const Launch& L, const float* theta, const float* v, float eta, T* plus,
+                                T* minus, int64_t n);
+// partial sums of squares / dots -> partials[nblocks * k]; finalize by reduce_partials
+int vec_nblocks(int64_t n);
+void sumsq_partials(const Launch& L, const float* x, int64_t n, double* partials);
+template <class T> void fd_w(const Launch& L, const T* gp, const T* gm, double inv2eta, const double* beta_k,
+                             const float* q_prev, float* w, const float* q_k, int64_t n, double* partials);
+template <class T> void fd_out(const Launch& L, const T* gp, const T* gm, double inv2eta, float* out,
+                               int64_t n, int* nonfinite);
+template <class T> void to_f32(const Launch& L, const T* g, float* out, int64_t n);
+void reduce_partials(const Launch& L, const double* partials, int nblocks, int k, double* out);
+void axpy_dev(const Launch& L, float* w, const float* q, const double* coef, double sign, int64_t n,
+              double* sumsq_partials_out);
+void scale_by_inv_sqrt(const Launch& L, const float* w, const double* sumsq, float* q_next, int64_t n);
+int reorth_nblocks(int64_t n);
+void reorth_dots(const Launch& L, const float* Q, int64_t ldq, int k, const float* w, int64_t n,
+                 double* partials);
+void reorth_update(const Launch& L, const float* Q, int64_t ldq, int k, const double* c, float* w,
+                   int64_t n, double* sumsq_partials_out);
+void nonfinite_check(const Launch& L, const float* x, int64_t n, int* flag);
+
+}  // namespace slq

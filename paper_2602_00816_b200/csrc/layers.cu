@@ -1,0 +1,494 @@
+// Row-wise and elementwise layers of the gradient passes:
+// embeddings (deterministic, atomics-free backward), LayerNorm / RMSNorm (warp-shuffle row
+// reductions, two-stage deterministic column reductions for the gains), causal softmax and its
+// backward, token cross-entropy (online max / log-sum-exp), RoPE and SwiGLU.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "kernels.h"
+
+namespace slq {
+
+namespace {
+
+constexpr int kWarp = 32;
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double dexp(double x) { return exp(x); }
+__device__ __forceinline__ float dexp(float x) { return expf(x); }
+__device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float dsqrt(float x) { return sqrtf(x); }
+
+inline int grid_for(int64_t n, int threads, int cap = 148 * 16) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), cap));
+}
+
+#define LAUNCH(cls, grid, block, kernel, ...)                          \
+  do {                                                                 \
+    LaunchScope scope_(L.prof, cls, L.stream);                         \
+    kernel<<<grid, block, 0, L.stream>>>(__VA_ARGS__);                 \
+    SLQ_CUDA(cudaGetLastError());                                      \
+    ++*L.launches;                                                     \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+template <class T>
+__global__ void k_convert(const float* __restrict__ x, T* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (T)x[i];
+}
+
+// x[b*T + t, :] = wte[tok[b][t], :] (+ wpe[t, :])
+template <class T>
+__global__ void k_embed_fwd(const int32_t* __restrict__ tok, int tok_stride, int nseq, int Tn,
+                            const T* __restrict__ wte, const T* __restrict__ wpe, T* __restrict__ x, int D) {
+  const int64_t total = (int64_t)nseq * Tn * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / D;
+    const int c = (int)(i % D);
+    const int b = (int)(row / Tn), t = (int)(row % Tn);
+    const int id = tok[(int64_t)b * tok_stride + t];
+    T v = wte[(int64_t)id * D + c];
+    if (wpe) v += wpe[(int64_t)t * D + c];
+    x[i] = v;
+  }
+}
+
+// dW[v, :] (+)= sum over the rows listed for token v (CSR built once at init; fixed order)
+template <class T>
+__global__ void k_embed_bwd_rows(const int32_t* __restrict__ off, const int32_t* __restrict__ pos,
+                                 const T* __restrict__ dx, T* __restrict__ dW, int V, int D, bool accumulate) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  const int nwarps = gridDim.x * blockDim.x / kWarp;
+  for (int v = warp; v < V; v += nwarps) {
+    const int s = off[v], e = off[v + 1];
+    for (int c = lane; c < D; c += kWarp) {
+      T acc = T(0);
+      for (int j = s; j < e; ++j) acc += dx[(int64_t)pos[j] * D + c];
+      T* dst = dW + (int64_t)v * D + c;
+      *dst = accumulate ? *dst + acc : acc;
+    }
+  }
+}
+
+template <class T>
+__global__ void k_pos_bwd(const T* __restrict__ dx, T* __restrict__ dwpe, int nseq, int Tn, int D) {
+  const int64_t total = (int64_t)Tn * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    T acc = T(0);
+    for (int b = 0; b < nseq; ++b) acc += dx[(int64_t)b * Tn * D + i];
+    dwpe[i] = acc;
+  }
+}
+
+// one warp per row
+template <class T>
+__global__ void k_layernorm_fwd(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
+                                T* __restrict__ y, T* __restrict__ mean, T* __restrict__ rstd, int rows, int D,
+                                T eps) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  if (row >= rows) return;
+  const T* xr = x + (int64_t)row * D;
+  T s = T(0);
+  for (int c = lane; c < D; c += kWarp) s += xr[c];
+  const T mu = warp_sum(s) / T(D);
+  T v = T(0);
+  for (int c = lane; c < D; c += kWarp) {
+    const T d = xr[c] - mu;
+    v += d * d;
+  }
+  const T rs = T(1) / dsqrt(warp_sum(v) / T(D) + eps);
+  T* yr = y + (int64_t)row * D;
+  for (int c = lane; c < D; c += kWarp) yr[c] = (xr[c] - mu) * rs * g[c] + b[c];
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+// dx = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)) (+ dres),  dxhat = dy * g
+template <class T>
+__global__ void k_layernorm_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ mean,
+                                const T* __restrict__ rstd, const T* __restrict__ g, const T* __restrict__ dres,
+                                T* __restrict__ dx, int rows, int D) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  if (row >= rows) return;
+  const int64_t o = (int64_t)row * D;
+  const T mu = mean[row], rs = rstd[row];
+  T s1 = T(0), s2 = T(0);
+  for (int c = lane; c < D; c += kWarp) {
+    const T dxh = dy[o + c] * g[c];
+    const T xh = (x[o + c] - mu) * rs;
+    s1 += dxh;
+    s2 += dxh * xh;
+  }
+  s1 = warp_sum(s1) / T(D);
+  s2 = warp_sum(s2) / T(D);
+  for (int c = lane; c < D; c += kWarp) {
+    const T dxh = dy[o + c] * g[c];
+    const T xh = (x[o + c] - mu) * rs;
+    T v = rs * (dxh - s1 - xh * s2);
+    if (dres) v += dres[o + c];
+    dx[o + c] = v;
+  }
+}
+
+template <class T>
+__global__ void k_rmsnorm_fwd(const T* __restrict__ x, const T* __restrict__ g, T* __restrict__ y,
+                              T* __restrict__ rstd, int rows, int D, T eps) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  if (row >= rows) return;
+  const T* xr = x + (int64_t)row * D;
+  T s = T(0);
+  for (int c = lane; c < D; c += kWarp) s += xr[c] * xr[c];
+  const T r = T(1) / dsqrt(warp_sum(s) / T(D) + eps);
+  T* yr = y + (int64_t)row * D;
+  for (int c = lane; c < D; c += kWarp) yr[c] = xr[c] * r * g[c];
+  if (lane == 0) rstd[row] = r;
+}
+
+// dx = r * dxhat - x * r^3 * mean(dxhat * x) (+ dres)
+template <class T>
+__global__ void k_rmsnorm_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ rstd,
+                              const T* __restrict__ g, const T* __restrict__ dres, T* __restrict__ dx, int rows,
+                              int D) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  if (row >= rows) return;
+  const int64_t o = (int64_t)row * D;
+  const T r = rstd[row];
+  T s = T(0);
+  for (int c = lane; c < D; c += kWarp) s += dy[o + c] * g[c] * x[o + c];
+  s = warp_sum(s) / T(D);
+  for (int c = lane; c < D; c += kWarp) {
+    T v = r * dy[o + c] * g[c] - x[o + c] * r * r * r * s;
+    if (dres) v += dres[o + c];
+    dx[o + c] = v;
+  }
+}
+
+// stage 1 of the column reductions: block (cx, cy) reduces rows [cy*rpb, (cy+1)*rpb) of
+// columns [cx*blockDim, ...) into part[cy][col]
+template <class T>
+__global__ void k_colreduce1(int mode, const T* __restrict__ dy, int64_t lddy, const T* __restrict__ x,
+                             const T* __restrict__ mean, const T* __restrict__ rstd, T* __restrict__ part0,
+                             T* __restrict__ part1, int rows, int cols, int rpb) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
+  T a0 = T(0), a1 = T(0);
+  for (int r = r0; r < r1; ++r) {
+    const T d = dy[(int64_t)r * lddy + c];
+    if (mode == 0) {
+      a0 += d;
+    } else if (mode == 1) {
+      a0 += d * (x[(int64_t)r * cols + c] - mean[r]) * rstd[r];
+      a1 += d;
+    } else {
+      a0 += d * x[(int64_t)r * cols + c] * rstd[r];
+    }
+  }
+  part0[(int64_t)blockIdx.y * cols + c] = a0;
+  if (mode == 1) part1[(int64_t)blockIdx.y * cols + c] = a1;
+}
+
+template <class T>
+__global__ void k_colreduce2(const T* __restrict__ part, int nparts, T* __restrict__ out, int cols, bool accumulate) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  T s = T(0);
+  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * cols + c];
+  out[c] = accumulate ? out[c] + s : s;
+}
+
+// causal softmax over rows of length Tn; row r is query position t = r % Tn (keys j <= t)
+template <class T>
+__global__ void k_softmax_causal(T* __restrict__ S, int64_t rows, int Tn) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  if (row >= rows) return;
+  const int t = (int)(row % Tn);
+  T* s = S + row * Tn;
+  T mx = -INFINITY;
+  for (int j = lane; j <= t; j += kWarp) mx = max(mx, s[j]);
+  mx = warp_max(mx);
+  T sum = T(0);
+  for (int j = lane; j <= t; j += kWarp) {
+    const T e = dexp(s[j] - mx);
+    s[j] = e;
+    sum += e;
+  }
+  const T inv = T(1) / warp_sum(sum);
+  for (int j = lane; j < Tn; j += kWarp) s[j] = (j <= t) ? s[j] * inv : T(0);
+}
+
+// dS = P * (dP - sum_j dP_j P_j), in place in dP
+template <class T>
+__global__ void k_softmax_bwd(const T* __restrict__ P, T* __restrict__ dP, int64_t rows, int Tn) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  if (row >= rows) return;
+  const T* p = P + row * Tn;
+  T* d = dP + row * Tn;
+  T s = T(0);
+  for (int j = lane; j < Tn; j += kWarp) s += p[j] * d[j];
+  s = warp_sum(s);
+  for (int j = lane; j < Tn; j += kWarp) d[j] = p[j] * (d[j] - s);
+}
+
+// one block per row: loss_row = lse - logit[tgt];  logits <- (softmax - onehot) * inv_ntok
+template <class T>
+__global__ void k_cross_entropy(T* __restrict__ logits, const int32_t* __restrict__ tgt, int tgt_stride, int Tn,
+                                double* __restrict__ loss_rows, int V, double inv_ntok) {
+  const int row = blockIdx.x;
+  T* z = logits + (int64_t)row * V;
+  const int b = row / Tn, t = row % Tn;
+  const int y = tgt[(int64_t)b * tgt_stride + t];
+  __shared__ T red[32];
+  T mx = -INFINITY;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) mx = max(mx, z[j]);
+  mx = warp_max(mx);
+  if (threadIdx.x % kWarp == 0) red[threadIdx.x / kWarp] = mx;
+  __syncthreads();
+  if (threadIdx.x < kWarp) {
+    T v = threadIdx.x < blockDim.x / kWarp ? red[threadIdx.x] : T(-INFINITY);
+    v = warp_max(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  mx = red[0];
+  __syncthreads();
+  T s = T(0);
+  for (int j = threadIdx.x; j < V; j += blockDim.x) s += dexp(z[j] - mx);
+  s = warp_sum(s);
+  if (threadIdx.x % kWarp == 0) red[threadIdx.x / kWarp] = s;
+  __syncthreads();
+  if (threadIdx.x < kWarp) {
+    T v = threadIdx.x < blockDim.x / kWarp ? red[threadIdx.x] : T(0);
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const T sum = red[0];
+  const T lse = mx + log(sum);
+  if (threadIdx.x == 0) loss_rows[row] = (double)(lse - z[y]);
+  __syncthreads();
+  const T inv = T(1) / sum, scale = (T)inv_ntok;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) {
+    T p = dexp(z[j] - mx) * inv;
+    if (j == y) p -= T(1);
+    z[j] = p * scale;
+  }
+}
+
+__global__ void k_sum_rows(const double* __restrict__ x, int n, double* out) {
+  __shared__ double red[32];
+  double s = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+  s = warp_sum(s);
+  if (threadIdx.x % kWarp == 0) red[threadIdx.x / kWarp] = s;
+  __syncthreads();
+  if (threadIdx.x < kWarp) {
+    double v = threadIdx.x < blockDim.x / kWarp ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *out = v;
+  }
+}
+
+// RoPE on a [rows, ld] buffer holding `heads` heads of width hd starting at column 0; row r has
+// position r % Tn.  Rotates pairs (i, i + hd/2) by +angle (inverse: -angle, the transpose).
+template <class T>
+__global__ void k_rope(T* __restrict__ x, int64_t ld, int rows, int Tn, int heads, int hd, const T* __restrict__ cs,
+                       const T* __restrict__ sn, bool inverse) {
+  const int half = hd / 2;
+  const int64_t total = (int64_t)rows * heads * half;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % half);
+    const int64_t rh = i / half;
+    const int h = (int)(rh % heads);
+    const int r = (int)(rh / heads);
+    const int t = r % Tn;
+    T* p = x + (int64_t)r * ld + (int64_t)h * hd;
+    const T c = cs[(int64_t)t * half + j], s = inverse ? -sn[(int64_t)t * half + j] : sn[(int64_t)t * half + j];
+    const T a = p[j], b = p[j + half];
+    p[j] = a * c - b * s;
+    p[j + half] = b * c + a * s;
+  }
+}
+
+template <class T>
+__global__ void k_swiglu_fwd(const T* __restrict__ ab, T* __restrict__ f, int rows, int F) {
+  const int64_t n = (int64_t)rows * F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / F, j = i % F;
+    const T a = ab[r * 2 * F + j], b = ab[r * 2 * F + F + j];
+    const T s = T(1) / (T(1) + dexp(-a));
+    f[i] = a * s * b;
+  }
+}
+
+template <class T>
+__global__ void k_swiglu_bwd(const T* __restrict__ df, const T* __restrict__ ab, T* __restrict__ dab, int rows, int F) {
+  const int64_t n = (int64_t)rows * F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / F, j = i % F;
+    const T a = ab[r * 2 * F + j], b = ab[r * 2 * F + F + j];
+    const T s = T(1) / (T(1) + dexp(-a));
+    const T d = df[i];
+    dab[r * 2 * F + j] = d * b * s * (T(1) + a * (T(1) - s));
+    dab[r * 2 * F + F + j] = d * a * s;
+  }
+}
+
+template <class T>
+__global__ void k_add(T* __restrict__ y, const T* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += x[i];
+}
+
+}  // namespace
+
+template <class T>
+void convert_f32(const Launch& L, const float* x, T* y, int64_t n) {
+  if (n == 0) return;
+  LAUNCH(KC_ELEM, grid_for(n, 256), 256, k_convert<T>, x, y, n);
+}
+template <class T>
+void embed_fwd(const Launch& L, const int32_t* tok, int tok_stride, int nseq, int Tn, const T* wte, const T* wpe,
+               T* x, int D) {
+  const int64_t n = (int64_t)nseq * Tn * D;
+  if (n == 0) return;
+  LAUNCH(KC_EMBED, grid_for(n, 256), 256, k_embed_fwd<T>, tok, tok_stride, nseq, Tn, wte, wpe, x, D);
+}
+template <class T>
+void embed_bwd_rows(const Launch& L, const int32_t* off, const int32_t* pos, const T* dx, T* dW, int V, int D,
+                    bool accumulate) {
+  LAUNCH(KC_EMBED, (int)std::min<int64_t>(ceil_div(V, 8), 148 * 32), 256, k_embed_bwd_rows<T>, off, pos, dx, dW,
+         V, D, accumulate);
+}
+template <class T>
+void pos_bwd(const Launch& L, const T* dx, T* dwpe, int nseq, int Tn, int D) {
+  LAUNCH(KC_EMBED, grid_for((int64_t)Tn * D, 256), 256, k_pos_bwd<T>, dx, dwpe, nseq, Tn, D);
+}
+template <class T>
+void layernorm_fwd(const Launch& L, const T* x, const T* g, const T* b, T* y, T* mean, T* rstd, int rows, int D,
+                   double eps) {
+  if (rows == 0) return;
+  LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_layernorm_fwd<T>, x, g, b, y, mean, rstd, rows, D, (T)eps);
+}
+template <class T>
+void layernorm_bwd(const Launch& L, const T* dy, const T* x, const T* mean, const T* rstd, const T* g,
+                   const T* dres, T* dx, int rows, int D) {
+  if (rows == 0) return;
+  LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_layernorm_bwd<T>, dy, x, mean, rstd, g, dres, dx, rows, D);
+}
+template <class T>
+void rmsnorm_fwd(const Launch& L, const T* x, const T* g, T* y, T* rstd, int rows, int D, double eps) {
+  if (rows == 0) return;
+  LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_rmsnorm_fwd<T>, x, g, y, rstd, rows, D, (T)eps);
+}
+template <class T>
+void rmsnorm_bwd(const Launch& L, const T* dy, const T* x, const T* rstd, const T* g, const T* dres, T* dx,
+                 int rows, int D) {
+  if (rows == 0) return;
+  LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_rmsnorm_bwd<T>, dy, x, rstd, g, dres, dx, rows, D);
+}
+template <class T>
+void colreduce(const Launch& L, int mode, const T* dy, int64_t lddy, const T* x, const T* mean, const T* rstd,
+               T* out0, T* out1, int rows, int cols, bool accumulate) {
+  if (cols == 0) return;
+  const int threads = 128;
+  const int cblocks = (int)ceil_div(cols, threads);
+  int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 16), ceil_div(148 * 8, cblocks)));
+  const int rpb = (int)ceil_div(std::max(rows, 1), rblocks);
+  rblocks = (int)ceil_div(std::max(rows, 1), rpb);
+  T* part = (T*)L.ws->get(sizeof(T) * 2 * (size_t)rblocks * cols, L.stream);
+  T* part1 = part + (size_t)rblocks * cols;
+  LAUNCH(KC_NORM, dim3(cblocks, rblocks), threads, k_colreduce1<T>, mode, dy, lddy, x, mean, rstd, part, part1,
+         rows, cols, rpb);
+  LAUNCH(KC_NORM, cblocks, threads, k_colreduce2<T>, part, rblocks, out0, cols, accumulate);
+  if (mode == 1) LAUNCH(KC_NORM, cblocks, threads, k_colreduce2<T>, part1, rblocks, out1, cols, accumulate);
+}
+template <class T>
+void softmax_causal_fwd(const Launch& L, T* S, int64_t rows, int Tn) {
+  if (rows == 0) return;
+  LAUNCH(KC_ATTN, (int)ceil_div(rows, 8), 256, k_softmax_causal<T>, S, rows, Tn);
+}
+template <class T>
+void softmax_bwd(const Launch& L, const T* P, T* dP, int64_t rows, int Tn) {
+  if (rows == 0) return;
+  LAUNCH(KC_ATTN, (int)ceil_div(rows, 8), 256, k_softmax_bwd<T>, P, dP, rows, Tn);
+}
+template <class T>
+void cross_entropy(const Launch& L, T* logits, const int32_t* tgt, int tgt_stride, int Tn, double* loss_rows,
+                   int rows, int V, double inv_ntok) {
+  if (rows == 0) return;
+  LAUNCH(KC_CE, rows, 256, k_cross_entropy<T>, logits, tgt, tgt_stride, Tn, loss_rows, V, inv_ntok);
+}
+void sum_rows_f64(const Launch& L, const double* x, int n, double* out) {
+  LAUNCH(KC_VEC, 1, 1024, k_sum_rows, x, n, out);
+}
+template <class T>
+void rope(const Launch& L, T* x, int64_t ld, int rows, int Tn, int heads, int hd, const T* cs, const T* sn,
+          bool inverse) {
+  const int64_t n = (int64_t)rows * heads * (hd / 2);
+  if (n == 0) return;
+  LAUNCH(KC_ELEM, grid_for(n, 256), 256, k_rope<T>, x, ld, rows, Tn, heads, hd, cs, sn, inverse);
+}
+template <class T>
+void swiglu_fwd(const Launch& L, const T* ab, T* f, int rows, int F) {
+  const int64_t n = (int64_t)rows * F;
+  if (n == 0) return;
+  LAUNCH(KC_ELEM, grid_for(n, 256), 256, k_swiglu_fwd<T>, ab, f, rows, F);
+}
+template <class T>
+void swiglu_bwd(const Launch& L, const T* df, const T* ab, T* dab, int rows, int F) {
+  const int64_t n = (int64_t)rows * F;
+  if (n == 0) return;
+  LAUNCH(KC_ELEM, grid_for(n, 256), 256, k_swiglu_bwd<T>, df, ab, dab, rows, F);
+}
+template <class T>
+void add_inplace(const Launch& L, T* y, const T* x, int64_t n) {
+  if (n == 0) return;
+  LAUNCH(KC_ELEM, grid_for(n, 256), 256, k_add<T>, y, x, n);
+}
+
+#define INST(T)                                                                                                 \
+  template void convert_f32<T>(const Launch&, const float*, T*, int64_t);                                       \
+  template void embed_fwd<T>(const Launch&, const int32_t*, int, int, int, const T*, const T*, T*, int);        \
+  template void embed_bwd_rows<T>(const Launch&, const int32_t*, const int32_t*, const T*, T*, int, int, bool); \
+  template void pos_bwd<T>(const Launch&, const T*, T*, int, int, int);                                         \
+  template void layernorm_fwd<T>(const Launch&, const T*, const T*, const T*, T*, T*, T*, int, int, double);    \
+  template void layernorm_bwd<T>(const Launch&, const T*, const T*, const T*, const T*, const T*, const T*, T*, \
+                                 int, int);                                                                     \
+  template void rmsnorm_fwd<T>(const Launch&, const T*, const T*, T*, T*, int, int, double);                    \
+  template void rmsnorm_bwd<T>(const Launch&, const T*, const T*, const T*, const T*, const T*, T*, int, int);   \
+  template void colreduce<T>(const Launch&, int, const T*, int64_t, const T*, const T*, const T*, T*, T*, int,  \
+                             int, bool);                                                                        \
+  template void softmax_causal_fwd<T>(const Launch&, T*, int64_t, int);                                         \
+  template void softmax_bwd<T>(const Launch&, const T*, T*, int64_t, int);                                      \
+  template void cross_entropy<T>(const Launch&, T*, const int32_t*, int, int, double*, int, int, double);       \
+  template void rope<T>(const Launch&, T*, int64_t, int, int, int, int, const T*, const T*, bool);              \
+  template void swiglu_fwd<T>(const Launch&, const T*, T*, int, int);                                           \
+  template void swiglu_bwd<T>(const Launch&, const T*, const T*, T*, int, int);                                 \
+  template void add_inplace<T>(const Launch&, T*, const T*, int64_t);
+
+INST(double)
+INST(float)
+
+}  // namespace slq

@@ -1,0 +1,511 @@
+// MLP / GPT / Llama gradient passes on the GPU (pass dtype T = double or float).
+//
+// The loss is the mean token cross-entropy over the GLOBAL batch (Alg. 1 sum_b w_b = 1, P:182;
+// SURVEY.md §8(c2) #1, #14): each rank scales its dlogits by 1/N_global, so the reduce-scatter
+// of the unit gradients sums to grad L.  Layer math follows the oracle's definitions
+// (DESIGN.md "Readings" #11); the code is independent of oracle/.
+#include <math.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "model.h"
+
+namespace slq {
+
+namespace {
+
+struct Arena {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* alloc(int64_t n) {
+    void* p = nullptr;
+    if (n > 0) SLQ_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)n));
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  ~Arena() {
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+// y[N x out] = x[N x in] . W[out x in]^T (+ bias) (+ resid), optional activation
+template <class T>
+void linear_fwd(const Launch& L, const T* x, int64_t ldx, const T* W, int out, int in, int N, T* y, int64_t ldy,
+                const T* bias, const T* resid = nullptr, int64_t ldr = 0, int act = ACT_NONE, T* C2 = nullptr,
+                int64_t ldc2 = 0) {
+  GemmArgs<T> a;
+  a.M = N; a.N = out; a.K = in;
+  a.A = x; a.sAm = ldx; a.sAk = 1;
+  a.B = W; a.sBk = 1; a.sBn = in;
+  a.C = y; a.ldc = ldy;
+  a.bias = bias; a.resid = resid; a.ldr = ldr; a.act = act; a.C2 = C2; a.ldc2 = ldc2;
+  gemm(L, a);
+}
+
+// dx[N x in] (+)= (dy[N x out] . W[out x in]) (* activation derivative at aux)
+template <class T>
+void linear_dgrad(const Launch& L, const T* dy, int64_t lddy, const T* W, int out, int in, int N, T* dx,
+                  int64_t lddx, int act = ACT_NONE, const T* aux = nullptr, int64_t ldaux = 0, bool acc = false) {
+  GemmArgs<T> a;
+  a.M = N; a.N = in; a.K = out;
+  a.A = dy; a.sAm = lddy; a.sAk = 1;
+  a.B = W; a.sBk = in; a.sBn = 1;
+  a.C = dx; a.ldc = lddx;
+  a.act = act; a.aux = aux; a.ldaux = ldaux; a.accumulate = acc;
+  gemm(L, a);
+}
+
+// dW[out x in] (+)= dy[N x out]^T . x[N x in]
+template <class T>
+void linear_wgrad(const Launch& L, const T* dy, int64_t lddy, const T* x, int64_t ldx, int out, int in, int N, T* dW,
+                  bool acc = false) {
+  GemmArgs<T> a;
+  a.M = out; a.N = in; a.K = N;
+  a.A = dy; a.sAm = 1; a.sAk = lddy;
+  a.B = x; a.sBk = ldx; a.sBn = 1;
+  a.C = dW; a.ldc = in;
+  a.accumulate = acc;
+  gemm(L, a);
+}
+
+// Causal multi-head attention over a packed projection buffer.
+//   qkv rows r = b*Tn + t (ld = W); q head h at column qo + h*hd, kv head g at ko/vo + g*hd;
+//   q head h reads kv head h / rep (GQA).  P = probabilities [nseq*Hq][Tn][Tn].
+template <class T>
+struct AttnGeom {
+  int nseq, Tn, Hq, Hkv, hd;
+  int64_t W;           // ld of the qkv buffer
+  int64_t qo, ko, vo;  // column offsets
+  int64_t ldo;         // ld of the merged output o [N x Hq*hd]
+  int rep() const { return Hq / Hkv; }
+  BatchOff qoff() const { return BatchOff{Tn * W, hd, Hq, 1}; }
+  BatchOff kvoff() const { return BatchOff{Tn * W, hd, Hq, rep()}; }
+  BatchOff poff() const { return BatchOff{(int64_t)Tn * Tn, 0, 1, 1}; }
+  BatchOff ooff() const { return BatchOff{Tn * ldo, hd, Hq, 1}; }
+};
+
+template <class T>
+void attention_fwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, T* P, T* o) {
+  const T scale = T(1.0 / sqrt((double)g.hd));
+  {  // S = scale * Q K^T
+    GemmArgs<T> a;
+    a.M = g.Tn; a.N = g.Tn; a.K = g.hd; a.batch = g.nseq * g.Hq;
+    a.A = qkv + g.qo; a.sAm = g.W; a.sAk = 1; a.offA = g.qoff();
+    a.B = qkv + g.ko; a.sBk = 1; a.sBn = g.W; a.offB = g.kvoff();
+    a.C = P; a.ldc = g.Tn; a.offC = g.poff();
+    a.alpha = scale;
+    gemm(L, a);
+  }
+  softmax_causal_fwd(L, P, (int64_t)g.nseq * g.Hq * g.Tn, g.Tn);
+  {  // O = P V
+    GemmArgs<T> a;
+    a.M = g.Tn; a.N = g.hd; a.K = g.Tn; a.batch = g.nseq * g.Hq;
+    a.A = P; a.sAm = g.Tn; a.sAk = 1; a.offA = g.poff();
+    a.B = qkv + g.vo; a.sBk = g.W; a.sBn = 1; a.offB = g.kvoff();
+    a.C = o; a.ldc = g.ldo; a.offC = g.ooff();
+    gemm(L, a);
+  }
+}
+
+// gradients w.r.t. q, k, v (written into dqkv with the qkv geometry); dP is scratch [like P]
+template <class T>
+void attention_bwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, const T* P, const T* dO, T* dP, T* dqkv) {
+  const T scale = T(1.0 / sqrt((double)g.hd));
+  const int rep = g.rep();
+  // dV[b, g] = sum_{r < rep} P[b, g*rep + r]^T dO[b, g*rep + r]
+  for (int r = 0; r < rep; ++r) {
+    GemmArgs<T> a;
+    a.M = g.Tn; a.N = g.hd; a.K = g.Tn; a.batch = g.nseq * g.Hkv;
+    a.A = P + (int64_t)r * g.Tn * g.Tn; a.sAm = 1; a.sAk = g.Tn;
+    a.offA = BatchOff{(int64_t)g.Hq * g.Tn * g.Tn, (int64_t)rep * g.Tn * g.Tn, g.Hkv, 1};
+    a.B = dO + (int64_t)r * g.hd; a.sBk = g.ldo; a.sBn = 1;
+    a.offB = BatchOff{g.Tn * g.ldo, (int64_t)rep * g.hd, g.Hkv, 1};
+    a.C = dqkv + g.vo; a.ldc = g.W; a.offC = BatchOff{g.Tn * g.W, g.hd, g.Hkv, 1};
+    a.accumulate = r > 0;
+    gemm(L, a);
+  }
+  {  // dP = dO V^T
+    GemmArgs<T> a;
+    a.M = g.Tn; a.N = g.Tn; a.K = g.hd; a.batch = g.nseq * g.Hq;
+    a.A = dO; a.sAm = g.ldo; a.sAk = 1; a.offA = g.ooff();
+    a.B = qkv + g.vo; a.sBk = 1; a.sBn = g.W; a.offB = g.kvoff();
+    a.C = dP; a.ldc = g.Tn; a.offC = g.poff();
+    gemm(L, a);
+  }
+  softmax_bwd(L, P, dP, (int64_t)g.nseq * g.Hq * g.Tn, g.Tn);  // dP <- dS
+  {  // dQ = scale * dS K
+    GemmArgs<T> a;
+    a.M = g.Tn; a.N = g.hd; a.K = g.Tn; a.batch = g.nseq * g.Hq;
+    a.A = dP; a.sAm = g.Tn; a.sAk = 1; a.offA = g.poff();
+    a.B = qkv + g.ko; a.sBk = g.W; a.sBn = 1; a.offB = g.kvoff();
+    a.C = dqkv + g.qo; a.ldc = g.W; a.offC = g.qoff();
+    a.alpha = scale;
+    gemm(L, a);
+  }
+  // dK[b, g] = scale * sum_r dS[b, g*rep + r]^T Q[b, g*rep + r]
+  for (int r = 0; r < rep; ++r) {
+    GemmArgs<T> a;
+    a.M = g.Tn; a.N = g.hd; a.K = g.Tn; a.batch = g.nseq * g.Hkv;
+    a.A = dP + (int64_t)r * g.Tn * g.Tn; a.sAm = 1; a.sAk = g.Tn;
+    a.offA = BatchOff{(int64_t)g.Hq * g.Tn * g.Tn, (int64_t)rep * g.Tn * g.Tn, g.Hkv, 1};
+    a.B = qkv + g.qo + (int64_t)r * g.hd; a.sBk = g.W; a.sBn = 1;
+    a.offB = BatchOff{g.Tn * g.W, (int64_t)rep * g.hd, g.Hkv, 1};
+    a.C = dqkv + g.ko; a.ldc = g.W; a.offC = BatchOff{g.Tn * g.W, g.hd, g.Hkv, 1};
+    a.alpha = scale;
+    a.accumulate = r > 0;
+    gemm(L, a);
+  }
+}
+
+void build_csr(const std::vector<int32_t>& tok, int nseq, int Tn, int V, std::vector<int32_t>& off,
+               std::vector<int32_t>& pos) {
+  off.assign(V + 1, 0);
+  for (int b = 0; b < nseq; ++b)
+    for (int t = 0; t < Tn; ++t) off[tok[(size_t)b * (Tn + 1) + t] + 1]++;
+  for (int v = 0; v < V; ++v) off[v + 1] += off[v];
+  pos.assign((size_t)nseq * Tn, 0);
+  std::vector<int32_t> fill(off.begin(), off.end() - 1);
+  for (int b = 0; b < nseq; ++b)
+    for (int t = 0; t < Tn; ++t) pos[fill[tok[(size_t)b * (Tn + 1) + t]]++] = b * Tn + t;
+}
+
+template <class T>
+T* upload(Arena& A, const void* host, int64_t n) {
+  T* d = A.alloc<T>(n);
+  if (n > 0) SLQ_CUDA(cudaMemcpy(d, host, sizeof(T) * (size_t)n, cudaMemcpyHostToDevice));
+  return d;
+}
+
+// ------------------------------------------------------------------------------------------
+template <class T>
+struct MlpRunner : Runner<T> {
+  Arena A;
+  Launch L;
+  const UnitPlan* u;
+  int n, din, H, C, n_glob;
+  T *x, *h, *z2, *dh;
+  int32_t* y;
+  double* loss_rows;
+
+  MlpRunner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b, const Launch& L_) : L(L_) {
+    u = &plan.units[0];
+    n = b.n_rows; n_glob = b.n_rows_global; din = d.d_in; H = d.d_hidden; C = d.n_classes;
+    float* xf = upload<float>(A, b.x.data(), (int64_t)n * din);
+    x = A.alloc<T>((int64_t)n * din);
+    convert_f32<T>(L, xf, x, (int64_t)n * din);
+    y = upload<int32_t>(A, b.y.data(), n);
+    h = A.alloc<T>((int64_t)n * H);
+    z2 = A.alloc<T>((int64_t)n * C);
+    dh = A.alloc<T>((int64_t)n * H);
+    loss_rows = A.alloc<double>(std::max(n, 1));
+  }
+  double tokens_global() const override { return n_glob; }
+  double flops_per_pass() const override { return 6.0 * n * ((double)din * H + (double)H * C); }
+
+  void fwd_bwd(PassIO<T>& io, double* loss_sum) override {
+    const T* P = io.params(0);
+    const T* W1 = P + u->t("fc1.w").offset;
+    const T* b1 = P + u->t("fc1.b").offset;
+    const T* W2 = P + u->t("fc2.w").offset;
+    const T* b2 = P + u->t("fc2.b").offset;
+    linear_fwd<T>(L, x, din, W1, H, din, n, h, H, b1, nullptr, 0, ACT_TANH);
+    linear_fwd<T>(L, h, H, W2, C, H, n, z2, C, b2);
+    cross_entropy<T>(L, z2, y, 1, 1, loss_rows, n, C, 1.0 / n_glob);
+    T* G = io.grads(0);
+    linear_wgrad<T>(L, z2, C, h, H, C, H, n, G + u->t("fc2.w").offset);
+    colreduce<T>(L, 0, z2, C, nullptr, nullptr, nullptr, G + u->t("fc2.b").offset, nullptr, n, C, false);
+    linear_dgrad<T>(L, z2, C, W2, C, H, n, dh, H, ACT_DTANH, h, H);
+    linear_wgrad<T>(L, dh, H, x, din, H, din, n, G + u->t("fc1.w").offset);
+    colreduce<T>(L, 0, dh, H, nullptr, nullptr, nullptr, G + u->t("fc1.b").offset, nullptr, n, H, false);
+    io.grads_done(0);
+    sum_rows_f64(L, loss_rows, n, loss_sum);
+  }
+};
+
+// ------------------------------------------------------------------------------------------
+template <class T>
+struct GptRunner : Runner<T> {
+  Arena A;
+  Launch L;
+  const LayoutPlan* plan;
+  int nseq, Tn, N, D, H, hd, F, V, Ly, nseq_glob;
+  bool tied;
+  double eps;
+  int32_t *tok, *csr_off, *csr_pos;
+  double* loss_rows;
+  std::vector<T*> xs;  // L+1 residual streams
+  struct Layer { T *mean1, *rstd1, *h1, *qkv, *P, *o, *x1, *mean2, *rstd2, *h2, *u, *gu; };
+  std::vector<Layer> ly;
+  T *meanf, *rstdf, *xf, *logits;
+  T *dx, *dx1, *dh, *dqkv, *dP, *do_, *du;
+
+  GptRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
+    nseq = b.n_seq; nseq_glob = b.n_seq_global; Tn = d.seq_len; N = nseq * Tn; D = d.d_model; H = d.n_heads;
+    hd = D / H; F = d.d_ff; V = d.vocab; Ly = d.n_layers; tied = d.tie_embeddings != 0; eps = d.norm_eps;
+    tok = upload<int32_t>(A, b.tokens.data(), (int64_t)nseq * (Tn + 1));
+    std::vector<int32_t> off, pos;
+    build_csr(b.tokens, nseq, Tn, V, off, pos);
+    csr_off = upload<int32_t>(A, off.data(), V + 1);
+    csr_pos = upload<int32_t>(A, pos.data(), (int64_t)N);
+    loss_rows = A.alloc<double>(std::max(N, 1));
+    for (int l = 0; l <= Ly; ++l) xs.push_back(A.alloc<T>((int64_t)N * D));
+    const int64_t PP = (int64_t)nseq * H * Tn * Tn;
+    for (int l = 0; l < Ly; ++l) {
+      Layer a;
+      a.mean1 = A.alloc<T>(N); a.rstd1 = A.alloc<T>(N); a.h1 = A.alloc<T>((int64_t)N * D);
+      a.qkv = A.alloc<T>((int64_t)N * 3 * D); a.P = A.alloc<T>(PP); a.o = A.alloc<T>((int64_t)N * D);
+      a.x1 = A.alloc<T>((int64_t)N * D); a.mean2 = A.alloc<T>(N); a.rstd2 = A.alloc<T>(N);
+      a.h2 = A.alloc<T>((int64_t)N * D); a.u = A.alloc<T>((int64_t)N * F); a.gu = A.alloc<T>((int64_t)N * F);
+      ly.push_back(a);
+    }
+    meanf = A.alloc<T>(N); rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D);
+    logits = A.alloc<T>((int64_t)N * V);
+    dx = A.alloc<T>((int64_t)N * D); dx1 = A.alloc<T>((int64_t)N * D); dh = A.alloc<T>((int64_t)N * D);
+    dqkv = A.alloc<T>((int64_t)N * 3 * D); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * D);
+    du = A.alloc<T>((int64_t)N * F);
+  }
+  double tokens_global() const override { return (double)nseq_glob * Tn; }
+  double flops_per_pass() const override {
+    const double lin = (double)Ly * (3.0 * D * D + D * D + 2.0 * D * F) + (double)V * D;
+    const double attn = (double)Ly * 4.0 * Tn * Tn * D * nseq;  // S and PV (full square)
+    return 3.0 * (2.0 * N * lin + attn);
+  }
+  AttnGeom<T> geom() const {
+    AttnGeom<T> g;
+    g.nseq = nseq; g.Tn = Tn; g.Hq = H; g.Hkv = H; g.hd = hd; g.W = 3 * D; g.qo = 0; g.ko = D; g.vo = 2 * D; g.ldo = D;
+    return g;
+  }
+
+  void fwd_bwd(PassIO<T>& io, double* loss_sum) override {
+    const UnitPlan& u0 = plan->units[0];
+    const UnitPlan& uf = plan->units[Ly + 1];
+    const AttnGeom<T> g = geom();
+    // ---------------- forward ----------------
+    {
+      const T* P0 = io.params(0);
+      embed_fwd<T>(L, tok, Tn + 1, nseq, Tn, P0 + u0.t("wte").offset, P0 + u0.t("wpe").offset, xs[0], D);
+    }
+    for (int l = 0; l < Ly; ++l) {
+      const UnitPlan& ub = plan->units[1 + l];
+      const T* Pl = io.params(1 + l);
+      auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
+      Layer& a = ly[l];
+      layernorm_fwd<T>(L, xs[l], w("ln1.g"), w("ln1.b"), a.h1, a.mean1, a.rstd1, N, D, eps);
+      linear_fwd<T>(L, a.h1, D, w("qkv.w"), 3 * D, D, N, a.qkv, 3 * D, w("qkv.b"));
+      attention_fwd<T>(L, g, a.qkv, a.P, a.o);
+      linear_fwd<T>(L, a.o, D, w("proj.w"), D, D, N, a.x1, D, w("proj.b"), xs[l], D);
+      layernorm_fwd<T>(L, a.x1, w("ln2.g"), w("ln2.b"), a.h2, a.mean2, a.rstd2, N, D, eps);
+      linear_fwd<T>(L, a.h2, D, w("fc.w"), F, D, N, a.gu, F, w("fc.b"), nullptr, 0, ACT_GELU, a.u, F);
+      linear_fwd<T>(L, a.gu, F, w("mproj.w"), D, F, N, xs[l + 1], D, w("mproj.b"), a.x1, D);
+    }
+    const T* Pf = io.params(Ly + 1);
+    const T* Whead = tied ? io.params(0) + u0.t("wte").offset : Pf + uf.t("head.w").offset;
+    layernorm_fwd<T>(L, xs[Ly], Pf + uf.t("lnf.g").offset, Pf + uf.t("lnf.b").offset, xf, meanf, rstdf, N, D, eps);
+    linear_fwd<T>(L, xf, D, Whead, V, D, N, logits, V, (const T*)nullptr);
+    cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
+    // ---------------- backward ----------------
+    T* G0 = tied ? io.grads(0) : nullptr;
+    T* Gf = io.grads(Ly + 1);
+    linear_wgrad<T>(L, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("wte").offset : Gf + uf.t("head.w").offset);
+    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dh, D);
+    colreduce<T>(L, 1, dh, D, xs[Ly], meanf, rstdf, Gf + uf.t("lnf.g").offset, Gf + uf.t("lnf.b").offset, N, D,
+                 false);
+    layernorm_bwd<T>(L, dh, xs[Ly], meanf, rstdf, Pf + uf.t("lnf.g").offset, nullptr, dx, N, D);
+    io.grads_done(Ly + 1);
+    for (int l = Ly - 1; l >= 0; --l) {
+      const UnitPlan& ub = plan->units[1 + l];
+      const T* Pl = io.params(1 + l);
+      T* Gl = io.grads(1 + l);
+      auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
+      auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
+      Layer& a = ly[l];
+      // MLP: xs[l+1] = x1 + mproj(gelu(fc(ln2(x1))))
+      linear_wgrad<T>(L, dx, D, a.gu, F, D, F, N, gw("mproj.w"));
+      colreduce<T>(L, 0, dx, D, nullptr, nullptr, nullptr, gw("mproj.b"), nullptr, N, D, false);
+      linear_dgrad<T>(L, dx, D, w("mproj.w"), D, F, N, du, F, ACT_DGELU, a.u, F);
+      linear_wgrad<T>(L, du, F, a.h2, D, F, D, N, gw("fc.w"));
+      colreduce<T>(L, 0, du, F, nullptr, nullptr, nullptr, gw("fc.b"), nullptr, N, F, false);
+      linear_dgrad<T>(L, du, F, w("fc.w"), F, D, N, dh, D);
+      colreduce<T>(L, 1, dh, D, a.x1, a.mean2, a.rstd2, gw("ln2.g"), gw("ln2.b"), N, D, false);
+      layernorm_bwd<T>(L, dh, a.x1, a.mean2, a.rstd2, w("ln2.g"), dx, dx1, N, D);
+      // attention: x1 = xs[l] + proj(attn(ln1(xs[l])))
+      linear_wgrad<T>(L, dx1, D, a.o, D, D, D, N, gw("proj.w"));
+      colreduce<T>(L, 0, dx1, D, nullptr, nullptr, nullptr, gw("proj.b"), nullptr, N, D, false);
+      linear_dgrad<T>(L, dx1, D, w("proj.w"), D, D, N, do_, D);
+      attention_bwd<T>(L, g, a.qkv, a.P, do_, dP, dqkv);
+      linear_wgrad<T>(L, dqkv, 3 * D, a.h1, D, 3 * D, D, N, gw("qkv.w"));
+      colreduce<T>(L, 0, dqkv, 3 * D, nullptr, nullptr, nullptr, gw("qkv.b"), nullptr, N, 3 * D, false);
+      linear_dgrad<T>(L, dqkv, 3 * D, w("qkv.w"), 3 * D, D, N, dh, D);
+      colreduce<T>(L, 1, dh, D, xs[l], a.mean1, a.rstd1, gw("ln1.g"), gw("ln1.b"), N, D, false);
+      layernorm_bwd<T>(L, dh, xs[l], a.mean1, a.rstd1, w("ln1.g"), dx1, dx, N, D);
+      io.grads_done(1 + l);
+    }
+    if (!tied) G0 = io.grads(0);
+    embed_bwd_rows<T>(L, csr_off, csr_pos, dx, G0 + u0.t("wte").offset, V, D, tied);
+    pos_bwd<T>(L, dx, G0 + u0.t("wpe").offset, nseq, Tn, D);
+    io.grads_done(0);
+    sum_rows_f64(L, loss_rows, N, loss_sum);
+  }
+};
+
+// ------------------------------------------------------------------------------------------
+template <class T>
+struct LlamaRunner : Runner<T> {
+  Arena A;
+  Launch L;
+  const LayoutPlan* plan;
+  int nseq, Tn, N, D, Hq, Hkv, hd, F, V, Ly, nseq_glob;
+  int64_t Wq;  // width of the packed q|k|v projection
+  bool tied;
+  double eps;
+  int32_t *tok, *csr_off, *csr_pos;
+  double* loss_rows;
+  T *cos_t, *sin_t;
+  std::vector<T*> xs;
+  struct Layer { T *rstd1, *h1, *qkv, *P, *o, *x1, *rstd2, *h2, *ab, *f; };
+  std::vector<Layer> ly;
+  T *rstdf, *xf, *logits;
+  T *dx, *dx1, *dh, *dqkv, *dP, *do_, *df, *dab;
+
+  LlamaRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
+    nseq = b.n_seq; nseq_glob = b.n_seq_global; Tn = d.seq_len; N = nseq * Tn; D = d.d_model; Hq = d.n_heads;
+    Hkv = d.n_kv_heads; hd = D / Hq; F = d.d_ff; V = d.vocab; Ly = d.n_layers; tied = d.tie_embeddings != 0;
+    eps = d.norm_eps;
+    Wq = (int64_t)(Hq + 2 * Hkv) * hd;
+    tok = upload<int32_t>(A, b.tokens.data(), (int64_t)nseq * (Tn + 1));
+    std::vector<int32_t> off, pos;
+    build_csr(b.tokens, nseq, Tn, V, off, pos);
+    csr_off = upload<int32_t>(A, off.data(), V + 1);
+    csr_pos = upload<int32_t>(A, pos.data(), (int64_t)N);
+    loss_rows = A.alloc<double>(std::max(N, 1));
+    {  // RoPE tables: angle(t, i) = t * theta^(-2i/hd)
+      const int half = hd / 2;
+      std::vector<T> c((size_t)Tn * half), s((size_t)Tn * half);
+      for (int t = 0; t < Tn; ++t)
+        for (int i = 0; i < half; ++i) {
+          const double inv = pow(d.rope_theta, -(2.0 * i) / hd);
+          const double ang = (double)t * inv;
+          c[(size_t)t * half + i] = (T)cos(ang);
+          s[(size_t)t * half + i] = (T)sin(ang);
+        }
+      cos_t = upload<T>(A, c.data(), (int64_t)c.size());
+      sin_t = upload<T>(A, s.data(), (int64_t)s.size());
+    }
+    for (int l = 0; l <= Ly; ++l) xs.push_back(A.alloc<T>((int64_t)N * D));
+    const int64_t PP = (int64_t)nseq * Hq * Tn * Tn;
+    for (int l = 0; l < Ly; ++l) {
+      Layer a;
+      a.rstd1 = A.alloc<T>(N); a.h1 = A.alloc<T>((int64_t)N * D); a.qkv = A.alloc<T>((int64_t)N * Wq);
+      a.P = A.alloc<T>(PP); a.o = A.alloc<T>((int64_t)N * Hq * hd); a.x1 = A.alloc<T>((int64_t)N * D);
+      a.rstd2 = A.alloc<T>(N); a.h2 = A.alloc<T>((int64_t)N * D); a.ab = A.alloc<T>((int64_t)N * 2 * F);
+      a.f = A.alloc<T>((int64_t)N * F);
+      ly.push_back(a);
+    }
+    rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D); logits = A.alloc<T>((int64_t)N * V);
+    dx = A.alloc<T>((int64_t)N * D); dx1 = A.alloc<T>((int64_t)N * D); dh = A.alloc<T>((int64_t)N * D);
+    dqkv = A.alloc<T>((int64_t)N * Wq); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * Hq * hd);
+    df = A.alloc<T>((int64_t)N * F); dab = A.alloc<T>((int64_t)N * 2 * F);
+  }
+  double tokens_global() const override { return (double)nseq_glob * Tn; }
+  double flops_per_pass() const override {
+    const double lin = (double)Ly * ((double)Wq * D + (double)Hq * hd * D + 3.0 * D * F) + (double)V * D;
+    const double attn = (double)Ly * 4.0 * Tn * Tn * Hq * hd * nseq;
+    return 3.0 * (2.0 * N * lin + attn);
+  }
+  AttnGeom<T> geom() const {
+    AttnGeom<T> g;
+    g.nseq = nseq; g.Tn = Tn; g.Hq = Hq; g.Hkv = Hkv; g.hd = hd; g.W = Wq;
+    g.qo = 0; g.ko = (int64_t)Hq * hd; g.vo = (int64_t)(Hq + Hkv) * hd; g.ldo = (int64_t)Hq * hd;
+    return g;
+  }
+
+  void fwd_bwd(PassIO<T>& io, double* loss_sum) override {
+    const UnitPlan& u0 = plan->units[0];
+    const UnitPlan& uf = plan->units[Ly + 1];
+    const AttnGeom<T> g = geom();
+    const int64_t HD = (int64_t)Hq * hd;
+    {
+      const T* P0 = io.params(0);
+      embed_fwd<T>(L, tok, Tn + 1, nseq, Tn, P0 + u0.t("tok").offset, (const T*)nullptr, xs[0], D);
+    }
+    for (int l = 0; l < Ly; ++l) {
+      const UnitPlan& ub = plan->units[1 + l];
+      const T* Pl = io.params(1 + l);
+      auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
+      Layer& a = ly[l];
+      rmsnorm_fwd<T>(L, xs[l], w("attn_norm"), a.h1, a.rstd1, N, D, eps);
+      // wq, wk, wv are contiguous rows of one [Wq x D] matrix in the canonical order
+      linear_fwd<T>(L, a.h1, D, w("wq"), (int)Wq, D, N, a.qkv, Wq, (const T*)nullptr);
+      rope<T>(L, a.qkv + g.qo, Wq, N, Tn, Hq, hd, cos_t, sin_t, false);
+      rope<T>(L, a.qkv + g.ko, Wq, N, Tn, Hkv, hd, cos_t, sin_t, false);
+      attention_fwd<T>(L, g, a.qkv, a.P, a.o);
+      linear_fwd<T>(L, a.o, HD, w("wo"), D, (int)HD, N, a.x1, D, (const T*)nullptr, xs[l], D);
+      rmsnorm_fwd<T>(L, a.x1, w("mlp_norm"), a.h2, a.rstd2, N, D, eps);
+      // wg, wu contiguous: ab = h2 [wg; wu]^T
+      linear_fwd<T>(L, a.h2, D, w("wg"), 2 * F, D, N, a.ab, 2 * F, (const T*)nullptr);
+      swiglu_fwd<T>(L, a.ab, a.f, N, F);
+      linear_fwd<T>(L, a.f, F, w("wd"), D, F, N, xs[l + 1], D, (const T*)nullptr, a.x1, D);
+    }
+    const T* Pf = io.params(Ly + 1);
+    const T* Whead = tied ? io.params(0) + u0.t("tok").offset : Pf + uf.t("head.w").offset;
+    rmsnorm_fwd<T>(L, xs[Ly], Pf + uf.t("norm").offset, xf, rstdf, N, D, eps);
+    linear_fwd<T>(L, xf, D, Whead, V, D, N, logits, V, (const T*)nullptr);
+    cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
+
+    T* G0 = tied ? io.grads(0) : nullptr;
+    T* Gf = io.grads(Ly + 1);
+    linear_wgrad<T>(L, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("tok").offset : Gf + uf.t("head.w").offset);
+    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dh, D);
+    colreduce<T>(L, 2, dh, D, xs[Ly], nullptr, rstdf, Gf + uf.t("norm").offset, nullptr, N, D, false);
+    rmsnorm_bwd<T>(L, dh, xs[Ly], rstdf, Pf + uf.t("norm").offset, nullptr, dx, N, D);
+    io.grads_done(Ly + 1);
+    for (int l = Ly - 1; l >= 0; --l) {
+      const UnitPlan& ub = plan->units[1 + l];
+      const T* Pl = io.params(1 + l);
+      T* Gl = io.grads(1 + l);
+      auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
+      auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
+      Layer& a = ly[l];
+      linear_wgrad<T>(L, dx, D, a.f, F, D, F, N, gw("wd"));
+      linear_dgrad<T>(L, dx, D, w("wd"), D, F, N, df, F);
+      swiglu_bwd<T>(L, df, a.ab, dab, N, F);
+      linear_wgrad<T>(L, dab, 2 * F, a.h2, D, 2 * F, D, N, gw("wg"));
+      linear_dgrad<T>(L, dab, 2 * F, w("wg"), 2 * F, D, N, dh, D);
+      colreduce<T>(L, 2, dh, D, a.x1, nullptr, a.rstd2, gw("mlp_norm"), nullptr, N, D, false);
+      rmsnorm_bwd<T>(L, dh, a.x1, a.rstd2, w("mlp_norm"), dx, dx1, N, D);
+      linear_wgrad<T>(L, dx1, D, a.o, HD, D, (int)HD, N, gw("wo"));
+      linear_dgrad<T>(L, dx1, D, w("wo"), D, (int)HD, N, do_, HD);
+      attention_bwd<T>(L, g, a.qkv, a.P, do_, dP, dqkv);
+      rope<T>(L, dqkv + g.qo, Wq, N, Tn, Hq, hd, cos_t, sin_t, true);
+      rope<T>(L, dqkv + g.ko, Wq, N, Tn, Hkv, hd, cos_t, sin_t, true);
+      linear_wgrad<T>(L, dqkv, Wq, a.h1, D, (int)Wq, D, N, gw("wq"));
+      linear_dgrad<T>(L, dqkv, Wq, w("wq"), (int)Wq, D, N, dh, D);
+      colreduce<T>(L, 2, dh, D, xs[l], nullptr, a.rstd1, gw("attn_norm"), nullptr, N, D, false);
+      rmsnorm_bwd<T>(L, dh, xs[l], a.rstd1, w("attn_norm"), dx1, dx, N, D);
+      io.grads_done(1 + l);
+    }
+    if (!tied) G0 = io.grads(0);
+    embed_bwd_rows<T>(L, csr_off, csr_pos, dx, G0 + u0.t("tok").offset, V, D, tied);
+    io.grads_done(0);
+    sum_rows_f64(L, loss_rows, N, loss_sum);
+  }
+};
+
+}  // namespace
+
+template <class T>
+std::unique_ptr<Runner<T>> make_runner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
+                                       const Launch& L) {
+  if (d.arch == SLQ_ARCH_MLP) return std::unique_ptr<Runner<T>>(new MlpRunner<T>(d, plan, b, L));
+  if (d.arch == SLQ_ARCH_GPT) return std::unique_ptr<Runner<T>>(new GptRunner<T>(d, plan, b, L));
+  return std::unique_ptr<Runner<T>>(new LlamaRunner<T>(d, plan, b, L));
+}
+
+template std::unique_ptr<Runner<double>> make_runner<double>(const slq_model_desc&, const LayoutPlan&,
+                                                             const HostBatch&, const Launch&);
+template std::unique_ptr<Runner<float>> make_runner<float>(const slq_model_desc&, const LayoutPlan&,
+                                                           const HostBatch&, const Launch&);
+
+}  // namespace slq

@@ -1,0 +1,48 @@
+// Gradient-pass runners: one forward + one backward of the dataset-mean loss over this rank's
+// data slice (Alg. 1 lines 5-8 / 10-13), unit by unit through a PassIO that hides the
+// FSDP collectives (per-unit all-gather before forward and again before backward; per-unit
+// reduce-scatter of the gradient after backward).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "kernels.h"
+#include "layout.h"
+
+namespace slq {
+
+template <class T>
+struct PassIO {
+  virtual ~PassIO() {}
+  // full (padded) parameters of unit u in the pass dtype; valid until params() is called for a
+  // unit that maps to the same slot (unit 0 has its own slot, so it may stay live with any other)
+  virtual const T* params(int u) = 0;
+  // buffer receiving the full gradient of unit u (kernels overwrite real entries; unit 0's
+  // buffer persists from the first grads(0) call to grads_done(0))
+  virtual T* grads(int u) = 0;
+  virtual void grads_done(int u) = 0;
+};
+
+struct HostBatch {
+  std::vector<int32_t> tokens;  // [n_seq][seq_len + 1]
+  int n_seq = 0, n_seq_global = 0;
+  std::vector<float> x;  // MLP
+  std::vector<int32_t> y;
+  int n_rows = 0, n_rows_global = 0;
+};
+
+template <class T>
+struct Runner {
+  virtual ~Runner() {}
+  // writes this rank's sum of per-token losses to *loss_sum_dev (device double)
+  virtual void fwd_bwd(PassIO<T>& io, double* loss_sum_dev) = 0;
+  virtual double tokens_global() const = 0;
+  virtual double flops_per_pass() const = 0;  // algorithmic fwd+bwd FLOPs (this rank)
+};
+
+template <class T>
+std::unique_ptr<Runner<T>> make_runner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
+                                       const Launch& L);
+
+}  // namespace slq

@@ -1,0 +1,311 @@
+// Shard-local vector kernels of the FD-HVP / Lanczos path:
+// Rademacher probe from the integer splitmix64 hash, out-of-place fp32 FMA perturbation,
+// the FD difference fused with the three-term update, deterministic fixed-grid reductions
+// (partials in fp64, finalised in a fixed order), and the CGS reorthogonalisation GEMVs.
+// All are HBM-bound streaming kernels: one pass, vectorised where aligned, grids sized in
+// multiples of the 148 SMs.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "kernels.h"
+
+namespace slq {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fixed-order block sum; result valid in thread 0
+__device__ __forceinline__ double block_sum_d(double v) {
+  __shared__ double red[32];
+  v = warp_sum_d(v);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = (l < (int)(blockDim.x / 32)) ? red[l] : 0.0;
+    r = warp_sum_d(r);
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// q[i] = s(seed, gid(i)) / sqrt(P); padding -> 0
+__global__ void k_probe(float* __restrict__ q, int64_t n, const UnitDev* __restrict__ units, int nu, uint64_t key,
+                        double inv_sqrt_P) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nu - 1;
+    while (lo < hi) {  // last unit with local_offset <= i
+      const int mid = (lo + hi + 1) / 2;
+      if (units[mid].local_offset <= i) lo = mid; else hi = mid - 1;
+    }
+    const UnitDev u = units[lo];
+    const int64_t p = u.start_in_unit + (i - u.local_offset);
+    float v = 0.0f;
+    if (p < u.numel) {
+      const uint64_t gid = (uint64_t)(u.global_offset + p);
+      const bool neg = (splitmix64(key ^ gid) >> 63) != 0;
+      v = (float)(neg ? -inv_sqrt_P : inv_sqrt_P);
+    }
+    q[i] = v;
+  }
+}
+
+template <class T>
+__global__ void k_perturb(const float* __restrict__ th, const float* __restrict__ v, float eta, T* __restrict__ plus,
+                          T* __restrict__ minus, int64_t n) {
+  const int64_t n4 = n / 4;
+  const float4* th4 = reinterpret_cast<const float4*>(th);
+  const float4* v4 = reinterpret_cast<const float4*>(v);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 t = th4[i], d = v4[i];
+    const int64_t b = 4 * i;
+    plus[b + 0] = (T)__fmaf_rn(eta, d.x, t.x);
+    plus[b + 1] = (T)__fmaf_rn(eta, d.y, t.y);
+    plus[b + 2] = (T)__fmaf_rn(eta, d.z, t.z);
+    plus[b + 3] = (T)__fmaf_rn(eta, d.w, t.w);
+    minus[b + 0] = (T)__fmaf_rn(-eta, d.x, t.x);
+    minus[b + 1] = (T)__fmaf_rn(-eta, d.y, t.y);
+    minus[b + 2] = (T)__fmaf_rn(-eta, d.z, t.z);
+    minus[b + 3] = (T)__fmaf_rn(-eta, d.w, t.w);
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    plus[i] = (T)__fmaf_rn(eta, v[i], th[i]);
+    minus[i] = (T)__fmaf_rn(-eta, v[i], th[i]);
+  }
+}
+
+__global__ void k_sumsq(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    s += v * v;
+  }
+  s = block_sum_d(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// w = (g+ - g-) * inv2eta - beta_k * q_prev ; partial <w, q_k> (w after fp32 rounding)
+template <class T>
+__global__ void k_fd_w(const T* __restrict__ gp, const T* __restrict__ gm, double inv2eta,
+                       const double* __restrict__ beta_k, const float* __restrict__ q_prev, float* __restrict__ w,
+                       const float* __restrict__ q_k, int64_t n, double* __restrict__ part) {
+  const double b = beta_k ? *beta_k : 0.0;
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double d = ((double)gp[i] - (double)gm[i]) * inv2eta;
+    if (beta_k) d -= b * (double)q_prev[i];
+    const float wf = (float)d;
+    w[i] = wf;
+    if (part) s += (double)wf * (double)q_k[i];
+  }
+  if (part) {
+    s = block_sum_d(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
+template <class T>
+__global__ void k_fd_out(const T* __restrict__ gp, const T* __restrict__ gm, double inv2eta, float* __restrict__ out,
+                         int64_t n, int* __restrict__ nonfinite) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = ((double)gp[i] - (double)gm[i]) * inv2eta;
+    if (!isfinite(d)) bad = 1;
+    out[i] = (float)d;
+  }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+}
+
+template <class T>
+__global__ void k_to_f32(const T* __restrict__ g, float* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)g[i];
+}
+
+// out[j] = sum_b part[b * k + j], fixed order (one block per j)
+__global__ void k_reduce_partials(const double* __restrict__ part, int nb, int k, double* __restrict__ out) {
+  const int j = blockIdx.x;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) s += part[(int64_t)b * k + j];
+  s = block_sum_d(s);
+  if (threadIdx.x == 0) out[j] = s;
+}
+
+// w += sign * coef * q ; optional partial ||w||^2
+__global__ void k_axpy(float* __restrict__ w, const float* __restrict__ q, const double* __restrict__ coef, double sign,
+                       int64_t n, double* __restrict__ part) {
+  const double c = sign * *coef;
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = (float)((double)w[i] + c * (double)q[i]);
+    w[i] = v;
+    s += (double)v * (double)v;
+  }
+  if (part) {
+    s = block_sum_d(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_scale_inv_sqrt(const float* __restrict__ w, const double* __restrict__ sumsq, float* __restrict__ q,
+                                 int64_t n) {
+  const double inv = 1.0 / sqrt(*sumsq);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = (float)((double)w[i] * inv);
+}
+
+constexpr int kReorthChunk = 4096;
+
+// partial c_j = Q[j, chunk] . w[chunk] for all j < k; w chunk staged in smem once
+__global__ void k_reorth_dots(const float* __restrict__ Q, int64_t ldq, int k, const float* __restrict__ w, int64_t n,
+                              double* __restrict__ part) {
+  __shared__ float ws[kReorthChunk];
+  const int64_t base = (int64_t)blockIdx.x * kReorthChunk;
+  const int len = (int)(n - base < (int64_t)kReorthChunk ? n - base : (int64_t)kReorthChunk);
+  for (int i = threadIdx.x; i < kReorthChunk; i += blockDim.x) ws[i] = i < len ? w[base + i] : 0.0f;
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int j = warp; j < k; j += nw) {
+    const float* q = Q + (int64_t)j * ldq + base;
+    double s = 0.0;
+    for (int i = lane; i < len; i += 32) s += (double)q[i] * (double)ws[i];
+    s = warp_sum_d(s);
+    if (lane == 0) part[(int64_t)blockIdx.x * k + j] = s;
+  }
+}
+
+// w -= sum_j c_j Q[j, :] ; optional partial ||w||^2
+__global__ void k_reorth_update(const float* __restrict__ Q, int64_t ldq, int k, const double* __restrict__ c,
+                                float* __restrict__ w, int64_t n, double* __restrict__ part) {
+  extern __shared__ double cs[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) cs[j] = c[j];
+  __syncthreads();
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < k; ++j) acc += cs[j] * (double)Q[(int64_t)j * ldq + i];
+    const float v = (float)((double)w[i] - acc);
+    w[i] = v;
+    s += (double)v * (double)v;
+  }
+  if (part) {
+    s = block_sum_d(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_nonfinite(const float* __restrict__ x, int64_t n, int* flag) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) bad = 1;
+  if (bad) atomicOr(flag, 1);
+}
+
+}  // namespace
+
+#define VLAUNCH(cls, flops, bytes, grid, block, smem, kernel, ...) \
+  do {                                                           \
+    LaunchScope scope_(L.prof, cls, L.stream, flops, bytes);     \
+    kernel<<<grid, block, smem, L.stream>>>(__VA_ARGS__);        \
+    SLQ_CUDA(cudaGetLastError());                                \
+    ++*L.launches;                                               \
+  } while (0)
+
+int vec_nblocks(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kThreads * 4), 148 * 4));
+}
+
+void probe_fill(const Launch& L, float* q, int64_t n, const UnitDev* units, int nu, uint64_t seed, double inv_sqrt_P) {
+  const uint64_t key = [](uint64_t x) {  // host splitmix64(seed)
+    x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }(seed);
+  VLAUNCH(KC_VEC, 0, 4.0 * n, vec_nblocks(n), kThreads, 0, k_probe, q, n, units, nu, key, inv_sqrt_P);
+}
+
+template <class T>
+void perturb(const Launch& L, const float* theta, const float* v, float eta, T* plus, T* minus, int64_t n) {
+  VLAUNCH(KC_PERTURB, 4.0 * n, (8.0 + 2.0 * sizeof(T)) * n, vec_nblocks(n), kThreads, 0, k_perturb<T>, theta, v, eta,
+          plus, minus, n);
+}
+
+void sumsq_partials(const Launch& L, const float* x, int64_t n, double* part) {
+  VLAUNCH(KC_VEC, 2.0 * n, 4.0 * n, vec_nblocks(n), kThreads, 0, k_sumsq, x, n, part);
+}
+
+template <class T>
+void fd_w(const Launch& L, const T* gp, const T* gm, double inv2eta, const double* beta_k, const float* q_prev,
+          float* w, const float* q_k, int64_t n, double* part) {
+  const double bytes = (2.0 * sizeof(T) + 4.0 + (beta_k ? 4.0 : 0.0) + (part ? 4.0 : 0.0)) * n;
+  VLAUNCH(KC_FD, 4.0 * n, bytes, vec_nblocks(n), kThreads, 0, k_fd_w<T>, gp, gm, inv2eta, beta_k, q_prev, w, q_k, n,
+          part);
+}
+
+template <class T>
+void fd_out(const Launch& L, const T* gp, const T* gm, double inv2eta, float* out, int64_t n, int* nonfinite) {
+  VLAUNCH(KC_FD, 2.0 * n, (2.0 * sizeof(T) + 4.0) * n, vec_nblocks(n), kThreads, 0, k_fd_out<T>, gp, gm, inv2eta,
+          out, n, nonfinite);
+}
+
+template <class T>
+void to_f32(const Launch& L, const T* g, float* out, int64_t n) {
+  VLAUNCH(KC_VEC, 0, (sizeof(T) + 4.0) * n, vec_nblocks(n), kThreads, 0, k_to_f32<T>, g, out, n);
+}
+
+void reduce_partials(const Launch& L, const double* part, int nb, int k, double* out) {
+  if (k == 0) return;
+  VLAUNCH(KC_VEC, 0, 8.0 * nb * k, k, 256, 0, k_reduce_partials, part, nb, k, out);
+}
+
+void axpy_dev(const Launch& L, float* w, const float* q, const double* coef, double sign, int64_t n, double* part) {
+  VLAUNCH(KC_VEC, 2.0 * n, 12.0 * n, vec_nblocks(n), kThreads, 0, k_axpy, w, q, coef, sign, n, part);
+}
+
+void scale_by_inv_sqrt(const Launch& L, const float* w, const double* sumsq, float* q, int64_t n) {
+  VLAUNCH(KC_VEC, 1.0 * n, 8.0 * n, vec_nblocks(n), kThreads, 0, k_scale_inv_sqrt, w, sumsq, q, n);
+}
+
+int reorth_nblocks(int64_t n) { return (int)std::max<int64_t>(1, ceil_div(n, kReorthChunk)); }
+
+void reorth_dots(const Launch& L, const float* Q, int64_t ldq, int k, const float* w, int64_t n, double* part) {
+  VLAUNCH(KC_REORTH, 2.0 * k * n, 4.0 * (k + 1.0) * n, reorth_nblocks(n), kThreads, 0, k_reorth_dots, Q, ldq, k, w,
+          n, part);
+}
+
+void reorth_update(const Launch& L, const float* Q, int64_t ldq, int k, const double* c, float* w, int64_t n,
+                   double* part) {
+  VLAUNCH(KC_REORTH, 2.0 * k * n, 4.0 * (k + 2.0) * n, vec_nblocks(n), kThreads, sizeof(double) * k,
+          k_reorth_update, Q, ldq, k, c, w, n, part);
+}
+
+void nonfinite_check(const Launch& L, const float* x, int64_t n, int* flag) {
+  VLAUNCH(KC_VEC, 0, 4.0 * n, vec_nblocks(n), kThreads, 0, k_nonfinite, x, n, flag);
+}
+
+#define VINST(T)                                                                                              \
+  template void perturb<T>(const Launch&, const float*, const float*, float, T*, T*, int64_t);                \
+  template void fd_w<T>(const Launch&, const T*, const T*, double, const double*, const float*, float*,       \
+                        const float*, int64_t, double*);                                                      \
+  template void fd_out<T>(const Launch&, const T*, const T*, double, float*, int64_t, int*);                  \
+  template void to_f32<T>(const Launch&, const T*, float*, int64_t);
+VINST(double)
+VINST(float)
+
+}  // namespace slq
