@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark of the SLQ / FD-HVP hot path (arXiv 2602.00816) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Workload (BASELINE.json configs[1], "c2"): GPT 4 layers, d 256, 4 heads, MLP 1024 GELU, LayerNorm,
+learned positions, vocab 4096, 5,322,240 fp32 params (N(0, 0.02^2) init); global batch 8 x 256
+Zipf(1.1) tokens; FD step eps = 1e-3; Lanczos m = 64 with full reorthogonalisation.  A "step" is
+one Lanczos iteration = one FD-HVP (perturb + two gradient passes + FD difference) + the
+recurrence + CGS2 reorthogonalisation, i.e. every SURVEY §8(a) row.  K steps run as
+ceil(K / 64) probes of <= 64 steps (the config's m), probe seeds 3200 + j.
+
+metric = HVPs/sec (= Lanczos steps/s, whole job).  With N > 1 (torchrun), the 8 sequences are
+split across ranks and theta / every P-vector is FSDP-sharded (strong scaling); each rank's
+CUDA-event time is max-reduced.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import slq_inputs as si  # noqa: E402
+
+METRIC = "HVPs/sec (FD-HVP Lanczos steps/s, c2, m=64 full reorth)"
+UNIT = "HVP/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=64)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def split_batch(cfg, rank, world):
+    tok = si.tokens(cfg)
+    n = tok.shape[0]
+    per = [n // world + (1 if r < n % world else 0) for r in range(world)]
+    s = sum(per[:rank])
+    return tok[s:s + per[rank]], n
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) >= 9:
+                for nm, val in zip(names, r[5:9]):
+                    if "Active" in val and "Not" not in val:
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(kernel_class: str):
+    """Per-launch DRAM bytes of the dominant kernel class from the committed ncu summary."""
+    try:
+        s = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return s.get(kernel_class)
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, budget_s=12.0):
+    """The oracle, as it stands, timed on this host: exact-mode FD-HVPs at the full c2 batch."""
+    from oracle import fdhvp, probe
+    th = si.init_params(cfg)
+    g = fdhvp.make_grad_fn(cfg, si.tokens(cfg))
+    q = probe.rademacher_probe(cfg.probe_seed0, th.size)
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact")
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{n} oracle FD-HVPs (fp64 numpy, 2 gradient passes each) on the full c2 batch "
+                      f"(8 x 256 tokens), {dt:.1f} s; the recurrence/reorth is <1% and excluded"}
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import fdhvp, lanczos as OL, probe
+    th = si.init_params(cfg)
+    g = fdhvp.make_grad_fn(cfg, si.tokens(cfg))
+    op = lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact")
+    OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + 99, th.size), max(args.warmup, 1), "full")
+    t0 = time.perf_counter()
+    done = 0
+    j = 0
+    while done < args.steps:
+        m = min(cfg.m, args.steps - done)
+        OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + j, th.size), m, "full")
+        done += m
+        j += 1
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c2 (oracle, CPU)", "global_batch": cfg.n_seq, "seq_len": cfg.seq_len},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                         "sample": f"{args.steps} oracle Lanczos steps (full reorth) on the full c2 batch"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = si.CONFIGS[args.config]
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2602_00816_b200 import build, slq
+
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    torch.cuda.set_device(local)
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+
+    uid = None
+    if world > 1:
+        obj = [slq.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    tok, n_glob = split_batch(cfg, rank, world)
+    m_run = min(cfg.m, max(args.steps, 1))
+    ctx = slq.SlqContext(cfg, si.init_params(cfg), tok, n_global=n_glob, rank=rank, world_size=world, device=local,
+                         unique_id=uid, pass_numerics="fp64", reorth="full", max_steps=max(cfg.m, args.warmup),
+                         perturb="exact")
+    stream = torch.cuda.ExternalStream(ctx.stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, n):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1)) / n
+
+    def lanczos_steps(K, seed0):
+        done, j = 0, 0
+        while done < K:
+            m = min(cfg.m, K - done)
+            ctx.lanczos(seed0 + j, m)
+            done += m
+            j += 1
+
+    # ---- warm-up (untimed) ----
+    ctx.lanczos(cfg.probe_seed0 + 1000, max(args.warmup, 1))
+
+    # ---- headline: K Lanczos steps, device-resident inputs ----
+    clocks = ClockSampler(local) if rank == 0 else None
+    l0 = ctx.launch_count()
+    ms_step = timed(lambda: lanczos_steps(args.steps, cfg.probe_seed0), args.steps)
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop() if clocks else None
+
+    # ---- per-kernel-class CUDA-event profile over the same K steps ----
+    ctx.profile(True, reset=True)
+    lanczos_steps(args.steps, cfg.probe_seed0)
+    torch.cuda.synchronize()
+    stats = ctx.kernel_stats()
+    ctx.profile(False)
+
+    # ---- standalone HVP, gradient step (same numerics), end-to-end HVP with host buffers ----
+    P_loc = ctx.P_loc
+    lay = ctx.layout()
+    v_full = si.random_vector(ctx.P, 5)
+    v_dev = torch.from_numpy(slq.shard_of(v_full, lay, rank, world)).cuda()
+    out_dev = torch.empty_like(v_dev)
+    nh = max(3, min(args.steps, 16))
+    ctx.hvp(v_dev, out_dev, cfg.eps)
+    hvp_ms = timed(lambda: [ctx.hvp(v_dev, out_dev, cfg.eps) for _ in range(nh)], nh)
+    ctx.grad(None)
+    grad_ms = timed(lambda: [ctx.grad(None) for _ in range(nh)], nh)
+    v_host = torch.from_numpy(slq.shard_of(v_full, lay, rank, world)).pin_memory()
+    out_host = torch.empty(P_loc, dtype=torch.float32).pin_memory()
+    ctx.hvp(v_host, out_host, cfg.eps)
+    e2e_ms = timed(lambda: [ctx.hvp(v_host, out_host, cfg.eps) for _ in range(nh)], nh)
+
+    if rank != 0:
+        ctx.close()
+        if world > 1:
+            dist.barrier()
+        return
+
+    # ---- roofline of the dominant kernel class ----
+    peaks = measured_peaks()
+    dom = max(stats, key=lambda k: stats[k]["ms"])
+    st = stats[dom]
+    total_ms = sum(s["ms"] for s in stats.values())
+    if dom == "gemm":
+        fp64_peak = slq.fp64_peak_tflops(local)
+        achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak,
+                "peak_source": "measured FP64 FMA throughput on this GPU (slq_diag_fp64_peak); "
+                               "fp64 has no tcgen05 kind, so the fp64 passes run on the FP64 pipe"}
+    else:
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        achieved = st["bytes"] / (st["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
+    roof["kernel"] = dom
+    roof["share_of_step"] = st["ms"] / total_ms if total_ms else None
+    roof["launches_per_step"] = st["launches"] / args.steps
+    roof["traffic"] = ncu_traffic(dom)
+
+    value = 1000.0 / ms_step * 1.0  # one global HVP per step, whole job
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: GPT {cfg.n_layers}L d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} "
+                               f"V{cfg.vocab}, {si.n_params(cfg)} fp32 params, {cfg.n_seq}x{cfg.seq_len} Zipf(1.1) "
+                               f"tokens, eps={cfg.eps}, Lanczos m={cfg.m} full CGS2 reorth",
+                   "global_batch": cfg.n_seq, "seq_len": cfg.seq_len, "parallelism": f"fsdp{world}",
+                   "pass_numerics": "fp64", "perturb": "exact",
+                   "l2": "no flush: per-step working set (theta+-, g+- fp64, activations, basis) > 0.5 GB > 126 MB L2"},
+        "s_per_lanczos_step": ms_step / 1000.0,
+        "hvp_per_s_standalone": 1000.0 / hvp_ms,
+        "grad_step_ms": grad_ms,
+        "hvp_over_grad": hvp_ms / grad_ms,
+        "e2e": {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 4 * P_loc,
+                "d2h_bytes_per_step": 4 * P_loc,
+                "what": "slq_hvp with pinned host v and host out (copies inside the call) per step"},
+        "gpu_launches": launches,
+        "kernel_ms_per_step": {k: s["ms"] / args.steps for k, s in stats.items() if s["launches"]},
+        "roofline": roof,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -70,7 +70,16 @@ typedef struct {
   int32_t reorth;          /* SLQ_REORTH_*: Lanczos reorthogonalisation */
   int32_t max_steps;       /* largest m slq_lanczos will be asked for (sizes the Krylov basis) */
   double eps_default;      /* FD step used by slq_lanczos (the north-star signature has no eps) */
+  int32_t perturb;         /* SLQ_PERTURB_*: how theta +- eta v is formed (reading R9) */
 } slq_model_desc;
+
+/* SLQ_PERTURB_EXACT: theta +- eta*v is evaluated in the pass precision (fp64 passes: an fp64
+ *   product and an fp64 sum, divisor 2*eta in fp64), so the perturbed point carries no
+ *   storage-rounding error.  Default.
+ * SLQ_PERTURB_STORAGE: Alg. 1's in-storage perturbation done out of place:
+ *   fmaf(+-fl32(eta), v, theta) rounded once to fp32, divisor 2*fl32(eta).
+ * With fp32 passes both modes form fp32 points (STORAGE semantics). */
+enum { SLQ_PERTURB_EXACT = 0, SLQ_PERTURB_STORAGE = 1 };
 
 /* This rank's slice of the data (Alg. 1 "dataloader").  The loss is the mean token
  * cross-entropy over the GLOBAL batch (sum of w_b = 1), so every rank passes the global
@@ -158,6 +167,10 @@ slq_status slq_collective_counts(const slq_ctx* ctx, int64_t* allgather, int64_t
 /* total kernel launches issued by the library since the context was created */
 int64_t slq_launch_count(const slq_ctx* ctx);
 void* slq_stream(const slq_ctx* ctx);
+
+/* Diagnostic, not on the hot path: measured FP64 FMA throughput of `device` in TFLOP/s (the
+ * roofline denominator of the fp64 gradient-pass GEMMs, which MEASURED_PEAKS.json lacks). */
+slq_status slq_diag_fp64_peak(int32_t device, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -173,6 +173,21 @@ struct EngineT : Engine {
     memcpy(host, hstage, sizeof(double) * cnt);
   }
 
+  // theta+- = theta +- eta v into thp / thm (reading R9); returns 1 / (2 eta_used)
+  double form_points(const float* v, double eta) {
+    if constexpr (sizeof(T) == 8) {
+      if (d.perturb == SLQ_PERTURB_EXACT) {
+        SLQ_CHECK_ARG(eta > 0 && std::isfinite(eta), "eps / ||v|| must be finite and > 0");
+        perturb_exact(L, theta, v, eta, thp, thm, n);
+        return 1.0 / (2.0 * eta);
+      }
+    }
+    const float ef = (float)eta;
+    SLQ_CHECK_ARG(ef > 0.0f && std::isfinite(ef), "eps / ||v|| not representable in fp32");
+    perturb<T>(L, theta, v, ef, thp, thm, n);
+    return 1.0 / (2.0 * (double)ef);
+  }
+
   void hvp(const float* v, float* out, double eps) override {
     sumsq_partials(L, v, n, partials);
     finish_reduce(vec_nblocks(n), 1, dscal + 0);
@@ -184,13 +199,11 @@ struct EngineT : Engine {
       SLQ_CUDA(cudaStreamSynchronize(L.stream));
       return;
     }
-    const float eta = (float)(eps / sqrt(ss));
-    SLQ_CHECK_ARG(eta > 0.0f && std::isfinite(eta), "eps / ||v|| not representable in fp32");
-    perturb<T>(L, theta, v, eta, thp, thm, n);
+    const double inv2eta = form_points(v, eps / sqrt(ss));
     pass(thp, gp, dscal + 2);
     pass(thm, gm, dscal + 2);
     SLQ_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), L.stream));
-    fd_out<T>(L, gp, gm, 1.0 / (2.0 * (double)eta), out, n, dflag);
+    fd_out<T>(L, gp, gm, inv2eta, out, n, dflag);
     int flag = 0;
     SLQ_CUDA(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, L.stream));
     SLQ_CUDA(cudaStreamSynchronize(L.stream));
@@ -216,8 +229,6 @@ struct EngineT : Engine {
     last_info = LanczosInfo();
     SLQ_CHECK_ARG(m >= 1 && m <= max_steps, "1 <= m <= max_steps");
     const bool full = d.reorth == SLQ_REORTH_FULL;
-    const float eps_f = (float)d.eps_default;
-    const double inv2eps = 1.0 / (2.0 * (double)eps_f);
     for (int i = 0; i < m; ++i) alpha[i] = NAN;
     for (int i = 0; i + 1 < m; ++i) beta[i] = NAN;
     LanczosInfo info;
@@ -230,7 +241,7 @@ struct EngineT : Engine {
     for (int k = 0; k < m; ++k) {
       float* qk = qrow(k);
       const float* qprev = k > 0 ? qrow(k - 1) : nullptr;
-      perturb<T>(L, theta, qk, eps_f, thp, thm, n);
+      const double inv2eps = form_points(qk, d.eps_default);
       pass(thp, gp, dscal + 2);
       pass(thm, gm, dscal + 2);
       if (full) {

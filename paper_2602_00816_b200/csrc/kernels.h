@@ -101,6 +101,9 @@ void probe_fill(const Launch& L, float* q, int64_t n_loc, const UnitDev* units, 
                 double inv_sqrt_P);
 template <class T> void perturb(const Launch& L, const float* theta, const float* v, float eta, T* plus,
                                 T* minus, int64_t n);
+// SLQ_PERTURB_EXACT with fp64 passes: plus/minus = theta +- eta*v in fp64 (rounded product, rounded sum)
+void perturb_exact(const Launch& L, const float* theta, const float* v, double eta, double* plus, double* minus,
+                   int64_t n);
 // partial sums of squares / dots -> partials[nblocks * k]; finalize by reduce_partials
 int vec_nblocks(int64_t n);
 void sumsq_partials(const Launch& L, const float* x, int64_t n, double* partials);

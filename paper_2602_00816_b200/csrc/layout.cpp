@@ -15,6 +15,7 @@ void validate_desc(const slq_model_desc& d) {
   SLQ_CHECK_ARG(d.pass_numerics == SLQ_PASS_FP64 || d.pass_numerics == SLQ_PASS_FP32, "pass_numerics");
   SLQ_CHECK_ARG(d.param_dtype == SLQ_PARAM_FP32 || d.param_dtype == SLQ_PARAM_BF16, "param_dtype");
   SLQ_CHECK_ARG(d.reorth == SLQ_REORTH_NONE || d.reorth == SLQ_REORTH_FULL, "reorth");
+  SLQ_CHECK_ARG(d.perturb == SLQ_PERTURB_EXACT || d.perturb == SLQ_PERTURB_STORAGE, "perturb");
   SLQ_CHECK_ARG(d.max_steps >= 1 && d.max_steps <= 4096, "max_steps in [1, 4096]");
   SLQ_CHECK_ARG(d.eps_default > 0, "eps_default > 0");
   if (d.arch == SLQ_ARCH_MLP) {

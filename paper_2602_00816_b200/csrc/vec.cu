@@ -89,6 +89,18 @@ __global__ void k_perturb(const float* __restrict__ th, const float* __restrict_
   }
 }
 
+// theta +- eta*v in fp64 with explicit roundings (product, then sum; no contraction) -- the
+// same two operations, in the same order, as evaluating theta + eta*v in fp64 elementwise
+__global__ void k_perturb_exact(const float* __restrict__ th, const float* __restrict__ v, double eta,
+                                double* __restrict__ plus, double* __restrict__ minus, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double t = (double)th[i];
+    const double d = __dmul_rn(eta, (double)v[i]);
+    plus[i] = __dadd_rn(t, d);
+    minus[i] = __dsub_rn(t, d);
+  }
+}
+
 __global__ void k_sumsq(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -244,6 +256,12 @@ template <class T>
 void perturb(const Launch& L, const float* theta, const float* v, float eta, T* plus, T* minus, int64_t n) {
   VLAUNCH(KC_PERTURB, 4.0 * n, (8.0 + 2.0 * sizeof(T)) * n, vec_nblocks(n), kThreads, 0, k_perturb<T>, theta, v, eta,
           plus, minus, n);
+}
+
+void perturb_exact(const Launch& L, const float* theta, const float* v, double eta, double* plus, double* minus,
+                   int64_t n) {
+  VLAUNCH(KC_PERTURB, 3.0 * n, 24.0 * n, vec_nblocks(n), kThreads, 0, k_perturb_exact, theta, v, eta, plus, minus,
+          n);
 }
 
 void sumsq_partials(const Launch& L, const float* x, int64_t n, double* part) {

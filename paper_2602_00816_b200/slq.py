@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libslq.so")
 SLQ_OK, SLQ_EINVAL, SLQ_ENUMERIC, SLQ_ECUDA, SLQ_ENCCL, SLQ_ETIMEOUT, SLQ_ENOMEM, SLQ_EUNSUPPORTED = 0, 2, 3, 4, 5, 6, 7, 8
 PASS = {"fp64": 0, "fp32": 1}
 REORTH = {"none": 0, "full": 1}
+PERTURB = {"exact": 0, "storage": 1}
 
 
 class SlqError(RuntimeError):
@@ -29,7 +30,8 @@ class ModelDescC(ctypes.Structure):
                 ("tie_embeddings", ctypes.c_int32), ("rope_theta", ctypes.c_double),
                 ("norm_eps", ctypes.c_double), ("param_dtype", ctypes.c_int32),
                 ("pass_numerics", ctypes.c_int32), ("reorth", ctypes.c_int32),
-                ("max_steps", ctypes.c_int32), ("eps_default", ctypes.c_double)]
+                ("max_steps", ctypes.c_int32), ("eps_default", ctypes.c_double),
+                ("perturb", ctypes.c_int32)]
 
 
 class BatchC(ctypes.Structure):
@@ -79,6 +81,7 @@ def lib() -> ctypes.CDLL:
         "slq_collective_counts": (I32, [P, P, P, P]),
         "slq_launch_count": (I64, [P]),
         "slq_stream": (P, [P]),
+        "slq_diag_fp64_peak": (I32, [I32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -95,7 +98,7 @@ def _check(st: int, ctx=None) -> None:
 
 
 def make_desc(cfg, pass_numerics: str = "fp64", reorth: Optional[str] = None, max_steps: Optional[int] = None,
-              eps: Optional[float] = None) -> ModelDescC:
+              eps: Optional[float] = None, perturb: str = "exact") -> ModelDescC:
     """slq_model_desc from a slq_inputs.ModelDesc-like object."""
     d = ModelDescC()
     d.arch = cfg.arch
@@ -110,6 +113,7 @@ def make_desc(cfg, pass_numerics: str = "fp64", reorth: Optional[str] = None, ma
     d.reorth = REORTH[reorth if reorth is not None else ("full" if cfg.reorth_full else "none")]
     d.max_steps = int(max_steps if max_steps is not None else cfg.m)
     d.eps_default = float(eps if eps is not None else cfg.eps)
+    d.perturb = PERTURB[perturb]
     return d
 
 
@@ -151,6 +155,12 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def fp64_peak_tflops(device: int = 0) -> float:
+    t = ctypes.c_double()
+    _check(lib().slq_diag_fp64_peak(device, ctypes.byref(t)))
+    return t.value
+
+
 def kernel_class_names():
     L = lib()
     return [L.slq_kernel_class_name(i).decode() for i in range(L.slq_num_kernel_classes())]
@@ -181,10 +191,10 @@ class SlqContext:
     def __init__(self, cfg, theta0: np.ndarray, batch, *, n_global: Optional[int] = None, rank: int = 0,
                  world_size: int = 1, device: int = 0, stream: Optional[int] = None, unique_id: Optional[bytes] = None,
                  pass_numerics: str = "fp64", reorth: Optional[str] = None, max_steps: Optional[int] = None,
-                 eps: Optional[float] = None):
+                 eps: Optional[float] = None, perturb: str = "exact"):
         L = lib()
         self._keep = []
-        self.desc = make_desc(cfg, pass_numerics, reorth, max_steps, eps)
+        self.desc = make_desc(cfg, pass_numerics, reorth, max_steps, eps, perturb)
         th = np.ascontiguousarray(theta0, dtype=np.float32)
         b = BatchC()
         b.params_host = th.ctypes.data
