@@ -171,6 +171,8 @@ void* slq_stream(const slq_ctx* ctx);
 /* Diagnostic, not on the hot path: measured FP64 FMA throughput of `device` in TFLOP/s (the
  * roofline denominator of the fp64 gradient-pass GEMMs, which MEASURED_PEAKS.json lacks). */
 slq_status slq_diag_fp64_peak(int32_t device, double* tflops);
+/* Diagnostic: measured FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) throughput in TFLOP/s. */
+slq_status slq_diag_dmma_peak(int32_t device, double* tflops);
 
 #ifdef __cplusplus
 }

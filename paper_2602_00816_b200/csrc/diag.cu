@@ -21,7 +21,57 @@ __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;  // keep the chains live
 }
 
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// 8 independent DMMA accumulators per warp
+__global__ void k_dmma_peak(double* out, int iters, double a, double b) {
+  double c[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) c[i] = threadIdx.x * 1e-9 + i;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dmma884(c[2 * j], c[2 * j + 1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += c[i];
+  if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace
+
+extern "C" slq_status slq_diag_dmma_peak(int32_t device, double* tflops) {
+  try {
+    SLQ_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    SLQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* d = nullptr;
+    SLQ_CUDA(cudaMalloc(&d, sizeof(double)));
+    cudaEvent_t a, b;
+    SLQ_CUDA(cudaEventCreate(&a));
+    SLQ_CUDA(cudaEventCreate(&b));
+    const int blocks = sms * 4, threads = 256, iters = 4096;
+    k_dmma_peak<<<blocks, threads>>>(d, 64, 0.5, 1e-3);
+    SLQ_CUDA(cudaEventRecord(a));
+    k_dmma_peak<<<blocks, threads>>>(d, iters, 0.5, 1e-3);
+    SLQ_CUDA(cudaEventRecord(b));
+    SLQ_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    SLQ_CUDA(cudaEventElapsedTime(&ms, a, b));
+    const double flops = 512.0 * 8 * (double)iters * blocks * (threads / 32);
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    return SLQ_OK;
+  } catch (const slq::Error& e) {
+    return e.status;
+  }
+}
 
 extern "C" slq_status slq_diag_fp64_peak(int32_t device, double* tflops) {
   try {

@@ -180,6 +180,139 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// fp64 tensor-core path: mma.sync m8n8k4 f64 (DMMA; measured 37 TFLOP/s on B200 vs 34 for DFMA).
+// CTA tile BM x BN, 4 warps in 2 x 2, warp tile (BM/2) x (BN/2) of 8x8 DMMA tiles; BK = 16;
+// STAGES-deep cp.async pipeline.  Each operand is staged in smem in its global layout (so the
+// copies are straight, coalesced 8-byte cp.async) with a 4-double row pad that makes the
+// fragment reads bank-conflict free: K-contiguous -> [row][k] ld 20, else [k][row] ld BM+4.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int bytes = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int BM, int BN, bool AK, bool BKm>
+struct DmmaCfg {
+  static constexpr int BK = 16, STAGES = 3, THREADS = 128;
+  static constexpr int LDA = AK ? BK + 4 : BM + 4;   // [m][k] or [k][m]
+  static constexpr int LDB = BKm ? BK + 4 : BN + 4;  // [n][k] or [k][n]
+  static constexpr int A_ELEMS = AK ? BM * LDA : BK * LDA;
+  static constexpr int B_ELEMS = BKm ? BN * LDB : BK * LDB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = sizeof(double) * STAGE * STAGES;
+};
+
+template <int BM, int BN, bool AK, bool BKm>
+__global__ void __launch_bounds__(128) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
+                                                        double* __restrict__ ws) {
+  using C = DmmaCfg<BM, BN, AK, BKm>;
+  constexpr int BK = C::BK, S = C::STAGES;
+  constexpr int WM = BM / 2, WN = BN / 2, TM = WM / 8, TN = WN / 8;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int g = lane / 4, t = lane % 4;
+  const int wm = warp / 2, wn = warp % 2;
+  const int z = blockIdx.z / splits, split = blockIdx.z % splits;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const double* __restrict__ A = p.A + boff(p.offA, z);
+  const double* __restrict__ B = p.B + boff(p.offB, z);
+  const int kb = split * kchunk;
+  const int ke = min(p.K, kb + kchunk);
+  const int nk = kb < ke ? (ke - kb + BK - 1) / BK : 0;
+
+  auto load_tile = [&](int kt, int stage) {
+    double* As = smem + stage * C::STAGE;
+    double* Bs = As + C::A_ELEMS;
+    const int k0 = kb + kt * BK;
+#pragma unroll
+    for (int i = tid; i < BM * BK; i += C::THREADS) {
+      int m, k;
+      if (AK) { m = i / BK; k = i % BK; } else { m = i % BM; k = i / BM; }
+      const int gm = m0 + m, gk = k0 + k;
+      const bool ok = gm < p.M && gk < ke;
+      const double* src = ok ? A + (int64_t)gm * p.sAm + (int64_t)gk * p.sAk : A;
+      cp_async8(AK ? &As[m * C::LDA + k] : &As[k * C::LDA + m], src, ok);
+    }
+#pragma unroll
+    for (int i = tid; i < BN * BK; i += C::THREADS) {
+      int n, k;
+      if (BKm) { n = i / BK; k = i % BK; } else { n = i % BN; k = i / BN; }
+      const int gn = n0 + n, gk = k0 + k;
+      const bool ok = gn < p.N && gk < ke;
+      const double* src = ok ? B + (int64_t)gk * p.sBk + (int64_t)gn * p.sBn : B;
+      cp_async8(BKm ? &Bs[n * C::LDB + k] : &Bs[k * C::LDB + n], src, ok);
+    }
+  };
+
+  double acc[TM][TN][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < nk) load_tile(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    if (kt + S - 1 < nk) load_tile(kt + S - 1, (kt + S - 1) % S);
+    cp_async_commit();
+    const double* As = smem + (kt % S) * C::STAGE;
+    const double* Bs = As + C::A_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int m = wm * WM + i * 8 + g, k = ks + t;
+        a[i] = AK ? As[m * C::LDA + k] : As[k * C::LDA + m];
+      }
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int n = wn * WN + j * 8 + g, k = ks + t;
+        b[j] = BKm ? Bs[n * C::LDB + k] : Bs[k * C::LDB + n];
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  double* C_ = splits > 1 ? ws + (int64_t)split * p.M * p.N : p.C + boff(p.offC, z);
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int m = m0 + wm * WM + i * 8 + g;
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + wn * WN + j * 8 + 2 * t + h;
+        if (n >= p.N) continue;
+        if (splits > 1)
+          C_[(int64_t)m * p.N + n] = acc[i][j][h];
+        else
+          epilogue_store(p, C_, m, n, acc[i][j][h]);
+      }
+    }
+  }
+}
+
 template <class T>
 __global__ void splitk_reduce(GemmArgs<T> p, int splits, const T* __restrict__ ws) {
   const int64_t mn = (int64_t)p.M * p.N;
@@ -220,7 +353,72 @@ void launch_cfg(const Launch& L, const GemmArgs<T>& a) {
   }
 }
 
+template <int BM, int BN, bool AK, bool BKm>
+void launch_dmma(const Launch& L, const GemmArgs<double>& a) {
+  using C = DmmaCfg<BM, BN, AK, BKm>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SLQ_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<BM, BN, AK, BKm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)C::SMEM));
+    attr_set = true;
+  }
+  const int tiles_m = (int)ceil_div(a.M, BM), tiles_n = (int)ceil_div(a.N, BN);
+  const int tiles = tiles_m * tiles_n * a.batch;
+  int splits = 1;
+  if (a.batch == 1 && tiles < 2 * 148 && a.K >= 256) {
+    splits = (int)ceil_div(2 * 148, tiles);
+    splits = std::min<int>(splits, (int)(a.K / 128));
+    splits = std::max(1, std::min(splits, 32));
+  }
+  const int kchunk = (int)ceil_div(ceil_div(a.K, splits), C::BK) * C::BK;
+  splits = std::max(1, (int)ceil_div(a.K, kchunk));
+  double* ws = nullptr;
+  if (splits > 1) ws = (double*)L.ws->get(sizeof(double) * (size_t)splits * a.M * a.N, L.stream);
+  dim3 grid(tiles_n, tiles_m, a.batch * splits);
+  LaunchScope scope(L.prof, KC_GEMM, L.stream, 2.0 * a.M * a.N * (double)a.K * a.batch,
+                    8.0 * ((double)a.M * a.K + (double)a.K * a.N + (double)a.M * a.N) * a.batch);
+  gemm_dmma_kernel<BM, BN, AK, BKm><<<grid, C::THREADS, C::SMEM, L.stream>>>(a, splits, kchunk, ws);
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+  if (splits > 1) {
+    const int64_t mn = (int64_t)a.M * a.N;
+    int blocks = (int)std::min<int64_t>(ceil_div(mn, 256), 148 * 8);
+    splitk_reduce<double><<<blocks, 256, 0, L.stream>>>(a, splits, ws);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+}
+
+template <bool AK, bool BKm>
+void dmma_dispatch(const Launch& L, const GemmArgs<double>& a) {
+  const int64_t t64 = ceil_div(a.M, 64) * ceil_div(a.N, 64) * a.batch;
+  if (t64 >= 148 || (a.batch == 1 && a.K >= 256)) {
+    launch_dmma<64, 64, AK, BKm>(L, a);
+  } else if (a.N >= a.M) {
+    launch_dmma<32, 64, AK, BKm>(L, a);
+  } else {
+    launch_dmma<64, 32, AK, BKm>(L, a);
+  }
+}
+
 }  // namespace
+
+template <>
+void gemm<double>(const Launch& L, const GemmArgs<double>& a) {
+  SLQ_CHECK_ARG(a.M >= 0 && a.N >= 0 && a.K >= 0 && a.batch >= 1, "gemm dims");
+  if (a.M == 0 || a.N == 0) return;
+  SLQ_CHECK_ARG(a.sAk == 1 || a.sAm == 1, "gemm A layout");
+  SLQ_CHECK_ARG(a.sBk == 1 || a.sBn == 1, "gemm B layout");
+  SLQ_CHECK_ARG(a.batch == 1 || (!a.resid && !a.aux && !a.C2), "batched gemm epilogue");
+  SLQ_CHECK_ARG(a.act != ACT_GELU || a.C2, "GELU epilogue needs C2");
+  SLQ_CHECK_ARG((a.act != ACT_DGELU && a.act != ACT_DTANH) || a.aux, "derivative epilogue needs aux");
+  const bool ak = a.sAk == 1 && !(a.sAm == 1 && a.K == 1);
+  const bool bk = a.sBk == 1 && !(a.sBn == 1 && a.K == 1);
+  if (ak && bk) dmma_dispatch<true, true>(L, a);
+  else if (ak && !bk) dmma_dispatch<true, false>(L, a);
+  else if (!ak && bk) dmma_dispatch<false, true>(L, a);
+  else dmma_dispatch<false, false>(L, a);
+}
 
 template <class T>
 void gemm(const Launch& L, const GemmArgs<T>& a) {
@@ -239,7 +437,6 @@ void gemm(const Launch& L, const GemmArgs<T>& a) {
   else launch_cfg<T, false, false>(L, a);
 }
 
-template void gemm<double>(const Launch&, const GemmArgs<double>&);
 template void gemm<float>(const Launch&, const GemmArgs<float>&);
 
 }  // namespace slq

@@ -69,17 +69,23 @@ __global__ void k_embed_fwd(const int32_t* __restrict__ tok, int tok_stride, int
 template <class T>
 __global__ void k_embed_bwd_rows(const int32_t* __restrict__ off, const int32_t* __restrict__ pos,
                                  const T* __restrict__ dx, T* __restrict__ dW, int V, int D, bool accumulate) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
-  const int lane = threadIdx.x % kWarp;
-  const int nwarps = gridDim.x * blockDim.x / kWarp;
-  for (int v = warp; v < V; v += nwarps) {
+  // one thread per (v, c); 4 independent partial sums over the token's rows (fixed order)
+  const int64_t total = (int64_t)V * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(i / D), c = (int)(i % D);
     const int s = off[v], e = off[v + 1];
-    for (int c = lane; c < D; c += kWarp) {
-      T acc = T(0);
-      for (int j = s; j < e; ++j) acc += dx[(int64_t)pos[j] * D + c];
-      T* dst = dW + (int64_t)v * D + c;
-      *dst = accumulate ? *dst + acc : acc;
+    T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+    int j = s;
+    for (; j + 3 < e; j += 4) {
+      a0 += dx[(int64_t)pos[j] * D + c];
+      a1 += dx[(int64_t)pos[j + 1] * D + c];
+      a2 += dx[(int64_t)pos[j + 2] * D + c];
+      a3 += dx[(int64_t)pos[j + 3] * D + c];
     }
+    for (; j < e; ++j) a0 += dx[(int64_t)pos[j] * D + c];
+    const T acc = (a0 + a1) + (a2 + a3);
+    T* dst = dW + i;
+    *dst = accumulate ? *dst + acc : acc;
   }
 }
 
@@ -184,36 +190,55 @@ __global__ void k_rmsnorm_bwd(const T* __restrict__ dy, const T* __restrict__ x,
 
 // stage 1 of the column reductions: block (cx, cy) reduces rows [cy*rpb, (cy+1)*rpb) of
 // columns [cx*blockDim, ...) into part[cy][col]
+// block = 32 columns x 8 row lanes; rows [r0, r1) of this block's slab, reduced over the row
+// lanes in shared memory in a fixed order
 template <class T>
 __global__ void k_colreduce1(int mode, const T* __restrict__ dy, int64_t lddy, const T* __restrict__ x,
                              const T* __restrict__ mean, const T* __restrict__ rstd, T* __restrict__ part0,
                              T* __restrict__ part1, int rows, int cols, int rpb) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+  __shared__ T s0[8][33], s1[8][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int c = blockIdx.x * 32 + tx;
   const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
   T a0 = T(0), a1 = T(0);
-  for (int r = r0; r < r1; ++r) {
-    const T d = dy[(int64_t)r * lddy + c];
-    if (mode == 0) {
-      a0 += d;
-    } else if (mode == 1) {
-      a0 += d * (x[(int64_t)r * cols + c] - mean[r]) * rstd[r];
-      a1 += d;
-    } else {
-      a0 += d * x[(int64_t)r * cols + c] * rstd[r];
+  if (c < cols) {
+    for (int r = r0 + ty; r < r1; r += 8) {
+      const T d = dy[(int64_t)r * lddy + c];
+      if (mode == 0) {
+        a0 += d;
+      } else if (mode == 1) {
+        a0 += d * (x[(int64_t)r * cols + c] - mean[r]) * rstd[r];
+        a1 += d;
+      } else {
+        a0 += d * x[(int64_t)r * cols + c] * rstd[r];
+      }
     }
   }
-  part0[(int64_t)blockIdx.y * cols + c] = a0;
-  if (mode == 1) part1[(int64_t)blockIdx.y * cols + c] = a1;
+  s0[ty][tx] = a0;
+  s1[ty][tx] = a1;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    T b0 = T(0), b1 = T(0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      b0 += s0[i][tx];
+      b1 += s1[i][tx];
+    }
+    part0[(int64_t)blockIdx.y * cols + c] = b0;
+    if (mode == 1) part1[(int64_t)blockIdx.y * cols + c] = b1;
+  }
 }
 
+// one warp per column
 template <class T>
 __global__ void k_colreduce2(const T* __restrict__ part, int nparts, T* __restrict__ out, int cols, bool accumulate) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
   if (c >= cols) return;
   T s = T(0);
-  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * cols + c];
-  out[c] = accumulate ? out[c] + s : s;
+  for (int p = lane; p < nparts; p += kWarp) s += part[(int64_t)p * cols + c];
+  s = warp_sum(s);
+  if (lane == 0) out[c] = accumulate ? out[c] + s : s;
 }
 
 // causal softmax over rows of length Tn; row r is query position t = r % Tn (keys j <= t)
@@ -378,8 +403,8 @@ void embed_fwd(const Launch& L, const int32_t* tok, int tok_stride, int nseq, in
 template <class T>
 void embed_bwd_rows(const Launch& L, const int32_t* off, const int32_t* pos, const T* dx, T* dW, int V, int D,
                     bool accumulate) {
-  LAUNCH(KC_EMBED, (int)std::min<int64_t>(ceil_div(V, 8), 148 * 32), 256, k_embed_bwd_rows<T>, off, pos, dx, dW,
-         V, D, accumulate);
+  LAUNCH(KC_EMBED, grid_for((int64_t)V * D, 256, 148 * 32), 256, k_embed_bwd_rows<T>, off, pos, dx, dW, V, D,
+         accumulate);
 }
 template <class T>
 void pos_bwd(const Launch& L, const T* dx, T* dwpe, int nseq, int Tn, int D) {
@@ -412,17 +437,17 @@ template <class T>
 void colreduce(const Launch& L, int mode, const T* dy, int64_t lddy, const T* x, const T* mean, const T* rstd,
                T* out0, T* out1, int rows, int cols, bool accumulate) {
   if (cols == 0) return;
-  const int threads = 128;
-  const int cblocks = (int)ceil_div(cols, threads);
-  int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 16), ceil_div(148 * 8, cblocks)));
+  const int cblocks = (int)ceil_div(cols, 32);
+  int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), ceil_div(2 * 148, cblocks)));
   const int rpb = (int)ceil_div(std::max(rows, 1), rblocks);
   rblocks = (int)ceil_div(std::max(rows, 1), rpb);
   T* part = (T*)L.ws->get(sizeof(T) * 2 * (size_t)rblocks * cols, L.stream);
   T* part1 = part + (size_t)rblocks * cols;
-  LAUNCH(KC_NORM, dim3(cblocks, rblocks), threads, k_colreduce1<T>, mode, dy, lddy, x, mean, rstd, part, part1,
-         rows, cols, rpb);
-  LAUNCH(KC_NORM, cblocks, threads, k_colreduce2<T>, part, rblocks, out0, cols, accumulate);
-  if (mode == 1) LAUNCH(KC_NORM, cblocks, threads, k_colreduce2<T>, part1, rblocks, out1, cols, accumulate);
+  LAUNCH(KC_NORM, dim3(cblocks, rblocks), 256, k_colreduce1<T>, mode, dy, lddy, x, mean, rstd, part, part1, rows,
+         cols, rpb);
+  const int wblocks = (int)ceil_div((int64_t)cols * kWarp, 256);
+  LAUNCH(KC_NORM, wblocks, 256, k_colreduce2<T>, part, rblocks, out0, cols, accumulate);
+  if (mode == 1) LAUNCH(KC_NORM, wblocks, 256, k_colreduce2<T>, part1, rblocks, out1, cols, accumulate);
 }
 template <class T>
 void softmax_causal_fwd(const Launch& L, T* S, int64_t rows, int Tn) {

@@ -82,6 +82,7 @@ def lib() -> ctypes.CDLL:
         "slq_launch_count": (I64, [P]),
         "slq_stream": (P, [P]),
         "slq_diag_fp64_peak": (I32, [I32, P]),
+        "slq_diag_dmma_peak": (I32, [I32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -155,10 +156,17 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def fp64_peak_tflops(device: int = 0) -> float:
-    t = ctypes.c_double()
-    _check(lib().slq_diag_fp64_peak(device, ctypes.byref(t)))
-    return t.value
+def fp64_peak_tflops(device: int = 0) -> dict:
+    """Measured FP64 peaks: DFMA (SIMT pipe) and DMMA (fp64 tensor core), TFLOP/s (best of 3)."""
+    out = {}
+    for key, fn in (("dfma", lib().slq_diag_fp64_peak), ("dmma", lib().slq_diag_dmma_peak)):
+        best = 0.0
+        for _ in range(3):
+            t = ctypes.c_double()
+            _check(fn(device, ctypes.byref(t)))
+            best = max(best, t.value)
+        out[key] = best
+    return out
 
 
 def kernel_class_names():
