@@ -54,9 +54,7 @@ def dist_env():
 def split_batch(cfg, rank, world):
     tok = si.tokens(cfg)
     n = tok.shape[0]
-    per = [n // world + (1 if r < n % world else 0) for r in range(world)]
-    s = sum(per[:rank])
-    return tok[s:s + per[rank]], n
+    return tok[si.rank_slice(n, rank, world)], n
 
 
 class ClockSampler:

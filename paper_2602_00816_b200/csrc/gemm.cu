@@ -4,6 +4,7 @@
 // fused (bias, residual add, GELU / tanh and their derivatives) and a deterministic split-K for
 // the weight-gradient contractions over tokens (K = tokens >> M, N).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "kernels.h"
 
@@ -80,10 +81,13 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   const int tx = tid % (BN / TN), ty = tid / (BN / TN);
   const int z = blockIdx.z / splits, split = blockIdx.z % splits;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (p.tri == TRI_SKIP_UPPER && n0 > m0 + BM - 1) return;
   const T* __restrict__ A = p.A + boff(p.offA, z);
   const T* __restrict__ B = p.B + boff(p.offB, z);
-  const int kb = split * kchunk;
-  const int ke = min(p.K, kb + kchunk);
+  int kb = split * kchunk;
+  int ke = min(p.K, kb + kchunk);
+  if (p.tri == TRI_K_LE_M) ke = min(ke, m0 + BM);
+  if (p.tri == TRI_K_GE_M) kb = max(kb, m0);
 
   T ra[ALD], rb[BLD];
   auto gload = [&](int k0) {
@@ -201,9 +205,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int BM, int BN, bool AK, bool BKm>
+template <int BM, int BN, bool AK, bool BKm, int NSTAGE>
 struct DmmaCfg {
-  static constexpr int BK = 16, STAGES = 3, THREADS = 128;
+  static constexpr int BK = 16, STAGES = NSTAGE, THREADS = 128;
   static constexpr int LDA = AK ? BK + 4 : BM + 4;   // [m][k] or [k][m]
   static constexpr int LDB = BKm ? BK + 4 : BN + 4;  // [n][k] or [k][n]
   static constexpr int A_ELEMS = AK ? BM * LDA : BK * LDA;
@@ -212,10 +216,10 @@ struct DmmaCfg {
   static constexpr size_t SMEM = sizeof(double) * STAGE * STAGES;
 };
 
-template <int BM, int BN, bool AK, bool BKm>
+template <int BM, int BN, bool AK, bool BKm, int NSTAGE>
 __global__ void __launch_bounds__(128) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
                                                         double* __restrict__ ws) {
-  using C = DmmaCfg<BM, BN, AK, BKm>;
+  using C = DmmaCfg<BM, BN, AK, BKm, NSTAGE>;
   constexpr int BK = C::BK, S = C::STAGES;
   constexpr int WM = BM / 2, WN = BN / 2, TM = WM / 8, TN = WN / 8;
   extern __shared__ __align__(16) double smem[];
@@ -224,10 +228,13 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(GemmArgs<double> p, int 
   const int wm = warp / 2, wn = warp % 2;
   const int z = blockIdx.z / splits, split = blockIdx.z % splits;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (p.tri == TRI_SKIP_UPPER && n0 > m0 + BM - 1) return;
   const double* __restrict__ A = p.A + boff(p.offA, z);
   const double* __restrict__ B = p.B + boff(p.offB, z);
-  const int kb = split * kchunk;
-  const int ke = min(p.K, kb + kchunk);
+  int kb = split * kchunk;
+  int ke = min(p.K, kb + kchunk);
+  if (p.tri == TRI_K_LE_M) ke = min(ke, m0 + BM);
+  if (p.tri == TRI_K_GE_M) kb = max(kb, m0);
   const int nk = kb < ke ? (ke - kb + BK - 1) / BK : 0;
 
   auto load_tile = [&](int kt, int stage) {
@@ -329,7 +336,7 @@ void launch_cfg(const Launch& L, const GemmArgs<T>& a) {
   const int tiles_m = (int)ceil_div(a.M, BM), tiles_n = (int)ceil_div(a.N, BN);
   const int tiles = tiles_m * tiles_n * a.batch;
   int splits = 1;
-  if (a.batch == 1 && tiles < 2 * 148 && a.K >= 512) {
+  if (a.batch == 1 && a.tri == TRI_NONE && tiles < 2 * 148 && a.K >= 512) {
     splits = (int)ceil_div(2 * 148, tiles);
     splits = std::min<int>(splits, (int)(a.K / 256));
     splits = std::max(1, std::min(splits, 32));
@@ -353,19 +360,26 @@ void launch_cfg(const Launch& L, const GemmArgs<T>& a) {
   }
 }
 
-template <int BM, int BN, bool AK, bool BKm>
+// algorithmic FLOPs of a (possibly causal-structured) GEMM
+double gemm_flops(const GemmArgs<double>& a, int BM) {
+  double f = 2.0 * a.M * a.N * (double)a.K * a.batch;
+  if (a.tri != TRI_NONE && a.M > 0) f *= std::min(1.0, (a.M + (double)BM) / (2.0 * a.M));
+  return f;
+}
+
+template <int BM, int BN, bool AK, bool BKm, int NSTAGE>
 void launch_dmma(const Launch& L, const GemmArgs<double>& a) {
-  using C = DmmaCfg<BM, BN, AK, BKm>;
+  using C = DmmaCfg<BM, BN, AK, BKm, NSTAGE>;
   static bool attr_set = false;
   if (!attr_set) {
-    SLQ_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<BM, BN, AK, BKm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SLQ_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<BM, BN, AK, BKm, NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)C::SMEM));
     attr_set = true;
   }
   const int tiles_m = (int)ceil_div(a.M, BM), tiles_n = (int)ceil_div(a.N, BN);
   const int tiles = tiles_m * tiles_n * a.batch;
   int splits = 1;
-  if (a.batch == 1 && tiles < 2 * 148 && a.K >= 256) {
+  if (a.batch == 1 && a.tri == TRI_NONE && tiles < 2 * 148 && a.K >= 256) {
     splits = (int)ceil_div(2 * 148, tiles);
     splits = std::min<int>(splits, (int)(a.K / 128));
     splits = std::max(1, std::min(splits, 32));
@@ -375,9 +389,9 @@ void launch_dmma(const Launch& L, const GemmArgs<double>& a) {
   double* ws = nullptr;
   if (splits > 1) ws = (double*)L.ws->get(sizeof(double) * (size_t)splits * a.M * a.N, L.stream);
   dim3 grid(tiles_n, tiles_m, a.batch * splits);
-  LaunchScope scope(L.prof, KC_GEMM, L.stream, 2.0 * a.M * a.N * (double)a.K * a.batch,
+  LaunchScope scope(L.prof, KC_GEMM, L.stream, gemm_flops(a, BM),
                     8.0 * ((double)a.M * a.K + (double)a.K * a.N + (double)a.M * a.N) * a.batch);
-  gemm_dmma_kernel<BM, BN, AK, BKm><<<grid, C::THREADS, C::SMEM, L.stream>>>(a, splits, kchunk, ws);
+  gemm_dmma_kernel<BM, BN, AK, BKm, NSTAGE><<<grid, C::THREADS, C::SMEM, L.stream>>>(a, splits, kchunk, ws);
   SLQ_CUDA(cudaGetLastError());
   ++*L.launches;
   if (splits > 1) {
@@ -389,15 +403,27 @@ void launch_dmma(const Launch& L, const GemmArgs<double>& a) {
   }
 }
 
+int dmma_stages() {
+  static int s = [] {
+    const char* e = getenv("SLQ_DMMA_STAGES");
+    return (e && atoi(e) == 2) ? 2 : 3;
+  }();
+  return s;
+}
+
 template <bool AK, bool BKm>
 void dmma_dispatch(const Launch& L, const GemmArgs<double>& a) {
+  const int stages = dmma_stages();
   const int64_t t64 = ceil_div(a.M, 64) * ceil_div(a.N, 64) * a.batch;
   if (t64 >= 148 || (a.batch == 1 && a.K >= 256)) {
-    launch_dmma<64, 64, AK, BKm>(L, a);
+    if (stages == 2) launch_dmma<64, 64, AK, BKm, 2>(L, a);
+    else launch_dmma<64, 64, AK, BKm, 3>(L, a);
   } else if (a.N >= a.M) {
-    launch_dmma<32, 64, AK, BKm>(L, a);
+    if (stages == 2) launch_dmma<32, 64, AK, BKm, 2>(L, a);
+    else launch_dmma<32, 64, AK, BKm, 3>(L, a);
   } else {
-    launch_dmma<64, 32, AK, BKm>(L, a);
+    if (stages == 2) launch_dmma<64, 32, AK, BKm, 2>(L, a);
+    else launch_dmma<64, 32, AK, BKm, 3>(L, a);
   }
 }
 

@@ -31,6 +31,13 @@ struct BatchOff {
 
 enum Act { ACT_NONE = 0, ACT_GELU = 1, ACT_TANH = 2, ACT_DGELU = 3, ACT_DTANH = 4 };
 
+// causal-attention structure exploited by the batched attention GEMMs (row index = query t,
+// column / k index = key j, nonzero only for j <= t):
+//   TRI_SKIP_UPPER: C tiles entirely above the diagonal are neither computed nor written
+//   TRI_K_LE_M:     A(m, k) == 0 for k > m  -> k loop stops at the tile's last row
+//   TRI_K_GE_M:     A(m, k) == 0 for k < m  -> k loop starts at the tile's first row
+enum Tri { TRI_NONE = 0, TRI_SKIP_UPPER = 1, TRI_K_LE_M = 2, TRI_K_GE_M = 3 };
+
 template <class T>
 struct GemmArgs {
   // C[z](m, n) (+)= epilogue( alpha * sum_k A[z](m, k) * B[z](k, n) )
@@ -54,6 +61,7 @@ struct GemmArgs {
   int64_t ldc2 = 0;
   int act = ACT_NONE;
   bool accumulate = false;  // C += result instead of C = result
+  int tri = TRI_NONE;
 };
 
 template <class T>

@@ -268,12 +268,13 @@ __global__ void k_softmax_bwd(const T* __restrict__ P, T* __restrict__ dP, int64
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kWarp;
   const int lane = threadIdx.x % kWarp;
   if (row >= rows) return;
+  const int t = (int)(row % Tn);
   const T* p = P + row * Tn;
   T* d = dP + row * Tn;
   T s = T(0);
-  for (int j = lane; j < Tn; j += kWarp) s += p[j] * d[j];
+  for (int j = lane; j <= t; j += kWarp) s += p[j] * d[j];  // entries j > t were never computed
   s = warp_sum(s);
-  for (int j = lane; j < Tn; j += kWarp) d[j] = p[j] * (d[j] - s);
+  for (int j = lane; j < Tn; j += kWarp) d[j] = (j <= t) ? p[j] * (d[j] - s) : T(0);
 }
 
 // one block per row: loss_row = lse - logit[tgt];  logits <- (softmax - onehot) * inv_ntok

@@ -96,6 +96,7 @@ void attention_fwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, T* P, T*
     a.B = qkv + g.ko; a.sBk = 1; a.sBn = g.W; a.offB = g.kvoff();
     a.C = P; a.ldc = g.Tn; a.offC = g.poff();
     a.alpha = scale;
+    a.tri = TRI_SKIP_UPPER;
     gemm(L, a);
   }
   softmax_causal_fwd(L, P, (int64_t)g.nseq * g.Hq * g.Tn, g.Tn);
@@ -105,6 +106,7 @@ void attention_fwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, T* P, T*
     a.A = P; a.sAm = g.Tn; a.sAk = 1; a.offA = g.poff();
     a.B = qkv + g.vo; a.sBk = g.W; a.sBn = 1; a.offB = g.kvoff();
     a.C = o; a.ldc = g.ldo; a.offC = g.ooff();
+    a.tri = TRI_K_LE_M;
     gemm(L, a);
   }
 }
@@ -124,6 +126,7 @@ void attention_bwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, const T*
     a.offB = BatchOff{g.Tn * g.ldo, (int64_t)rep * g.hd, g.Hkv, 1};
     a.C = dqkv + g.vo; a.ldc = g.W; a.offC = BatchOff{g.Tn * g.W, g.hd, g.Hkv, 1};
     a.accumulate = r > 0;
+    a.tri = TRI_K_GE_M;
     gemm(L, a);
   }
   {  // dP = dO V^T
@@ -132,6 +135,7 @@ void attention_bwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, const T*
     a.A = dO; a.sAm = g.ldo; a.sAk = 1; a.offA = g.ooff();
     a.B = qkv + g.vo; a.sBk = 1; a.sBn = g.W; a.offB = g.kvoff();
     a.C = dP; a.ldc = g.Tn; a.offC = g.poff();
+    a.tri = TRI_SKIP_UPPER;
     gemm(L, a);
   }
   softmax_bwd(L, P, dP, (int64_t)g.nseq * g.Hq * g.Tn, g.Tn);  // dP <- dS
@@ -142,6 +146,7 @@ void attention_bwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, const T*
     a.B = qkv + g.ko; a.sBk = g.W; a.sBn = 1; a.offB = g.kvoff();
     a.C = dqkv + g.qo; a.ldc = g.W; a.offC = g.qoff();
     a.alpha = scale;
+    a.tri = TRI_K_LE_M;
     gemm(L, a);
   }
   // dK[b, g] = scale * sum_r dS[b, g*rep + r]^T Q[b, g*rep + r]
@@ -155,6 +160,7 @@ void attention_bwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, const T*
     a.C = dqkv + g.ko; a.ldc = g.W; a.offC = BatchOff{g.Tn * g.W, g.hd, g.Hkv, 1};
     a.alpha = scale;
     a.accumulate = r > 0;
+    a.tri = TRI_K_GE_M;
     gemm(L, a);
   }
 }

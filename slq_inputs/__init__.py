@@ -228,6 +228,17 @@ def mlp_data(d: ModelDesc) -> Tuple[np.ndarray, np.ndarray]:
     return x, y
 
 
+def split_counts(n: int, world: int) -> List[int]:
+    """Rows / sequences per rank: the first n % world ranks get one extra (data-parallel slice)."""
+    return [n // world + (1 if r < n % world else 0) for r in range(world)]
+
+
+def rank_slice(n: int, rank: int, world: int) -> slice:
+    c = split_counts(n, world)
+    s = sum(c[:rank])
+    return slice(s, s + c[rank])
+
+
 def random_vector(n: int, seed: int) -> np.ndarray:
     """A generic seeded fp32 direction (for hvp tests with a non-unit v)."""
     return _rng(seed, 77).standard_normal(n).astype(np.float32)
