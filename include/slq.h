@@ -173,6 +173,12 @@ void* slq_stream(const slq_ctx* ctx);
 slq_status slq_diag_fp64_peak(int32_t device, double* tflops);
 /* Diagnostic: measured FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) throughput in TFLOP/s. */
 slq_status slq_diag_dmma_peak(int32_t device, double* tflops);
+/* Diagnostic: time the library's fp64 GEMM on one shape.  A [M x K] (K-contiguous if a_kmajor,
+ * else M-contiguous), B [K x N] (stored [N x K] if b_kmajor, else [K x N]); variant = tile
+ * configuration (-1: production heuristic), splits = split-K factor (0: auto).  Outputs TFLOP/s
+ * over `iters` back-to-back launches and a weighted checksum of C (variants must agree). */
+slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, int32_t K, int32_t a_kmajor, int32_t b_kmajor,
+                             int32_t variant, int32_t splits, int32_t iters, double* tflops, double* checksum);
 
 #ifdef __cplusplus
 }

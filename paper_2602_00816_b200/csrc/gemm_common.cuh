@@ -1,0 +1,75 @@
+// Shared device helpers of the GEMM kernels: epilogues, batch addressing, split-K reduce.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace slq {
+namespace gemm_detail {
+
+
+__device__ __forceinline__ double dtanh_(double x) { return tanh(x); }
+__device__ __forceinline__ float dtanh_(float x) { return tanhf(x); }
+
+template <class T>
+__device__ __forceinline__ T gelu_tanh(T u) {
+  const T c = T(0.7978845608028654);  // sqrt(2/pi)
+  T t = dtanh_(c * (u + T(0.044715) * u * u * u));
+  return T(0.5) * u * (T(1) + t);
+}
+
+template <class T>
+__device__ __forceinline__ T gelu_tanh_grad(T u) {
+  const T c = T(0.7978845608028654);
+  T t = dtanh_(c * (u + T(0.044715) * u * u * u));
+  return T(0.5) * (T(1) + t) + T(0.5) * u * (T(1) - t * t) * c * (T(1) + T(3) * T(0.044715) * u * u);
+}
+
+__device__ __forceinline__ int64_t boff(const BatchOff& o, int z) {
+  return (int64_t)(z / o.div) * o.outer + (int64_t)((z % o.div) / o.rep) * o.inner;
+}
+
+template <class T>
+__device__ __forceinline__ void epilogue_store(const GemmArgs<T>& p, T* C, int m, int n, T acc) {
+  T v = p.alpha * acc;
+  if (p.bias) v += p.bias[n];
+  if (p.resid) v += p.resid[(int64_t)m * p.ldr + n];
+  T out;
+  switch (p.act) {
+    case ACT_GELU:
+      p.C2[(int64_t)m * p.ldc2 + n] = v;
+      out = gelu_tanh(v);
+      break;
+    case ACT_TANH:
+      out = dtanh_(v);
+      break;
+    case ACT_DGELU:
+      out = v * gelu_tanh_grad(p.aux[(int64_t)m * p.ldaux + n]);
+      break;
+    case ACT_DTANH: {
+      T h = p.aux[(int64_t)m * p.ldaux + n];
+      out = v * (T(1) - h * h);
+      break;
+    }
+    default:
+      out = v;
+  }
+  T* dst = C + (int64_t)m * p.ldc + n;
+  if (p.accumulate)
+    *dst += out;
+  else
+    *dst = out;
+}
+
+template <class T>
+__global__ void splitk_reduce(GemmArgs<T> p, int splits, const T* __restrict__ ws) {
+  const int64_t mn = (int64_t)p.M * p.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mn; i += (int64_t)gridDim.x * blockDim.x) {
+    T s = T(0);
+    for (int k = 0; k < splits; ++k) s += ws[k * mn + i];
+    epilogue_store(p, p.C, (int)(i / p.N), (int)(i % p.N), s);
+  }
+}
+
+}  // namespace gemm_detail
+}  // namespace slq

@@ -1,0 +1,364 @@
+// fp64 contractions of the parity gradient passes on the FP64 tensor core:
+// mma.sync.m8n8k4.f64 (DMMA; measured 37 TFLOP/s on B200 vs 34 for DFMA; tcgen05 has no fp64 kind).
+//
+// CTA tile BM x BN, WGM x WGN warps, warp tile (BM/WGM) x (BN/WGN) of 8x8 DMMA tiles; BK-deep
+// k-slices through a STAGES-deep cp.async pipeline.  Each operand is staged in shared memory in
+// its global layout (straight, coalesced 8-byte cp.async) with a row pitch = 4 (mod 16) doubles,
+// which makes the DMMA fragment reads bank-conflict free: K-contiguous -> [row][k], else [k][row].
+// Epilogues (bias, residual, GELU / tanh and derivatives, accumulate) are fused; the weight-
+// gradient contractions over tokens (K >> M, N) use a deterministic split-K.
+#include <cuda_runtime.h>
+#include <stdlib.h>
+
+#include <vector>
+
+#include "gemm_common.cuh"
+
+namespace slq {
+
+namespace {
+
+using namespace gemm_detail;
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int bytes = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int BM_, int BN_, int BK_, int WGM_, int WGN_, int STAGES_>
+struct Tile {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WGM = WGM_, WGN = WGN_, STAGES = STAGES_;
+  static constexpr int THREADS = 32 * WGM * WGN;
+  static constexpr int WM = BM / WGM, WN = BN / WGN, TM = WM / 8, TN = WN / 8;
+  static_assert(TM >= 1 && TN >= 1 && WM % 8 == 0 && WN % 8 == 0, "warp tile");
+};
+
+template <class TL, bool AK, bool BKm>
+struct Smem {
+  static constexpr int LDA = AK ? TL::BK + 4 : TL::BM + 4;
+  static constexpr int LDB = BKm ? TL::BK + 4 : TL::BN + 4;
+  static constexpr int A_ELEMS = AK ? TL::BM * LDA : TL::BK * LDA;
+  static constexpr int B_ELEMS = BKm ? TL::BN * LDB : TL::BK * LDB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr int PIPE = STAGE * TL::STAGES;
+  static constexpr int CTILE = TL::BM * (TL::BN + 1);  // epilogue staging tile
+  static constexpr size_t BYTES = sizeof(double) * (PIPE > CTILE ? PIPE : CTILE);
+};
+
+template <class TL, bool AK, bool BKm>
+__global__ void __launch_bounds__(TL::THREADS) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
+                                                                double* __restrict__ ws) {
+  using SM = Smem<TL, AK, BKm>;
+  constexpr int BM = TL::BM, BN = TL::BN, BK = TL::BK, S = TL::STAGES;
+  constexpr int WM = TL::WM, WN = TL::WN, TM = TL::TM, TN = TL::TN;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int g = lane / 4, t = lane % 4;
+  const int wm = warp / TL::WGN, wn = warp % TL::WGN;
+  const int z = blockIdx.z / splits, split = blockIdx.z % splits;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (p.tri == TRI_SKIP_UPPER && n0 > m0 + BM - 1) return;
+  const double* __restrict__ A = p.A + boff(p.offA, z);
+  const double* __restrict__ B = p.B + boff(p.offB, z);
+  int kb = split * kchunk;
+  int ke = min(p.K, kb + kchunk);
+  if (p.tri == TRI_K_LE_M) ke = min(ke, m0 + BM);
+  if (p.tri == TRI_K_GE_M) kb = max(kb, m0);
+  const int nk = kb < ke ? (ke - kb + BK - 1) / BK : 0;
+
+  auto load_tile = [&](int kt, int stage) {
+    double* As = smem + stage * SM::STAGE;
+    double* Bs = As + SM::A_ELEMS;
+    const int k0 = kb + kt * BK;
+#pragma unroll
+    for (int i = tid; i < BM * BK; i += TL::THREADS) {
+      int m, k;
+      if (AK) { m = i / BK; k = i % BK; } else { m = i % BM; k = i / BM; }
+      const int gm = m0 + m, gk = k0 + k;
+      const bool ok = gm < p.M && gk < ke;
+      const double* src = ok ? A + (int64_t)gm * p.sAm + (int64_t)gk * p.sAk : A;
+      cp_async8(AK ? &As[m * SM::LDA + k] : &As[k * SM::LDA + m], src, ok);
+    }
+#pragma unroll
+    for (int i = tid; i < BN * BK; i += TL::THREADS) {
+      int n, k;
+      if (BKm) { n = i / BK; k = i % BK; } else { n = i % BN; k = i / BN; }
+      const int gn = n0 + n, gk = k0 + k;
+      const bool ok = gn < p.N && gk < ke;
+      const double* src = ok ? B + (int64_t)gk * p.sBk + (int64_t)gn * p.sBn : B;
+      cp_async8(BKm ? &Bs[n * SM::LDB + k] : &Bs[k * SM::LDB + n], src, ok);
+    }
+  };
+
+  double acc[TM][TN][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < nk) load_tile(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    if (kt + S - 1 < nk) load_tile(kt + S - 1, (kt + S - 1) % S);
+    cp_async_commit();
+    const double* As = smem + (kt % S) * SM::STAGE;
+    const double* Bs = As + SM::A_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int m = wm * WM + i * 8 + g, k = ks + t;
+        a[i] = AK ? As[m * SM::LDA + k] : As[k * SM::LDA + m];
+      }
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int n = wn * WN + j * 8 + g, k = ks + t;
+        b[j] = BKm ? Bs[n * SM::LDB + k] : Bs[k * SM::LDB + n];
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // Epilogue: stage the accumulator tile in shared memory (reusing the pipeline buffers), then
+  // one compact loop applies the fused epilogue with row-contiguous, coalesced global stores.
+  // (Inlining the epilogue per accumulator register blew the kernel up to ~15k instructions and
+  // made instruction fetch the top stall.)
+  constexpr int LDC = BN + 1;
+  double* Cs = smem;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int r = wm * WM + i * 8 + g, c = wn * WN + j * 8 + 2 * t;
+      Cs[r * LDC + c] = acc[i][j][0];
+      Cs[r * LDC + c + 1] = acc[i][j][1];
+    }
+  __syncthreads();
+  double* C_ = splits > 1 ? ws + (int64_t)split * p.M * p.N : p.C + boff(p.offC, z);
+  const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
+#pragma unroll 1
+  for (int e = tid; e < BM * BN; e += TL::THREADS) {
+    const int r = e / BN, c = e % BN;
+    if (r >= rows || c >= cols) continue;
+    const double v = Cs[r * LDC + c];
+    if (splits > 1)
+      C_[(int64_t)(m0 + r) * p.N + n0 + c] = v;
+    else
+      epilogue_store(p, C_, m0 + r, n0 + c, v);
+  }
+}
+
+// algorithmic FLOPs of a (possibly causal-structured) GEMM
+double gemm_flops(const GemmArgs<double>& a) {
+  double f = 2.0 * a.M * a.N * (double)a.K * a.batch;
+  if (a.tri != TRI_NONE && a.M > 0) f *= std::min(1.0, (a.M + 64.0) / (2.0 * a.M));
+  return f;
+}
+
+// auto split-K: fill ~2 waves of CTAs when the tile grid is small and K is long
+template <class TL>
+int choose_splits(const GemmArgs<double>& a, int tiles, int forced) {
+  if (forced > 0) return forced;
+  if (a.batch != 1 || a.tri != TRI_NONE || a.K < 256 || tiles >= 2 * 148) return 1;
+  int s = (int)ceil_div(2 * 148, tiles);
+  s = std::min<int>(s, (int)(a.K / (4 * TL::BK)));
+  return std::max(1, std::min(s, 32));
+}
+
+template <class TL, bool AK, bool BKm>
+void launch(const Launch& L, const GemmArgs<double>& a, int forced_splits) {
+  using SM = Smem<TL, AK, BKm>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SLQ_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<TL, AK, BKm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)SM::BYTES));
+    attr_set = true;
+  }
+  const int tiles_m = (int)ceil_div(a.M, TL::BM), tiles_n = (int)ceil_div(a.N, TL::BN);
+  int splits = choose_splits<TL>(a, tiles_m * tiles_n * a.batch, forced_splits);
+  const int kchunk = (int)ceil_div(ceil_div(a.K, splits), TL::BK) * TL::BK;
+  splits = std::max(1, (int)ceil_div(a.K, kchunk));
+  double* ws = nullptr;
+  if (splits > 1) ws = (double*)L.ws->get(sizeof(double) * (size_t)splits * a.M * a.N, L.stream);
+  dim3 grid(tiles_n, tiles_m, a.batch * splits);
+  LaunchScope scope(L.prof, KC_GEMM, L.stream, gemm_flops(a),
+                    8.0 * ((double)a.M * a.K + (double)a.K * a.N + (double)a.M * a.N) * a.batch);
+  gemm_dmma_kernel<TL, AK, BKm><<<grid, TL::THREADS, SM::BYTES, L.stream>>>(a, splits, kchunk, ws);
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+  if (splits > 1) {
+    const int64_t mn = (int64_t)a.M * a.N;
+    int blocks = (int)std::min<int64_t>(ceil_div(mn, 256), 148 * 8);
+    splitk_reduce<double><<<blocks, 256, 0, L.stream>>>(a, splits, ws);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+}
+
+// tile variants (the sweep in tools/gemm_sweep.py picks the heuristic below)
+using V0 = Tile<64, 64, 16, 2, 2, 3>;
+using V1 = Tile<64, 64, 16, 2, 2, 2>;
+using V2 = Tile<64, 64, 32, 2, 2, 2>;
+using V3 = Tile<128, 64, 16, 4, 2, 3>;
+using V4 = Tile<64, 128, 16, 2, 4, 3>;
+using V5 = Tile<128, 128, 16, 2, 4, 2>;
+using V6 = Tile<32, 64, 16, 2, 2, 3>;
+using V7 = Tile<64, 32, 16, 2, 2, 3>;
+using V8 = Tile<128, 64, 32, 4, 2, 2>;
+using V9 = Tile<64, 64, 16, 4, 2, 2>;
+using V10 = Tile<64, 64, 16, 4, 4, 2>;
+using V11 = Tile<64, 32, 16, 4, 2, 3>;
+using V12 = Tile<32, 64, 16, 2, 4, 3>;
+using V13 = Tile<128, 64, 16, 8, 2, 2>;
+using V14 = Tile<64, 64, 32, 4, 4, 2>;
+constexpr int kVariants = 15;
+
+template <bool AK, bool BKm>
+void launch_variant(const Launch& L, const GemmArgs<double>& a, int v, int splits) {
+  switch (v) {
+    case 0: launch<V0, AK, BKm>(L, a, splits); break;
+    case 1: launch<V1, AK, BKm>(L, a, splits); break;
+    case 2: launch<V2, AK, BKm>(L, a, splits); break;
+    case 3: launch<V3, AK, BKm>(L, a, splits); break;
+    case 4: launch<V4, AK, BKm>(L, a, splits); break;
+    case 5: launch<V5, AK, BKm>(L, a, splits); break;
+    case 6: launch<V6, AK, BKm>(L, a, splits); break;
+    case 7: launch<V7, AK, BKm>(L, a, splits); break;
+    case 8: launch<V8, AK, BKm>(L, a, splits); break;
+    case 9: launch<V9, AK, BKm>(L, a, splits); break;
+    case 10: launch<V10, AK, BKm>(L, a, splits); break;
+    case 11: launch<V11, AK, BKm>(L, a, splits); break;
+    case 12: launch<V12, AK, BKm>(L, a, splits); break;
+    case 13: launch<V13, AK, BKm>(L, a, splits); break;
+    default: launch<V14, AK, BKm>(L, a, splits); break;
+  }
+}
+
+int forced_variant() {
+  static int v = [] {
+    const char* e = getenv("SLQ_DMMA_VARIANT");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+
+int pick_variant(const GemmArgs<double>& a) {
+  const int fv = forced_variant();
+  if (fv >= 0 && fv < kVariants) return fv;
+  const int64_t t64 = ceil_div(a.M, 64) * ceil_div(a.N, 64) * a.batch;
+  if (t64 >= 148 || (a.batch == 1 && a.K >= 256)) return 1;
+  return a.N >= a.M ? 6 : 7;
+}
+
+void check(const GemmArgs<double>& a) {
+  SLQ_CHECK_ARG(a.M >= 0 && a.N >= 0 && a.K >= 0 && a.batch >= 1, "gemm dims");
+  SLQ_CHECK_ARG(a.sAk == 1 || a.sAm == 1, "gemm A layout");
+  SLQ_CHECK_ARG(a.sBk == 1 || a.sBn == 1, "gemm B layout");
+  SLQ_CHECK_ARG(a.batch == 1 || (!a.resid && !a.aux && !a.C2), "batched gemm epilogue");
+  SLQ_CHECK_ARG(a.act != ACT_GELU || a.C2, "GELU epilogue needs C2");
+  SLQ_CHECK_ARG((a.act != ACT_DGELU && a.act != ACT_DTANH) || a.aux, "derivative epilogue needs aux");
+}
+
+void run(const Launch& L, const GemmArgs<double>& a, int v, int splits) {
+  const bool ak = a.sAk == 1 && !(a.sAm == 1 && a.K == 1);
+  const bool bk = a.sBk == 1 && !(a.sBn == 1 && a.K == 1);
+  if (ak && bk) launch_variant<true, true>(L, a, v, splits);
+  else if (ak && !bk) launch_variant<true, false>(L, a, v, splits);
+  else if (!ak && bk) launch_variant<false, true>(L, a, v, splits);
+  else launch_variant<false, false>(L, a, v, splits);
+}
+
+__global__ void k_fill(double* x, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    x[i] = (double)((z >> 11) & 0xFFFFF) / 1048576.0 - 0.5;
+  }
+}
+
+}  // namespace
+
+template <>
+void gemm<double>(const Launch& L, const GemmArgs<double>& a) {
+  check(a);
+  if (a.M == 0 || a.N == 0) return;
+  run(L, a, pick_variant(a), 0);
+}
+
+}  // namespace slq
+
+// Diagnostic (not on the hot path): time one fp64 GEMM shape with a given tile variant
+// (-1 = the production heuristic) and split count (0 = auto).  A is [M x K] (K-contiguous when
+// a_kmajor) and B is [K x N] given as [N x K] when b_kmajor.  Returns TFLOP/s and a checksum
+// of C so that variants can be compared for equality.
+extern "C" slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, int32_t K, int32_t a_kmajor,
+                                        int32_t b_kmajor, int32_t variant, int32_t splits, int32_t iters,
+                                        double* tflops, double* checksum) {
+  using namespace slq;
+  double *A = nullptr, *B = nullptr, *C = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  try {
+    SLQ_CUDA(cudaSetDevice(device));
+    SLQ_CUDA(cudaMalloc(&A, sizeof(double) * (size_t)M * K));
+    SLQ_CUDA(cudaMalloc(&B, sizeof(double) * (size_t)N * K));
+    SLQ_CUDA(cudaMalloc(&C, sizeof(double) * (size_t)M * N));
+    k_fill<<<1024, 256>>>(A, (int64_t)M * K, 1);
+    k_fill<<<1024, 256>>>(B, (int64_t)N * K, 2);
+    Workspace ws;
+    int64_t launches = 0;
+    Launch L{0, nullptr, &ws, &launches};
+    GemmArgs<double> a;
+    a.M = M; a.N = N; a.K = K;
+    a.A = A; a.sAm = a_kmajor ? K : 1; a.sAk = a_kmajor ? 1 : M;
+    a.B = B; a.sBk = b_kmajor ? 1 : N; a.sBn = b_kmajor ? K : 1;
+    a.C = C; a.ldc = N;
+    const int v = variant < 0 ? pick_variant(a) : variant;
+    run(L, a, v, splits);  // warm-up (also sets the smem attribute)
+    SLQ_CUDA(cudaEventCreate(&e0));
+    SLQ_CUDA(cudaEventCreate(&e1));
+    SLQ_CUDA(cudaEventRecord(e0));
+    for (int i = 0; i < iters; ++i) run(L, a, v, splits);
+    SLQ_CUDA(cudaEventRecord(e1));
+    SLQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    SLQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *tflops = 2.0 * M * N * (double)K * iters / (ms * 1e-3) / 1e12;
+    std::vector<double> h((size_t)M * N);
+    SLQ_CUDA(cudaMemcpy(h.data(), C, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+    double s = 0;
+    for (size_t i = 0; i < h.size(); ++i) s += h[i] * (double)((i % 7) + 1);
+    *checksum = s;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(A);
+    cudaFree(B);
+    cudaFree(C);
+    return SLQ_OK;
+  } catch (const Error& e) {
+    if (A) cudaFree(A);
+    if (B) cudaFree(B);
+    if (C) cudaFree(C);
+    return e.status;
+  }
+}

@@ -177,6 +177,40 @@ void build_csr(const std::vector<int32_t>& tok, int nseq, int Tn, int V, std::ve
     for (int t = 0; t < Tn; ++t) pos[fill[tok[(size_t)b * (Tn + 1) + t]]++] = b * Tn + t;
 }
 
+// A second stream for the backward work that nothing on the critical path consumes (weight /
+// bias / norm-gain gradients): fork() makes the side stream wait for everything issued on the
+// main stream so far; join() makes the main stream wait for the side stream.  Small GEMMs do not
+// fill the 148 SMs, so the weight-gradient GEMMs overlap the data-gradient chain.
+struct SideStream {
+  Launch main, side;
+  Workspace ws;
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void init(const Launch& L) {
+    main = L;
+    SLQ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    SLQ_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    SLQ_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    side = L;
+    side.stream = s;
+    side.ws = &ws;
+  }
+  void fork() {
+    SLQ_CUDA(cudaEventRecord(ev_fork, main.stream));
+    SLQ_CUDA(cudaStreamWaitEvent(side.stream, ev_fork, 0));
+  }
+  void join() {
+    SLQ_CUDA(cudaEventRecord(ev_join, side.stream));
+    SLQ_CUDA(cudaStreamWaitEvent(main.stream, ev_join, 0));
+  }
+  ~SideStream() {
+    if (s) cudaStreamSynchronize(s);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
 template <class T>
 T* upload(Arena& A, const void* host, int64_t n) {
   T* d = A.alloc<T>(n);
@@ -245,9 +279,11 @@ struct GptRunner : Runner<T> {
   struct Layer { T *mean1, *rstd1, *h1, *qkv, *P, *o, *x1, *mean2, *rstd2, *h2, *u, *gu; };
   std::vector<Layer> ly;
   T *meanf, *rstdf, *xf, *logits;
-  T *dx, *dx1, *dh, *dqkv, *dP, *do_, *du;
+  T *dxs[2], *dx1, *dh1, *dh2, *dqkv, *dP, *do_, *du;
+  SideStream ss;
 
   GptRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
+    ss.init(L);
     nseq = b.n_seq; nseq_glob = b.n_seq_global; Tn = d.seq_len; N = nseq * Tn; D = d.d_model; H = d.n_heads;
     hd = D / H; F = d.d_ff; V = d.vocab; Ly = d.n_layers; tied = d.tie_embeddings != 0; eps = d.norm_eps;
     tok = upload<int32_t>(A, b.tokens.data(), (int64_t)nseq * (Tn + 1));
@@ -268,7 +304,8 @@ struct GptRunner : Runner<T> {
     }
     meanf = A.alloc<T>(N); rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D);
     logits = A.alloc<T>((int64_t)N * V);
-    dx = A.alloc<T>((int64_t)N * D); dx1 = A.alloc<T>((int64_t)N * D); dh = A.alloc<T>((int64_t)N * D);
+    dxs[0] = A.alloc<T>((int64_t)N * D); dxs[1] = A.alloc<T>((int64_t)N * D);
+    dx1 = A.alloc<T>((int64_t)N * D); dh1 = A.alloc<T>((int64_t)N * D); dh2 = A.alloc<T>((int64_t)N * D);
     dqkv = A.alloc<T>((int64_t)N * 3 * D); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * D);
     du = A.alloc<T>((int64_t)N * F);
   }
@@ -312,13 +349,19 @@ struct GptRunner : Runner<T> {
     linear_fwd<T>(L, xf, D, Whead, V, D, N, logits, V, (const T*)nullptr);
     cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
     // ---------------- backward ----------------
+    // weight / bias / gain gradients go to the side stream (Ls); the data-gradient chain stays on L
+    const Launch& Ls = ss.side;
     T* G0 = tied ? io.grads(0) : nullptr;
     T* Gf = io.grads(Ly + 1);
-    linear_wgrad<T>(L, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("wte").offset : Gf + uf.t("head.w").offset);
-    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dh, D);
-    colreduce<T>(L, 1, dh, D, xs[Ly], meanf, rstdf, Gf + uf.t("lnf.g").offset, Gf + uf.t("lnf.b").offset, N, D,
+    int cur = 0;  // dxs[cur] = dL/d(residual stream) entering the current block from above
+    ss.fork();
+    linear_wgrad<T>(Ls, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("wte").offset : Gf + uf.t("head.w").offset);
+    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dh2, D);
+    ss.fork();
+    colreduce<T>(Ls, 1, dh2, D, xs[Ly], meanf, rstdf, Gf + uf.t("lnf.g").offset, Gf + uf.t("lnf.b").offset, N, D,
                  false);
-    layernorm_bwd<T>(L, dh, xs[Ly], meanf, rstdf, Pf + uf.t("lnf.g").offset, nullptr, dx, N, D);
+    layernorm_bwd<T>(L, dh2, xs[Ly], meanf, rstdf, Pf + uf.t("lnf.g").offset, nullptr, dxs[cur], N, D);
+    ss.join();
     io.grads_done(Ly + 1);
     for (int l = Ly - 1; l >= 0; --l) {
       const UnitPlan& ub = plan->units[1 + l];
@@ -327,30 +370,40 @@ struct GptRunner : Runner<T> {
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
       Layer& a = ly[l];
+      T* dx = dxs[cur];
+      T* dxn = dxs[cur ^ 1];
       // MLP: xs[l+1] = x1 + mproj(gelu(fc(ln2(x1))))
-      linear_wgrad<T>(L, dx, D, a.gu, F, D, F, N, gw("mproj.w"));
-      colreduce<T>(L, 0, dx, D, nullptr, nullptr, nullptr, gw("mproj.b"), nullptr, N, D, false);
+      ss.fork();
+      linear_wgrad<T>(Ls, dx, D, a.gu, F, D, F, N, gw("mproj.w"));
+      colreduce<T>(Ls, 0, dx, D, nullptr, nullptr, nullptr, gw("mproj.b"), nullptr, N, D, false);
       linear_dgrad<T>(L, dx, D, w("mproj.w"), D, F, N, du, F, ACT_DGELU, a.u, F);
-      linear_wgrad<T>(L, du, F, a.h2, D, F, D, N, gw("fc.w"));
-      colreduce<T>(L, 0, du, F, nullptr, nullptr, nullptr, gw("fc.b"), nullptr, N, F, false);
-      linear_dgrad<T>(L, du, F, w("fc.w"), F, D, N, dh, D);
-      colreduce<T>(L, 1, dh, D, a.x1, a.mean2, a.rstd2, gw("ln2.g"), gw("ln2.b"), N, D, false);
-      layernorm_bwd<T>(L, dh, a.x1, a.mean2, a.rstd2, w("ln2.g"), dx, dx1, N, D);
+      ss.fork();
+      linear_wgrad<T>(Ls, du, F, a.h2, D, F, D, N, gw("fc.w"));
+      colreduce<T>(Ls, 0, du, F, nullptr, nullptr, nullptr, gw("fc.b"), nullptr, N, F, false);
+      linear_dgrad<T>(L, du, F, w("fc.w"), F, D, N, dh2, D);
+      ss.fork();
+      colreduce<T>(Ls, 1, dh2, D, a.x1, a.mean2, a.rstd2, gw("ln2.g"), gw("ln2.b"), N, D, false);
+      layernorm_bwd<T>(L, dh2, a.x1, a.mean2, a.rstd2, w("ln2.g"), dx, dx1, N, D);
       // attention: x1 = xs[l] + proj(attn(ln1(xs[l])))
-      linear_wgrad<T>(L, dx1, D, a.o, D, D, D, N, gw("proj.w"));
-      colreduce<T>(L, 0, dx1, D, nullptr, nullptr, nullptr, gw("proj.b"), nullptr, N, D, false);
+      ss.fork();
+      linear_wgrad<T>(Ls, dx1, D, a.o, D, D, D, N, gw("proj.w"));
+      colreduce<T>(Ls, 0, dx1, D, nullptr, nullptr, nullptr, gw("proj.b"), nullptr, N, D, false);
       linear_dgrad<T>(L, dx1, D, w("proj.w"), D, D, N, do_, D);
       attention_bwd<T>(L, g, a.qkv, a.P, do_, dP, dqkv);
-      linear_wgrad<T>(L, dqkv, 3 * D, a.h1, D, 3 * D, D, N, gw("qkv.w"));
-      colreduce<T>(L, 0, dqkv, 3 * D, nullptr, nullptr, nullptr, gw("qkv.b"), nullptr, N, 3 * D, false);
-      linear_dgrad<T>(L, dqkv, 3 * D, w("qkv.w"), 3 * D, D, N, dh, D);
-      colreduce<T>(L, 1, dh, D, xs[l], a.mean1, a.rstd1, gw("ln1.g"), gw("ln1.b"), N, D, false);
-      layernorm_bwd<T>(L, dh, xs[l], a.mean1, a.rstd1, w("ln1.g"), dx1, dx, N, D);
+      ss.fork();
+      linear_wgrad<T>(Ls, dqkv, 3 * D, a.h1, D, 3 * D, D, N, gw("qkv.w"));
+      colreduce<T>(Ls, 0, dqkv, 3 * D, nullptr, nullptr, nullptr, gw("qkv.b"), nullptr, N, 3 * D, false);
+      linear_dgrad<T>(L, dqkv, 3 * D, w("qkv.w"), 3 * D, D, N, dh1, D);
+      ss.fork();
+      colreduce<T>(Ls, 1, dh1, D, xs[l], a.mean1, a.rstd1, gw("ln1.g"), gw("ln1.b"), N, D, false);
+      layernorm_bwd<T>(L, dh1, xs[l], a.mean1, a.rstd1, w("ln1.g"), dx1, dxn, N, D);
+      ss.join();  // side reads of dx, du, dx1, dqkv, dh* done before the next block reuses them
       io.grads_done(1 + l);
+      cur ^= 1;
     }
     if (!tied) G0 = io.grads(0);
-    embed_bwd_rows<T>(L, csr_off, csr_pos, dx, G0 + u0.t("wte").offset, V, D, tied);
-    pos_bwd<T>(L, dx, G0 + u0.t("wpe").offset, nseq, Tn, D);
+    embed_bwd_rows<T>(L, csr_off, csr_pos, dxs[cur], G0 + u0.t("wte").offset, V, D, tied);
+    pos_bwd<T>(L, dxs[cur], G0 + u0.t("wpe").offset, nseq, Tn, D);
     io.grads_done(0);
     sum_rows_f64(L, loss_rows, N, loss_sum);
   }
@@ -373,9 +426,11 @@ struct LlamaRunner : Runner<T> {
   struct Layer { T *rstd1, *h1, *qkv, *P, *o, *x1, *rstd2, *h2, *ab, *f; };
   std::vector<Layer> ly;
   T *rstdf, *xf, *logits;
-  T *dx, *dx1, *dh, *dqkv, *dP, *do_, *df, *dab;
+  T *dxs[2], *dx1, *dh1, *dh2, *dqkv, *dP, *do_, *df, *dab;
+  SideStream ss;
 
   LlamaRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
+    ss.init(L);
     nseq = b.n_seq; nseq_glob = b.n_seq_global; Tn = d.seq_len; N = nseq * Tn; D = d.d_model; Hq = d.n_heads;
     Hkv = d.n_kv_heads; hd = D / Hq; F = d.d_ff; V = d.vocab; Ly = d.n_layers; tied = d.tie_embeddings != 0;
     eps = d.norm_eps;
@@ -410,7 +465,8 @@ struct LlamaRunner : Runner<T> {
       ly.push_back(a);
     }
     rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D); logits = A.alloc<T>((int64_t)N * V);
-    dx = A.alloc<T>((int64_t)N * D); dx1 = A.alloc<T>((int64_t)N * D); dh = A.alloc<T>((int64_t)N * D);
+    dxs[0] = A.alloc<T>((int64_t)N * D); dxs[1] = A.alloc<T>((int64_t)N * D);
+    dx1 = A.alloc<T>((int64_t)N * D); dh1 = A.alloc<T>((int64_t)N * D); dh2 = A.alloc<T>((int64_t)N * D);
     dqkv = A.alloc<T>((int64_t)N * Wq); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * Hq * hd);
     df = A.alloc<T>((int64_t)N * F); dab = A.alloc<T>((int64_t)N * 2 * F);
   }
@@ -460,12 +516,17 @@ struct LlamaRunner : Runner<T> {
     linear_fwd<T>(L, xf, D, Whead, V, D, N, logits, V, (const T*)nullptr);
     cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
 
+    const Launch& Ls = ss.side;
     T* G0 = tied ? io.grads(0) : nullptr;
     T* Gf = io.grads(Ly + 1);
-    linear_wgrad<T>(L, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("tok").offset : Gf + uf.t("head.w").offset);
-    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dh, D);
-    colreduce<T>(L, 2, dh, D, xs[Ly], nullptr, rstdf, Gf + uf.t("norm").offset, nullptr, N, D, false);
-    rmsnorm_bwd<T>(L, dh, xs[Ly], rstdf, Pf + uf.t("norm").offset, nullptr, dx, N, D);
+    int cur = 0;
+    ss.fork();
+    linear_wgrad<T>(Ls, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("tok").offset : Gf + uf.t("head.w").offset);
+    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dh2, D);
+    ss.fork();
+    colreduce<T>(Ls, 2, dh2, D, xs[Ly], nullptr, rstdf, Gf + uf.t("norm").offset, nullptr, N, D, false);
+    rmsnorm_bwd<T>(L, dh2, xs[Ly], rstdf, Pf + uf.t("norm").offset, nullptr, dxs[cur], N, D);
+    ss.join();
     io.grads_done(Ly + 1);
     for (int l = Ly - 1; l >= 0; --l) {
       const UnitPlan& ub = plan->units[1 + l];
@@ -474,26 +535,36 @@ struct LlamaRunner : Runner<T> {
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
       Layer& a = ly[l];
-      linear_wgrad<T>(L, dx, D, a.f, F, D, F, N, gw("wd"));
+      T* dx = dxs[cur];
+      T* dxn = dxs[cur ^ 1];
+      ss.fork();
+      linear_wgrad<T>(Ls, dx, D, a.f, F, D, F, N, gw("wd"));
       linear_dgrad<T>(L, dx, D, w("wd"), D, F, N, df, F);
       swiglu_bwd<T>(L, df, a.ab, dab, N, F);
-      linear_wgrad<T>(L, dab, 2 * F, a.h2, D, 2 * F, D, N, gw("wg"));
-      linear_dgrad<T>(L, dab, 2 * F, w("wg"), 2 * F, D, N, dh, D);
-      colreduce<T>(L, 2, dh, D, a.x1, nullptr, a.rstd2, gw("mlp_norm"), nullptr, N, D, false);
-      rmsnorm_bwd<T>(L, dh, a.x1, a.rstd2, w("mlp_norm"), dx, dx1, N, D);
-      linear_wgrad<T>(L, dx1, D, a.o, HD, D, (int)HD, N, gw("wo"));
+      ss.fork();
+      linear_wgrad<T>(Ls, dab, 2 * F, a.h2, D, 2 * F, D, N, gw("wg"));
+      linear_dgrad<T>(L, dab, 2 * F, w("wg"), 2 * F, D, N, dh2, D);
+      ss.fork();
+      colreduce<T>(Ls, 2, dh2, D, a.x1, nullptr, a.rstd2, gw("mlp_norm"), nullptr, N, D, false);
+      rmsnorm_bwd<T>(L, dh2, a.x1, a.rstd2, w("mlp_norm"), dx, dx1, N, D);
+      ss.fork();
+      linear_wgrad<T>(Ls, dx1, D, a.o, HD, D, (int)HD, N, gw("wo"));
       linear_dgrad<T>(L, dx1, D, w("wo"), D, (int)HD, N, do_, HD);
       attention_bwd<T>(L, g, a.qkv, a.P, do_, dP, dqkv);
       rope<T>(L, dqkv + g.qo, Wq, N, Tn, Hq, hd, cos_t, sin_t, true);
       rope<T>(L, dqkv + g.ko, Wq, N, Tn, Hkv, hd, cos_t, sin_t, true);
-      linear_wgrad<T>(L, dqkv, Wq, a.h1, D, (int)Wq, D, N, gw("wq"));
-      linear_dgrad<T>(L, dqkv, Wq, w("wq"), (int)Wq, D, N, dh, D);
-      colreduce<T>(L, 2, dh, D, xs[l], nullptr, a.rstd1, gw("attn_norm"), nullptr, N, D, false);
-      rmsnorm_bwd<T>(L, dh, xs[l], a.rstd1, w("attn_norm"), dx1, dx, N, D);
+      ss.fork();
+      linear_wgrad<T>(Ls, dqkv, Wq, a.h1, D, (int)Wq, D, N, gw("wq"));
+      linear_dgrad<T>(L, dqkv, Wq, w("wq"), (int)Wq, D, N, dh1, D);
+      ss.fork();
+      colreduce<T>(Ls, 2, dh1, D, xs[l], nullptr, a.rstd1, gw("attn_norm"), nullptr, N, D, false);
+      rmsnorm_bwd<T>(L, dh1, xs[l], a.rstd1, w("attn_norm"), dx1, dxn, N, D);
+      ss.join();
       io.grads_done(1 + l);
+      cur ^= 1;
     }
     if (!tied) G0 = io.grads(0);
-    embed_bwd_rows<T>(L, csr_off, csr_pos, dx, G0 + u0.t("tok").offset, V, D, tied);
+    embed_bwd_rows<T>(L, csr_off, csr_pos, dxs[cur], G0 + u0.t("tok").offset, V, D, tied);
     io.grads_done(0);
     sum_rows_f64(L, loss_rows, N, loss_sum);
   }

@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
         "slq_stream": (P, [P]),
         "slq_diag_fp64_peak": (I32, [I32, P]),
         "slq_diag_dmma_peak": (I32, [I32, P]),
+        "slq_diag_gemm_f64": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
