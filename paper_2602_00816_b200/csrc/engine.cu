@@ -251,12 +251,12 @@ struct EngineT : Engine {
         reorth_dots(L, basis, n, k + 1, w, n, partials);
         finish_reduce(nb, k + 1, d_coef);
         SLQ_CUDA(cudaMemcpyAsync(d_alpha + k, d_coef + k, sizeof(double), cudaMemcpyDeviceToDevice, L.stream));
-        reorth_update(L, basis, n, k + 1, d_coef, w, n, nullptr);
-        // CGS pass 2
-        reorth_dots(L, basis, n, k + 1, w, n, partials);
+        // update of pass 1 fused with the partial dots of CGS pass 2
+        reorth_update(L, basis, n, k + 1, d_coef, w, n, partials, nullptr);
         finish_reduce(nb, k + 1, d_coef);
-        reorth_update(L, basis, n, k + 1, d_coef, w, n, partials);
-        finish_reduce(vec_nblocks(n), 1, dscal + 0);
+        // update of pass 2 fused with ||w||^2
+        reorth_update(L, basis, n, k + 1, d_coef, w, n, nullptr, partials);
+        finish_reduce(nb, 1, dscal + 0);
       } else {
         fd_w<T>(L, gp, gm, inv2eps, k > 0 ? d_beta : nullptr, qprev, w, qk, n, partials);
         finish_reduce(vec_nblocks(n), 1, d_alpha + k);

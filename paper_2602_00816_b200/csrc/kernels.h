@@ -127,8 +127,9 @@ void scale_by_inv_sqrt(const Launch& L, const float* w, const double* sumsq, flo
 int reorth_nblocks(int64_t n);
 void reorth_dots(const Launch& L, const float* Q, int64_t ldq, int k, const float* w, int64_t n,
                  double* partials);
+// w -= Q[0:k]^T c; optionally the next pass's partial dots (part_dots [nb x k]) and/or ||w||^2 (part_norm [nb])
 void reorth_update(const Launch& L, const float* Q, int64_t ldq, int k, const double* c, float* w,
-                   int64_t n, double* sumsq_partials_out);
+                   int64_t n, double* part_dots, double* part_norm);
 void nonfinite_check(const Launch& L, const float* x, int64_t n, int* flag);
 
 }  // namespace slq

@@ -183,41 +183,101 @@ __global__ void k_scale_inv_sqrt(const float* __restrict__ w, const double* __re
 
 constexpr int kReorthChunk = 4096;
 
-// partial c_j = Q[j, chunk] . w[chunk] for all j < k; w chunk staged in smem once
-__global__ void k_reorth_dots(const float* __restrict__ Q, int64_t ldq, int k, const float* __restrict__ w, int64_t n,
-                              double* __restrict__ part) {
-  __shared__ float ws[kReorthChunk];
-  const int64_t base = (int64_t)blockIdx.x * kReorthChunk;
-  const int len = (int)(n - base < (int64_t)kReorthChunk ? n - base : (int64_t)kReorthChunk);
-  for (int i = threadIdx.x; i < kReorthChunk; i += blockDim.x) ws[i] = i < len ? w[base + i] : 0.0f;
-  __syncthreads();
+// The CGS kernels work on 4096-element chunks (one block each; the chunk of w lives in shared
+// memory).  Q rows are P_loc apart and P_loc is a multiple of 16, so every chunk is float4-aligned.
+constexpr int kRThreads = 256;
+constexpr int kRGroups = kReorthChunk / 4 / kRThreads;  // float4 groups per thread in the update
+
+// partial dots of the shared-memory chunk ws[0, len) with rows 0..k-1 of Q (one warp per row)
+__device__ __forceinline__ void chunk_dots(const float* __restrict__ Q, int64_t ldq, int k, int64_t base, int len,
+                                           const float* ws, double* __restrict__ part_row) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int n4 = len / 4;
+  const float4* w4 = reinterpret_cast<const float4*>(ws);
   for (int j = warp; j < k; j += nw) {
-    const float* q = Q + (int64_t)j * ldq + base;
-    double s = 0.0;
-    for (int i = lane; i < len; i += 32) s += (double)q[i] * (double)ws[i];
-    s = warp_sum_d(s);
-    if (lane == 0) part[(int64_t)blockIdx.x * k + j] = s;
+    const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + base);
+    double s0 = 0.0, s1 = 0.0;
+    int i = lane;
+    for (; i + 32 < n4; i += 64) {
+      const float4 a = q4[i], b = q4[i + 32], x = w4[i], y = w4[i + 32];
+      s0 += (double)a.x * x.x + (double)a.y * x.y + (double)a.z * x.z + (double)a.w * x.w;
+      s1 += (double)b.x * y.x + (double)b.y * y.y + (double)b.z * y.z + (double)b.w * y.w;
+    }
+    for (; i < n4; i += 32) {
+      const float4 a = q4[i], x = w4[i];
+      s0 += (double)a.x * x.x + (double)a.y * x.y + (double)a.z * x.z + (double)a.w * x.w;
+    }
+    const double s = warp_sum_d(s0 + s1);
+    if (lane == 0) part_row[j] = s;
   }
 }
 
-// w -= sum_j c_j Q[j, :] ; optional partial ||w||^2
-__global__ void k_reorth_update(const float* __restrict__ Q, int64_t ldq, int k, const double* __restrict__ c,
-                                float* __restrict__ w, int64_t n, double* __restrict__ part) {
+// partial c_j = Q[j, chunk] . w[chunk] for all j < k
+__global__ void __launch_bounds__(kRThreads) k_reorth_dots(const float* __restrict__ Q, int64_t ldq, int k,
+                                                           const float* __restrict__ w, int64_t n,
+                                                           double* __restrict__ part) {
+  __shared__ __align__(16) float ws[kReorthChunk];
+  const int64_t base = (int64_t)blockIdx.x * kReorthChunk;
+  const int len = (int)(n - base < (int64_t)kReorthChunk ? n - base : (int64_t)kReorthChunk);
+  const float4* w4 = reinterpret_cast<const float4*>(w + base);
+  for (int i = threadIdx.x; i < len / 4; i += blockDim.x) reinterpret_cast<float4*>(ws)[i] = w4[i];
+  __syncthreads();
+  chunk_dots(Q, ldq, k, base, len, ws, part + (int64_t)blockIdx.x * k);
+}
+
+// w[chunk] -= sum_j c_j Q[j, chunk]; then optionally the next CGS pass's partial dots of the
+// updated chunk (the Q chunk was just streamed, so the re-read mostly hits L2) and/or the
+// partial ||w||^2
+__global__ void __launch_bounds__(kRThreads) k_reorth_update(const float* __restrict__ Q, int64_t ldq, int k,
+                                                             const double* __restrict__ c, float* __restrict__ w,
+                                                             int64_t n, double* __restrict__ part_dots,
+                                                             double* __restrict__ part_norm) {
   extern __shared__ double cs[];
+  __shared__ __align__(16) float ws[kReorthChunk];
   for (int j = threadIdx.x; j < k; j += blockDim.x) cs[j] = c[j];
   __syncthreads();
-  double s = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int j = 0; j < k; ++j) acc += cs[j] * (double)Q[(int64_t)j * ldq + i];
-    const float v = (float)((double)w[i] - acc);
-    w[i] = v;
-    s += (double)v * (double)v;
+  const int64_t base = (int64_t)blockIdx.x * kReorthChunk;
+  const int len = (int)(n - base < (int64_t)kReorthChunk ? n - base : (int64_t)kReorthChunk);
+  const int n4 = len / 4;
+  double acc[kRGroups][4];
+#pragma unroll
+  for (int gi = 0; gi < kRGroups; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.0;
+  for (int j = 0; j < k; ++j) {
+    const double cj = cs[j];
+    const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + base);
+#pragma unroll
+    for (int gi = 0; gi < kRGroups; ++gi) {
+      const int i4 = threadIdx.x + gi * kRThreads;
+      if (i4 < n4) {
+        const float4 q = q4[i4];
+        acc[gi][0] += cj * q.x; acc[gi][1] += cj * q.y; acc[gi][2] += cj * q.z; acc[gi][3] += cj * q.w;
+      }
+    }
   }
-  if (part) {
+  double s = 0.0;
+  float4* wg = reinterpret_cast<float4*>(w + base);
+#pragma unroll
+  for (int gi = 0; gi < kRGroups; ++gi) {
+    const int i4 = threadIdx.x + gi * kRThreads;
+    if (i4 < n4) {
+      const float4 o = wg[i4];
+      float4 v;
+      v.x = (float)((double)o.x - acc[gi][0]);
+      v.y = (float)((double)o.y - acc[gi][1]);
+      v.z = (float)((double)o.z - acc[gi][2]);
+      v.w = (float)((double)o.w - acc[gi][3]);
+      wg[i4] = v;
+      reinterpret_cast<float4*>(ws)[i4] = v;
+      s += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+    }
+  }
+  if (part_norm) {
     s = block_sum_d(s);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    if (threadIdx.x == 0) part_norm[blockIdx.x] = s;
+  }
+  if (part_dots) {
+    __syncthreads();
+    chunk_dots(Q, ldq, k, base, len, ws, part_dots + (int64_t)blockIdx.x * k);
   }
 }
 
@@ -303,14 +363,17 @@ void scale_by_inv_sqrt(const Launch& L, const float* w, const double* sumsq, flo
 int reorth_nblocks(int64_t n) { return (int)std::max<int64_t>(1, ceil_div(n, kReorthChunk)); }
 
 void reorth_dots(const Launch& L, const float* Q, int64_t ldq, int k, const float* w, int64_t n, double* part) {
-  VLAUNCH(KC_REORTH, 2.0 * k * n, 4.0 * (k + 1.0) * n, reorth_nblocks(n), kThreads, 0, k_reorth_dots, Q, ldq, k, w,
-          n, part);
+  SLQ_CHECK_ARG(n % 4 == 0 && ldq % 4 == 0, "reorth needs float4-aligned shards");
+  VLAUNCH(KC_REORTH, 2.0 * k * n, 4.0 * (k + 1.0) * n, reorth_nblocks(n), kRThreads, 0, k_reorth_dots, Q, ldq, k,
+          w, n, part);
 }
 
 void reorth_update(const Launch& L, const float* Q, int64_t ldq, int k, const double* c, float* w, int64_t n,
-                   double* part) {
-  VLAUNCH(KC_REORTH, 2.0 * k * n, 4.0 * (k + 2.0) * n, vec_nblocks(n), kThreads, sizeof(double) * k,
-          k_reorth_update, Q, ldq, k, c, w, n, part);
+                   double* part_dots, double* part_norm) {
+  SLQ_CHECK_ARG(n % 4 == 0 && ldq % 4 == 0, "reorth needs float4-aligned shards");
+  // algorithmic bytes: Q once from HBM (the fused dots re-read is the L2-resident chunk) + w r/w
+  VLAUNCH(KC_REORTH, (part_dots ? 4.0 : 2.0) * k * n, 4.0 * (k + 2.0) * n, reorth_nblocks(n), kRThreads,
+          sizeof(double) * k, k_reorth_update, Q, ldq, k, c, w, n, part_dots, part_norm);
 }
 
 void nonfinite_check(const Launch& L, const float* x, int64_t n, int* flag) {
