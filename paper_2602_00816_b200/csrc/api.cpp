@@ -68,6 +68,8 @@ struct Profiler {
   }
 };
 
+bool prof_enabled(const Profiler* p) { return p && p->on; }
+
 void prof_begin(Profiler* p, int, cudaStream_t s) {
   if (!p || !p->on) return;
   p->open = p->take();

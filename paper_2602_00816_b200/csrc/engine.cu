@@ -142,13 +142,15 @@ struct EngineT : Engine {
   }
   ~EngineT() override {
     cudaStreamSynchronize(L.stream);
+    for (auto& x : graphs)
+      if (x.exec) cudaGraphExecDestroy(x.exec);
     for (void* p : allocs) cudaFree(p);
     if (hstage) cudaFreeHost(hstage);
   }
 
   double pass_flops() const override { return runner->flops_per_pass(); }
 
-  void pass(const T* th, T* g, double* loss_dev) {
+  void pass_eager(const T* th, T* g, double* loss_dev) {
     if (comm) {
       fio.shard = th;
       fio.gshard = g;
@@ -158,6 +160,57 @@ struct EngineT : Engine {
       lio.gshard = g;
       runner->fwd_bwd(lio, loss_dev);
     }
+  }
+
+  // One gradient pass.  After a first eager run (which sizes every workspace), the ~400 launches
+  // of a pass are captured once per (theta, grad) buffer pair into a CUDA graph and replayed;
+  // the per-class profiler needs eager launches, so profiling runs bypass the graphs.
+  struct PassGraph {
+    const void* th;
+    void* g;
+    cudaGraphExec_t exec;
+    int64_t launches;
+    int eager_runs;
+  };
+  std::vector<PassGraph> graphs;
+  bool use_graphs = getenv("SLQ_NO_GRAPHS") == nullptr;
+
+  void pass(const T* th, T* g, double* loss_dev) {
+    if (!use_graphs || (L.prof && prof_enabled(L.prof))) {
+      pass_eager(th, g, loss_dev);
+      return;
+    }
+    PassGraph* pg = nullptr;
+    for (auto& x : graphs)
+      if (x.th == th && x.g == g) pg = &x;
+    if (!pg) {
+      graphs.push_back(PassGraph{th, g, nullptr, 0, 0});
+      pg = &graphs.back();
+    }
+    if (pg->exec) {
+      SLQ_CUDA(cudaGraphLaunch(pg->exec, L.stream));
+      *L.launches += pg->launches;
+      return;
+    }
+    if (pg->eager_runs++ == 0) {  // warm-up: allocate workspaces at their final sizes
+      pass_eager(th, g, loss_dev);
+      return;
+    }
+    const int64_t l0 = *L.launches;
+    cudaGraph_t graph = nullptr;
+    SLQ_CUDA(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      pass_eager(th, g, loss_dev);
+    } catch (...) {
+      cudaStreamEndCapture(L.stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    SLQ_CUDA(cudaStreamEndCapture(L.stream, &graph));
+    SLQ_CUDA(cudaGraphInstantiate(&pg->exec, graph, 0));
+    SLQ_CUDA(cudaGraphDestroy(graph));
+    pg->launches = *L.launches - l0;
+    SLQ_CUDA(cudaGraphLaunch(pg->exec, L.stream));
   }
 
   // fixed-order reduction of `k` partial columns into out (device), then all-reduce
