@@ -57,6 +57,97 @@ struct FsdpIO : PassIO<T> {
   }
 };
 
+// One gradient-pass executor: a runner (its own activation buffers) bound to a stream.  After a
+// first eager run (which sizes every workspace) the ~400 launches of a pass are captured once per
+// (theta, grad) buffer pair into a CUDA graph and replayed; profiling runs stay eager because the
+// per-class profiler records events around individual launches.
+template <class T>
+struct PassExec {
+  Launch L;
+  Workspace own_ws;
+  cudaStream_t own_stream = nullptr;
+  std::unique_ptr<Runner<T>> runner;
+  LocalIO<T> lio;
+  FsdpIO<T>* fio = nullptr;
+  struct Graph {
+    const void* th;
+    void* g;
+    cudaGraphExec_t exec;
+    int64_t launches;
+    int eager_runs;
+  };
+  std::vector<Graph> graphs;
+  bool use_graphs = getenv("SLQ_NO_GRAPHS") == nullptr;
+
+  PassExec(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b, const Launch& base, bool own) {
+    L = base;
+    if (own) {
+      SLQ_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+      L.stream = own_stream;
+      L.ws = &own_ws;
+    }
+    runner = make_runner<T>(d, plan, b, L);
+    lio.plan = &plan;
+  }
+  ~PassExec() {
+    if (L.stream) cudaStreamSynchronize(L.stream);
+    for (auto& x : graphs)
+      if (x.exec) cudaGraphExecDestroy(x.exec);
+    runner.reset();
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+
+  void eager(const T* th, T* g, double* loss_dev) {
+    if (fio) {
+      fio->shard = th;
+      fio->gshard = g;
+      runner->fwd_bwd(*fio, loss_dev);
+    } else {
+      lio.shard = th;
+      lio.gshard = g;
+      runner->fwd_bwd(lio, loss_dev);
+    }
+  }
+
+  void run(const T* th, T* g, double* loss_dev) {
+    if (!use_graphs || prof_enabled(L.prof)) {
+      eager(th, g, loss_dev);
+      return;
+    }
+    Graph* pg = nullptr;
+    for (auto& x : graphs)
+      if (x.th == th && x.g == g) pg = &x;
+    if (!pg) {
+      graphs.push_back(Graph{th, g, nullptr, 0, 0});
+      pg = &graphs.back();
+    }
+    if (pg->exec) {
+      SLQ_CUDA(cudaGraphLaunch(pg->exec, L.stream));
+      *L.launches += pg->launches;
+      return;
+    }
+    if (pg->eager_runs++ == 0) {
+      eager(th, g, loss_dev);
+      return;
+    }
+    const int64_t l0 = *L.launches;
+    cudaGraph_t graph = nullptr;
+    SLQ_CUDA(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      eager(th, g, loss_dev);
+    } catch (...) {
+      cudaStreamEndCapture(L.stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    SLQ_CUDA(cudaStreamEndCapture(L.stream, &graph));
+    SLQ_CUDA(cudaGraphInstantiate(&pg->exec, graph, 0));
+    SLQ_CUDA(cudaGraphDestroy(graph));
+    pg->launches = *L.launches - l0;
+    SLQ_CUDA(cudaGraphLaunch(pg->exec, L.stream));
+  }
+};
+
 template <class T>
 struct EngineT : Engine {
   slq_model_desc d;
@@ -74,9 +165,14 @@ struct EngineT : Engine {
   int* dflag;
   UnitDev* units_dev;
   int max_steps;
-  std::unique_ptr<Runner<T>> runner;
-  LocalIO<T> lio;
   FsdpIO<T> fio;
+  // pe[0] runs on the context stream; with world_size == 1 a second executor on its own stream
+  // evaluates the theta- pass concurrently with the theta+ pass (the two gradient evaluations of
+  // Eq. (1) are independent until the FD difference).  With FSDP both passes share the NCCL
+  // communicator, so they stay serial.
+  std::unique_ptr<PassExec<T>> pe[2];
+  bool dual = false;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   double* hstage;  // pinned host scalars
 
   template <class U>
@@ -125,8 +221,7 @@ struct EngineT : Engine {
       SLQ_CUDA(cudaMemcpy(units_dev, ud.data(), sizeof(UnitDev) * ud.size(), cudaMemcpyHostToDevice));
     }
     SLQ_CUDA(cudaMallocHost(&hstage, 64 * sizeof(double)));
-    runner = make_runner<T>(d, plan, b, L);
-    lio.plan = &plan;
+    pe[0].reset(new PassExec<T>(d, plan, b, L, false));
     fio.plan = &plan;
     fio.comm = comm;
     fio.s = L.stream;
@@ -137,81 +232,41 @@ struct EngineT : Engine {
       fio.gbuf0 = dalloc<T>(plan.units[0].padded);
       fio.pbuf1 = dalloc<T>(mx);
       fio.gbuf1 = dalloc<T>(mx);
+      pe[0]->fio = &fio;
+    } else if (getenv("SLQ_SERIAL_PASSES") == nullptr) {
+      pe[1].reset(new PassExec<T>(d, plan, b, L, true));
+      dual = true;
+      SLQ_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
+      SLQ_CUDA(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
     }
-    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    SLQ_CUDA(cudaDeviceSynchronize());
   }
   ~EngineT() override {
     cudaStreamSynchronize(L.stream);
-    for (auto& x : graphs)
-      if (x.exec) cudaGraphExecDestroy(x.exec);
+    pe[1].reset();
+    pe[0].reset();
+    if (ev_a) cudaEventDestroy(ev_a);
+    if (ev_b) cudaEventDestroy(ev_b);
     for (void* p : allocs) cudaFree(p);
     if (hstage) cudaFreeHost(hstage);
   }
 
-  double pass_flops() const override { return runner->flops_per_pass(); }
-
-  void pass_eager(const T* th, T* g, double* loss_dev) {
-    if (comm) {
-      fio.shard = th;
-      fio.gshard = g;
-      runner->fwd_bwd(fio, loss_dev);
-    } else {
-      lio.shard = th;
-      lio.gshard = g;
-      runner->fwd_bwd(lio, loss_dev);
+  // g+ = grad L(theta+), g- = grad L(theta-): concurrently on two streams when dual
+  void two_passes() {
+    if (!dual) {
+      pe[0]->run(thp, gp, dscal + 2);
+      pe[0]->run(thm, gm, dscal + 3);
+      return;
     }
+    SLQ_CUDA(cudaEventRecord(ev_a, L.stream));
+    SLQ_CUDA(cudaStreamWaitEvent(pe[1]->L.stream, ev_a, 0));
+    pe[0]->run(thp, gp, dscal + 2);
+    pe[1]->run(thm, gm, dscal + 3);
+    SLQ_CUDA(cudaEventRecord(ev_b, pe[1]->L.stream));
+    SLQ_CUDA(cudaStreamWaitEvent(L.stream, ev_b, 0));
   }
 
-  // One gradient pass.  After a first eager run (which sizes every workspace), the ~400 launches
-  // of a pass are captured once per (theta, grad) buffer pair into a CUDA graph and replayed;
-  // the per-class profiler needs eager launches, so profiling runs bypass the graphs.
-  struct PassGraph {
-    const void* th;
-    void* g;
-    cudaGraphExec_t exec;
-    int64_t launches;
-    int eager_runs;
-  };
-  std::vector<PassGraph> graphs;
-  bool use_graphs = getenv("SLQ_NO_GRAPHS") == nullptr;
-
-  void pass(const T* th, T* g, double* loss_dev) {
-    if (!use_graphs || (L.prof && prof_enabled(L.prof))) {
-      pass_eager(th, g, loss_dev);
-      return;
-    }
-    PassGraph* pg = nullptr;
-    for (auto& x : graphs)
-      if (x.th == th && x.g == g) pg = &x;
-    if (!pg) {
-      graphs.push_back(PassGraph{th, g, nullptr, 0, 0});
-      pg = &graphs.back();
-    }
-    if (pg->exec) {
-      SLQ_CUDA(cudaGraphLaunch(pg->exec, L.stream));
-      *L.launches += pg->launches;
-      return;
-    }
-    if (pg->eager_runs++ == 0) {  // warm-up: allocate workspaces at their final sizes
-      pass_eager(th, g, loss_dev);
-      return;
-    }
-    const int64_t l0 = *L.launches;
-    cudaGraph_t graph = nullptr;
-    SLQ_CUDA(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
-    try {
-      pass_eager(th, g, loss_dev);
-    } catch (...) {
-      cudaStreamEndCapture(L.stream, &graph);
-      if (graph) cudaGraphDestroy(graph);
-      throw;
-    }
-    SLQ_CUDA(cudaStreamEndCapture(L.stream, &graph));
-    SLQ_CUDA(cudaGraphInstantiate(&pg->exec, graph, 0));
-    SLQ_CUDA(cudaGraphDestroy(graph));
-    pg->launches = *L.launches - l0;
-    SLQ_CUDA(cudaGraphLaunch(pg->exec, L.stream));
-  }
+  double pass_flops() const override { return pe[0]->runner->flops_per_pass(); }
 
   // fixed-order reduction of `k` partial columns into out (device), then all-reduce
   void finish_reduce(int nb, int k, double* out) {
@@ -253,8 +308,7 @@ struct EngineT : Engine {
       return;
     }
     const double inv2eta = form_points(v, eps / sqrt(ss));
-    pass(thp, gp, dscal + 2);
-    pass(thm, gm, dscal + 2);
+    two_passes();
     SLQ_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), L.stream));
     fd_out<T>(L, gp, gm, inv2eta, out, n, dflag);
     int flag = 0;
@@ -265,12 +319,12 @@ struct EngineT : Engine {
 
   double grad(float* g) override {
     convert_f32<T>(L, theta, thp, n);
-    pass(thp, gp, dscal + 2);
+    pe[0]->run(thp, gp, dscal + 2);
     if (comm) comm->allreduce_sum_f64(dscal + 2, 1, L.stream);
     if (g) to_f32<T>(L, gp, g, n);
     double loss;
     to_host(dscal + 2, 1, &loss);
-    return loss / runner->tokens_global();
+    return loss / pe[0]->runner->tokens_global();
   }
 
   void probe(uint64_t seed, float* q) override {
@@ -295,8 +349,7 @@ struct EngineT : Engine {
       float* qk = qrow(k);
       const float* qprev = k > 0 ? qrow(k - 1) : nullptr;
       const double inv2eps = form_points(qk, d.eps_default);
-      pass(thp, gp, dscal + 2);
-      pass(thm, gm, dscal + 2);
+      two_passes();
       if (full) {
         fd_w<T>(L, gp, gm, inv2eps, k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
         const int nb = reorth_nblocks(n);
