@@ -1,0 +1,318 @@
+// bf16 GEMM on the 5th-generation tensor cores (tcgen05.mma, accumulators in TMEM), operands
+// streamed by TMA (cp.async.bulk.tensor, 128B swizzle) through an mbarrier pipeline.
+//
+//   C[M x N] (fp32) = A[M x K] . B[N x K]^T      A, B bf16, both K-contiguous ("TN")
+//
+// Warp-specialised CTA (192 threads): warp 0 = TMA producer (one elected lane), warp 1 = TMEM
+// allocator + MMA issuer (one elected lane issues tcgen05.mma for the whole CTA), warps 2..5 =
+// epilogue (tcgen05.ld from TMEM -> registers -> global).  Tile 128 x BN x 64, STAGES-deep ring of
+// {full, empty} mbarriers; tcgen05.commit releases a stage when the MMAs that read it complete.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+
+namespace slq {
+namespace tc {
+
+constexpr int BM = 128, BK = 64, UMMA_K = 16;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major operand staged by TMA with 128-byte swizzle:
+// start address, SBO = 1024 B (8 rows x 128 B swizzle atom), version 1, layout SWIZZLE_128B (2)
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;    // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor for kind::f16: D f32, A/B bf16, both K-major, shape M x N
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (1u << 4)                    // D format F32
+         | (1u << 7)                  // A format BF16
+         | (1u << 10)                 // B format BF16
+         | ((uint32_t)(N >> 3) << 17)  // N
+         | ((uint32_t)(M >> 4) << 24);  // M
+}
+
+template <int BN, int STAGES>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;  // power of two >= 32
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* __restrict__ C,
+              int M, int N, int K, int64_t ldc) {
+  using CF = Cfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_holder)),
+                 "n"(CF::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer ----
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % STAGES;
+        const uint32_t ph = (kt / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * CF::STAGE_BYTES;
+        uint8_t* sb = sa + CF::A_BYTES;
+        mbar_expect_tx(&full[s], CF::STAGE_BYTES);
+        tma_load_2d(sa, &tmA, &full[s], kt * BK, m0);
+        tma_load_2d(sb, &tmB, &full[s], kt * BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      constexpr uint32_t idesc = make_idesc(BM, BN);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % STAGES;
+        const uint32_t ph = (kt / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
+        const uint32_t sb = sa + CF::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+          const uint64_t da = make_desc_sw128(sa + kk * UMMA_K * 2);
+          const uint64_t db = make_desc_sw128(sb + kk * UMMA_K * 2);
+          const uint32_t acc = (kt | kk) ? 1u : 0u;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(&empty[s])));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          smem_u32(tmem_full)));
+    }
+  } else {  // ---- epilogue: warps 2..5, warp w owns TMEM lanes 32*(w%4) .. +31 ----
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const int lg = (warp % 4) * 32;
+    const int row = m0 + lg + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)lg << 16) + (uint32_t)c;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+      if (row < M) {
+        float* dst = C + (int64_t)row * ldc + n0 + c;
+        if (n0 + c + 16 <= N && (ldc % 4) == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + i) =
+                make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
+                            __uint_as_float(r[i + 3]));
+        } else {
+          for (int i = 0; i < 16; ++i)
+            if (n0 + c + i < N) dst[i] = __uint_as_float(r[i]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(CF::TMEM_COLS));
+  }
+}
+
+// ---- host: tensor maps through the driver entry point (no libcuda link) ----
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    SLQ_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw Error(SLQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [rows x cols] with row pitch `ld` elements, K (=cols) innermost; box {64, box_rows}
+static CUtensorMap make_map_bf16(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(SLQ_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+template <int BN, int STAGES>
+void launch(cudaStream_t s, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc, int M,
+            int N, int K) {
+  using CF = Cfg<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    SLQ_CUDA(cudaFuncSetAttribute(k_tc_gemm<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    attr = true;
+  }
+  SLQ_CHECK_ARG((lda * 2) % 16 == 0 && (ldb * 2) % 16 == 0, "TMA needs 16-byte row pitches");
+  SLQ_CHECK_ARG(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0, "TMA needs 16-byte aligned bases");
+  const CUtensorMap ta = make_map_bf16(A, M, K, lda, BM);
+  const CUtensorMap tb = make_map_bf16(B, N, K, ldb, BN);
+  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM));
+  k_tc_gemm<BN, STAGES><<<grid, 192, CF::SMEM, s>>>(ta, tb, C, M, N, K, ldc);
+  SLQ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_fill_bf16(__nv_bfloat16* x, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    x[i] = __float2bfloat16((float)((z >> 40) & 0xFFFF) / 65536.0f - 0.5f);
+  }
+}
+
+// reference: one thread per output, fp32 accumulation of the same bf16 products
+__global__ void k_ref_gemm(const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N, int K) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * N) return;
+  const int m = (int)(i / N), n = (int)(i % N);
+  double s = 0;
+  for (int k = 0; k < K; ++k) s += (double)__bfloat162float(A[(int64_t)m * K + k]) * __bfloat162float(B[(int64_t)n * K + k]);
+  C[i] = (float)s;
+}
+
+}  // namespace tc
+}  // namespace slq
+
+// Diagnostic (not yet on the pass path): time the tcgen05 bf16 GEMM on one shape and check it
+// against a naive reference kernel.  variant: 0 = 128x128x64 4 stages, 1 = 128x256x64 3 stages.
+extern "C" slq_status slq_diag_gemm_bf16(int32_t device, int32_t M, int32_t N, int32_t K, int32_t variant,
+                                         int32_t iters, double* tflops, double* max_rel_err) {
+  using namespace slq;
+  __nv_bfloat16 *A = nullptr, *B = nullptr;
+  float *C = nullptr, *R = nullptr;
+  try {
+    SLQ_CUDA(cudaSetDevice(device));
+    SLQ_CUDA(cudaMalloc(&A, 2 * (size_t)M * K));
+    SLQ_CUDA(cudaMalloc(&B, 2 * (size_t)N * K));
+    SLQ_CUDA(cudaMalloc(&C, 4 * (size_t)M * N));
+    SLQ_CUDA(cudaMalloc(&R, 4 * (size_t)M * N));
+    tc::k_fill_bf16<<<1024, 256>>>(A, (int64_t)M * K, 11);
+    tc::k_fill_bf16<<<1024, 256>>>(B, (int64_t)N * K, 12);
+    auto run = [&] {
+      if (variant == 1)
+        tc::launch<256, 3>(0, A, K, B, K, C, N, M, N, K);
+      else
+        tc::launch<128, 4>(0, A, K, B, K, C, N, M, N, K);
+    };
+    run();
+    SLQ_CUDA(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    SLQ_CUDA(cudaEventCreate(&e0));
+    SLQ_CUDA(cudaEventCreate(&e1));
+    SLQ_CUDA(cudaEventRecord(e0));
+    for (int i = 0; i < iters; ++i) run();
+    SLQ_CUDA(cudaEventRecord(e1));
+    SLQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    SLQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *tflops = 2.0 * M * N * (double)K * iters / (ms * 1e-3) / 1e12;
+    tc::k_ref_gemm<<<(unsigned)ceil_div((int64_t)M * N, 256), 256>>>(A, B, R, M, N, K);
+    SLQ_CUDA(cudaDeviceSynchronize());
+    std::vector<float> hc((size_t)M * N), hr((size_t)M * N);
+    SLQ_CUDA(cudaMemcpy(hc.data(), C, 4 * hc.size(), cudaMemcpyDeviceToHost));
+    SLQ_CUDA(cudaMemcpy(hr.data(), R, 4 * hr.size(), cudaMemcpyDeviceToHost));
+    double mx = 0, scale = 1e-30;
+    for (size_t i = 0; i < hc.size(); ++i) {
+      mx = std::max(mx, (double)std::fabs(hc[i] - hr[i]));
+      scale = std::max(scale, (double)std::fabs(hr[i]));
+    }
+    *max_rel_err = mx / scale;
+    cudaFree(A); cudaFree(B); cudaFree(C); cudaFree(R);
+    return SLQ_OK;
+  } catch (const Error& e) {
+    if (A) cudaFree(A);
+    if (B) cudaFree(B);
+    if (C) cudaFree(C);
+    if (R) cudaFree(R);
+    return e.status;
+  }
+}
