@@ -105,6 +105,22 @@ CONFIGS: Dict[str, ModelDesc] = {
                             n_heads=4, n_kv_heads=2, d_ff=96, vocab=211, seq_len=33, n_seq=3,
                             rope_theta=10000.0, eps=1e-3, m=16, probes=1,
                             init_seed=31, data_seed=32, probe_seed0=33),
+    # ---- parity batches of the large configs (same layer shapes) ----
+    # c3 at R=1 with 2 of its 8 sequences
+    "c3_parity": ModelDesc(name="c3_parity", arch=ARCH_GPT, n_layers=12, d_model=768, n_heads=12,
+                           n_kv_heads=12, d_ff=3072, vocab=50257, seq_len=1024, n_seq=2,
+                           tie_embeddings=True, param_bf16=True, eps=1e-3, m=3, probes=1,
+                           reorth_full=True, init_seed=1003, data_seed=2003, probe_seed0=3300),
+    # c4 (Llama 1B): 2 sequences of 256 tokens (SURVEY: 8 x 256 at R=8)
+    "c4_parity": ModelDesc(name="c4_parity", arch=ARCH_LLAMA, n_layers=16, d_model=2048, n_heads=32,
+                           n_kv_heads=8, d_ff=8192, vocab=32000, seq_len=256, n_seq=2,
+                           rope_theta=10000.0, param_bf16=True, eps=1e-3, m=2, probes=1,
+                           reorth_full=True, init_seed=1004, data_seed=2004, probe_seed0=3400),
+    # c5 twin: every layer shape of Llama-3-8B, 2 blocks, 1 x 512 tokens, no stored basis
+    "c5_twin": ModelDesc(name="c5_twin", arch=ARCH_LLAMA, n_layers=2, d_model=4096, n_heads=32,
+                         n_kv_heads=8, d_ff=14336, vocab=128256, seq_len=512, n_seq=1,
+                         rope_theta=500000.0, param_bf16=True, eps=1e-3, m=2, probes=1,
+                         reorth_full=False, init_seed=1005, data_seed=2005, probe_seed0=3500),
     "mlp_tiny": ModelDesc(name="mlp_tiny", arch=ARCH_MLP, d_in=7, d_hidden=9, n_classes=4,
                           n_rows=13, eps=1e-3, m=8, probes=1, init_seed=41, data_seed=42,
                           probe_seed0=43),
