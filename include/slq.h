@@ -51,9 +51,12 @@ typedef enum {
 } slq_status;
 
 enum { SLQ_ARCH_MLP = 0, SLQ_ARCH_GPT = 1, SLQ_ARCH_LLAMA = 2 };
-/* arithmetic of the two gradient passes.  FP64: fp64 activations/accumulation on the GPU
- * (the parity mode of the fp32 models); FP32: fp32 passes (reported only). */
-enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1 };
+/* arithmetic of the two gradient passes.  FP64: fp64 activations/accumulation on the GPU, GEMMs
+ * on the FP64 tensor core (the parity mode of the fp32 models); FP32: fp32
+ * passes on SIMT GEMMs (reported only); BF16X3: fp32 activations, every non-batched GEMM on the
+ * tcgen05 tensor cores with operands split into three bf16 terms (fp32-faithful; the mode for the
+ * bf16 models' gates). */
+enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2 };
 enum { SLQ_REORTH_NONE = 0, SLQ_REORTH_FULL = 1 };
 enum { SLQ_PARAM_FP32 = 0, SLQ_PARAM_BF16 = 1 };
 

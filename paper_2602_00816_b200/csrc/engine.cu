@@ -332,10 +332,80 @@ struct EngineT : Engine {
     SLQ_CUDA(cudaStreamSynchronize(L.stream));
   }
 
+  // Three-term recurrence without a stored basis (c5 mode; "only the essential Lanczos
+  // vectors").  Per step two vector kernels and one 3-scalar reduction:
+  //   perturb:  q_k = (w_raw - alpha_{k-1} q_{k-1}) / beta_k  (deferred normalisation) and theta+-
+  //   passes:   g+, g-
+  //   fd:       w_raw = (g+ - g-)/(2 eta) - beta_k q_{k-1};  s1 = <w_raw,q_k>, s2 = |w_raw|^2, s3 = |q_k|^2
+  //   host:     alpha_k = s1;  beta_{k+1}^2 = |w_raw - alpha_k q_k|^2 = s2 - 2 alpha s1 + alpha^2 s3
+  // If that Pythagorean form loses more than 3 digits to cancellation, the residual is formed
+  // explicitly (one extra pass) and its norm taken directly.
+  LanczosInfo lanczos_nobasis(uint64_t seed, int m, double* alpha, double* beta) {
+    for (int i = 0; i < m; ++i) alpha[i] = NAN;
+    for (int i = 0; i + 1 < m; ++i) beta[i] = NAN;
+    LanczosInfo info;
+    const bool exact = d.perturb == SLQ_PERTURB_EXACT && sizeof(T) == 8;
+    const double eps = d.eps_default;
+    const float eps_f = (float)eps;
+    const double inv2eps = exact ? 1.0 / (2.0 * eps) : 1.0 / (2.0 * (double)eps_f);
+    float* q[2] = {vq[0], vq[1]};  // q[k % 2] = q_k
+    float* wr = vq[2];
+    double a_prev = 0.0, b_k = 0.0, tmax = 0.0;
+    const int nb = vec_nblocks(n);
+    probe_fill(L, q[0], n, units_dev, (int)plan.units.size(), seed, 1.0 / sqrt((double)plan.P));
+    for (int k = 0; k < m; ++k) {
+      float* qk = q[k % 2];
+      const float* qprev = k > 0 ? q[(k + 1) % 2] : nullptr;
+      if (k == 0) {
+        form_points(qk, eps);
+      } else {
+        perturb_lanczos<T>(L, exact, theta, wr, q[(k + 1) % 2], a_prev, b_k, eps, qk, thp, thm, n);
+      }
+      two_passes();
+      fd_partials3<T>(L, gp, gm, inv2eps, b_k, qprev, qk, wr, n, partials);
+      finish_reduce(nb, 3, dscal + 8);  // reduce_partials reads [nb x 3] row-major
+      double s[3];
+      to_host(dscal + 8, 3, s);
+      const double a = s[0];
+      double b2 = s[1] - 2.0 * a * s[0] + a * a * s[2];
+      double a_carry = a;
+      if (!(b2 > 1e-3 * s[1])) {  // cancellation: form w = w_raw - alpha q_k explicitly
+        SLQ_CUDA(cudaMemcpyAsync(dscal + 4, &a, sizeof(double), cudaMemcpyHostToDevice, L.stream));
+        axpy_dev(L, wr, qk, dscal + 4, -1.0, n, partials);
+        finish_reduce(nb, 1, dscal + 0);
+        to_host(dscal + 0, 1, &b2);
+        a_carry = 0.0;  // wr now holds the residual itself
+      }
+      if (!std::isfinite(a) || !std::isfinite(b2)) {
+        info.nonfinite = 1;
+        info.m_done = k;
+        last_info = info;
+        throw Error(SLQ_ENUMERIC, "non-finite Lanczos coefficient at step " + std::to_string(k + 1));
+      }
+      const double bnext = sqrt(std::max(b2, 0.0));
+      alpha[k] = a;
+      if (k + 1 < m) beta[k] = bnext;
+      tmax = std::max(tmax, fabs(a));
+      if (k > 0) tmax = std::max(tmax, b_k);
+      info.m_done = k + 1;
+      info.beta_next = bnext;
+      if (k + 1 < m && bnext <= 1e-7 * tmax) {
+        beta[k] = NAN;
+        break;
+      }
+      a_prev = a_carry;
+      b_k = bnext;
+    }
+    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    last_info = info;
+    return info;
+  }
+
   LanczosInfo lanczos(uint64_t seed, int m, double* alpha, double* beta) override {
     last_info = LanczosInfo();
     SLQ_CHECK_ARG(m >= 1 && m <= max_steps, "1 <= m <= max_steps");
     const bool full = d.reorth == SLQ_REORTH_FULL;
+    if (!full) return lanczos_nobasis(seed, m, alpha, beta);
     for (int i = 0; i < m; ++i) alpha[i] = NAN;
     for (int i = 0; i + 1 < m; ++i) beta[i] = NAN;
     LanczosInfo info;
@@ -363,11 +433,6 @@ struct EngineT : Engine {
         // update of pass 2 fused with ||w||^2
         reorth_update(L, basis, n, k + 1, d_coef, w, n, nullptr, partials);
         finish_reduce(nb, 1, dscal + 0);
-      } else {
-        fd_w<T>(L, gp, gm, inv2eps, k > 0 ? d_beta : nullptr, qprev, w, qk, n, partials);
-        finish_reduce(vec_nblocks(n), 1, d_alpha + k);
-        axpy_dev(L, w, qk, d_alpha + k, -1.0, n, partials);
-        finish_reduce(vec_nblocks(n), 1, dscal + 0);
       }
       double h[2];
       to_host(d_alpha + k, 1, &h[0]);
@@ -407,7 +472,9 @@ std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& p
                                     const float* theta_host, int rank, Comm* comm, const Launch& L) {
   if (d.pass_numerics == SLQ_PASS_FP64)
     return std::unique_ptr<Engine>(new EngineT<double>(d, plan, b, theta_host, rank, comm, L));
-  return std::unique_ptr<Engine>(new EngineT<float>(d, plan, b, theta_host, rank, comm, L));
+  Launch Lf = L;
+  Lf.gemm_mode = d.pass_numerics == SLQ_PASS_BF16X3 ? 1 : 0;
+  return std::unique_ptr<Engine>(new EngineT<float>(d, plan, b, theta_host, rank, comm, Lf));
 }
 
 }  // namespace slq

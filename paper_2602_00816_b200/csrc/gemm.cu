@@ -173,6 +173,12 @@ void gemm(const Launch& L, const GemmArgs<T>& a) {
   SLQ_CHECK_ARG((a.act != ACT_DGELU && a.act != ACT_DTANH) || a.aux, "derivative epilogue needs aux");
   const bool ak = a.sAk == 1 && !(a.sAm == 1 && a.K == 1);
   const bool bk = a.sBk == 1 && !(a.sBn == 1 && a.K == 1);
+  if constexpr (sizeof(T) == 4) {
+    if (L.gemm_mode == 1 && a.batch == 1 && a.K > 0) {
+      gemm_tc_bf16x3(L, a);
+      return;
+    }
+  }
   if (ak && bk) launch_cfg<T, true, true>(L, a);
   else if (ak && !bk) launch_cfg<T, true, false>(L, a);
   else if (!ak && bk) launch_cfg<T, false, true>(L, a);

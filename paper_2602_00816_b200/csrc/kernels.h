@@ -21,6 +21,7 @@ struct Launch {
   Profiler* prof;
   Workspace* ws;      // split-K / reduction scratch
   int64_t* launches;  // launch counter
+  int gemm_mode = 0;  // float GEMMs: 0 = SIMT fp32, 1 = tcgen05 bf16x3 split (fp32-faithful)
 };
 
 // batch addressing of one operand: offset(z) = (z / div) * outer + ((z % div) / rep) * inner
@@ -67,6 +68,11 @@ struct GemmArgs {
 template <class T>
 void gemm(const Launch& L, const GemmArgs<T>& a);
 
+// fp32-faithful GEMM on the tcgen05 tensor cores: every fp32 operand is split into three bf16
+// terms (x = x0 + x1 + x2, 24 significant bits) and the six products with i + j <= 2 are
+// accumulated in one fp32 TMEM accumulator (tc_gemm.cu).  batch == 1 only.
+void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a);
+
 // ---- layers (layers.cu) ----
 template <class T> void convert_f32(const Launch& L, const float* x, T* y, int64_t n);
 template <class T> void embed_fwd(const Launch& L, const int32_t* tok, int tok_stride, int nseq, int T_,
@@ -112,6 +118,13 @@ template <class T> void perturb(const Launch& L, const float* theta, const float
 // SLQ_PERTURB_EXACT with fp64 passes: plus/minus = theta +- eta*v in fp64 (rounded product, rounded sum)
 void perturb_exact(const Launch& L, const float* theta, const float* v, double eta, double* plus, double* minus,
                    int64_t n);
+// no-basis Lanczos: q_k = (w_raw - alpha_prev q_prev) / beta_k formed, stored and used for theta+- in one pass
+template <class T> void perturb_lanczos(const Launch& L, bool exact, const float* theta, const float* w_raw,
+                                        const float* q_prev, double alpha_prev, double beta_k, double eps,
+                                        float* q_out, T* plus, T* minus, int64_t n);
+// w = (g+ - g-) inv2eta - beta_k q_prev; partials[3 * block + {0,1,2}] = <w,q_k>, <w,w>, <q_k,q_k>
+template <class T> void fd_partials3(const Launch& L, const T* gp, const T* gm, double inv2eta, double beta_k,
+                                     const float* q_prev, const float* q_k, float* w, int64_t n, double* partials);
 // partial sums of squares / dots -> partials[nblocks * k]; finalize by reduce_partials
 int vec_nblocks(int64_t n);
 void sumsq_partials(const Launch& L, const float* x, int64_t n, double* partials);

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "common.h"
+#include "gemm_common.cuh"
 #include "kernels.h"
 
 namespace slq {
@@ -239,6 +240,273 @@ void launch(cudaStream_t s, const void* A, int64_t lda, const void* B, int64_t l
   k_tc_gemm<BN, STAGES><<<grid, 192, CF::SMEM, s>>>(ta, tb, C, M, N, K, ldc);
   SLQ_CUDA(cudaGetLastError());
 }
+
+// ------------------------------------------------------------------------------------------
+// Multi-product variant: C = epilogue( sum_p A[ai_p] . B[bi_p]^T ), all products accumulated in
+// one TMEM accumulator; the K loop runs over (product, k-tile) pairs, so a split-operand GEMM is
+// one long-K tensor-core GEMM.  Optional split-K over that sequence (partials to a workspace,
+// deterministic reduce).
+constexpr int kMaxTerms = 3, kMaxPairs = 8;
+struct MultiOps {
+  CUtensorMap a[kMaxTerms];
+  CUtensorMap b[kMaxTerms];
+  int npairs;
+  int ai[kMaxPairs], bi[kMaxPairs];
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    k_tc_multi(const __grid_constant__ MultiOps ops, GemmArgs<float> p, int nk, int tiles_per_split, int splits,
+               float* __restrict__ ws) {
+  using CF = Cfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int split = blockIdx.z;
+  const int total = ops.npairs * nk;
+  const int t0 = split * tiles_per_split;
+  const int t1 = min(total, t0 + tiles_per_split);
+  const int nloc = t1 > t0 ? t1 - t0 : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_holder)),
+                 "n"(CF::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nloc; ++i) {
+        const int t = t0 + i, pr = t / nk, kt = t % nk;
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * CF::STAGE_BYTES;
+        uint8_t* sb = sa + CF::A_BYTES;
+        mbar_expect_tx(&full[s], CF::STAGE_BYTES);
+        tma_load_2d(sa, &ops.a[ops.ai[pr]], &full[s], kt * BK, m0);
+        tma_load_2d(sb, &ops.b[ops.bi[pr]], &full[s], kt * BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BM, BN);
+      for (int i = 0; i < nloc; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
+        const uint32_t sb = sa + CF::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+          const uint64_t da = make_desc_sw128(sa + kk * UMMA_K * 2);
+          const uint64_t db = make_desc_sw128(sb + kk * UMMA_K * 2);
+          const uint32_t acc = (i | kk) ? 1u : 0u;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(&empty[s])));
+      }
+      if (nloc > 0) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(tmem_full)));
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_full)));
+      }
+    }
+  } else {
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const int lg = (warp % 4) * 32;
+    const int row = m0 + lg + lane;
+    float* W = splits > 1 ? ws + (int64_t)split * p.M * p.N : nullptr;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)lg << 16) + (uint32_t)c;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+      if (row >= p.M) continue;
+#pragma unroll 1
+      for (int i = 0; i < 16; ++i) {
+        const int col = n0 + c + i;
+        if (col >= p.N) break;
+        const float v = nloc > 0 ? __uint_as_float(r[i]) : 0.0f;
+        if (W)
+          W[(int64_t)row * p.N + col] = v;
+        else
+          gemm_detail::epilogue_store(p, p.C, row, col, v);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(CF::TMEM_COLS));
+  }
+}
+
+// x = t0 + t1 + t2 in bf16 terms (each residual is exact in fp32); optional transpose through a
+// 32 x 32 shared tile so that every operand reaches the tensor core K-contiguous
+template <bool TRANS>
+__global__ void k_split3(const float* __restrict__ X, int64_t R, int64_t C, int64_t ld, __nv_bfloat16* __restrict__ o0,
+                         __nv_bfloat16* __restrict__ o1, __nv_bfloat16* __restrict__ o2, int64_t ldo) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8 threads
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + tx;
+    tile[i][tx] = (r < R && c < C) ? X[r * ld + c] : 0.0f;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    float x;
+    int64_t orow, ocol;
+    if (TRANS) {
+      x = tile[tx][i];
+      orow = c0 + i;
+      ocol = r0 + tx;
+      if (orow >= C || ocol >= R) continue;
+    } else {
+      x = tile[i][tx];
+      orow = r0 + i;
+      ocol = c0 + tx;
+      if (orow >= R || ocol >= C) continue;
+    }
+    const __nv_bfloat16 b0 = __float2bfloat16_rn(x);
+    const float e1 = x - __bfloat162float(b0);
+    const __nv_bfloat16 b1 = __float2bfloat16_rn(e1);
+    const float e2 = e1 - __bfloat162float(b1);
+    const int64_t o = orow * ldo + ocol;
+    o0[o] = b0;
+    o1[o] = b1;
+    o2[o] = __float2bfloat16_rn(e2);
+  }
+}
+
+template <int BN>
+void launch_multi(const Launch& L, const MultiOps& ops, const GemmArgs<float>& a, int nk, int splits, int tps,
+                  float* ws) {
+  constexpr int STAGES = BN == 256 ? 3 : 4;
+  using CF = Cfg<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    SLQ_CUDA(cudaFuncSetAttribute(k_tc_multi<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(a.N, BN), (unsigned)ceil_div(a.M, BM), (unsigned)splits);
+  k_tc_multi<BN, STAGES><<<grid, 192, CF::SMEM, L.stream>>>(ops, a, nk, tps, splits, ws);
+  SLQ_CUDA(cudaGetLastError());
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace tc
+
+void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a) {
+  using namespace tc;
+  SLQ_CHECK_ARG(a.batch == 1 && a.M > 0 && a.N > 0 && a.K > 0, "tc gemm: batch 1, non-empty");
+  const int M = a.M, N = a.N, K = a.K;
+  const int64_t ldk = (K + 7) / 8 * 8;  // 16-byte row pitch for TMA
+  const size_t a_bytes = align256(2 * (size_t)M * ldk), b_bytes = align256(2 * (size_t)N * ldk);
+  // product list (i + j <= 2)
+  static const int AI[6] = {0, 0, 1, 1, 0, 2}, BI[6] = {0, 1, 0, 1, 2, 0};
+  const int npairs = 6, nk = (K + BK - 1) / BK;
+  const int64_t t128 = ceil_div(M, BM) * ceil_div(N, 128);
+  const int bn = t128 >= 148 ? 128 : 64;
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, bn));
+  const int total = npairs * nk;
+  int splits = 1;
+  if (tiles < 148) splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * 148, tiles), total / 4));
+  const int tps = (int)ceil_div(total, splits);
+  splits = (int)ceil_div(total, tps);
+  const size_t w_bytes = splits > 1 ? align256(4 * (size_t)M * N * splits) : 0;
+  uint8_t* base = (uint8_t*)L.ws->get(3 * a_bytes + 3 * b_bytes + w_bytes, L.stream);
+  __nv_bfloat16* at[3];
+  __nv_bfloat16* bt[3];
+  for (int i = 0; i < 3; ++i) {
+    at[i] = (__nv_bfloat16*)(base + i * a_bytes);
+    bt[i] = (__nv_bfloat16*)(base + 3 * a_bytes + i * b_bytes);
+  }
+  float* ws = splits > 1 ? (float*)(base + 3 * a_bytes + 3 * b_bytes) : nullptr;
+  {  // split (and transpose to K-contiguous where needed)
+    LaunchScope scope(L.prof, KC_ELEM, L.stream, 0, (4.0 + 6.0) * ((double)M * K + (double)N * K));
+    if (a.sAk == 1) {
+      dim3 g((unsigned)ceil_div(K, 32), (unsigned)ceil_div(M, 32));
+      k_split3<false><<<g, 256, 0, L.stream>>>(a.A, M, K, a.sAm, at[0], at[1], at[2], ldk);
+    } else {  // A stored [K x M] (M contiguous) -> [M x K]
+      dim3 g((unsigned)ceil_div(M, 32), (unsigned)ceil_div(K, 32));
+      k_split3<true><<<g, 256, 0, L.stream>>>(a.A, K, M, a.sAk, at[0], at[1], at[2], ldk);
+    }
+    SLQ_CUDA(cudaGetLastError());
+    if (a.sBk == 1) {  // B(k, n) at n*sBn + k: stored [N x K]
+      dim3 g((unsigned)ceil_div(K, 32), (unsigned)ceil_div(N, 32));
+      k_split3<false><<<g, 256, 0, L.stream>>>(a.B, N, K, a.sBn, bt[0], bt[1], bt[2], ldk);
+    } else {  // stored [K x N] -> [N x K]
+      dim3 g((unsigned)ceil_div(N, 32), (unsigned)ceil_div(K, 32));
+      k_split3<true><<<g, 256, 0, L.stream>>>(a.B, K, N, a.sBk, bt[0], bt[1], bt[2], ldk);
+    }
+    SLQ_CUDA(cudaGetLastError());
+    *L.launches += 2;
+  }
+  MultiOps ops;
+  for (int i = 0; i < 3; ++i) {
+    ops.a[i] = make_map_bf16(at[i], M, K, ldk, BM);
+    ops.b[i] = make_map_bf16(bt[i], N, K, ldk, bn);
+  }
+  ops.npairs = npairs;
+  for (int i = 0; i < npairs; ++i) {
+    ops.ai[i] = AI[i];
+    ops.bi[i] = BI[i];
+  }
+  {
+    LaunchScope scope(L.prof, KC_GEMM, L.stream, 2.0 * M * N * (double)K * npairs,
+                      2.0 * 3 * ((double)M * K + (double)N * K) + 4.0 * M * N);
+    if (bn == 128)
+      launch_multi<128>(L, ops, a, nk, splits, tps, ws);
+    else
+      launch_multi<64>(L, ops, a, nk, splits, tps, ws);
+    ++*L.launches;
+  }
+  if (splits > 1) {
+    LaunchScope scope(L.prof, KC_GEMM, L.stream, 0, 4.0 * (double)M * N * (splits + 1));
+    const int64_t mn = (int64_t)M * N;
+    int blocks = (int)std::min<int64_t>(ceil_div(mn, 256), 148 * 8);
+    gemm_detail::splitk_reduce<float><<<blocks, 256, 0, L.stream>>>(a, splits, ws);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+}
+
+namespace tc {
 
 __global__ void k_fill_bf16(__nv_bfloat16* x, int64_t n, uint64_t seed) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {

@@ -101,6 +101,57 @@ __global__ void k_perturb_exact(const float* __restrict__ th, const float* __res
   }
 }
 
+// Lanczos step without a stored basis (deferred normalisation): forms
+// q_k = (w_raw - alpha_prev q_prev) / beta_k from the previous step's residual, stores it, and
+// writes theta +- eps q_k in the same pass.  EXACT: fp64 points (rounded product, rounded sum)
+// from the stored fp32 q_k; STORAGE: fmaf into fp32.
+template <class T, bool EXACT>
+__global__ void k_perturb_lanczos(const float* __restrict__ th, const float* __restrict__ w_raw,
+                                  const float* __restrict__ q_prev, double alpha_prev, double inv_beta, double eps,
+                                  float eps_f, float* __restrict__ q_out, T* __restrict__ plus, T* __restrict__ minus,
+                                  int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float q = (float)(((double)w_raw[i] - alpha_prev * (double)q_prev[i]) * inv_beta);
+    q_out[i] = q;
+    if (EXACT) {
+      const double t = (double)th[i];
+      const double d = __dmul_rn(eps, (double)q);
+      plus[i] = (T)__dadd_rn(t, d);
+      minus[i] = (T)__dsub_rn(t, d);
+    } else {
+      plus[i] = (T)__fmaf_rn(eps_f, q, th[i]);
+      minus[i] = (T)__fmaf_rn(-eps_f, q, th[i]);
+    }
+  }
+}
+
+// FD difference fused with the three-term update and the three Lanczos partials (one HBM pass,
+// north-star row (d)): w = (g+ - g-) inv2eta - beta_k q_prev;  partials <w,q_k>, <w,w>, <q_k,q_k>
+template <class T>
+__global__ void k_fd_partials3(const T* __restrict__ gp, const T* __restrict__ gm, double inv2eta, double beta_k,
+                               const float* __restrict__ q_prev, const float* __restrict__ q_k, float* __restrict__ w,
+                               int64_t n, double* __restrict__ part) {
+  double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double d = ((double)gp[i] - (double)gm[i]) * inv2eta;
+    if (q_prev) d -= beta_k * (double)q_prev[i];
+    const float wf = (float)d;
+    w[i] = wf;
+    const double wd = wf, qd = q_k[i];
+    s1 += wd * qd;
+    s2 += wd * wd;
+    s3 += qd * qd;
+  }
+  s1 = block_sum_d(s1);
+  s2 = block_sum_d(s2);
+  s3 = block_sum_d(s3);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x + 0] = s1;
+    part[3 * blockIdx.x + 1] = s2;
+    part[3 * blockIdx.x + 2] = s3;
+  }
+}
+
 __global__ void k_sumsq(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -324,6 +375,28 @@ void perturb_exact(const Launch& L, const float* theta, const float* v, double e
           n);
 }
 
+template <class T>
+void perturb_lanczos(const Launch& L, bool exact, const float* theta, const float* w_raw, const float* q_prev,
+                     double alpha_prev, double beta_k, double eps, float* q_out, T* plus, T* minus, int64_t n) {
+  const double inv_beta = 1.0 / beta_k;
+  const double bytes = (16.0 + 2.0 * sizeof(T)) * n;  // theta, w_raw, q_prev in; q_k, theta+- out
+  if (exact && sizeof(T) == 8) {
+    VLAUNCH(KC_PERTURB, 6.0 * n, bytes, vec_nblocks(n), kThreads, 0, (k_perturb_lanczos<T, true>), theta, w_raw,
+            q_prev, alpha_prev, inv_beta, eps, (float)eps, q_out, plus, minus, n);
+  } else {
+    VLAUNCH(KC_PERTURB, 6.0 * n, bytes, vec_nblocks(n), kThreads, 0, (k_perturb_lanczos<T, false>), theta, w_raw,
+            q_prev, alpha_prev, inv_beta, eps, (float)eps, q_out, plus, minus, n);
+  }
+}
+
+template <class T>
+void fd_partials3(const Launch& L, const T* gp, const T* gm, double inv2eta, double beta_k, const float* q_prev,
+                  const float* q_k, float* w, int64_t n, double* part) {
+  const double bytes = (2.0 * sizeof(T) + 8.0 + (q_prev ? 4.0 : 0.0)) * n;
+  VLAUNCH(KC_FD, 8.0 * n, bytes, vec_nblocks(n), kThreads, 0, k_fd_partials3<T>, gp, gm, inv2eta, beta_k, q_prev,
+          q_k, w, n, part);
+}
+
 void sumsq_partials(const Launch& L, const float* x, int64_t n, double* part) {
   VLAUNCH(KC_VEC, 2.0 * n, 4.0 * n, vec_nblocks(n), kThreads, 0, k_sumsq, x, n, part);
 }
@@ -385,7 +458,11 @@ void nonfinite_check(const Launch& L, const float* x, int64_t n, int* flag) {
   template void fd_w<T>(const Launch&, const T*, const T*, double, const double*, const float*, float*,       \
                         const float*, int64_t, double*);                                                      \
   template void fd_out<T>(const Launch&, const T*, const T*, double, float*, int64_t, int*);                  \
-  template void to_f32<T>(const Launch&, const T*, float*, int64_t);
+  template void to_f32<T>(const Launch&, const T*, float*, int64_t);                                          \
+  template void perturb_lanczos<T>(const Launch&, bool, const float*, const float*, const float*, double,     \
+                                   double, double, float*, T*, T*, int64_t);                                  \
+  template void fd_partials3<T>(const Launch&, const T*, const T*, double, double, const float*, const float*, \
+                                float*, int64_t, double*);
 VINST(double)
 VINST(float)
 
