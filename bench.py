@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
+    p.add_argument("--numerics", default="fp64", choices=["fp64", "fp32", "bf16x3"],
+                   help="gradient-pass arithmetic (fp64 = the c2 parity path; bf16x3 = tcgen05)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -185,7 +187,8 @@ def main():
     tok, n_glob = split_batch(cfg, rank, world)
     m_run = min(cfg.m, max(args.steps, 1))
     ctx = slq.SlqContext(cfg, si.init_params(cfg), tok, n_global=n_glob, rank=rank, world_size=world, device=local,
-                         unique_id=uid, pass_numerics="fp64", reorth="full", max_steps=max(cfg.m, args.warmup),
+                         unique_id=uid, pass_numerics=args.numerics,
+                         reorth="full" if cfg.reorth_full else "none", max_steps=max(cfg.m, args.warmup),
                          perturb="exact")
     stream = torch.cuda.ExternalStream(ctx.stream)
 
@@ -263,7 +266,15 @@ def main():
     dom = max(stats, key=lambda k: stats[k]["ms"])
     st = stats[dom]
     total_ms = sum(s["ms"] for s in stats.values())
-    if dom == "gemm":
+    if dom == "gemm" and args.numerics != "fp64":
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12
+        tc_note = ("tcgen05 kind::f16 bf16 products (6 per fp32-faithful GEMM, all counted)"
+                   if args.numerics == "bf16x3" else "SIMT fp32 (no tensor core)")
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s", "frac": achieved / bf16,
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks
+                                else "fallback 1590 TFLOP/s") + "; " + tc_note}
+    elif dom == "gemm":
         pk = slq.fp64_peak_tflops(local)
         fp64_peak = max(pk["dmma"], pk["dfma"])
         achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12
@@ -286,12 +297,15 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: GPT {cfg.n_layers}L d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} "
-                               f"V{cfg.vocab}, {si.n_params(cfg)} fp32 params, {cfg.n_seq}x{cfg.seq_len} Zipf(1.1) "
-                               f"tokens, eps={cfg.eps}, Lanczos m={cfg.m} full CGS2 reorth",
+        "vs_baseline": None, "dtype": {"fp64": "f64", "fp32": "f32", "bf16x3": "bf16x3"}[args.numerics],
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {'GPT' if cfg.arch == si.ARCH_GPT else 'Llama'} {cfg.n_layers}L "
+                               f"d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} V{cfg.vocab}, {si.n_params(cfg)} params "
+                               f"({'bf16' if cfg.param_bf16 else 'fp32'}), {cfg.n_seq}x{cfg.seq_len} Zipf(1.1) "
+                               f"tokens, eps={cfg.eps}, Lanczos m={cfg.m} "
+                               f"{'full CGS2 reorth' if cfg.reorth_full else 'no reorth'}",
                    "global_batch": cfg.n_seq, "seq_len": cfg.seq_len, "parallelism": f"fsdp{world}",
-                   "pass_numerics": "fp64", "perturb": "exact",
+                   "pass_numerics": args.numerics, "perturb": "exact",
                    "l2": "no flush: per-step working set (theta+-, g+- fp64, activations, basis) > 0.5 GB > 126 MB L2"},
         "s_per_lanczos_step": ms_step / 1000.0,
         "hvp_per_s_standalone": 1000.0 / hvp_ms,
