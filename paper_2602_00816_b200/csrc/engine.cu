@@ -253,7 +253,7 @@ struct EngineT : Engine {
 
   // g+ = grad L(theta+), g- = grad L(theta-): concurrently on two streams when dual
   void two_passes() {
-    if (!dual) {
+    if (!dual || prof_enabled(L.prof)) {  // profiled runs are serial: per-launch durations stay honest
       pe[0]->run(thp, gp, dscal + 2);
       pe[0]->run(thm, gm, dscal + 3);
       return;

@@ -195,11 +195,17 @@ struct SideStream {
     side.stream = s;
     side.ws = &ws;
   }
+  // While the per-class profiler is on, everything runs on the main stream so that each launch's
+  // event-timed duration is its own (concurrent kernels would inflate each other's durations).
+  bool serial() const { return prof_enabled(main.prof); }
+  const Launch& lane() const { return serial() ? main : side; }
   void fork() {
+    if (serial()) return;
     SLQ_CUDA(cudaEventRecord(ev_fork, main.stream));
     SLQ_CUDA(cudaStreamWaitEvent(side.stream, ev_fork, 0));
   }
   void join() {
+    if (serial()) return;
     SLQ_CUDA(cudaEventRecord(ev_join, side.stream));
     SLQ_CUDA(cudaStreamWaitEvent(main.stream, ev_join, 0));
   }
@@ -350,7 +356,7 @@ struct GptRunner : Runner<T> {
     cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
     // ---------------- backward ----------------
     // weight / bias / gain gradients go to the side stream (Ls); the data-gradient chain stays on L
-    const Launch& Ls = ss.side;
+    const Launch& Ls = ss.lane();
     T* G0 = tied ? io.grads(0) : nullptr;
     T* Gf = io.grads(Ly + 1);
     int cur = 0;  // dxs[cur] = dL/d(residual stream) entering the current block from above
@@ -516,7 +522,7 @@ struct LlamaRunner : Runner<T> {
     linear_fwd<T>(L, xf, D, Whead, V, D, N, logits, V, (const T*)nullptr);
     cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
 
-    const Launch& Ls = ss.side;
+    const Launch& Ls = ss.lane();
     T* G0 = tied ? io.grads(0) : nullptr;
     T* Gf = io.grads(Ly + 1);
     int cur = 0;
