@@ -338,11 +338,13 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
+    // Epilogue: TMEM -> registers -> shared tile (the pipeline buffers are free once the last
+    // MMA committed) -> coalesced row-contiguous global stores with the fused epilogue.
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
     const int lg = (warp % 4) * 32;
-    const int row = m0 + lg + lane;
-    float* W = splits > 1 ? ws + (int64_t)split * p.M * p.N : nullptr;
+    constexpr int LDS = BN + 1;
+    float* Cs = reinterpret_cast<float*>(smem);
 #pragma unroll 1
     for (int c = 0; c < BN; c += 16) {
       uint32_t r[16];
@@ -353,17 +355,22 @@ __global__ void __launch_bounds__(192, 1)
             "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-      if (row >= p.M) continue;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) Cs[(lg + lane) * LDS + c + i] = nloc > 0 ? __uint_as_float(r[i]) : 0.0f;
+    }
+    asm volatile("bar.sync 1, 128;\n" ::);  // the four epilogue warps only
+    float* W = splits > 1 ? ws + (int64_t)split * p.M * p.N : nullptr;
+    const int et = threadIdx.x - 64;
+    const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
 #pragma unroll 1
-      for (int i = 0; i < 16; ++i) {
-        const int col = n0 + c + i;
-        if (col >= p.N) break;
-        const float v = nloc > 0 ? __uint_as_float(r[i]) : 0.0f;
-        if (W)
-          W[(int64_t)row * p.N + col] = v;
-        else
-          gemm_detail::epilogue_store(p, p.C, row, col, v);
-      }
+    for (int e = et; e < BM * BN; e += 128) {
+      const int rr = e / BN, cc = e % BN;
+      if (rr >= rows || cc >= cols) continue;
+      const float v = Cs[rr * LDS + cc];
+      if (W)
+        W[(int64_t)(m0 + rr) * p.N + n0 + cc] = v;
+      else
+        gemm_detail::epilogue_store(p, p.C, m0 + rr, n0 + cc, v);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -415,8 +422,11 @@ __global__ void k_split3(const float* __restrict__ X, int64_t R, int64_t C, int6
 template <int BN>
 void launch_multi(const Launch& L, const MultiOps& ops, const GemmArgs<float>& a, int nk, int splits, int tps,
                   float* ws) {
-  constexpr int STAGES = BN == 256 ? 3 : 4;
+  // two CTAs per SM (one's epilogue overlaps the other's MMAs); the smem also hosts the fp32
+  // epilogue tile BM x (BN + 1)
+  constexpr int STAGES = BN == 128 ? 3 : 4;
   using CF = Cfg<BN, STAGES>;
+  static_assert(BM * (BN + 1) * 4 <= STAGES * CF::STAGE_BYTES, "epilogue tile fits the pipeline smem");
   static bool attr = false;
   if (!attr) {
     SLQ_CUDA(cudaFuncSetAttribute(k_tc_multi<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
