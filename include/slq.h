@@ -56,7 +56,12 @@ enum { SLQ_ARCH_MLP = 0, SLQ_ARCH_GPT = 1, SLQ_ARCH_LLAMA = 2 };
  * passes on SIMT GEMMs (reported only); BF16X3: fp32 activations, every non-batched GEMM on the
  * tcgen05 tensor cores with operands split into three bf16 terms (fp32-faithful; the mode for the
  * bf16 models' gates). */
-enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2 };
+enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2, SLQ_PASS_PAIRED = 3, SLQ_PASS_PAIRED_FP32 = 4 };
+/* SLQ_PASS_PAIRED: the two gradient evaluations of Eq. (1) carried as (mean, half-difference)
+ * pairs through ONE pass, so (g+ - g-) is never formed by subtracting rounded gradients
+ * (SURVEY.md §8(f1)); non-batched pair GEMMs on tcgen05 (fp32-faithful three-term bf16 splits),
+ * nonlinear steps evaluated at both points in fp64.  SLQ_PASS_PAIRED_FP32: same with fp32 SIMT
+ * GEMMs.  GPT arch, world_size 1. */
 enum { SLQ_REORTH_NONE = 0, SLQ_REORTH_FULL = 1 };
 enum { SLQ_PARAM_FP32 = 0, SLQ_PARAM_BF16 = 1 };
 

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "paired.h"
 
 namespace slq {
 
@@ -79,15 +80,25 @@ struct PassExec {
   std::vector<Graph> graphs;
   bool use_graphs = getenv("SLQ_NO_GRAPHS") == nullptr;
 
-  PassExec(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b, const Launch& base, bool own) {
+  LocalIO<T> lio2;  // paired evaluation: (thetatil, gtil)
+
+  PassExec(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b, const Launch& base, bool own,
+           bool paired = false) {
     L = base;
     if (own) {
       SLQ_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
       L.stream = own_stream;
       L.ws = &own_ws;
     }
-    runner = make_runner<T>(d, plan, b, L);
+    if constexpr (sizeof(T) == 4) {
+      if (paired) {
+        runner = make_paired_runner(d, plan, b, L);
+        if (!runner) throw Error(SLQ_EUNSUPPORTED, "paired evaluation is implemented for the GPT arch only");
+      }
+    }
+    if (!runner) runner = make_runner<T>(d, plan, b, L);
     lio.plan = &plan;
+    lio2.plan = &plan;
   }
   ~PassExec() {
     if (L.stream) cudaStreamSynchronize(L.stream);
@@ -98,6 +109,12 @@ struct PassExec {
   }
 
   void eager(const T* th, T* g, double* loss_dev) {
+    if (runner->paired()) {
+      lio.shard = th;
+      lio.gshard = g;
+      runner->fwd_bwd_pair(lio, lio2, loss_dev);
+      return;
+    }
     if (fio) {
       fio->shard = th;
       fio->gshard = g;
@@ -107,6 +124,13 @@ struct PassExec {
       lio.gshard = g;
       runner->fwd_bwd(lio, loss_dev);
     }
+  }
+
+  // paired: (th, g) = (theta, gbar) and (th2, g2) = (thetatil, gtil)
+  void run_pair(const T* th, T* g, const T* th2, T* g2, double* loss_dev) {
+    lio2.shard = th2;
+    lio2.gshard = g2;
+    run(th, g, loss_dev);
   }
 
   void run(const T* th, T* g, double* loss_dev) {
@@ -172,6 +196,12 @@ struct EngineT : Engine {
   // communicator, so they stay serial.
   std::unique_ptr<PassExec<T>> pe[2];
   bool dual = false;
+  // paired evaluation (SLQ_PASS_PAIRED*): thm holds thetatil = eta v, gp gets gbar, gm gets gtil;
+  // the FD kernels then read gtil alone with scale 1/eta
+  bool paired_ = false;
+  const T* fd_a() const { return paired_ ? gm : gp; }
+  const T* fd_b() const { return paired_ ? nullptr : gm; }
+  double fd_scale(double inv2eta) const { return paired_ ? 2.0 * inv2eta : inv2eta; }
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   double* hstage;  // pinned host scalars
 
@@ -221,11 +251,15 @@ struct EngineT : Engine {
       SLQ_CUDA(cudaMemcpy(units_dev, ud.data(), sizeof(UnitDev) * ud.size(), cudaMemcpyHostToDevice));
     }
     SLQ_CUDA(cudaMallocHost(&hstage, 64 * sizeof(double)));
-    pe[0].reset(new PassExec<T>(d, plan, b, L, false));
+    paired_ = d.pass_numerics == SLQ_PASS_PAIRED || d.pass_numerics == SLQ_PASS_PAIRED_FP32;
+    if (paired_ && comm) throw Error(SLQ_EUNSUPPORTED, "paired evaluation with world_size > 1 is not implemented");
+    pe[0].reset(new PassExec<T>(d, plan, b, L, false, paired_));
     fio.plan = &plan;
     fio.comm = comm;
     fio.s = L.stream;
-    if (comm) {
+    if (paired_) {
+      // one pass evaluates both points; nothing to run concurrently
+    } else if (comm) {
       int64_t mx = 0;
       for (const UnitPlan& u : plan.units) mx = std::max(mx, u.padded);
       fio.pbuf0 = dalloc<T>(plan.units[0].padded);
@@ -253,6 +287,10 @@ struct EngineT : Engine {
 
   // g+ = grad L(theta+), g- = grad L(theta-): concurrently on two streams when dual
   void two_passes() {
+    if (paired_) {
+      pe[0]->run_pair(reinterpret_cast<const T*>(theta), gp, thm, gm, dscal + 2);
+      return;
+    }
     if (!dual || prof_enabled(L.prof)) {  // profiled runs are serial: per-launch durations stay honest
       pe[0]->run(thp, gp, dscal + 2);
       pe[0]->run(thm, gm, dscal + 3);
@@ -283,6 +321,13 @@ struct EngineT : Engine {
 
   // theta+- = theta +- eta v into thp / thm (reading R9); returns 1 / (2 eta_used)
   double form_points(const float* v, double eta) {
+    if constexpr (sizeof(T) == 4) {
+      if (paired_) {  // thetabar = theta (read in place), thetatil = eta v
+        SLQ_CHECK_ARG(eta > 0 && std::isfinite(eta), "eps / ||v|| must be finite and > 0");
+        pair_scale(L, v, eta, thm, n);
+        return 1.0 / (2.0 * eta);
+      }
+    }
     if constexpr (sizeof(T) == 8) {
       if (d.perturb == SLQ_PERTURB_EXACT) {
         SLQ_CHECK_ARG(eta > 0 && std::isfinite(eta), "eps / ||v|| must be finite and > 0");
@@ -310,7 +355,7 @@ struct EngineT : Engine {
     const double inv2eta = form_points(v, eps / sqrt(ss));
     two_passes();
     SLQ_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), L.stream));
-    fd_out<T>(L, gp, gm, inv2eta, out, n, dflag);
+    fd_out<T>(L, fd_a(), fd_b(), fd_scale(inv2eta), out, n, dflag);
     int flag = 0;
     SLQ_CUDA(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, L.stream));
     SLQ_CUDA(cudaStreamSynchronize(L.stream));
@@ -318,8 +363,13 @@ struct EngineT : Engine {
   }
 
   double grad(float* g) override {
-    convert_f32<T>(L, theta, thp, n);
-    pe[0]->run(thp, gp, dscal + 2);
+    if (paired_) {  // thetatil = 0: gbar is the gradient at theta
+      SLQ_CUDA(cudaMemsetAsync(thm, 0, sizeof(T) * (size_t)n, L.stream));
+      pe[0]->run_pair(reinterpret_cast<const T*>(theta), gp, thm, gm, dscal + 2);
+    } else {
+      convert_f32<T>(L, theta, thp, n);
+      pe[0]->run(thp, gp, dscal + 2);
+    }
     if (comm) comm->allreduce_sum_f64(dscal + 2, 1, L.stream);
     if (g) to_f32<T>(L, gp, g, n);
     double loss;
@@ -362,7 +412,7 @@ struct EngineT : Engine {
         perturb_lanczos<T>(L, exact, theta, wr, q[(k + 1) % 2], a_prev, b_k, eps, qk, thp, thm, n);
       }
       two_passes();
-      fd_partials3<T>(L, gp, gm, inv2eps, b_k, qprev, qk, wr, n, partials);
+      fd_partials3<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), b_k, qprev, qk, wr, n, partials);
       finish_reduce(nb, 3, dscal + 8);  // reduce_partials reads [nb x 3] row-major
       double s[3];
       to_host(dscal + 8, 3, s);
@@ -421,7 +471,7 @@ struct EngineT : Engine {
       const double inv2eps = form_points(qk, d.eps_default);
       two_passes();
       if (full) {
-        fd_w<T>(L, gp, gm, inv2eps, k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
+        fd_w<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
         const int nb = reorth_nblocks(n);
         // CGS pass 1 over q_1..q_k (its coefficient on q_k is alpha_k)
         reorth_dots(L, basis, n, k + 1, w, n, partials);
@@ -473,7 +523,7 @@ std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& p
   if (d.pass_numerics == SLQ_PASS_FP64)
     return std::unique_ptr<Engine>(new EngineT<double>(d, plan, b, theta_host, rank, comm, L));
   Launch Lf = L;
-  Lf.gemm_mode = d.pass_numerics == SLQ_PASS_BF16X3 ? 1 : 0;
+  Lf.gemm_mode = (d.pass_numerics == SLQ_PASS_BF16X3 || d.pass_numerics == SLQ_PASS_PAIRED) ? 1 : 0;
   return std::unique_ptr<Engine>(new EngineT<float>(d, plan, b, theta_host, rank, comm, Lf));
 }
 

@@ -73,6 +73,28 @@ void gemm(const Launch& L, const GemmArgs<T>& a);
 // accumulated in one fp32 TMEM accumulator (tc_gemm.cu).  batch == 1 only.
 void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a);
 
+// building blocks of multi-operand tcgen05 GEMMs (tc_gemm.cu)
+struct TcTerms {  // three bf16 terms of one fp32 operand, K-contiguous [rows x ldk]
+  void* t[3];
+  int rows;
+  int64_t ldk;
+};
+struct TcProd {  // one product A[ia].t[ta] . B[ib].t[tb]^T
+  int ia, ta, ib, tb;
+};
+struct TcPlan {
+  int bn, splits, tps;
+  size_t partial_bytes;
+};
+size_t tc_terms_bytes(int rows, int K);
+// X viewed as [rows x K], element (r, k) at r * s_row + k * s_k (one stride 1); writes 3 terms at dst
+TcTerms tc_split_terms(const Launch& L, const float* X, int rows, int K, int64_t s_row, int64_t s_k, void* dst);
+TcPlan tc_plan(int M, int N, int K, int nprods);
+// epi.C (+)= epilogue(sum_p A[ia].t[ta] . B[ib].t[tb]^T) with epi's bias / resid / accumulate
+void tc_gemm_products(const Launch& L, const TcPlan& plan, int M, int N, int K, const TcTerms* A, int nA,
+                      const TcTerms* B, int nB, const TcProd* prods, int nprods, const GemmArgs<float>& epi,
+                      void* partial_ws);
+
 // ---- layers (layers.cu) ----
 template <class T> void convert_f32(const Launch& L, const float* x, T* y, int64_t n);
 template <class T> void embed_fwd(const Launch& L, const int32_t* tok, int tok_stride, int nseq, int T_,

@@ -39,10 +39,18 @@ struct Runner {
   virtual void fwd_bwd(PassIO<T>& io, double* loss_sum_dev) = 0;
   virtual double tokens_global() const = 0;
   virtual double flops_per_pass() const = 0;  // algorithmic fwd+bwd FLOPs (this rank)
+  // paired evaluation (model_paired.cu): mean = (theta, gbar), diff = (eta v, gtil) in one pass
+  virtual bool paired() const { return false; }
+  virtual void fwd_bwd_pair(PassIO<T>& mean, PassIO<T>& diff, double* loss_sum) {
+    throw Error(SLQ_EUNSUPPORTED, "paired evaluation not available for this runner");
+  }
 };
 
 template <class T>
 std::unique_ptr<Runner<T>> make_runner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
                                        const Launch& L);
+// paired-evaluation runner (GPT); nullptr if the arch has none yet
+std::unique_ptr<Runner<float>> make_paired_runner(const slq_model_desc& d, const LayoutPlan& plan,
+                                                  const HostBatch& b, const Launch& L);
 
 }  // namespace slq

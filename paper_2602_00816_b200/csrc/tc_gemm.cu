@@ -246,7 +246,7 @@ void launch(cudaStream_t s, const void* A, int64_t lda, const void* B, int64_t l
 // one TMEM accumulator; the K loop runs over (product, k-tile) pairs, so a split-operand GEMM is
 // one long-K tensor-core GEMM.  Optional split-K over that sequence (partials to a workspace,
 // deterministic reduce).
-constexpr int kMaxTerms = 3, kMaxPairs = 8;
+constexpr int kMaxTerms = 6, kMaxPairs = 12;
 struct MultiOps {
   CUtensorMap a[kMaxTerms];
   CUtensorMap b[kMaxTerms];
@@ -511,6 +511,94 @@ void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a) {
     const int64_t mn = (int64_t)M * N;
     int blocks = (int)std::min<int64_t>(ceil_div(mn, 256), 148 * 8);
     gemm_detail::splitk_reduce<float><<<blocks, 256, 0, L.stream>>>(a, splits, ws);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+}
+
+// ---- general split / multi-product launch (used by the paired evaluation) ----
+
+size_t tc_terms_bytes(int rows, int K) {
+  const int64_t ldk = (K + 7) / 8 * 8;
+  return 3 * tc::align256(2 * (size_t)rows * ldk);
+}
+
+TcTerms tc_split_terms(const Launch& L, const float* X, int rows, int K, int64_t s_row, int64_t s_k, void* dst) {
+  using namespace tc;
+  SLQ_CHECK_ARG(s_k == 1 || s_row == 1, "tc split: one stride must be 1");
+  TcTerms t;
+  t.rows = rows;
+  t.ldk = (K + 7) / 8 * 8;
+  const size_t one = align256(2 * (size_t)rows * t.ldk);
+  for (int i = 0; i < 3; ++i) t.t[i] = (uint8_t*)dst + i * one;
+  auto* o0 = (__nv_bfloat16*)t.t[0];
+  auto* o1 = (__nv_bfloat16*)t.t[1];
+  auto* o2 = (__nv_bfloat16*)t.t[2];
+  LaunchScope scope(L.prof, KC_ELEM, L.stream, 0, 10.0 * (double)rows * K);
+  if (s_k == 1) {  // [rows x K] with row pitch s_row
+    dim3 g((unsigned)ceil_div(K, 32), (unsigned)ceil_div(rows, 32));
+    k_split3<false><<<g, 256, 0, L.stream>>>(X, rows, K, s_row, o0, o1, o2, t.ldk);
+  } else {  // stored [K x rows] with row pitch s_k -> transposed
+    dim3 g((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(K, 32));
+    k_split3<true><<<g, 256, 0, L.stream>>>(X, K, rows, s_k, o0, o1, o2, t.ldk);
+  }
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+  return t;
+}
+
+TcPlan tc_plan(int M, int N, int K, int nprods) {
+  using namespace tc;
+  TcPlan p;
+  const int64_t t128 = ceil_div(M, BM) * ceil_div(N, 128);
+  p.bn = t128 >= 148 ? 128 : 64;
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, p.bn));
+  const int nk = (K + BK - 1) / BK;
+  const int total = nprods * nk;
+  int splits = 1;
+  if (tiles < 148) splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * 148, tiles), total / 4));
+  p.tps = (int)ceil_div(total, splits);
+  p.splits = (int)ceil_div(total, p.tps);
+  p.partial_bytes = p.splits > 1 ? align256(4 * (size_t)M * N * p.splits) : 0;
+  return p;
+}
+
+void tc_gemm_products(const Launch& L, const TcPlan& plan, int M, int N, int K, const TcTerms* A, int nA,
+                      const TcTerms* B, int nB, const TcProd* prods, int nprods, const GemmArgs<float>& epi,
+                      void* partial_ws) {
+  using namespace tc;
+  SLQ_CHECK_ARG(nA * 3 <= kMaxTerms && nB * 3 <= kMaxTerms && nprods <= kMaxPairs, "tc products: too many terms");
+  MultiOps ops;
+  for (int i = 0; i < nA; ++i)
+    for (int t = 0; t < 3; ++t) ops.a[3 * i + t] = make_map_bf16(A[i].t[t], M, K, A[i].ldk, BM);
+  for (int i = 0; i < nB; ++i)
+    for (int t = 0; t < 3; ++t) ops.b[3 * i + t] = make_map_bf16(B[i].t[t], N, K, B[i].ldk, plan.bn);
+  ops.npairs = nprods;
+  for (int i = 0; i < nprods; ++i) {
+    ops.ai[i] = 3 * prods[i].ia + prods[i].ta;
+    ops.bi[i] = 3 * prods[i].ib + prods[i].tb;
+  }
+  GemmArgs<float> a = epi;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.batch = 1;
+  const int nk = (K + BK - 1) / BK;
+  float* ws = plan.splits > 1 ? (float*)partial_ws : nullptr;
+  {
+    LaunchScope scope(L.prof, KC_GEMM, L.stream, 2.0 * M * N * (double)K * nprods,
+                      2.0 * ((double)M * K * nA * 3 + (double)N * K * nB * 3) + 4.0 * M * N);
+    if (plan.bn == 128)
+      launch_multi<128>(L, ops, a, nk, plan.splits, plan.tps, ws);
+    else
+      launch_multi<64>(L, ops, a, nk, plan.splits, plan.tps, ws);
+    ++*L.launches;
+  }
+  if (plan.splits > 1) {
+    LaunchScope scope(L.prof, KC_GEMM, L.stream, 0, 4.0 * (double)M * N * (plan.splits + 1));
+    const int64_t mn = (int64_t)M * N;
+    int blocks = (int)std::min<int64_t>(ceil_div(mn, 256), 148 * 8);
+    gemm_detail::splitk_reduce<float><<<blocks, 256, 0, L.stream>>>(a, plan.splits, ws);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }

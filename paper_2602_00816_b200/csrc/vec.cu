@@ -133,7 +133,7 @@ __global__ void k_fd_partials3(const T* __restrict__ gp, const T* __restrict__ g
                                int64_t n, double* __restrict__ part) {
   double s1 = 0.0, s2 = 0.0, s3 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double d = ((double)gp[i] - (double)gm[i]) * inv2eta;
+    double d = (gm ? (double)gp[i] - (double)gm[i] : (double)gp[i]) * inv2eta;
     if (q_prev) d -= beta_k * (double)q_prev[i];
     const float wf = (float)d;
     w[i] = wf;
@@ -170,7 +170,7 @@ __global__ void k_fd_w(const T* __restrict__ gp, const T* __restrict__ gm, doubl
   const double b = beta_k ? *beta_k : 0.0;
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double d = ((double)gp[i] - (double)gm[i]) * inv2eta;
+    double d = (gm ? (double)gp[i] - (double)gm[i] : (double)gp[i]) * inv2eta;
     if (beta_k) d -= b * (double)q_prev[i];
     const float wf = (float)d;
     w[i] = wf;
@@ -187,7 +187,7 @@ __global__ void k_fd_out(const T* __restrict__ gp, const T* __restrict__ gm, dou
                          int64_t n, int* __restrict__ nonfinite) {
   int bad = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double d = ((double)gp[i] - (double)gm[i]) * inv2eta;
+    const double d = (gm ? (double)gp[i] - (double)gm[i] : (double)gp[i]) * inv2eta;
     if (!isfinite(d)) bad = 1;
     out[i] = (float)d;
   }

@@ -1,0 +1,72 @@
+"""Paired (mean, half-difference) evaluation of Eq. (1) on the GPU.
+
+One pass carries both gradient evaluations as pairs, so g+ - g- is never formed from rounded
+gradients; with fp32-faithful arithmetic (tcgen05 three-term splits, or fp32 SIMT) it must meet
+the FP32 gates of the north star against the fp64 oracle (exact perturbed points): HVP relative
+L2 <= 1e-4 and alpha/beta <= 1e-5 over the first 32 Lanczos steps.
+"""
+import numpy as np
+import pytest
+
+import slq_inputs as si
+from oracle import fdhvp, lanczos as OL, models, probe
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_00816_b200 import build
+    build.build()
+
+
+from paper_2602_00816_b200 import slq  # noqa: E402
+
+MODES = ["paired", "paired_fp32"]
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", ["gpt_tiny", "gpt_tiny_tied", "c2"])
+def test_paired_grad_and_hvp(name, mode):
+    cfg = si.CONFIGS[name]
+    th = si.init_params(cfg)
+    tok = si.tokens(cfg)
+    v = si.random_vector(th.size, 5)
+    with slq.SlqContext(cfg, th, tok, pass_numerics=mode) as c:
+        lay = c.layout()
+        g = torch.empty(c.P_loc, dtype=torch.float32, device="cuda")
+        loss = c.grad(g)
+        gfull = slq.unshard([g.cpu().numpy()], lay)
+        vd = torch.from_numpy(slq.shard_of(v, lay, 0, 1)).cuda()
+        out = torch.empty_like(vd)
+        c.hvp(vd, out, cfg.eps)
+        hv = slq.unshard([out.cpu().numpy()], lay)
+    l_ref, g_ref = models.loss_grad(th, cfg, tok)
+    ref = fdhvp.hvp(fdhvp.make_grad_fn(cfg, tok), th, v, cfg.eps, "exact")
+    eg = np.linalg.norm(gfull - g_ref) / np.linalg.norm(g_ref)
+    eh = np.linalg.norm(hv - ref) / np.linalg.norm(ref)
+    print(f"{name} [{mode}]: loss {abs(loss - l_ref) / abs(l_ref):.1e} grad {eg:.2e} HVP {eh:.2e}")
+    assert abs(loss - l_ref) <= 1e-6 * abs(l_ref)
+    assert eg <= 2e-5
+    assert eh <= 1e-4
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name,m", [("gpt_tiny", 16), ("c2", 32)])
+def test_paired_lanczos_fp32_gates(name, m, mode):
+    cfg = si.CONFIGS[name]
+    th = si.init_params(cfg)
+    tok = si.tokens(cfg)
+    with slq.SlqContext(cfg, th, tok, pass_numerics=mode, reorth="full", max_steps=m) as c:
+        a, b = c.lanczos(cfg.probe_seed0, m)
+    g = fdhvp.make_grad_fn(cfg, tok)
+    r = OL.lanczos(lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact"),
+                   probe.rademacher_probe(cfg.probe_seed0, th.size), m, "full")
+    scale = np.abs(r.alpha).max()
+    ea = np.abs(a - r.alpha) / np.maximum(np.abs(r.alpha), 1e-2 * scale)
+    eb = np.abs(b - r.beta) / np.abs(r.beta)
+    print(f"{name} [{mode}]: max rel alpha {ea.max():.2e} beta {eb.max():.2e}")
+    assert ea.max() <= 1e-5 and eb.max() <= 1e-5
