@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
-    p.add_argument("--numerics", default="fp64", choices=["fp64", "fp32", "bf16x3"],
+    p.add_argument("--numerics", default="fp64", choices=["fp64", "fp32", "bf16x3", "paired", "paired_fp32"],
                    help="gradient-pass arithmetic (fp64 = the c2 parity path; bf16x3 = tcgen05)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -269,8 +269,9 @@ def main():
     if dom == "gemm" and args.numerics != "fp64":
         bf16 = peaks.get("bf16_tflops", 1590.0)
         achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12
-        tc_note = ("tcgen05 kind::f16 bf16 products (6 per fp32-faithful GEMM, all counted)"
-                   if args.numerics == "bf16x3" else "SIMT fp32 (no tensor core)")
+        tc_note = {"bf16x3": "tcgen05 kind::f16 bf16 products (6 per fp32-faithful GEMM, all counted)",
+                   "paired": "tcgen05 pair GEMMs (7 + 12 bf16 products per pair GEMM) and SIMT fp32 attention",
+                   }.get(args.numerics, "SIMT fp32 (no tensor core)")
         roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s", "frac": achieved / bf16,
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks
                                 else "fallback 1590 TFLOP/s") + "; " + tc_note}
@@ -297,7 +298,7 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": {"fp64": "f64", "fp32": "f32", "bf16x3": "bf16x3"}[args.numerics],
+        "vs_baseline": None, "dtype": {"fp64": "f64", "fp32": "f32", "bf16x3": "bf16x3", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {'GPT' if cfg.arch == si.ARCH_GPT else 'Llama'} {cfg.n_layers}L "
                                f"d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} V{cfg.vocab}, {si.n_params(cfg)} params "
