@@ -84,21 +84,22 @@ void prof_end(Profiler* p, int cls, cudaStream_t s, double flops, double bytes) 
   if (p->pending.size() > 200000) p->flush();
 }
 
-void* Workspace::get(size_t need, cudaStream_t s) {
+// A grown workspace keeps its previous buffers alive until destruction: captured CUDA graphs may
+// still reference them (freeing them made later graph replays fault).
+void* Workspace::get(size_t need, cudaStream_t) {
   if (need <= bytes) return ptr;
-  if (ptr) {
-    SLQ_CUDA(cudaStreamSynchronize(s));
-    SLQ_CUDA(cudaFree(ptr));
-    ptr = nullptr;
-    bytes = 0;
-  }
+  if (ptr) retired.push_back(ptr);
+  ptr = nullptr;
+  bytes = 0;
   const size_t nb = need + need / 4 + 4096;
   SLQ_CUDA(cudaMalloc(&ptr, nb));
   bytes = nb;
   return ptr;
 }
 Workspace::~Workspace() {
+  cudaDeviceSynchronize();
   if (ptr) cudaFree(ptr);
+  for (void* p : retired) cudaFree(p);
 }
 
 }  // namespace slq

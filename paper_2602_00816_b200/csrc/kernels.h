@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "common.h"
 
 namespace slq {
@@ -12,7 +14,8 @@ namespace slq {
 struct Workspace {
   void* ptr = nullptr;
   size_t bytes = 0;
-  void* get(size_t need, cudaStream_t s);  // grows (stream-synchronised) when too small
+  std::vector<void*> retired;              // outgrown buffers (graphs may reference them)
+  void* get(size_t need, cudaStream_t s);  // grows when too small; never frees a live buffer
   ~Workspace();
 };
 
