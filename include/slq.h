@@ -157,6 +157,21 @@ slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_ne
 slq_status slq_quadrature(const double* alpha, const double* beta, int32_t m, double* nodes,
                           double* weights);
 
+/* Conjugate-gradient inverse-HVP ("repeated HVP calls plus
+ * scalar reductions and shard-local vector operations"): solves (H + damping I) x = b with x_0 = 0,
+ * each H p one FD-HVP with step eps_default (same normalisation as slq_hvp), until
+ * ||r|| <= tol ||b|| or max_iter.  H is indefinite: damping must make H + damping I positive
+ * definite (SLQ_ENUMERIC if p^T (H + damping I) p <= 0).  b, x: shards, device or host.  Collective. */
+slq_status slq_cg(slq_ctx* ctx, const float* b_shard, float* x_shard, double damping, int32_t max_iter, double tol,
+                  int32_t* iters, double* rel_residual);
+
+/* Block-diagonal hypothesis test: v = the Rademacher probe of probe_seed
+ * (unit norm), h = H v; for each FSDP unit b (embedding, transformer blocks, final norm + head):
+ * h_b = H v^(b) with v zeroed outside b; rel_err[b] = ||h|_b - h_b|_b|| / ||h|_b||,
+ * cosine[b] = cos(h|_b, h_b|_b).  rel_err / cosine: host arrays of slq_num_units.  Costs
+ * 1 + n_units HVPs.  Collective. */
+slq_status slq_blockdiag(slq_ctx* ctx, uint64_t probe_seed, double* rel_err, double* cosine);
+
 /* Writes the Lanczos start vector q_1 (probe) for probe_seed into a caller shard (device or host).
  * Exposed so the probe can be checked bit-exactly against an independent generator. */
 slq_status slq_probe(slq_ctx* ctx, uint64_t probe_seed, float* q_shard);

@@ -20,4 +20,4 @@ Modules
 Parity status of each function is listed in DESIGN.md §"Oracle pins"; every function here is
 pinned by at least one `-m "not gpu"` test in tests/test_oracle_*.py.
 """
-from . import probe, models, fdhvp, lanczos  # noqa: F401
+from . import probe, models, fdhvp, lanczos, cg, blockdiag  # noqa: F401

@@ -359,6 +359,43 @@ slq_status slq_probe(slq_ctx* ctx, uint64_t seed, float* q) {
   });
 }
 
+slq_status slq_cg(slq_ctx* ctx, const float* b, float* x, double damping, int32_t max_iter, double tol,
+                  int32_t* iters, double* rel_residual) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    SLQ_CHECK_ARG(b && x && b != x, "b / x (non-aliasing)");
+    SLQ_CHECK_ARG(max_iter >= 1 && damping >= 0 && tol >= 0, "max_iter >= 1, damping >= 0, tol >= 0");
+    check_device(ctx);
+    const size_t bytes = sizeof(float) * (size_t)ctx->plan.P_loc;
+    const bool bdev = is_device_ptr(b), xdev = is_device_ptr(x);
+    ensure_stage(ctx);
+    const float* bd = b;
+    float* xd = x;
+    if (!bdev) {
+      SLQ_CUDA(cudaMemcpyAsync(ctx->stage_in, b, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      bd = ctx->stage_in;
+    }
+    if (!xdev) xd = ctx->stage_out;
+    double rr = 0;
+    const int it = ctx->engine->cg(bd, xd, damping, max_iter, tol, &rr);
+    if (!xdev) {
+      SLQ_CUDA(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      SLQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    if (iters) *iters = it;
+    if (rel_residual) *rel_residual = rr;
+  });
+}
+
+slq_status slq_blockdiag(slq_ctx* ctx, uint64_t probe_seed, double* rel_err, double* cosine) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    SLQ_CHECK_ARG(rel_err && cosine, "rel_err / cosine");
+    check_device(ctx);
+    ctx->engine->blockdiag(probe_seed, rel_err, cosine);
+  });
+}
+
 slq_status slq_profile(slq_ctx* ctx, int32_t enable, int32_t reset) {
   if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
   return guarded(ctx, [&] {

@@ -24,6 +24,10 @@ struct Engine {
   virtual LanczosInfo lanczos(uint64_t seed, int m, double* alpha, double* beta) = 0;
   virtual void probe(uint64_t seed, float* q) = 0;
   virtual double pass_flops() const = 0;  // algorithmic FLOPs of one fwd+bwd (this rank)
+  // CG on (H + damping I) x = b; returns iterations, writes the relative residual
+  virtual int cg(const float* b, float* x, double damping, int max_iter, double tol, double* relres) = 0;
+  // block-diagonal test over the FSDP units: rel_err[u], cosine[u]
+  virtual void blockdiag(uint64_t seed, double* rel_err, double* cosine) = 0;
   LanczosInfo last_info;
 };
 

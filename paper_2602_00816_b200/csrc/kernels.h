@@ -169,5 +169,10 @@ void reorth_dots(const Launch& L, const float* Q, int64_t ldq, int k, const floa
 void reorth_update(const Launch& L, const float* Q, int64_t ldq, int k, const double* c, float* w,
                    int64_t n, double* part_dots, double* part_norm);
 void nonfinite_check(const Launch& L, const float* x, int64_t n, int* flag);
+void dot_partials(const Launch& L, const float* a, const float* b, int64_t n, double* partials);  // [vec_nblocks(n)]
+void axpby(const Launch& L, float* y, const float* x, double a, double b, int64_t n);             // y = a x + b y
+void mask_range(const Launch& L, const float* v, float* out, int64_t lo, int64_t hi, int64_t n);
+// over [lo, hi): partials[4 * block + {0..3}] = sum (a-b)^2, a.a, a.b, b.b; returns the block count
+int cmp4_partials(const Launch& L, const float* a, const float* b, int64_t lo, int64_t hi, double* partials);
 
 }  // namespace slq

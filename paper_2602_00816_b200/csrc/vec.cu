@@ -332,6 +332,49 @@ __global__ void __launch_bounds__(kRThreads) k_reorth_update(const float* __rest
   }
 }
 
+__global__ void k_dot(const float* __restrict__ a, const float* __restrict__ b, int64_t n, double* __restrict__ part) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += (double)a[i] * (double)b[i];
+  s = block_sum_d(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// y = a x + b y
+__global__ void k_axpby(float* __restrict__ y, const float* __restrict__ x, double a, double b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (float)(a * (double)x[i] + b * (double)y[i]);
+}
+
+// out = v on [lo, hi), 0 elsewhere
+__global__ void k_mask_range(const float* __restrict__ v, float* __restrict__ out, int64_t lo, int64_t hi, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (i >= lo && i < hi) ? v[i] : 0.0f;
+}
+
+// over [lo, hi): sum (a-b)^2, a.a, a.b, b.b  -> part[4 * block + j]
+__global__ void k_cmp4(const float* __restrict__ a, const float* __restrict__ b, int64_t lo, int64_t hi,
+                       double* __restrict__ part) {
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a[i], y = b[i];
+    s0 += (x - y) * (x - y);
+    s1 += x * x;
+    s2 += x * y;
+    s3 += y * y;
+  }
+  s0 = block_sum_d(s0);
+  s1 = block_sum_d(s1);
+  s2 = block_sum_d(s2);
+  s3 = block_sum_d(s3);
+  if (threadIdx.x == 0) {
+    part[4 * blockIdx.x + 0] = s0;
+    part[4 * blockIdx.x + 1] = s1;
+    part[4 * blockIdx.x + 2] = s2;
+    part[4 * blockIdx.x + 3] = s3;
+  }
+}
+
 __global__ void k_nonfinite(const float* __restrict__ x, int64_t n, int* flag) {
   int bad = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -447,6 +490,24 @@ void reorth_update(const Launch& L, const float* Q, int64_t ldq, int k, const do
   // algorithmic bytes: Q once from HBM (the fused dots re-read is the L2-resident chunk) + w r/w
   VLAUNCH(KC_REORTH, (part_dots ? 4.0 : 2.0) * k * n, 4.0 * (k + 2.0) * n, reorth_nblocks(n), kRThreads,
           sizeof(double) * k, k_reorth_update, Q, ldq, k, c, w, n, part_dots, part_norm);
+}
+
+void dot_partials(const Launch& L, const float* a, const float* b, int64_t n, double* part) {
+  VLAUNCH(KC_VEC, 2.0 * n, 8.0 * n, vec_nblocks(n), kThreads, 0, k_dot, a, b, n, part);
+}
+
+void axpby(const Launch& L, float* y, const float* x, double a, double b, int64_t n) {
+  VLAUNCH(KC_VEC, 3.0 * n, 12.0 * n, vec_nblocks(n), kThreads, 0, k_axpby, y, x, a, b, n);
+}
+
+void mask_range(const Launch& L, const float* v, float* out, int64_t lo, int64_t hi, int64_t n) {
+  VLAUNCH(KC_VEC, 0, 8.0 * n, vec_nblocks(n), kThreads, 0, k_mask_range, v, out, lo, hi, n);
+}
+
+int cmp4_partials(const Launch& L, const float* a, const float* b, int64_t lo, int64_t hi, double* part) {
+  const int nb = vec_nblocks(std::max<int64_t>(hi - lo, 1));
+  VLAUNCH(KC_VEC, 8.0 * (hi - lo), 8.0 * (hi - lo), nb, kThreads, 0, k_cmp4, a, b, lo, hi, part);
+  return nb;
 }
 
 void nonfinite_check(const Launch& L, const float* x, int64_t n, int* flag) {

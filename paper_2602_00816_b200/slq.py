@@ -84,6 +84,8 @@ def lib() -> ctypes.CDLL:
         "slq_diag_fp64_peak": (I32, [I32, P]),
         "slq_diag_dmma_peak": (I32, [I32, P]),
         "slq_diag_gemm_f64": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
+        "slq_cg": (I32, [P, P, P, D, I32, D, P, P]),
+        "slq_blockdiag": (I32, [P, U64, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -290,6 +292,18 @@ class SlqContext:
         md, bn, nf = ctypes.c_int32(), ctypes.c_double(), ctypes.c_int32()
         _check(lib().slq_lanczos_info(self._h, ctypes.byref(md), ctypes.byref(bn), ctypes.byref(nf)), self._h)
         return {"m_done": md.value, "beta_next": bn.value, "nonfinite": nf.value}
+
+    def cg(self, b, x, damping: float, max_iter: int, tol: float = 0.0):
+        it, rr = ctypes.c_int32(), ctypes.c_double()
+        _check(lib().slq_cg(self._h, _ptr(b), _ptr(x), float(damping), int(max_iter), float(tol), ctypes.byref(it),
+                            ctypes.byref(rr)), self._h)
+        return it.value, rr.value
+
+    def blockdiag(self, seed: int):
+        nu = lib().slq_num_units(self._h)
+        rel, cos = np.empty(nu), np.empty(nu)
+        _check(lib().slq_blockdiag(self._h, ctypes.c_uint64(seed), rel.ctypes.data, cos.ctypes.data), self._h)
+        return rel, cos
 
     def probe(self, seed: int, q) -> None:
         _check(lib().slq_probe(self._h, ctypes.c_uint64(seed), _ptr(q)), self._h)
