@@ -16,6 +16,20 @@ Readings:
   * Quadrature nodes/weights: eigen-decomposition of T_m by cyclic Jacobi rotations (an
     algorithm independent of the library's implicit-shift QL); nodes ascending, weights =
     squared first components of the normalised eigenvectors.
+  * Sliding-window reorthogonalisation ("sliding-window reorthogonalisation of size
+    r"; "orthogonalised against up to r previously stored Lanczos vectors"): the same
+    CGS2 as `full`, restricted to the r most recent vectors q_{k-r+1} .. q_k (DESIGN.md reading
+    R17; r >= k reduces to full).
+  * Basis storage precision ("only the Lanczos basis vectors are stored in
+    either bfloat16 or float32", scalars in higher precision): q_{k+1} = round(w / beta_{k+1})
+    to the storage format, and every later use of q_j (the HVP direction, the three-term
+    recurrence, alpha, the reorthogonalisation) reads the stored, rounded vector.  bf16 rounding
+    is round-to-nearest-even from the fp64 value (`bf16_round`).
+  * Ghosts ("loss of orthogonality yields ghost eigenvalues"; Theorem 3's "spurious
+    duplicate eigenvalues"): `ghost_clusters` groups the sorted Ritz values whose neighbour gaps
+    are <= tol; a cluster with two or more members is a duplicate ("ghost") cluster.  An
+    unreduced T_m has distinct eigenvalues, so in exact arithmetic such clusters arise only
+    from genuinely clustered eigenvalues of H or from lost orthogonality (R18).
 """
 from __future__ import annotations
 
@@ -36,12 +50,48 @@ class LanczosResult:
     basis: np.ndarray | None = None   # [m_done, P] when kept
 
 
+def bf16_round(x) -> np.ndarray:
+    """Round fp64 values to the nearest bfloat16 (8 significant bits, exponent range of fp32),
+    ties to even; returned as fp64.  Written out from the format's definition: with e the
+    binary exponent of |x| (clamped to the fp32 subnormal floor -126), the bf16 spacing near x
+    is 2^(e-7); x / spacing is exact (power-of-two scaling) and np.round rounds half to even."""
+    x = np.asarray(x, dtype=np.float64)
+    out = np.zeros_like(x)
+    nz = (x != 0) & np.isfinite(x)
+    e = np.floor(np.log2(np.abs(x[nz])))
+    # log2 can be off by one ulp near powers of two: fix e so that 2^e <= |x| < 2^(e+1)
+    ax = np.abs(x[nz])
+    e = np.where(np.ldexp(1.0, e.astype(np.int64)) > ax, e - 1, e)
+    e = np.where(np.ldexp(1.0, (e + 1).astype(np.int64)) <= ax, e + 1, e)
+    e = np.maximum(e, -126.0)
+    spacing = np.ldexp(1.0, (e - 7).astype(np.int64))
+    out[nz] = np.round(x[nz] / spacing) * spacing
+    out[~np.isfinite(x)] = x[~np.isfinite(x)]
+    return out
+
+
+def store(x: np.ndarray, basis: str) -> np.ndarray:
+    """Basis storage rounding: fp64 (none), fp32 (RNE) or bf16 (RNE)."""
+    if basis == "fp64":
+        return np.asarray(x, dtype=np.float64)
+    if basis == "fp32":
+        return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+    if basis == "bf16":
+        return bf16_round(x)
+    raise ValueError(basis)
+
+
 def lanczos(apply_h: Callable[[np.ndarray], np.ndarray], q1: np.ndarray, m: int,
-            reorth: str = "full", tol: float = 1e-10, keep_basis: bool = False) -> LanczosResult:
-    """m steps of symmetric Lanczos from unit q1, A(2,7) order, fp64."""
-    q = np.asarray(q1, dtype=np.float64).copy()
+            reorth: str = "full", tol: float = 1e-10, keep_basis: bool = False,
+            window: int = 0, basis: str = "fp64") -> LanczosResult:
+    """m steps of symmetric Lanczos from unit q1, A(2,7) order, fp64 scalars.
+    reorth: "none" | "full" | "window" (CGS2 against the `window` most recent vectors);
+    basis: storage of the Lanczos vectors, "fp64" | "fp32" | "bf16"."""
+    if reorth == "window" and window < 1:
+        raise ValueError("window reorthogonalisation needs window >= 1")
+    q = store(q1, basis).copy()
     P = q.size
-    Q = np.empty((m, P)) if (reorth == "full" or keep_basis) else None
+    Q = np.empty((m, P)) if (reorth in ("full", "window") or keep_basis) else None
     alpha: List[float] = []
     betas: List[float] = []          # beta_{k+1} for k = 1..m_done
     q_prev = np.zeros(P)
@@ -53,8 +103,8 @@ def lanczos(apply_h: Callable[[np.ndarray], np.ndarray], q1: np.ndarray, m: int,
         w = w - a * q
         if Q is not None:
             Q[k] = q
-        if reorth == "full":
-            Qk = Q[:k + 1]
+        if reorth in ("full", "window"):
+            Qk = Q[:k + 1] if reorth == "full" else Q[max(0, k + 1 - window):k + 1]
             for _ in range(2):                       # CGS2
                 c = Qk @ w
                 w = w - Qk.T @ c
@@ -67,7 +117,7 @@ def lanczos(apply_h: Callable[[np.ndarray], np.ndarray], q1: np.ndarray, m: int,
         if b_next <= tol * tmax:
             breakdown = True
             break
-        q_prev, q = q, w / b_next
+        q_prev, q = q, store(w / b_next, basis)
         b = b_next
     md = len(alpha)
     return LanczosResult(alpha=np.array(alpha), beta=np.array(betas[:md - 1]),
@@ -138,3 +188,20 @@ def slq_density(grid: np.ndarray, node_sets, weight_sets, sigma: float) -> np.nd
     for nodes, w in zip(node_sets, weight_sets):
         out += (w[None, :] * np.exp(-0.5 * ((grid[:, None] - nodes[None, :]) / sigma) ** 2)).sum(1)
     return out / (len(node_sets) * sigma * math.sqrt(2 * math.pi))
+
+
+def ghost_clusters(nodes: Sequence[float], tol: float) -> Tuple[np.ndarray, List[Tuple[int, int, float]]]:
+    """Single-linkage clusters of the ascending Ritz values: nodes i and i+1 share a cluster when
+    nodes[i+1] - nodes[i] <= tol.  Returns the cluster id of every node and, for every cluster
+    with >= 2 members (a duplicate / "ghost" cluster), (first index, size, splitting =
+    max - min).  tol = 0 separates distinct values (an unreduced T_m has distinct eigenvalues)."""
+    x = np.asarray(nodes, dtype=np.float64)
+    ids = np.zeros(x.size, dtype=np.int64)
+    for i in range(1, x.size):
+        ids[i] = ids[i - 1] + (0 if x[i] - x[i - 1] <= tol else 1)
+    ghosts = []
+    for c in range(int(ids[-1]) + 1 if x.size else 0):
+        idx = np.nonzero(ids == c)[0]
+        if idx.size >= 2:
+            ghosts.append((int(idx[0]), int(idx.size), float(x[idx[-1]] - x[idx[0]])))
+    return ids, ghosts
