@@ -62,7 +62,15 @@ enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2, SLQ_PASS_PAIRE
  * (SURVEY.md §8(f1)); non-batched pair GEMMs on tcgen05 (fp32-faithful three-term bf16 splits),
  * nonlinear steps evaluated at both points in fp64.  SLQ_PASS_PAIRED_FP32: same with fp32 SIMT
  * GEMMs.  GPT arch, world_size 1. */
-enum { SLQ_REORTH_NONE = 0, SLQ_REORTH_FULL = 1 };
+/* Lanczos reorthogonalisation: NONE = three-term recurrence with three
+ * rotating vectors and no stored basis; FULL = CGS2 against every stored vector; WINDOW = CGS2
+ * against the reorth_window most recent vectors q_{k-r+1} .. q_k (ring buffer of r rows;
+ * DESIGN.md reading R17). */
+enum { SLQ_REORTH_NONE = 0, SLQ_REORTH_FULL = 1, SLQ_REORTH_WINDOW = 2 };
+/* Storage of the Lanczos basis: FP32, or BF16 (each q_{k+1} rounded once,
+ * RNE, from fp64 w / beta_{k+1}; every later use reads the stored value; R19).  Scalars
+ * are fp64 either way.  BF16 needs reorth FULL or WINDOW. */
+enum { SLQ_BASIS_FP32 = 0, SLQ_BASIS_BF16 = 1 };
 enum { SLQ_PARAM_FP32 = 0, SLQ_PARAM_BF16 = 1 };
 
 /* Model + numerics description.  Fields unused by an arch are ignored (set them to 0). */
@@ -79,6 +87,8 @@ typedef struct {
   int32_t max_steps;       /* largest m slq_lanczos will be asked for (sizes the Krylov basis) */
   double eps_default;      /* FD step used by slq_lanczos (the north-star signature has no eps) */
   int32_t perturb;         /* SLQ_PERTURB_*: how theta +- eta v is formed (reading R9) */
+  int32_t reorth_window;   /* r for SLQ_REORTH_WINDOW (2 <= r); ignored otherwise */
+  int32_t basis_dtype;     /* SLQ_BASIS_* */
 } slq_model_desc;
 
 /* SLQ_PERTURB_EXACT: theta +- eta*v is evaluated in the pass precision (fp64 passes: an fp64
@@ -156,6 +166,15 @@ slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_ne
  * beta may be NULL when m == 1.  Implicit-shift QL (Golub-Welsch). */
 slq_status slq_quadrature(const double* alpha, const double* beta, int32_t m, double* nodes,
                           double* weights);
+
+/* Ghost diagnostic (host only, no context, pure; Theorem 3 "spurious duplicate
+ * eigenvalues"; R18): single-linkage clusters of ascending Ritz values `nodes[m]`,
+ * neighbours joined when nodes[i+1] - nodes[i] <= tol.  cluster_id[m] (may be NULL) gets each
+ * node's cluster index (0-based, ascending); *n_ghost = number of clusters with >= 2 members;
+ * *max_split = the largest max - min over those clusters (0 if none).  SLQ_EINVAL if nodes are
+ * not ascending / finite or tol < 0. */
+slq_status slq_ghost_clusters(const double* nodes, int32_t m, double tol, int32_t* cluster_id, int32_t* n_ghost,
+                              double* max_split);
 
 /* Conjugate-gradient inverse-HVP ("repeated HVP calls plus
  * scalar reductions and shard-local vector operations"): solves (H + damping I) x = b with x_0 = 0,

@@ -15,6 +15,7 @@
 
 namespace slq {
 void tridiag_gauss(const double* alpha, const double* beta, int m, double* nodes, double* weights);
+void ghost_clusters(const double* nodes, int m, double tol, int32_t* cluster_id, int32_t* n_ghost, double* max_split);
 
 const char* kernel_class_name(int c) {
   static const char* names[KC_COUNT] = {"gemm", "attention", "norm", "cross_entropy", "embedding",
@@ -342,6 +343,11 @@ slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_ne
 
 slq_status slq_quadrature(const double* alpha, const double* beta, int32_t m, double* nodes, double* weights) {
   return guarded(nullptr, [&] { tridiag_gauss(alpha, beta, m, nodes, weights); });
+}
+
+slq_status slq_ghost_clusters(const double* nodes, int32_t m, double tol, int32_t* cluster_id, int32_t* n_ghost,
+                              double* max_split) {
+  return guarded(nullptr, [&] { ghost_clusters(nodes, m, tol, cluster_id, n_ghost, max_split); });
 }
 
 slq_status slq_probe(slq_ctx* ctx, uint64_t seed, float* q) {

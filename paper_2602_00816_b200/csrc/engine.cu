@@ -183,7 +183,11 @@ struct EngineT : Engine {
   std::vector<void*> allocs;
   float* theta;
   T *thp, *thm, *gp, *gm;
+  // Krylov basis (reorth FULL: max_steps + 1 rows; WINDOW: a ring of r rows, q_j in row j % r):
+  // fp32 rows, or bf16 rows plus two fp32 working copies of q_k, q_{k-1} (qf[k % 2])
   float *basis = nullptr, *w = nullptr, *vq[3] = {nullptr, nullptr, nullptr};
+  __nv_bfloat16* basis16 = nullptr;
+  float* qf[2] = {nullptr, nullptr};
   double* dscal;      // [0] sumsq, [1] beta_k, [2] loss, [3..] alpha / reorth coefficients
   double* partials;
   int* dflag;
@@ -234,8 +238,15 @@ struct EngineT : Engine {
     SLQ_CUDA(cudaMemset(gp, 0, sizeof(T) * (size_t)n));
     SLQ_CUDA(cudaMemset(gm, 0, sizeof(T) * (size_t)n));
     w = dalloc<float>(n);
-    if (d.reorth == SLQ_REORTH_FULL) {
-      basis = dalloc<float>((int64_t)(max_steps + 1) * n);
+    if (d.reorth == SLQ_REORTH_FULL || d.reorth == SLQ_REORTH_WINDOW) {
+      const int64_t rows = d.reorth == SLQ_REORTH_FULL ? max_steps + 1 : d.reorth_window;
+      if (d.basis_dtype == SLQ_BASIS_BF16) {
+        basis16 = dalloc<__nv_bfloat16>(rows * n);
+        qf[0] = dalloc<float>(n);
+        qf[1] = dalloc<float>(n);
+      } else {
+        basis = dalloc<float>(rows * n);
+      }
     } else {
       for (int i = 0; i < 3; ++i) vq[i] = dalloc<float>(n);
     }
@@ -516,39 +527,57 @@ struct EngineT : Engine {
     return info;
   }
 
+  // CGS over the `cnt` basis rows [0, cnt) (the window's ring holds exactly the last r vectors)
+  template <class B>
+  void cgs2(const B* Q, int cnt, int kslot, double* d_coef, double* d_alpha_k) {
+    const int nb = reorth_nblocks(n);
+    // CGS pass 1 over the window (its coefficient on q_k is alpha_k)
+    reorth_dots<B>(L, Q, n, cnt, w, n, partials);
+    finish_reduce(nb, cnt, d_coef);
+    SLQ_CUDA(cudaMemcpyAsync(d_alpha_k, d_coef + kslot, sizeof(double), cudaMemcpyDeviceToDevice, L.stream));
+    // update of pass 1 fused with the partial dots of CGS pass 2
+    reorth_update<B>(L, Q, n, cnt, d_coef, w, n, partials, nullptr);
+    finish_reduce(nb, cnt, d_coef);
+    // update of pass 2 fused with ||w||^2
+    reorth_update<B>(L, Q, n, cnt, d_coef, w, n, nullptr, partials);
+    finish_reduce(nb, 1, dscal + 0);
+  }
+
   LanczosInfo lanczos(uint64_t seed, int m, double* alpha, double* beta) override {
     last_info = LanczosInfo();
     SLQ_CHECK_ARG(m >= 1 && m <= max_steps, "1 <= m <= max_steps");
-    const bool full = d.reorth == SLQ_REORTH_FULL;
-    if (!full) return lanczos_nobasis(seed, m, alpha, beta);
+    if (d.reorth == SLQ_REORTH_NONE) return lanczos_nobasis(seed, m, alpha, beta);
     for (int i = 0; i < m; ++i) alpha[i] = NAN;
     for (int i = 0; i + 1 < m; ++i) beta[i] = NAN;
     LanczosInfo info;
-    auto qrow = [&](int k) -> float* { return full ? basis + (int64_t)k * n : vq[k % 3]; };
+    const bool window = d.reorth == SLQ_REORTH_WINDOW;
+    const bool b16 = basis16 != nullptr;
+    const int r = d.reorth_window;
+    auto slot = [&](int k) { return window ? k % r : k; };
+    // fp32 view of q_k: the basis row itself (fp32 basis) or the exact working copy (bf16 basis)
+    auto qvec = [&](int k) -> float* { return b16 ? qf[k % 2] : basis + (int64_t)slot(k) * n; };
     double* d_beta = dscal + 1;
-    double* d_coef = dscal + 8;                  // [max_steps + 1]
+    double* d_coef = dscal + 8;                     // [max_steps + 1]
     double* d_alpha = dscal + 8 + (max_steps + 1);  // [max_steps + 1]
-    probe_fill(L, qrow(0), n, units_dev, (int)plan.units.size(), seed, 1.0 / sqrt((double)plan.P));
+    const double inv_sqrt_P = 1.0 / sqrt((double)plan.P);
+    if (b16) {  // q_1 = bf16(s / sqrt(P)): signs first, one rounding from fp64
+      probe_fill(L, qf[0], n, units_dev, (int)plan.units.size(), seed, 1.0);
+      store_bf16(L, qf[0], nullptr, inv_sqrt_P, basis16, qf[0], n);
+    } else {
+      probe_fill(L, qvec(0), n, units_dev, (int)plan.units.size(), seed, inv_sqrt_P);
+    }
     double tmax = 0.0;
     for (int k = 0; k < m; ++k) {
-      float* qk = qrow(k);
-      const float* qprev = k > 0 ? qrow(k - 1) : nullptr;
+      float* qk = qvec(k);
+      const float* qprev = k > 0 ? qvec(k - 1) : nullptr;
       const double inv2eps = form_points(qk, d.eps_default);
       two_passes();
-      if (full) {
-        fd_w<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
-        const int nb = reorth_nblocks(n);
-        // CGS pass 1 over q_1..q_k (its coefficient on q_k is alpha_k)
-        reorth_dots(L, basis, n, k + 1, w, n, partials);
-        finish_reduce(nb, k + 1, d_coef);
-        SLQ_CUDA(cudaMemcpyAsync(d_alpha + k, d_coef + k, sizeof(double), cudaMemcpyDeviceToDevice, L.stream));
-        // update of pass 1 fused with the partial dots of CGS pass 2
-        reorth_update(L, basis, n, k + 1, d_coef, w, n, partials, nullptr);
-        finish_reduce(nb, k + 1, d_coef);
-        // update of pass 2 fused with ||w||^2
-        reorth_update(L, basis, n, k + 1, d_coef, w, n, nullptr, partials);
-        finish_reduce(nb, 1, dscal + 0);
-      }
+      fd_w<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
+      const int cnt = window ? std::min(k + 1, r) : k + 1;
+      if (b16)
+        cgs2<__nv_bfloat16>(basis16, cnt, slot(k), d_coef, d_alpha + k);
+      else
+        cgs2<float>(basis, cnt, slot(k), d_coef, d_alpha + k);
       double h[2];
       to_host(d_alpha + k, 1, &h[0]);
       to_host(dscal + 0, 1, &h[1]);
@@ -570,7 +599,10 @@ struct EngineT : Engine {
         break;
       }
       if (k + 1 < m) {
-        scale_by_inv_sqrt(L, w, dscal + 0, qrow(k + 1), n);
+        if (b16)
+          store_bf16(L, w, dscal + 0, 0.0, basis16 + (int64_t)slot(k + 1) * n, qf[(k + 1) % 2], n);
+        else
+          scale_by_inv_sqrt(L, w, dscal + 0, qvec(k + 1), n);
         SLQ_CUDA(cudaMemcpyAsync(d_beta, &bnext, sizeof(double), cudaMemcpyHostToDevice, L.stream));
         SLQ_CUDA(cudaStreamSynchronize(L.stream));
       }

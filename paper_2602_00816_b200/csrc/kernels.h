@@ -2,6 +2,7 @@
 // per-class profiler.  T is the pass arithmetic type (double for SLQ_PASS_FP64, float for FP32).
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -163,11 +164,16 @@ void axpy_dev(const Launch& L, float* w, const float* q, const double* coef, dou
               double* sumsq_partials_out);
 void scale_by_inv_sqrt(const Launch& L, const float* w, const double* sumsq, float* q_next, int64_t n);
 int reorth_nblocks(int64_t n);
-void reorth_dots(const Launch& L, const float* Q, int64_t ldq, int k, const float* w, int64_t n,
-                 double* partials);
+// Q: the stored Lanczos basis, fp32 or bf16 rows (B = float | __nv_bfloat16)
+template <class B>
+void reorth_dots(const Launch& L, const B* Q, int64_t ldq, int k, const float* w, int64_t n, double* partials);
 // w -= Q[0:k]^T c; optionally the next pass's partial dots (part_dots [nb x k]) and/or ||w||^2 (part_norm [nb])
-void reorth_update(const Launch& L, const float* Q, int64_t ldq, int k, const double* c, float* w,
+template <class B>
+void reorth_update(const Launch& L, const B* Q, int64_t ldq, int k, const double* c, float* w,
                    int64_t n, double* part_dots, double* part_norm);
+// bf16 basis row + exact fp32 working copy: q = bf16(x / sqrt(*sumsq)), or bf16(x * mul) if sumsq == null
+void store_bf16(const Launch& L, const float* x, const double* sumsq, double mul, __nv_bfloat16* row, float* qf,
+                int64_t n);
 void nonfinite_check(const Launch& L, const float* x, int64_t n, int* flag);
 void dot_partials(const Launch& L, const float* a, const float* b, int64_t n, double* partials);  // [vec_nblocks(n)]
 void axpby(const Launch& L, float* y, const float* x, double a, double b, int64_t n);             // y = a x + b y

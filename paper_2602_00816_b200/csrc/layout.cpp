@@ -14,7 +14,12 @@ void validate_desc(const slq_model_desc& d) {
   SLQ_CHECK_ARG(d.arch == SLQ_ARCH_MLP || d.arch == SLQ_ARCH_GPT || d.arch == SLQ_ARCH_LLAMA, "arch");
   SLQ_CHECK_ARG(d.pass_numerics >= SLQ_PASS_FP64 && d.pass_numerics <= SLQ_PASS_PAIRED_FP32, "pass_numerics");
   SLQ_CHECK_ARG(d.param_dtype == SLQ_PARAM_FP32 || d.param_dtype == SLQ_PARAM_BF16, "param_dtype");
-  SLQ_CHECK_ARG(d.reorth == SLQ_REORTH_NONE || d.reorth == SLQ_REORTH_FULL, "reorth");
+  SLQ_CHECK_ARG(d.reorth == SLQ_REORTH_NONE || d.reorth == SLQ_REORTH_FULL || d.reorth == SLQ_REORTH_WINDOW,
+                "reorth");
+  SLQ_CHECK_ARG(d.reorth != SLQ_REORTH_WINDOW || d.reorth_window >= 2, "reorth_window >= 2 for SLQ_REORTH_WINDOW");
+  SLQ_CHECK_ARG(d.basis_dtype == SLQ_BASIS_FP32 || d.basis_dtype == SLQ_BASIS_BF16, "basis_dtype");
+  SLQ_CHECK_ARG(d.basis_dtype == SLQ_BASIS_FP32 || d.reorth != SLQ_REORTH_NONE,
+                "a bf16 basis needs reorth FULL or WINDOW (NONE keeps no basis)");
   SLQ_CHECK_ARG(d.perturb == SLQ_PERTURB_EXACT || d.perturb == SLQ_PERTURB_STORAGE, "perturb");
   SLQ_CHECK_ARG(d.max_steps >= 1 && d.max_steps <= 4096, "max_steps in [1, 4096]");
   SLQ_CHECK_ARG(d.eps_default > 0, "eps_default > 0");

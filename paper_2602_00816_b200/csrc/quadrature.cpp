@@ -81,4 +81,33 @@ void tridiag_gauss(const double* alpha, const double* beta, int m, double* nodes
   }
 }
 
+// Ghost clusters (R18): single linkage on the ascending Ritz values.
+void ghost_clusters(const double* nodes, int m, double tol, int32_t* cluster_id, int32_t* n_ghost, double* max_split) {
+  SLQ_CHECK_ARG(m >= 1 && nodes, "nodes[m], m >= 1");
+  SLQ_CHECK_ARG(tol >= 0 && std::isfinite(tol), "tol >= 0");
+  for (int i = 0; i < m; ++i) {
+    SLQ_CHECK_ARG(std::isfinite(nodes[i]), "finite nodes");
+    SLQ_CHECK_ARG(i == 0 || nodes[i] >= nodes[i - 1], "nodes ascending");
+  }
+  int id = 0, start = 0, ghosts = 0;
+  double split = 0.0;
+  auto close_cluster = [&](int end) {  // members [start, end)
+    if (end - start >= 2) {
+      ++ghosts;
+      split = std::max(split, nodes[end - 1] - nodes[start]);
+    }
+  };
+  for (int i = 0; i < m; ++i) {
+    if (i > 0 && nodes[i] - nodes[i - 1] > tol) {
+      close_cluster(i);
+      ++id;
+      start = i;
+    }
+    if (cluster_id) cluster_id[i] = id;
+  }
+  close_cluster(m);
+  if (n_ghost) *n_ghost = ghosts;
+  if (max_split) *max_split = split;
+}
+
 }  // namespace slq

@@ -4,6 +4,7 @@
 // (partials in fp64, finalised in a fixed order), and the CGS reorthogonalisation GEMVs.
 // All are HBM-bound streaming kernels: one pass, vectorised where aligned, grids sized in
 // multiples of the 148 SMs.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -239,23 +240,34 @@ constexpr int kReorthChunk = 4096;
 constexpr int kRThreads = 256;
 constexpr int kRGroups = kReorthChunk / 4 / kRThreads;  // float4 groups per thread in the update
 
+// 4 consecutive basis elements as float4 (the basis is stored fp32 or bf16)
+__device__ __forceinline__ float4 ld_q4(const float* p, int i4) { return reinterpret_cast<const float4*>(p)[i4]; }
+__device__ __forceinline__ float4 ld_q4(const __nv_bfloat16* p, int i4) {
+  const uint2 u = reinterpret_cast<const uint2*>(p)[i4];
+  const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+  const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+  const float2 a = __bfloat1622float2(lo), b = __bfloat1622float2(hi);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
 // partial dots of the shared-memory chunk ws[0, len) with rows 0..k-1 of Q (one warp per row)
-__device__ __forceinline__ void chunk_dots(const float* __restrict__ Q, int64_t ldq, int k, int64_t base, int len,
+template <class B>
+__device__ __forceinline__ void chunk_dots(const B* __restrict__ Q, int64_t ldq, int k, int64_t base, int len,
                                            const float* ws, double* __restrict__ part_row) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int n4 = len / 4;
   const float4* w4 = reinterpret_cast<const float4*>(ws);
   for (int j = warp; j < k; j += nw) {
-    const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + base);
+    const B* q = Q + (int64_t)j * ldq + base;
     double s0 = 0.0, s1 = 0.0;
     int i = lane;
     for (; i + 32 < n4; i += 64) {
-      const float4 a = q4[i], b = q4[i + 32], x = w4[i], y = w4[i + 32];
+      const float4 a = ld_q4(q, i), b = ld_q4(q, i + 32), x = w4[i], y = w4[i + 32];
       s0 += (double)a.x * x.x + (double)a.y * x.y + (double)a.z * x.z + (double)a.w * x.w;
       s1 += (double)b.x * y.x + (double)b.y * y.y + (double)b.z * y.z + (double)b.w * y.w;
     }
     for (; i < n4; i += 32) {
-      const float4 a = q4[i], x = w4[i];
+      const float4 a = ld_q4(q, i), x = w4[i];
       s0 += (double)a.x * x.x + (double)a.y * x.y + (double)a.z * x.z + (double)a.w * x.w;
     }
     const double s = warp_sum_d(s0 + s1);
@@ -264,7 +276,8 @@ __device__ __forceinline__ void chunk_dots(const float* __restrict__ Q, int64_t 
 }
 
 // partial c_j = Q[j, chunk] . w[chunk] for all j < k
-__global__ void __launch_bounds__(kRThreads) k_reorth_dots(const float* __restrict__ Q, int64_t ldq, int k,
+template <class B>
+__global__ void __launch_bounds__(kRThreads) k_reorth_dots(const B* __restrict__ Q, int64_t ldq, int k,
                                                            const float* __restrict__ w, int64_t n,
                                                            double* __restrict__ part) {
   __shared__ __align__(16) float ws[kReorthChunk];
@@ -279,7 +292,8 @@ __global__ void __launch_bounds__(kRThreads) k_reorth_dots(const float* __restri
 // w[chunk] -= sum_j c_j Q[j, chunk]; then optionally the next CGS pass's partial dots of the
 // updated chunk (the Q chunk was just streamed, so the re-read mostly hits L2) and/or the
 // partial ||w||^2
-__global__ void __launch_bounds__(kRThreads) k_reorth_update(const float* __restrict__ Q, int64_t ldq, int k,
+template <class B>
+__global__ void __launch_bounds__(kRThreads) k_reorth_update(const B* __restrict__ Q, int64_t ldq, int k,
                                                              const double* __restrict__ c, float* __restrict__ w,
                                                              int64_t n, double* __restrict__ part_dots,
                                                              double* __restrict__ part_norm) {
@@ -295,12 +309,12 @@ __global__ void __launch_bounds__(kRThreads) k_reorth_update(const float* __rest
   for (int gi = 0; gi < kRGroups; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.0;
   for (int j = 0; j < k; ++j) {
     const double cj = cs[j];
-    const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + base);
+    const B* qrow = Q + (int64_t)j * ldq + base;
 #pragma unroll
     for (int gi = 0; gi < kRGroups; ++gi) {
       const int i4 = threadIdx.x + gi * kRThreads;
       if (i4 < n4) {
-        const float4 q = q4[i4];
+        const float4 q = ld_q4(qrow, i4);
         acc[gi][0] += cj * q.x; acc[gi][1] += cj * q.y; acc[gi][2] += cj * q.z; acc[gi][3] += cj * q.w;
       }
     }
@@ -329,6 +343,19 @@ __global__ void __launch_bounds__(kRThreads) k_reorth_update(const float* __rest
   if (part_dots) {
     __syncthreads();
     chunk_dots(Q, ldq, k, base, len, ws, part_dots + (int64_t)blockIdx.x * k);
+  }
+}
+
+// bf16 basis store (R19): q = bf16_RNE(x / sqrt(*sumsq)) (or x * mul when sumsq is
+// null: the probe), rounded once from fp64; the fp32 working copy holds the stored value exactly
+__global__ void k_store_bf16(const float* __restrict__ x, const double* __restrict__ sumsq, double mul,
+                             __nv_bfloat16* __restrict__ row, float* __restrict__ qf, int64_t n) {
+  const double beta = sumsq ? sqrt(*sumsq) : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = sumsq ? (double)x[i] / beta : (double)x[i] * mul;
+    const __nv_bfloat16 r = __double2bfloat16(v);
+    row[i] = r;
+    qf[i] = __bfloat162float(r);
   }
 }
 
@@ -478,18 +505,33 @@ void scale_by_inv_sqrt(const Launch& L, const float* w, const double* sumsq, flo
 
 int reorth_nblocks(int64_t n) { return (int)std::max<int64_t>(1, ceil_div(n, kReorthChunk)); }
 
-void reorth_dots(const Launch& L, const float* Q, int64_t ldq, int k, const float* w, int64_t n, double* part) {
+template <class B>
+void reorth_dots(const Launch& L, const B* Q, int64_t ldq, int k, const float* w, int64_t n, double* part) {
   SLQ_CHECK_ARG(n % 4 == 0 && ldq % 4 == 0, "reorth needs float4-aligned shards");
-  VLAUNCH(KC_REORTH, 2.0 * k * n, 4.0 * (k + 1.0) * n, reorth_nblocks(n), kRThreads, 0, k_reorth_dots, Q, ldq, k,
-          w, n, part);
+  VLAUNCH(KC_REORTH, 2.0 * k * n, (sizeof(B) * (double)k + 4.0) * n, reorth_nblocks(n), kRThreads, 0,
+          k_reorth_dots<B>, Q, ldq, k, w, n, part);
 }
 
-void reorth_update(const Launch& L, const float* Q, int64_t ldq, int k, const double* c, float* w, int64_t n,
+template <class B>
+void reorth_update(const Launch& L, const B* Q, int64_t ldq, int k, const double* c, float* w, int64_t n,
                    double* part_dots, double* part_norm) {
   SLQ_CHECK_ARG(n % 4 == 0 && ldq % 4 == 0, "reorth needs float4-aligned shards");
   // algorithmic bytes: Q once from HBM (the fused dots re-read is the L2-resident chunk) + w r/w
-  VLAUNCH(KC_REORTH, (part_dots ? 4.0 : 2.0) * k * n, 4.0 * (k + 2.0) * n, reorth_nblocks(n), kRThreads,
-          sizeof(double) * k, k_reorth_update, Q, ldq, k, c, w, n, part_dots, part_norm);
+  VLAUNCH(KC_REORTH, (part_dots ? 4.0 : 2.0) * k * n, (sizeof(B) * (double)k + 8.0) * n, reorth_nblocks(n),
+          kRThreads, sizeof(double) * k, k_reorth_update<B>, Q, ldq, k, c, w, n, part_dots, part_norm);
+}
+
+template void reorth_dots<float>(const Launch&, const float*, int64_t, int, const float*, int64_t, double*);
+template void reorth_dots<__nv_bfloat16>(const Launch&, const __nv_bfloat16*, int64_t, int, const float*, int64_t,
+                                         double*);
+template void reorth_update<float>(const Launch&, const float*, int64_t, int, const double*, float*, int64_t,
+                                   double*, double*);
+template void reorth_update<__nv_bfloat16>(const Launch&, const __nv_bfloat16*, int64_t, int, const double*, float*,
+                                           int64_t, double*, double*);
+
+void store_bf16(const Launch& L, const float* x, const double* sumsq, double mul, __nv_bfloat16* row, float* qf,
+                int64_t n) {
+  VLAUNCH(KC_VEC, 1.0 * n, 10.0 * n, vec_nblocks(n), kThreads, 0, k_store_bf16, x, sumsq, mul, row, qf, n);
 }
 
 void dot_partials(const Launch& L, const float* a, const float* b, int64_t n, double* part) {

@@ -12,7 +12,8 @@ LIB_PATH = os.path.join(_HERE, "libslq.so")
 
 SLQ_OK, SLQ_EINVAL, SLQ_ENUMERIC, SLQ_ECUDA, SLQ_ENCCL, SLQ_ETIMEOUT, SLQ_ENOMEM, SLQ_EUNSUPPORTED = 0, 2, 3, 4, 5, 6, 7, 8
 PASS = {"fp64": 0, "fp32": 1, "bf16x3": 2, "paired": 3, "paired_fp32": 4}
-REORTH = {"none": 0, "full": 1}
+REORTH = {"none": 0, "full": 1, "window": 2}
+BASIS = {"fp32": 0, "bf16": 1}
 PERTURB = {"exact": 0, "storage": 1}
 
 
@@ -31,7 +32,8 @@ class ModelDescC(ctypes.Structure):
                 ("norm_eps", ctypes.c_double), ("param_dtype", ctypes.c_int32),
                 ("pass_numerics", ctypes.c_int32), ("reorth", ctypes.c_int32),
                 ("max_steps", ctypes.c_int32), ("eps_default", ctypes.c_double),
-                ("perturb", ctypes.c_int32)]
+                ("perturb", ctypes.c_int32), ("reorth_window", ctypes.c_int32),
+                ("basis_dtype", ctypes.c_int32)]
 
 
 class BatchC(ctypes.Structure):
@@ -73,6 +75,7 @@ def lib() -> ctypes.CDLL:
         "slq_lanczos": (I32, [P, U64, I32, P, P]),
         "slq_lanczos_info": (I32, [P, P, P, P]),
         "slq_quadrature": (I32, [P, P, I32, P, P]),
+        "slq_ghost_clusters": (I32, [P, I32, D, P, P, P]),
         "slq_probe": (I32, [P, U64, P]),
         "slq_profile": (I32, [P, I32, I32]),
         "slq_num_kernel_classes": (I32, []),
@@ -102,7 +105,8 @@ def _check(st: int, ctx=None) -> None:
 
 
 def make_desc(cfg, pass_numerics: str = "fp64", reorth: Optional[str] = None, max_steps: Optional[int] = None,
-              eps: Optional[float] = None, perturb: str = "exact") -> ModelDescC:
+              eps: Optional[float] = None, perturb: str = "exact", window: int = 0,
+              basis: str = "fp32") -> ModelDescC:
     """slq_model_desc from a slq_inputs.ModelDesc-like object."""
     d = ModelDescC()
     d.arch = cfg.arch
@@ -118,6 +122,8 @@ def make_desc(cfg, pass_numerics: str = "fp64", reorth: Optional[str] = None, ma
     d.max_steps = int(max_steps if max_steps is not None else cfg.m)
     d.eps_default = float(eps if eps is not None else cfg.eps)
     d.perturb = PERTURB[perturb]
+    d.reorth_window = int(window)
+    d.basis_dtype = BASIS[basis]
     return d
 
 
@@ -187,6 +193,16 @@ def quadrature(alpha, beta) -> Tuple[np.ndarray, np.ndarray]:
     return nodes, w
 
 
+def ghost_clusters(nodes, tol: float) -> Tuple[np.ndarray, int, float]:
+    """(cluster id per node, number of duplicate clusters, largest splitting) -- slq_ghost_clusters."""
+    x = np.ascontiguousarray(nodes, dtype=np.float64)
+    ids = np.empty(x.size, dtype=np.int32)
+    ng, ms = ctypes.c_int32(), ctypes.c_double()
+    _check(lib().slq_ghost_clusters(x.ctypes.data, x.size, float(tol), ids.ctypes.data, ctypes.byref(ng),
+                                    ctypes.byref(ms)))
+    return ids, ng.value, ms.value
+
+
 def _ptr(x) -> int:
     """Raw pointer of a torch tensor (device or host) or numpy array."""
     if isinstance(x, np.ndarray):
@@ -202,10 +218,10 @@ class SlqContext:
     def __init__(self, cfg, theta0: np.ndarray, batch, *, n_global: Optional[int] = None, rank: int = 0,
                  world_size: int = 1, device: int = 0, stream: Optional[int] = None, unique_id: Optional[bytes] = None,
                  pass_numerics: str = "fp64", reorth: Optional[str] = None, max_steps: Optional[int] = None,
-                 eps: Optional[float] = None, perturb: str = "exact"):
+                 eps: Optional[float] = None, perturb: str = "exact", window: int = 0, basis: str = "fp32"):
         L = lib()
         self._keep = []
-        self.desc = make_desc(cfg, pass_numerics, reorth, max_steps, eps, perturb)
+        self.desc = make_desc(cfg, pass_numerics, reorth, max_steps, eps, perturb, window, basis)
         th = np.ascontiguousarray(theta0, dtype=np.float32)
         b = BatchC()
         b.params_host = th.ctypes.data

@@ -117,3 +117,43 @@ def test_init_without_gpu_fails_loudly():
     with pytest.raises(slq.SlqError) as e:
         slq.SlqContext(cfg, si.init_params(cfg), si.mlp_data(cfg))
     assert e.value.status == slq.SLQ_ECUDA
+
+
+def test_ghost_clusters_host_matches_oracle():
+    """slq_ghost_clusters (host, R18) vs the oracle's definition on random node sets
+    with planted duplicates, plus the tol = 0 and error cases."""
+    from oracle import lanczos as OL
+    rng = np.random.default_rng(3)
+    for trial in range(50):
+        x = np.sort(np.concatenate([rng.uniform(-5, 5, 30), np.repeat(rng.uniform(-5, 5, 3), 3) +
+                                    rng.uniform(-1e-7, 1e-7, 9)]))
+        for tol in (0.0, 1e-6, 1e-3, 0.3):
+            ids, ng, ms = slq.ghost_clusters(x, tol)
+            rid, rg = OL.ghost_clusters(x, tol)
+            assert np.array_equal(ids, rid)
+            assert ng == len(rg)
+            assert ms == (max(s for _, _, s in rg) if rg else 0.0)
+    ids, ng, ms = slq.ghost_clusters([1.0, 2.0, 3.0], 0.0)
+    assert ids.tolist() == [0, 1, 2] and ng == 0 and ms == 0.0
+    ids, ng, ms = slq.ghost_clusters([1.0, 1.0, 3.0], 0.0)
+    assert ids.tolist() == [0, 0, 1] and ng == 1 and ms == 0.0
+    for bad in (([2.0, 1.0], 0.1), ([1.0, float("nan")], 0.1), ([1.0, 2.0], -1.0)):
+        with pytest.raises(slq.SlqError) as e:
+            slq.ghost_clusters(*bad)
+        assert e.value.status == slq.SLQ_EINVAL
+
+
+def test_descriptor_validation_window_and_basis():
+    """reorth WINDOW needs r >= 2; a bf16 basis needs a stored basis (host layout planner
+    validates the descriptor without a GPU)."""
+    cfg = si.CONFIGS["gpt_tiny"]
+    for kw, ok in ((dict(reorth="window", window=1), False), (dict(reorth="window", window=4), True),
+                   (dict(reorth="none", basis="bf16"), False), (dict(reorth="full", basis="bf16"), True),
+                   (dict(reorth="window", window=3, basis="bf16"), True)):
+        d = slq.make_desc(cfg, **kw)
+        if ok:
+            slq.plan_layout(d, 1)
+        else:
+            with pytest.raises(slq.SlqError) as e:
+                slq.plan_layout(d, 1)
+            assert e.value.status == slq.SLQ_EINVAL
