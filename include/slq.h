@@ -56,7 +56,13 @@ enum { SLQ_ARCH_MLP = 0, SLQ_ARCH_GPT = 1, SLQ_ARCH_LLAMA = 2 };
  * passes on SIMT GEMMs (reported only); BF16X3: fp32 activations, every non-batched GEMM on the
  * tcgen05 tensor cores with operands split into three bf16 terms (fp32-faithful; the mode for the
  * bf16 models' gates). */
-enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2, SLQ_PASS_PAIRED = 3, SLQ_PASS_PAIRED_FP32 = 4 };
+enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2, SLQ_PASS_PAIRED = 3, SLQ_PASS_PAIRED_FP32 = 4,
+       SLQ_PASS_FP64_OZ = 5 };
+/* SLQ_PASS_FP64_OZ: as FP64 (fp64 activations and nonlinearities), but every dense non-batched
+ * GEMM runs on the tcgen05 INT8 tensor cores as exact digit products (Ozaki scheme: each operand
+ * row/column scaled by a power of two and cut into S = 6 signed 7-bit digit planes; the
+ * S(S+1)/2 leading products accumulate exactly in INT32 TMEM; error <~ 8 * 2^-42 K max|a| max|b|).
+ * The batched causal attention GEMMs stay on the FP64 DMMA path. */
 /* SLQ_PASS_PAIRED: the two gradient evaluations of Eq. (1) carried as (mean, half-difference)
  * pairs through ONE pass, so (g+ - g-) is never formed by subtracting rounded gradients
  * (SURVEY.md §8(f1)); non-batched pair GEMMs on tcgen05 (fp32-faithful three-term bf16 splits),
@@ -213,6 +219,11 @@ void* slq_stream(const slq_ctx* ctx);
 /* Diagnostic, not on the hot path: measured FP64 FMA throughput of `device` in TFLOP/s (the
  * roofline denominator of the fp64 gradient-pass GEMMs, which MEASURED_PEAKS.json lacks). */
 slq_status slq_diag_fp64_peak(int32_t device, double* tflops);
+/* Diagnostic: the int8 Ozaki fp64 GEMM (S digit planes) against the DMMA fp64 GEMM on random data
+ * (ragged shapes allowed): *max_err = max |C_oz - C_dmma| / (K max_k|A_ik| max_k|B_kj|) over all
+ * (i, j); *tflops = fp64-equivalent rate of the Ozaki GEMM (2 M N K / time, slicing included). */
+slq_status slq_diag_oz_check(int32_t device, int32_t M, int32_t N, int32_t K, int32_t a_kmajor, int32_t b_kmajor,
+                             int32_t S, int32_t iters, double* max_err, double* tflops);
 /* Diagnostic: measured FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) throughput in TFLOP/s. */
 slq_status slq_diag_dmma_peak(int32_t device, double* tflops);
 /* Diagnostic: time the library's fp64 GEMM on one shape.  A [M x K] (K-contiguous if a_kmajor,

@@ -617,8 +617,11 @@ struct EngineT : Engine {
 
 std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
                                     const float* theta_host, int rank, Comm* comm, const Launch& L) {
-  if (d.pass_numerics == SLQ_PASS_FP64)
-    return std::unique_ptr<Engine>(new EngineT<double>(d, plan, b, theta_host, rank, comm, L));
+  if (d.pass_numerics == SLQ_PASS_FP64 || d.pass_numerics == SLQ_PASS_FP64_OZ) {
+    Launch Ld = L;
+    Ld.gemm_mode = d.pass_numerics == SLQ_PASS_FP64_OZ ? 2 : 0;
+    return std::unique_ptr<Engine>(new EngineT<double>(d, plan, b, theta_host, rank, comm, Ld));
+  }
   Launch Lf = L;
   Lf.gemm_mode = (d.pass_numerics == SLQ_PASS_BF16X3 || d.pass_numerics == SLQ_PASS_PAIRED) ? 1 : 0;
   return std::unique_ptr<Engine>(new EngineT<float>(d, plan, b, theta_host, rank, comm, Lf));

@@ -303,6 +303,10 @@ template <>
 void gemm<double>(const Launch& L, const GemmArgs<double>& a) {
   check(a);
   if (a.M == 0 || a.N == 0) return;
+  if (L.gemm_mode == 2 && a.batch == 1 && a.tri == TRI_NONE && a.K > 0) {
+    gemm_oz(L, a, oz_slices());
+    return;
+  }
   run(L, a, pick_variant(a), 0);
 }
 
@@ -333,12 +337,17 @@ extern "C" slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, in
     a.A = A; a.sAm = a_kmajor ? K : 1; a.sAk = a_kmajor ? 1 : M;
     a.B = B; a.sBk = b_kmajor ? 1 : N; a.sBn = b_kmajor ? K : 1;
     a.C = C; a.ldc = N;
+    // variant <= -4: the tcgen05 int8 Ozaki path with S = -variant digit planes
     const int v = variant < 0 ? pick_variant(a) : variant;
-    run(L, a, v, splits);  // warm-up (also sets the smem attribute)
+    auto go = [&] {
+      if (variant <= -4) gemm_oz(L, a, -variant);
+      else run(L, a, v, splits);
+    };
+    go();  // warm-up (also sets the smem attribute)
     SLQ_CUDA(cudaEventCreate(&e0));
     SLQ_CUDA(cudaEventCreate(&e1));
     SLQ_CUDA(cudaEventRecord(e0));
-    for (int i = 0; i < iters; ++i) run(L, a, v, splits);
+    for (int i = 0; i < iters; ++i) go();
     SLQ_CUDA(cudaEventRecord(e1));
     SLQ_CUDA(cudaEventSynchronize(e1));
     float ms = 0;

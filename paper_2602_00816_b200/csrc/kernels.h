@@ -25,7 +25,8 @@ struct Launch {
   Profiler* prof;
   Workspace* ws;      // split-K / reduction scratch
   int64_t* launches;  // launch counter
-  int gemm_mode = 0;  // float GEMMs: 0 = SIMT fp32, 1 = tcgen05 bf16x3 split (fp32-faithful)
+  int gemm_mode = 0;  // float GEMMs: 0 = SIMT fp32, 1 = tcgen05 bf16x3 split (fp32-faithful);
+                      // double GEMMs: 0 = DMMA (mma.sync f64), 2 = tcgen05 int8 Ozaki (gemm_oz)
 };
 
 // batch addressing of one operand: offset(z) = (z / div) * outer + ((z % div) / rep) * inner
@@ -71,6 +72,11 @@ struct GemmArgs {
 
 template <class T>
 void gemm(const Launch& L, const GemmArgs<T>& a);
+
+// fp64 GEMM as exact INT8 digit products on the tcgen05 tensor cores (Ozaki scheme, S digit
+// planes of 7 bits per operand; oz_gemm.cu).  batch == 1, dense (tri == TRI_NONE) only.
+void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S);
+int oz_slices();  // S for the pass path: SLQ_OZ_SLICES (4..7), default 6
 
 // fp32-faithful GEMM on the tcgen05 tensor cores: every fp32 operand is split into three bf16
 // terms (x = x0 + x1 + x2, 24 significant bits) and the six products with i + j <= 2 are

@@ -1,0 +1,503 @@
+// fp64 GEMM emulated exactly-accumulated on the tcgen05 INT8 tensor cores (Ozaki scheme, int8
+// slices; pass mode SLQ_PASS_FP64_OZ).
+//
+//   C[M x N] = epilogue( A[M x K] . B[K x N] ),  A, B, C fp64.
+//
+// Every row i of A (every column j of B) is scaled by a power of two 2^e_i with |A_ik| < 2^e_i and
+// cut into S signed 7-bit digits (truncation, exact in fp64):
+//     A_ik = 2^e_i * sum_{p<S} a_p(i,k) 2^{-7(p+1)} + r,   |a_p| <= 127,  |r| < 2^{e_i - 7S}
+// so   A.B ~= 2^{e_i + f_j} sum_{g<S} 2^{-7(g+2)} sum_{p+q=g} (a_p . b_q)
+// Each a_p . b_q is an exact INT8 x INT8 -> INT32 tensor-core product; the products of one digit
+// weight g share one INT32 TMEM accumulator (no rounding anywhere in the contraction; |acc| <=
+// S K 127^2 < 2^31 is enforced by capping K per split).  The only error is the dropped digits,
+// |error| <~ (S + 2) 2^{-7S} K max|A_i.| max|B_.j|; S = 6 keeps the FD-HVP of c2 at ~7e-7 of the
+// fp64 result (measured by emulation).
+//
+// Kernel: BM = 128 x BN = 64 output tile per CTA, K in 64-byte k-tiles (SWIZZLE_64B TMA boxes);
+// one pipeline stage holds all S digit planes of the A and B k-tiles, and the MMA issuer runs the
+// S(S+1)/2 products from them (each plane is read from L2 once per k-tile, not once per product).
+// Warp-specialised: warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA issuer, warps
+// 2..5 epilogue (TMEM -> fp64 combine -> shared tile -> fused epilogue with coalesced stores).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.h"
+#include "gemm_common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace slq {
+namespace oz {
+
+using namespace tc;
+
+constexpr int BM = 128, BN = 64, BK = 64, UMMA_K = 32;
+
+template <int S>
+struct Cfg {
+  static constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;  // bytes
+  static constexpr int A_BYTES = S * A_PLANE, B_BYTES = S * B_PLANE;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (3 * STAGE_BYTES + 2048 <= 227 * 1024) ? 3 : 2;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = S * BN <= 128 ? 128 : (S * BN <= 256 ? 256 : 512);
+  static constexpr int NPROD = S * (S + 1) / 2;
+  static_assert(S * BN <= 512, "S accumulators of BN columns must fit TMEM");
+  static_assert(BM * (BN + 1) * 8 <= STAGES * STAGE_BYTES, "fp64 epilogue tile fits the pipeline smem");
+};
+
+// instruction descriptor, kind::i8: D s32, A and B signed 8-bit, both K-major, M x N
+__host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+struct OzArgs {
+  int M, N, nk;          // nk: k-tiles of the whole K
+  int kt_per_split, splits;
+  const int* ea;         // [M] row exponents of A
+  const int* eb;         // [N] column exponents of B
+};
+
+template <int S>
+__global__ void __launch_bounds__(192, 1)
+    k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
+              GemmArgs<double> p, double* __restrict__ ws) {
+  using CF = Cfg<S>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES);
+  uint64_t* empty = full + CF::STAGES;
+  uint64_t* tmem_full = empty + CF::STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int split = blockIdx.z;
+  const int kt0 = split * o.kt_per_split;
+  const int kt1 = min(o.nk, kt0 + o.kt_per_split);
+  const int nloc = kt1 > kt0 ? kt1 - kt0 : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CF::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_holder)),
+                 "n"(CF::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: all S digit planes of A and B for one k-tile per stage ----
+      for (int i = 0; i < nloc; ++i) {
+        const int kt = kt0 + i, s = i % CF::STAGES;
+        const uint32_t ph = (i / CF::STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * CF::STAGE_BYTES;
+        uint8_t* sb = sa + CF::A_BYTES;
+        mbar_expect_tx(&full[s], CF::STAGE_BYTES);
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          tma_load_2d(sa + q * CF::A_PLANE, &tmA, &full[s], kt * BK, q * o.M + m0);
+          tma_load_2d(sb + q * CF::B_PLANE, &tmB, &full[s], kt * BK, q * o.N + n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer: S(S+1)/2 digit products per k-tile ----
+      constexpr uint32_t idesc = make_idesc_i8(BM, BN);
+      uint32_t started = 0;  // bit g: accumulator g has been initialised
+      for (int i = 0; i < nloc; ++i) {
+        const int s = i % CF::STAGES;
+        const uint32_t ph = (i / CF::STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
+        const uint32_t sb = sa + CF::A_BYTES;
+#pragma unroll
+        for (int g = 0; g < S; ++g) {
+#pragma unroll
+          for (int pa = 0; pa <= g; ++pa) {
+            const int qb = g - pa;
+#pragma unroll
+            for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+              const uint64_t da = make_desc_sw64(sa + pa * CF::A_PLANE + kk * UMMA_K);
+              const uint64_t db = make_desc_sw64(sb + qb * CF::B_PLANE + kk * UMMA_K);
+              const uint32_t acc = (started >> g) & 1u;
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(g * BN)),
+                  "l"(da), "l"(db), "r"(idesc), "r"(acc));
+              started |= 1u << g;
+            }
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(&empty[s])));
+      }
+      if (nloc > 0) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(tmem_full)));
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_full)));
+      }
+    }
+  } else {
+    // ---- epilogue: combine the S digit-weight accumulators in fp64, stage, store ----
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const int lg = (warp % 4) * 32;
+    constexpr int LDS = BN + 1;
+    double* Cs = reinterpret_cast<double*>(smem);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.0;
+#pragma unroll
+      for (int g = 0; g < S; ++g) {
+        uint32_t r[16];
+        const uint32_t taddr = tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+            "[%16];\n"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+        const double w = ldexp(1.0, -7 * (g + 2));
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += (double)(int32_t)r[i] * w;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) Cs[(lg + lane) * LDS + c + i] = nloc > 0 ? v[i] : 0.0;
+    }
+    asm volatile("bar.sync 1, 128;\n" ::);  // the four epilogue warps only
+    double* W = o.splits > 1 ? ws + (int64_t)split * p.M * p.N : nullptr;
+    const int et = threadIdx.x - 64;
+    const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
+#pragma unroll 1
+    for (int e = et; e < BM * BN; e += 128) {
+      const int rr = e / BN, cc = e % BN;
+      if (rr >= rows || cc >= cols) continue;
+      const double v = ldexp(Cs[rr * LDS + cc], o.ea[m0 + rr] + o.eb[n0 + cc]);
+      if (W)
+        W[(int64_t)(m0 + rr) * p.N + n0 + cc] = v;
+      else
+        gemm_detail::epilogue_store(p, p.C, m0 + rr, n0 + cc, v);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(CF::TMEM_COLS));
+  }
+}
+
+// exponent e with |x| < 2^e for the largest |x| (0 for an all-zero row), and the S digits of x:
+// r = x 2^-e in (-1, 1); d_p = trunc(128 r); r = 128 r - d_p   (all exact in fp64)
+template <int S>
+__device__ __forceinline__ void digits(double x, int e, int8_t* d) {
+  double r = ldexp(x, -e);
+#pragma unroll
+  for (int q = 0; q < S; ++q) {
+    r *= 128.0;
+    const double t = trunc(r);
+    d[q] = (int8_t)(int)t;
+    r -= t;
+  }
+}
+
+__device__ __forceinline__ int exp_of(double mx) {
+  if (!(mx > 0.0)) return 0;
+  int e;
+  frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)  ->  mx < 2^e
+  return e;
+}
+
+// K-contiguous operand X[row * ld + k] -> planes out[q][row][Kp], exponents ex[row]; warp per row
+template <int S>
+__global__ void k_oz_slice_rows(const double* __restrict__ X, int64_t ld, int rows, int K, int Kp,
+                                int8_t* __restrict__ out, int* __restrict__ ex) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const double* xr = X + (int64_t)row * ld;
+  double mx = 0.0;
+  for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(xr[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int e = exp_of(mx);
+  if (lane == 0) ex[row] = e;
+  const int64_t plane = (int64_t)rows * Kp;
+  for (int k4 = lane * 4; k4 < Kp; k4 += 128) {
+    int8_t d[4][S];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double x = (k4 + j < K) ? xr[k4 + j] : 0.0;
+      digits<S>(x, e, d[j]);
+    }
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      const uint32_t w = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
+                         ((uint32_t)(uint8_t)d[2][q] << 16) | ((uint32_t)(uint8_t)d[3][q] << 24);
+      *reinterpret_cast<uint32_t*>(out + q * plane + (int64_t)row * Kp + k4) = w;
+    }
+  }
+}
+
+// operand stored transposed: element (row r, k) at X[k * ld + r] (r contiguous).  Block of 256
+// threads per 32 rows: column max over K, then 32 x 32 tiles transposed through shared memory.
+template <int S>
+__global__ void __launch_bounds__(256) k_oz_slice_cols(const double* __restrict__ X, int64_t ld, int rows, int K,
+                                                      int Kp, int8_t* __restrict__ out, int* __restrict__ ex) {
+  __shared__ double tile[32][33];
+  __shared__ double red[8][33];
+  __shared__ int es[32];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int r0 = blockIdx.x * 32;
+  const int r = r0 + tx;
+  double mx = 0.0;
+  if (r < rows)
+    for (int k = ty; k < K; k += 8) mx = fmax(mx, fabs(X[(int64_t)k * ld + r]));
+  red[ty][tx] = mx;
+  __syncthreads();
+  if (ty == 0) {
+    double m = red[0][tx];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) m = fmax(m, red[i][tx]);
+    const int e = exp_of(m);
+    es[tx] = e;
+    if (r < rows) ex[r] = e;
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)rows * Kp;
+  const int wr = threadIdx.x / 8, kq = threadIdx.x % 8;  // writer: row r0 + wr, k = 4 kq .. 4 kq + 3
+  for (int k0 = 0; k0 < Kp; k0 += 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = k0 + ty + 8 * i;
+      tile[ty + 8 * i][tx] = (r < rows && k < K) ? X[(int64_t)k * ld + r] : 0.0;
+    }
+    __syncthreads();
+    if (r0 + wr < rows && k0 + 4 * kq < Kp) {
+      int8_t d[4][S];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) digits<S>(tile[4 * kq + j][wr], es[wr], d[j]);
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint32_t w = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
+                           ((uint32_t)(uint8_t)d[2][q] << 16) | ((uint32_t)(uint8_t)d[3][q] << 24);
+        *reinterpret_cast<uint32_t*>(out + q * plane + (int64_t)(r0 + wr) * Kp + k0 + 4 * kq) = w;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// 2-D int8 tensor [rows x cols] (row pitch ld bytes), box {64, box_rows}, 64-byte swizzle
+static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(SLQ_ECUDA, "cuTensorMapEncodeTiled (int8) failed: " + std::to_string((int)r));
+  return m;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+template <int S>
+void slice(const Launch& L, const double* X, bool kmajor, int64_t ld, int rows, int K, int Kp, int8_t* out, int* ex) {
+  if (kmajor) {
+    k_oz_slice_rows<S><<<(unsigned)ceil_div((int64_t)rows * 32, 256), 256, 0, L.stream>>>(X, ld, rows, K, Kp, out, ex);
+  } else {
+    k_oz_slice_cols<S><<<(unsigned)ceil_div(rows, 32), 256, 0, L.stream>>>(X, ld, rows, K, Kp, out, ex);
+  }
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+}
+
+template <int S>
+void run(const Launch& L, const GemmArgs<double>& a) {
+  using CF = Cfg<S>;
+  static bool attr = false;
+  if (!attr) {
+    SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    attr = true;
+  }
+  const int M = a.M, N = a.N, K = a.K;
+  const int Kp = (int)ceil_div(K, 16) * 16;
+  const int nk = (int)ceil_div(K, BK);
+  // split-K: one CTA per SM (the stage ring fills the shared memory), so fill the 148 SMs with
+  // tiles x splits <= 148; every split's K range keeps |acc| <= S * Ksplit * 127^2 < 2^31
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
+  const int kt_cap = (int)std::max<int64_t>(1, ((int64_t)2147483647 / ((int64_t)S * 127 * 127)) / BK);
+  int splits = tiles < 148 ? std::max(1, std::min(148 / tiles, nk / 2)) : 1;
+  splits = std::max<int>(splits, (int)ceil_div(nk, kt_cap));
+  const int ktps = (int)ceil_div(nk, splits);
+  splits = (int)ceil_div(nk, ktps);
+  const size_t a_bytes = align256((size_t)S * M * Kp), b_bytes = align256((size_t)S * N * Kp);
+  const size_t e_bytes = align256(4 * (size_t)(M + N));
+  const size_t w_bytes = splits > 1 ? align256(8 * (size_t)M * N * splits) : 0;
+  uint8_t* base = (uint8_t*)L.ws->get(a_bytes + b_bytes + e_bytes + w_bytes, L.stream);
+  int8_t* as = (int8_t*)base;
+  int8_t* bs = (int8_t*)(base + a_bytes);
+  int* ea = (int*)(base + a_bytes + b_bytes);
+  int* eb = ea + M;
+  double* ws = splits > 1 ? (double*)(base + a_bytes + b_bytes + e_bytes) : nullptr;
+  {
+    LaunchScope scope(L.prof, KC_ELEM, L.stream, 0, (8.0 + S) * ((double)M * K + (double)N * K));
+    // A(m, k): K-contiguous when sAk == 1 (rows = M, pitch sAm), else stored [K x M] with pitch sAk
+    slice<S>(L, a.A, a.sAk == 1, a.sAk == 1 ? a.sAm : a.sAk, M, K, Kp, as, ea);
+    // B(k, n) = B[k * sBk + n * sBn]: K-contiguous rows per n when sBk == 1 (pitch sBn)
+    slice<S>(L, a.B, a.sBk == 1, a.sBk == 1 ? a.sBn : a.sBk, N, K, Kp, bs, eb);
+  }
+  const CUtensorMap ta = make_map_i8(as, (int64_t)S * M, Kp, Kp, BM);
+  const CUtensorMap tb = make_map_i8(bs, (int64_t)S * N, Kp, Kp, BN);
+  OzArgs o{M, N, nk, ktps, splits, ea, eb};
+  {
+    LaunchScope scope(L.prof, KC_GEMM, L.stream, 2.0 * M * N * (double)K * CF::NPROD,
+                      (double)S * ((double)M * K + (double)N * K) + 8.0 * M * N);
+    dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
+    k_oz_gemm<S><<<grid, 192, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+  if (splits > 1) {
+    LaunchScope scope(L.prof, KC_GEMM, L.stream, 0, 8.0 * (double)M * N * (splits + 1));
+    const int64_t mn = (int64_t)M * N;
+    int blocks = (int)std::min<int64_t>(ceil_div(mn, 256), 148 * 8);
+    gemm_detail::splitk_reduce<double><<<blocks, 256, 0, L.stream>>>(a, splits, ws);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+}
+
+}  // namespace oz
+
+int oz_slices() {
+  static int s = [] {
+    const char* e = getenv("SLQ_OZ_SLICES");
+    const int v = e ? atoi(e) : 6;
+    return (v >= 4 && v <= 7) ? v : 6;
+  }();
+  return s;
+}
+
+void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
+  SLQ_CHECK_ARG(a.batch == 1 && a.tri == TRI_NONE && a.M > 0 && a.N > 0 && a.K > 0, "oz gemm: batch 1, dense");
+  switch (S) {
+    case 4: oz::run<4>(L, a); break;
+    case 5: oz::run<5>(L, a); break;
+    case 6: oz::run<6>(L, a); break;
+    default: oz::run<7>(L, a); break;
+  }
+}
+
+}  // namespace slq
+
+namespace slq {
+namespace oz {
+__global__ void k_fill_f64(double* x, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    // wide dynamic range: mantissa in [-1, 1) times 2^(-8 .. 7)
+    const double m = (double)(int64_t)(z >> 11) / 4503599627370496.0 - 1.0;
+    x[i] = ldexp(m, (int)((z >> 3) & 15) - 8);
+  }
+}
+}  // namespace oz
+}  // namespace slq
+
+extern "C" slq_status slq_diag_oz_check(int32_t device, int32_t M, int32_t N, int32_t K, int32_t a_kmajor,
+                                        int32_t b_kmajor, int32_t S, int32_t iters, double* max_err,
+                                        double* tflops) {
+  using namespace slq;
+  double *A = nullptr, *B = nullptr, *C1 = nullptr, *C2 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  auto cleanup = [&] {
+    if (A) cudaFree(A);
+    if (B) cudaFree(B);
+    if (C1) cudaFree(C1);
+    if (C2) cudaFree(C2);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  };
+  try {
+    SLQ_CHECK_ARG(M > 0 && N > 0 && K > 0 && S >= 4 && S <= 7 && iters >= 1 && max_err && tflops, "arguments");
+    SLQ_CUDA(cudaSetDevice(device));
+    SLQ_CUDA(cudaMalloc(&A, sizeof(double) * (size_t)M * K));
+    SLQ_CUDA(cudaMalloc(&B, sizeof(double) * (size_t)N * K));
+    SLQ_CUDA(cudaMalloc(&C1, sizeof(double) * (size_t)M * N));
+    SLQ_CUDA(cudaMalloc(&C2, sizeof(double) * (size_t)M * N));
+    oz::k_fill_f64<<<1024, 256>>>(A, (int64_t)M * K, 11);
+    oz::k_fill_f64<<<1024, 256>>>(B, (int64_t)N * K, 12);
+    Workspace ws;
+    int64_t launches = 0;
+    Launch L{0, nullptr, &ws, &launches};
+    GemmArgs<double> a;
+    a.M = M; a.N = N; a.K = K;
+    a.A = A; a.sAm = a_kmajor ? K : 1; a.sAk = a_kmajor ? 1 : M;
+    a.B = B; a.sBk = b_kmajor ? 1 : N; a.sBn = b_kmajor ? K : 1;
+    a.ldc = N;
+    a.C = C1;
+    gemm<double>(L, a);  // DMMA reference (gemm_mode 0)
+    a.C = C2;
+    gemm_oz(L, a, S);
+    SLQ_CUDA(cudaDeviceSynchronize());
+    SLQ_CUDA(cudaEventCreate(&e0));
+    SLQ_CUDA(cudaEventCreate(&e1));
+    SLQ_CUDA(cudaEventRecord(e0));
+    for (int i = 0; i < iters; ++i) gemm_oz(L, a, S);
+    SLQ_CUDA(cudaEventRecord(e1));
+    SLQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    SLQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *tflops = 2.0 * M * N * (double)K * iters / (ms * 1e-3) / 1e12;
+    std::vector<double> hA((size_t)M * K), hB((size_t)N * K), h1((size_t)M * N), h2((size_t)M * N);
+    SLQ_CUDA(cudaMemcpy(hA.data(), A, sizeof(double) * hA.size(), cudaMemcpyDeviceToHost));
+    SLQ_CUDA(cudaMemcpy(hB.data(), B, sizeof(double) * hB.size(), cudaMemcpyDeviceToHost));
+    SLQ_CUDA(cudaMemcpy(h1.data(), C1, sizeof(double) * h1.size(), cudaMemcpyDeviceToHost));
+    SLQ_CUDA(cudaMemcpy(h2.data(), C2, sizeof(double) * h2.size(), cudaMemcpyDeviceToHost));
+    std::vector<double> ra(M, 0.0), cb(N, 0.0);
+    for (int m = 0; m < M; ++m)
+      for (int k = 0; k < K; ++k) ra[m] = std::max(ra[m], fabs(hA[a_kmajor ? (size_t)m * K + k : (size_t)k * M + m]));
+    for (int n = 0; n < N; ++n)
+      for (int k = 0; k < K; ++k) cb[n] = std::max(cb[n], fabs(hB[b_kmajor ? (size_t)n * K + k : (size_t)k * N + n]));
+    double worst = 0.0;
+    for (int m = 0; m < M; ++m)
+      for (int n = 0; n < N; ++n) {
+        const double den = (double)K * ra[m] * cb[n];
+        const double d = fabs(h1[(size_t)m * N + n] - h2[(size_t)m * N + n]);
+        if (!std::isfinite(h2[(size_t)m * N + n])) worst = INFINITY;
+        else if (den > 0) worst = std::max(worst, d / den);
+      }
+    *max_err = worst;
+    cleanup();
+    return SLQ_OK;
+  } catch (const Error& e) {
+    cleanup();
+    return e.status;
+  }
+}

@@ -11,7 +11,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libslq.so")
 
 SLQ_OK, SLQ_EINVAL, SLQ_ENUMERIC, SLQ_ECUDA, SLQ_ENCCL, SLQ_ETIMEOUT, SLQ_ENOMEM, SLQ_EUNSUPPORTED = 0, 2, 3, 4, 5, 6, 7, 8
-PASS = {"fp64": 0, "fp32": 1, "bf16x3": 2, "paired": 3, "paired_fp32": 4}
+PASS = {"fp64": 0, "fp32": 1, "bf16x3": 2, "paired": 3, "paired_fp32": 4, "fp64_oz": 5}
 REORTH = {"none": 0, "full": 1, "window": 2}
 BASIS = {"fp32": 0, "bf16": 1}
 PERTURB = {"exact": 0, "storage": 1}
@@ -87,6 +87,7 @@ def lib() -> ctypes.CDLL:
         "slq_diag_fp64_peak": (I32, [I32, P]),
         "slq_diag_dmma_peak": (I32, [I32, P]),
         "slq_diag_gemm_f64": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
+        "slq_diag_oz_check": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
         "slq_cg": (I32, [P, P, P, D, I32, D, P, P]),
         "slq_blockdiag": (I32, [P, U64, P, P]),
     }
@@ -176,6 +177,15 @@ def fp64_peak_tflops(device: int = 0) -> dict:
             best = max(best, t.value)
         out[key] = best
     return out
+
+
+def oz_check(M: int, N: int, K: int, a_kmajor: bool = True, b_kmajor: bool = True, S: int = 6, iters: int = 5,
+             device: int = 0) -> Tuple[float, float]:
+    """(max normalised error vs the DMMA fp64 GEMM, fp64-equivalent TFLOP/s) of the Ozaki GEMM."""
+    e, t = ctypes.c_double(), ctypes.c_double()
+    _check(lib().slq_diag_oz_check(device, M, N, K, int(a_kmajor), int(b_kmajor), S, iters, ctypes.byref(e),
+                                   ctypes.byref(t)))
+    return e.value, t.value
 
 
 def kernel_class_names():

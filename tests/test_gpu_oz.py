@@ -1,0 +1,79 @@
+"""The int8 Ozaki fp64 GEMM on tcgen05 (SLQ_PASS_FP64_OZ; oz_gemm.cu) against the DMMA fp64 GEMM,
+and the FP64_OZ pass mode against the fp64 oracle at the north star's fp32 gates (HVP rel-L2 <= 1e-4,
+alpha/beta <= 1e-5 over the first 32 Lanczos steps)."""
+import numpy as np
+import pytest
+
+import slq_inputs as si
+from oracle import fdhvp, lanczos as OL, models, probe
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_00816_b200 import build
+    build.build()
+
+
+from paper_2602_00816_b200 import slq  # noqa: E402
+
+
+@pytest.mark.parametrize("M,N,K,ak,bk", [(128, 64, 64, 1, 1), (300, 70, 100, 1, 1), (2048, 768, 256, 1, 1),
+                                         (2048, 256, 1024, 1, 0), (768, 256, 2048, 0, 0), (37, 203, 64, 0, 1),
+                                         (1, 5, 3, 1, 1), (129, 65, 4000, 1, 1), (64, 4096, 20000, 1, 1)])
+@pytest.mark.parametrize("S", [4, 6, 7])
+def test_oz_gemm_error_bound(M, N, K, ak, bk, S):
+    """Truncated digits only: |C_oz - C| <= (S + 2) 2^-7S K 2^(e_i + f_j) (oz_gemm.cu header) and
+    2^e_i < 2 max|A_i.|, so <= 4 (S + 2) 2^-7S K max|A_i.| max|B_.j|; covers ragged tiles, every
+    operand layout, split-K and the K cap that keeps INT32 exact."""
+    err, tf = slq.oz_check(M, N, K, bool(ak), bool(bk), S, iters=1)
+    bound = 4 * (S + 2) * 2.0 ** (-7 * S)
+    print(f"oz S={S} {M}x{N}x{K} ak={ak} bk={bk}: err {err:.2e} (bound {bound:.1e}), {tf:.1f} TFLOP/s")
+    assert err <= bound
+
+
+def _batch(cfg):
+    return si.mlp_data(cfg) if cfg.arch == si.ARCH_MLP else si.tokens(cfg)
+
+
+@pytest.mark.parametrize("name", ["mlp_tiny", "c1", "gpt_tiny", "gpt_tiny_tied", "llama_tiny", "c2"])
+def test_fp64_oz_grad_and_hvp(name):
+    cfg = si.CONFIGS[name]
+    th = si.init_params(cfg)
+    v = si.random_vector(th.size, 5)
+    with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="fp64_oz") as c:
+        lay = c.layout()
+        g = torch.empty(c.P_loc, dtype=torch.float32, device="cuda")
+        loss = c.grad(g)
+        vd = torch.from_numpy(slq.shard_of(v, lay, 0, 1)).cuda()
+        out = torch.empty_like(vd)
+        c.hvp(vd, out, cfg.eps)
+        hv = slq.unshard([out.cpu().numpy()], lay)
+        gf = slq.unshard([g.cpu().numpy()], lay)
+    l_ref, g_ref = models.loss_grad(th, cfg, _batch(cfg))
+    ref = fdhvp.hvp(fdhvp.make_grad_fn(cfg, _batch(cfg)), th, v, cfg.eps, "exact")
+    eg = np.linalg.norm(gf - g_ref) / np.linalg.norm(g_ref)
+    eh = np.linalg.norm(hv - ref) / np.linalg.norm(ref)
+    print(f"{name} [fp64_oz]: loss {abs(loss - l_ref) / abs(l_ref):.1e} grad {eg:.2e} HVP {eh:.2e}")
+    assert abs(loss - l_ref) <= 1e-9 * abs(l_ref)
+    assert eg <= 1e-7 and eh <= 1e-4
+
+
+@pytest.mark.parametrize("name,m", [("gpt_tiny", 16), ("llama_tiny", 16), ("c1", 32), ("c2", 32)])
+def test_fp64_oz_lanczos_fp32_gates(name, m):
+    cfg = si.CONFIGS[name]
+    th = si.init_params(cfg)
+    with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="fp64_oz", reorth="full", max_steps=m) as c:
+        a, b = c.lanczos(cfg.probe_seed0, m)
+    g = fdhvp.make_grad_fn(cfg, _batch(cfg))
+    r = OL.lanczos(lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact"),
+                   probe.rademacher_probe(cfg.probe_seed0, th.size), m, "full")
+    scale = np.abs(r.alpha).max()
+    ea = np.abs(a - r.alpha) / np.maximum(np.abs(r.alpha), 1e-2 * scale)  # reading R14
+    eb = np.abs(b - r.beta) / np.abs(r.beta)
+    print(f"{name} [fp64_oz]: max rel alpha {ea.max():.2e} beta {eb.max():.2e}")
+    assert ea.max() <= 1e-5 and eb.max() <= 1e-5
