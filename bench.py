@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
-    p.add_argument("--numerics", default="fp64", choices=["fp64", "fp32", "bf16x3", "paired", "paired_fp32"],
+    p.add_argument("--numerics", default="fp64", choices=["fp64", "fp64_oz", "fp32", "bf16x3", "paired", "paired_fp32"],
                    help="gradient-pass arithmetic (fp64 = the c2 parity path; bf16x3 = tcgen05)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -266,7 +266,20 @@ def main():
     dom = max(stats, key=lambda k: stats[k]["ms"])
     st = stats[dom]
     total_ms = sum(s["ms"] for s in stats.values())
-    if dom == "gemm" and args.numerics != "fp64":
+    if dom == "gemm_i8":
+        # INT8 tensor-core products of the Ozaki fp64 GEMMs: peak = the measured bf16 burst x the
+        # nominal dense INT8 / BF16 ratio (4.5 / 2.25 POPS per B200)
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        i8_peak = 2.0 * bf16
+        achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12
+        nprod = {4: 10, 5: 15, 6: 21, 7: 28}[int(os.environ.get("SLQ_OZ_SLICES", "6"))]
+        roof = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOP/s", "frac": achieved / i8_peak,
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks
+                                else "fallback 1590 TFLOP/s") + " x 2 (nominal INT8 / BF16 dense ratio)",
+                "fp64_equiv_tflops": achieved / nprod,
+                "note": f"tcgen05 kind::i8 digit products, {nprod} INT8 GEMMs per fp64 GEMM (S = "
+                        f"{os.environ.get('SLQ_OZ_SLICES', '6')} digit planes); achieved counts every INT8 op issued"}
+    elif dom == "gemm" and args.numerics not in ("fp64", "fp64_oz"):
         bf16 = peaks.get("bf16_tflops", 1590.0)
         achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12
         tc_note = {"bf16x3": "tcgen05 kind::f16 bf16 products (6 per fp32-faithful GEMM, all counted)",
@@ -298,7 +311,7 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": {"fp64": "f64", "fp32": "f32", "bf16x3": "bf16x3", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
+        "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": "f64 (GEMMs: int8 Ozaki digit products)", "fp32": "f32", "bf16x3": "bf16x3", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {'GPT' if cfg.arch == si.ARCH_GPT else 'Llama'} {cfg.n_layers}L "
                                f"d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} V{cfg.vocab}, {si.n_params(cfg)} params "

@@ -19,7 +19,8 @@ void ghost_clusters(const double* nodes, int m, double tol, int32_t* cluster_id,
 
 const char* kernel_class_name(int c) {
   static const char* names[KC_COUNT] = {"gemm", "attention", "norm", "cross_entropy", "embedding",
-                                        "elementwise", "perturb", "fd_lanczos", "reorth", "vector"};
+                                        "elementwise", "perturb", "fd_lanczos", "reorth", "vector", "gemm_i8",
+                                        "oz_slice"};
   return (c >= 0 && c < KC_COUNT) ? names[c] : "?";
 }
 

@@ -42,6 +42,8 @@ enum KernelClass {
   KC_FD,           // (d) FD difference + Lanczos partials
   KC_REORTH,       // (e) reorthogonalisation GEMV
   KC_VEC,          // other vector ops (probe, normalise, reductions)
+  KC_GEMM_I8,      // fp64 GEMMs as tcgen05 INT8 digit products (Ozaki); flops = INT8 ops issued
+  KC_OZ_SLICE,     // Ozaki operand scaling + digit slicing (HBM / L2 bound)
   KC_COUNT
 };
 const char* kernel_class_name(int c);

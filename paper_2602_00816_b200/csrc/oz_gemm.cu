@@ -365,7 +365,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   int* eb = ea + M;
   double* ws = splits > 1 ? (double*)(base + a_bytes + b_bytes + e_bytes) : nullptr;
   {
-    LaunchScope scope(L.prof, KC_ELEM, L.stream, 0, (8.0 + S) * ((double)M * K + (double)N * K));
+    LaunchScope scope(L.prof, KC_OZ_SLICE, L.stream, 0, (8.0 + S) * ((double)M * K + (double)N * K));
     // A(m, k): K-contiguous when sAk == 1 (rows = M, pitch sAm), else stored [K x M] with pitch sAk
     slice<S>(L, a.A, a.sAk == 1, a.sAk == 1 ? a.sAm : a.sAk, M, K, Kp, as, ea);
     // B(k, n) = B[k * sBk + n * sBn]: K-contiguous rows per n when sBk == 1 (pitch sBn)
@@ -375,7 +375,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   const CUtensorMap tb = make_map_i8(bs, (int64_t)S * N, Kp, Kp, BN);
   OzArgs o{M, N, nk, ktps, splits, ea, eb};
   {
-    LaunchScope scope(L.prof, KC_GEMM, L.stream, 2.0 * M * N * (double)K * CF::NPROD,
+    LaunchScope scope(L.prof, KC_GEMM_I8, L.stream, 2.0 * M * N * (double)K * CF::NPROD,
                       (double)S * ((double)M * K + (double)N * K) + 8.0 * M * N);
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
     k_oz_gemm<S><<<grid, 192, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
