@@ -17,7 +17,7 @@
 // one pipeline stage holds all S digit planes of the A and B k-tiles, and the MMA issuer runs the
 // S(S+1)/2 products from them (each plane is read from L2 once per k-tile, not once per product).
 // Warp-specialised: warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA issuer, warps
-// 2..5 epilogue (TMEM -> fp64 combine -> shared tile -> fused epilogue with coalesced stores).
+// 2..9 epilogue (TMEM -> fp64 combine -> shared tile -> fused epilogue with coalesced stores).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -47,7 +47,6 @@ struct Cfg {
   static constexpr int TMEM_COLS = S * BN <= 128 ? 128 : (S * BN <= 256 ? 256 : 512);
   static constexpr int NPROD = S * (S + 1) / 2;
   static_assert(S * BN <= 512, "S accumulators of BN columns must fit TMEM");
-  static_assert(BM * (BN + 1) * 8 <= STAGES * STAGE_BYTES, "fp64 epilogue tile fits the pipeline smem");
 };
 
 // instruction descriptor, kind::i8: D s32, A and B signed 8-bit, both K-major, M x N
@@ -60,10 +59,67 @@ struct OzArgs {
   int kt_per_split, splits;
   const int* ea;         // [M] row exponents of A
   const int* eb;         // [N] column exponents of B
+  int debug;             // diagnostic only (SLQ_OZ_DEBUG): 1 = skip the MMAs, 2 = skip the TMA loads
 };
 
+// 2^e as a double (e within the normal range), built from the exponent bits
+__device__ __forceinline__ double exp2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+
+// Fused epilogue of one row segment held in registers: C[m, n + j] for j < cnt (cnt <= 32).
+// Loads of bias / residual / aux / old C are issued before any store of the segment.
+__device__ __forceinline__ void store_segment(const GemmArgs<double>& p, double* __restrict__ W, int64_t ldw,
+                                              bool partial, int64_t m, int n, int cnt, const double* v) {
+  double* dst = (partial ? W : p.C) + m * (partial ? ldw : p.ldc) + n;
+  if (partial || (!p.bias && !p.resid && !p.aux && !p.accumulate && p.act == ACT_NONE && p.alpha == 1.0)) {
+    if (cnt == 32 && ((uintptr_t)dst & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(v[j], v[j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < cnt) dst[j] = v[j];
+    }
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < 32; h += 8) {
+    double bs[8], rs[8], ax[8], cold[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool ok = h + j < cnt;
+      const int nn = n + h + j;
+      bs[j] = (ok && p.bias) ? p.bias[nn] : 0.0;
+      rs[j] = (ok && p.resid) ? p.resid[m * p.ldr + nn] : 0.0;
+      ax[j] = (ok && p.aux) ? p.aux[m * p.ldaux + nn] : 0.0;
+      cold[j] = (ok && p.accumulate) ? p.C[m * p.ldc + nn] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (h + j >= cnt) continue;
+      const int nn = n + h + j;
+      const double x = p.alpha * v[h + j] + bs[j] + rs[j];
+      double out;
+      switch (p.act) {
+        case ACT_GELU:
+          p.C2[m * p.ldc2 + nn] = x;
+          out = gemm_detail::gelu_tanh(x);
+          break;
+        case ACT_TANH: out = tanh(x); break;
+        case ACT_DGELU: out = x * gemm_detail::gelu_tanh_grad(ax[j]); break;
+        case ACT_DTANH: out = x * (1.0 - ax[j] * ax[j]); break;
+        default: out = x;
+      }
+      dst[h + j] = p.accumulate ? cold[j] + out : out;
+    }
+  }
+}
+
+// Persistent kernel: grid <= #SMs, CTA c processes work units c, c + grid, ... (unit = output
+// tile x K split).  The TMA producer runs ahead across unit boundaries (ring of STAGES k-tiles);
+// the epilogue drains the S accumulators from TMEM into registers, releases TMEM (the next unit's
+// MMAs start), then does the scaling and the global stores while the next unit computes.
 template <int S>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
               GemmArgs<double> p, double* __restrict__ ws) {
   using CF = Cfg<S>;
@@ -72,14 +128,22 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES);
   uint64_t* empty = full + CF::STAGES;
   uint64_t* tmem_full = empty + CF::STAGES;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int split = blockIdx.z;
-  const int kt0 = split * o.kt_per_split;
-  const int kt1 = min(o.nk, kt0 + o.kt_per_split);
-  const int nloc = kt1 > kt0 ? kt1 - kt0 : 0;
+  const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + BM - 1) / BM;
+  const int nwork = tiles_n * tiles_m * o.splits;
+  // unit w -> (split, tile_m, tile_n), n fastest (neighbouring CTAs share the A k-tiles in L2)
+  auto decode = [&](int w, int& m0, int& n0, int& sp, int& kt0, int& nloc) {
+    sp = w % o.splits;
+    const int t = w / o.splits;
+    n0 = (t % tiles_n) * BN;
+    m0 = (t / tiles_n) * BM;
+    kt0 = sp * o.kt_per_split;
+    const int kt1 = min(o.nk, kt0 + o.kt_per_split);
+    nloc = kt1 > kt0 ? kt1 - kt0 : 0;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < CF::STAGES; ++s) {
@@ -87,6 +151,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 8);  // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     asm volatile("fence.proxy.async.shared::cta;\n" ::);
   }
@@ -102,102 +167,120 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer: all S digit planes of A and B for one k-tile per stage ----
-      for (int i = 0; i < nloc; ++i) {
-        const int kt = kt0 + i, s = i % CF::STAGES;
-        const uint32_t ph = (i / CF::STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * CF::STAGE_BYTES;
-        uint8_t* sb = sa + CF::A_BYTES;
-        mbar_expect_tx(&full[s], CF::STAGE_BYTES);
+      int it = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        int m0, n0, sp, kt0, nloc;
+        decode(w, m0, n0, sp, kt0, nloc);
+        for (int i = 0; i < nloc; ++i, ++it) {
+          const int kt = kt0 + i, s = it % CF::STAGES;
+          const uint32_t ph = (it / CF::STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * CF::STAGE_BYTES;
+          uint8_t* sb = sa + CF::A_BYTES;
+          if (o.debug & 2) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&full[s])));
+            continue;
+          }
+          mbar_expect_tx(&full[s], CF::STAGE_BYTES);
 #pragma unroll
-        for (int q = 0; q < S; ++q) {
-          tma_load_2d(sa + q * CF::A_PLANE, &tmA, &full[s], kt * BK, q * o.M + m0);
-          tma_load_2d(sb + q * CF::B_PLANE, &tmB, &full[s], kt * BK, q * o.N + n0);
+          for (int q = 0; q < S; ++q) {
+            tma_load_2d(sa + q * CF::A_PLANE, &tmA, &full[s], kt * BK, q * o.M + m0);
+            tma_load_2d(sb + q * CF::B_PLANE, &tmB, &full[s], kt * BK, q * o.N + n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer: S(S+1)/2 digit products per k-tile ----
       constexpr uint32_t idesc = make_idesc_i8(BM, BN);
-      uint32_t started = 0;  // bit g: accumulator g has been initialised
-      for (int i = 0; i < nloc; ++i) {
-        const int s = i % CF::STAGES;
-        const uint32_t ph = (i / CF::STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int it = 0, tl = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
+        int m0, n0, sp, kt0, nloc;
+        decode(w, m0, n0, sp, kt0, nloc);
+        mbar_wait(tmem_empty, (tl & 1) ^ 1);  // the previous unit's accumulators have been drained
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-        const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
-        const uint32_t sb = sa + CF::A_BYTES;
+        uint32_t started = 0;  // bit g: accumulator g has been initialised
+        for (int i = 0; i < nloc; ++i, ++it) {
+          const int s = it % CF::STAGES;
+          const uint32_t ph = (it / CF::STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
+          const uint32_t sb = sa + CF::A_BYTES;
 #pragma unroll
-        for (int g = 0; g < S; ++g) {
+          for (int g = 0; g < ((o.debug & 1) ? 0 : S); ++g) {
 #pragma unroll
-          for (int pa = 0; pa <= g; ++pa) {
-            const int qb = g - pa;
+            for (int pa = 0; pa <= g; ++pa) {
+              const int qb = g - pa;
 #pragma unroll
-            for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-              const uint64_t da = make_desc_sw64(sa + pa * CF::A_PLANE + kk * UMMA_K);
-              const uint64_t db = make_desc_sw64(sb + qb * CF::B_PLANE + kk * UMMA_K);
-              const uint32_t acc = (started >> g) & 1u;
-              asm volatile(
-                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(g * BN)),
-                  "l"(da), "l"(db), "r"(idesc), "r"(acc));
-              started |= 1u << g;
+              for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                const uint64_t da = make_desc_sw64(sa + pa * CF::A_PLANE + kk * UMMA_K);
+                const uint64_t db = make_desc_sw64(sb + qb * CF::B_PLANE + kk * UMMA_K);
+                const uint32_t acc = (started >> g) & 1u;
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(g * BN)),
+                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                started |= 1u << g;
+              }
             }
           }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              smem_u32(&empty[s])));
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-            smem_u32(&empty[s])));
-      }
-      if (nloc > 0) {
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-            smem_u32(tmem_full)));
-      } else {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_full)));
+        if (nloc > 0) {
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              smem_u32(tmem_full)));
+        } else {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_full)));
+        }
       }
     }
   } else {
-    // ---- epilogue: combine the S digit-weight accumulators in fp64, stage, store ----
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    // ---- epilogue (warps 2..9): warp w drains TMEM lanes 32 (w % 4) .. +31 (its quadrant), columns
+    // [32 h, 32 h + 32) with h = (w - 2) / 4, combining the S digit weights in fp64 ----
     const int lg = (warp % 4) * 32;
-    constexpr int LDS = BN + 1;
-    double* Cs = reinterpret_cast<double*>(smem);
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      double v[16];
+    const int c0 = ((warp - 2) / 4) * 32;
+    int tl = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
+      int m0, n0, sp, kt0, nloc;
+      decode(w, m0, n0, sp, kt0, nloc);
+      mbar_wait(tmem_full, tl & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      double v[32];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.0;
+      for (int i = 0; i < 32; ++i) v[i] = 0.0;
 #pragma unroll
       for (int g = 0; g < S; ++g) {
-        uint32_t r[16];
-        const uint32_t taddr = tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-            "[%16];\n"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-        const double w = ldexp(1.0, -7 * (g + 2));
+        const double wg = exp2i(-7 * (g + 2));
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += (double)(int32_t)r[i] * w;
+        for (int h = 0; h < 32; h += 16) {
+          uint32_t r[16];
+          const uint32_t taddr = tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0 + h);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+              "[%16];\n"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[h + i] = fma((double)(int32_t)r[i], wg, v[h + i]);
+        }
       }
+      // accumulators drained: release TMEM to the next unit's MMAs
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
+      const int row = m0 + lg + lane;
+      const int cols = min(32, p.N - (n0 + c0));
+      if (row < p.M && cols > 0) {
+        const double sr = nloc > 0 ? exp2i(o.ea[row]) : 0.0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) Cs[(lg + lane) * LDS + c + i] = nloc > 0 ? v[i] : 0.0;
-    }
-    asm volatile("bar.sync 1, 128;\n" ::);  // the four epilogue warps only
-    double* W = o.splits > 1 ? ws + (int64_t)split * p.M * p.N : nullptr;
-    const int et = threadIdx.x - 64;
-    const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
-#pragma unroll 1
-    for (int e = et; e < BM * BN; e += 128) {
-      const int rr = e / BN, cc = e % BN;
-      if (rr >= rows || cc >= cols) continue;
-      const double v = ldexp(Cs[rr * LDS + cc], o.ea[m0 + rr] + o.eb[n0 + cc]);
-      if (W)
-        W[(int64_t)(m0 + rr) * p.N + n0 + cc] = v;
-      else
-        gemm_detail::epilogue_store(p, p.C, m0 + rr, n0 + cc, v);
+        for (int i = 0; i < 32; ++i) v[i] *= sr * (i < cols ? exp2i(o.eb[n0 + c0 + i]) : 0.0);
+        store_segment(p, ws + (int64_t)sp * p.M * p.N, p.N, o.splits > 1, row, n0 + c0, cols, v);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -260,34 +343,47 @@ __global__ void k_oz_slice_rows(const double* __restrict__ X, int64_t ld, int ro
   }
 }
 
-// operand stored transposed: element (row r, k) at X[k * ld + r] (r contiguous).  Block of 256
-// threads per 32 rows: column max over K, then 32 x 32 tiles transposed through shared memory.
+// operand stored transposed: element (row r, k) at X[k * ld + r] (r contiguous).
+// Pass 1: column exponents.  Block = 32 rows x 256 k; exp_of is monotone in the maximum, so the
+// per-block exponents combine with an integer atomicMax (deterministic); ex[] starts at kExNone.
+constexpr int kExNone = (int)0x80808080;  // memset byte 0x80
+__global__ void __launch_bounds__(256) k_oz_colexp(const double* __restrict__ X, int64_t ld, int rows, int K,
+                                                  int* __restrict__ ex) {
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int r = blockIdx.x * 32 + tx;
+  const int k0 = blockIdx.y * 256, k1 = min(K, k0 + 256);
+  double mx = 0.0;
+  if (r < rows)
+    for (int k = k0 + ty; k < k1; k += 8) mx = fmax(mx, fabs(X[(int64_t)k * ld + r]));
+  red[ty][tx] = mx;
+  __syncthreads();
+  if (ty == 0 && r < rows) {
+    double m = red[0][tx];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) m = fmax(m, red[i][tx]);
+    if (m > 0.0) atomicMax(&ex[r], exp_of(m));
+  }
+}
+
+// Pass 2: digits.  Block = 32 rows x 128 k, four 32 x 32 tiles transposed through shared memory.
 template <int S>
 __global__ void __launch_bounds__(256) k_oz_slice_cols(const double* __restrict__ X, int64_t ld, int rows, int K,
                                                       int Kp, int8_t* __restrict__ out, int* __restrict__ ex) {
   __shared__ double tile[32][33];
-  __shared__ double red[8][33];
   __shared__ int es[32];
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   const int r0 = blockIdx.x * 32;
   const int r = r0 + tx;
-  double mx = 0.0;
-  if (r < rows)
-    for (int k = ty; k < K; k += 8) mx = fmax(mx, fabs(X[(int64_t)k * ld + r]));
-  red[ty][tx] = mx;
-  __syncthreads();
-  if (ty == 0) {
-    double m = red[0][tx];
-#pragma unroll
-    for (int i = 1; i < 8; ++i) m = fmax(m, red[i][tx]);
-    const int e = exp_of(m);
-    es[tx] = e;
-    if (r < rows) ex[r] = e;
+  if (threadIdx.x < 32) {
+    const int e = r < rows ? ex[r] : 0;
+    es[threadIdx.x] = e == kExNone ? 0 : e;
   }
-  __syncthreads();
   const int64_t plane = (int64_t)rows * Kp;
   const int wr = threadIdx.x / 8, kq = threadIdx.x % 8;  // writer: row r0 + wr, k = 4 kq .. 4 kq + 3
-  for (int k0 = 0; k0 < Kp; k0 += 32) {
+  const int kb = blockIdx.y * 128, ke = min(Kp, kb + 128);
+  for (int k0 = kb; k0 < ke; k0 += 32) {
+    __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int k = k0 + ty + 8 * i;
@@ -305,7 +401,6 @@ __global__ void __launch_bounds__(256) k_oz_slice_cols(const double* __restrict_
         *reinterpret_cast<uint32_t*>(out + q * plane + (int64_t)(r0 + wr) * Kp + k0 + 4 * kq) = w;
       }
     }
-    __syncthreads();
   }
 }
 
@@ -330,7 +425,13 @@ void slice(const Launch& L, const double* X, bool kmajor, int64_t ld, int rows, 
   if (kmajor) {
     k_oz_slice_rows<S><<<(unsigned)ceil_div((int64_t)rows * 32, 256), 256, 0, L.stream>>>(X, ld, rows, K, Kp, out, ex);
   } else {
-    k_oz_slice_cols<S><<<(unsigned)ceil_div(rows, 32), 256, 0, L.stream>>>(X, ld, rows, K, Kp, out, ex);
+    SLQ_CUDA(cudaMemsetAsync(ex, 0x80, sizeof(int) * (size_t)rows, L.stream));
+    k_oz_colexp<<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(K, 256)), 256, 0, L.stream>>>(X, ld, rows, K,
+                                                                                                     ex);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+    k_oz_slice_cols<S><<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(Kp, 128)), 256, 0, L.stream>>>(
+        X, ld, rows, K, Kp, out, ex);
   }
   SLQ_CUDA(cudaGetLastError());
   ++*L.launches;
@@ -373,12 +474,13 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   }
   const CUtensorMap ta = make_map_i8(as, (int64_t)S * M, Kp, Kp, BM);
   const CUtensorMap tb = make_map_i8(bs, (int64_t)S * N, Kp, Kp, BN);
-  OzArgs o{M, N, nk, ktps, splits, ea, eb};
+  static const int dbg = getenv("SLQ_OZ_DEBUG") ? atoi(getenv("SLQ_OZ_DEBUG")) : 0;
+  OzArgs o{M, N, nk, ktps, splits, ea, eb, dbg};
   {
     LaunchScope scope(L.prof, KC_GEMM_I8, L.stream, 2.0 * M * N * (double)K * CF::NPROD,
                       (double)S * ((double)M * K + (double)N * K) + 8.0 * M * N);
-    dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
-    k_oz_gemm<S><<<grid, 192, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
+    const int nwork = tiles * splits;
+    k_oz_gemm<S><<<std::min(nwork, 148), 320, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }
