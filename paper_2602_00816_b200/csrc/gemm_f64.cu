@@ -303,7 +303,8 @@ template <>
 void gemm<double>(const Launch& L, const GemmArgs<double>& a) {
   check(a);
   if (a.M == 0 || a.N == 0) return;
-  if (L.gemm_mode == 2 && a.batch == 1 && a.tri == TRI_NONE && a.K > 0) {
+  if (L.gemm_mode == 2 && a.batch == 1 && a.tri == TRI_NONE && a.K > 0 &&
+      (double)a.M * a.N * (double)a.K >= oz_min_mnk()) {
     gemm_oz(L, a, oz_slices());
     return;
   }

@@ -291,17 +291,18 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-// exponent e with |x| < 2^e for the largest |x| (0 for an all-zero row), and the S digits of x:
-// r = x 2^-e in (-1, 1); d_p = trunc(128 r); r = 128 r - d_p   (all exact in fp64)
+// The S digits of x for row exponent e (|x| < 2^e): the truncated base-128 expansion of x 2^-e,
+// d_p = trunc(128 r_p), r_{p+1} = 128 r_p - d_p.  Computed exactly in integers:
+// Q = trunc(x 2^(7S - e)) (an exact power-of-two scaling, |Q| < 2^(7S)), d_p = sign(x) *
+// ((|Q| >> 7 (S - 1 - p)) & 127) -- the same digits as the fp64 recurrence.
 template <int S>
 __device__ __forceinline__ void digits(double x, int e, int8_t* d) {
-  double r = ldexp(x, -e);
+  const long long q = __double2ll_rz(x * __longlong_as_double((long long)(7 * S - e + 1023) << 52));
+  const long long mag = q < 0 ? -q : q;
 #pragma unroll
-  for (int q = 0; q < S; ++q) {
-    r *= 128.0;
-    const double t = trunc(r);
-    d[q] = (int8_t)(int)t;
-    r -= t;
+  for (int p = 0; p < S; ++p) {
+    const int v = (int)((mag >> (7 * (S - 1 - p))) & 127);
+    d[p] = (int8_t)(q < 0 ? -v : v);
   }
 }
 
@@ -503,6 +504,14 @@ int oz_slices() {
     return (v >= 4 && v <= 7) ? v : 6;
   }();
   return s;
+}
+
+double oz_min_mnk() {
+  static double v = [] {
+    const char* e = getenv("SLQ_OZ_MIN_MNK");
+    return e ? atof(e) : 0.0;
+  }();
+  return v;
 }
 
 void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
