@@ -272,13 +272,13 @@ def main():
         bf16 = peaks.get("bf16_tflops", 1590.0)
         i8_peak = 2.0 * bf16
         achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12
-        nprod = {4: 10, 5: 15, 6: 21, 7: 28}[int(os.environ.get("SLQ_OZ_SLICES", "6"))]
+        nprod = {4: 10, 5: 15, 6: 21, 7: 28}[int(os.environ.get("SLQ_OZ_SLICES", "7"))]
         roof = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOP/s", "frac": achieved / i8_peak,
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks
                                 else "fallback 1590 TFLOP/s") + " x 2 (nominal INT8 / BF16 dense ratio)",
                 "fp64_equiv_tflops": achieved / nprod,
                 "note": f"tcgen05 kind::i8 digit products, {nprod} INT8 GEMMs per fp64 GEMM (S = "
-                        f"{os.environ.get('SLQ_OZ_SLICES', '6')} digit planes); achieved counts every INT8 op issued"}
+                        f"{os.environ.get('SLQ_OZ_SLICES', '7')} digit planes); achieved counts every INT8 op issued"}
     elif dom == "gemm" and args.numerics not in ("fp64", "fp64_oz"):
         bf16 = peaks.get("bf16_tflops", 1590.0)
         achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12

@@ -60,8 +60,8 @@ enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2, SLQ_PASS_PAIRE
        SLQ_PASS_FP64_OZ = 5 };
 /* SLQ_PASS_FP64_OZ: as FP64 (fp64 activations and nonlinearities), but every dense non-batched
  * GEMM runs on the tcgen05 INT8 tensor cores as exact digit products (Ozaki scheme: each operand
- * row/column scaled by a power of two and cut into S = 6 signed 7-bit digit planes; the
- * S(S+1)/2 leading products accumulate exactly in INT32 TMEM; error <~ 8 * 2^-42 K max|a| max|b|).
+ * row/column scaled by a power of two and cut into S = 7 signed 7-bit digit planes; the
+ * S(S+1)/2 leading products accumulate exactly in INT32 TMEM; error <~ 9 * 2^-49 K max|a| max|b|).
  * The batched causal attention GEMMs stay on the FP64 DMMA path. */
 /* SLQ_PASS_PAIRED: the two gradient evaluations of Eq. (1) carried as (mean, half-difference)
  * pairs through ONE pass, so (g+ - g-) is never formed by subtracting rounded gradients

@@ -76,7 +76,7 @@ void gemm(const Launch& L, const GemmArgs<T>& a);
 // fp64 GEMM as exact INT8 digit products on the tcgen05 tensor cores (Ozaki scheme, S digit
 // planes of 7 bits per operand; oz_gemm.cu).  batch == 1, dense (tri == TRI_NONE) only.
 void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S);
-int oz_slices();      // S for the pass path: SLQ_OZ_SLICES (4..7), default 6
+int oz_slices();      // S for the pass path: SLQ_OZ_SLICES (4..7), default 7
 double oz_min_mnk();  // FP64_OZ: smaller GEMMs (M N K below this) stay on DMMA (SLQ_OZ_MIN_MNK)
 
 // fp32-faithful GEMM on the tcgen05 tensor cores: every fp32 operand is split into three bf16

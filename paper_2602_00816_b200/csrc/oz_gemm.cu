@@ -10,8 +10,8 @@
 // Each a_p . b_q is an exact INT8 x INT8 -> INT32 tensor-core product; the products of one digit
 // weight g share one INT32 TMEM accumulator (no rounding anywhere in the contraction; |acc| <=
 // S K 127^2 < 2^31 is enforced by capping K per split).  The only error is the dropped digits,
-// |error| <~ (S + 2) 2^{-7S} K max|A_i.| max|B_.j|; S = 6 keeps the FD-HVP of c2 at ~7e-7 of the
-// fp64 result (measured by emulation).
+// |error| <~ (S + 2) 2^{-7S} K max|A_i.| max|B_.j|.  S = 7 (default) meets the fp32 alpha/beta
+// gate on c2 (S = 6: HVP 1.2e-6 but alpha drifts to 1.9e-4 by step 32; measured on B200).
 //
 // Kernel: BM = 128 x BN = 64 output tile per CTA, K in 64-byte k-tiles (SWIZZLE_64B TMA boxes);
 // one pipeline stage holds all S digit planes of the A and B k-tiles, and the MMA issuer runs the
@@ -43,7 +43,8 @@ struct Cfg {
   static constexpr int A_BYTES = S * A_PLANE, B_BYTES = S * B_PLANE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (3 * STAGE_BYTES + 2048 <= 227 * 1024) ? 3 : 2;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 8 * 128 * 8 /*epilogue*/;
+  static_assert(SMEM <= 232448, "dynamic shared memory per CTA");
   static constexpr int TMEM_COLS = S * BN <= 128 ? 128 : (S * BN <= 256 ? 256 : 512);
   static constexpr int NPROD = S * (S + 1) / 2;
   static_assert(S * BN <= 512, "S accumulators of BN columns must fit TMEM");
@@ -59,60 +60,29 @@ struct OzArgs {
   int kt_per_split, splits;
   const int* ea;         // [M] row exponents of A
   const int* eb;         // [N] column exponents of B
-  int debug;             // diagnostic only (SLQ_OZ_DEBUG): 1 = skip the MMAs, 2 = skip the TMA loads
+  int debug;  // diagnostic only (SLQ_OZ_DEBUG bits): 1 no MMAs, 2 no TMA loads, 4 no stores, 8 no TMEM drain
 };
+
+// 32 consecutive TMEM columns of the warp's 32 lanes (one 32-bit value per lane per column)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+// int32 (two's complement bits) -> double, exactly, with one integer op and one fp64 add (the
+// I2F.F64 conversion is a slow-path instruction): 2^52 + 2^31 + x has x + 2^31 in its low word
+__device__ __forceinline__ double i2d(uint32_t x) {
+  return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
+}
 
 // 2^e as a double (e within the normal range), built from the exponent bits
 __device__ __forceinline__ double exp2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
-
-// Fused epilogue of one row segment held in registers: C[m, n + j] for j < cnt (cnt <= 32).
-// Loads of bias / residual / aux / old C are issued before any store of the segment.
-__device__ __forceinline__ void store_segment(const GemmArgs<double>& p, double* __restrict__ W, int64_t ldw,
-                                              bool partial, int64_t m, int n, int cnt, const double* v) {
-  double* dst = (partial ? W : p.C) + m * (partial ? ldw : p.ldc) + n;
-  if (partial || (!p.bias && !p.resid && !p.aux && !p.accumulate && p.act == ACT_NONE && p.alpha == 1.0)) {
-    if (cnt == 32 && ((uintptr_t)dst & 15) == 0) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(v[j], v[j + 1]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < cnt) dst[j] = v[j];
-    }
-    return;
-  }
-#pragma unroll
-  for (int h = 0; h < 32; h += 8) {
-    double bs[8], rs[8], ax[8], cold[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const bool ok = h + j < cnt;
-      const int nn = n + h + j;
-      bs[j] = (ok && p.bias) ? p.bias[nn] : 0.0;
-      rs[j] = (ok && p.resid) ? p.resid[m * p.ldr + nn] : 0.0;
-      ax[j] = (ok && p.aux) ? p.aux[m * p.ldaux + nn] : 0.0;
-      cold[j] = (ok && p.accumulate) ? p.C[m * p.ldc + nn] : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (h + j >= cnt) continue;
-      const int nn = n + h + j;
-      const double x = p.alpha * v[h + j] + bs[j] + rs[j];
-      double out;
-      switch (p.act) {
-        case ACT_GELU:
-          p.C2[m * p.ldc2 + nn] = x;
-          out = gemm_detail::gelu_tanh(x);
-          break;
-        case ACT_TANH: out = tanh(x); break;
-        case ACT_DGELU: out = x * gemm_detail::gelu_tanh_grad(ax[j]); break;
-        case ACT_DTANH: out = x * (1.0 - ax[j] * ax[j]); break;
-        default: out = x;
-      }
-      dst[h + j] = p.accumulate ? cold[j] + out : out;
-    }
-  }
-}
 
 // Persistent kernel: grid <= #SMs, CTA c processes work units c, c + grid, ... (unit = output
 // tile x K split).  The TMA producer runs ahead across unit boundaries (ring of STAGES k-tiles);
@@ -130,6 +100,7 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* tmem_full = empty + CF::STAGES;
   uint64_t* tmem_empty = tmem_full + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+  double* stage_t = reinterpret_cast<double*>(smem + CF::STAGES * CF::STAGE_BYTES + 256);  // 8 x 32 x 4
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + BM - 1) / BM;
@@ -245,41 +216,89 @@ __global__ void __launch_bounds__(320, 1)
     for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
       int m0, n0, sp, kt0, nloc;
       decode(w, m0, n0, sp, kt0, nloc);
+      // scales first (their global-load latency overlaps the wait for the accumulators):
+      // lane l holds 2^f for column n0 + c0 + l and 2^e for row m0 + lg + l
+      const int n_l = n0 + c0 + lane, row_l = m0 + lg + lane;
+      const double sc_l = n_l < p.N ? exp2i(o.eb[n_l]) : 0.0;
+      const double sr = (nloc > 0 && row_l < p.M) ? exp2i(o.ea[row_l]) : 0.0;
       mbar_wait(tmem_full, tl & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       double v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.0;
+      // two digit-weight groups per TMEM round trip (2 x 32 columns, one wait)
 #pragma unroll
-      for (int g = 0; g < S; ++g) {
-        const double wg = exp2i(-7 * (g + 2));
+      for (int g = 0; g < ((o.debug & 8) ? 0 : S); g += 2) {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
+        if (g + 1 < S) tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)((g + 1) * BN + c0), r1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+        const double w0 = exp2i(-7 * (g + 2)), w1 = exp2i(-7 * (g + 3));
 #pragma unroll
-        for (int h = 0; h < 32; h += 16) {
-          uint32_t r[16];
-          const uint32_t taddr = tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0 + h);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-              "[%16];\n"
-              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                "=r"(r[15])
-              : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+        for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r0[i]), w0, v[i]);
+        if (g + 1 < S) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[h + i] = fma((double)(int32_t)r[i], wg, v[h + i]);
+          for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r1[i]), w1, v[i]);
         }
       }
       // accumulators drained: release TMEM to the next unit's MMAs
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
-      const int row = m0 + lg + lane;
-      const int cols = min(32, p.N - (n0 + c0));
-      if (row < p.M && cols > 0) {
-        const double sr = nloc > 0 ? exp2i(o.ea[row]) : 0.0;
+      // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
+      // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
+      // sectors) instead of 32 rows x 8 bytes
+      const int ncol = p.N - (n0 + c0);  // valid columns of this warp's 32 (may be <= 0)
+      double* T = stage_t + (warp - 2) * 128;
+      const bool plain = o.splits > 1 || (!p.bias && !p.resid && !p.aux && !p.accumulate && p.act == ACT_NONE &&
+                                          p.alpha == 1.0);
+      double* Wd = o.splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
+      const int64_t ldw = o.splits > 1 ? p.N : p.ldc;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= sr * (i < cols ? exp2i(o.eb[n0 + c0 + i]) : 0.0);
-        store_segment(p, ws + (int64_t)sp * p.M * p.N, p.N, o.splits > 1, row, n0 + c0, cols, v);
+      for (int c = 0; c < ((o.debug & 4) ? 0 : 32); c += 4) {
+        __syncwarp();
+        *reinterpret_cast<double2*>(&T[lane * 4]) = make_double2(v[c] * sr, v[c + 1] * sr);
+        *reinterpret_cast<double2*>(&T[lane * 4 + 2]) = make_double2(v[c + 2] * sr, v[c + 3] * sr);
+        __syncwarp();
+        const int cc = c + (lane & 3);          // column within the warp's 32
+        const int n = n0 + c0 + cc;
+        const bool colok = cc < ncol;
+        const double sc = __shfl_sync(0xffffffffu, sc_l, cc);
+        double x[4], bs = 0.0, rs[4], ax[4], cold[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int m = m0 + lg + 8 * j + (lane >> 2);
+          const bool ok = colok && m < p.M;
+          x[j] = T[(8 * j + (lane >> 2)) * 4 + (lane & 3)] * sc;
+          if (!plain) {
+            rs[j] = (ok && p.resid) ? p.resid[(int64_t)m * p.ldr + n] : 0.0;
+            ax[j] = (ok && p.aux) ? p.aux[(int64_t)m * p.ldaux + n] : 0.0;
+            cold[j] = (ok && p.accumulate) ? p.C[(int64_t)m * p.ldc + n] : 0.0;
+          }
+        }
+        if (!plain && colok && p.bias) bs = p.bias[n];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int m = m0 + lg + 8 * j + (lane >> 2);
+          if (!colok || m >= p.M) continue;
+          if (plain) {
+            Wd[(int64_t)m * ldw + n] = x[j];
+            continue;
+          }
+          const double y = p.alpha * x[j] + bs + rs[j];
+          double out;
+          switch (p.act) {
+            case ACT_GELU:
+              p.C2[(int64_t)m * p.ldc2 + n] = y;
+              out = gemm_detail::gelu_tanh(y);
+              break;
+            case ACT_TANH: out = tanh(y); break;
+            case ACT_DGELU: out = y * gemm_detail::gelu_tanh_grad(ax[j]); break;
+            case ACT_DTANH: out = y * (1.0 - ax[j] * ax[j]); break;
+            default: out = y;
+          }
+          p.C[(int64_t)m * p.ldc + n] = p.accumulate ? cold[j] + out : out;
+        }
       }
     }
   }
@@ -500,8 +519,8 @@ void run(const Launch& L, const GemmArgs<double>& a) {
 int oz_slices() {
   static int s = [] {
     const char* e = getenv("SLQ_OZ_SLICES");
-    const int v = e ? atoi(e) : 6;
-    return (v >= 4 && v <= 7) ? v : 6;
+    const int v = e ? atoi(e) : 7;
+    return (v >= 4 && v <= 7) ? v : 7;
   }();
   return s;
 }
