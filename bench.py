@@ -43,8 +43,10 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
-    p.add_argument("--numerics", default="fp64", choices=["fp64", "fp64_oz", "fp32", "bf16x3", "paired", "paired_fp32"],
-                   help="gradient-pass arithmetic (fp64 = the c2 parity path; bf16x3 = tcgen05)")
+    p.add_argument("--numerics", default="fp64_oz", choices=["fp64", "fp64_oz", "fp32", "bf16x3", "paired", "paired_fp32"],
+                   help="gradient-pass arithmetic: fp64_oz (default) = fp64 passes with the large GEMMs as "
+                        "exact int8 digit products on tcgen05 (Ozaki) and the rest on DMMA; fp64 = all DMMA; "
+                        "bf16x3 = fp32-faithful tcgen05")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -311,7 +313,7 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": "f64 (GEMMs: int8 Ozaki digit products)", "fp32": "f32", "bf16x3": "bf16x3", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
+        "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": f"f64 (dense GEMMs with M*N*K >= {float(os.environ.get('SLQ_OZ_MIN_MNK', '1e9')):.0e} as exact int8 digit products on tcgen05, S={os.environ.get('SLQ_OZ_SLICES', '7')}; the rest fp64 DMMA)", "fp32": "f32", "bf16x3": "bf16x3", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {'GPT' if cfg.arch == si.ARCH_GPT else 'Llama'} {cfg.n_layers}L "
                                f"d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} V{cfg.vocab}, {si.n_params(cfg)} params "

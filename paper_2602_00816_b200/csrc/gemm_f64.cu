@@ -55,7 +55,7 @@ struct Smem {
 };
 
 template <class TL, bool AK, bool BKm>
-__global__ void __launch_bounds__(TL::THREADS) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
+__global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : 1) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
                                                                 double* __restrict__ ws) {
   using SM = Smem<TL, AK, BKm>;
   constexpr int BM = TL::BM, BN = TL::BN, BK = TL::BK, S = TL::STAGES;

@@ -527,8 +527,10 @@ int oz_slices() {
 
 double oz_min_mnk() {
   static double v = [] {
+    // measured on B200 (c2 step, tools/exp_oz.sh): the int8 path wins on the 2e9-MNK head GEMMs and
+    // breaks even below ~1e9, where slicing launches and the fp64 epilogue dominate
     const char* e = getenv("SLQ_OZ_MIN_MNK");
-    return e ? atof(e) : 0.0;
+    return e ? atof(e) : 1e9;
   }();
   return v;
 }

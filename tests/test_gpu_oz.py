@@ -1,11 +1,17 @@
 """The int8 Ozaki fp64 GEMM on tcgen05 (SLQ_PASS_FP64_OZ; oz_gemm.cu) against the DMMA fp64 GEMM,
 and the FP64_OZ pass mode against the fp64 oracle at the north star's fp32 gates (HVP rel-L2 <= 1e-4,
 alpha/beta <= 1e-5 over the first 32 Lanczos steps)."""
+import os
+
 import numpy as np
 import pytest
 
 import slq_inputs as si
 from oracle import fdhvp, lanczos as OL, models, probe
+
+# every dense GEMM through the int8 path (the production default keeps GEMMs below 1e9 M N K on
+# DMMA); read by the library on first use, so set before any FP64_OZ context exists
+os.environ["SLQ_OZ_MIN_MNK"] = "0"
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
