@@ -49,6 +49,7 @@ struct FsdpIO : PassIO<T> {
     return dst;
   }
   T* grads(int u) override { return u == 0 ? gbuf0 : gbuf1; }
+  bool collective() const override { return true; }
   void grads_done(int u) override {
     const UnitPlan& up = plan->units[u];
     T* g = u == 0 ? gbuf0 : gbuf1;

@@ -179,8 +179,10 @@ double gemm_flops(const GemmArgs<double>& a) {
 template <class TL>
 int choose_splits(const GemmArgs<double>& a, int tiles, int forced) {
   if (forced > 0) return forced;
-  if (a.batch != 1 || a.tri != TRI_NONE || a.K < 256 || tiles >= 2 * 148) return 1;
-  int s = (int)ceil_div(2 * 148, tiles);
+  static const int min_k = getenv("SLQ_DMMA_SPLIT_MIN_K") ? atoi(getenv("SLQ_DMMA_SPLIT_MIN_K")) : 256;
+  static const int waves = getenv("SLQ_DMMA_SPLIT_WAVES") ? atoi(getenv("SLQ_DMMA_SPLIT_WAVES")) : 2;
+  if (a.batch != 1 || a.tri != TRI_NONE || a.K < min_k || tiles >= waves * 148) return 1;
+  int s = (int)ceil_div(waves * 148, tiles);
   s = std::min<int>(s, (int)(a.K / (4 * TL::BK)));
   return std::max(1, std::min(s, 32));
 }

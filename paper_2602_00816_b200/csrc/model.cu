@@ -209,10 +209,28 @@ struct SideStream {
     SLQ_CUDA(cudaEventRecord(ev_join, side.stream));
     SLQ_CUDA(cudaStreamWaitEvent(main.stream, ev_join, 0));
   }
+  // Lag-1 pipelining of the backward: the side stream may run up to two layers behind the data-
+  // gradient chain.  mark(k) records the side stream's progress after a layer that used scratch
+  // set k; wait_mark(k) makes the main stream wait for it before set k is overwritten again.
+  cudaEvent_t ev_mark[2] = {nullptr, nullptr};
+  bool marked[2] = {false, false};
+  void begin_pass() { marked[0] = marked[1] = false; }
+  void mark(int k) {
+    if (serial()) return;
+    if (!ev_mark[k]) SLQ_CUDA(cudaEventCreateWithFlags(&ev_mark[k], cudaEventDisableTiming));
+    SLQ_CUDA(cudaEventRecord(ev_mark[k], side.stream));
+    marked[k] = true;
+  }
+  void wait_mark(int k) {
+    if (serial() || !marked[k]) return;
+    SLQ_CUDA(cudaStreamWaitEvent(main.stream, ev_mark[k], 0));
+  }
   ~SideStream() {
     if (s) cudaStreamSynchronize(s);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    for (cudaEvent_t e : ev_mark)
+      if (e) cudaEventDestroy(e);
     if (s) cudaStreamDestroy(s);
   }
 };
@@ -285,7 +303,10 @@ struct GptRunner : Runner<T> {
   struct Layer { T *mean1, *rstd1, *h1, *qkv, *P, *o, *x1, *mean2, *rstd2, *h2, *u, *gu; };
   std::vector<Layer> ly;
   T *meanf, *rstdf, *xf, *logits;
-  T *dxs[2], *dx1, *dh1, *dh2, *dqkv, *dP, *do_, *du;
+  // backward scratch: two sets (the side stream lags by up to one layer) and three residual-
+  // gradient buffers
+  struct Bwd { T *dx1, *dh1, *dh2, *dqkv, *du; } bb[2];
+  T *dxs[3], *dhf, *dP, *do_;
   SideStream ss;
 
   GptRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
@@ -310,10 +331,12 @@ struct GptRunner : Runner<T> {
     }
     meanf = A.alloc<T>(N); rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D);
     logits = A.alloc<T>((int64_t)N * V);
-    dxs[0] = A.alloc<T>((int64_t)N * D); dxs[1] = A.alloc<T>((int64_t)N * D);
-    dx1 = A.alloc<T>((int64_t)N * D); dh1 = A.alloc<T>((int64_t)N * D); dh2 = A.alloc<T>((int64_t)N * D);
-    dqkv = A.alloc<T>((int64_t)N * 3 * D); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * D);
-    du = A.alloc<T>((int64_t)N * F);
+    for (int i = 0; i < 3; ++i) dxs[i] = A.alloc<T>((int64_t)N * D);
+    for (Bwd& b2 : bb) {
+      b2.dx1 = A.alloc<T>((int64_t)N * D); b2.dh1 = A.alloc<T>((int64_t)N * D); b2.dh2 = A.alloc<T>((int64_t)N * D);
+      b2.dqkv = A.alloc<T>((int64_t)N * 3 * D); b2.du = A.alloc<T>((int64_t)N * F);
+    }
+    dhf = A.alloc<T>((int64_t)N * D); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * D);
   }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
   double flops_per_pass() const override {
@@ -356,18 +379,20 @@ struct GptRunner : Runner<T> {
     cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
     // ---------------- backward ----------------
     // weight / bias / gain gradients go to the side stream (Ls); the data-gradient chain stays on L
+    // and only waits for the side stream when a scratch set is about to be reused (lag 1)
     const Launch& Ls = ss.lane();
+    ss.begin_pass();
     T* G0 = tied ? io.grads(0) : nullptr;
     T* Gf = io.grads(Ly + 1);
     int cur = 0;  // dxs[cur] = dL/d(residual stream) entering the current block from above
     ss.fork();
     linear_wgrad<T>(Ls, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("wte").offset : Gf + uf.t("head.w").offset);
-    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dh2, D);
+    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dhf, D);
     ss.fork();
-    colreduce<T>(Ls, 1, dh2, D, xs[Ly], meanf, rstdf, Gf + uf.t("lnf.g").offset, Gf + uf.t("lnf.b").offset, N, D,
+    colreduce<T>(Ls, 1, dhf, D, xs[Ly], meanf, rstdf, Gf + uf.t("lnf.g").offset, Gf + uf.t("lnf.b").offset, N, D,
                  false);
-    layernorm_bwd<T>(L, dh2, xs[Ly], meanf, rstdf, Pf + uf.t("lnf.g").offset, nullptr, dxs[cur], N, D);
-    ss.join();
+    layernorm_bwd<T>(L, dhf, xs[Ly], meanf, rstdf, Pf + uf.t("lnf.g").offset, nullptr, dxs[cur], N, D);
+    if (io.collective()) ss.join();
     io.grads_done(Ly + 1);
     for (int l = Ly - 1; l >= 0; --l) {
       const UnitPlan& ub = plan->units[1 + l];
@@ -376,8 +401,11 @@ struct GptRunner : Runner<T> {
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
       Layer& a = ly[l];
+      const int set = (Ly - 1 - l) & 1;
+      ss.wait_mark(set);  // the side stream is done with this set (and with dxs[cur + 1]) from two layers up
+      T *dx1 = bb[set].dx1, *dh1 = bb[set].dh1, *dh2 = bb[set].dh2, *dqkv = bb[set].dqkv, *du = bb[set].du;
       T* dx = dxs[cur];
-      T* dxn = dxs[cur ^ 1];
+      T* dxn = dxs[(cur + 1) % 3];
       // MLP: xs[l+1] = x1 + mproj(gelu(fc(ln2(x1))))
       ss.fork();
       linear_wgrad<T>(Ls, dx, D, a.gu, F, D, F, N, gw("mproj.w"));
@@ -403,10 +431,12 @@ struct GptRunner : Runner<T> {
       ss.fork();
       colreduce<T>(Ls, 1, dh1, D, xs[l], a.mean1, a.rstd1, gw("ln1.g"), gw("ln1.b"), N, D, false);
       layernorm_bwd<T>(L, dh1, xs[l], a.mean1, a.rstd1, w("ln1.g"), dx1, dxn, N, D);
-      ss.join();  // side reads of dx, du, dx1, dqkv, dh* done before the next block reuses them
+      ss.mark(set);
+      if (io.collective()) ss.join();  // the unit's reduce-scatter needs its weight gradients
       io.grads_done(1 + l);
-      cur ^= 1;
+      cur = (cur + 1) % 3;
     }
+    ss.join();  // all side work (incl. the tied head gradient into G0) before the embedding backward
     if (!tied) G0 = io.grads(0);
     embed_bwd_rows<T>(L, csr_off, csr_pos, dxs[cur], G0 + u0.t("wte").offset, V, D, tied);
     pos_bwd<T>(L, dxs[cur], G0 + u0.t("wpe").offset, nseq, Tn, D);
@@ -432,7 +462,9 @@ struct LlamaRunner : Runner<T> {
   struct Layer { T *rstd1, *h1, *qkv, *P, *o, *x1, *rstd2, *h2, *ab, *f; };
   std::vector<Layer> ly;
   T *rstdf, *xf, *logits;
-  T *dxs[2], *dx1, *dh1, *dh2, *dqkv, *dP, *do_, *df, *dab;
+  // backward scratch: two sets for what the side stream reads (lag 1), three residual gradients
+  struct Bwd { T *dx1, *dh1, *dh2, *dqkv, *dab; } bb[2];
+  T *dxs[3], *dhf, *dP, *do_, *df;
   SideStream ss;
 
   LlamaRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
@@ -471,10 +503,13 @@ struct LlamaRunner : Runner<T> {
       ly.push_back(a);
     }
     rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D); logits = A.alloc<T>((int64_t)N * V);
-    dxs[0] = A.alloc<T>((int64_t)N * D); dxs[1] = A.alloc<T>((int64_t)N * D);
-    dx1 = A.alloc<T>((int64_t)N * D); dh1 = A.alloc<T>((int64_t)N * D); dh2 = A.alloc<T>((int64_t)N * D);
-    dqkv = A.alloc<T>((int64_t)N * Wq); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * Hq * hd);
-    df = A.alloc<T>((int64_t)N * F); dab = A.alloc<T>((int64_t)N * 2 * F);
+    for (int i = 0; i < 3; ++i) dxs[i] = A.alloc<T>((int64_t)N * D);
+    for (Bwd& b2 : bb) {
+      b2.dx1 = A.alloc<T>((int64_t)N * D); b2.dh1 = A.alloc<T>((int64_t)N * D); b2.dh2 = A.alloc<T>((int64_t)N * D);
+      b2.dqkv = A.alloc<T>((int64_t)N * Wq); b2.dab = A.alloc<T>((int64_t)N * 2 * F);
+    }
+    dhf = A.alloc<T>((int64_t)N * D); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * Hq * hd);
+    df = A.alloc<T>((int64_t)N * F);
   }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
   double flops_per_pass() const override {
@@ -523,16 +558,17 @@ struct LlamaRunner : Runner<T> {
     cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
 
     const Launch& Ls = ss.lane();
+    ss.begin_pass();
     T* G0 = tied ? io.grads(0) : nullptr;
     T* Gf = io.grads(Ly + 1);
     int cur = 0;
     ss.fork();
     linear_wgrad<T>(Ls, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("tok").offset : Gf + uf.t("head.w").offset);
-    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dh2, D);
+    linear_dgrad<T>(L, logits, V, Whead, V, D, N, dhf, D);
     ss.fork();
-    colreduce<T>(Ls, 2, dh2, D, xs[Ly], nullptr, rstdf, Gf + uf.t("norm").offset, nullptr, N, D, false);
-    rmsnorm_bwd<T>(L, dh2, xs[Ly], rstdf, Pf + uf.t("norm").offset, nullptr, dxs[cur], N, D);
-    ss.join();
+    colreduce<T>(Ls, 2, dhf, D, xs[Ly], nullptr, rstdf, Gf + uf.t("norm").offset, nullptr, N, D, false);
+    rmsnorm_bwd<T>(L, dhf, xs[Ly], rstdf, Pf + uf.t("norm").offset, nullptr, dxs[cur], N, D);
+    if (io.collective()) ss.join();
     io.grads_done(Ly + 1);
     for (int l = Ly - 1; l >= 0; --l) {
       const UnitPlan& ub = plan->units[1 + l];
@@ -541,8 +577,11 @@ struct LlamaRunner : Runner<T> {
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
       Layer& a = ly[l];
+      const int set = (Ly - 1 - l) & 1;
+      ss.wait_mark(set);  // side stream done with this scratch set (two layers up)
+      T *dx1 = bb[set].dx1, *dh1 = bb[set].dh1, *dh2 = bb[set].dh2, *dqkv = bb[set].dqkv, *dab = bb[set].dab;
       T* dx = dxs[cur];
-      T* dxn = dxs[cur ^ 1];
+      T* dxn = dxs[(cur + 1) % 3];
       ss.fork();
       linear_wgrad<T>(Ls, dx, D, a.f, F, D, F, N, gw("wd"));
       linear_dgrad<T>(L, dx, D, w("wd"), D, F, N, df, F);
@@ -565,10 +604,12 @@ struct LlamaRunner : Runner<T> {
       ss.fork();
       colreduce<T>(Ls, 2, dh1, D, xs[l], nullptr, a.rstd1, gw("attn_norm"), nullptr, N, D, false);
       rmsnorm_bwd<T>(L, dh1, xs[l], a.rstd1, w("attn_norm"), dx1, dxn, N, D);
-      ss.join();
+      ss.mark(set);
+      if (io.collective()) ss.join();
       io.grads_done(1 + l);
-      cur ^= 1;
+      cur = (cur + 1) % 3;
     }
+    ss.join();
     if (!tied) G0 = io.grads(0);
     embed_bwd_rows<T>(L, csr_off, csr_pos, dxs[cur], G0 + u0.t("tok").offset, V, D, tied);
     io.grads_done(0);

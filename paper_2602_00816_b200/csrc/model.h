@@ -22,6 +22,9 @@ struct PassIO {
   // buffer persists from the first grads(0) call to grads_done(0))
   virtual T* grads(int u) = 0;
   virtual void grads_done(int u) = 0;
+  // true when grads_done() starts a collective on the unit's gradient (FSDP reduce-scatter): the
+  // runner must then finish the unit's side-stream gradient work first
+  virtual bool collective() const { return false; }
 };
 
 struct HostBatch {
