@@ -245,8 +245,15 @@ slq_status slq_init(const slq_model_desc* desc, const slq_batch* batch, const sl
       SLQ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
       ctx->own_stream = true;
     }
-    if (world->world_size > 1)
+    if (world->world_size > 1) {
       ctx->comm.reset(new Comm(world->nccl_unique_id, world->rank, world->world_size, world->device));
+    } else if (getenv("SLQ_FORCE_NCCL") && atoi(getenv("SLQ_FORCE_NCCL")) != 0) {
+      // diagnostic: a one-rank NCCL communicator, so the FSDP path (per-unit all-gather /
+      // reduce-scatter, scalar all-reduces) runs on a single GPU (tests/test_gpu_fsdp1.py)
+      char uid[128];
+      nccl_unique_id(uid);
+      ctx->comm.reset(new Comm(uid, 0, 1, world->device));
+    }
     ctx->engine = make_engine(*desc, ctx->plan, hb, batch->params_host, world->rank, ctx->comm.get(),
                               ctx->launch());
   });

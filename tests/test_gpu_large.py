@@ -28,7 +28,7 @@ def built():
     build.build()
 
 
-def _case(name):
+def _case(name, numerics="fp64"):
     from paper_2602_00816_b200 import slq
     cfg = si.CONFIGS[name]
     t0 = time.time()
@@ -36,7 +36,8 @@ def _case(name):
     tok = si.tokens(cfg)
     P = th.size
     q1 = probe.rademacher_probe(cfg.probe_seed0, P)
-    with slq.SlqContext(cfg, th, tok, reorth="full" if cfg.reorth_full else "none", max_steps=cfg.m) as c:
+    with slq.SlqContext(cfg, th, tok, reorth="full" if cfg.reorth_full else "none", max_steps=cfg.m,
+                        pass_numerics=numerics) as c:
         lay = c.layout()
         qd = torch.from_numpy(slq.shard_of(q1.astype(np.float32), lay, 0, 1)).cuda()
         out = torch.empty_like(qd)
@@ -63,19 +64,25 @@ def _case(name):
     n1, _ = OL.gauss_quadrature(a, b)
     n2, _ = OL.gauss_quadrature(r.alpha, r.beta)
     scale = max(abs(n2[0]), abs(n2[-1]))
-    print(f"{name}: P={P} HVP rel {err:.2e}; alpha {a} vs {r.alpha}; beta {b} vs {r.beta}; "
+    print(f"{name} [{numerics}]: P={P} HVP rel {err:.2e}; alpha {a} vs {r.alpha}; beta {b} vs {r.beta}; "
           f"mu1 {mu_gpu[0]:.6e}/{mu_orc[0]:.6e} mu2 {mu_gpu[1]:.6e}/{mu_orc[1]:.6e}; "
           f"ritz {n1[0]:.6e},{n1[-1]:.6e} vs {n2[0]:.6e},{n2[-1]:.6e}; gpu {t_gpu:.0f}s total {t_all:.0f}s")
-    assert err <= 1e-4
-    assert np.all(np.abs(a - r.alpha) <= 1e-5 * np.maximum(np.abs(r.alpha), 1e-2 * np.abs(r.alpha).max()))
-    assert np.all(np.abs(b - r.beta) <= 1e-5 * np.abs(r.beta))
+    if numerics != "bf16x3":  # fp64-faithful passes also meet the fp32 gates
+        assert err <= 1e-4
+        assert np.all(np.abs(a - r.alpha) <= 1e-5 * np.maximum(np.abs(r.alpha), 1e-2 * np.abs(r.alpha).max()))
+        assert np.all(np.abs(b - r.beta) <= 1e-5 * np.abs(r.beta))
     assert abs(mu_gpu[0] - mu_orc[0]) <= 1e-2 * np.sqrt(mu_orc[1])
     assert abs(mu_gpu[1] - mu_orc[1]) <= 1e-2 * mu_orc[1]
     assert abs(n1[0] - n2[0]) <= 2e-2 * scale and abs(n1[-1] - n2[-1]) <= 2e-2 * scale
 
 
-def test_c3_parity_batch():
-    _case("c3_parity")
+@pytest.mark.parametrize("numerics", ["fp64", "fp64_oz"])
+def test_c3_parity_batch(numerics):
+    """fp64: DMMA; fp64_oz: the c3 GEMMs (>= 1e9 M N K) on the tcgen05 INT8 Ozaki path.  (The
+    fp32-faithful BF16X3 mode misses even the bf16 gates here -- HVP 7.1e-2, mu2 9%, extreme Ritz
+    2.6% on B200 -- because Theorem 1's round-off floor u ||g|| / (eps ||Hv||) is large on c3;
+    DESIGN.md "Numerics".)"""
+    _case("c3_parity", numerics)
 
 
 @pytest.mark.skipif(os.environ.get("SLQ_LARGE_TESTS") != "1", reason="set SLQ_LARGE_TESTS=1 (~60 GB host RAM)")
