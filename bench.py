@@ -1,18 +1,20 @@
 #!/usr/bin/env python
 """Benchmark of the SLQ / FD-HVP hot path (arXiv 2602.00816) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c2|...]
 
-Workload (BASELINE.json configs[1], "c2"): GPT 4 layers, d 256, 4 heads, MLP 1024 GELU, LayerNorm,
-learned positions, vocab 4096, 5,322,240 fp32 params (N(0, 0.02^2) init); global batch 8 x 256
-Zipf(1.1) tokens; FD step eps = 1e-3; Lanczos m = 64 with full reorthogonalisation.  A "step" is
-one Lanczos iteration = one FD-HVP (perturb + two gradient passes + FD difference) + the
-recurrence + CGS2 reorthogonalisation, i.e. every SURVEY §8(a) row.  K steps run as
-ceil(K / 64) probes of <= 64 steps (the config's m), probe seeds 3200 + j.
+Default workload: BASELINE.json configs[1] ("c2"): GPT 4 layers, d 256, 4 heads, MLP 1024 GELU,
+LayerNorm, learned positions, vocab 4096, 5,322,240 fp32 params; global batch 8 x 256 Zipf(1.1)
+tokens split across ranks (strong scaling); eps = 1e-3; Lanczos m = 64 with full
+reorthogonalisation; pass numerics FP64_OZ (fp64 passes, head GEMMs as exact int8 digit products
+on tcgen05, the rest on DMMA).  `--config c3` gives the GPT-2-small line (8 x 1024 tokens PER GPU:
+weak scaling; its oracle legs use a bounded, token-extrapolated sample).
 
-metric = HVPs/sec (= Lanczos steps/s, whole job).  With N > 1 (torchrun), the 8 sequences are
-split across ranks and theta / every P-vector is FSDP-sharded (strong scaling); each rank's
-CUDA-event time is max-reduced.
+A "step" is one Lanczos iteration = one FD-HVP (perturb + two gradient passes + FD difference) +
+the recurrence + CGS2 reorthogonalisation, i.e. every SURVEY §8(a) row.  K steps run as probes of
+<= m steps.  metric = HVPs/sec, whole job: for the weak-scaling configs one unit is an HVP over one
+GPU's batch (value = N / T_step); for c2 one unit is the HVP over the fixed global batch.  Each
+rank's CUDA-event time is max-reduced.
 """
 from __future__ import annotations
 
@@ -32,8 +34,15 @@ sys.path.insert(0, ROOT)
 
 import slq_inputs as si  # noqa: E402
 
-METRIC = "HVPs/sec (FD-HVP Lanczos steps/s, c2, m=64 full reorth)"
 UNIT = "HVP/s"
+WEAK = {"c3": 8, "c4": 4, "c5": 2}  # sequences per GPU (BASELINE "batch B/GPU")
+
+
+def metric_name(cfg_name: str) -> str:
+    if cfg_name in WEAK:
+        return (f"HVPs/sec (FD-HVP Lanczos steps/s x N; unit = an HVP over one GPU's {WEAK[cfg_name]} x "
+                f"seq batch; {cfg_name}, full reorth)")
+    return f"HVPs/sec (FD-HVP Lanczos steps/s over the global batch; {cfg_name})"
 
 
 def parse():
@@ -56,6 +65,11 @@ def dist_env():
 
 
 def split_batch(cfg, rank, world):
+    """Weak-scaling configs: rank r holds sequences [r B, (r + 1) B) of the data stream (B per GPU);
+    otherwise the config's global batch is split across ranks."""
+    if cfg.name in WEAK:
+        b = WEAK[cfg.name]
+        return si.tokens(cfg, n_seq=b, first_seq=rank * b), b * world
     tok = si.tokens(cfg)
     n = tok.shape[0]
     return tok[si.rank_slice(n, rank, world)], n
@@ -113,11 +127,23 @@ def ncu_traffic(kernel_class: str):
         return None
 
 
+def oracle_sample(cfg):
+    """(tokens, scale): the oracle's bounded sample of one HVP unit and the linear-in-tokens factor
+    that converts sample HVPs/s into unit HVPs/s.  c2: the full global batch (factor 1); weak-
+    scaling configs: 1 sequence truncated to 128 tokens of the 8 x 1024 per-GPU unit."""
+    if cfg.name in WEAK:
+        t = 32
+        tok = si.tokens(cfg, n_seq=1)[:, :t + 1]
+        return tok, t / float(WEAK[cfg.name] * cfg.seq_len)
+    return si.tokens(cfg), 1.0
+
+
 def cpu_baseline(cfg, budget_s=12.0):
-    """The oracle, as it stands, timed on this host: exact-mode FD-HVPs at the full c2 batch."""
+    """The oracle, as it stands, timed on this host: exact-mode FD-HVPs on a bounded sample."""
     from oracle import fdhvp, probe
     th = si.init_params(cfg)
-    g = fdhvp.make_grad_fn(cfg, si.tokens(cfg))
+    tok, scale = oracle_sample(cfg)
+    g = fdhvp.make_grad_fn(cfg, tok)
     q = probe.rademacher_probe(cfg.probe_seed0, th.size)
     n = 0
     t0 = time.perf_counter()
@@ -127,9 +153,12 @@ def cpu_baseline(cfg, budget_s=12.0):
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"{n} oracle FD-HVPs (fp64 numpy, 2 gradient passes each) on the full c2 batch "
-                      f"(8 x 256 tokens), {dt:.1f} s; the recurrence/reorth is <1% and excluded"}
+    what = (f"{n} oracle FD-HVPs (fp64 numpy, 2 gradient passes each) on {tok.shape[0]} x {tok.shape[1] - 1} "
+            f"tokens, {dt:.1f} s")
+    if scale != 1.0:
+        what += f"; scaled to the {cfg.name} unit by linear-in-tokens extrapolation (x {scale:.4g})"
+    return {"value": n / dt * scale, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": what + "; the recurrence/reorth is <1% and excluded"}
 
 
 def run_reference(args, cfg):
@@ -138,26 +167,33 @@ def run_reference(args, cfg):
         return
     from oracle import fdhvp, lanczos as OL, probe
     th = si.init_params(cfg)
-    g = fdhvp.make_grad_fn(cfg, si.tokens(cfg))
+    tok, scale = oracle_sample(cfg)
+    g = fdhvp.make_grad_fn(cfg, tok)
     op = lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact")
-    OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + 99, th.size), max(args.warmup, 1), "full")
+    # the weak-scaling configs' basis (m x P fp64: 99 GB on c3) does not fit a host: the reference
+    # step there is the FD-HVP + three-term recurrence without a stored basis
+    reorth = "none" if cfg.name in WEAK else "full"
+    OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + 99, th.size), max(args.warmup, 1), reorth)
     t0 = time.perf_counter()
     done = 0
     j = 0
     while done < args.steps:
         m = min(cfg.m, args.steps - done)
-        OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + j, th.size), m, "full")
+        OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + j, th.size), m, reorth)
         done += m
         j += 1
     dt = time.perf_counter() - t0
-    v = args.steps / dt
+    v = args.steps / dt * scale
+    what = (f"{args.steps} oracle Lanczos steps ({reorth} reorth) on {tok.shape[0]} x {tok.shape[1] - 1} tokens"
+            + ("" if scale == 1.0 else f", scaled to the {cfg.name} unit by linear-in-tokens extrapolation "
+                                       f"(x {scale:.4g})"))
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
+        "impl": "reference", "metric": metric_name(cfg.name), "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps / scale,
+        "higher_is_better": True, "scaling": "weak" if cfg.name in WEAK else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c2 (oracle, CPU)", "global_batch": cfg.n_seq, "seq_len": cfg.seq_len},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                         "sample": f"{args.steps} oracle Lanczos steps (full reorth) on the full c2 batch"},
+        "config": {"workload": f"{cfg.name} (oracle, CPU)", "global_batch": cfg.n_seq, "seq_len": cfg.seq_len},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": what},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
 
 
@@ -309,26 +345,30 @@ def main():
     roof["launches_per_step"] = st["launches"] / args.steps
     roof["traffic"] = ncu_traffic(dom)
 
-    value = 1000.0 / ms_step * 1.0  # one global HVP per step, whole job
+    units = world if cfg.name in WEAK else 1  # HVP units per step, whole job
+    value = 1000.0 / ms_step * units
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "metric": metric_name(cfg.name), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if cfg.name in WEAK else "strong",
         "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": f"f64 (dense GEMMs with M*N*K >= {float(os.environ.get('SLQ_OZ_MIN_MNK', '1e9')):.0e} as exact int8 digit products on tcgen05, S={os.environ.get('SLQ_OZ_SLICES', '7')}; the rest fp64 DMMA)", "fp32": "f32", "bf16x3": "bf16x3", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {'GPT' if cfg.arch == si.ARCH_GPT else 'Llama'} {cfg.n_layers}L "
                                f"d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} V{cfg.vocab}, {si.n_params(cfg)} params "
-                               f"({'bf16' if cfg.param_bf16 else 'fp32'}), {cfg.n_seq}x{cfg.seq_len} Zipf(1.1) "
-                               f"tokens, eps={cfg.eps}, Lanczos m={cfg.m} "
+                               f"({'bf16' if cfg.param_bf16 else 'fp32'}), "
+                               + (f"{WEAK[cfg.name]}x{cfg.seq_len} Zipf(1.1) tokens per GPU" if cfg.name in WEAK
+                                  else f"{cfg.n_seq}x{cfg.seq_len} Zipf(1.1) tokens in total")
+                               + f", eps={cfg.eps}, Lanczos m={cfg.m} "
                                f"{'full CGS2 reorth' if cfg.reorth_full else 'no reorth'}",
-                   "global_batch": cfg.n_seq, "seq_len": cfg.seq_len, "parallelism": f"fsdp{world}",
+                   "global_batch": n_glob, "seq_len": cfg.seq_len, "parallelism": f"fsdp{world}",
                    "pass_numerics": args.numerics, "perturb": "exact",
                    "l2": "no flush: per-step working set (theta+-, g+- fp64, activations, basis) > 0.5 GB > 126 MB L2"},
         "s_per_lanczos_step": ms_step / 1000.0,
-        "hvp_per_s_standalone": 1000.0 / hvp_ms,
+        "hvp_per_s_standalone": 1000.0 / hvp_ms * units,
         "grad_step_ms": grad_ms,
         "hvp_over_grad": hvp_ms / grad_ms,
-        "e2e": {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 4 * P_loc,
-                "d2h_bytes_per_step": 4 * P_loc,
+        "e2e": {"value": 1000.0 / e2e_ms * units, "unit": UNIT, "h2d_bytes_per_step": 4 * P_loc * world,
+                "d2h_bytes_per_step": 4 * P_loc * world,
                 "what": "slq_hvp with pinned host v and host out (copies inside the call) per step"},
         "gpu_launches": launches,
         "kernel_ms_per_step": {k: s["ms"] / args.steps for k, s in stats.items() if s["launches"]},
