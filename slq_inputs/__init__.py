@@ -121,6 +121,12 @@ CONFIGS: Dict[str, ModelDesc] = {
                          n_kv_heads=8, d_ff=14336, vocab=128256, seq_len=512, n_seq=1,
                          rope_theta=500000.0, param_bf16=True, eps=1e-3, m=2, probes=1,
                          reorth_full=False, init_seed=1005, data_seed=2005, probe_seed0=3500),
+    # GEMM-shape evidence only (not a c5 step): every Llama-3-8B layer shape at c5's per-GPU batch
+    # (2 x 2048 tokens) on 2 of the 32 blocks
+    "c5_gemm": ModelDesc(name="c5_gemm", arch=ARCH_LLAMA, n_layers=2, d_model=4096, n_heads=32,
+                         n_kv_heads=8, d_ff=14336, vocab=128256, seq_len=2048, n_seq=2,
+                         rope_theta=500000.0, param_bf16=True, eps=1e-3, m=8, probes=1,
+                         reorth_full=False, init_seed=1005, data_seed=2005, probe_seed0=3500),
     "mlp_tiny": ModelDesc(name="mlp_tiny", arch=ARCH_MLP, d_in=7, d_hidden=9, n_classes=4,
                           n_rows=13, eps=1e-3, m=8, probes=1, init_seed=41, data_seed=42,
                           probe_seed0=43),
