@@ -30,6 +30,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
   const int bytes = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
 }
+// 16-byte variant: copies `bytes` (0, 8 or 16) and zero-fills the rest of the 16-byte destination
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -75,27 +80,58 @@ __global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : 1) gemm_
   if (p.tri == TRI_K_GE_M) kb = max(kb, m0);
   const int nk = kb < ke ? (ke - kb + BK - 1) / BK : 0;
 
+  // 16-byte copies of element pairs along each operand's contiguous axis when the global strides
+  // and bases allow it (pairs are aligned and a pair's validity is a prefix: first, or both)
+  const bool vecA = AK ? ((p.sAm % 2) == 0 && ((uintptr_t)A % 16) == 0)
+                       : ((p.sAk % 2) == 0 && ((uintptr_t)A % 16) == 0);
+  const bool vecB = BKm ? ((p.sBn % 2) == 0 && ((uintptr_t)B % 16) == 0)
+                        : ((p.sBk % 2) == 0 && ((uintptr_t)B % 16) == 0);
   auto load_tile = [&](int kt, int stage) {
     double* As = smem + stage * SM::STAGE;
     double* Bs = As + SM::A_ELEMS;
     const int k0 = kb + kt * BK;
+    if (vecA) {
 #pragma unroll
-    for (int i = tid; i < BM * BK; i += TL::THREADS) {
-      int m, k;
-      if (AK) { m = i / BK; k = i % BK; } else { m = i % BM; k = i / BM; }
-      const int gm = m0 + m, gk = k0 + k;
-      const bool ok = gm < p.M && gk < ke;
-      const double* src = ok ? A + (int64_t)gm * p.sAm + (int64_t)gk * p.sAk : A;
-      cp_async8(AK ? &As[m * SM::LDA + k] : &As[k * SM::LDA + m], src, ok);
+      for (int i = tid; i < BM * BK / 2; i += TL::THREADS) {
+        int m, k;
+        if (AK) { m = i / (BK / 2); k = 2 * (i % (BK / 2)); } else { m = 2 * (i % (BM / 2)); k = i / (BM / 2); }
+        const int gm = m0 + m, gk = k0 + k;
+        // elements (gm, gk) and the next along the contiguous axis
+        const int n_ok = AK ? (gm < p.M ? max(0, min(2, ke - gk)) : 0) : (gk < ke ? max(0, min(2, p.M - gm)) : 0);
+        const double* src = n_ok ? A + (int64_t)gm * p.sAm + (int64_t)gk * p.sAk : A;
+        cp_async16(AK ? &As[m * SM::LDA + k] : &As[k * SM::LDA + m], src, 8 * n_ok);
+      }
+    } else {
+#pragma unroll
+      for (int i = tid; i < BM * BK; i += TL::THREADS) {
+        int m, k;
+        if (AK) { m = i / BK; k = i % BK; } else { m = i % BM; k = i / BM; }
+        const int gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < ke;
+        const double* src = ok ? A + (int64_t)gm * p.sAm + (int64_t)gk * p.sAk : A;
+        cp_async8(AK ? &As[m * SM::LDA + k] : &As[k * SM::LDA + m], src, ok);
+      }
     }
+    if (vecB) {
 #pragma unroll
-    for (int i = tid; i < BN * BK; i += TL::THREADS) {
-      int n, k;
-      if (BKm) { n = i / BK; k = i % BK; } else { n = i % BN; k = i / BN; }
-      const int gn = n0 + n, gk = k0 + k;
-      const bool ok = gn < p.N && gk < ke;
-      const double* src = ok ? B + (int64_t)gk * p.sBk + (int64_t)gn * p.sBn : B;
-      cp_async8(BKm ? &Bs[n * SM::LDB + k] : &Bs[k * SM::LDB + n], src, ok);
+      for (int i = tid; i < BN * BK / 2; i += TL::THREADS) {
+        int n, k;
+        if (BKm) { n = i / (BK / 2); k = 2 * (i % (BK / 2)); } else { n = 2 * (i % (BN / 2)); k = i / (BN / 2); }
+        const int gn = n0 + n, gk = k0 + k;
+        const int n_ok = BKm ? (gn < p.N ? max(0, min(2, ke - gk)) : 0) : (gk < ke ? max(0, min(2, p.N - gn)) : 0);
+        const double* src = n_ok ? B + (int64_t)gk * p.sBk + (int64_t)gn * p.sBn : B;
+        cp_async16(BKm ? &Bs[n * SM::LDB + k] : &Bs[k * SM::LDB + n], src, 8 * n_ok);
+      }
+    } else {
+#pragma unroll
+      for (int i = tid; i < BN * BK; i += TL::THREADS) {
+        int n, k;
+        if (BKm) { n = i / BK; k = i % BK; } else { n = i % BN; k = i / BN; }
+        const int gn = n0 + n, gk = k0 + k;
+        const bool ok = gn < p.N && gk < ke;
+        const double* src = ok ? B + (int64_t)gk * p.sBk + (int64_t)gn * p.sBn : B;
+        cp_async8(BKm ? &Bs[n * SM::LDB + k] : &Bs[k * SM::LDB + n], src, ok);
+      }
     }
   };
 
