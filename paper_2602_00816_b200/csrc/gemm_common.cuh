@@ -61,6 +61,43 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs<T>& p, T* C, int m
     *dst = out;
 }
 
+// two consecutive columns (n, n + 1) of row m; `vec`: every row pitch involved is even and every
+// base 16-byte aligned, so the pair is one 16-byte access per array
+__device__ __forceinline__ double epi_act(const GemmArgs<double>& p, double v, double aux) {
+  switch (p.act) {
+    case ACT_GELU: return gelu_tanh(v);
+    case ACT_TANH: return dtanh_(v);
+    case ACT_DGELU: return v * gelu_tanh_grad(aux);
+    case ACT_DTANH: return v * (1.0 - aux * aux);
+    default: return v;
+  }
+}
+__device__ __forceinline__ void epilogue_store2(const GemmArgs<double>& p, double* C, int m, int n, double a0,
+                                                double a1, bool vec) {
+  const int64_t m64 = m;
+  double2 b = make_double2(0.0, 0.0), r = b, x = b, c = b;
+  if (vec) {
+    if (p.bias) b = *reinterpret_cast<const double2*>(p.bias + n);
+    if (p.resid) r = *reinterpret_cast<const double2*>(p.resid + m64 * p.ldr + n);
+    if (p.aux) x = *reinterpret_cast<const double2*>(p.aux + m64 * p.ldaux + n);
+    if (p.accumulate) c = *reinterpret_cast<const double2*>(C + m64 * p.ldc + n);
+  } else {
+    if (p.bias) b = make_double2(p.bias[n], p.bias[n + 1]);
+    if (p.resid) r = make_double2(p.resid[m64 * p.ldr + n], p.resid[m64 * p.ldr + n + 1]);
+    if (p.aux) x = make_double2(p.aux[m64 * p.ldaux + n], p.aux[m64 * p.ldaux + n + 1]);
+    if (p.accumulate) c = make_double2(C[m64 * p.ldc + n], C[m64 * p.ldc + n + 1]);
+  }
+  const double v0 = p.alpha * a0 + b.x + r.x, v1 = p.alpha * a1 + b.y + r.y;
+  if (p.act == ACT_GELU) {
+    if (vec) *reinterpret_cast<double2*>(p.C2 + m64 * p.ldc2 + n) = make_double2(v0, v1);
+    else { p.C2[m64 * p.ldc2 + n] = v0; p.C2[m64 * p.ldc2 + n + 1] = v1; }
+  }
+  double o0 = epi_act(p, v0, x.x), o1 = epi_act(p, v1, x.y);
+  if (p.accumulate) { o0 += c.x; o1 += c.y; }
+  if (vec) *reinterpret_cast<double2*>(C + m64 * p.ldc + n) = make_double2(o0, o1);
+  else { C[m64 * p.ldc + n] = o0; C[m64 * p.ldc + n + 1] = o1; }
+}
+
 template <class T>
 __global__ void splitk_reduce(GemmArgs<T> p, int splits, const T* __restrict__ ws) {
   const int64_t mn = (int64_t)p.M * p.N;

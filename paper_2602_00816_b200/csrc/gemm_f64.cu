@@ -192,15 +192,40 @@ __global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : 1) gemm_
   __syncthreads();
   double* C_ = splits > 1 ? ws + (int64_t)split * p.M * p.N : p.C + boff(p.offC, z);
   const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
+  // column pairs; 16-byte accesses when every pitch is even and every base 16-byte aligned
+  const int64_t ldo = splits > 1 ? p.N : p.ldc;
+  auto al = [](const void* q) { return ((uintptr_t)q & 15) == 0; };
+  const bool plain = splits > 1 || (!p.bias && !p.resid && !p.aux && !p.accumulate && p.act == ACT_NONE &&
+                                    p.alpha == 1.0);
+  const bool vec = (ldo % 2) == 0 && al(C_) && (!p.bias || al(p.bias)) &&
+                   (splits > 1 || ((!p.resid || ((p.ldr % 2) == 0 && al(p.resid))) &&
+                                   (!p.aux || ((p.ldaux % 2) == 0 && al(p.aux))) &&
+                                   (!p.C2 || ((p.ldc2 % 2) == 0 && al(p.C2)))));
+  if (plain) {
+#pragma unroll 4
+    for (int e = tid; e < BM * BN / 2; e += TL::THREADS) {
+      const int r = e / (BN / 2), c = 2 * (e % (BN / 2));
+      if (r >= rows || c >= cols) continue;
+      double* dst = C_ + (int64_t)(m0 + r) * ldo + n0 + c;
+      const double v0 = Cs[r * LDC + c], v1 = Cs[r * LDC + c + 1];
+      if (c + 1 < cols && vec) {
+        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+      } else {
+        dst[0] = v0;
+        if (c + 1 < cols) dst[1] = v1;
+      }
+    }
+    return;
+  }
 #pragma unroll 1
-  for (int e = tid; e < BM * BN; e += TL::THREADS) {
-    const int r = e / BN, c = e % BN;
+  for (int e = tid; e < BM * BN / 2; e += TL::THREADS) {
+    const int r = e / (BN / 2), c = 2 * (e % (BN / 2));
     if (r >= rows || c >= cols) continue;
-    const double v = Cs[r * LDC + c];
-    if (splits > 1)
-      C_[(int64_t)(m0 + r) * p.N + n0 + c] = v;
-    else
-      epilogue_store(p, C_, m0 + r, n0 + c, v);
+    if (c + 1 < cols) {
+      epilogue_store2(p, C_, m0 + r, n0 + c, Cs[r * LDC + c], Cs[r * LDC + c + 1], vec);
+    } else {
+      epilogue_store(p, C_, m0 + r, n0 + c, Cs[r * LDC + c]);
+    }
   }
 }
 
