@@ -333,6 +333,30 @@ int pick_variant(const GemmArgs<double>& a) {
   return a.N >= a.M ? 6 : 7;
 }
 
+// Per-shape plan for the dense (batch 1, non-causal) GEMMs, from the B200 sweep of every tile
+// variant x split count on the c2 shapes (tools/gemm_sweep2.py): 64 x 32 tiles with 8 warps and
+// no split for the N <= 256, K <= 1024 chain GEMMs (+50% on 2048 x 256 x 256); split-K 8 for
+// the token-contracting weight gradients; 32-wide tiles for 2048 x 1024 x 256.  Returns the
+// variant and sets *splits (0 = automatic).
+int plan_variant(const GemmArgs<double>& a, int* splits) {
+  *splits = 0;
+  const int fv = forced_variant();
+  if (fv >= 0 && fv < kVariants) return fv;
+  if (a.batch != 1 || a.tri != TRI_NONE) return pick_variant(a);
+  const double mn = (double)a.M * a.N;
+  if (a.K >= 2048) {
+    if (mn <= 65536.0) { *splits = 8; return 11; }    // 256 x 256
+    if (mn <= 200000.0) { *splits = 3; return 11; }   // 768 x 256
+    if (mn <= 300000.0) { *splits = 8; return 7; }    // 1024 x 256, 256 x 1024
+    if (mn <= 600000.0) { *splits = 8; return 0; }    // 2048 x 256
+    *splits = 4;
+    return 1;
+  }
+  if (a.N <= 256 && a.K <= 1024) { *splits = 1; return 11; }
+  if (a.N >= 1024 && a.N <= 2048 && a.K <= 256) { *splits = 1; return 6; }
+  return pick_variant(a);
+}
+
 void check(const GemmArgs<double>& a) {
   SLQ_CHECK_ARG(a.M >= 0 && a.N >= 0 && a.K >= 0 && a.batch >= 1, "gemm dims");
   SLQ_CHECK_ARG(a.sAk == 1 || a.sAm == 1, "gemm A layout");
@@ -371,7 +395,9 @@ void gemm<double>(const Launch& L, const GemmArgs<double>& a) {
     gemm_oz(L, a, oz_slices());
     return;
   }
-  run(L, a, pick_variant(a), 0);
+  int splits = 0;
+  const int v = plan_variant(a, &splits);
+  run(L, a, v, splits);
 }
 
 }  // namespace slq
@@ -402,7 +428,9 @@ extern "C" slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, in
     a.B = B; a.sBk = b_kmajor ? 1 : N; a.sBn = b_kmajor ? K : 1;
     a.C = C; a.ldc = N;
     // variant <= -4: the tcgen05 int8 Ozaki path with S = -variant digit planes
-    const int v = variant < 0 ? pick_variant(a) : variant;
+    int planned_splits = 0;
+    const int v = variant < 0 ? plan_variant(a, &planned_splits) : variant;
+    if (variant < 0 && splits == 0) splits = planned_splits;
     auto go = [&] {
       if (variant <= -4) gemm_oz(L, a, -variant);
       else run(L, a, v, splits);
