@@ -190,6 +190,9 @@ struct EngineT : Engine {
   __nv_bfloat16* basis16 = nullptr;
   float* qf[2] = {nullptr, nullptr};
   double* dscal;      // [0] sumsq, [1] beta_k, [2] loss, [3..] alpha / reorth coefficients
+  double* gram = nullptr;  // Gram matrix of the stored basis rows (two-pass CGS2), ldg x ldg
+  int ldg = 0;
+  bool cgs3 = getenv("SLQ_CGS_3PASS") != nullptr;  // the explicit three-pass CGS2 (diagnostic)
   double* partials;
   int* dflag;
   UnitDev* units_dev;
@@ -251,8 +254,12 @@ struct EngineT : Engine {
     } else {
       for (int i = 0; i < 3; ++i) vq[i] = dalloc<float>(n);
     }
-    dscal = dalloc<double>(8 + 2 * (int64_t)(max_steps + 1));
-    const int64_t np = std::max<int64_t>(vec_nblocks(n), (int64_t)reorth_nblocks(n) * (max_steps + 1));
+    dscal = dalloc<double>(8 + 4 * (int64_t)(max_steps + 1));
+    const int64_t np = std::max<int64_t>(vec_nblocks(n), (int64_t)reorth_nblocks(n) * 2 * (max_steps + 1));
+    if (d.reorth != SLQ_REORTH_NONE) {
+      ldg = d.reorth == SLQ_REORTH_FULL ? max_steps + 1 : d.reorth_window;
+      gram = dalloc<double>((int64_t)ldg * ldg);
+    }
     partials = dalloc<double>(np);
     dflag = dalloc<int>(1);
     {
@@ -528,18 +535,28 @@ struct EngineT : Engine {
     return info;
   }
 
-  // CGS over the `cnt` basis rows [0, cnt) (the window's ring holds exactly the last r vectors)
+  // CGS2 over the `cnt` basis rows [0, cnt) (the window's ring holds exactly the last r vectors).
+  // Two passes over the basis: (1) c1 = Q^T w together with the Gram row Q^T q_k of the newest
+  // vector, (2) w -= Q (c1 + c2) fused with ||w||^2, where c2 = c1 - G c1 is the second classical
+  // Gram-Schmidt pass's coefficient vector Q^T (w - Q c1) evaluated through the Gram matrix
+  // G = Q^T Q (equal in exact arithmetic).  SLQ_CGS_3PASS runs the explicit passes.
   template <class B>
-  void cgs2(const B* Q, int cnt, int kslot, double* d_coef, double* d_alpha_k) {
+  void cgs2(const B* Q, int cnt, int kslot, const float* qk, double* d_coef, double* d_alpha_k) {
     const int nb = reorth_nblocks(n);
-    // CGS pass 1 over the window (its coefficient on q_k is alpha_k)
-    reorth_dots<B>(L, Q, n, cnt, w, n, partials);
-    finish_reduce(nb, cnt, d_coef);
-    SLQ_CUDA(cudaMemcpyAsync(d_alpha_k, d_coef + kslot, sizeof(double), cudaMemcpyDeviceToDevice, L.stream));
-    // update of pass 1 fused with the partial dots of CGS pass 2
-    reorth_update<B>(L, Q, n, cnt, d_coef, w, n, partials, nullptr);
-    finish_reduce(nb, cnt, d_coef);
-    // update of pass 2 fused with ||w||^2
+    if (cgs3) {
+      reorth_dots<B>(L, Q, n, cnt, w, n, partials);
+      finish_reduce(nb, cnt, d_coef);
+      SLQ_CUDA(cudaMemcpyAsync(d_alpha_k, d_coef + kslot, sizeof(double), cudaMemcpyDeviceToDevice, L.stream));
+      reorth_update<B>(L, Q, n, cnt, d_coef, w, n, partials, nullptr);
+      finish_reduce(nb, cnt, d_coef);
+      reorth_update<B>(L, Q, n, cnt, d_coef, w, n, nullptr, partials);
+      finish_reduce(nb, 1, dscal + 0);
+      return;
+    }
+    double* d_cg = d_coef + (max_steps + 1);  // [2 cnt]
+    reorth_dots2<B>(L, Q, n, cnt, w, qk, n, partials);
+    finish_reduce(nb, 2 * cnt, d_cg);
+    gram_coef(L, d_cg, cnt, kslot, gram, ldg, d_coef, d_alpha_k);
     reorth_update<B>(L, Q, n, cnt, d_coef, w, n, nullptr, partials);
     finish_reduce(nb, 1, dscal + 0);
   }
@@ -558,8 +575,8 @@ struct EngineT : Engine {
     // fp32 view of q_k: the basis row itself (fp32 basis) or the exact working copy (bf16 basis)
     auto qvec = [&](int k) -> float* { return b16 ? qf[k % 2] : basis + (int64_t)slot(k) * n; };
     double* d_beta = dscal + 1;
-    double* d_coef = dscal + 8;                     // [max_steps + 1]
-    double* d_alpha = dscal + 8 + (max_steps + 1);  // [max_steps + 1]
+    double* d_coef = dscal + 8;                         // [max_steps + 1], then [2 (max_steps + 1)] dots
+    double* d_alpha = dscal + 8 + 3 * (max_steps + 1);  // [max_steps + 1]
     const double inv_sqrt_P = 1.0 / sqrt((double)plan.P);
     if (b16) {  // q_1 = bf16(s / sqrt(P)): signs first, one rounding from fp64
       probe_fill(L, qf[0], n, units_dev, (int)plan.units.size(), seed, 1.0);
@@ -576,9 +593,9 @@ struct EngineT : Engine {
       fd_w<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
       const int cnt = window ? std::min(k + 1, r) : k + 1;
       if (b16)
-        cgs2<__nv_bfloat16>(basis16, cnt, slot(k), d_coef, d_alpha + k);
+        cgs2<__nv_bfloat16>(basis16, cnt, slot(k), qk, d_coef, d_alpha + k);
       else
-        cgs2<float>(basis, cnt, slot(k), d_coef, d_alpha + k);
+        cgs2<float>(basis, cnt, slot(k), qk, d_coef, d_alpha + k);
       double h[2];
       to_host(d_alpha + k, 1, &h[0]);
       to_host(dscal + 0, 1, &h[1]);

@@ -178,6 +178,13 @@ void reorth_dots(const Launch& L, const B* Q, int64_t ldq, int k, const float* w
 template <class B>
 void reorth_update(const Launch& L, const B* Q, int64_t ldq, int k, const double* c, float* w,
                    int64_t n, double* part_dots, double* part_norm);
+// one pass over Q: partials [nb x 2k] of Q^T w (first k) and Q^T q (last k)
+template <class B>
+void reorth_dots2(const Launch& L, const B* Q, int64_t ldq, int k, const float* w, const float* q, int64_t n,
+                  double* partials);
+// Gram step of the two-pass CGS2: cg = [Q^T w | Q^T q_ks] (reduced); updates row/col ks of the Gram
+// matrix G (ldg), writes alpha = (Q^T w)[ks] and coef = c1 + (c1 - G c1)
+void gram_coef(const Launch& L, const double* cg, int k, int ks, double* G, int ldg, double* coef, double* alpha);
 // bf16 basis row + exact fp32 working copy: q = bf16(x / sqrt(*sumsq)), or bf16(x * mul) if sumsq == null
 void store_bf16(const Launch& L, const float* x, const double* sumsq, double mul, __nv_bfloat16* row, float* qf,
                 int64_t n);

@@ -346,6 +346,64 @@ __global__ void __launch_bounds__(kRThreads) k_reorth_update(const B* __restrict
   }
 }
 
+// partial c_j = Q[j, chunk] . w[chunk] and g_j = Q[j, chunk] . q[chunk] for all j < k (one pass
+// over Q for both; part rows hold [c_0 .. c_{k-1}, g_0 .. g_{k-1}])
+template <class B>
+__global__ void __launch_bounds__(kRThreads) k_reorth_dots2(const B* __restrict__ Q, int64_t ldq, int k,
+                                                            const float* __restrict__ w,
+                                                            const float* __restrict__ q, int64_t n,
+                                                            double* __restrict__ part) {
+  __shared__ __align__(16) float ws[kReorthChunk];
+  __shared__ __align__(16) float qs[kReorthChunk];
+  const int64_t base = (int64_t)blockIdx.x * kReorthChunk;
+  const int len = (int)(n - base < (int64_t)kReorthChunk ? n - base : (int64_t)kReorthChunk);
+  for (int i = threadIdx.x; i < len / 4; i += blockDim.x) {
+    reinterpret_cast<float4*>(ws)[i] = reinterpret_cast<const float4*>(w + base)[i];
+    reinterpret_cast<float4*>(qs)[i] = reinterpret_cast<const float4*>(q + base)[i];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int n4 = len / 4;
+  double* prow = part + (int64_t)blockIdx.x * 2 * k;
+  for (int j = warp; j < k; j += nw) {
+    const B* qr = Q + (int64_t)j * ldq + base;
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = lane; i < n4; i += 32) {
+      const float4 a = ld_q4(qr, i);
+      const float4 x = reinterpret_cast<const float4*>(ws)[i], y = reinterpret_cast<const float4*>(qs)[i];
+      s0 += (double)a.x * x.x + (double)a.y * x.y + (double)a.z * x.z + (double)a.w * x.w;
+      s1 += (double)a.x * y.x + (double)a.y * y.y + (double)a.z * y.z + (double)a.w * y.w;
+    }
+    s0 = warp_sum_d(s0);
+    s1 = warp_sum_d(s1);
+    if (lane == 0) {
+      prow[j] = s0;
+      prow[k + j] = s1;
+    }
+  }
+}
+
+// Gram step of the two-pass CGS2 (one block): with c1 = Q^T w and g = Q^T q_k (slot ks) from
+// k_reorth_dots2, set G[ks][.] = G[.][ks] = g, alpha = c1[ks], and coef = c1 + (c1 - G c1), the sum
+// of the two classical Gram-Schmidt passes' coefficients (the second pass's Q^T (w - Q c1) equals
+// c1 - G c1 in exact arithmetic), in a fixed summation order.
+__global__ void k_gram_coef(const double* __restrict__ cg, int k, int ks, double* __restrict__ G, int ldg,
+                            double* __restrict__ coef, double* __restrict__ alpha) {
+  extern __shared__ double c1s[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    c1s[j] = cg[j];
+    G[(int64_t)ks * ldg + j] = cg[k + j];
+    G[(int64_t)j * ldg + ks] = cg[k + j];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    double gc = 0.0;
+    for (int i = 0; i < k; ++i) gc += G[(int64_t)j * ldg + i] * c1s[i];
+    coef[j] = c1s[j] + (c1s[j] - gc);
+  }
+  if (threadIdx.x == 0) *alpha = c1s[ks];
+}
+
 // bf16 basis store (R19): q = bf16_RNE(x / sqrt(*sumsq)) (or x * mul when sumsq is
 // null: the probe), rounded once from fp64; the fp32 working copy holds the stored value exactly
 __global__ void k_store_bf16(const float* __restrict__ x, const double* __restrict__ sumsq, double mul,
@@ -519,6 +577,23 @@ void reorth_update(const Launch& L, const B* Q, int64_t ldq, int k, const double
   // algorithmic bytes: Q once from HBM (the fused dots re-read is the L2-resident chunk) + w r/w
   VLAUNCH(KC_REORTH, (part_dots ? 4.0 : 2.0) * k * n, (sizeof(B) * (double)k + 8.0) * n, reorth_nblocks(n),
           kRThreads, sizeof(double) * k, k_reorth_update<B>, Q, ldq, k, c, w, n, part_dots, part_norm);
+}
+
+template <class B>
+void reorth_dots2(const Launch& L, const B* Q, int64_t ldq, int k, const float* w, const float* q, int64_t n,
+                  double* part) {
+  SLQ_CHECK_ARG(n % 4 == 0 && ldq % 4 == 0, "reorth needs float4-aligned shards");
+  VLAUNCH(KC_REORTH, 4.0 * k * n, (sizeof(B) * (double)k + 8.0) * n, reorth_nblocks(n), kRThreads, 0,
+          k_reorth_dots2<B>, Q, ldq, k, w, q, n, part);
+}
+template void reorth_dots2<float>(const Launch&, const float*, int64_t, int, const float*, const float*, int64_t,
+                                  double*);
+template void reorth_dots2<__nv_bfloat16>(const Launch&, const __nv_bfloat16*, int64_t, int, const float*,
+                                          const float*, int64_t, double*);
+
+void gram_coef(const Launch& L, const double* cg, int k, int ks, double* G, int ldg, double* coef, double* alpha) {
+  VLAUNCH(KC_REORTH, 2.0 * k * k, 8.0 * k * k, 1, 128, sizeof(double) * k, k_gram_coef, cg, k, ks, G, ldg, coef,
+          alpha);
 }
 
 template void reorth_dots<float>(const Launch&, const float*, int64_t, int, const float*, int64_t, double*);
