@@ -254,7 +254,7 @@ struct EngineT : Engine {
     } else {
       for (int i = 0; i < 3; ++i) vq[i] = dalloc<float>(n);
     }
-    dscal = dalloc<double>(8 + 4 * (int64_t)(max_steps + 1));
+    dscal = dalloc<double>(8 + 5 * (int64_t)(max_steps + 1));
     const int64_t np = std::max<int64_t>(vec_nblocks(n), (int64_t)reorth_nblocks(n) * 2 * (max_steps + 1));
     if (d.reorth != SLQ_REORTH_NONE) {
       ldg = d.reorth == SLQ_REORTH_FULL ? max_steps + 1 : d.reorth_window;
@@ -269,7 +269,7 @@ struct EngineT : Engine {
       units_dev = dalloc<UnitDev>((int64_t)ud.size());
       SLQ_CUDA(cudaMemcpy(units_dev, ud.data(), sizeof(UnitDev) * ud.size(), cudaMemcpyHostToDevice));
     }
-    SLQ_CUDA(cudaMallocHost(&hstage, 64 * sizeof(double)));
+    SLQ_CUDA(cudaMallocHost(&hstage, (64 + 2 * (size_t)(max_steps + 1)) * sizeof(double)));
     paired_ = d.pass_numerics == SLQ_PASS_PAIRED || d.pass_numerics == SLQ_PASS_PAIRED_FP32;
     if (paired_ && comm) throw Error(SLQ_EUNSUPPORTED, "paired evaluation with world_size > 1 is not implemented");
     pe[0].reset(new PassExec<T>(d, plan, b, L, false, paired_));
@@ -577,6 +577,7 @@ struct EngineT : Engine {
     double* d_beta = dscal + 1;
     double* d_coef = dscal + 8;                         // [max_steps + 1], then [2 (max_steps + 1)] dots
     double* d_alpha = dscal + 8 + 3 * (max_steps + 1);  // [max_steps + 1]
+    double* d_bhist = dscal + 8 + 4 * (max_steps + 1);  // [max_steps + 1]: beta_{k+1}
     const double inv_sqrt_P = 1.0 / sqrt((double)plan.P);
     if (b16) {  // q_1 = bf16(s / sqrt(P)): signs first, one rounding from fp64
       probe_fill(L, qf[0], n, units_dev, (int)plan.units.size(), seed, 1.0);
@@ -596,11 +597,28 @@ struct EngineT : Engine {
         cgs2<__nv_bfloat16>(basis16, cnt, slot(k), qk, d_coef, d_alpha + k);
       else
         cgs2<float>(basis, cnt, slot(k), qk, d_coef, d_alpha + k);
-      double h[2];
-      to_host(d_alpha + k, 1, &h[0]);
-      to_host(dscal + 0, 1, &h[1]);
-      const double a = h[0], bnext = sqrt(std::max(h[1], 0.0));
-      if (!std::isfinite(a) || !std::isfinite(h[1])) {
+      // beta_{k+1} = ||w|| on the device (the next step's FD kernel reads it there); no host round
+      // trip inside the recurrence -- breakdown is detected after the loop (below)
+      step_beta(L, dscal + 0, d_beta, d_bhist + k);
+      if (k + 1 < m) {
+        if (b16)
+          store_bf16(L, w, dscal + 0, 0.0, basis16 + (int64_t)slot(k + 1) * n, qf[(k + 1) % 2], n);
+        else
+          scale_by_inv_sqrt(L, w, dscal + 0, qvec(k + 1), n);
+      }
+    }
+    std::vector<double> ha((size_t)m), hb((size_t)m);
+    double* ha_pin = hstage + 64;
+    double* hb_pin = hstage + 64 + (max_steps + 1);
+    SLQ_CUDA(cudaMemcpyAsync(ha_pin, d_alpha, sizeof(double) * m, cudaMemcpyDeviceToHost, L.stream));
+    SLQ_CUDA(cudaMemcpyAsync(hb_pin, d_bhist, sizeof(double) * m, cudaMemcpyDeviceToHost, L.stream));
+    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    memcpy(ha.data(), ha_pin, sizeof(double) * m);
+    memcpy(hb.data(), hb_pin, sizeof(double) * m);
+    // steps after a breakdown ran on a noise direction; they are discarded here
+    for (int k = 0; k < m; ++k) {
+      const double a = ha[k], bnext = hb[k];
+      if (!std::isfinite(a) || !std::isfinite(bnext)) {
         info.nonfinite = 1;
         info.m_done = k;
         last_info = info;
@@ -615,14 +633,6 @@ struct EngineT : Engine {
       if (k + 1 < m && bnext <= 1e-7 * tmax) {  // breakdown: invariant subspace (fp32 vectors)
         beta[k] = NAN;
         break;
-      }
-      if (k + 1 < m) {
-        if (b16)
-          store_bf16(L, w, dscal + 0, 0.0, basis16 + (int64_t)slot(k + 1) * n, qf[(k + 1) % 2], n);
-        else
-          scale_by_inv_sqrt(L, w, dscal + 0, qvec(k + 1), n);
-        SLQ_CUDA(cudaMemcpyAsync(d_beta, &bnext, sizeof(double), cudaMemcpyHostToDevice, L.stream));
-        SLQ_CUDA(cudaStreamSynchronize(L.stream));
       }
     }
     SLQ_CUDA(cudaStreamSynchronize(L.stream));

@@ -185,6 +185,8 @@ void reorth_dots2(const Launch& L, const B* Q, int64_t ldq, int k, const float* 
 // Gram step of the two-pass CGS2: cg = [Q^T w | Q^T q_ks] (reduced); updates row/col ks of the Gram
 // matrix G (ldg), writes alpha = (Q^T w)[ks] and coef = c1 + (c1 - G c1)
 void gram_coef(const Launch& L, const double* cg, int k, int ks, double* G, int ldg, double* coef, double* alpha);
+// *beta = *hist = sqrt(max(*sumsq, 0)) (device-side recurrence scalar)
+void step_beta(const Launch& L, const double* sumsq, double* beta, double* hist);
 // bf16 basis row + exact fp32 working copy: q = bf16(x / sqrt(*sumsq)), or bf16(x * mul) if sumsq == null
 void store_bf16(const Launch& L, const float* x, const double* sumsq, double mul, __nv_bfloat16* row, float* qf,
                 int64_t n);

@@ -404,6 +404,13 @@ __global__ void k_gram_coef(const double* __restrict__ cg, int k, int ks, double
   if (threadIdx.x == 0) *alpha = c1s[ks];
 }
 
+// beta_{k+1} = sqrt(||w||^2) into the recurrence's device scalar and the step history
+__global__ void k_step_beta(const double* __restrict__ sumsq, double* __restrict__ beta, double* __restrict__ hist) {
+  const double b = sqrt(fmax(*sumsq, 0.0));
+  *beta = b;
+  *hist = b;
+}
+
 // bf16 basis store (R19): q = bf16_RNE(x / sqrt(*sumsq)) (or x * mul when sumsq is
 // null: the probe), rounded once from fp64; the fp32 working copy holds the stored value exactly
 __global__ void k_store_bf16(const float* __restrict__ x, const double* __restrict__ sumsq, double mul,
@@ -590,6 +597,10 @@ template void reorth_dots2<float>(const Launch&, const float*, int64_t, int, con
                                   double*);
 template void reorth_dots2<__nv_bfloat16>(const Launch&, const __nv_bfloat16*, int64_t, int, const float*,
                                           const float*, int64_t, double*);
+
+void step_beta(const Launch& L, const double* sumsq, double* beta, double* hist) {
+  VLAUNCH(KC_VEC, 1.0, 24.0, 1, 1, 0, k_step_beta, sumsq, beta, hist);
+}
 
 void gram_coef(const Launch& L, const double* cg, int k, int ks, double* G, int ldg, double* coef, double* alpha) {
   VLAUNCH(KC_REORTH, 2.0 * k * k, 8.0 * k * k, 1, 128, sizeof(double) * k, k_gram_coef, cg, k, ks, G, ldg, coef,
