@@ -99,8 +99,10 @@ __global__ void k_pos_bwd(const T* __restrict__ dx, T* __restrict__ dwpe, int ns
   }
 }
 
-// one warp per row
-template <class T>
+// One warp per row.  V > 0: the row's values (D <= 32 V) are kept in registers across the passes
+// (one global read per operand instead of two or three); the summation order is the same as the
+// streaming V = 0 form, so both give identical results.
+template <class T, int V>
 __global__ void k_layernorm_fwd(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
                                 T* __restrict__ y, T* __restrict__ mean, T* __restrict__ rstd, int rows, int D,
                                 T eps) {
@@ -108,17 +110,45 @@ __global__ void k_layernorm_fwd(const T* __restrict__ x, const T* __restrict__ g
   const int lane = threadIdx.x % kWarp;
   if (row >= rows) return;
   const T* xr = x + (int64_t)row * D;
-  T s = T(0);
-  for (int c = lane; c < D; c += kWarp) s += xr[c];
-  const T mu = warp_sum(s) / T(D);
-  T v = T(0);
-  for (int c = lane; c < D; c += kWarp) {
-    const T d = xr[c] - mu;
-    v += d * d;
-  }
-  const T rs = T(1) / dsqrt(warp_sum(v) / T(D) + eps);
   T* yr = y + (int64_t)row * D;
-  for (int c = lane; c < D; c += kWarp) yr[c] = (xr[c] - mu) * rs * g[c] + b[c];
+  T mu, rs;
+  if constexpr (V > 0) {
+    T xv[V];
+    T s = T(0);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      xv[i] = c < D ? xr[c] : T(0);
+      if (c < D) s += xv[i];
+    }
+    mu = warp_sum(s) / T(D);
+    T v = T(0);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      if (c < D) {
+        const T d = xv[i] - mu;
+        v += d * d;
+      }
+    }
+    rs = T(1) / dsqrt(warp_sum(v) / T(D) + eps);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      if (c < D) yr[c] = (xv[i] - mu) * rs * g[c] + b[c];
+    }
+  } else {
+    T s = T(0);
+    for (int c = lane; c < D; c += kWarp) s += xr[c];
+    mu = warp_sum(s) / T(D);
+    T v = T(0);
+    for (int c = lane; c < D; c += kWarp) {
+      const T d = xr[c] - mu;
+      v += d * d;
+    }
+    rs = T(1) / dsqrt(warp_sum(v) / T(D) + eps);
+    for (int c = lane; c < D; c += kWarp) yr[c] = (xr[c] - mu) * rs * g[c] + b[c];
+  }
   if (lane == 0) {
     mean[row] = mu;
     rstd[row] = rs;
@@ -126,7 +156,7 @@ __global__ void k_layernorm_fwd(const T* __restrict__ x, const T* __restrict__ g
 }
 
 // dx = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)) (+ dres),  dxhat = dy * g
-template <class T>
+template <class T, int V>
 __global__ void k_layernorm_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ mean,
                                 const T* __restrict__ rstd, const T* __restrict__ g, const T* __restrict__ dres,
                                 T* __restrict__ dx, int rows, int D) {
@@ -135,41 +165,87 @@ __global__ void k_layernorm_bwd(const T* __restrict__ dy, const T* __restrict__ 
   if (row >= rows) return;
   const int64_t o = (int64_t)row * D;
   const T mu = mean[row], rs = rstd[row];
-  T s1 = T(0), s2 = T(0);
-  for (int c = lane; c < D; c += kWarp) {
-    const T dxh = dy[o + c] * g[c];
-    const T xh = (x[o + c] - mu) * rs;
-    s1 += dxh;
-    s2 += dxh * xh;
-  }
-  s1 = warp_sum(s1) / T(D);
-  s2 = warp_sum(s2) / T(D);
-  for (int c = lane; c < D; c += kWarp) {
-    const T dxh = dy[o + c] * g[c];
-    const T xh = (x[o + c] - mu) * rs;
-    T v = rs * (dxh - s1 - xh * s2);
-    if (dres) v += dres[o + c];
-    dx[o + c] = v;
+  if constexpr (V > 0) {
+    T dh[V], xh[V];
+    T s1 = T(0), s2 = T(0);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      if (c < D) {
+        dh[i] = dy[o + c] * g[c];
+        xh[i] = (x[o + c] - mu) * rs;
+        s1 += dh[i];
+        s2 += dh[i] * xh[i];
+      } else {
+        dh[i] = xh[i] = T(0);
+      }
+    }
+    s1 = warp_sum(s1) / T(D);
+    s2 = warp_sum(s2) / T(D);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      if (c < D) {
+        T v = rs * (dh[i] - s1 - xh[i] * s2);
+        if (dres) v += dres[o + c];
+        dx[o + c] = v;
+      }
+    }
+  } else {
+    T s1 = T(0), s2 = T(0);
+    for (int c = lane; c < D; c += kWarp) {
+      const T dxh = dy[o + c] * g[c];
+      const T xh = (x[o + c] - mu) * rs;
+      s1 += dxh;
+      s2 += dxh * xh;
+    }
+    s1 = warp_sum(s1) / T(D);
+    s2 = warp_sum(s2) / T(D);
+    for (int c = lane; c < D; c += kWarp) {
+      const T dxh = dy[o + c] * g[c];
+      const T xh = (x[o + c] - mu) * rs;
+      T v = rs * (dxh - s1 - xh * s2);
+      if (dres) v += dres[o + c];
+      dx[o + c] = v;
+    }
   }
 }
 
-template <class T>
+template <class T, int V>
 __global__ void k_rmsnorm_fwd(const T* __restrict__ x, const T* __restrict__ g, T* __restrict__ y,
                               T* __restrict__ rstd, int rows, int D, T eps) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
   const int lane = threadIdx.x % kWarp;
   if (row >= rows) return;
   const T* xr = x + (int64_t)row * D;
-  T s = T(0);
-  for (int c = lane; c < D; c += kWarp) s += xr[c] * xr[c];
-  const T r = T(1) / dsqrt(warp_sum(s) / T(D) + eps);
   T* yr = y + (int64_t)row * D;
-  for (int c = lane; c < D; c += kWarp) yr[c] = xr[c] * r * g[c];
+  T r;
+  if constexpr (V > 0) {
+    T xv[V];
+    T s = T(0);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      xv[i] = c < D ? xr[c] : T(0);
+      if (c < D) s += xv[i] * xv[i];
+    }
+    r = T(1) / dsqrt(warp_sum(s) / T(D) + eps);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      if (c < D) yr[c] = xv[i] * r * g[c];
+    }
+  } else {
+    T s = T(0);
+    for (int c = lane; c < D; c += kWarp) s += xr[c] * xr[c];
+    r = T(1) / dsqrt(warp_sum(s) / T(D) + eps);
+    for (int c = lane; c < D; c += kWarp) yr[c] = xr[c] * r * g[c];
+  }
   if (lane == 0) rstd[row] = r;
 }
 
 // dx = r * dxhat - x * r^3 * mean(dxhat * x) (+ dres)
-template <class T>
+template <class T, int V>
 __global__ void k_rmsnorm_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ rstd,
                               const T* __restrict__ g, const T* __restrict__ dres, T* __restrict__ dx, int rows,
                               int D) {
@@ -178,13 +254,39 @@ __global__ void k_rmsnorm_bwd(const T* __restrict__ dy, const T* __restrict__ x,
   if (row >= rows) return;
   const int64_t o = (int64_t)row * D;
   const T r = rstd[row];
-  T s = T(0);
-  for (int c = lane; c < D; c += kWarp) s += dy[o + c] * g[c] * x[o + c];
-  s = warp_sum(s) / T(D);
-  for (int c = lane; c < D; c += kWarp) {
-    T v = r * dy[o + c] * g[c] - x[o + c] * r * r * r * s;
-    if (dres) v += dres[o + c];
-    dx[o + c] = v;
+  if constexpr (V > 0) {
+    T dv[V], xv[V];
+    T s = T(0);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      if (c < D) {
+        dv[i] = dy[o + c] * g[c];
+        xv[i] = x[o + c];
+        s += dv[i] * xv[i];
+      } else {
+        dv[i] = xv[i] = T(0);
+      }
+    }
+    s = warp_sum(s) / T(D);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = lane + kWarp * i;
+      if (c < D) {
+        T v = r * dv[i] - xv[i] * r * r * r * s;
+        if (dres) v += dres[o + c];
+        dx[o + c] = v;
+      }
+    }
+  } else {
+    T s = T(0);
+    for (int c = lane; c < D; c += kWarp) s += dy[o + c] * g[c] * x[o + c];
+    s = warp_sum(s) / T(D);
+    for (int c = lane; c < D; c += kWarp) {
+      T v = r * dy[o + c] * g[c] - x[o + c] * r * r * r * s;
+      if (dres) v += dres[o + c];
+      dx[o + c] = v;
+    }
   }
 }
 
@@ -415,24 +517,44 @@ template <class T>
 void layernorm_fwd(const Launch& L, const T* x, const T* g, const T* b, T* y, T* mean, T* rstd, int rows, int D,
                    double eps) {
   if (rows == 0) return;
-  LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_layernorm_fwd<T>, x, g, b, y, mean, rstd, rows, D, (T)eps);
+  if (D <= 256)
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_fwd<T, 8>), x, g, b, y, mean, rstd, rows, D, (T)eps);
+  else if (D <= 768)
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_fwd<T, 24>), x, g, b, y, mean, rstd, rows, D, (T)eps);
+  else
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_fwd<T, 0>), x, g, b, y, mean, rstd, rows, D, (T)eps);
 }
 template <class T>
 void layernorm_bwd(const Launch& L, const T* dy, const T* x, const T* mean, const T* rstd, const T* g,
                    const T* dres, T* dx, int rows, int D) {
   if (rows == 0) return;
-  LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_layernorm_bwd<T>, dy, x, mean, rstd, g, dres, dx, rows, D);
+  if (D <= 256)
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_bwd<T, 8>), dy, x, mean, rstd, g, dres, dx, rows, D);
+  else if (D <= 768)
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_bwd<T, 24>), dy, x, mean, rstd, g, dres, dx, rows, D);
+  else
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_bwd<T, 0>), dy, x, mean, rstd, g, dres, dx, rows, D);
 }
 template <class T>
 void rmsnorm_fwd(const Launch& L, const T* x, const T* g, T* y, T* rstd, int rows, int D, double eps) {
   if (rows == 0) return;
-  LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_rmsnorm_fwd<T>, x, g, y, rstd, rows, D, (T)eps);
+  if (D <= 256)
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_rmsnorm_fwd<T, 8>), x, g, y, rstd, rows, D, (T)eps);
+  else if (D <= 768)
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_rmsnorm_fwd<T, 24>), x, g, y, rstd, rows, D, (T)eps);
+  else
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_rmsnorm_fwd<T, 0>), x, g, y, rstd, rows, D, (T)eps);
 }
 template <class T>
 void rmsnorm_bwd(const Launch& L, const T* dy, const T* x, const T* rstd, const T* g, const T* dres, T* dx,
                  int rows, int D) {
   if (rows == 0) return;
-  LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_rmsnorm_bwd<T>, dy, x, rstd, g, dres, dx, rows, D);
+  if (D <= 256)
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_rmsnorm_bwd<T, 8>), dy, x, rstd, g, dres, dx, rows, D);
+  else if (D <= 768)
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_rmsnorm_bwd<T, 24>), dy, x, rstd, g, dres, dx, rows, D);
+  else
+    LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_rmsnorm_bwd<T, 0>), dy, x, rstd, g, dres, dx, rows, D);
 }
 template <class T>
 void colreduce(const Launch& L, int mode, const T* dy, int64_t lddy, const T* x, const T* mean, const T* rstd,
