@@ -31,31 +31,113 @@ struct LocalIO : PassIO<T> {
 };
 
 // ZeRO-3: gather a unit's parameters before its forward and again before its backward; reduce-
-// scatter its gradient after its backward.  Unit 0 (embedding) has its own
-// parameter and gradient buffers so it can stay live with any other unit (tied head).
+// scatter its gradient after its backward.  Every NCCL call of a pass is issued on
+// ONE communication stream (so all ranks execute them in the same order), linked to the compute
+// stream by events: the runner's prefetch(u) hint starts unit u's all-gather into the free buffer
+// of a ping-pong pair while the current unit computes; grads_done(u) reduce-scatters from one of
+// two gradient buffers while the next unit's backward fills the other.  Unit 0 (embedding) has its
+// own parameter and gradient buffers so it can stay live with any other unit (tied head).
 template <class T>
 struct FsdpIO : PassIO<T> {
   const LayoutPlan* plan;
   Comm* comm;
-  cudaStream_t s;
+  cudaStream_t s = nullptr;   // compute stream
+  cudaStream_t cs = nullptr;  // communication stream
   const T* shard = nullptr;
   T* gshard = nullptr;
-  T *pbuf0, *pbuf1, *gbuf0, *gbuf1;
+  T *pbuf0, *gbuf0;
+  T *pb[2], *gb[2];
+  int holder[2] = {-1, -1};  // unit whose gather was issued into pb[i]
+  int cur = -1;              // pb index of the unit returned last
+  int gcur = 0;              // gb index for the next grads(u >= 1)
+  bool gather0 = false;      // unit 0 gather issued and not yet consumed
+  cudaEvent_t ev_main = nullptr, ev_ready[3] = {}, ev_gfree[3] = {}, ev_comm = nullptr;
+  bool gpending[3] = {false, false, false};
   CommType ct() const { return sizeof(T) == 8 ? COMM_F64 : COMM_F32; }
-  const T* params(int u) override {
-    const UnitPlan& up = plan->units[u];
-    T* dst = u == 0 ? pbuf0 : pbuf1;
-    comm->allgather(shard + up.local_offset, dst, (size_t)up.chunk, ct(), s);
-    return dst;
+  void init() {
+    SLQ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    SLQ_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
+    SLQ_CUDA(cudaEventCreateWithFlags(&ev_comm, cudaEventDisableTiming));
+    for (int i = 0; i < 3; ++i) {
+      SLQ_CUDA(cudaEventCreateWithFlags(&ev_ready[i], cudaEventDisableTiming));
+      SLQ_CUDA(cudaEventCreateWithFlags(&ev_gfree[i], cudaEventDisableTiming));
+    }
   }
-  T* grads(int u) override { return u == 0 ? gbuf0 : gbuf1; }
+  ~FsdpIO() {
+    if (cs) cudaStreamSynchronize(cs);
+    if (ev_main) cudaEventDestroy(ev_main);
+    if (ev_comm) cudaEventDestroy(ev_comm);
+    for (int i = 0; i < 3; ++i) {
+      if (ev_ready[i]) cudaEventDestroy(ev_ready[i]);
+      if (ev_gfree[i]) cudaEventDestroy(ev_gfree[i]);
+    }
+    if (cs) cudaStreamDestroy(cs);
+  }
+  void begin_pass() {
+    holder[0] = holder[1] = -1;
+    cur = -1;
+    gather0 = false;
+  }
+  // the comm stream waits for everything issued so far on the compute stream
+  void comm_after_main() {
+    SLQ_CUDA(cudaEventRecord(ev_main, s));
+    SLQ_CUDA(cudaStreamWaitEvent(cs, ev_main, 0));
+  }
+  void gather(int u, T* dst, cudaEvent_t done) {
+    const UnitPlan& up = plan->units[u];
+    comm_after_main();  // dst's previous contents are no longer read
+    comm->allgather(shard + up.local_offset, dst, (size_t)up.chunk, ct(), cs);
+    SLQ_CUDA(cudaEventRecord(done, cs));
+  }
+  void prefetch(int u) override {
+    if (u < 0 || u >= (int)plan->units.size()) return;
+    if (u == 0) {
+      if (!gather0) gather(0, pbuf0, ev_ready[2]);
+      gather0 = true;
+      return;
+    }
+    if (holder[0] == u || holder[1] == u) return;
+    const int i = cur == 0 ? 1 : 0;  // never the buffer of the unit in use
+    holder[i] = u;
+    gather(u, pb[i], ev_ready[i]);
+  }
+  const T* params(int u) override {
+    if (u == 0) {
+      prefetch(0);
+      gather0 = false;
+      SLQ_CUDA(cudaStreamWaitEvent(s, ev_ready[2], 0));
+      return pbuf0;
+    }
+    prefetch(u);
+    const int i = holder[0] == u ? 0 : 1;
+    SLQ_CUDA(cudaStreamWaitEvent(s, ev_ready[i], 0));
+    cur = i;
+    return pb[i];
+  }
+  T* grads(int u) override {
+    const int i = u == 0 ? 2 : gcur;
+    if (gpending[i]) SLQ_CUDA(cudaStreamWaitEvent(s, ev_gfree[i], 0));  // its reduce-scatter has read it
+    gpending[i] = false;
+    return u == 0 ? gbuf0 : gb[i];
+  }
   bool collective() const override { return true; }
   void grads_done(int u) override {
     const UnitPlan& up = plan->units[u];
-    T* g = u == 0 ? gbuf0 : gbuf1;
+    const int i = u == 0 ? 2 : gcur;
+    T* g = u == 0 ? gbuf0 : gb[i];
+    comm_after_main();
     if (up.padded > up.numel)
-      SLQ_CUDA(cudaMemsetAsync(g + up.numel, 0, sizeof(T) * (size_t)(up.padded - up.numel), s));
-    comm->reduce_scatter(g, gshard + up.local_offset, (size_t)up.chunk, ct(), s);
+      SLQ_CUDA(cudaMemsetAsync(g + up.numel, 0, sizeof(T) * (size_t)(up.padded - up.numel), cs));
+    comm->reduce_scatter(g, gshard + up.local_offset, (size_t)up.chunk, ct(), cs);
+    SLQ_CUDA(cudaEventRecord(ev_gfree[i], cs));
+    gpending[i] = true;
+    if (u != 0) gcur ^= 1;
+  }
+  // the compute stream waits for every collective of the pass (the reduce-scattered gradient)
+  void end_pass() {
+    SLQ_CUDA(cudaEventRecord(ev_comm, cs));
+    SLQ_CUDA(cudaStreamWaitEvent(s, ev_comm, 0));
+    gpending[0] = gpending[1] = gpending[2] = false;  // every buffer's reduce-scatter is behind us
   }
 };
 
@@ -119,7 +201,9 @@ struct PassExec {
     if (fio) {
       fio->shard = th;
       fio->gshard = g;
+      fio->begin_pass();
       runner->fwd_bwd(*fio, loss_dev);
+      fio->end_pass();
     } else {
       lio.shard = th;
       lio.gshard = g;
@@ -283,8 +367,11 @@ struct EngineT : Engine {
       for (const UnitPlan& u : plan.units) mx = std::max(mx, u.padded);
       fio.pbuf0 = dalloc<T>(plan.units[0].padded);
       fio.gbuf0 = dalloc<T>(plan.units[0].padded);
-      fio.pbuf1 = dalloc<T>(mx);
-      fio.gbuf1 = dalloc<T>(mx);
+      for (int i = 0; i < 2; ++i) {
+        fio.pb[i] = dalloc<T>(mx);
+        fio.gb[i] = dalloc<T>(mx);
+      }
+      fio.init();
       pe[0]->fio = &fio;
     } else if (getenv("SLQ_SERIAL_PASSES") == nullptr) {
       pe[1].reset(new PassExec<T>(d, plan, b, L, true));

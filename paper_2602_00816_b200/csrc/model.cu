@@ -357,11 +357,13 @@ struct GptRunner : Runner<T> {
     // ---------------- forward ----------------
     {
       const T* P0 = io.params(0);
+      io.prefetch(1);
       embed_fwd<T>(L, tok, Tn + 1, nseq, Tn, P0 + u0.t("wte").offset, P0 + u0.t("wpe").offset, xs[0], D);
     }
     for (int l = 0; l < Ly; ++l) {
       const UnitPlan& ub = plan->units[1 + l];
       const T* Pl = io.params(1 + l);
+      io.prefetch(l + 2);
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       Layer& a = ly[l];
       layernorm_fwd<T>(L, xs[l], w("ln1.g"), w("ln1.b"), a.h1, a.mean1, a.rstd1, N, D, eps);
@@ -373,7 +375,9 @@ struct GptRunner : Runner<T> {
       linear_fwd<T>(L, a.gu, F, w("mproj.w"), D, F, N, xs[l + 1], D, w("mproj.b"), a.x1, D);
     }
     const T* Pf = io.params(Ly + 1);
+    io.prefetch(tied ? 0 : Ly);
     const T* Whead = tied ? io.params(0) + u0.t("wte").offset : Pf + uf.t("head.w").offset;
+    if (tied) io.prefetch(Ly);
     layernorm_fwd<T>(L, xs[Ly], Pf + uf.t("lnf.g").offset, Pf + uf.t("lnf.b").offset, xf, meanf, rstdf, N, D, eps);
     linear_fwd<T>(L, xf, D, Whead, V, D, N, logits, V, (const T*)nullptr);
     cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
@@ -397,6 +401,7 @@ struct GptRunner : Runner<T> {
     for (int l = Ly - 1; l >= 0; --l) {
       const UnitPlan& ub = plan->units[1 + l];
       const T* Pl = io.params(1 + l);
+      if (l >= 1) io.prefetch(l);
       T* Gl = io.grads(1 + l);
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
@@ -531,11 +536,13 @@ struct LlamaRunner : Runner<T> {
     const int64_t HD = (int64_t)Hq * hd;
     {
       const T* P0 = io.params(0);
+      io.prefetch(1);
       embed_fwd<T>(L, tok, Tn + 1, nseq, Tn, P0 + u0.t("tok").offset, (const T*)nullptr, xs[0], D);
     }
     for (int l = 0; l < Ly; ++l) {
       const UnitPlan& ub = plan->units[1 + l];
       const T* Pl = io.params(1 + l);
+      io.prefetch(l + 2);
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       Layer& a = ly[l];
       rmsnorm_fwd<T>(L, xs[l], w("attn_norm"), a.h1, a.rstd1, N, D, eps);
@@ -552,7 +559,9 @@ struct LlamaRunner : Runner<T> {
       linear_fwd<T>(L, a.f, F, w("wd"), D, F, N, xs[l + 1], D, (const T*)nullptr, a.x1, D);
     }
     const T* Pf = io.params(Ly + 1);
+    io.prefetch(tied ? 0 : Ly);
     const T* Whead = tied ? io.params(0) + u0.t("tok").offset : Pf + uf.t("head.w").offset;
+    if (tied) io.prefetch(Ly);
     rmsnorm_fwd<T>(L, xs[Ly], Pf + uf.t("norm").offset, xf, rstdf, N, D, eps);
     linear_fwd<T>(L, xf, D, Whead, V, D, N, logits, V, (const T*)nullptr);
     cross_entropy<T>(L, logits, tok + 1, Tn + 1, Tn, loss_rows, N, V, 1.0 / ((double)nseq_glob * Tn));
@@ -573,6 +582,7 @@ struct LlamaRunner : Runner<T> {
     for (int l = Ly - 1; l >= 0; --l) {
       const UnitPlan& ub = plan->units[1 + l];
       const T* Pl = io.params(1 + l);
+      if (l >= 1) io.prefetch(l);
       T* Gl = io.grads(1 + l);
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };

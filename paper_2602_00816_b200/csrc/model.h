@@ -25,6 +25,9 @@ struct PassIO {
   // true when grads_done() starts a collective on the unit's gradient (FSDP reduce-scatter): the
   // runner must then finish the unit's side-stream gradient work first
   virtual bool collective() const { return false; }
+  // hint: unit u's parameters will be requested next (FSDP: start its all-gather now, overlapped
+  // with the compute of the current unit)
+  virtual void prefetch(int) {}
 };
 
 struct HostBatch {
