@@ -110,8 +110,21 @@ void tc_gemm_products(const Launch& L, const TcPlan& plan, int M, int N, int K, 
 template <class T> void convert_f32(const Launch& L, const float* x, T* y, int64_t n);
 template <class T> void embed_fwd(const Launch& L, const int32_t* tok, int tok_stride, int nseq, int T_,
                                   const T* wte, const T* wpe, T* x, int D);
-template <class T> void embed_bwd_rows(const Launch& L, const int32_t* csr_off, const int32_t* csr_pos,
-                                       const T* dx, T* dW, int V, int D, bool accumulate);
+// token positions grouped by vocabulary row (CSR), and each row's list cut into chunks of at most
+// kEmbedChunk positions: chunk c covers pos[cbeg[c] .. cbeg[c + 1]), row v owns chunks
+// [coff[v], coff[v + 1])
+constexpr int kEmbedChunk = 16;
+struct EmbedCSR {
+  const int32_t* off = nullptr;
+  const int32_t* pos = nullptr;
+  const int32_t* coff = nullptr;
+  const int32_t* cbeg = nullptr;
+  int nchunks = 0;
+};
+void build_embed_csr(const std::vector<int32_t>& tok, int nseq, int Tn, int V, std::vector<int32_t>& off,
+                     std::vector<int32_t>& pos, std::vector<int32_t>& coff, std::vector<int32_t>& cbeg);
+template <class T> void embed_bwd_rows(const Launch& L, const EmbedCSR& csr, const T* dx, T* dW, int V, int D,
+                                       bool accumulate);
 template <class T> void pos_bwd(const Launch& L, const T* dx, T* dwpe, int nseq, int T_, int D);
 template <class T> void layernorm_fwd(const Launch& L, const T* x, const T* g, const T* b, T* y, T* mean,
                                       T* rstd, int rows, int D, double eps);

@@ -66,24 +66,36 @@ __global__ void k_embed_fwd(const int32_t* __restrict__ tok, int tok_stride, int
 }
 
 // dW[v, :] (+)= sum over the rows listed for token v (CSR built once at init; fixed order)
+// Embedding backward, stage 1: partial[c][col] = sum of dx rows over the <= kEmbedChunk token
+// positions of chunk c (fixed order).  Stage 2: dW[v][col] (+)= sum of row v's chunk partials in
+// chunk order.  Splitting the long token lists of frequent tokens (Zipf: the top token is ~14% of
+// all positions) keeps every thread's dependent-load chain short.
 template <class T>
-__global__ void k_embed_bwd_rows(const int32_t* __restrict__ off, const int32_t* __restrict__ pos,
-                                 const T* __restrict__ dx, T* __restrict__ dW, int V, int D, bool accumulate) {
-  // one thread per (v, c); 4 independent partial sums over the token's rows (fixed order)
+__global__ void k_embed_bwd_chunks(const int32_t* __restrict__ pos, const int32_t* __restrict__ cbeg, int nchunks,
+                                   const T* __restrict__ dx, T* __restrict__ part, int D) {
+  const int64_t total = (int64_t)nchunks * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / D), col = (int)(i % D);
+    const int s = cbeg[c], e = cbeg[c + 1];
+    int p[kEmbedChunk];
+#pragma unroll
+    for (int j = 0; j < kEmbedChunk; ++j) p[j] = s + j < e ? pos[s + j] : -1;
+    T acc = T(0);
+#pragma unroll
+    for (int j = 0; j < kEmbedChunk; ++j)
+      if (p[j] >= 0) acc += dx[(int64_t)p[j] * D + col];
+    part[i] = acc;
+  }
+}
+
+template <class T>
+__global__ void k_embed_bwd_rows(const int32_t* __restrict__ coff, const T* __restrict__ part, T* __restrict__ dW,
+                                 int V, int D, bool accumulate) {
   const int64_t total = (int64_t)V * D;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int v = (int)(i / D), c = (int)(i % D);
-    const int s = off[v], e = off[v + 1];
-    T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
-    int j = s;
-    for (; j + 3 < e; j += 4) {
-      a0 += dx[(int64_t)pos[j] * D + c];
-      a1 += dx[(int64_t)pos[j + 1] * D + c];
-      a2 += dx[(int64_t)pos[j + 2] * D + c];
-      a3 += dx[(int64_t)pos[j + 3] * D + c];
-    }
-    for (; j < e; ++j) a0 += dx[(int64_t)pos[j] * D + c];
-    const T acc = (a0 + a1) + (a2 + a3);
+    const int v = (int)(i / D), col = (int)(i % D);
+    T acc = T(0);
+    for (int c = coff[v]; c < coff[v + 1]; ++c) acc += part[(int64_t)c * D + col];
     T* dst = dW + i;
     *dst = accumulate ? *dst + acc : acc;
   }
@@ -504,10 +516,31 @@ void embed_fwd(const Launch& L, const int32_t* tok, int tok_stride, int nseq, in
   LAUNCH(KC_EMBED, grid_for(n, 256), 256, k_embed_fwd<T>, tok, tok_stride, nseq, Tn, wte, wpe, x, D);
 }
 template <class T>
-void embed_bwd_rows(const Launch& L, const int32_t* off, const int32_t* pos, const T* dx, T* dW, int V, int D,
-                    bool accumulate) {
-  LAUNCH(KC_EMBED, grid_for((int64_t)V * D, 256, 148 * 32), 256, k_embed_bwd_rows<T>, off, pos, dx, dW, V, D,
-         accumulate);
+void embed_bwd_rows(const Launch& L, const EmbedCSR& csr, const T* dx, T* dW, int V, int D, bool accumulate) {
+  T* part = (T*)L.ws->get(sizeof(T) * (size_t)std::max(csr.nchunks, 1) * D, L.stream);
+  if (csr.nchunks > 0)
+    LAUNCH(KC_EMBED, grid_for((int64_t)csr.nchunks * D, 256), 256, k_embed_bwd_chunks<T>, csr.pos, csr.cbeg,
+           csr.nchunks, dx, part, D);
+  LAUNCH(KC_EMBED, grid_for((int64_t)V * D, 256), 256, k_embed_bwd_rows<T>, csr.coff, part, dW, V, D, accumulate);
+}
+
+void build_embed_csr(const std::vector<int32_t>& tok, int nseq, int Tn, int V, std::vector<int32_t>& off,
+                     std::vector<int32_t>& pos, std::vector<int32_t>& coff, std::vector<int32_t>& cbeg) {
+  off.assign(V + 1, 0);
+  for (int b = 0; b < nseq; ++b)
+    for (int t = 0; t < Tn; ++t) off[tok[(size_t)b * (Tn + 1) + t] + 1]++;
+  for (int v = 0; v < V; ++v) off[v + 1] += off[v];
+  pos.assign((size_t)nseq * Tn, 0);
+  std::vector<int32_t> fill(off.begin(), off.end() - 1);
+  for (int b = 0; b < nseq; ++b)
+    for (int t = 0; t < Tn; ++t) pos[fill[tok[(size_t)b * (Tn + 1) + t]]++] = b * Tn + t;
+  coff.assign(V + 1, 0);
+  cbeg.clear();
+  for (int v = 0; v < V; ++v) {
+    for (int s = off[v]; s < off[v + 1]; s += kEmbedChunk) cbeg.push_back(s);
+    coff[v + 1] = (int32_t)cbeg.size();
+  }
+  cbeg.push_back(off[V]);
 }
 template <class T>
 void pos_bwd(const Launch& L, const T* dx, T* dwpe, int nseq, int Tn, int D) {
@@ -619,7 +652,7 @@ void add_inplace(const Launch& L, T* y, const T* x, int64_t n) {
 #define INST(T)                                                                                                 \
   template void convert_f32<T>(const Launch&, const float*, T*, int64_t);                                       \
   template void embed_fwd<T>(const Launch&, const int32_t*, int, int, int, const T*, const T*, T*, int);        \
-  template void embed_bwd_rows<T>(const Launch&, const int32_t*, const int32_t*, const T*, T*, int, int, bool); \
+  template void embed_bwd_rows<T>(const Launch&, const EmbedCSR&, const T*, T*, int, int, bool);             \
   template void pos_bwd<T>(const Launch&, const T*, T*, int, int, int);                                         \
   template void layernorm_fwd<T>(const Launch&, const T*, const T*, const T*, T*, T*, T*, int, int, double);    \
   template void layernorm_bwd<T>(const Launch&, const T*, const T*, const T*, const T*, const T*, const T*, T*, \

@@ -165,18 +165,6 @@ void attention_bwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, const T*
   }
 }
 
-void build_csr(const std::vector<int32_t>& tok, int nseq, int Tn, int V, std::vector<int32_t>& off,
-               std::vector<int32_t>& pos) {
-  off.assign(V + 1, 0);
-  for (int b = 0; b < nseq; ++b)
-    for (int t = 0; t < Tn; ++t) off[tok[(size_t)b * (Tn + 1) + t] + 1]++;
-  for (int v = 0; v < V; ++v) off[v + 1] += off[v];
-  pos.assign((size_t)nseq * Tn, 0);
-  std::vector<int32_t> fill(off.begin(), off.end() - 1);
-  for (int b = 0; b < nseq; ++b)
-    for (int t = 0; t < Tn; ++t) pos[fill[tok[(size_t)b * (Tn + 1) + t]]++] = b * Tn + t;
-}
-
 // A second stream for the backward work that nothing on the critical path consumes (weight /
 // bias / norm-gain gradients): fork() makes the side stream wait for everything issued on the
 // main stream so far; join() makes the main stream wait for the side stream.  Small GEMMs do not
@@ -297,7 +285,8 @@ struct GptRunner : Runner<T> {
   int nseq, Tn, N, D, H, hd, F, V, Ly, nseq_glob;
   bool tied;
   double eps;
-  int32_t *tok, *csr_off, *csr_pos;
+  int32_t* tok;
+  EmbedCSR csr;
   double* loss_rows;
   std::vector<T*> xs;  // L+1 residual streams
   struct Layer { T *mean1, *rstd1, *h1, *qkv, *P, *o, *x1, *mean2, *rstd2, *h2, *u, *gu; };
@@ -314,10 +303,15 @@ struct GptRunner : Runner<T> {
     nseq = b.n_seq; nseq_glob = b.n_seq_global; Tn = d.seq_len; N = nseq * Tn; D = d.d_model; H = d.n_heads;
     hd = D / H; F = d.d_ff; V = d.vocab; Ly = d.n_layers; tied = d.tie_embeddings != 0; eps = d.norm_eps;
     tok = upload<int32_t>(A, b.tokens.data(), (int64_t)nseq * (Tn + 1));
-    std::vector<int32_t> off, pos;
-    build_csr(b.tokens, nseq, Tn, V, off, pos);
-    csr_off = upload<int32_t>(A, off.data(), V + 1);
-    csr_pos = upload<int32_t>(A, pos.data(), (int64_t)N);
+    {
+      std::vector<int32_t> off, pos, coff, cbeg;
+      build_embed_csr(b.tokens, nseq, Tn, V, off, pos, coff, cbeg);
+      csr.off = upload<int32_t>(A, off.data(), V + 1);
+      csr.pos = upload<int32_t>(A, pos.data(), (int64_t)N);
+      csr.coff = upload<int32_t>(A, coff.data(), V + 1);
+      csr.cbeg = upload<int32_t>(A, cbeg.data(), (int64_t)cbeg.size());
+      csr.nchunks = (int)cbeg.size() - 1;
+    }
     loss_rows = A.alloc<double>(std::max(N, 1));
     for (int l = 0; l <= Ly; ++l) xs.push_back(A.alloc<T>((int64_t)N * D));
     const int64_t PP = (int64_t)nseq * H * Tn * Tn;
@@ -443,7 +437,7 @@ struct GptRunner : Runner<T> {
     }
     ss.join();  // all side work (incl. the tied head gradient into G0) before the embedding backward
     if (!tied) G0 = io.grads(0);
-    embed_bwd_rows<T>(L, csr_off, csr_pos, dxs[cur], G0 + u0.t("wte").offset, V, D, tied);
+    embed_bwd_rows<T>(L, csr, dxs[cur], G0 + u0.t("wte").offset, V, D, tied);
     pos_bwd<T>(L, dxs[cur], G0 + u0.t("wpe").offset, nseq, Tn, D);
     io.grads_done(0);
     sum_rows_f64(L, loss_rows, N, loss_sum);
@@ -460,7 +454,8 @@ struct LlamaRunner : Runner<T> {
   int64_t Wq;  // width of the packed q|k|v projection
   bool tied;
   double eps;
-  int32_t *tok, *csr_off, *csr_pos;
+  int32_t* tok;
+  EmbedCSR csr;
   double* loss_rows;
   T *cos_t, *sin_t;
   std::vector<T*> xs;
@@ -479,10 +474,15 @@ struct LlamaRunner : Runner<T> {
     eps = d.norm_eps;
     Wq = (int64_t)(Hq + 2 * Hkv) * hd;
     tok = upload<int32_t>(A, b.tokens.data(), (int64_t)nseq * (Tn + 1));
-    std::vector<int32_t> off, pos;
-    build_csr(b.tokens, nseq, Tn, V, off, pos);
-    csr_off = upload<int32_t>(A, off.data(), V + 1);
-    csr_pos = upload<int32_t>(A, pos.data(), (int64_t)N);
+    {
+      std::vector<int32_t> off, pos, coff, cbeg;
+      build_embed_csr(b.tokens, nseq, Tn, V, off, pos, coff, cbeg);
+      csr.off = upload<int32_t>(A, off.data(), V + 1);
+      csr.pos = upload<int32_t>(A, pos.data(), (int64_t)N);
+      csr.coff = upload<int32_t>(A, coff.data(), V + 1);
+      csr.cbeg = upload<int32_t>(A, cbeg.data(), (int64_t)cbeg.size());
+      csr.nchunks = (int)cbeg.size() - 1;
+    }
     loss_rows = A.alloc<double>(std::max(N, 1));
     {  // RoPE tables: angle(t, i) = t * theta^(-2i/hd)
       const int half = hd / 2;
@@ -621,7 +621,7 @@ struct LlamaRunner : Runner<T> {
     }
     ss.join();
     if (!tied) G0 = io.grads(0);
-    embed_bwd_rows<T>(L, csr_off, csr_pos, dxs[cur], G0 + u0.t("tok").offset, V, D, tied);
+    embed_bwd_rows<T>(L, csr, dxs[cur], G0 + u0.t("tok").offset, V, D, tied);
     io.grads_done(0);
     sum_rows_f64(L, loss_rows, N, loss_sum);
   }

@@ -29,17 +29,6 @@ struct ArenaP {
   }
 };
 
-void csr_of(const std::vector<int32_t>& tok, int nseq, int Tn, int V, std::vector<int32_t>& off,
-            std::vector<int32_t>& pos) {
-  off.assign(V + 1, 0);
-  for (int b = 0; b < nseq; ++b)
-    for (int t = 0; t < Tn; ++t) off[tok[(size_t)b * (Tn + 1) + t] + 1]++;
-  for (int v = 0; v < V; ++v) off[v + 1] += off[v];
-  pos.assign((size_t)nseq * Tn, 0);
-  std::vector<int32_t> fill(off.begin(), off.end() - 1);
-  for (int b = 0; b < nseq; ++b)
-    for (int t = 0; t < Tn; ++t) pos[fill[tok[(size_t)b * (Tn + 1) + t]]++] = b * Tn + t;
-}
 
 // y = x W^T (+ bias) (+ resid), all pairs
 void plinear_fwd(const Launch& L, CPair x, int64_t ldx, CPair W, int out, int in, int N, Pair y, int64_t ldy,
@@ -82,7 +71,8 @@ struct PairedGptRunner : Runner<float> {
   int nseq, Tn, N, D, H, hd, F, V, Ly, nseq_glob;
   bool tied;
   double eps;
-  int32_t *tok, *csr_off, *csr_pos;
+  int32_t* tok;
+  EmbedCSR csr;
   double* loss_rows;
   std::vector<Pair> xs;
   struct Layer {
@@ -99,12 +89,20 @@ struct PairedGptRunner : Runner<float> {
     hd = D / H; F = d.d_ff; V = d.vocab; Ly = d.n_layers; tied = d.tie_embeddings != 0; eps = d.norm_eps;
     tok = A.alloc<int32_t>((int64_t)nseq * (Tn + 1));
     SLQ_CUDA(cudaMemcpy(tok, b.tokens.data(), 4 * b.tokens.size(), cudaMemcpyHostToDevice));
-    std::vector<int32_t> o, ps;
-    csr_of(b.tokens, nseq, Tn, V, o, ps);
-    csr_off = A.alloc<int32_t>(V + 1);
-    csr_pos = A.alloc<int32_t>(N);
-    SLQ_CUDA(cudaMemcpy(csr_off, o.data(), 4 * o.size(), cudaMemcpyHostToDevice));
-    SLQ_CUDA(cudaMemcpy(csr_pos, ps.data(), 4 * ps.size(), cudaMemcpyHostToDevice));
+    {
+      std::vector<int32_t> o, ps, co, cb;
+      build_embed_csr(b.tokens, nseq, Tn, V, o, ps, co, cb);
+      auto up = [&](const std::vector<int32_t>& v) {
+        int32_t* d_ = A.alloc<int32_t>((int64_t)v.size());
+        SLQ_CUDA(cudaMemcpy(d_, v.data(), 4 * v.size(), cudaMemcpyHostToDevice));
+        return d_;
+      };
+      csr.off = up(o);
+      csr.pos = up(ps);
+      csr.coff = up(co);
+      csr.cbeg = up(cb);
+      csr.nchunks = (int)cb.size() - 1;
+    }
     loss_rows = A.alloc<double>(std::max(N, 1));
     for (int l = 0; l <= Ly; ++l) xs.push_back(A.pair((int64_t)N * D));
     const int64_t PP = (int64_t)nseq * H * Tn * Tn;
@@ -236,8 +234,8 @@ struct PairedGptRunner : Runner<float> {
       cur ^= 1;
     }
     const Pair gwte = grd(0, u0, "wte"), gwpe = grd(0, u0, "wpe");
-    embed_bwd_rows<float>(L, csr_off, csr_pos, dxs[cur].m, gwte.m, V, D, tied);
-    embed_bwd_rows<float>(L, csr_off, csr_pos, dxs[cur].d, gwte.d, V, D, tied);
+    embed_bwd_rows<float>(L, csr, dxs[cur].m, gwte.m, V, D, tied);
+    embed_bwd_rows<float>(L, csr, dxs[cur].d, gwte.d, V, D, tied);
     pos_bwd<float>(L, dxs[cur].m, gwpe.m, nseq, Tn, D);
     pos_bwd<float>(L, dxs[cur].d, gwpe.d, nseq, Tn, D);
     im.grads_done(0);
