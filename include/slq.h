@@ -173,6 +173,15 @@ slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_ne
 slq_status slq_quadrature(const double* alpha, const double* beta, int32_t m, double* nodes,
                           double* weights);
 
+/* SLQ probe average (host only, no context, pure): n_probes node/weight sets
+ * of m_p = m_counts[p] nodes each, packed back to back in nodes[] / weights[] (sum of m_counts).
+ * moments (may be NULL): [jmax + 1] probe-averaged e_1^T T^j e_1 = (1/s) sum_p sum_i w_i theta_i^j;
+ * density (may be NULL): Gaussian-smoothed spectral density (1/s) sum_p sum_i w_i N(x_g; theta_i,
+ * sigma^2) at the n_grid points grid[] (sigma > 0).  SLQ_EINVAL on bad sizes / sigma. */
+slq_status slq_density(const double* nodes, const double* weights, const int32_t* m_counts, int32_t n_probes,
+                       int32_t jmax, double* moments, const double* grid, int32_t n_grid, double sigma,
+                       double* density);
+
 /* Ghost diagnostic (host only, no context, pure; Theorem 3 "spurious duplicate
  * eigenvalues"; R18): single-linkage clusters of ascending Ritz values `nodes[m]`,
  * neighbours joined when nodes[i+1] - nodes[i] <= tol.  cluster_id[m] (may be NULL) gets each

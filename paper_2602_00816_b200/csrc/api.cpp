@@ -16,6 +16,8 @@
 namespace slq {
 void tridiag_gauss(const double* alpha, const double* beta, int m, double* nodes, double* weights);
 void ghost_clusters(const double* nodes, int m, double tol, int32_t* cluster_id, int32_t* n_ghost, double* max_split);
+void slq_average(const double* nodes, const double* weights, const int32_t* mc, int np, int jmax, double* mom,
+                 const double* grid, int ng, double sigma, double* dens);
 
 const char* kernel_class_name(int c) {
   static const char* names[KC_COUNT] = {"gemm", "attention", "norm", "cross_entropy", "embedding",
@@ -351,6 +353,14 @@ slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_ne
 
 slq_status slq_quadrature(const double* alpha, const double* beta, int32_t m, double* nodes, double* weights) {
   return guarded(nullptr, [&] { tridiag_gauss(alpha, beta, m, nodes, weights); });
+}
+
+slq_status slq_density(const double* nodes, const double* weights, const int32_t* m_counts, int32_t n_probes,
+                       int32_t jmax, double* moments, const double* grid, int32_t n_grid, double sigma,
+                       double* density) {
+  return guarded(nullptr, [&] {
+    slq_average(nodes, weights, m_counts, n_probes, jmax, moments, grid, n_grid, sigma, density);
+  });
 }
 
 slq_status slq_ghost_clusters(const double* nodes, int32_t m, double tol, int32_t* cluster_id, int32_t* n_ghost,

@@ -110,4 +110,42 @@ void ghost_clusters(const double* nodes, int m, double tol, int32_t* cluster_id,
   if (max_split) *max_split = split;
 }
 
+// Probe-averaged SLQ moments and smoothed density.
+void slq_average(const double* nodes, const double* weights, const int32_t* mc, int np, int jmax, double* mom,
+                 const double* grid, int ng, double sigma, double* dens) {
+  SLQ_CHECK_ARG(nodes && weights && mc && np >= 1, "nodes / weights / m_counts, n_probes >= 1");
+  SLQ_CHECK_ARG(!mom || jmax >= 0, "jmax >= 0");
+  SLQ_CHECK_ARG(!dens || (grid && ng >= 1 && sigma > 0 && std::isfinite(sigma)), "grid / n_grid / sigma > 0");
+  if (mom)
+    for (int j = 0; j <= jmax; ++j) mom[j] = 0.0;
+  if (dens)
+    for (int g = 0; g < ng; ++g) dens[g] = 0.0;
+  const double norm = 1.0 / (sigma * sqrt(2.0 * M_PI));
+  int64_t off = 0;
+  for (int p = 0; p < np; ++p) {
+    SLQ_CHECK_ARG(mc[p] >= 1, "m_counts >= 1");
+    for (int i = 0; i < mc[p]; ++i) {
+      const double x = nodes[off + i], w = weights[off + i];
+      SLQ_CHECK_ARG(std::isfinite(x) && std::isfinite(w), "finite nodes / weights");
+      if (mom) {
+        double xp = 1.0;
+        for (int j = 0; j <= jmax; ++j) {
+          mom[j] += w * xp;
+          xp *= x;
+        }
+      }
+      if (dens)
+        for (int g = 0; g < ng; ++g) {
+          const double u = (grid[g] - x) / sigma;
+          dens[g] += w * exp(-0.5 * u * u) * norm;
+        }
+    }
+    off += mc[p];
+  }
+  if (mom)
+    for (int j = 0; j <= jmax; ++j) mom[j] /= np;
+  if (dens)
+    for (int g = 0; g < ng; ++g) dens[g] /= np;
+}
+
 }  // namespace slq

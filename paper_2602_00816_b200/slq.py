@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
         "slq_lanczos_info": (I32, [P, P, P, P]),
         "slq_quadrature": (I32, [P, P, I32, P, P]),
         "slq_ghost_clusters": (I32, [P, I32, D, P, P, P]),
+        "slq_density": (I32, [P, P, P, I32, I32, P, P, I32, D, P]),
         "slq_probe": (I32, [P, U64, P]),
         "slq_profile": (I32, [P, I32, I32]),
         "slq_num_kernel_classes": (I32, []),
@@ -201,6 +202,20 @@ def quadrature(alpha, beta) -> Tuple[np.ndarray, np.ndarray]:
     _check(lib().slq_quadrature(a.ctypes.data, b.ctypes.data if b.size else None, m, nodes.ctypes.data,
                                 w.ctypes.data))
     return nodes, w
+
+
+def density(node_sets, weight_sets, jmax: int = 2, grid=None, sigma: float = 0.0):
+    """Probe-averaged moments [jmax + 1] and (if grid is given) the smoothed density -- slq_density."""
+    mc = np.array([len(n) for n in node_sets], dtype=np.int32)
+    nodes = np.ascontiguousarray(np.concatenate(node_sets), dtype=np.float64)
+    w = np.ascontiguousarray(np.concatenate(weight_sets), dtype=np.float64)
+    mom = np.empty(jmax + 1)
+    g = None if grid is None else np.ascontiguousarray(grid, dtype=np.float64)
+    dens = None if g is None else np.empty(g.size)
+    _check(lib().slq_density(nodes.ctypes.data, w.ctypes.data, mc.ctypes.data, mc.size, jmax, mom.ctypes.data,
+                             g.ctypes.data if g is not None else None, 0 if g is None else g.size, float(sigma),
+                             dens.ctypes.data if dens is not None else None))
+    return mom, dens
 
 
 def ghost_clusters(nodes, tol: float) -> Tuple[np.ndarray, int, float]:

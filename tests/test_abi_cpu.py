@@ -157,3 +157,27 @@ def test_descriptor_validation_window_and_basis():
             with pytest.raises(slq.SlqError) as e:
                 slq.plan_layout(d, 1)
             assert e.value.status == slq.SLQ_EINVAL
+
+
+def test_density_host_matches_oracle():
+    """slq_density (host): probe-averaged moments and Gaussian-smoothed density vs the oracle's
+    slq_moments / slq_density; mu_0 = 1 for weights summing to 1."""
+    from oracle import lanczos as OL
+    rng = np.random.default_rng(7)
+    node_sets, weight_sets = [], []
+    for m in (5, 9, 1):
+        a = rng.standard_normal(m)
+        b = np.abs(rng.standard_normal(m - 1)) + 0.1
+        n, w = OL.gauss_quadrature(a, b)
+        node_sets.append(n)
+        weight_sets.append(w)
+    grid = np.linspace(-4, 4, 41)
+    mom, dens = slq.density(node_sets, weight_sets, jmax=4, grid=grid, sigma=0.3)
+    ref_m = OL.slq_moments(node_sets, weight_sets, jmax=4)
+    ref_d = OL.slq_density(grid, node_sets, weight_sets, 0.3)
+    assert np.allclose(mom, ref_m, rtol=1e-13, atol=1e-14) and abs(mom[0] - 1) < 1e-13
+    assert np.allclose(dens, ref_d, rtol=1e-13, atol=1e-15)
+    mom2, d2 = slq.density(node_sets, weight_sets, jmax=1)
+    assert d2 is None and np.allclose(mom2, ref_m[:2], rtol=1e-13)
+    with pytest.raises(slq.SlqError):
+        slq.density(node_sets, weight_sets, jmax=1, grid=grid, sigma=0.0)

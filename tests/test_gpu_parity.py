@@ -207,3 +207,29 @@ def test_fp32_pass_mode_reported():
     err = _rel(hv, ref)
     print(f"c1 fp32-pass HVP rel-L2 = {err:.3e}")
     assert err < 5e-2
+
+
+def test_lanczos_breakdown_detected_post_hoc():
+    """mlp_tiny has P = 112 parameters and an invariant Krylov subspace of dimension 103 from its
+    probe (fp64 oracle: beta_104 ~ 4e-13).  Asked for P + 10 steps, the GPU recurrence (device-
+    resident scalars, breakdown detected after the loop) must stop at the invariant subspace:
+    m_done within a few steps of the oracle's, unfilled entries NaN, and the Ritz values of the
+    computed T an invariant set (extremes agree with the oracle's)."""
+    cfg = si.CONFIGS["mlp_tiny"]
+    th = si.init_params(cfg)
+    P = th.size
+    m = P + 10
+    with _ctx(cfg, reorth="full", max_steps=m) as c:
+        a, b = c.lanczos(cfg.probe_seed0, m)
+        info = c.lanczos_info()
+    r = _oracle_lanczos(cfg, m, "full")
+    md = info["m_done"]
+    print(f"mlp_tiny breakdown: GPU m_done {md}, oracle {r.m_done}, beta_next {info['beta_next']:.2e}")
+    assert r.breakdown and abs(md - r.m_done) <= 3 and md <= P
+    assert np.all(np.isnan(a[md:])) and np.all(np.isnan(b[md - 1:]))
+    assert np.all(np.isfinite(a[:md])) and np.all(np.isfinite(b[:md - 1]))
+    n1, w1 = slq.quadrature(a[:md], b[:md - 1])
+    n2, _ = OL.gauss_quadrature(r.alpha, r.beta)
+    scale = max(abs(n2[0]), abs(n2[-1]))
+    assert abs(n1[0] - n2[0]) <= 1e-5 * scale and abs(n1[-1] - n2[-1]) <= 1e-5 * scale
+    assert abs(w1.sum() - 1) < 1e-12
