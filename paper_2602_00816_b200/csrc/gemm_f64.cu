@@ -342,7 +342,12 @@ int plan_variant(const GemmArgs<double>& a, int* splits) {
   *splits = 0;
   const int fv = forced_variant();
   if (fv >= 0 && fv < kVariants) return fv;
-  if (a.batch != 1 || a.tri != TRI_NONE) return pick_variant(a);
+  if (a.batch != 1 || a.tri != TRI_NONE) {
+    // batched causal attention GEMMs at T <= 256 (tools/gemm_sweep_attn.py on B200: +12..28%)
+    if (a.M <= 256 && a.N <= 256 && a.K <= 64) return 7;
+    if (a.M <= 256 && a.N <= 64) return 11;
+    return pick_variant(a);
+  }
   const double mn = (double)a.M * a.N;
   if (a.K >= 2048) {
     if (mn <= 65536.0) { *splits = 8; return 11; }    // 256 x 256
@@ -412,13 +417,16 @@ extern "C" slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, in
   using namespace slq;
   double *A = nullptr, *B = nullptr, *C = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // diagnostic knobs: SLQ_DIAG_BATCH = b (contiguous batches), SLQ_DIAG_TRI = causal structure
+  const int nb = getenv("SLQ_DIAG_BATCH") ? std::max(1, atoi(getenv("SLQ_DIAG_BATCH"))) : 1;
+  const int tri = getenv("SLQ_DIAG_TRI") ? atoi(getenv("SLQ_DIAG_TRI")) : TRI_NONE;
   try {
     SLQ_CUDA(cudaSetDevice(device));
-    SLQ_CUDA(cudaMalloc(&A, sizeof(double) * (size_t)M * K));
-    SLQ_CUDA(cudaMalloc(&B, sizeof(double) * (size_t)N * K));
-    SLQ_CUDA(cudaMalloc(&C, sizeof(double) * (size_t)M * N));
-    k_fill<<<1024, 256>>>(A, (int64_t)M * K, 1);
-    k_fill<<<1024, 256>>>(B, (int64_t)N * K, 2);
+    SLQ_CUDA(cudaMalloc(&A, sizeof(double) * (size_t)M * K * nb));
+    SLQ_CUDA(cudaMalloc(&B, sizeof(double) * (size_t)N * K * nb));
+    SLQ_CUDA(cudaMalloc(&C, sizeof(double) * (size_t)M * N * nb));
+    k_fill<<<1024, 256>>>(A, (int64_t)M * K * nb, 1);
+    k_fill<<<1024, 256>>>(B, (int64_t)N * K * nb, 2);
     Workspace ws;
     int64_t launches = 0;
     Launch L{0, nullptr, &ws, &launches};
@@ -427,6 +435,11 @@ extern "C" slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, in
     a.A = A; a.sAm = a_kmajor ? K : 1; a.sAk = a_kmajor ? 1 : M;
     a.B = B; a.sBk = b_kmajor ? 1 : N; a.sBn = b_kmajor ? K : 1;
     a.C = C; a.ldc = N;
+    a.batch = nb;
+    a.tri = tri;
+    a.offA = BatchOff{(int64_t)M * K, 0, 1, 1};
+    a.offB = BatchOff{(int64_t)N * K, 0, 1, 1};
+    a.offC = BatchOff{(int64_t)M * N, 0, 1, 1};
     // variant <= -4: the tcgen05 int8 Ozaki path with S = -variant digit planes
     int planned_splits = 0;
     const int v = variant < 0 ? plan_variant(a, &planned_splits) : variant;
@@ -444,7 +457,7 @@ extern "C" slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, in
     SLQ_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
     SLQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    *tflops = 2.0 * M * N * (double)K * iters / (ms * 1e-3) / 1e12;
+    *tflops = gemm_flops(a) * iters / (ms * 1e-3) / 1e12;
     std::vector<double> h((size_t)M * N);
     SLQ_CUDA(cudaMemcpy(h.data(), C, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
     double s = 0;
