@@ -121,6 +121,10 @@ CONFIGS: Dict[str, ModelDesc] = {
                          n_kv_heads=8, d_ff=14336, vocab=128256, seq_len=512, n_seq=1,
                          rope_theta=500000.0, param_bf16=True, eps=1e-3, m=2, probes=1,
                          reorth_full=False, init_seed=1005, data_seed=2005, probe_seed0=3500),
+    # c2 at twice the batch (diagnostic: what one pass costs at 2 x the rows)
+    "c2x2": ModelDesc(name="c2x2", arch=ARCH_GPT, n_layers=4, d_model=256, n_heads=4, n_kv_heads=4,
+                      d_ff=1024, vocab=4096, seq_len=256, n_seq=16, eps=1e-3, m=64, probes=4,
+                      reorth_full=True, init_seed=1002, data_seed=2002, probe_seed0=3200),
     # GEMM-shape evidence only (not a c5 step): every Llama-3-8B layer shape at c5's per-GPU batch
     # (2 x 2048 tokens) on 2 of the 32 blocks
     "c5_gemm": ModelDesc(name="c5_gemm", arch=ARCH_LLAMA, n_layers=2, d_model=4096, n_heads=32,
