@@ -86,6 +86,7 @@ def test_c3_parity_batch(numerics):
 
 
 @pytest.mark.skipif(os.environ.get("SLQ_LARGE_TESTS") != "1", reason="set SLQ_LARGE_TESTS=1 (~60 GB host RAM)")
+@pytest.mark.parametrize("numerics", ["fp64", "fp64_oz"])
 @pytest.mark.parametrize("name", ["c4_parity", "c5_twin"])
-def test_large_parity(name):
-    _case(name)
+def test_large_parity(name, numerics):
+    _case(name, numerics)
