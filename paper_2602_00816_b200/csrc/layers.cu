@@ -309,7 +309,8 @@ __global__ void k_rmsnorm_bwd(const T* __restrict__ dy, const T* __restrict__ x,
 template <class T>
 __global__ void k_colreduce1(int mode, const T* __restrict__ dy, int64_t lddy, const T* __restrict__ x,
                              const T* __restrict__ mean, const T* __restrict__ rstd, T* __restrict__ part0,
-                             T* __restrict__ part1, int rows, int cols, int rpb) {
+                             T* __restrict__ part1, int rows, int cols, int rpb, unsigned* __restrict__ counter,
+                             T* __restrict__ out0, T* __restrict__ out1, bool accumulate) {
   __shared__ T s0[8][33], s1[8][33];
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   const int c = blockIdx.x * 32 + tx;
@@ -341,19 +342,32 @@ __global__ void k_colreduce1(int mode, const T* __restrict__ dy, int64_t lddy, c
     part0[(int64_t)blockIdx.y * cols + c] = b0;
     if (mode == 1) part1[(int64_t)blockIdx.y * cols + c] = b1;
   }
+  // stage 2 in the last block to finish (threadfence + counter): every column's partials are
+  // summed in slab order, so the result does not depend on which block finishes last
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned nb = gridDim.x * gridDim.y;
+    last = atomicAdd(counter, 1u) == nb - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nparts = gridDim.y;
+  for (int cc = threadIdx.x; cc < cols; cc += blockDim.x) {
+    T s0v = T(0), s1v = T(0);
+    for (int p = 0; p < nparts; ++p) {
+      s0v += part0[(int64_t)p * cols + cc];
+      if (mode == 1) s1v += part1[(int64_t)p * cols + cc];
+    }
+    out0[cc] = accumulate ? out0[cc] + s0v : s0v;
+    if (mode == 1) out1[cc] = accumulate ? out1[cc] + s1v : s1v;
+  }
+  if (threadIdx.x == 0) *counter = 0u;  // ready for the next call on this stream
 }
 
 // one warp per column
-template <class T>
-__global__ void k_colreduce2(const T* __restrict__ part, int nparts, T* __restrict__ out, int cols, bool accumulate) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
-  const int lane = threadIdx.x % kWarp;
-  if (c >= cols) return;
-  T s = T(0);
-  for (int p = lane; p < nparts; p += kWarp) s += part[(int64_t)p * cols + c];
-  s = warp_sum(s);
-  if (lane == 0) out[c] = accumulate ? out[c] + s : s;
-}
 
 // causal softmax over rows of length Tn; row r is query position t = r % Tn (keys j <= t)
 template <class T>
@@ -597,13 +611,14 @@ void colreduce(const Launch& L, int mode, const T* dy, int64_t lddy, const T* x,
   int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), ceil_div(2 * 148, cblocks)));
   const int rpb = (int)ceil_div(std::max(rows, 1), rblocks);
   rblocks = (int)ceil_div(std::max(rows, 1), rpb);
-  T* part = (T*)L.ws->get(sizeof(T) * 2 * (size_t)rblocks * cols, L.stream);
+  const size_t pbytes = (sizeof(T) * 2 * (size_t)rblocks * cols + 255) & ~(size_t)255;
+  uint8_t* base = (uint8_t*)L.ws->get(pbytes + 256, L.stream);
+  T* part = (T*)base;
   T* part1 = part + (size_t)rblocks * cols;
+  unsigned* counter = (unsigned*)(base + pbytes);
+  SLQ_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), L.stream));
   LAUNCH(KC_NORM, dim3(cblocks, rblocks), 256, k_colreduce1<T>, mode, dy, lddy, x, mean, rstd, part, part1, rows,
-         cols, rpb);
-  const int wblocks = (int)ceil_div((int64_t)cols * kWarp, 256);
-  LAUNCH(KC_NORM, wblocks, 256, k_colreduce2<T>, part, rblocks, out0, cols, accumulate);
-  if (mode == 1) LAUNCH(KC_NORM, wblocks, 256, k_colreduce2<T>, part1, rblocks, out1, cols, accumulate);
+         cols, rpb, counter, out0, out1, accumulate);
 }
 template <class T>
 void softmax_causal_fwd(const Launch& L, T* S, int64_t rows, int Tn) {
