@@ -332,85 +332,123 @@ __device__ __forceinline__ int exp_of(double mx) {
   return e;
 }
 
-// K-contiguous operand X[row * ld + k] -> planes out[q][row][Kp], exponents ex[row]; warp per row
-template <int S>
-__global__ void k_oz_slice_rows(const double* __restrict__ X, int64_t ld, int rows, int K, int Kp,
-                                int8_t* __restrict__ out, int* __restrict__ ex) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  if (row >= rows) return;
-  const double* xr = X + (int64_t)row * ld;
-  double mx = 0.0;
-  for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(xr[k]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const int e = exp_of(mx);
-  if (lane == 0) ex[row] = e;
-  const int64_t plane = (int64_t)rows * Kp;
-  for (int k4 = lane * 4; k4 < Kp; k4 += 128) {
-    int8_t d[4][S];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double x = (k4 + j < K) ? xr[k4 + j] : 0.0;
-      digits<S>(x, e, d[j]);
-    }
-#pragma unroll
-    for (int q = 0; q < S; ++q) {
-      const uint32_t w = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
-                         ((uint32_t)(uint8_t)d[2][q] << 16) | ((uint32_t)(uint8_t)d[3][q] << 24);
-      *reinterpret_cast<uint32_t*>(out + q * plane + (int64_t)row * Kp + k4) = w;
-    }
-  }
+constexpr int kExNone = (int)0x80808080;  // "no nonzero element" marker of a partial exponent
+
+// ---- merged slicing of both GEMM operands (one or two launches per GEMM) ----
+// A job slices one operand into S digit planes [S][rows][Kp] and row exponents ex[rows].
+// kmajor: element (r, k) at X[r * ld + k]; else at X[k * ld + r] (the exponent pass then writes
+// one partial exponent per 256-deep k block into xp[kb * rows + r], combined by the slice pass).
+struct SliceJob {
+  const double* X;
+  int64_t ld;
+  int rows, K, Kp, kmajor;
+  int8_t* out;
+  int* ex;
+  int* xp;       // [ceil(K / 256)][rows] partial exponents (cols path)
+  int blocks0;   // first block of this job in the launch
+};
+struct SliceJobs {
+  SliceJob j[2];
+  int n;
+};
+constexpr int kColK = 256;  // k extent of one exponent-pass block
+
+__device__ __forceinline__ const SliceJob& job_of(const SliceJobs& js, int b) {
+  return (js.n > 1 && b >= js.j[1].blocks0) ? js.j[1] : js.j[0];
 }
 
-// operand stored transposed: element (row r, k) at X[k * ld + r] (r contiguous).
-// Pass 1: column exponents.  Block = 32 rows x 256 k; exp_of is monotone in the maximum, so the
-// per-block exponents combine with an integer atomicMax (deterministic); ex[] starts at kExNone.
-constexpr int kExNone = (int)0x80808080;  // memset byte 0x80
-__global__ void __launch_bounds__(256) k_oz_colexp(const double* __restrict__ X, int64_t ld, int rows, int K,
-                                                  int* __restrict__ ex) {
+// exponent pass of the cols-path jobs: block (32 rows, 256 k) -> xp[kb][r]
+__global__ void __launch_bounds__(256) k_oz_colexp2(const __grid_constant__ SliceJobs js) {
+  const SliceJob& jb = job_of(js, blockIdx.x);
+  const int b = blockIdx.x - jb.blocks0;
+  const int rb = (jb.rows + 31) / 32;
+  const int r0 = (b % rb) * 32, kb = b / rb;
   __shared__ double red[8][33];
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  const int r = blockIdx.x * 32 + tx;
-  const int k0 = blockIdx.y * 256, k1 = min(K, k0 + 256);
+  const int r = r0 + tx;
+  const int k0 = kb * kColK, k1 = min(jb.K, k0 + kColK);
   double mx = 0.0;
-  if (r < rows)
-    for (int k = k0 + ty; k < k1; k += 8) mx = fmax(mx, fabs(X[(int64_t)k * ld + r]));
+  if (r < jb.rows) {
+#pragma unroll 4
+    for (int k = k0 + ty; k < k1; k += 8) mx = fmax(mx, fabs(jb.X[(int64_t)k * jb.ld + r]));
+  }
   red[ty][tx] = mx;
   __syncthreads();
-  if (ty == 0 && r < rows) {
+  if (ty == 0 && r < jb.rows) {
     double m = red[0][tx];
 #pragma unroll
     for (int i = 1; i < 8; ++i) m = fmax(m, red[i][tx]);
-    if (m > 0.0) atomicMax(&ex[r], exp_of(m));
+    jb.xp[(int64_t)kb * jb.rows + r] = m > 0.0 ? exp_of(m) : kExNone;
   }
 }
 
-// Pass 2: digits.  Block = 32 rows x 128 k, four 32 x 32 tiles transposed through shared memory.
+// slice pass: rows-path job = one warp per row (the max pass issues 32 independent loads per lane
+// per 1024-wide sweep; the digit pass re-reads the row from L1/L2); cols-path job = 32 rows x 128 k
+// per block through a shared tile, exponent = max of the row's partial exponents
 template <int S>
-__global__ void __launch_bounds__(256) k_oz_slice_cols(const double* __restrict__ X, int64_t ld, int rows, int K,
-                                                      int Kp, int8_t* __restrict__ out, int* __restrict__ ex) {
+__global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ SliceJobs js) {
+  const SliceJob& jb = job_of(js, blockIdx.x);
+  const int b = blockIdx.x - jb.blocks0;
+  const int64_t plane = (int64_t)jb.rows * jb.Kp;
+  if (jb.kmajor) {
+    const int row = b * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= jb.rows) return;
+    const double* xr = jb.X + (int64_t)row * jb.ld;
+    constexpr int V = 32;  // values per lane per sweep (1024-wide sweeps)
+    double mx = 0.0;
+    for (int k0 = 0; k0 < jb.K; k0 += 32 * V) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const int k = k0 + i * 32 + lane;
+        if (k < jb.K) mx = fmax(mx, fabs(xr[k]));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int e = exp_of(mx);
+    if (lane == 0) jb.ex[row] = e;
+    for (int k4 = lane * 4; k4 < jb.Kp; k4 += 128) {
+      double x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[j] = (k4 + j < jb.K) ? xr[k4 + j] : 0.0;
+      int8_t d[4][S];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) digits<S>(x[j], e, d[j]);
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint32_t w = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
+                           ((uint32_t)(uint8_t)d[2][q] << 16) | ((uint32_t)(uint8_t)d[3][q] << 24);
+        *reinterpret_cast<uint32_t*>(jb.out + q * plane + (int64_t)row * jb.Kp + k4) = w;
+      }
+    }
+    return;
+  }
   __shared__ double tile[32][33];
   __shared__ int es[32];
+  const int rb = (jb.rows + 31) / 32;
+  const int r0 = (b % rb) * 32, kblk = b / rb;
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  const int r0 = blockIdx.x * 32;
   const int r = r0 + tx;
   if (threadIdx.x < 32) {
-    const int e = r < rows ? ex[r] : 0;
+    int e = kExNone;
+    if (r < jb.rows) {
+      const int nkb = (jb.K + kColK - 1) / kColK;
+      for (int kb = 0; kb < nkb; ++kb) e = max(e, jb.xp[(int64_t)kb * jb.rows + r]);
+    }
     es[threadIdx.x] = e == kExNone ? 0 : e;
+    if (kblk == 0 && r < jb.rows) jb.ex[r] = es[threadIdx.x];
   }
-  const int64_t plane = (int64_t)rows * Kp;
-  const int wr = threadIdx.x / 8, kq = threadIdx.x % 8;  // writer: row r0 + wr, k = 4 kq .. 4 kq + 3
-  const int kb = blockIdx.y * 128, ke = min(Kp, kb + 128);
-  for (int k0 = kb; k0 < ke; k0 += 32) {
+  const int wr = threadIdx.x / 8, kq = threadIdx.x % 8;
+  const int kb0 = kblk * 128, kb1 = min(jb.Kp, kb0 + 128);
+  for (int k0 = kb0; k0 < kb1; k0 += 32) {
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int k = k0 + ty + 8 * i;
-      tile[ty + 8 * i][tx] = (r < rows && k < K) ? X[(int64_t)k * ld + r] : 0.0;
+      tile[ty + 8 * i][tx] = (r < jb.rows && k < jb.K) ? jb.X[(int64_t)k * jb.ld + r] : 0.0;
     }
     __syncthreads();
-    if (r0 + wr < rows && k0 + 4 * kq < Kp) {
+    if (r0 + wr < jb.rows && k0 + 4 * kq < jb.Kp) {
       int8_t d[4][S];
 #pragma unroll
       for (int j = 0; j < 4; ++j) digits<S>(tile[4 * kq + j][wr], es[wr], d[j]);
@@ -418,7 +456,7 @@ __global__ void __launch_bounds__(256) k_oz_slice_cols(const double* __restrict_
       for (int q = 0; q < S; ++q) {
         const uint32_t w = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
                            ((uint32_t)(uint8_t)d[2][q] << 16) | ((uint32_t)(uint8_t)d[3][q] << 24);
-        *reinterpret_cast<uint32_t*>(out + q * plane + (int64_t)(r0 + wr) * Kp + k0 + 4 * kq) = w;
+        *reinterpret_cast<uint32_t*>(jb.out + q * plane + (int64_t)(r0 + wr) * jb.Kp + k0 + 4 * kq) = w;
       }
     }
   }
@@ -441,23 +479,6 @@ static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 template <int S>
-void slice(const Launch& L, const double* X, bool kmajor, int64_t ld, int rows, int K, int Kp, int8_t* out, int* ex) {
-  if (kmajor) {
-    k_oz_slice_rows<S><<<(unsigned)ceil_div((int64_t)rows * 32, 256), 256, 0, L.stream>>>(X, ld, rows, K, Kp, out, ex);
-  } else {
-    SLQ_CUDA(cudaMemsetAsync(ex, 0x80, sizeof(int) * (size_t)rows, L.stream));
-    k_oz_colexp<<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(K, 256)), 256, 0, L.stream>>>(X, ld, rows, K,
-                                                                                                     ex);
-    SLQ_CUDA(cudaGetLastError());
-    ++*L.launches;
-    k_oz_slice_cols<S><<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(Kp, 128)), 256, 0, L.stream>>>(
-        X, ld, rows, K, Kp, out, ex);
-  }
-  SLQ_CUDA(cudaGetLastError());
-  ++*L.launches;
-}
-
-template <int S>
 void run(const Launch& L, const GemmArgs<double>& a) {
   using CF = Cfg<S>;
   static bool attr = false;
@@ -478,19 +499,50 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   splits = (int)ceil_div(nk, ktps);
   const size_t a_bytes = align256((size_t)S * M * Kp), b_bytes = align256((size_t)S * N * Kp);
   const size_t e_bytes = align256(4 * (size_t)(M + N));
+  const int nkb = (int)ceil_div(K, kColK);
+  const size_t xp_bytes = align256(4 * (size_t)(M + N) * nkb);
   const size_t w_bytes = splits > 1 ? align256(8 * (size_t)M * N * splits) : 0;
-  uint8_t* base = (uint8_t*)L.ws->get(a_bytes + b_bytes + e_bytes + w_bytes, L.stream);
+  uint8_t* base = (uint8_t*)L.ws->get(a_bytes + b_bytes + e_bytes + xp_bytes + w_bytes, L.stream);
   int8_t* as = (int8_t*)base;
   int8_t* bs = (int8_t*)(base + a_bytes);
   int* ea = (int*)(base + a_bytes + b_bytes);
   int* eb = ea + M;
-  double* ws = splits > 1 ? (double*)(base + a_bytes + b_bytes + e_bytes) : nullptr;
+  int* xpa = (int*)(base + a_bytes + b_bytes + e_bytes);
+  int* xpb = xpa + (size_t)M * nkb;
+  double* ws = splits > 1 ? (double*)(base + a_bytes + b_bytes + e_bytes + xp_bytes) : nullptr;
   {
     LaunchScope scope(L.prof, KC_OZ_SLICE, L.stream, 0, (8.0 + S) * ((double)M * K + (double)N * K));
-    // A(m, k): K-contiguous when sAk == 1 (rows = M, pitch sAm), else stored [K x M] with pitch sAk
-    slice<S>(L, a.A, a.sAk == 1, a.sAk == 1 ? a.sAm : a.sAk, M, K, Kp, as, ea);
+    // A(m, k): K-contiguous when sAk == 1 (rows = M, pitch sAm), else stored [K x M] with pitch sAk;
     // B(k, n) = B[k * sBk + n * sBn]: K-contiguous rows per n when sBk == 1 (pitch sBn)
-    slice<S>(L, a.B, a.sBk == 1, a.sBk == 1 ? a.sBn : a.sBk, N, K, Kp, bs, eb);
+    SliceJobs js;
+    js.n = 2;
+    js.j[0] = SliceJob{a.A, a.sAk == 1 ? a.sAm : a.sAk, M, K, Kp, a.sAk == 1 ? 1 : 0, as, ea, xpa, 0};
+    js.j[1] = SliceJob{a.B, a.sBk == 1 ? a.sBn : a.sBk, N, K, Kp, a.sBk == 1 ? 1 : 0, bs, eb, xpb, 0};
+    // exponent pass (cols-path jobs only)
+    int nexp = 0;
+    SliceJobs je;
+    je.n = 0;
+    for (int i = 0; i < 2; ++i)
+      if (!js.j[i].kmajor) {
+        SliceJob jj = js.j[i];
+        jj.blocks0 = nexp;
+        nexp += (int)(ceil_div(jj.rows, 32) * ceil_div(K, kColK));
+        je.j[je.n++] = jj;
+      }
+    if (je.n == 1) je.j[1] = je.j[0];
+    if (nexp > 0) {
+      k_oz_colexp2<<<nexp, 256, 0, L.stream>>>(je);
+      SLQ_CUDA(cudaGetLastError());
+      ++*L.launches;
+    }
+    int nsl = 0;
+    for (int i = 0; i < 2; ++i) {
+      js.j[i].blocks0 = nsl;
+      nsl += js.j[i].kmajor ? (int)ceil_div(js.j[i].rows, 8) : (int)(ceil_div(js.j[i].rows, 32) * ceil_div(Kp, 128));
+    }
+    k_oz_slice2<S><<<nsl, 256, 0, L.stream>>>(js);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
   }
   const CUtensorMap ta = make_map_i8(as, (int64_t)S * M, Kp, Kp, BM);
   const CUtensorMap tb = make_map_i8(bs, (int64_t)S * N, Kp, Kp, BN);
