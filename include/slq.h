@@ -166,6 +166,12 @@ slq_status slq_grad(slq_ctx* ctx, float* g_shard, double* loss);
 slq_status slq_lanczos(slq_ctx* ctx, uint64_t probe_seed, int32_t m, double* alpha, double* beta);
 slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_next,
                             int32_t* nonfinite);
+/* Stochastic Lanczos quadrature's probe loop ("T_SLQ ~ s m T_Lanczos iter"):
+ * slq_lanczos for each of the n_probes seeds; alpha [n_probes][m], beta [n_probes][m - 1] (host),
+ * m_done [n_probes] (may be NULL).  Feed each probe's (alpha, beta) to slq_quadrature and the node
+ * sets to slq_density for the probe average.  Collective. */
+slq_status slq_slq(slq_ctx* ctx, const uint64_t* seeds, int32_t n_probes, int32_t m, double* alpha, double* beta,
+                   int32_t* m_done);
 
 /* Gauss quadrature of T_m (host only, no context, pure): nodes ascending (Ritz values) and
  * weights = squared first components of the normalised eigenvectors (sum 1).

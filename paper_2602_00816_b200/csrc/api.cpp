@@ -342,6 +342,21 @@ slq_status slq_lanczos(slq_ctx* ctx, uint64_t seed, int32_t m, double* alpha, do
   });
 }
 
+slq_status slq_slq(slq_ctx* ctx, const uint64_t* seeds, int32_t n_probes, int32_t m, double* alpha, double* beta,
+                   int32_t* m_done) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    SLQ_CHECK_ARG(seeds && n_probes >= 1 && m >= 1 && alpha && (m == 1 || beta), "seeds / n_probes / m / outputs");
+    check_device(ctx);
+    std::vector<double> b(std::max(m - 1, 1));
+    for (int p = 0; p < n_probes; ++p) {
+      ctx->engine->lanczos(seeds[p], m, alpha + (int64_t)p * m, b.data());
+      for (int i = 0; i + 1 < m; ++i) beta[(int64_t)p * (m - 1) + i] = b[i];
+      if (m_done) m_done[p] = ctx->engine->last_info.m_done;
+    }
+  });
+}
+
 slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_next, int32_t* nonfinite) {
   if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
   const LanczosInfo& i = ctx->engine->last_info;

@@ -74,6 +74,7 @@ def lib() -> ctypes.CDLL:
         "slq_grad": (I32, [P, P, P]),
         "slq_lanczos": (I32, [P, U64, I32, P, P]),
         "slq_lanczos_info": (I32, [P, P, P, P]),
+        "slq_slq": (I32, [P, P, I32, I32, P, P, P]),
         "slq_quadrature": (I32, [P, P, I32, P, P]),
         "slq_ghost_clusters": (I32, [P, I32, D, P, P, P]),
         "slq_density": (I32, [P, P, P, I32, I32, P, P, I32, D, P]),
@@ -328,6 +329,16 @@ class SlqContext:
         b = np.empty(max(m - 1, 1))
         _check(lib().slq_lanczos(self._h, ctypes.c_uint64(seed), m, a.ctypes.data, b.ctypes.data), self._h)
         return a, b[:m - 1]
+
+    def slq(self, seeds, m: int):
+        """All probes' (alpha [s][m], beta [s][m-1], m_done [s]) -- slq_slq."""
+        sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+        a = np.empty((sd.size, m))
+        b = np.empty((sd.size, max(m - 1, 1)))
+        md = np.empty(sd.size, dtype=np.int32)
+        _check(lib().slq_slq(self._h, sd.ctypes.data, sd.size, m, a.ctypes.data, b.ctypes.data, md.ctypes.data),
+               self._h)
+        return a, b[:, :m - 1], md
 
     def lanczos_info(self) -> dict:
         md, bn, nf = ctypes.c_int32(), ctypes.c_double(), ctypes.c_int32()

@@ -233,3 +233,32 @@ def test_lanczos_breakdown_detected_post_hoc():
     scale = max(abs(n2[0]), abs(n2[-1]))
     assert abs(n1[0] - n2[0]) <= 1e-5 * scale and abs(n1[-1] - n2[-1]) <= 1e-5 * scale
     assert abs(w1.sum() - 1) < 1e-12
+
+
+def test_slq_probe_loop_and_density():
+    """slq_slq runs the probe loop of SLQ: every probe equals its own slq_lanczos call
+    bit for bit, and the probe-averaged moments of the GPU node sets match the oracle's SLQ on the
+    same probes (mu_0 = 1, mu_1 and mu_2 within the fp32 gates)."""
+    cfg = si.CONFIGS["gpt_tiny"]
+    m, seeds = 8, [cfg.probe_seed0 + j for j in range(3)]
+    with _ctx(cfg, reorth="full", max_steps=m) as c:
+        A, B, md = c.slq(seeds, m)
+        single = [c.lanczos(sd, m) for sd in seeds]
+    for p in range(3):
+        assert md[p] == m
+        assert np.array_equal(A[p], single[p][0]) and np.array_equal(B[p], single[p][1])
+    th = si.init_params(cfg)
+    g = fdhvp.make_grad_fn(cfg, _batch(cfg))
+    ns, ws, rn, rw = [], [], [], []
+    for p, sd in enumerate(seeds):
+        n, w = slq.quadrature(A[p], B[p])
+        ns.append(n); ws.append(w)
+        r = OL.lanczos(lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact"), probe.rademacher_probe(sd, th.size),
+                       m, "full")
+        n2, w2 = OL.gauss_quadrature(r.alpha, r.beta)
+        rn.append(n2); rw.append(w2)
+    mom, _ = slq.density(ns, ws, jmax=2)
+    ref = OL.slq_moments(rn, rw, jmax=2)
+    print(f"gpt_tiny SLQ moments {mom} vs {ref}")
+    assert abs(mom[0] - 1) < 1e-12
+    assert abs(mom[1] - ref[1]) <= 1e-5 * np.sqrt(ref[2]) and abs(mom[2] - ref[2]) <= 1e-5 * ref[2]
