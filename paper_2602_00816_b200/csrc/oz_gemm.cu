@@ -35,9 +35,9 @@ namespace oz {
 
 using namespace tc;
 
-constexpr int BM = 128, BN = 64, BK = 64, UMMA_K = 32;
+constexpr int BM = 128, BK = 64, UMMA_K = 32;
 
-template <int S>
+template <int S, int BN>
 struct Cfg {
   static constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;  // bytes
   static constexpr int A_BYTES = S * A_PLANE, B_BYTES = S * B_PLANE;
@@ -88,11 +88,11 @@ __device__ __forceinline__ double exp2i(int e) { return __longlong_as_double((lo
 // tile x K split).  The TMA producer runs ahead across unit boundaries (ring of STAGES k-tiles);
 // the epilogue drains the S accumulators from TMEM into registers, releases TMEM (the next unit's
 // MMAs start), then does the scaling and the global stores while the next unit computes.
-template <int S>
+template <int S, int BN>
 __global__ void __launch_bounds__(320, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
               GemmArgs<double> p, double* __restrict__ ws) {
-  using CF = Cfg<S>;
+  using CF = Cfg<S, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES);
@@ -211,18 +211,21 @@ __global__ void __launch_bounds__(320, 1)
     // ---- epilogue (warps 2..9): warp w drains TMEM lanes 32 (w % 4) .. +31 (its quadrant), columns
     // [32 h, 32 h + 32) with h = (w - 2) / 4, combining the S digit weights in fp64 ----
     const int lg = (warp % 4) * 32;
-    const int c0 = ((warp - 2) / 4) * 32;
     int tl = 0;
     for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
       int m0, n0, sp, kt0, nloc;
       decode(w, m0, n0, sp, kt0, nloc);
+     for (int jb = 0; jb < BN / 64; ++jb) {  // 64-column blocks of the tile
+      const int c0 = ((warp - 2) / 4) * 32 + 64 * jb;
       // scales first (their global-load latency overlaps the wait for the accumulators):
       // lane l holds 2^f for column n0 + c0 + l and 2^e for row m0 + lg + l
       const int n_l = n0 + c0 + lane, row_l = m0 + lg + lane;
       const double sc_l = n_l < p.N ? exp2i(o.eb[n_l]) : 0.0;
       const double sr = (nloc > 0 && row_l < p.M) ? exp2i(o.ea[row_l]) : 0.0;
-      mbar_wait(tmem_full, tl & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      if (jb == 0) {
+        mbar_wait(tmem_full, tl & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      }
       double v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.0;
@@ -241,10 +244,12 @@ __global__ void __launch_bounds__(320, 1)
           for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r1[i]), w1, v[i]);
         }
       }
-      // accumulators drained: release TMEM to the next unit's MMAs
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
+      // accumulators drained (all column blocks): release TMEM to the next unit's MMAs
+      if (jb == BN / 64 - 1) {
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
+      }
       // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
       // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
       // sectors) instead of 32 rows x 8 bytes
@@ -300,6 +305,7 @@ __global__ void __launch_bounds__(320, 1)
           p.C[(int64_t)m * p.ldc + n] = p.accumulate ? cold[j] + out : out;
         }
       }
+     }  // column blocks
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -478,12 +484,12 @@ static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-template <int S>
+template <int S, int BN>
 void run(const Launch& L, const GemmArgs<double>& a) {
-  using CF = Cfg<S>;
+  using CF = Cfg<S, BN>;
   static bool attr = false;
   if (!attr) {
-    SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr = true;
   }
   const int M = a.M, N = a.N, K = a.K;
@@ -552,7 +558,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     LaunchScope scope(L.prof, KC_GEMM_I8, L.stream, 2.0 * M * N * (double)K * CF::NPROD,
                       (double)S * ((double)M * K + (double)N * K) + 8.0 * M * N);
     const int nwork = tiles * splits;
-    k_oz_gemm<S><<<std::min(nwork, 148), 320, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
+    k_oz_gemm<S, BN><<<std::min(nwork, 148), 320, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }
@@ -589,11 +595,15 @@ double oz_min_mnk() {
 
 void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
   SLQ_CHECK_ARG(a.batch == 1 && a.tri == TRI_NONE && a.M > 0 && a.N > 0 && a.K > 0, "oz gemm: batch 1, dense");
+  static const bool wide = getenv("SLQ_OZ_BN") && atoi(getenv("SLQ_OZ_BN")) == 128;  // diagnostic
   switch (S) {
-    case 4: oz::run<4>(L, a); break;
-    case 5: oz::run<5>(L, a); break;
-    case 6: oz::run<6>(L, a); break;
-    default: oz::run<7>(L, a); break;
+    case 4:
+      if (wide) oz::run<4, 128>(L, a);
+      else oz::run<4, 64>(L, a);
+      break;
+    case 5: oz::run<5, 64>(L, a); break;
+    case 6: oz::run<6, 64>(L, a); break;
+    default: oz::run<7, 64>(L, a); break;
   }
 }
 
