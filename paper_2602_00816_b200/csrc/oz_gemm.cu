@@ -316,6 +316,244 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+// ---- wide variant: S = 7, 128 x 128 tiles, accumulators in two phases ----
+// The INT8 pipe runs far closer to its peak with N = 128 MMAs than with N = 64 (75% vs 41% pipe
+// activity), but 7 accumulators of 128 columns exceed the 512 TMEM columns.  So each
+// tile is computed in two phases over its k-range: digit weights g = 0..3 (4 x 128 columns, digit
+// planes 0..3 of both operands, 10 products), drained into fp64 registers, then g = 4..6 (3 x 128
+// columns, planes 0..6, 18 products) -- the same 28 products, with the phase-0 planes re-streamed.
+// 32-byte k-tiles (SWIZZLE_32B, one MMA per product per k-tile) keep three 56 KB stages.
+constexpr int WBN = 128, WBK = 32, WS = 7;
+struct CfgW {
+  static constexpr int PLANE = BM * WBK;  // bytes (A and B planes are both 128 x 32)
+  static constexpr int STAGE_BYTES = 2 * WS * PLANE;
+  static constexpr int STAGES = 3;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 8 * 128 * 8;
+  static_assert(SMEM <= 232448, "dynamic shared memory per CTA");
+};
+
+__global__ void __launch_bounds__(320, 1)
+    k_oz_gemm_w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
+                GemmArgs<double> p, double* __restrict__ ws) {
+  using CF = CfgW;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES);
+  uint64_t* empty = full + CF::STAGES;
+  uint64_t* tmem_full = empty + CF::STAGES;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+  double* stage_t = reinterpret_cast<double*>(smem + CF::STAGES * CF::STAGE_BYTES + 256);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles_n = (p.N + WBN - 1) / WBN, tiles_m = (p.M + BM - 1) / BM;
+  const int nwork = tiles_n * tiles_m * o.splits;
+  auto decode = [&](int w, int& m0, int& n0, int& sp, int& kt0, int& nloc) {
+    sp = w % o.splits;
+    const int t = w / o.splits;
+    n0 = (t % tiles_n) * WBN;
+    m0 = (t / tiles_n) * BM;
+    kt0 = sp * o.kt_per_split;
+    const int kt1 = min(o.nk, kt0 + o.kt_per_split);
+    nloc = kt1 > kt0 ? kt1 - kt0 : 0;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CF::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_holder)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: per tile, phase 0 (planes 0..3) then phase 1 (planes 0..6) ----
+      int it = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        int m0, n0, sp, kt0, nloc;
+        decode(w, m0, n0, sp, kt0, nloc);
+        for (int ph = 0; ph < 2; ++ph) {
+          const int np = ph == 0 ? 4 : WS;
+          for (int i = 0; i < nloc; ++i, ++it) {
+            const int kt = kt0 + i, s = it % CF::STAGES;
+            mbar_wait(&empty[s], ((it / CF::STAGES) & 1) ^ 1);
+            uint8_t* sa = smem + s * CF::STAGE_BYTES;
+            uint8_t* sb = sa + WS * CF::PLANE;
+            mbar_expect_tx(&full[s], 2 * np * CF::PLANE);
+            for (int q = 0; q < np; ++q) {
+              tma_load_2d(sa + q * CF::PLANE, &tmA, &full[s], kt * WBK, q * o.M + m0);
+              tma_load_2d(sb + q * CF::PLANE, &tmB, &full[s], kt * WBK, q * o.N + n0);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      constexpr uint32_t idesc = make_idesc_i8(BM, WBN);
+      int it = 0, use = 0;  // use: tmem_full / tmem_empty handshakes so far
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        int m0, n0, sp, kt0, nloc;
+        decode(w, m0, n0, sp, kt0, nloc);
+        for (int ph = 0; ph < 2; ++ph, ++use) {
+          mbar_wait(tmem_empty, (use & 1) ^ 1);  // the epilogue drained the previous phase
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          const int g0 = ph == 0 ? 0 : 4, g1 = ph == 0 ? 4 : WS;
+          uint32_t started = 0;
+          for (int i = 0; i < nloc; ++i, ++it) {
+            const int s = it % CF::STAGES;
+            mbar_wait(&full[s], (it / CF::STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+            const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
+            const uint32_t sb = sa + WS * CF::PLANE;
+            for (int g = g0; g < g1; ++g) {
+              const uint32_t acc_col = (uint32_t)((g - g0) * WBN);
+              for (int pa = 0; pa <= g; ++pa) {
+                const int qb = g - pa;
+                if (pa >= WS || qb >= WS) continue;
+                const uint64_t da = make_desc_sw32(sa + pa * CF::PLANE);
+                const uint64_t db = make_desc_sw32(sb + qb * CF::PLANE);
+                const uint32_t acc = (started >> g) & 1u;
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + acc_col),
+                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                started |= 1u << g;
+              }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(&empty[s])));
+          }
+          if (nloc > 0) {
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(tmem_full)));
+          } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_full)));
+          }
+        }
+      }
+    }
+  } else {
+    // ---- epilogue (warps 2..9): lanes 32 (w % 4) .. +31, columns [64 h, 64 h + 64) with h = (w-2)/4 ----
+    const int lg = (warp % 4) * 32;
+    const int ch = ((warp - 2) / 4) * 64;
+    int use = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+      int m0, n0, sp, kt0, nloc;
+      decode(w, m0, n0, sp, kt0, nloc);
+      const int row_l = m0 + lg + lane;
+      const double sr = (nloc > 0 && row_l < p.M) ? exp2i(o.ea[row_l]) : 0.0;
+      double sc_l[2];
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        const int n_l = n0 + ch + 32 * jb + lane;
+        sc_l[jb] = n_l < p.N ? exp2i(o.eb[n_l]) : 0.0;
+      }
+      double v[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = 0.0;
+#pragma unroll 1
+      for (int ph = 0; ph < 2; ++ph, ++use) {
+        mbar_wait(tmem_full, use & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const int g0 = ph == 0 ? 0 : 4, g1 = ph == 0 ? 4 : WS;
+#pragma unroll 1
+        for (int g = g0; g < g1; ++g) {
+          uint32_t r0[32], r1[32];
+          const uint32_t base = tmem + ((uint32_t)lg << 16) + (uint32_t)((g - g0) * WBN + ch);
+          tmem_ld32(base, r0);
+          tmem_ld32(base + 32, r1);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+          const double wg = exp2i(-7 * (g + 2));
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v[i] = fma(i2d(r0[i]), wg, v[i]);
+            v[32 + i] = fma(i2d(r1[i]), wg, v[32 + i]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
+      }
+      double* T = stage_t + (warp - 2) * 128;
+      const bool plain = o.splits > 1 || (!p.bias && !p.resid && !p.aux && !p.accumulate && p.act == ACT_NONE &&
+                                          p.alpha == 1.0);
+      double* Wd = o.splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
+      const int64_t ldw = o.splits > 1 ? p.N : p.ldc;
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        const int c0 = ch + 32 * jb;
+        const int ncol = p.N - (n0 + c0);
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          __syncwarp();
+          *reinterpret_cast<double2*>(&T[lane * 4]) = make_double2(v[32 * jb + c] * sr, v[32 * jb + c + 1] * sr);
+          *reinterpret_cast<double2*>(&T[lane * 4 + 2]) =
+              make_double2(v[32 * jb + c + 2] * sr, v[32 * jb + c + 3] * sr);
+          __syncwarp();
+          const int cc = c + (lane & 3);
+          const int n = n0 + c0 + cc;
+          const bool colok = cc < ncol;
+          const double sc = __shfl_sync(0xffffffffu, sc_l[jb], cc);
+          double x[4], bs = 0.0, rs[4], ax[4], cold[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int m = m0 + lg + 8 * j + (lane >> 2);
+            const bool ok = colok && m < p.M;
+            x[j] = T[(8 * j + (lane >> 2)) * 4 + (lane & 3)] * sc;
+            if (!plain) {
+              rs[j] = (ok && p.resid) ? p.resid[(int64_t)m * p.ldr + n] : 0.0;
+              ax[j] = (ok && p.aux) ? p.aux[(int64_t)m * p.ldaux + n] : 0.0;
+              cold[j] = (ok && p.accumulate) ? p.C[(int64_t)m * p.ldc + n] : 0.0;
+            }
+          }
+          if (!plain && colok && p.bias) bs = p.bias[n];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int m = m0 + lg + 8 * j + (lane >> 2);
+            if (!colok || m >= p.M) continue;
+            if (plain) {
+              Wd[(int64_t)m * ldw + n] = x[j];
+              continue;
+            }
+            const double y = p.alpha * x[j] + bs + rs[j];
+            double out;
+            switch (p.act) {
+              case ACT_GELU:
+                p.C2[(int64_t)m * p.ldc2 + n] = y;
+                out = gemm_detail::gelu_tanh(y);
+                break;
+              case ACT_TANH: out = tanh(y); break;
+              case ACT_DGELU: out = y * gemm_detail::gelu_tanh_grad(ax[j]); break;
+              case ACT_DTANH: out = y * (1.0 - ax[j] * ax[j]); break;
+              default: out = y;
+            }
+            p.C[(int64_t)m * p.ldc + n] = p.accumulate ? cold[j] + out : out;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512));
+  }
+}
+
 // The S digits of x for row exponent e (|x| < 2^e): the truncated base-128 expansion of x 2^-e,
 // d_p = trunc(128 r_p), r_{p+1} = 128 r_p - d_p.  Computed exactly in integers:
 // Q = trunc(x 2^(7S - e)) (an exact power-of-two scaling, |Q| < 2^(7S)), d_p = sign(x) *
@@ -469,14 +707,16 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
 }
 
 // 2-D int8 tensor [rows x cols] (row pitch ld bytes), box {64, box_rows}, 64-byte swizzle
-static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                               int box_cols = BK) {
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(SLQ_ECUDA, "cuTensorMapEncodeTiled (int8) failed: " + std::to_string((int)r));
   return m;
@@ -484,21 +724,26 @@ static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-template <int S, int BN>
+// W: the wide two-phase kernel (S = 7, BN = 128, 32-byte k-tiles)
+template <int S, int BN, bool W = false>
 void run(const Launch& L, const GemmArgs<double>& a) {
-  using CF = Cfg<S, BN>;
+  using CF = Cfg<S, W ? 64 : BN>;  // (the wide kernel has its own CfgW; NPROD is the same)
+  constexpr int KT = W ? WBK : BK;
   static bool attr = false;
   if (!attr) {
-    SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    if constexpr (W)
+      SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgW::SMEM));
+    else
+      SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr = true;
   }
   const int M = a.M, N = a.N, K = a.K;
   const int Kp = (int)ceil_div(K, 16) * 16;
-  const int nk = (int)ceil_div(K, BK);
+  const int nk = (int)ceil_div(K, KT);
   // split-K: one CTA per SM (the stage ring fills the shared memory), so fill the 148 SMs with
   // tiles x splits <= 148; every split's K range keeps |acc| <= S * Ksplit * 127^2 < 2^31
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
-  const int kt_cap = (int)std::max<int64_t>(1, ((int64_t)2147483647 / ((int64_t)S * 127 * 127)) / BK);
+  const int kt_cap = (int)std::max<int64_t>(1, ((int64_t)2147483647 / ((int64_t)S * 127 * 127)) / KT);
   int splits = tiles < 148 ? std::max(1, std::min(148 / tiles, nk / 2)) : 1;
   splits = std::max<int>(splits, (int)ceil_div(nk, kt_cap));
   const int ktps = (int)ceil_div(nk, splits);
@@ -550,15 +795,18 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }
-  const CUtensorMap ta = make_map_i8(as, (int64_t)S * M, Kp, Kp, BM);
-  const CUtensorMap tb = make_map_i8(bs, (int64_t)S * N, Kp, Kp, BN);
+  const CUtensorMap ta = make_map_i8(as, (int64_t)S * M, Kp, Kp, BM, KT);
+  const CUtensorMap tb = make_map_i8(bs, (int64_t)S * N, Kp, Kp, BN, KT);
   static const int dbg = getenv("SLQ_OZ_DEBUG") ? atoi(getenv("SLQ_OZ_DEBUG")) : 0;
   OzArgs o{M, N, nk, ktps, splits, ea, eb, dbg};
   {
     LaunchScope scope(L.prof, KC_GEMM_I8, L.stream, 2.0 * M * N * (double)K * CF::NPROD,
                       (double)S * ((double)M * K + (double)N * K) + 8.0 * M * N);
     const int nwork = tiles * splits;
-    k_oz_gemm<S, BN><<<std::min(nwork, 148), 320, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
+    if constexpr (W)
+      k_oz_gemm_w<<<std::min(nwork, 148), 320, CfgW::SMEM, L.stream>>>(ta, tb, o, a, ws);
+    else
+      k_oz_gemm<S, BN><<<std::min(nwork, 148), 320, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }
@@ -603,7 +851,16 @@ void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
       break;
     case 5: oz::run<5, 64>(L, a); break;
     case 6: oz::run<6, 64>(L, a); break;
-    default: oz::run<7, 64>(L, a); break;
+    default: {
+      // the wide two-phase kernel when it has enough 128 x 128 tiles to fill the GPU
+      static const int wide_env = getenv("SLQ_OZ_WIDE") ? atoi(getenv("SLQ_OZ_WIDE")) : 0;
+      const int64_t t128 = ceil_div(a.M, oz::BM) * ceil_div(a.N, oz::WBN);
+      if (wide_env == 2 || (wide_env == 1 && t128 >= 148))
+        oz::run<7, 128, true>(L, a);
+      else
+        oz::run<7, 64>(L, a);
+      break;
+    }
   }
 }
 

@@ -59,6 +59,18 @@ __device__ __forceinline__ uint64_t make_desc_sw64(uint32_t saddr) {
   return d;
 }
 
+// UMMA shared-memory descriptor, K-major operand staged by TMA with 32-byte swizzle:
+// SBO = 256 B (8 rows x 32 B swizzle atom), version 1, layout SWIZZLE_32B (6)
+__device__ __forceinline__ uint64_t make_desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;   // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(256 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;           // descriptor version (sm_100)
+  d |= (uint64_t)6 << 61;           // SWIZZLE_32B
+  return d;
+}
+
 // ---- host: tensor maps through the driver entry point (no libcuda link) ----
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
