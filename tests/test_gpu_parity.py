@@ -262,3 +262,23 @@ def test_slq_probe_loop_and_density():
     print(f"gpt_tiny SLQ moments {mom} vs {ref}")
     assert abs(mom[0] - 1) < 1e-12
     assert abs(mom[1] - ref[1]) <= 1e-5 * np.sqrt(ref[2]) and abs(mom[2] - ref[2]) <= 1e-5 * ref[2]
+
+
+def test_error_codes():
+    """Documented failure modes (include/slq.h): bad arguments -> SLQ_EINVAL, a non-finite
+    direction -> SLQ_ENUMERIC; the context stays usable afterwards."""
+    cfg = si.CONFIGS["gpt_tiny"]
+    with _ctx(cfg, reorth="full", max_steps=4) as c:
+        v = torch.zeros(c.P_loc, dtype=torch.float32, device="cuda")
+        out = torch.empty_like(v)
+        for bad in (lambda: c.lanczos(cfg.probe_seed0, 0), lambda: c.lanczos(cfg.probe_seed0, 5),
+                    lambda: c.hvp(v, out, -1.0), lambda: c.cg(v, v, 0.1, 3)):
+            with pytest.raises(slq.SlqError) as e:
+                bad()
+            assert e.value.status == slq.SLQ_EINVAL
+        v[3] = float("nan")
+        with pytest.raises(slq.SlqError) as e:
+            c.hvp(v, out, 1e-3)
+        assert e.value.status == slq.SLQ_ENUMERIC
+        a, b = c.lanczos(cfg.probe_seed0, 4)  # still usable
+        assert np.all(np.isfinite(a)) and np.all(np.isfinite(b))
