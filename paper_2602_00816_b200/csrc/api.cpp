@@ -100,9 +100,18 @@ void* Workspace::get(size_t need, cudaStream_t) {
   bytes = nb;
   return ptr;
 }
+unsigned* Workspace::counters(size_t n) {
+  if (n > kCounters) return nullptr;
+  if (!cnt) {
+    SLQ_CUDA(cudaMalloc(&cnt, sizeof(unsigned) * kCounters));
+    SLQ_CUDA(cudaMemset(cnt, 0, sizeof(unsigned) * kCounters));
+  }
+  return cnt;
+}
 Workspace::~Workspace() {
   cudaDeviceSynchronize();
   if (ptr) cudaFree(ptr);
+  if (cnt) cudaFree(cnt);
   for (void* p : retired) cudaFree(p);
 }
 

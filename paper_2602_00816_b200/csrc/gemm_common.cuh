@@ -98,13 +98,18 @@ __device__ __forceinline__ void epilogue_store2(const GemmArgs<double>& p, doubl
   else { C[m64 * p.ldc + n] = o0; C[m64 * p.ldc + n + 1] = o1; }
 }
 
+// ws holds the fp32/fp64 partials of batch entry z, split k at ws[(z * splits + k) * M * N]
+// (row-major M x N); the sum over k in fixed order goes through the regular epilogue into C(z)
 template <class T>
 __global__ void splitk_reduce(GemmArgs<T> p, int splits, const T* __restrict__ ws) {
-  const int64_t mn = (int64_t)p.M * p.N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mn; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t mn = (int64_t)p.M * p.N, tot = mn * p.batch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int z = (int)(i / mn);
+    const int64_t e = i - z * mn;
+    const T* w = ws + (int64_t)z * splits * mn + e;
     T s = T(0);
-    for (int k = 0; k < splits; ++k) s += ws[k * mn + i];
-    epilogue_store(p, p.C, (int)(i / p.N), (int)(i % p.N), s);
+    for (int k = 0; k < splits; ++k) s += w[k * mn];
+    epilogue_store(p, p.C + boff(p.offC, z), (int)(e / p.N), (int)(e % p.N), s);
   }
 }
 

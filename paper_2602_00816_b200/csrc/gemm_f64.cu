@@ -61,7 +61,7 @@ struct Smem {
 
 template <class TL, bool AK, bool BKm>
 __global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : 1) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
-                                                                double* __restrict__ ws) {
+                                                                double* __restrict__ ws, unsigned* __restrict__ cnt) {
   using SM = Smem<TL, AK, BKm>;
   constexpr int BM = TL::BM, BN = TL::BN, BK = TL::BK, S = TL::STAGES;
   constexpr int WM = TL::WM, WN = TL::WN, TM = TL::TM, TN = TL::TN;
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : 1) gemm_
       Cs[r * LDC + c + 1] = acc[i][j][1];
     }
   __syncthreads();
-  double* C_ = splits > 1 ? ws + (int64_t)split * p.M * p.N : p.C + boff(p.offC, z);
+  double* C_ = splits > 1 ? ws + ((int64_t)z * splits + split) * p.M * p.N : p.C + boff(p.offC, z);
   const int rows = min(BM, p.M - m0), cols = min(BN, p.N - n0);
   // column pairs; 16-byte accesses when every pitch is even and every base 16-byte aligned
   const int64_t ldo = splits > 1 ? p.N : p.ldc;
@@ -215,6 +215,39 @@ __global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : 1) gemm_
         if (c + 1 < cols) dst[1] = v1;
       }
     }
+    if (splits == 1 || !cnt) return;
+    // split-K reduction in the last CTA of the tile to arrive (threadfence + per-tile counter):
+    // it sums the splits' partials in split order 0..splits-1 -- the order of splitk_reduce, so
+    // the result does not depend on which CTA arrives last -- and applies the fused epilogue
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    const int64_t tile = ((int64_t)z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (tid == 0) last = atomicAdd(cnt + tile, 1u) == (unsigned)splits - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int64_t mn = (int64_t)p.M * p.N;
+    const double* part = ws + (int64_t)z * splits * mn;
+    double* Cz = p.C + boff(p.offC, z);
+    const bool vc = (p.ldc % 2) == 0 && al(Cz) && (!p.bias || al(p.bias)) &&
+                    (!p.resid || ((p.ldr % 2) == 0 && al(p.resid))) &&
+                    (!p.aux || ((p.ldaux % 2) == 0 && al(p.aux))) &&
+                    (!p.C2 || ((p.ldc2 % 2) == 0 && al(p.C2)));
+#pragma unroll 1
+    for (int e = tid; e < BM * BN / 2; e += TL::THREADS) {
+      const int r = e / (BN / 2), c = 2 * (e % (BN / 2));
+      if (r >= rows || c >= cols) continue;
+      const int64_t o = (int64_t)(m0 + r) * p.N + n0 + c;
+      double s0 = 0.0, s1 = 0.0;
+      for (int k = 0; k < splits; ++k) {
+        s0 += __ldcg(part + k * mn + o);
+        if (c + 1 < cols) s1 += __ldcg(part + k * mn + o + 1);
+      }
+      if (c + 1 < cols) epilogue_store2(p, Cz, m0 + r, n0 + c, s0, s1, vc);
+      else epilogue_store(p, Cz, m0 + r, n0 + c, s0);
+    }
+    if (tid == 0) cnt[tile] = 0u;  // ready for the next launch on this stream
     return;
   }
 #pragma unroll 1
@@ -242,7 +275,8 @@ int choose_splits(const GemmArgs<double>& a, int tiles, int forced) {
   if (forced > 0) return forced;
   static const int min_k = getenv("SLQ_DMMA_SPLIT_MIN_K") ? atoi(getenv("SLQ_DMMA_SPLIT_MIN_K")) : 256;
   static const int waves = getenv("SLQ_DMMA_SPLIT_WAVES") ? atoi(getenv("SLQ_DMMA_SPLIT_WAVES")) : 2;
-  if (a.batch != 1 || a.tri != TRI_NONE || a.K < min_k || tiles >= waves * 148) return 1;
+  // batched: only the long-K weight-gradient batches (attention batches keep their tuned plans)
+  if ((a.batch != 1 && a.K < 2048) || a.tri != TRI_NONE || a.K < min_k || tiles >= waves * 148) return 1;
   int s = (int)ceil_div(waves * 148, tiles);
   s = std::min<int>(s, (int)(a.K / (4 * TL::BK)));
   return std::max(1, std::min(s, 32));
@@ -262,15 +296,20 @@ void launch(const Launch& L, const GemmArgs<double>& a, int forced_splits) {
   const int kchunk = (int)ceil_div(ceil_div(a.K, splits), TL::BK) * TL::BK;
   splits = std::max(1, (int)ceil_div(a.K, kchunk));
   double* ws = nullptr;
-  if (splits > 1) ws = (double*)L.ws->get(sizeof(double) * (size_t)splits * a.M * a.N, L.stream);
+  unsigned* cnt = nullptr;
+  if (splits > 1) {
+    ws = (double*)L.ws->get(sizeof(double) * (size_t)splits * a.M * a.N * a.batch, L.stream);
+    static const bool ext = getenv("SLQ_DMMA_SPLIT_EXT") && atoi(getenv("SLQ_DMMA_SPLIT_EXT"));
+    if (!ext) cnt = L.ws->counters((size_t)tiles_m * tiles_n * a.batch);
+  }
   dim3 grid(tiles_n, tiles_m, a.batch * splits);
   LaunchScope scope(L.prof, KC_GEMM, L.stream, gemm_flops(a),
                     8.0 * ((double)a.M * a.K + (double)a.K * a.N + (double)a.M * a.N) * a.batch);
-  gemm_dmma_kernel<TL, AK, BKm><<<grid, TL::THREADS, SM::BYTES, L.stream>>>(a, splits, kchunk, ws);
+  gemm_dmma_kernel<TL, AK, BKm><<<grid, TL::THREADS, SM::BYTES, L.stream>>>(a, splits, kchunk, ws, cnt);
   SLQ_CUDA(cudaGetLastError());
   ++*L.launches;
-  if (splits > 1) {
-    const int64_t mn = (int64_t)a.M * a.N;
+  if (splits > 1 && !cnt) {
+    const int64_t mn = (int64_t)a.M * a.N * a.batch;
     int blocks = (int)std::min<int64_t>(ceil_div(mn, 256), 148 * 8);
     splitk_reduce<double><<<blocks, 256, 0, L.stream>>>(a, splits, ws);
     SLQ_CUDA(cudaGetLastError());
@@ -410,7 +449,7 @@ void gemm<double>(const Launch& L, const GemmArgs<double>& a) {
 // Diagnostic (not on the hot path): time one fp64 GEMM shape with a given tile variant
 // (-1 = the production heuristic) and split count (0 = auto).  A is [M x K] (K-contiguous when
 // a_kmajor) and B is [K x N] given as [N x K] when b_kmajor.  Returns TFLOP/s and a checksum
-// of C so that variants can be compared for equality.
+// of C (all batch entries) so that variants can be compared for equality.
 extern "C" slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, int32_t K, int32_t a_kmajor,
                                         int32_t b_kmajor, int32_t variant, int32_t splits, int32_t iters,
                                         double* tflops, double* checksum) {
@@ -458,7 +497,7 @@ extern "C" slq_status slq_diag_gemm_f64(int32_t device, int32_t M, int32_t N, in
     float ms = 0;
     SLQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     *tflops = gemm_flops(a) * iters / (ms * 1e-3) / 1e12;
-    std::vector<double> h((size_t)M * N);
+    std::vector<double> h((size_t)M * N * nb);
     SLQ_CUDA(cudaMemcpy(h.data(), C, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
     double s = 0;
     for (size_t i = 0; i < h.size(); ++i) s += h[i] * (double)((i % 7) + 1);

@@ -17,6 +17,11 @@ struct Workspace {
   size_t bytes = 0;
   std::vector<void*> retired;              // outgrown buffers (graphs may reference them)
   void* get(size_t need, cudaStream_t s);  // grows when too small; never frees a live buffer
+  // zero-initialised arrival counters (fixed size, allocated on first use outside graph capture);
+  // every kernel that uses them leaves them zero again.  nullptr when n exceeds the array.
+  unsigned* cnt = nullptr;
+  static constexpr size_t kCounters = 1 << 16;
+  unsigned* counters(size_t n);
   ~Workspace();
 };
 

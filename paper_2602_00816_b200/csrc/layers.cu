@@ -317,7 +317,34 @@ __global__ void k_colreduce1(int mode, const T* __restrict__ dy, int64_t lddy, c
   const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
   T a0 = T(0), a1 = T(0);
   if (c < cols) {
-    for (int r = r0 + ty; r < r1; r += 8) {
+    // four rows per iteration with every load issued before the first use (memory-level
+    // parallelism: the loop is latency-bound otherwise); rows are summed in increasing order
+    int r = r0 + ty;
+    for (; r + 24 < r1; r += 32) {
+      T d[4], xv[4], mu[4], rs[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t rr = r + 8 * i;
+        d[i] = dy[rr * lddy + c];
+        if (mode != 0) {
+          xv[i] = x[rr * cols + c];
+          rs[i] = rstd[rr];
+          mu[i] = mode == 1 ? mean[rr] : T(0);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (mode == 0) {
+          a0 += d[i];
+        } else if (mode == 1) {
+          a0 += d[i] * (xv[i] - mu[i]) * rs[i];
+          a1 += d[i];
+        } else {
+          a0 += d[i] * xv[i] * rs[i];
+        }
+      }
+    }
+    for (; r < r1; r += 8) {
       const T d = dy[(int64_t)r * lddy + c];
       if (mode == 0) {
         a0 += d;
@@ -611,12 +638,9 @@ void colreduce(const Launch& L, int mode, const T* dy, int64_t lddy, const T* x,
   int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), ceil_div(2 * 148, cblocks)));
   const int rpb = (int)ceil_div(std::max(rows, 1), rblocks);
   rblocks = (int)ceil_div(std::max(rows, 1), rpb);
-  const size_t pbytes = (sizeof(T) * 2 * (size_t)rblocks * cols + 255) & ~(size_t)255;
-  uint8_t* base = (uint8_t*)L.ws->get(pbytes + 256, L.stream);
-  T* part = (T*)base;
+  T* part = (T*)L.ws->get(sizeof(T) * 2 * (size_t)rblocks * cols, L.stream);
   T* part1 = part + (size_t)rblocks * cols;
-  unsigned* counter = (unsigned*)(base + pbytes);
-  SLQ_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), L.stream));
+  unsigned* counter = L.ws->counters(1);  // zero on entry, reset by the last block
   LAUNCH(KC_NORM, dim3(cblocks, rblocks), 256, k_colreduce1<T>, mode, dy, lddy, x, mean, rstd, part, part1, rows,
          cols, rpb, counter, out0, out1, accumulate);
 }
