@@ -441,6 +441,10 @@ void gemm<double>(const Launch& L, const GemmArgs<double>& a) {
   }
   int splits = 0;
   const int v = plan_variant(a, &splits);
+  // experiment knob: divide the planned split counts (the plan was swept on an otherwise idle
+  // GPU; inside the step two or three kernels share it)
+  static const int div = getenv("SLQ_DMMA_SPLIT_DIV") ? std::max(1, atoi(getenv("SLQ_DMMA_SPLIT_DIV"))) : 1;
+  if (div > 1 && splits > 0) splits = std::max(1, splits / div);
   run(L, a, v, splits);
 }
 

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(320, 1)
         decode(w, m0, n0, sp, kt0, nloc);
         mbar_wait(tmem_empty, (tl & 1) ^ 1);  // the previous unit's accumulators have been drained
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-        uint32_t started = 0;  // bit g: accumulator g has been initialised
+        uint32_t started = 0;  // the unit's accumulators have been initialised
         for (int i = 0; i < nloc; ++i, ++it) {
           const int s = it % CF::STAGES;
           const uint32_t ph = (it / CF::STAGES) & 1;
@@ -178,24 +178,30 @@ __global__ void __launch_bounds__(320, 1)
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
           const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
           const uint32_t sb = sa + CF::A_BYTES;
+          // descriptors: one base per operand and stage, plane / k offsets added to the 14-bit
+          // address field (16-byte units; every address stays below 256 KB, so no carry out)
+          const uint64_t da0 = make_desc_sw64(sa), db0 = make_desc_sw64(sb);
+          const uint32_t first = started == 0u;  // first k-tile of the unit: overwrite
+          if (!(o.debug & 1)) {
 #pragma unroll
-          for (int g = 0; g < ((o.debug & 1) ? 0 : S); ++g) {
+            for (int g = 0; g < S; ++g) {
 #pragma unroll
-            for (int pa = 0; pa <= g; ++pa) {
-              const int qb = g - pa;
+              for (int pa = 0; pa <= g; ++pa) {
+                const int qb = g - pa;
 #pragma unroll
-              for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-                const uint64_t da = make_desc_sw64(sa + pa * CF::A_PLANE + kk * UMMA_K);
-                const uint64_t db = make_desc_sw64(sb + qb * CF::B_PLANE + kk * UMMA_K);
-                const uint32_t acc = (started >> g) & 1u;
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(g * BN)),
-                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
-                started |= 1u << g;
+                for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                  const uint64_t da = da0 + (uint64_t)((pa * CF::A_PLANE + kk * UMMA_K) >> 4);
+                  const uint64_t db = db0 + (uint64_t)((qb * CF::B_PLANE + kk * UMMA_K) >> 4);
+                  const uint32_t acc = (pa == 0 && kk == 0) ? (first ^ 1u) : 1u;
+                  asm volatile(
+                      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(g * BN)),
+                      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
               }
             }
           }
+          started = 1u;
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
               smem_u32(&empty[s])));
         }
