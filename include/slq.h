@@ -231,6 +231,14 @@ slq_status slq_collective_counts(const slq_ctx* ctx, int64_t* allgather, int64_t
 int64_t slq_launch_count(const slq_ctx* ctx);
 void* slq_stream(const slq_ctx* ctx);
 
+/* Diagnostic of the collective watchdog: enqueue a kernel that stalls the
+ * context's stream for `stall_ms` (0..10000) milliseconds, then wait for the stream the way every
+ * collective call does, with `timeout_s` (<= 0: no timeout).  Returns SLQ_ETIMEOUT when the stall
+ * outlasts the timeout -- the context's NCCL communicator (if any) is then aborted and every later
+ * collective call returns SLQ_ENCCL -- else SLQ_OK.  Collective calls use the timeout from the
+ * environment variable SLQ_TIMEOUT_S (default 1800 s, 0 = none) and also return SLQ_ENCCL on an
+ * asynchronous NCCL error (e.g. a failed peer), after aborting the communicator. */
+slq_status slq_diag_watchdog(slq_ctx* ctx, int32_t stall_ms, double timeout_s);
 /* Diagnostic, not on the hot path: measured FP64 FMA throughput of `device` in TFLOP/s (the
  * roofline denominator of the fp64 gradient-pass GEMMs, which MEASURED_PEAKS.json lacks). */
 slq_status slq_diag_fp64_peak(int32_t device, double* tflops);

@@ -176,7 +176,13 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-void check_device(slq_ctx* ctx) { SLQ_CUDA(cudaSetDevice(ctx->world.device)); }
+// entry check of every call that runs the engine: the device, and a communicator that a watchdog
+// or an asynchronous NCCL error aborted (its captured graphs reference it: never replay them)
+void check_device(slq_ctx* ctx) {
+  SLQ_CUDA(cudaSetDevice(ctx->world.device));
+  if (ctx->comm && ctx->comm->aborted())
+    throw Error(SLQ_ENCCL, "the NCCL communicator was aborted (watchdog or peer failure); destroy the context");
+}
 
 void ensure_stage(slq_ctx* ctx) {
   if (!ctx->stage_in) {
@@ -317,6 +323,16 @@ slq_status slq_hvp(slq_ctx* ctx, const float* v, float* out, double eps) {
       SLQ_CUDA(cudaMemcpyAsync(out, od, bytes, cudaMemcpyDeviceToHost, ctx->stream));
       SLQ_CUDA(cudaStreamSynchronize(ctx->stream));
     }
+  });
+}
+
+slq_status slq_diag_watchdog(slq_ctx* ctx, int32_t stall_ms, double timeout_s) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  if (stall_ms < 0 || stall_ms > 10000) return fail(ctx, SLQ_EINVAL, "stall_ms must be in [0, 10000]");
+  return guarded(ctx, [&] {
+    check_device(ctx);
+    diag_stall(ctx->stream, stall_ms);
+    watchdog_wait(ctx->stream, ctx->comm.get(), timeout_s);
   });
 }
 

@@ -1,9 +1,12 @@
 #include "comm.h"
 
 #include <nccl.h>
+#include <stdlib.h>
 #include <string.h>
 
+#include <chrono>
 #include <string>
+#include <thread>
 
 #include "common.h"
 
@@ -44,22 +47,61 @@ void Comm::abort() {
   comm_ = nullptr;
 }
 
+#define SLQ_LIVE() \
+  if (!comm_) throw Error(SLQ_ENCCL, "the NCCL communicator was aborted (watchdog or peer failure)")
+
 void Comm::allgather(const void* send, void* recv, size_t count, CommType t, cudaStream_t s) {
+  SLQ_LIVE();
   SLQ_NCCL(ncclAllGather(send, recv, count, nt(t), (ncclComm_t)comm_, s));
   counts.allgather++;
   counts.ag_bytes += (double)count * nsize(t) * world_;
 }
 
 void Comm::reduce_scatter(const void* send, void* recv, size_t count, CommType t, cudaStream_t s) {
+  SLQ_LIVE();
   SLQ_NCCL(ncclReduceScatter(send, recv, count, nt(t), ncclSum, (ncclComm_t)comm_, s));
   counts.reduce_scatter++;
   counts.rs_bytes += (double)count * nsize(t) * world_;
 }
 
 void Comm::allreduce_sum_f64(double* buf, size_t count, cudaStream_t s) {
+  SLQ_LIVE();
   SLQ_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)comm_, s));
   counts.allreduce++;
   counts.ar_bytes += 8.0 * count;
+}
+
+double watchdog_timeout_s() {
+  static const double t = getenv("SLQ_TIMEOUT_S") ? atof(getenv("SLQ_TIMEOUT_S")) : 1800.0;
+  return t;
+}
+
+void watchdog_wait(cudaStream_t s, Comm* comm, double timeout_s) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  for (int polls = 0;; ++polls) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) throw Error(SLQ_ECUDA, std::string("stream: ") + cudaGetErrorString(e));
+    if (comm && !comm->aborted()) comm->check_async();
+    const double dt = std::chrono::duration<double>(clk::now() - t0).count();
+    if (timeout_s > 0 && dt > timeout_s) {
+      if (comm) comm->abort();
+      throw Error(SLQ_ETIMEOUT, "watchdog: the stream did not drain within " + std::to_string(timeout_s) +
+                                    " s (communicator aborted)");
+    }
+    // spin briefly (short kernels), then back off to 50 us sleeps
+    if (polls > 200) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+void Comm::check_async() {
+  ncclResult_t ae = ncclSuccess;
+  if (ncclCommGetAsyncError((ncclComm_t)comm_, &ae) != ncclSuccess) ae = ncclSystemError;
+  if (ae != ncclSuccess && ae != ncclInProgress) {
+    abort();
+    throw Error(SLQ_ENCCL, std::string("NCCL asynchronous error (peer failure?): ") + ncclGetErrorString(ae));
+  }
 }
 
 }  // namespace slq

@@ -25,6 +25,8 @@ class Comm {
   void reduce_scatter(const void* send, void* recv, size_t count_per_rank, CommType t, cudaStream_t s);
   void allreduce_sum_f64(double* buf, size_t count, cudaStream_t s);
   void abort();
+  bool aborted() const { return comm_ == nullptr; }
+  void check_async();  // throws SLQ_ENCCL (after aborting) on an asynchronous NCCL error
   int rank() const { return rank_; }
   int world() const { return world_; }
   CommCounts counts;
@@ -35,5 +37,16 @@ class Comm {
 };
 
 void nccl_unique_id(void* out128);
+
+// Collective watchdog: wait for `s` to drain, polling the stream and, when `comm`
+// is given, the communicator's asynchronous error state.  A NCCL error (e.g. a peer that died)
+// aborts the communicator and throws SLQ_ENCCL; no completion within `timeout_s` seconds
+// (<= 0: wait forever) aborts it and throws SLQ_ETIMEOUT.  Without a communicator (world size 1)
+// only the timeout applies.  After an abort every later collective throws SLQ_ENCCL.
+void watchdog_wait(cudaStream_t s, Comm* comm, double timeout_s);
+// SLQ_TIMEOUT_S from the environment (default 1800 s; 0 disables the timeout)
+double watchdog_timeout_s();
+// diagnostic: a one-thread kernel that keeps `s` busy for `ms` milliseconds (diag.cu)
+void diag_stall(cudaStream_t s, int ms);
 
 }  // namespace slq

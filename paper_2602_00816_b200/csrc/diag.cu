@@ -42,7 +42,24 @@ __global__ void k_dmma_peak(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
+// one thread that spins on the global nanosecond timer for `ns` (the watchdog test's stall)
+__global__ void k_diag_stall(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 }  // namespace
+
+namespace slq {
+void diag_stall(cudaStream_t s, int ms) {
+  k_diag_stall<<<1, 1, 0, s>>>((uint64_t)ms * 1000000ull);
+  SLQ_CUDA(cudaGetLastError());
+}
+}  // namespace slq
 
 extern "C" slq_status slq_diag_dmma_peak(int32_t device, double* tflops) {
   try {

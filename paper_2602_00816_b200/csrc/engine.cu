@@ -419,9 +419,15 @@ struct EngineT : Engine {
   }
 
   // host copy of `cnt` device doubles (synchronises the stream)
+  // every host wait of the engine: with a communicator, through the collective watchdog
+  // (asynchronous NCCL errors -> SLQ_ENCCL, no progress within SLQ_TIMEOUT_S -> SLQ_ETIMEOUT)
+  void sync() {
+    if (comm) watchdog_wait(L.stream, comm, watchdog_timeout_s());
+    else SLQ_CUDA(cudaStreamSynchronize(L.stream));
+  }
   void to_host(const double* dev, int cnt, double* host) {
     SLQ_CUDA(cudaMemcpyAsync(hstage, dev, sizeof(double) * cnt, cudaMemcpyDeviceToHost, L.stream));
-    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    sync();
     memcpy(host, hstage, sizeof(double) * cnt);
   }
 
@@ -455,7 +461,7 @@ struct EngineT : Engine {
     if (!std::isfinite(ss)) throw Error(SLQ_ENUMERIC, "non-finite direction v");
     if (ss == 0.0) {
       SLQ_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)n, L.stream));
-      SLQ_CUDA(cudaStreamSynchronize(L.stream));
+      sync();
       return;
     }
     const double inv2eta = form_points(v, eps / sqrt(ss));
@@ -464,7 +470,7 @@ struct EngineT : Engine {
     fd_out<T>(L, fd_a(), fd_b(), fd_scale(inv2eta), out, n, dflag);
     int flag = 0;
     SLQ_CUDA(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, L.stream));
-    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    sync();
     if (flag) throw Error(SLQ_ENUMERIC, "non-finite gradient in the FD-HVP");
   }
 
@@ -524,7 +530,7 @@ struct EngineT : Engine {
       axpby(L, p, r, 1.0, rr_new / rr, n);
       rr = rr_new;
     }
-    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    sync();
     return std::min(it, max_iter);
   }
 
@@ -550,7 +556,7 @@ struct EngineT : Engine {
 
   void probe(uint64_t seed, float* q) override {
     probe_fill(L, q, n, units_dev, (int)plan.units.size(), seed, 1.0 / sqrt((double)plan.P));
-    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    sync();
   }
 
   // Three-term recurrence without a stored basis (c5 mode; "only the essential Lanczos
@@ -617,7 +623,7 @@ struct EngineT : Engine {
       a_prev = a_carry;
       b_k = bnext;
     }
-    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    sync();
     last_info = info;
     return info;
   }
@@ -699,7 +705,7 @@ struct EngineT : Engine {
     double* hb_pin = hstage + 64 + (max_steps + 1);
     SLQ_CUDA(cudaMemcpyAsync(ha_pin, d_alpha, sizeof(double) * m, cudaMemcpyDeviceToHost, L.stream));
     SLQ_CUDA(cudaMemcpyAsync(hb_pin, d_bhist, sizeof(double) * m, cudaMemcpyDeviceToHost, L.stream));
-    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    sync();
     memcpy(ha.data(), ha_pin, sizeof(double) * m);
     memcpy(hb.data(), hb_pin, sizeof(double) * m);
     // steps after a breakdown ran on a noise direction; they are discarded here
@@ -722,7 +728,7 @@ struct EngineT : Engine {
         break;
       }
     }
-    SLQ_CUDA(cudaStreamSynchronize(L.stream));
+    sync();
     last_info = info;
     return info;
   }

@@ -90,6 +90,7 @@ def lib() -> ctypes.CDLL:
         "slq_diag_dmma_peak": (I32, [I32, P]),
         "slq_diag_gemm_f64": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
         "slq_diag_oz_check": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
+        "slq_diag_watchdog": (I32, [P, I32, D]),
         "slq_cg": (I32, [P, P, P, D, I32, D, P, P]),
         "slq_blockdiag": (I32, [P, U64, P, P]),
     }
@@ -378,6 +379,11 @@ class SlqContext:
         ag, rs, ar = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().slq_collective_counts(self._h, ctypes.byref(ag), ctypes.byref(rs), ctypes.byref(ar)), self._h)
         return {"allgather": ag.value, "reduce_scatter": rs.value, "allreduce": ar.value}
+
+    def diag_watchdog(self, stall_ms: int, timeout_s: float) -> int:
+        """Stall the context's stream for stall_ms, wait through the collective watchdog with
+        timeout_s; returns the status code (SLQ_ETIMEOUT when the stall outlasts the timeout)."""
+        return int(lib().slq_diag_watchdog(self._h, int(stall_ms), float(timeout_s)))
 
     def launch_count(self) -> int:
         return lib().slq_launch_count(self._h)
