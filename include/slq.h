@@ -166,6 +166,11 @@ slq_status slq_grad(slq_ctx* ctx, float* g_shard, double* loss);
 slq_status slq_lanczos(slq_ctx* ctx, uint64_t probe_seed, int32_t m, double* alpha, double* beta);
 slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_next,
                             int32_t* nonfinite);
+/* After slq_hvp returned SLQ_ENUMERIC (non-finite gradient, "error carrying the offending
+ * batch id"): *seq = local index of the first sequence (MLP: data row) whose loss was non-finite
+ * in the theta+ or theta- pass, or -1 when every loss was finite (overflow inside the backward
+ * only).  -1 after a successful slq_hvp.  Host-only, no device work. */
+slq_status slq_nonfinite_seq(const slq_ctx* ctx, int32_t* seq);
 /* Stochastic Lanczos quadrature's probe loop ("T_SLQ ~ s m T_Lanczos iter"):
  * slq_lanczos for each of the n_probes seeds; alpha [n_probes][m], beta [n_probes][m - 1] (host),
  * m_done [n_probes] (may be NULL).  Feed each probe's (alpha, beta) to slq_quadrature and the node

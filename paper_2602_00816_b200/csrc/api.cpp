@@ -382,6 +382,12 @@ slq_status slq_slq(slq_ctx* ctx, const uint64_t* seeds, int32_t n_probes, int32_
   });
 }
 
+slq_status slq_nonfinite_seq(const slq_ctx* ctx, int32_t* seq) {
+  if (!ctx || !seq) return fail(nullptr, SLQ_EINVAL, "ctx / seq");
+  *seq = ctx->engine->nonfinite_seq;
+  return SLQ_OK;
+}
+
 slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_next, int32_t* nonfinite) {
   if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
   const LanczosInfo& i = ctx->engine->last_info;

@@ -454,6 +454,7 @@ struct EngineT : Engine {
   }
 
   void hvp(const float* v, float* out, double eps) override {
+    nonfinite_seq = -1;
     sumsq_partials(L, v, n, partials);
     finish_reduce(vec_nblocks(n), 1, dscal + 0);
     double ss;
@@ -471,7 +472,17 @@ struct EngineT : Engine {
     int flag = 0;
     SLQ_CUDA(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, L.stream));
     sync();
-    if (flag) throw Error(SLQ_ENUMERIC, "non-finite gradient in the FD-HVP");
+    if (flag) {
+      for (auto& x : pe) {
+        if (!x) continue;
+        const int q = x->runner->first_nonfinite_seq();
+        if (q >= 0 && (nonfinite_seq < 0 || q < nonfinite_seq)) nonfinite_seq = q;
+      }
+      throw Error(SLQ_ENUMERIC, "non-finite gradient in the FD-HVP" +
+                                    (nonfinite_seq >= 0 ? " (local sequence " + std::to_string(nonfinite_seq) +
+                                                              " has a non-finite loss)"
+                                                        : std::string(" (all losses finite)")));
+    }
   }
 
   double grad(float* g) override {

@@ -29,6 +29,9 @@ struct Engine {
   // block-diagonal test over the FSDP units: rel_err[u], cosine[u]
   virtual void blockdiag(uint64_t seed, double* rel_err, double* cosine) = 0;
   LanczosInfo last_info;
+  // set by a failing hvp (SLQ_ENUMERIC): local index of the first sequence (MLP: row) with a
+  // non-finite loss in the two passes, -1 if the losses were finite (S:114's "offending batch id")
+  int nonfinite_seq = -1;
 };
 
 std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,

@@ -7,11 +7,23 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "model.h"
 
 namespace slq {
+
+int first_nonfinite_group(const double* dev, int n, int per, cudaStream_t s) {
+  if (n <= 0) return -1;
+  std::vector<double> h((size_t)n);
+  SLQ_CUDA(cudaMemcpyAsync(h.data(), dev, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, s));
+  SLQ_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(h[i])) return i / std::max(per, 1);
+  return -1;
+}
 
 namespace {
 
@@ -254,6 +266,7 @@ struct MlpRunner : Runner<T> {
     loss_rows = A.alloc<double>(std::max(n, 1));
   }
   double tokens_global() const override { return n_glob; }
+  int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, n, 1, L.stream); }
   double flops_per_pass() const override { return 6.0 * n * ((double)din * H + (double)H * C); }
 
   void fwd_bwd(PassIO<T>& io, double* loss_sum) override {
@@ -333,6 +346,7 @@ struct GptRunner : Runner<T> {
     dhf = A.alloc<T>((int64_t)N * D); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * D);
   }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
+  int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, N, Tn, L.stream); }
   double flops_per_pass() const override {
     const double lin = (double)Ly * (3.0 * D * D + D * D + 2.0 * D * F) + (double)V * D;
     const double attn = (double)Ly * 4.0 * Tn * Tn * D * nseq;  // S and PV (full square)
@@ -517,6 +531,7 @@ struct LlamaRunner : Runner<T> {
     df = A.alloc<T>((int64_t)N * F);
   }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
+  int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, N, Tn, L.stream); }
   double flops_per_pass() const override {
     const double lin = (double)Ly * ((double)Wq * D + (double)Hq * hd * D + 3.0 * D * F) + (double)V * D;
     const double attn = (double)Ly * 4.0 * Tn * Tn * Hq * hd * nseq;

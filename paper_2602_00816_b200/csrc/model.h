@@ -47,10 +47,17 @@ struct Runner {
   virtual double flops_per_pass() const = 0;  // algorithmic fwd+bwd FLOPs (this rank)
   // paired evaluation (model_paired.cu): mean = (theta, gbar), diff = (eta v, gtil) in one pass
   virtual bool paired() const { return false; }
+  // after a failed pass: local index of the first sequence (MLP: row) whose loss in this runner's
+  // last pass is non-finite, -1 if every loss was finite (error attribution)
+  virtual int first_nonfinite_seq() { return -1; }
   virtual void fwd_bwd_pair(PassIO<T>& mean, PassIO<T>& diff, double* loss_sum) {
     throw Error(SLQ_EUNSUPPORTED, "paired evaluation not available for this runner");
   }
 };
+
+// first group of `per` consecutive rows of dev[n] (device doubles) holding a non-finite value,
+// -1 if none (synchronous device -> host copy; error paths only)
+int first_nonfinite_group(const double* dev, int n, int per, cudaStream_t s);
 
 template <class T>
 std::unique_ptr<Runner<T>> make_runner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,

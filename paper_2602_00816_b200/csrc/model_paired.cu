@@ -122,6 +122,7 @@ struct PairedGptRunner : Runner<float> {
   }
   bool paired() const override { return true; }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
+  int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, N, Tn, L.stream); }
   double flops_per_pass() const override {  // one paired pass = the FLOPs of two plain passes x2 (pair products)
     const double lin = (double)Ly * (3.0 * D * D + D * D + 2.0 * D * F) + (double)V * D;
     const double attn = (double)Ly * 4.0 * Tn * Tn * D * nseq;

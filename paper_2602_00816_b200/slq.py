@@ -91,6 +91,7 @@ def lib() -> ctypes.CDLL:
         "slq_diag_gemm_f64": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
         "slq_diag_oz_check": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
         "slq_diag_watchdog": (I32, [P, I32, D]),
+        "slq_nonfinite_seq": (I32, [P, P]),
         "slq_cg": (I32, [P, P, P, D, I32, D, P, P]),
         "slq_blockdiag": (I32, [P, U64, P, P]),
     }
@@ -379,6 +380,12 @@ class SlqContext:
         ag, rs, ar = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().slq_collective_counts(self._h, ctypes.byref(ag), ctypes.byref(rs), ctypes.byref(ar)), self._h)
         return {"allgather": ag.value, "reduce_scatter": rs.value, "allreduce": ar.value}
+
+    def nonfinite_seq(self) -> int:
+        """Local sequence (MLP: row) whose loss was non-finite in the last failing hvp, else -1."""
+        q = ctypes.c_int32()
+        _check(lib().slq_nonfinite_seq(self._h, ctypes.byref(q)), self._h)
+        return q.value
 
     def diag_watchdog(self, stall_ms: int, timeout_s: float) -> int:
         """Stall the context's stream for stall_ms, wait through the collective watchdog with

@@ -280,5 +280,26 @@ def test_error_codes():
         with pytest.raises(slq.SlqError) as e:
             c.hvp(v, out, 1e-3)
         assert e.value.status == slq.SLQ_ENUMERIC
+        assert c.nonfinite_seq() == -1  # rejected before any pass ran
         a, b = c.lanczos(cfg.probe_seed0, 4)  # still usable
         assert np.all(np.isfinite(a)) and np.all(np.isfinite(b))
+
+
+@pytest.mark.parametrize("row", [0, 5, 255])
+def test_nonfinite_gradient_names_the_batch(row):
+    """a non-finite gradient is an error "carrying the offending batch id": with one data
+    row of c1's MLP batch set to inf, slq_hvp returns SLQ_ENUMERIC and slq_nonfinite_seq names that
+    row."""
+    cfg = si.CONFIGS["mlp_tiny"] if row < si.CONFIGS["mlp_tiny"].n_rows else si.CONFIGS["c1"]
+    x, y = si.mlp_data(cfg)
+    x = x.copy()
+    x[row, :] = np.inf
+    th = si.init_params(cfg)
+    with slq.SlqContext(cfg, th, (x, y), max_steps=4) as c:
+        v = _to_dev(slq.shard_of(si.random_vector(th.size, 3), c.layout(), 0, 1))
+        out = torch.empty_like(v)
+        with pytest.raises(slq.SlqError) as e:
+            c.hvp(v, out, cfg.eps)
+        assert e.value.status == slq.SLQ_ENUMERIC
+        assert c.nonfinite_seq() == row
+        assert f"local sequence {row}" in str(e.value)
