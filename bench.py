@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
-    p.add_argument("--numerics", default="fp64_oz", choices=["fp64", "fp64_oz", "fp32", "bf16x3", "paired", "paired_fp32"],
+    p.add_argument("--numerics", default="fp64_oz", choices=["fp64", "fp64_oz", "fp32", "bf16x3", "bf16", "paired", "paired_fp32"],
                    help="gradient-pass arithmetic: fp64_oz (default) = fp64 passes with the large GEMMs as "
                         "exact int8 digit products on tcgen05 (Ozaki) and the rest on DMMA; fp64 = all DMMA; "
                         "bf16x3 = fp32-faithful tcgen05")
@@ -321,6 +321,7 @@ def main():
         bf16 = peaks.get("bf16_tflops", 1590.0)
         achieved = st["flops"] / (st["ms"] * 1e-3) / 1e12
         tc_note = {"bf16x3": "tcgen05 kind::f16 bf16 products (6 per fp32-faithful GEMM, all counted)",
+                   "bf16": "tcgen05 kind::f16, one bf16 product per GEMM (native bf16 operands, fp32 accumulation)",
                    "paired": "tcgen05 pair GEMMs (7 + 12 bf16 products per pair GEMM) and SIMT fp32 attention",
                    }.get(args.numerics, "SIMT fp32 (no tensor core)")
         roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s", "frac": achieved / bf16,
@@ -351,7 +352,7 @@ def main():
         "metric": metric_name(cfg.name), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if cfg.name in WEAK else "strong",
-        "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": f"f64 (dense GEMMs with M*N*K >= {float(os.environ.get('SLQ_OZ_MIN_MNK', '1e9')):.0e} as exact int8 digit products on tcgen05, S={os.environ.get('SLQ_OZ_SLICES', '7')}; the rest fp64 DMMA)", "fp32": "f32", "bf16x3": "bf16x3", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
+        "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": f"f64 (dense GEMMs with M*N*K >= {float(os.environ.get('SLQ_OZ_MIN_MNK', '1e9')):.0e} as exact int8 digit products on tcgen05, S={os.environ.get('SLQ_OZ_SLICES', '7')}; the rest fp64 DMMA)", "fp32": "f32", "bf16x3": "bf16x3", "bf16": "bf16", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {'GPT' if cfg.arch == si.ARCH_GPT else 'Llama'} {cfg.n_layers}L "
                                f"d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} V{cfg.vocab}, {si.n_params(cfg)} params "

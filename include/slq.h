@@ -57,7 +57,11 @@ enum { SLQ_ARCH_MLP = 0, SLQ_ARCH_GPT = 1, SLQ_ARCH_LLAMA = 2 };
  * tcgen05 tensor cores with operands split into three bf16 terms (fp32-faithful; the mode for the
  * bf16 models' gates). */
 enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2, SLQ_PASS_PAIRED = 3, SLQ_PASS_PAIRED_FP32 = 4,
-       SLQ_PASS_FP64_OZ = 5 };
+       SLQ_PASS_FP64_OZ = 5, SLQ_PASS_BF16 = 6 };
+/* SLQ_PASS_BF16: "BF16 native" (SURVEY.md §8(a) numerics modes; the paper's own bf16 runs,
+ * P:602): fp32 activations, every non-batched GEMM on tcgen05 with operands rounded once to bf16
+ * (one product, fp32 accumulation).  The throughput mode of the bf16 models; its FD-HVP carries
+ * Theorem 1's bf16 round-off floor and does not meet the parity gates. */
 /* SLQ_PASS_FP64_OZ: as FP64 (fp64 activations and nonlinearities), but every dense non-batched
  * GEMM runs on the tcgen05 INT8 tensor cores as exact digit products (Ozaki scheme: each operand
  * row/column scaled by a power of two and cut into S = 7 signed 7-bit digit planes; the

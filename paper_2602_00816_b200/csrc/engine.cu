@@ -755,7 +755,9 @@ std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& p
     return std::unique_ptr<Engine>(new EngineT<double>(d, plan, b, theta_host, rank, comm, Ld));
   }
   Launch Lf = L;
-  Lf.gemm_mode = (d.pass_numerics == SLQ_PASS_BF16X3 || d.pass_numerics == SLQ_PASS_PAIRED) ? 1 : 0;
+  Lf.gemm_mode = (d.pass_numerics == SLQ_PASS_BF16X3 || d.pass_numerics == SLQ_PASS_PAIRED) ? 1
+                  : d.pass_numerics == SLQ_PASS_BF16                                         ? 3
+                                                                                             : 0;
   return std::unique_ptr<Engine>(new EngineT<float>(d, plan, b, theta_host, rank, comm, Lf));
 }
 

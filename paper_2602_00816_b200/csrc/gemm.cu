@@ -174,8 +174,8 @@ void gemm(const Launch& L, const GemmArgs<T>& a) {
   const bool ak = a.sAk == 1 && !(a.sAm == 1 && a.K == 1);
   const bool bk = a.sBk == 1 && !(a.sBn == 1 && a.K == 1);
   if constexpr (sizeof(T) == 4) {
-    if (L.gemm_mode == 1 && a.batch == 1 && a.K > 0) {
-      gemm_tc_bf16x3(L, a);
+    if ((L.gemm_mode == 1 || L.gemm_mode == 3) && a.batch == 1 && a.K > 0) {
+      gemm_tc_bf16x3(L, a, L.gemm_mode == 3 ? 1 : 3);
       return;
     }
   }

@@ -30,7 +30,8 @@ struct Launch {
   Profiler* prof;
   Workspace* ws;      // split-K / reduction scratch
   int64_t* launches;  // launch counter
-  int gemm_mode = 0;  // float GEMMs: 0 = SIMT fp32, 1 = tcgen05 bf16x3 split (fp32-faithful);
+  int gemm_mode = 0;  // float GEMMs: 0 = SIMT fp32, 1 = tcgen05 bf16x3 split (fp32-faithful),
+                      // 3 = tcgen05 single bf16 term (native bf16);
                       // double GEMMs: 0 = DMMA (mma.sync f64), 2 = tcgen05 int8 Ozaki (gemm_oz)
 };
 
@@ -86,8 +87,9 @@ double oz_min_mnk();  // FP64_OZ: smaller GEMMs (M N K below this) stay on DMMA 
 
 // fp32-faithful GEMM on the tcgen05 tensor cores: every fp32 operand is split into three bf16
 // terms (x = x0 + x1 + x2, 24 significant bits) and the six products with i + j <= 2 are
-// accumulated in one fp32 TMEM accumulator (tc_gemm.cu).  batch == 1 only.
-void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a);
+// accumulated in one fp32 TMEM accumulator (tc_gemm.cu).  batch == 1 only.  terms = 1: the
+// operands are rounded once to bf16 and one product is formed (the native-bf16 pass mode).
+void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a, int terms = 3);
 
 // building blocks of multi-operand tcgen05 GEMMs (tc_gemm.cu)
 struct TcTerms {  // three bf16 terms of one fp32 operand, K-contiguous [rows x ldk]

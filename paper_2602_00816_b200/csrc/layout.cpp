@@ -12,7 +12,7 @@ const TensorSlot& UnitPlan::t(const std::string& n) const {
 
 void validate_desc(const slq_model_desc& d) {
   SLQ_CHECK_ARG(d.arch == SLQ_ARCH_MLP || d.arch == SLQ_ARCH_GPT || d.arch == SLQ_ARCH_LLAMA, "arch");
-  SLQ_CHECK_ARG(d.pass_numerics >= SLQ_PASS_FP64 && d.pass_numerics <= SLQ_PASS_FP64_OZ, "pass_numerics");
+  SLQ_CHECK_ARG(d.pass_numerics >= SLQ_PASS_FP64 && d.pass_numerics <= SLQ_PASS_BF16, "pass_numerics");
   SLQ_CHECK_ARG(d.param_dtype == SLQ_PARAM_FP32 || d.param_dtype == SLQ_PARAM_BF16, "param_dtype");
   SLQ_CHECK_ARG(d.reorth == SLQ_REORTH_NONE || d.reorth == SLQ_REORTH_FULL || d.reorth == SLQ_REORTH_WINDOW,
                 "reorth");

@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(192, 1)
 
 // x = t0 + t1 + t2 in bf16 terms (each residual is exact in fp32); optional transpose through a
 // 32 x 32 shared tile so that every operand reaches the tensor core K-contiguous
-template <bool TRANS>
+template <bool TRANS, int NT = 3>
 __global__ void k_split3(const float* __restrict__ X, int64_t R, int64_t C, int64_t ld, __nv_bfloat16* __restrict__ o0,
                          __nv_bfloat16* __restrict__ o1, __nv_bfloat16* __restrict__ o2, int64_t ldo) {
   __shared__ float tile[32][33];
@@ -355,13 +355,15 @@ __global__ void k_split3(const float* __restrict__ X, int64_t R, int64_t C, int6
       if (orow >= R || ocol >= C) continue;
     }
     const __nv_bfloat16 b0 = __float2bfloat16_rn(x);
-    const float e1 = x - __bfloat162float(b0);
-    const __nv_bfloat16 b1 = __float2bfloat16_rn(e1);
-    const float e2 = e1 - __bfloat162float(b1);
     const int64_t o = orow * ldo + ocol;
     o0[o] = b0;
-    o1[o] = b1;
-    o2[o] = __float2bfloat16_rn(e2);
+    if constexpr (NT == 3) {
+      const float e1 = x - __bfloat162float(b0);
+      const __nv_bfloat16 b1 = __float2bfloat16_rn(e1);
+      const float e2 = e1 - __bfloat162float(b1);
+      o1[o] = b1;
+      o2[o] = __float2bfloat16_rn(e2);
+    }
   }
 }
 
@@ -387,15 +389,16 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace tc
 
-void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a) {
+void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a, int terms) {
   using namespace tc;
   SLQ_CHECK_ARG(a.batch == 1 && a.M > 0 && a.N > 0 && a.K > 0, "tc gemm: batch 1, non-empty");
+  SLQ_CHECK_ARG(terms == 1 || terms == 3, "tc gemm: 1 or 3 bf16 terms");
   const int M = a.M, N = a.N, K = a.K;
   const int64_t ldk = (K + 7) / 8 * 8;  // 16-byte row pitch for TMA
   const size_t a_bytes = align256(2 * (size_t)M * ldk), b_bytes = align256(2 * (size_t)N * ldk);
-  // product list (i + j <= 2)
+  // product list (i + j <= 2); one term: the leading product only
   static const int AI[6] = {0, 0, 1, 1, 0, 2}, BI[6] = {0, 1, 0, 1, 2, 0};
-  const int npairs = 6, nk = (K + BK - 1) / BK;
+  const int npairs = terms == 1 ? 1 : 6, nk = (K + BK - 1) / BK;
   const int64_t t128 = ceil_div(M, BM) * ceil_div(N, 128);
   const int bn = t128 >= 148 ? 128 : 64;
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, bn));
@@ -405,36 +408,35 @@ void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a) {
   const int tps = (int)ceil_div(total, splits);
   splits = (int)ceil_div(total, tps);
   const size_t w_bytes = splits > 1 ? align256(4 * (size_t)M * N * splits) : 0;
-  uint8_t* base = (uint8_t*)L.ws->get(3 * a_bytes + 3 * b_bytes + w_bytes, L.stream);
-  __nv_bfloat16* at[3];
-  __nv_bfloat16* bt[3];
-  for (int i = 0; i < 3; ++i) {
+  uint8_t* base = (uint8_t*)L.ws->get(terms * (a_bytes + b_bytes) + w_bytes, L.stream);
+  __nv_bfloat16* at[3] = {nullptr, nullptr, nullptr};
+  __nv_bfloat16* bt[3] = {nullptr, nullptr, nullptr};
+  for (int i = 0; i < terms; ++i) {
     at[i] = (__nv_bfloat16*)(base + i * a_bytes);
-    bt[i] = (__nv_bfloat16*)(base + 3 * a_bytes + i * b_bytes);
+    bt[i] = (__nv_bfloat16*)(base + terms * a_bytes + i * b_bytes);
   }
-  float* ws = splits > 1 ? (float*)(base + 3 * a_bytes + 3 * b_bytes) : nullptr;
+  float* ws = splits > 1 ? (float*)(base + terms * (a_bytes + b_bytes)) : nullptr;
   {  // split (and transpose to K-contiguous where needed)
-    LaunchScope scope(L.prof, KC_ELEM, L.stream, 0, (4.0 + 6.0) * ((double)M * K + (double)N * K));
-    if (a.sAk == 1) {
-      dim3 g((unsigned)ceil_div(K, 32), (unsigned)ceil_div(M, 32));
-      k_split3<false><<<g, 256, 0, L.stream>>>(a.A, M, K, a.sAm, at[0], at[1], at[2], ldk);
-    } else {  // A stored [K x M] (M contiguous) -> [M x K]
-      dim3 g((unsigned)ceil_div(M, 32), (unsigned)ceil_div(K, 32));
-      k_split3<true><<<g, 256, 0, L.stream>>>(a.A, K, M, a.sAk, at[0], at[1], at[2], ldk);
-    }
-    SLQ_CUDA(cudaGetLastError());
-    if (a.sBk == 1) {  // B(k, n) at n*sBn + k: stored [N x K]
-      dim3 g((unsigned)ceil_div(K, 32), (unsigned)ceil_div(N, 32));
-      k_split3<false><<<g, 256, 0, L.stream>>>(a.B, N, K, a.sBn, bt[0], bt[1], bt[2], ldk);
-    } else {  // stored [K x N] -> [N x K]
-      dim3 g((unsigned)ceil_div(N, 32), (unsigned)ceil_div(K, 32));
-      k_split3<true><<<g, 256, 0, L.stream>>>(a.B, K, N, a.sBk, bt[0], bt[1], bt[2], ldk);
-    }
-    SLQ_CUDA(cudaGetLastError());
+    LaunchScope scope(L.prof, KC_ELEM, L.stream, 0, (4.0 + 2.0 * terms) * ((double)M * K + (double)N * K));
+    auto split = [&](const float* X, int64_t R, int64_t C, int64_t ld, bool trans, __nv_bfloat16** o) {
+      dim3 g((unsigned)ceil_div(C, 32), (unsigned)ceil_div(R, 32));
+      if (terms == 1) {
+        if (trans) k_split3<true, 1><<<g, 256, 0, L.stream>>>(X, R, C, ld, o[0], o[1], o[2], ldk);
+        else k_split3<false, 1><<<g, 256, 0, L.stream>>>(X, R, C, ld, o[0], o[1], o[2], ldk);
+      } else {
+        if (trans) k_split3<true, 3><<<g, 256, 0, L.stream>>>(X, R, C, ld, o[0], o[1], o[2], ldk);
+        else k_split3<false, 3><<<g, 256, 0, L.stream>>>(X, R, C, ld, o[0], o[1], o[2], ldk);
+      }
+      SLQ_CUDA(cudaGetLastError());
+    };
+    if (a.sAk == 1) split(a.A, M, K, a.sAm, false, at);
+    else split(a.A, K, M, a.sAk, true, at);  // A stored [K x M] (M contiguous) -> [M x K]
+    if (a.sBk == 1) split(a.B, N, K, a.sBn, false, bt);  // B(k, n) at n*sBn + k: stored [N x K]
+    else split(a.B, K, N, a.sBk, true, bt);               // stored [K x N] -> [N x K]
     *L.launches += 2;
   }
   MultiOps ops;
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < terms; ++i) {
     ops.a[i] = make_map_bf16(at[i], M, K, ldk, BM);
     ops.b[i] = make_map_bf16(bt[i], N, K, ldk, bn);
   }

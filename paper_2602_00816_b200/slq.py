@@ -11,7 +11,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libslq.so")
 
 SLQ_OK, SLQ_EINVAL, SLQ_ENUMERIC, SLQ_ECUDA, SLQ_ENCCL, SLQ_ETIMEOUT, SLQ_ENOMEM, SLQ_EUNSUPPORTED = 0, 2, 3, 4, 5, 6, 7, 8
-PASS = {"fp64": 0, "fp32": 1, "bf16x3": 2, "paired": 3, "paired_fp32": 4, "fp64_oz": 5}
+PASS = {"fp64": 0, "fp32": 1, "bf16x3": 2, "paired": 3, "paired_fp32": 4, "fp64_oz": 5, "bf16": 6}
 REORTH = {"none": 0, "full": 1, "window": 2}
 BASIS = {"fp32": 0, "bf16": 1}
 PERTURB = {"exact": 0, "storage": 1}
