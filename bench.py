@@ -366,6 +366,8 @@ def main():
                    "l2": "no flush: per-step working set (theta+-, g+- fp64, activations, basis) > 0.5 GB > 126 MB L2"},
         "s_per_lanczos_step": ms_step / 1000.0,
         "hvp_per_s_standalone": 1000.0 / hvp_ms * units,
+        # normalised throughput, tokens of the global batch x Lanczos steps per second
+        "tokens_x_hvp_per_s": 1000.0 / ms_step * n_glob * cfg.seq_len,
         "grad_step_ms": grad_ms,
         "hvp_over_grad": hvp_ms / grad_ms,
         "e2e": {"value": 1000.0 / e2e_ms * units, "unit": UNIT, "h2d_bytes_per_step": 4 * P_loc * world,

@@ -657,10 +657,18 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const int e = exp_of(mx);
     if (lane == 0) jb.ex[row] = e;
+    // 16-byte loads when the row base is 16-byte aligned (even pitch, aligned base)
+    const bool v2 = (jb.ld % 2) == 0 && ((uintptr_t)jb.X & 15) == 0;
     for (int k4 = lane * 4; k4 < jb.Kp; k4 += 128) {
       double x[4];
+      if (v2 && k4 + 3 < jb.K) {
+        const double2 p0 = *reinterpret_cast<const double2*>(xr + k4);
+        const double2 p1 = *reinterpret_cast<const double2*>(xr + k4 + 2);
+        x[0] = p0.x; x[1] = p0.y; x[2] = p1.x; x[3] = p1.y;
+      } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) x[j] = (k4 + j < jb.K) ? xr[k4 + j] : 0.0;
+        for (int j = 0; j < 4; ++j) x[j] = (k4 + j < jb.K) ? xr[k4 + j] : 0.0;
+      }
       int8_t d[4][S];
 #pragma unroll
       for (int j = 0; j < 4; ++j) digits<S>(x[j], e, d[j]);
