@@ -416,7 +416,6 @@ __global__ void __launch_bounds__(320, 1)
         for (int ph = 0; ph < 2; ++ph, ++use) {
           mbar_wait(tmem_empty, (use & 1) ^ 1);  // the epilogue drained the previous phase
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-          const int g0 = ph == 0 ? 0 : 4, g1 = ph == 0 ? 4 : WS;
           uint32_t started = 0;
           for (int i = 0; i < nloc; ++i, ++it) {
             const int s = it % CF::STAGES;
@@ -424,21 +423,31 @@ __global__ void __launch_bounds__(320, 1)
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
             const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
             const uint32_t sb = sa + WS * CF::PLANE;
-            for (int g = g0; g < g1; ++g) {
-              const uint32_t acc_col = (uint32_t)((g - g0) * WBN);
-              for (int pa = 0; pa <= g; ++pa) {
-                const int qb = g - pa;
-                if (pa >= WS || qb >= WS) continue;
-                const uint64_t da = make_desc_sw32(sa + pa * CF::PLANE);
-                const uint64_t db = make_desc_sw32(sb + qb * CF::PLANE);
-                const uint32_t acc = (started >> g) & 1u;
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + acc_col),
-                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
-                started |= 1u << g;
-              }
+            // descriptors: one base per operand and stage plus constant plane offsets (16-byte
+            // units); fully unrolled per phase, accumulate flag constant after the first k-tile
+            const uint64_t da0 = make_desc_sw32(sa), db0 = make_desc_sw32(sb);
+            const uint32_t first = started == 0u;
+            auto mma = [&](int g, int pa, int qb, int gl) {
+              const uint64_t da = da0 + (uint64_t)((pa * CF::PLANE) >> 4);
+              const uint64_t db = db0 + (uint64_t)((qb * CF::PLANE) >> 4);
+              const uint32_t acc = pa == 0 ? (first ^ 1u) : 1u;
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(gl * WBN)),
+                  "l"(da), "l"(db), "r"(idesc), "r"(acc));
+            };
+            if (ph == 0) {
+#pragma unroll
+              for (int g = 0; g < 4; ++g)
+#pragma unroll
+                for (int pa = 0; pa <= g; ++pa) mma(g, pa, g - pa, g);
+            } else {
+#pragma unroll
+              for (int g = 4; g < WS; ++g)
+#pragma unroll
+                for (int pa = 0; pa <= g; ++pa) mma(g, pa, g - pa, g - 4);
             }
+            started = 1u;
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                 smem_u32(&empty[s])));
           }
