@@ -161,6 +161,21 @@ def cpu_baseline(cfg, budget_s=12.0):
             "sample": what + "; the recurrence/reorth is <1% and excluded"}
 
 
+def config_dict(args, cfg, world, n_glob):
+    """The bench line's `config` (both arms print the same one)."""
+    arch = {si.ARCH_GPT: "GPT", si.ARCH_LLAMA: "Llama"}.get(cfg.arch, "MLP")
+    return {"workload": f"{args.config}: {arch} {cfg.n_layers}L "
+                        f"d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} V{cfg.vocab}, {si.n_params(cfg)} params "
+                        f"({'bf16' if cfg.param_bf16 else 'fp32'}), "
+                        + (f"{WEAK[cfg.name]}x{cfg.seq_len} Zipf(1.1) tokens per GPU" if cfg.name in WEAK
+                           else f"{cfg.n_seq}x{cfg.seq_len} Zipf(1.1) tokens in total")
+                        + f", eps={cfg.eps}, Lanczos m={cfg.m} "
+                        f"{'full CGS2 reorth' if cfg.reorth_full else 'no reorth'}",
+            "global_batch": n_glob, "seq_len": cfg.seq_len, "parallelism": f"fsdp{world}",
+            "pass_numerics": args.numerics, "perturb": "exact",
+            "l2": "no flush: per-step working set (theta+-, g+- fp64, activations, basis) > 0.5 GB > 126 MB L2"}
+
+
 def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -192,7 +207,8 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps / scale,
         "higher_is_better": True, "scaling": "weak" if cfg.name in WEAK else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} (oracle, CPU)", "global_batch": cfg.n_seq, "seq_len": cfg.seq_len},
+        "config": config_dict(args, cfg, world, WEAK.get(cfg.name, cfg.n_seq) * world if cfg.name in WEAK
+                              else cfg.n_seq),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": what},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
 
@@ -354,16 +370,7 @@ def main():
         "scaling": "weak" if cfg.name in WEAK else "strong",
         "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": f"f64 (dense GEMMs with M*N*K >= {float(os.environ.get('SLQ_OZ_MIN_MNK', '1e9')):.0e} as exact int8 digit products on tcgen05, S={os.environ.get('SLQ_OZ_SLICES', '7')}; the rest fp64 DMMA)", "fp32": "f32", "bf16x3": "bf16x3", "bf16": "bf16", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: {'GPT' if cfg.arch == si.ARCH_GPT else 'Llama'} {cfg.n_layers}L "
-                               f"d{cfg.d_model} {cfg.n_heads}h ff{cfg.d_ff} V{cfg.vocab}, {si.n_params(cfg)} params "
-                               f"({'bf16' if cfg.param_bf16 else 'fp32'}), "
-                               + (f"{WEAK[cfg.name]}x{cfg.seq_len} Zipf(1.1) tokens per GPU" if cfg.name in WEAK
-                                  else f"{cfg.n_seq}x{cfg.seq_len} Zipf(1.1) tokens in total")
-                               + f", eps={cfg.eps}, Lanczos m={cfg.m} "
-                               f"{'full CGS2 reorth' if cfg.reorth_full else 'no reorth'}",
-                   "global_batch": n_glob, "seq_len": cfg.seq_len, "parallelism": f"fsdp{world}",
-                   "pass_numerics": args.numerics, "perturb": "exact",
-                   "l2": "no flush: per-step working set (theta+-, g+- fp64, activations, basis) > 0.5 GB > 126 MB L2"},
+        "config": config_dict(args, cfg, world, n_glob),
         "s_per_lanczos_step": ms_step / 1000.0,
         "hvp_per_s_standalone": 1000.0 / hvp_ms * units,
         # normalised throughput, tokens of the global batch x Lanczos steps per second
