@@ -37,12 +37,16 @@ using namespace tc;
 
 constexpr int BM = 128, BK = 64, UMMA_K = 32;
 
-template <int S, int BN>
+// KT: k-tile width in bytes = int8 elements (64: SWIZZLE_64B, two MMAs per product per k-tile;
+// 32: SWIZZLE_32B, one MMA per product, twice the stages in the same shared memory)
+template <int S, int BN, int KT = BK>
 struct Cfg {
-  static constexpr int A_PLANE = BM * BK, B_PLANE = BN * BK;  // bytes
+  static constexpr int A_PLANE = BM * KT, B_PLANE = BN * KT;  // bytes
   static constexpr int A_BYTES = S * A_PLANE, B_BYTES = S * B_PLANE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (3 * STAGE_BYTES + 2048 <= 227 * 1024) ? 3 : 2;
+  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - 8 * 128 * 8) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
+  static_assert(STAGES >= 2, "two stages at least");
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 8 * 128 * 8 /*epilogue*/;
   static_assert(SMEM <= 232448, "dynamic shared memory per CTA");
   static constexpr int TMEM_COLS = S * BN <= 128 ? 128 : (S * BN <= 256 ? 256 : 512);
@@ -88,11 +92,11 @@ __device__ __forceinline__ double exp2i(int e) { return __longlong_as_double((lo
 // tile x K split).  The TMA producer runs ahead across unit boundaries (ring of STAGES k-tiles);
 // the epilogue drains the S accumulators from TMEM into registers, releases TMEM (the next unit's
 // MMAs start), then does the scaling and the global stores while the next unit computes.
-template <int S, int BN>
+template <int S, int BN, int KT = BK>
 __global__ void __launch_bounds__(320, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
               GemmArgs<double> p, double* __restrict__ ws) {
-  using CF = Cfg<S, BN>;
+  using CF = Cfg<S, BN, KT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES);
@@ -155,8 +159,8 @@ __global__ void __launch_bounds__(320, 1)
           mbar_expect_tx(&full[s], CF::STAGE_BYTES);
 #pragma unroll
           for (int q = 0; q < S; ++q) {
-            tma_load_2d(sa + q * CF::A_PLANE, &tmA, &full[s], kt * BK, q * o.M + m0);
-            tma_load_2d(sb + q * CF::B_PLANE, &tmB, &full[s], kt * BK, q * o.N + n0);
+            tma_load_2d(sa + q * CF::A_PLANE, &tmA, &full[s], kt * KT, q * o.M + m0);
+            tma_load_2d(sb + q * CF::B_PLANE, &tmB, &full[s], kt * KT, q * o.N + n0);
           }
         }
       }
@@ -180,7 +184,8 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t sb = sa + CF::A_BYTES;
           // descriptors: one base per operand and stage, plane / k offsets added to the 14-bit
           // address field (16-byte units; every address stays below 256 KB, so no carry out)
-          const uint64_t da0 = make_desc_sw64(sa), db0 = make_desc_sw64(sb);
+          const uint64_t da0 = KT == 64 ? make_desc_sw64(sa) : make_desc_sw32(sa);
+          const uint64_t db0 = KT == 64 ? make_desc_sw64(sb) : make_desc_sw32(sb);
           const uint32_t first = started == 0u;  // first k-tile of the unit: overwrite
           if (!(o.debug & 1)) {
 #pragma unroll
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(320, 1)
               for (int pa = 0; pa <= g; ++pa) {
                 const int qb = g - pa;
 #pragma unroll
-                for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                for (int kk = 0; kk < KT / UMMA_K; ++kk) {
                   const uint64_t da = da0 + (uint64_t)((pa * CF::A_PLANE + kk * UMMA_K) >> 4);
                   const uint64_t db = db0 + (uint64_t)((qb * CF::B_PLANE + kk * UMMA_K) >> 4);
                   const uint32_t acc = (pa == 0 && kk == 0) ? (first ^ 1u) : 1u;
@@ -748,16 +753,16 @@ static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // W: the wide two-phase kernel (S = 7, BN = 128, 32-byte k-tiles)
-template <int S, int BN, bool W = false>
+template <int S, int BN, bool W = false, int KTN = BK>
 void run(const Launch& L, const GemmArgs<double>& a) {
-  using CF = Cfg<S, W ? 64 : BN>;  // (the wide kernel has its own CfgW; NPROD is the same)
-  constexpr int KT = W ? WBK : BK;
+  using CF = Cfg<S, W ? 64 : BN, KTN>;  // (the wide kernel has its own CfgW; NPROD is the same)
+  constexpr int KT = W ? WBK : KTN;
   static bool attr = false;
   if (!attr) {
     if constexpr (W)
       SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgW::SMEM));
     else
-      SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+      SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN, KTN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr = true;
   }
   const int M = a.M, N = a.N, K = a.K;
@@ -829,7 +834,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     if constexpr (W)
       k_oz_gemm_w<<<std::min(nwork, 148), 320, CfgW::SMEM, L.stream>>>(ta, tb, o, a, ws);
     else
-      k_oz_gemm<S, BN><<<std::min(nwork, 148), 320, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
+      k_oz_gemm<S, BN, KTN><<<std::min(nwork, 148), 320, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }
@@ -878,8 +883,11 @@ void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
       // the wide two-phase kernel when it has enough 128 x 128 tiles to fill the GPU
       static const int wide_env = getenv("SLQ_OZ_WIDE") ? atoi(getenv("SLQ_OZ_WIDE")) : 0;
       const int64_t t128 = ceil_div(a.M, oz::BM) * ceil_div(a.N, oz::WBN);
+      static const int kt_env = getenv("SLQ_OZ_BK") ? atoi(getenv("SLQ_OZ_BK")) : 64;
       if (wide_env == 2 || (wide_env == 1 && t128 >= 148))
         oz::run<7, 128, true>(L, a);
+      else if (kt_env == 32)
+        oz::run<7, 64, false, 32>(L, a);
       else
         oz::run<7, 64>(L, a);
       break;
