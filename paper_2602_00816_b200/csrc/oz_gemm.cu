@@ -92,10 +92,18 @@ __device__ __forceinline__ double exp2i(int e) { return __longlong_as_double((lo
 // tile x K split).  The TMA producer runs ahead across unit boundaries (ring of STAGES k-tiles);
 // the epilogue drains the S accumulators from TMEM into registers, releases TMEM (the next unit's
 // MMAs start), then does the scaling and the global stores while the next unit computes.
-template <int S, int BN, int KT = BK>
-__global__ void __launch_bounds__(320, 1)
+// NI > 1 (S = 7): the digit weights are split over NI MMA-issuing warps (warp 1, then warps 10,
+// 11), each a single issuing thread: NI = 2 -> {0, 5, 6} / {1..4} (14 + 14 products), NI = 3 ->
+// {1, 6} / {2, 5} / {0, 3, 4} (9 + 9 + 10).  One thread cannot issue 128 x 64 x 32 MMAs as fast as
+// the tensor pipe retires them; several threads can.
+__host__ __device__ constexpr int oz_owner(int NI, int g) {
+  return NI == 2 ? (g >= 1 && g <= 4 ? 1 : 0) : NI == 3 ? (g == 1 || g == 6 ? 0 : (g == 2 || g == 5 ? 1 : 2)) : 0;
+}
+template <int S, int BN, int KT = BK, int NI = 1>
+__global__ void __launch_bounds__(288 + 32 * NI, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
               GemmArgs<double> p, double* __restrict__ ws) {
+  static_assert(NI == 1 || ((NI == 2 || NI == 3) && S == 7), "several issuers: S = 7 only");
   using CF = Cfg<S, BN, KT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -123,9 +131,9 @@ __global__ void __launch_bounds__(320, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < CF::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], NI);  // one commit per issuing warp
     }
-    mbar_init(tmem_full, 1);
+    mbar_init(tmem_full, NI);
     mbar_init(tmem_empty, 8);  // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     asm volatile("fence.proxy.async.shared::cta;\n" ::);
@@ -165,8 +173,9 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer: S(S+1)/2 digit products per k-tile ----
+  } else if (warp == 1 || warp >= 10) {
+    if (lane == 0) {  // ---- MMA issuer(s): S(S+1)/2 digit products per k-tile ----
+      const int iss = warp == 1 ? 0 : warp - 9;
       constexpr uint32_t idesc = make_idesc_i8(BM, BN);
       int it = 0, tl = 0;
       for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
@@ -190,6 +199,7 @@ __global__ void __launch_bounds__(320, 1)
           if (!(o.debug & 1)) {
 #pragma unroll
             for (int g = 0; g < S; ++g) {
+              if (NI > 1 && oz_owner(NI, g) != iss) continue;
 #pragma unroll
               for (int pa = 0; pa <= g; ++pa) {
                 const int qb = g - pa;
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 10) {
     // ---- epilogue (warps 2..9): warp w drains TMEM lanes 32 (w % 4) .. +31 (its quadrant), columns
     // [32 h, 32 h + 32) with h = (w - 2) / 4, combining the S digit weights in fp64 ----
     const int lg = (warp % 4) * 32;
@@ -753,7 +763,7 @@ static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // W: the wide two-phase kernel (S = 7, BN = 128, 32-byte k-tiles)
-template <int S, int BN, bool W = false, int KTN = BK>
+template <int S, int BN, bool W = false, int KTN = BK, int NI = 1>
 void run(const Launch& L, const GemmArgs<double>& a) {
   using CF = Cfg<S, W ? 64 : BN, KTN>;  // (the wide kernel has its own CfgW; NPROD is the same)
   constexpr int KT = W ? WBK : KTN;
@@ -762,7 +772,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     if constexpr (W)
       SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgW::SMEM));
     else
-      SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN, KTN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+      SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN, KTN, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr = true;
   }
   const int M = a.M, N = a.N, K = a.K;
@@ -834,7 +844,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     if constexpr (W)
       k_oz_gemm_w<<<std::min(nwork, 148), 320, CfgW::SMEM, L.stream>>>(ta, tb, o, a, ws);
     else
-      k_oz_gemm<S, BN, KTN><<<std::min(nwork, 148), 320, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
+      k_oz_gemm<S, BN, KTN, NI><<<std::min(nwork, 148), 288 + 32 * NI, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }
@@ -884,12 +894,17 @@ void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
       static const int wide_env = getenv("SLQ_OZ_WIDE") ? atoi(getenv("SLQ_OZ_WIDE")) : 0;
       const int64_t t128 = ceil_div(a.M, oz::BM) * ceil_div(a.N, oz::WBN);
       static const int kt_env = getenv("SLQ_OZ_BK") ? atoi(getenv("SLQ_OZ_BK")) : 64;
+      static const int ni_env = getenv("SLQ_OZ_ISSUERS") ? atoi(getenv("SLQ_OZ_ISSUERS")) : 2;
       if (wide_env == 2 || (wide_env == 1 && t128 >= 148))
         oz::run<7, 128, true>(L, a);
       else if (kt_env == 32)
         oz::run<7, 64, false, 32>(L, a);
-      else
+      else if (ni_env == 3)
+        oz::run<7, 64, false, oz::BK, 3>(L, a);
+      else if (ni_env == 1)
         oz::run<7, 64>(L, a);
+      else
+        oz::run<7, 64, false, oz::BK, 2>(L, a);
       break;
     }
   }
