@@ -65,6 +65,8 @@ struct OzArgs {
   const int* ea;         // [M] row exponents of A
   const int* eb;         // [N] column exponents of B
   int debug;  // diagnostic only (SLQ_OZ_DEBUG bits): 1 no MMAs, 2 no TMA loads, 4 no stores, 8 no TMEM drain
+  int mfast;  // tile order: 1 = m fastest (the B tile is shared by the CTAs in flight and streamed
+              // from DRAM once; the smaller A planes are re-read from L2), 0 = n fastest
 };
 
 // 32 consecutive TMEM columns of the warp's 32 lanes (one 32-bit value per lane per column)
@@ -117,12 +119,19 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + BM - 1) / BM;
   const int nwork = tiles_n * tiles_m * o.splits;
-  // unit w -> (split, tile_m, tile_n), n fastest (neighbouring CTAs share the A k-tiles in L2)
+  // unit w -> (split, tile_m, tile_n): the larger operand's tile is the one the CTAs in flight
+  // share (o.mfast), so its digit planes stream from DRAM once and the smaller operand's planes are
+  // the ones re-read (from L2)
   auto decode = [&](int w, int& m0, int& n0, int& sp, int& kt0, int& nloc) {
     sp = w % o.splits;
     const int t = w / o.splits;
-    n0 = (t % tiles_n) * BN;
-    m0 = (t / tiles_n) * BM;
+    if (o.mfast) {
+      m0 = (t % tiles_m) * BM;
+      n0 = (t / tiles_m) * BN;
+    } else {
+      n0 = (t % tiles_n) * BN;
+      m0 = (t / tiles_n) * BM;
+    }
     kt0 = sp * o.kt_per_split;
     const int kt1 = min(o.nk, kt0 + o.kt_per_split);
     nloc = kt1 > kt0 ? kt1 - kt0 : 0;
@@ -836,7 +845,8 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   const CUtensorMap ta = make_map_i8(as, (int64_t)S * M, Kp, Kp, BM, KT);
   const CUtensorMap tb = make_map_i8(bs, (int64_t)S * N, Kp, Kp, BN, KT);
   static const int dbg = getenv("SLQ_OZ_DEBUG") ? atoi(getenv("SLQ_OZ_DEBUG")) : 0;
-  OzArgs o{M, N, nk, ktps, splits, ea, eb, dbg};
+  static const int order = getenv("SLQ_OZ_ORDER") ? atoi(getenv("SLQ_OZ_ORDER")) : -1;  // 0 n-fast, 1 m-fast
+  OzArgs o{M, N, nk, ktps, splits, ea, eb, dbg, order >= 0 ? order : (N > M ? 1 : 0)};
   {
     LaunchScope scope(L.prof, KC_GEMM_I8, L.stream, 2.0 * M * N * (double)K * CF::NPROD,
                       (double)S * ((double)M * K + (double)N * K) + 8.0 * M * N);
