@@ -82,6 +82,18 @@ void linear_wgrad(const Launch& L, const T* dy, int64_t lddy, const T* x, int64_
   gemm(L, a);
 }
 
+// dW_z[out x in] = dy_z^T . x_z for z = 0..nb-1 (one batched launch; operand z at base + z * stride)
+template <class T>
+void linear_wgrad_batched(const Launch& L, const T* dy, int64_t lddy, int64_t sdy, const T* x, int64_t ldx,
+                          int64_t sx, int out, int in, int N, T* dW, int64_t sdw, int nb) {
+  GemmArgs<T> a;
+  a.M = out; a.N = in; a.K = N; a.batch = nb;
+  a.A = dy; a.sAm = 1; a.sAk = lddy; a.offA = BatchOff{sdy, 0, 1, 1};
+  a.B = x; a.sBk = ldx; a.sBn = 1; a.offB = BatchOff{sx, 0, 1, 1};
+  a.C = dW; a.ldc = in; a.offC = BatchOff{sdw, 0, 1, 1};
+  gemm(L, a);
+}
+
 // Causal multi-head attention over a packed projection buffer.
 //   qkv rows r = b*Tn + t (ld = W); q head h at column qo + h*hd, kv head g at ko/vo + g*hd;
 //   q head h reads kv head h / rep (GQA).  P = probabilities [nseq*Hq][Tn][Tn].
@@ -310,6 +322,12 @@ struct GptRunner : Runner<T> {
   struct Bwd { T *dx1, *dh1, *dh2, *dqkv, *du; } bb[2];
   T *dxs[3], *dhf, *dP, *do_;
   SideStream ss;
+  // deferred weight gradients (SLQ_DEFER_WGRAD=1, fp64 DMMA passes, no collective): every layer's
+  // output gradients stay in per-layer slabs and the four weight-gradient contractions run as one
+  // batched launch each over the layers after the data-gradient chain
+  bool defer_ok = false;
+  T *s_h1 = nullptr, *s_o = nullptr, *s_h2 = nullptr, *s_gu = nullptr;
+  T *s_dx = nullptr, *s_du = nullptr, *s_dx1 = nullptr, *s_dqkv = nullptr;
 
   GptRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
     ss.init(L);
@@ -328,13 +346,25 @@ struct GptRunner : Runner<T> {
     loss_rows = A.alloc<double>(std::max(N, 1));
     for (int l = 0; l <= Ly; ++l) xs.push_back(A.alloc<T>((int64_t)N * D));
     const int64_t PP = (int64_t)nseq * H * Tn * Tn;
+    // the weight-gradient operands of all layers in slabs (constant stride for batched launches)
+    s_h1 = A.alloc<T>((int64_t)Ly * N * D); s_o = A.alloc<T>((int64_t)Ly * N * D);
+    s_h2 = A.alloc<T>((int64_t)Ly * N * D); s_gu = A.alloc<T>((int64_t)Ly * N * F);
     for (int l = 0; l < Ly; ++l) {
       Layer a;
-      a.mean1 = A.alloc<T>(N); a.rstd1 = A.alloc<T>(N); a.h1 = A.alloc<T>((int64_t)N * D);
-      a.qkv = A.alloc<T>((int64_t)N * 3 * D); a.P = A.alloc<T>(PP); a.o = A.alloc<T>((int64_t)N * D);
+      a.mean1 = A.alloc<T>(N); a.rstd1 = A.alloc<T>(N); a.h1 = s_h1 + (int64_t)l * N * D;
+      a.qkv = A.alloc<T>((int64_t)N * 3 * D); a.P = A.alloc<T>(PP); a.o = s_o + (int64_t)l * N * D;
       a.x1 = A.alloc<T>((int64_t)N * D); a.mean2 = A.alloc<T>(N); a.rstd2 = A.alloc<T>(N);
-      a.h2 = A.alloc<T>((int64_t)N * D); a.u = A.alloc<T>((int64_t)N * F); a.gu = A.alloc<T>((int64_t)N * F);
+      a.h2 = s_h2 + (int64_t)l * N * D; a.u = A.alloc<T>((int64_t)N * F); a.gu = s_gu + (int64_t)l * N * F;
       ly.push_back(a);
+    }
+    {
+      const char* e = getenv("SLQ_DEFER_WGRAD");
+      const double mnk = (double)std::max(F, 3 * D) * D * N;  // largest per-layer weight gradient
+      defer_ok = sizeof(T) == 8 && e && atoi(e) == 1 && Ly > 1 && (L.gemm_mode != 2 || mnk < oz_min_mnk());
+      if (defer_ok) {
+        s_dx = A.alloc<T>((int64_t)Ly * N * D); s_du = A.alloc<T>((int64_t)Ly * N * F);
+        s_dx1 = A.alloc<T>((int64_t)Ly * N * D); s_dqkv = A.alloc<T>((int64_t)Ly * N * 3 * D);
+      }
     }
     meanf = A.alloc<T>(N); rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D);
     logits = A.alloc<T>((int64_t)N * V);
@@ -396,14 +426,24 @@ struct GptRunner : Runner<T> {
     ss.begin_pass();
     T* G0 = tied ? io.grads(0) : nullptr;
     T* Gf = io.grads(Ly + 1);
+    // deferral needs the layers' gradient buffers at a constant stride (no collective: one
+    // contiguous gradient shard with identical block units)
+    bool defer = defer_ok && !io.collective();
+    int64_t gstride = 0;
+    if (defer) {
+      gstride = io.grads(2) - io.grads(1);
+      for (int l = 2; l < Ly && defer; ++l) defer = io.grads(1 + l) - io.grads(1) == (int64_t)l * gstride;
+    }
     int cur = 0;  // dxs[cur] = dL/d(residual stream) entering the current block from above
+    T* dx_top = defer ? s_dx + (int64_t)(Ly - 1) * N * D : dxs[0];
+    T* dx_emb = dx_top;  // the gradient leaving block 0 (input of the embedding backward)
     ss.fork();
     linear_wgrad<T>(Ls, logits, V, xf, D, V, D, N, tied ? G0 + u0.t("wte").offset : Gf + uf.t("head.w").offset);
     linear_dgrad<T>(L, logits, V, Whead, V, D, N, dhf, D);
     ss.fork();
     colreduce<T>(Ls, 1, dhf, D, xs[Ly], meanf, rstdf, Gf + uf.t("lnf.g").offset, Gf + uf.t("lnf.b").offset, N, D,
                  false);
-    layernorm_bwd<T>(L, dhf, xs[Ly], meanf, rstdf, Pf + uf.t("lnf.g").offset, nullptr, dxs[cur], N, D);
+    layernorm_bwd<T>(L, dhf, xs[Ly], meanf, rstdf, Pf + uf.t("lnf.g").offset, nullptr, dx_top, N, D);
     if (io.collective()) ss.join();
     io.grads_done(Ly + 1);
     for (int l = Ly - 1; l >= 0; --l) {
@@ -419,13 +459,19 @@ struct GptRunner : Runner<T> {
       T *dx1 = bb[set].dx1, *dh1 = bb[set].dh1, *dh2 = bb[set].dh2, *dqkv = bb[set].dqkv, *du = bb[set].du;
       T* dx = dxs[cur];
       T* dxn = dxs[(cur + 1) % 3];
+      if (defer) {
+        dx1 = s_dx1 + (int64_t)l * N * D; dqkv = s_dqkv + (int64_t)l * N * 3 * D; du = s_du + (int64_t)l * N * F;
+        dx = s_dx + (int64_t)l * N * D;
+        dxn = l > 0 ? s_dx + (int64_t)(l - 1) * N * D : dxs[1];
+      }
+      dx_emb = dxn;
       // MLP: xs[l+1] = x1 + mproj(gelu(fc(ln2(x1))))
       ss.fork();
-      linear_wgrad<T>(Ls, dx, D, a.gu, F, D, F, N, gw("mproj.w"));
+      if (!defer) linear_wgrad<T>(Ls, dx, D, a.gu, F, D, F, N, gw("mproj.w"));
       colreduce<T>(Ls, 0, dx, D, nullptr, nullptr, nullptr, gw("mproj.b"), nullptr, N, D, false);
       linear_dgrad<T>(L, dx, D, w("mproj.w"), D, F, N, du, F, ACT_DGELU, a.u, F);
       ss.fork();
-      linear_wgrad<T>(Ls, du, F, a.h2, D, F, D, N, gw("fc.w"));
+      if (!defer) linear_wgrad<T>(Ls, du, F, a.h2, D, F, D, N, gw("fc.w"));
       colreduce<T>(Ls, 0, du, F, nullptr, nullptr, nullptr, gw("fc.b"), nullptr, N, F, false);
       linear_dgrad<T>(L, du, F, w("fc.w"), F, D, N, dh2, D);
       ss.fork();
@@ -433,12 +479,12 @@ struct GptRunner : Runner<T> {
       layernorm_bwd<T>(L, dh2, a.x1, a.mean2, a.rstd2, w("ln2.g"), dx, dx1, N, D);
       // attention: x1 = xs[l] + proj(attn(ln1(xs[l])))
       ss.fork();
-      linear_wgrad<T>(Ls, dx1, D, a.o, D, D, D, N, gw("proj.w"));
+      if (!defer) linear_wgrad<T>(Ls, dx1, D, a.o, D, D, D, N, gw("proj.w"));
       colreduce<T>(Ls, 0, dx1, D, nullptr, nullptr, nullptr, gw("proj.b"), nullptr, N, D, false);
       linear_dgrad<T>(L, dx1, D, w("proj.w"), D, D, N, do_, D);
       attention_bwd<T>(L, g, a.qkv, a.P, do_, dP, dqkv);
       ss.fork();
-      linear_wgrad<T>(Ls, dqkv, 3 * D, a.h1, D, 3 * D, D, N, gw("qkv.w"));
+      if (!defer) linear_wgrad<T>(Ls, dqkv, 3 * D, a.h1, D, 3 * D, D, N, gw("qkv.w"));
       colreduce<T>(Ls, 0, dqkv, 3 * D, nullptr, nullptr, nullptr, gw("qkv.b"), nullptr, N, 3 * D, false);
       linear_dgrad<T>(L, dqkv, 3 * D, w("qkv.w"), 3 * D, D, N, dh1, D);
       ss.fork();
@@ -449,10 +495,21 @@ struct GptRunner : Runner<T> {
       io.grads_done(1 + l);
       cur = (cur + 1) % 3;
     }
+    if (defer) {  // the four weight gradients of every block, one batched launch each
+      const UnitPlan& u1 = plan->units[1];
+      T* G1 = io.grads(1);
+      const int64_t nd = (int64_t)N * D, nf = (int64_t)N * F;
+      ss.fork();
+      linear_wgrad_batched<T>(Ls, s_dx, D, nd, s_gu, F, nf, D, F, N, G1 + u1.t("mproj.w").offset, gstride, Ly);
+      linear_wgrad_batched<T>(Ls, s_du, F, nf, s_h2, D, nd, F, D, N, G1 + u1.t("fc.w").offset, gstride, Ly);
+      linear_wgrad_batched<T>(Ls, s_dx1, D, nd, s_o, D, nd, D, D, N, G1 + u1.t("proj.w").offset, gstride, Ly);
+      linear_wgrad_batched<T>(Ls, s_dqkv, 3 * D, 3 * nd, s_h1, D, nd, 3 * D, D, N, G1 + u1.t("qkv.w").offset,
+                              gstride, Ly);
+    }
     ss.join();  // all side work (incl. the tied head gradient into G0) before the embedding backward
     if (!tied) G0 = io.grads(0);
-    embed_bwd_rows<T>(L, csr, dxs[cur], G0 + u0.t("wte").offset, V, D, tied);
-    pos_bwd<T>(L, dxs[cur], G0 + u0.t("wpe").offset, nseq, Tn, D);
+    embed_bwd_rows<T>(L, csr, dx_emb, G0 + u0.t("wte").offset, V, D, tied);
+    pos_bwd<T>(L, dx_emb, G0 + u0.t("wpe").offset, nseq, Tn, D);
     io.grads_done(0);
     sum_rows_f64(L, loss_rows, N, loss_sum);
   }
