@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : 1) gemm_
       if (r >= rows || c >= cols) continue;
       const int64_t o = (int64_t)(m0 + r) * p.N + n0 + c;
       double s0 = 0.0, s1 = 0.0;
+#pragma unroll 4
       for (int k = 0; k < splits; ++k) {
         s0 += __ldcg(part + k * mn + o);
         if (c + 1 < cols) s1 += __ldcg(part + k * mn + o + 1);

@@ -384,9 +384,24 @@ __global__ void k_colreduce1(int mode, const T* __restrict__ dy, int64_t lddy, c
   const int nparts = gridDim.y;
   for (int cc = threadIdx.x; cc < cols; cc += blockDim.x) {
     T s0v = T(0), s1v = T(0);
-    for (int p = 0; p < nparts; ++p) {
-      s0v += part0[(int64_t)p * cols + cc];
-      if (mode == 1) s1v += part1[(int64_t)p * cols + cc];
+    int p = 0;
+    // eight partial rows' loads in flight before the (in-order) additions
+    for (; p + 8 <= nparts; p += 8) {
+      T a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        a[i] = __ldcg(part0 + (int64_t)(p + i) * cols + cc);
+        b[i] = mode == 1 ? __ldcg(part1 + (int64_t)(p + i) * cols + cc) : T(0);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s0v += a[i];
+        if (mode == 1) s1v += b[i];
+      }
+    }
+    for (; p < nparts; ++p) {
+      s0v += __ldcg(part0 + (int64_t)p * cols + cc);
+      if (mode == 1) s1v += __ldcg(part1 + (int64_t)p * cols + cc);
     }
     out0[cc] = accumulate ? out0[cc] + s0v : s0v;
     if (mode == 1) out1[cc] = accumulate ? out1[cc] + s1v : s1v;
