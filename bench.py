@@ -57,6 +57,10 @@ def parse():
                         "exact int8 digit products on tcgen05 (Ozaki) and the rest on DMMA; fp64 = all DMMA; "
                         "bf16x3 = fp32-faithful tcgen05")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    # "report with reorth on and off where the config asks"; window / bf16 basis (f3)
+    p.add_argument("--reorth", default="config", choices=["config", "full", "none", "window"])
+    p.add_argument("--window", type=int, default=8)
+    p.add_argument("--basis", default="fp32", choices=["fp32", "bf16"])
     return p.parse_args()
 
 
@@ -161,6 +165,16 @@ def cpu_baseline(cfg, budget_s=12.0):
             "sample": what + "; the recurrence/reorth is <1% and excluded"}
 
 
+def reorth_of(args, cfg):
+    return ("full" if cfg.reorth_full else "none") if args.reorth == "config" else args.reorth
+
+
+def reorth_label(args, cfg):
+    r = reorth_of(args, cfg)
+    lab = {"full": "full CGS2 reorth", "none": "no reorth", "window": f"window-{args.window} CGS2 reorth"}[r]
+    return lab + (", bf16 basis" if args.basis == "bf16" and r != "none" else "")
+
+
 def config_dict(args, cfg, world, n_glob):
     """The bench line's `config` (both arms print the same one)."""
     arch = {si.ARCH_GPT: "GPT", si.ARCH_LLAMA: "Llama"}.get(cfg.arch, "MLP")
@@ -169,8 +183,7 @@ def config_dict(args, cfg, world, n_glob):
                         f"({'bf16' if cfg.param_bf16 else 'fp32'}), "
                         + (f"{WEAK[cfg.name]}x{cfg.seq_len} Zipf(1.1) tokens per GPU" if cfg.name in WEAK
                            else f"{cfg.n_seq}x{cfg.seq_len} Zipf(1.1) tokens in total")
-                        + f", eps={cfg.eps}, Lanczos m={cfg.m} "
-                        f"{'full CGS2 reorth' if cfg.reorth_full else 'no reorth'}",
+                        + f", eps={cfg.eps}, Lanczos m={cfg.m} {reorth_label(args, cfg)}",
             "global_batch": n_glob, "seq_len": cfg.seq_len, "parallelism": f"fsdp{world}",
             "pass_numerics": args.numerics, "perturb": "exact",
             "l2": "no flush: per-step working set (theta+-, g+- fp64, activations, basis) > 0.5 GB > 126 MB L2"}
@@ -187,14 +200,15 @@ def run_reference(args, cfg):
     op = lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact")
     # the weak-scaling configs' basis (m x P fp64: 99 GB on c3) does not fit a host: the reference
     # step there is the FD-HVP + three-term recurrence without a stored basis
-    reorth = "none" if cfg.name in WEAK else "full"
-    OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + 99, th.size), max(args.warmup, 1), reorth)
+    reorth = "none" if cfg.name in WEAK else reorth_of(args, cfg)
+    okw = dict(window=args.window if reorth == "window" else 0, basis=args.basis)
+    OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + 99, th.size), max(args.warmup, 1), reorth, **okw)
     t0 = time.perf_counter()
     done = 0
     j = 0
     while done < args.steps:
         m = min(cfg.m, args.steps - done)
-        OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + j, th.size), m, reorth)
+        OL.lanczos(op, probe.rademacher_probe(cfg.probe_seed0 + j, th.size), m, reorth, **okw)
         done += m
         j += 1
     dt = time.perf_counter() - t0
@@ -242,8 +256,8 @@ def main():
     m_run = min(cfg.m, max(args.steps, 1))
     ctx = slq.SlqContext(cfg, si.init_params(cfg), tok, n_global=n_glob, rank=rank, world_size=world, device=local,
                          unique_id=uid, pass_numerics=args.numerics,
-                         reorth="full" if cfg.reorth_full else "none", max_steps=max(cfg.m, args.warmup),
-                         perturb="exact")
+                         reorth=reorth_of(args, cfg), window=args.window if args.reorth == "window" else 0,
+                         basis=args.basis, max_steps=max(cfg.m, args.warmup), perturb="exact")
     stream = torch.cuda.ExternalStream(ctx.stream)
 
     def barrier():
