@@ -382,7 +382,8 @@ def main():
         "metric": metric_name(cfg.name), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if cfg.name in WEAK else "strong",
-        "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": f"f64 (dense GEMMs with M*N*K >= {float(os.environ.get('SLQ_OZ_MIN_MNK', '1e9')):.0e} as exact int8 digit products on tcgen05, S={os.environ.get('SLQ_OZ_SLICES', '7')}; the rest fp64 DMMA)", "fp32": "f32", "bf16x3": "bf16x3", "bf16": "bf16", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
+        "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": "f64", "fp32": "f32", "bf16x3": "bf16x3", "bf16": "bf16", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
+        "dtype_note": {"fp64_oz": f"fp64 results; dense GEMMs with M*N*K >= {float(os.environ.get('SLQ_OZ_MIN_MNK', '1e9')):.0e} as exact int8 digit products on tcgen05 (Ozaki, S={os.environ.get('SLQ_OZ_SLICES', '7')}), the rest fp64 DMMA"}.get(args.numerics, ""),
         "data": "synthetic",
         "config": config_dict(args, cfg, world, n_glob),
         "s_per_lanczos_step": ms_step / 1000.0,
