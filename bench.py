@@ -133,8 +133,10 @@ def ncu_traffic(kernel_class: str):
 
 def oracle_sample(cfg):
     """(tokens, scale): the oracle's bounded sample of one HVP unit and the linear-in-tokens factor
-    that converts sample HVPs/s into unit HVPs/s.  c2: the full global batch (factor 1); weak-
-    scaling configs: 1 sequence truncated to 128 tokens of the 8 x 1024 per-GPU unit."""
+    that converts sample HVPs/s into unit HVPs/s.  c2: the full global batch (factor 1: a smaller
+    batch is not proportionally cheaper for the numpy oracle, ~4 s per step at 2 of 8 sequences vs
+    5.2 s at 8, so a token-scaled sample would understate it); weak-scaling configs: 1 sequence
+    truncated to 32 tokens of the per-GPU unit."""
     if cfg.name in WEAK:
         t = 32
         tok = si.tokens(cfg, n_seq=1)[:, :t + 1]
