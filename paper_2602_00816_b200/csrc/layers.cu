@@ -492,6 +492,70 @@ __global__ void k_cross_entropy(T* __restrict__ logits, const int32_t* __restric
   }
 }
 
+// Register-resident variant for V <= 256 NV (one read and one write of the row instead of three
+// reads): thread t holds z[t + 256 i]; the max, the sum of exponentials (summed in the same
+// per-thread order as k_cross_entropy) and the gradient are formed from registers.
+template <class T, int NV>
+__global__ void __launch_bounds__(256) k_cross_entropy_reg(T* __restrict__ logits, const int32_t* __restrict__ tgt,
+                                                           int tgt_stride, int Tn, double* __restrict__ loss_rows,
+                                                           int V, double inv_ntok) {
+  const int row = blockIdx.x;
+  T* z = logits + (int64_t)row * V;
+  const int b = row / Tn, t = row % Tn;
+  const int y = tgt[(int64_t)b * tgt_stride + t];
+  __shared__ T red[32];
+  T v[NV];
+  T mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = threadIdx.x + 256 * i;
+    v[i] = j < V ? z[j] : T(-INFINITY);
+    mx = max(mx, v[i]);
+  }
+  mx = warp_max(mx);
+  if (threadIdx.x % kWarp == 0) red[threadIdx.x / kWarp] = mx;
+  __syncthreads();
+  if (threadIdx.x < kWarp) {
+    T w = threadIdx.x < blockDim.x / kWarp ? red[threadIdx.x] : T(-INFINITY);
+    w = warp_max(w);
+    if (threadIdx.x == 0) red[0] = w;
+  }
+  __syncthreads();
+  mx = red[0];
+  __syncthreads();
+  T s = T(0);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (threadIdx.x + 256 * i < V) {
+      v[i] = dexp(v[i] - mx);
+      s += v[i];
+    }
+  }
+  s = warp_sum(s);
+  if (threadIdx.x % kWarp == 0) red[threadIdx.x / kWarp] = s;
+  __syncthreads();
+  if (threadIdx.x < kWarp) {
+    T w = threadIdx.x < blockDim.x / kWarp ? red[threadIdx.x] : T(0);
+    w = warp_sum(w);
+    if (threadIdx.x == 0) red[0] = w;
+  }
+  __syncthreads();
+  const T sum = red[0];
+  const T lse = mx + log(sum);
+  if (threadIdx.x == 0) loss_rows[row] = (double)(lse - z[y]);
+  __syncthreads();
+  const T inv = T(1) / sum, scale = (T)inv_ntok;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = threadIdx.x + 256 * i;
+    if (j < V) {
+      T p = v[i] * inv;
+      if (j == y) p -= T(1);
+      z[j] = p * scale;
+    }
+  }
+}
+
 __global__ void k_sum_rows(const double* __restrict__ x, int n, double* out) {
   __shared__ double red[32];
   double s = 0;
@@ -673,7 +737,10 @@ template <class T>
 void cross_entropy(const Launch& L, T* logits, const int32_t* tgt, int tgt_stride, int Tn, double* loss_rows,
                    int rows, int V, double inv_ntok) {
   if (rows == 0) return;
-  LAUNCH(KC_CE, rows, 256, k_cross_entropy<T>, logits, tgt, tgt_stride, Tn, loss_rows, V, inv_ntok);
+  if (V <= 256 * 16)
+    LAUNCH(KC_CE, rows, 256, (k_cross_entropy_reg<T, 16>), logits, tgt, tgt_stride, Tn, loss_rows, V, inv_ntok);
+  else
+    LAUNCH(KC_CE, rows, 256, k_cross_entropy<T>, logits, tgt, tgt_stride, Tn, loss_rows, V, inv_ntok);
 }
 void sum_rows_f64(const Launch& L, const double* x, int n, double* out) {
   LAUNCH(KC_VEC, 1, 1024, k_sum_rows, x, n, out);
