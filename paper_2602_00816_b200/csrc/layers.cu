@@ -169,7 +169,7 @@ __global__ void k_layernorm_fwd(const T* __restrict__ x, const T* __restrict__ g
 
 // dx = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)) (+ dres),  dxhat = dy * g
 template <class T, int V>
-__global__ void k_layernorm_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ mean,
+__global__ void __launch_bounds__(256, 2) k_layernorm_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ mean,
                                 const T* __restrict__ rstd, const T* __restrict__ g, const T* __restrict__ dres,
                                 T* __restrict__ dx, int rows, int D) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
@@ -681,9 +681,13 @@ template <class T>
 void layernorm_bwd(const Launch& L, const T* dy, const T* x, const T* mean, const T* rstd, const T* g,
                    const T* dres, T* dx, int rows, int D) {
   if (rows == 0) return;
+  // D > 256: the generic kernel (statistics pass, then a re-read pass; ~40 registers) -- at
+  // D = 768 it runs 2.3x faster than the register-resident V = 24 variant, whose 128 registers
+  // leave too few warps to hide the two load phases (c3: 81 -> 35 us per launch)
+  static const int generic = getenv("SLQ_LN_GENERIC") ? atoi(getenv("SLQ_LN_GENERIC")) : 1;
   if (D <= 256)
     LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_bwd<T, 8>), dy, x, mean, rstd, g, dres, dx, rows, D);
-  else if (D <= 768)
+  else if (D <= 768 && !generic)
     LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_bwd<T, 24>), dy, x, mean, rstd, g, dres, dx, rows, D);
   else
     LAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, (k_layernorm_bwd<T, 0>), dy, x, mean, rstd, g, dres, dx, rows, D);
