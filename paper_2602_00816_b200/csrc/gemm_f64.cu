@@ -386,6 +386,9 @@ int plan_variant(const GemmArgs<double>& a, int* splits) {
     // batched causal attention GEMMs at T <= 256 (tools/gemm_sweep_attn.py on B200: +12..28%)
     if (a.M <= 256 && a.N <= 256 && a.K <= 64) return 7;
     if (a.M <= 256 && a.N <= 64) return 11;
+    // T = 1024 (c3): the K = T contractions (P V, P^T dO, dS K, dS^T Q) on 32 x 64 tiles (+8%,
+    // tools/gemm_sweep_attn.py with T=1024 NB=96)
+    if (a.N <= 64 && a.K >= 512) return 6;
     return pick_variant(a);
   }
   const double mn = (double)a.M * a.N;
