@@ -61,7 +61,11 @@ def parse():
     p.add_argument("--reorth", default="config", choices=["config", "full", "none", "window"])
     p.add_argument("--window", type=int, default=8)
     p.add_argument("--basis", default="fp32", choices=["fp32", "bf16"])
-    return p.parse_args()
+    a = p.parse_args()
+    if a.config not in si.CONFIGS or si.CONFIGS[a.config].arch == si.ARCH_MLP:
+        p.error(f"--config {a.config}: bench lines are for the transformer configs "
+                f"({', '.join(k for k, c in si.CONFIGS.items() if c.arch != si.ARCH_MLP)}); c1 is a parity case")
+    return a
 
 
 def dist_env():
