@@ -30,6 +30,31 @@ __device__ __forceinline__ float dexp(float x) { return expf(x); }
 __device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
 __device__ __forceinline__ float dsqrt(float x) { return sqrtf(x); }
 
+// online softmax statistics: (m, s) with s = sum_j exp(x_j - m), m = max_j x_j
+template <class T>
+__device__ __forceinline__ void online_add(T& m, T& s, T x) {
+  if (x > m) {
+    s = s * dexp(m - x) + T(1);
+    m = x;
+  } else if (x > T(-INFINITY)) {  // (x = m = -inf would give exp(nan))
+    s += dexp(x - m);
+  }
+}
+template <class T>
+__device__ __forceinline__ void online_merge(T& m, T& s, T m2, T s2) {
+  const T mm = max(m, m2);
+  s = (m == mm ? s : s * dexp(m - mm)) + (m2 == mm ? s2 : s2 * dexp(m2 - mm));
+  m = mm;
+}
+template <class T>
+__device__ __forceinline__ void warp_online(T& m, T& s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    online_merge(m, s, m2, s2);
+  }
+}
+
 inline int grid_for(int64_t n, int threads, int cap = 148 * 16) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), cap));
 }
@@ -419,17 +444,12 @@ __global__ void k_softmax_causal(T* __restrict__ S, int64_t rows, int Tn) {
   if (row >= rows) return;
   const int t = (int)(row % Tn);
   T* s = S + row * Tn;
-  T mx = -INFINITY;
-  for (int j = lane; j <= t; j += kWarp) mx = max(mx, s[j]);
-  mx = warp_max(mx);
-  T sum = T(0);
-  for (int j = lane; j <= t; j += kWarp) {
-    const T e = dexp(s[j] - mx);
-    s[j] = e;
-    sum += e;
-  }
-  const T inv = T(1) / warp_sum(sum);
-  for (int j = lane; j < Tn; j += kWarp) s[j] = (j <= t) ? s[j] * inv : T(0);
+  // one read for the (online) max and sum, one read + write for the probabilities
+  T mx = -INFINITY, sum = T(0);
+  for (int j = lane; j <= t; j += kWarp) online_add(mx, sum, s[j]);
+  warp_online(mx, sum);
+  const T inv = T(1) / sum;
+  for (int j = lane; j < Tn; j += kWarp) s[j] = (j <= t) ? dexp(s[j] - mx) * inv : T(0);
 }
 
 // register-resident variant for Tn <= 32 V: lane l holds s[l + 32 i]; one read of the causal part
@@ -489,32 +509,28 @@ __global__ void k_cross_entropy(T* __restrict__ logits, const int32_t* __restric
   T* z = logits + (int64_t)row * V;
   const int b = row / Tn, t = row % Tn;
   const int y = tgt[(int64_t)b * tgt_stride + t];
-  __shared__ T red[32];
-  T mx = -INFINITY;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) mx = max(mx, z[j]);
-  mx = warp_max(mx);
-  if (threadIdx.x % kWarp == 0) red[threadIdx.x / kWarp] = mx;
+  __shared__ T red[32], red2[32];
+  // one read of the row for the online (max, sum of exponentials); one read + write for the gradient
+  T mx = -INFINITY, sm = T(0);
+  for (int j = threadIdx.x; j < V; j += blockDim.x) online_add(mx, sm, z[j]);
+  warp_online(mx, sm);
+  if (threadIdx.x % kWarp == 0) {
+    red[threadIdx.x / kWarp] = mx;
+    red2[threadIdx.x / kWarp] = sm;
+  }
   __syncthreads();
   if (threadIdx.x < kWarp) {
-    T v = threadIdx.x < blockDim.x / kWarp ? red[threadIdx.x] : T(-INFINITY);
-    v = warp_max(v);
-    if (threadIdx.x == 0) red[0] = v;
+    const bool ok = threadIdx.x < blockDim.x / kWarp;
+    T m = ok ? red[threadIdx.x] : T(-INFINITY), s2 = ok ? red2[threadIdx.x] : T(0);
+    warp_online(m, s2);
+    if (threadIdx.x == 0) {
+      red[0] = m;
+      red2[0] = s2;
+    }
   }
   __syncthreads();
   mx = red[0];
-  __syncthreads();
-  T s = T(0);
-  for (int j = threadIdx.x; j < V; j += blockDim.x) s += dexp(z[j] - mx);
-  s = warp_sum(s);
-  if (threadIdx.x % kWarp == 0) red[threadIdx.x / kWarp] = s;
-  __syncthreads();
-  if (threadIdx.x < kWarp) {
-    T v = threadIdx.x < blockDim.x / kWarp ? red[threadIdx.x] : T(0);
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  const T sum = red[0];
+  const T sum = red2[0];
   const T lse = mx + log(sum);
   if (threadIdx.x == 0) loss_rows[row] = (double)(lse - z[y]);
   __syncthreads();
@@ -526,9 +542,9 @@ __global__ void k_cross_entropy(T* __restrict__ logits, const int32_t* __restric
   }
 }
 
-// Register-resident variant for V <= 256 NV (one read and one write of the row instead of three
-// reads): thread t holds z[t + 256 i]; the max, the sum of exponentials (summed in the same
-// per-thread order as k_cross_entropy) and the gradient are formed from registers.
+// Register-resident variant for V <= 256 NV (one read and one write of the row): thread t holds
+// z[t + 256 i]; the exact max, then the sum of exponentials, and the gradient are formed from
+// registers.
 template <class T, int NV>
 __global__ void __launch_bounds__(256) k_cross_entropy_reg(T* __restrict__ logits, const int32_t* __restrict__ tgt,
                                                            int tgt_stride, int Tn, double* __restrict__ loss_rows,
