@@ -2,6 +2,8 @@
 """Benchmark of the SLQ / FD-HVP hot path (arXiv 2602.00816) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c2|...]
+                    [--numerics fp64_oz|fp64|bf16x3|bf16|fp32|paired|paired_fp32]
+                    [--reorth config|full|none|window [--window r]] [--basis fp32|bf16]
 
 Default workload: BASELINE.json configs[1] ("c2"): GPT 4 layers, d 256, 4 heads, MLP 1024 GELU,
 LayerNorm, learned positions, vocab 4096, 5,322,240 fp32 params; global batch 8 x 256 Zipf(1.1)
