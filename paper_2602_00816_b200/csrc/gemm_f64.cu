@@ -60,7 +60,7 @@ struct Smem {
 };
 
 template <class TL, bool AK, bool BKm>
-__global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : 1) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
+__global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : (TL::THREADS == 256 && TL::BM * TL::BN <= 4096 ? 3 : 1)) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
                                                                 double* __restrict__ ws, unsigned* __restrict__ cnt) {
   using SM = Smem<TL, AK, BKm>;
   constexpr int BM = TL::BM, BN = TL::BN, BK = TL::BK, S = TL::STAGES;
