@@ -99,6 +99,15 @@ typedef struct {
   int32_t perturb;         /* SLQ_PERTURB_*: how theta +- eta v is formed (reading R9) */
   int32_t reorth_window;   /* r for SLQ_REORTH_WINDOW (2 <= r); ignored otherwise */
   int32_t basis_dtype;     /* SLQ_BASIS_* */
+  /* SLQ_PASS_FP64_OZ only: dense GEMMs with M*N*K below oz_min_mnk stay on the FP64 DMMA pipe, the
+   * rest run as int8 digit products.  0 = library default (1e9, the measured break-even on B200);
+   * 1 puts every dense GEMM on the int8 path.  Per context (no process-global state). */
+  double oz_min_mnk;
+  int32_t oz_slices;       /* SLQ_PASS_FP64_OZ digit planes S (4..7); 0 = default 7 (< 7 misses the fp32 gates) */
+  /* 1: activation checkpointing (BASELINE configs[4]): each transformer block keeps only its input
+   * residual stream from the forward and recomputes its forward inside its backward (bit-identical
+   * gradients, +1 block forward per block, block activations for 2 blocks instead of n_layers) */
+  int32_t act_ckpt;
 } slq_model_desc;
 
 /* SLQ_PERTURB_EXACT: theta +- eta*v is evaluated in the pass precision (fp64 passes: an fp64
@@ -121,15 +130,34 @@ typedef struct {
   int32_t n_rows_local, n_rows_global;
 } slq_batch;
 
+/* Communication backend of a world_size > 1 context.  NCCL: the product path (one process per GPU).
+ * LOOPBACK: TEST ONLY -- world_size ranks as contexts of ONE process on one GPU, driven by one
+ * host thread each; every collective is host-synchronous (stream sync, host barrier, device
+ * copies / a fixed rank-order sum), so no kernel ever waits on another rank's kernel.  It runs
+ * the FSDP engine (per-unit all-gather / reduce-scatter, ping-pong buffers, prefetch, scalar
+ * all-reduces) at world_size > 1 without a second GPU; CUDA graphs are off in this mode.  The
+ * ranks of one group pass the same 128-byte key in nccl_unique_id. */
+enum { SLQ_COMM_NCCL = 0, SLQ_COMM_LOOPBACK = 1 };
+
 typedef struct {
   int32_t rank, world_size, device;
   const void* nccl_unique_id; /* 128 bytes from slq_nccl_unique_id() on rank 0, broadcast by the
-                                 caller; ignored when world_size == 1 */
-  void* cuda_stream;          /* cudaStream_t to run on, or NULL for a library-owned stream */
+                                 caller (LOOPBACK: the group key); ignored when world_size == 1 */
+  void* cuda_stream;          /* cudaStream_t to run on, or NULL for a library-owned stream.  A
+                                 library-owned stream orders every call after the work already
+                                 queued on the legacy default stream (where a caller's device
+                                 pointers are typically written); with a caller stream, ordering
+                                 is the caller's */
+  int32_t comm_backend;       /* SLQ_COMM_* (world_size > 1) */
 } slq_world;
 
-/* Create a context: validate, plan the FSDP layout, create the NCCL communicator (world > 1),
- * allocate device state, upload this rank's chunks of theta_0 and its data slice.  Collective. */
+/* Create a context: validate, plan the FSDP layout ("perturbations ... applied to each
+ * rank's local DTensor shard"), create the NCCL communicators (world > 1: one
+ * for the scalar all-reduces and one per concurrent gradient pass, split from it), check the
+ * device memory plan (slq_plan_memory) against the free memory (SLQ_ENOMEM with the plan in the
+ * message when it does not fit), allocate device state, upload this rank's chunks of theta_0 and
+ * its data slice (Alg. 1 "dataloader").  Every pointer in desc / batch / world is read
+ * during the call only.  Collective. */
 slq_status slq_init(const slq_model_desc* desc, const slq_batch* batch, const slq_world* world,
                     slq_ctx** out);
 slq_status slq_destroy(slq_ctx* ctx);
@@ -147,15 +175,28 @@ slq_status slq_unit_info(const slq_ctx* ctx, int32_t u, int64_t* global_offset, 
 slq_status slq_plan_layout(const slq_model_desc* desc, int32_t world_size, int64_t* P,
                            int64_t* P_loc, int32_t* n_units, int64_t* unit_table);
 
+/* Host-only device-memory plan (no GPU, no context) of one rank: the bytes slq_init would allocate
+ * for desc at world_size ranks with n_local sequences (MLP: rows) on this rank.  bytes[SLQ_MEM_COUNT]
+ * gets one entry per category below (SLQ_MEM_TOTAL = their sum).  Activations, logits, backward
+ * scratch and FSDP buffers are per gradient-pass executor (two run concurrently unless the paired
+ * mode is used); GEMM workspace is the largest Ozaki / split-K scratch of one pass (estimate). */
+enum { SLQ_MEM_THETA = 0, SLQ_MEM_POINTS, SLQ_MEM_GRADS, SLQ_MEM_LANCZOS, SLQ_MEM_FSDP, SLQ_MEM_ACTIVATIONS,
+       SLQ_MEM_LOGITS, SLQ_MEM_SCRATCH, SLQ_MEM_WORKSPACE, SLQ_MEM_TOTAL, SLQ_MEM_COUNT };
+slq_status slq_plan_memory(const slq_model_desc* desc, int32_t world_size, int32_t n_local, int64_t* bytes);
+
 /* 128-byte NCCL unique id for slq_world.nccl_unique_id (call on rank 0 only). */
 slq_status slq_nccl_unique_id(void* out128);
 
 /* Hv for a caller direction: out = ||v|| (grad L(theta + eps vhat) - grad L(theta - eps vhat))/(2 eps)
- * (Eq. (1); Alg. 1).  Implemented as a step eta = fl32(eps/||v||) along v:
- * theta+- = fmaf(+-eta, v, theta) out of place in fp32 (theta is never written, so it is
- * bit-identical afterwards), two gradient passes, out = (g+ - g-)/(2 eta).  ||v|| costs the
- * one scalar all-reduce P:197 allows.  v == 0 returns 0.  v_shard/out_shard must not alias.
- * Collective. */
+ * (Eq. (1); Alg. 1).  Implemented as a step eta = eps/||v|| along v with
+ * theta+- formed out of place (theta is never written, so it is bit-identical afterwards),
+ * two gradient passes, out = (g+ - g-)/(2 eta).  How theta+- is formed follows desc.perturb
+ * (reading R9): SLQ_PERTURB_EXACT (default) with fp64 passes forms theta +- eta v in
+ * fp64 (rounded product, rounded sum) with an fp64 divisor 2 eta; SLQ_PERTURB_STORAGE, and every
+ * fp32 pass mode, forms fmaf(+-fl32(eta), v, theta) rounded once to fp32 with divisor
+ * 2 fl32(eta).  ||v|| costs the one scalar all-reduce P:197 allows.  v == 0 returns 0.
+ * v_shard / out_shard: P_loc fp32 each, device or host, must not alias.  SLQ_ENUMERIC on a
+ * non-finite v or gradient (slq_nonfinite_seq names the sequence).  Collective. */
 slq_status slq_hvp(slq_ctx* ctx, const float* v_shard, float* out_shard, double eps);
 
 /* One gradient evaluation = the paper's T_grad (one forward + one backward with all

@@ -100,6 +100,14 @@ void* Workspace::get(size_t need, cudaStream_t) {
   bytes = nb;
   return ptr;
 }
+void Workspace::reserve(size_t need) {
+  if (need <= bytes) return;
+  if (ptr) retired.push_back(ptr);
+  ptr = nullptr;
+  bytes = 0;
+  SLQ_CUDA(cudaMalloc(&ptr, need));
+  bytes = need;
+}
 unsigned* Workspace::counters(size_t n) {
   if (n > kCounters) return nullptr;
   if (!cnt) {
@@ -109,6 +117,7 @@ unsigned* Workspace::counters(size_t n) {
   return cnt;
 }
 Workspace::~Workspace() {
+  if (!ptr && !cnt && retired.empty()) return;
   cudaDeviceSynchronize();
   if (ptr) cudaFree(ptr);
   if (cnt) cudaFree(cnt);
@@ -133,12 +142,14 @@ struct slq_ctx {
   std::string err;
   float* stage_in = nullptr;  // device staging for host-pointer calls
   float* stage_out = nullptr;
+  cudaEvent_t ev_entry = nullptr;  // library-owned stream: orders each call after the legacy stream
   Launch launch() { return Launch{stream, &prof, &ws, &launches}; }
   ~slq_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     engine.reset();
     if (stage_in) cudaFree(stage_in);
     if (stage_out) cudaFree(stage_out);
+    if (ev_entry) cudaEventDestroy(ev_entry);
     comm.reset();
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -178,10 +189,17 @@ bool is_device_ptr(const void* p) {
 
 // entry check of every call that runs the engine: the device, and a communicator that a watchdog
 // or an asynchronous NCCL error aborted (its captured graphs reference it: never replay them)
+// A library-owned stream is non-blocking (the library's internal streams synchronise with it by
+// events only), so each entry point makes it wait for the work already queued on the legacy
+// default stream, where callers (e.g. torch's default stream) write the device shards they pass.
 void check_device(slq_ctx* ctx) {
   SLQ_CUDA(cudaSetDevice(ctx->world.device));
   if (ctx->comm && ctx->comm->aborted())
     throw Error(SLQ_ENCCL, "the NCCL communicator was aborted (watchdog or peer failure); destroy the context");
+  if (ctx->own_stream && ctx->ev_entry) {
+    SLQ_CUDA(cudaEventRecord(ctx->ev_entry, cudaStreamLegacy));
+    SLQ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_entry, 0));
+  }
 }
 
 void ensure_stage(slq_ctx* ctx) {
@@ -214,6 +232,13 @@ slq_status slq_plan_layout(const slq_model_desc* desc, int32_t world, int64_t* P
         table[4 * u + 2] = p.units[u].local_offset;
         table[4 * u + 3] = p.units[u].chunk;
       }
+  });
+}
+
+slq_status slq_plan_memory(const slq_model_desc* desc, int32_t world_size, int32_t n_local, int64_t* bytes) {
+  return guarded(nullptr, [&] {
+    SLQ_CHECK_ARG(desc != nullptr && bytes != nullptr, "desc / bytes");
+    plan_memory(*desc, world_size, n_local, bytes);
   });
 }
 
@@ -261,15 +286,34 @@ slq_status slq_init(const slq_model_desc* desc, const slq_batch* batch, const sl
     } else {
       SLQ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
       ctx->own_stream = true;
+      SLQ_CUDA(cudaEventCreateWithFlags(&ctx->ev_entry, cudaEventDisableTiming));
+    }
+    SLQ_CHECK_ARG(world->comm_backend == SLQ_COMM_NCCL || world->comm_backend == SLQ_COMM_LOOPBACK, "comm_backend");
+    {  // the device-memory plan against the free memory, before allocating anything
+      int64_t mem[SLQ_MEM_COUNT];
+      plan_memory(*desc, world->world_size,
+                  desc->arch == SLQ_ARCH_MLP ? batch->n_rows_local : batch->n_seq_local, mem);
+      size_t free_b = 0, total_b = 0;
+      SLQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      if ((size_t)mem[SLQ_MEM_TOTAL] > free_b) {
+        static const char* names[SLQ_MEM_COUNT] = {"theta", "points", "grads", "lanczos", "fsdp", "activations",
+                                                   "logits", "scratch", "workspace", "total"};
+        std::string m = "device memory plan exceeds the free memory (" + std::to_string(free_b >> 20) + " MiB):";
+        for (int i = 0; i < SLQ_MEM_COUNT; ++i) m += std::string(" ") + names[i] + "=" + std::to_string(mem[i] >> 20) + "MiB";
+        throw Error(SLQ_ENOMEM, m + " (try act_ckpt = 1, a larger world_size or a smaller batch)");
+      }
     }
     if (world->world_size > 1) {
-      ctx->comm.reset(new Comm(world->nccl_unique_id, world->rank, world->world_size, world->device));
+      if (world->comm_backend == SLQ_COMM_LOOPBACK)
+        ctx->comm = make_loopback_comm(world->nccl_unique_id, world->rank, world->world_size, world->device);
+      else
+        ctx->comm = make_nccl_comm(world->nccl_unique_id, world->rank, world->world_size, world->device);
     } else if (getenv("SLQ_FORCE_NCCL") && atoi(getenv("SLQ_FORCE_NCCL")) != 0) {
       // diagnostic: a one-rank NCCL communicator, so the FSDP path (per-unit all-gather /
       // reduce-scatter, scalar all-reduces) runs on a single GPU (tests/test_gpu_fsdp1.py)
       char uid[128];
       nccl_unique_id(uid);
-      ctx->comm.reset(new Comm(uid, 0, 1, world->device));
+      ctx->comm = make_nccl_comm(uid, 0, 1, world->device);
     }
     ctx->engine = make_engine(*desc, ctx->plan, hb, batch->params_host, world->rank, ctx->comm.get(),
                               ctx->launch());
@@ -495,7 +539,7 @@ void* slq_stream(const slq_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr
 slq_status slq_collective_counts(const slq_ctx* ctx, int64_t* ag, int64_t* rs, int64_t* ar) {
   if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
   CommCounts c;
-  if (ctx->comm) c = ctx->comm->counts;
+  if (ctx->comm) c = ctx->comm->total_counts();
   if (ag) *ag = c.allgather;
   if (rs) *rs = c.reduce_scatter;
   if (ar) *ar = c.allreduce;

@@ -1,10 +1,19 @@
-// NCCL collectives of the FSDP path: per-unit all-gather of the working
-// parameters, per-unit reduce-scatter (sum) of gradients, and the small fp64 all-reduces of the
-// Lanczos scalars.  All calls are stream-ordered on the caller's stream.
+// Collectives of the FSDP path: per-unit all-gather of the working parameters,
+// per-unit reduce-scatter (sum) of gradients, and the small fp64 all-reduces of the Lanczos
+// scalars.  All calls are stream-ordered on the caller's stream.
+//
+// Two backends behind one interface: NCCL (the product path, one process per GPU) and LOOPBACK
+// (test only, SLQ_COMM_LOOPBACK in slq.h): the ranks are contexts of one process on one GPU, one
+// host thread each, and every collective is host-synchronous -- the caller's stream is drained, the
+// ranks meet at a host barrier, the data moves by device copies / a fixed rank-order sum kernel,
+// and a second barrier releases the send buffers.  No kernel ever waits on another rank's kernel.
 #pragma once
 
 #include <stddef.h>
 #include <stdint.h>
+
+#include <memory>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -19,22 +28,32 @@ struct CommCounts {
 
 class Comm {
  public:
-  Comm(const void* unique_id128, int rank, int world, int device);
-  ~Comm();
-  void allgather(const void* send, void* recv, size_t count_per_rank, CommType t, cudaStream_t s);
-  void reduce_scatter(const void* send, void* recv, size_t count_per_rank, CommType t, cudaStream_t s);
-  void allreduce_sum_f64(double* buf, size_t count, cudaStream_t s);
-  void abort();
-  bool aborted() const { return comm_ == nullptr; }
-  void check_async();  // throws SLQ_ENCCL (after aborting) on an asynchronous NCCL error
+  virtual ~Comm() {}
+  virtual void allgather(const void* send, void* recv, size_t count_per_rank, CommType t, cudaStream_t s) = 0;
+  virtual void reduce_scatter(const void* send, void* recv, size_t count_per_rank, CommType t, cudaStream_t s) = 0;
+  virtual void allreduce_sum_f64(double* buf, size_t count, cudaStream_t s) = 0;
+  // abort this communicator and every communicator split from it
+  virtual void abort() = 0;
+  virtual bool aborted() const = 0;
+  // throws SLQ_ENCCL (after aborting) on an asynchronous error of this or a split communicator
+  virtual void check_async() = 0;
+  // collective: a new communicator over the same ranks (one per concurrent gradient pass), owned
+  // by this one (aborted with it, counted in total_counts)
+  virtual Comm* split(int color) = 0;
+  // true: collectives block the host (loopback) -- they cannot be captured into CUDA graphs
+  virtual bool host_sync() const { return false; }
   int rank() const { return rank_; }
   int world() const { return world_; }
   CommCounts counts;
+  CommCounts total_counts() const;  // this communicator plus its splits
 
- private:
-  void* comm_ = nullptr;  // ncclComm_t
-  int rank_, world_;
+ protected:
+  int rank_ = 0, world_ = 1;
+  std::vector<std::unique_ptr<Comm>> children_;
 };
+
+std::unique_ptr<Comm> make_nccl_comm(const void* unique_id128, int rank, int world, int device);
+std::unique_ptr<Comm> make_loopback_comm(const void* key128, int rank, int world, int device);
 
 void nccl_unique_id(void* out128);
 

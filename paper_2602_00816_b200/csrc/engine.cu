@@ -183,6 +183,12 @@ struct PassExec {
     lio.plan = &plan;
     lio2.plan = &plan;
   }
+  // FSDP: this executor's collectives go through f (host-synchronous loopback collectives cannot
+  // be captured, so such a pass stays eager)
+  void attach(FsdpIO<T>* f) {
+    fio = f;
+    if (f->comm->host_sync()) use_graphs = false;
+  }
   ~PassExec() {
     if (L.stream) cudaStreamSynchronize(L.stream);
     for (auto& x : graphs)
@@ -281,11 +287,12 @@ struct EngineT : Engine {
   int* dflag;
   UnitDev* units_dev;
   int max_steps;
-  FsdpIO<T> fio;
-  // pe[0] runs on the context stream; with world_size == 1 a second executor on its own stream
-  // evaluates the theta- pass concurrently with the theta+ pass (the two gradient evaluations of
-  // Eq. (1) are independent until the FD difference).  With FSDP both passes share the NCCL
-  // communicator, so they stay serial.
+  // pe[0] runs on the context stream; a second executor on its own stream evaluates the theta-
+  // pass concurrently with the theta+ pass (the two gradient evaluations of Eq. (1) are independent
+  // until the FD difference).  With FSDP each executor has its own FsdpIO (ping-pong buffers) and
+  // its own communicator split from the context's, so the two passes' collectives never have to
+  // be ordered against each other; the context communicator carries the scalar all-reduces.
+  FsdpIO<T> fio[2];
   std::unique_ptr<PassExec<T>> pe[2];
   bool dual = false;
   // paired evaluation (SLQ_PASS_PAIRED*): thm holds thetatil = eta v, gp gets gbar, gm gets gtil;
@@ -356,26 +363,28 @@ struct EngineT : Engine {
     SLQ_CUDA(cudaMallocHost(&hstage, (64 + 2 * (size_t)(max_steps + 1)) * sizeof(double)));
     paired_ = d.pass_numerics == SLQ_PASS_PAIRED || d.pass_numerics == SLQ_PASS_PAIRED_FP32;
     if (paired_ && comm) throw Error(SLQ_EUNSUPPORTED, "paired evaluation with world_size > 1 is not implemented");
-    pe[0].reset(new PassExec<T>(d, plan, b, L, false, paired_));
-    fio.plan = &plan;
-    fio.comm = comm;
-    fio.s = L.stream;
-    if (paired_) {
-      // one pass evaluates both points; nothing to run concurrently
-    } else if (comm) {
+    // one pass evaluates both points in the paired modes: nothing to run concurrently
+    dual = !paired_ && getenv("SLQ_SERIAL_PASSES") == nullptr;
+    const int nexec = dual ? 2 : 1;
+    for (int i = 0; i < nexec; ++i) {
+      pe[i].reset(new PassExec<T>(d, plan, b, L, i > 0, paired_));
+      if (!comm) continue;
+      FsdpIO<T>& f = fio[i];
+      f.plan = &plan;
+      f.comm = comm->split(i);
+      f.s = pe[i]->L.stream;
       int64_t mx = 0;
       for (const UnitPlan& u : plan.units) mx = std::max(mx, u.padded);
-      fio.pbuf0 = dalloc<T>(plan.units[0].padded);
-      fio.gbuf0 = dalloc<T>(plan.units[0].padded);
-      for (int i = 0; i < 2; ++i) {
-        fio.pb[i] = dalloc<T>(mx);
-        fio.gb[i] = dalloc<T>(mx);
+      f.pbuf0 = dalloc<T>(plan.units[0].padded);
+      f.gbuf0 = dalloc<T>(plan.units[0].padded);
+      for (int k = 0; k < 2; ++k) {
+        f.pb[k] = dalloc<T>(mx);
+        f.gb[k] = dalloc<T>(mx);
       }
-      fio.init();
-      pe[0]->fio = &fio;
-    } else if (getenv("SLQ_SERIAL_PASSES") == nullptr) {
-      pe[1].reset(new PassExec<T>(d, plan, b, L, true));
-      dual = true;
+      f.init();
+      pe[i]->attach(&f);
+    }
+    if (dual) {
       SLQ_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
       SLQ_CUDA(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
     }
@@ -747,18 +756,89 @@ struct EngineT : Engine {
 
 }  // namespace
 
+// the pass-mode fields of a Launch (GEMM route, Ozaki settings) from the descriptor
+Launch pass_launch(const slq_model_desc& d, const Launch& L) {
+  Launch Lp = L;
+  if (d.pass_numerics == SLQ_PASS_FP64 || d.pass_numerics == SLQ_PASS_FP64_OZ) {
+    Lp.gemm_mode = d.pass_numerics == SLQ_PASS_FP64_OZ ? 2 : 0;
+    // measured on B200 (c2 step, tools/exp_oz.sh): the int8 path wins on the 2e9-MNK head GEMMs and
+    // breaks even below ~1e9, where the slicing launches and the fp64 epilogue dominate
+    Lp.oz_min_mnk = d.oz_min_mnk > 0 ? d.oz_min_mnk : 1e9;
+    Lp.oz_S = d.oz_slices > 0 ? d.oz_slices : 7;
+    SLQ_CHECK_ARG(Lp.oz_S >= 4 && Lp.oz_S <= 7, "oz_slices must be 0 (default 7) or 4..7");
+  } else {
+    Lp.gemm_mode = (d.pass_numerics == SLQ_PASS_BF16X3 || d.pass_numerics == SLQ_PASS_PAIRED) ? 1
+                   : d.pass_numerics == SLQ_PASS_BF16                                         ? 3
+                                                                                              : 0;
+  }
+  return Lp;
+}
+
 std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
                                     const float* theta_host, int rank, Comm* comm, const Launch& L) {
-  if (d.pass_numerics == SLQ_PASS_FP64 || d.pass_numerics == SLQ_PASS_FP64_OZ) {
-    Launch Ld = L;
-    Ld.gemm_mode = d.pass_numerics == SLQ_PASS_FP64_OZ ? 2 : 0;
-    return std::unique_ptr<Engine>(new EngineT<double>(d, plan, b, theta_host, rank, comm, Ld));
+  const Launch Lp = pass_launch(d, L);
+  if (d.pass_numerics == SLQ_PASS_FP64 || d.pass_numerics == SLQ_PASS_FP64_OZ)
+    return std::unique_ptr<Engine>(new EngineT<double>(d, plan, b, theta_host, rank, comm, Lp));
+  return std::unique_ptr<Engine>(new EngineT<float>(d, plan, b, theta_host, rank, comm, Lp));
+}
+
+namespace {
+template <class T>
+void plan_runner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& hb, const Launch& Lp,
+                 int64_t* out, int nexec) {
+  auto r = make_runner<T>(d, plan, hb, Lp, true);
+  size_t wm = 0, wsd = 0;
+  r->plan_ws(wm, wsd);
+  out[SLQ_MEM_ACTIVATIONS] += nexec * (int64_t)r->arena_bytes(0);
+  out[SLQ_MEM_LOGITS] += nexec * (int64_t)r->arena_bytes(1);
+  out[SLQ_MEM_SCRATCH] += nexec * (int64_t)r->arena_bytes(2);
+  const int64_t counters = (int64_t)(sizeof(unsigned) * Workspace::kCounters);
+  out[SLQ_MEM_WORKSPACE] += nexec * ((int64_t)wm + (int64_t)wsd + 2 * counters);
+}
+}  // namespace
+
+// Host-only mirror of the allocations of EngineT + its PassExecs + their runners (the runners are
+// built in dry mode, so their byte counts are the real allocation code's)
+void plan_memory(const slq_model_desc& d, int world, int n_local, int64_t* out) {
+  SLQ_CHECK_ARG(world >= 1 && n_local >= 1, "world_size >= 1, n_local >= 1");
+  for (int i = 0; i < SLQ_MEM_COUNT; ++i) out[i] = 0;
+  const LayoutPlan plan = plan_layout(d, world);
+  const bool f64 = d.pass_numerics == SLQ_PASS_FP64 || d.pass_numerics == SLQ_PASS_FP64_OZ;
+  const bool paired = d.pass_numerics == SLQ_PASS_PAIRED || d.pass_numerics == SLQ_PASS_PAIRED_FP32;
+  const int64_t esz = f64 ? 8 : 4, n = plan.P_loc, ms = d.max_steps;
+  const int nexec = (paired || getenv("SLQ_SERIAL_PASSES")) ? 1 : 2;
+  out[SLQ_MEM_THETA] = 4 * n;
+  out[SLQ_MEM_POINTS] = 2 * esz * n;
+  out[SLQ_MEM_GRADS] = 2 * esz * n;
+  int64_t lz = 4 * n + 8 * (8 + 5 * (ms + 1));  // w, device scalars
+  if (d.reorth == SLQ_REORTH_FULL || d.reorth == SLQ_REORTH_WINDOW) {
+    const int64_t rows = d.reorth == SLQ_REORTH_FULL ? ms + 1 : d.reorth_window;
+    lz += d.basis_dtype == SLQ_BASIS_BF16 ? rows * n * 2 + 2 * 4 * n : rows * n * 4;
+    const int64_t ldg = d.reorth == SLQ_REORTH_FULL ? ms + 1 : d.reorth_window;
+    lz += 8 * ldg * ldg;
+  } else {
+    lz += 3 * 4 * n;
   }
-  Launch Lf = L;
-  Lf.gemm_mode = (d.pass_numerics == SLQ_PASS_BF16X3 || d.pass_numerics == SLQ_PASS_PAIRED) ? 1
-                  : d.pass_numerics == SLQ_PASS_BF16                                         ? 3
-                                                                                             : 0;
-  return std::unique_ptr<Engine>(new EngineT<float>(d, plan, b, theta_host, rank, comm, Lf));
+  lz += 8 * std::max<int64_t>(vec_nblocks(n), (int64_t)reorth_nblocks(n) * 2 * (ms + 1));
+  out[SLQ_MEM_LANCZOS] = lz;
+  if (world > 1) {
+    int64_t mx = 0;
+    for (const UnitPlan& u : plan.units) mx = std::max(mx, u.padded);
+    out[SLQ_MEM_FSDP] = nexec * esz * (2 * plan.units[0].padded + 4 * mx);
+  }
+  HostBatch hb;
+  if (d.arch == SLQ_ARCH_MLP) {
+    hb.n_rows = n_local;
+    hb.n_rows_global = n_local * world;
+  } else {
+    hb.n_seq = n_local;
+    hb.n_seq_global = n_local * world;
+  }
+  const Launch Lp = pass_launch(d, Launch{nullptr, nullptr, nullptr, nullptr});
+  if (f64) plan_runner<double>(d, plan, hb, Lp, out, nexec);
+  else plan_runner<float>(d, plan, hb, Lp, out, nexec);
+  out[SLQ_MEM_WORKSPACE] += 2 * 4 * n;  // staging of host-pointer calls (allocated on first use)
+  for (int i = 0; i < SLQ_MEM_TOTAL; ++i) out[SLQ_MEM_TOTAL] += out[i];
 }
 
 }  // namespace slq

@@ -34,6 +34,9 @@ struct Engine {
   int nonfinite_seq = -1;
 };
 
+// slq_plan_memory: the per-rank device bytes by category (slq.h SLQ_MEM_*)
+void plan_memory(const slq_model_desc& d, int world, int n_local, int64_t* out);
+
 std::unique_ptr<Engine> make_engine(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
                                     const float* theta_host_full, int rank, Comm* comm, const Launch& L);
 

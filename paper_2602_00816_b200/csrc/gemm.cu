@@ -187,4 +187,22 @@ void gemm(const Launch& L, const GemmArgs<T>& a) {
 
 template void gemm<float>(const Launch&, const GemmArgs<float>&);
 
+template <>
+size_t gemm_ws_bytes<float>(const Launch& L, const GemmArgs<float>& a) {
+  if (a.M == 0 || a.N == 0) return 0;
+  if ((L.gemm_mode == 1 || L.gemm_mode == 3) && a.batch == 1 && a.K > 0)
+    return tc_ws_bytes(a.M, a.N, a.K, L.gemm_mode == 3 ? 1 : 3);
+  constexpr int BM = 64, BN = 64, BK = 16;  // launch_cfg's decisions
+  const int tiles = (int)(ceil_div(a.M, BM) * ceil_div(a.N, BN)) * a.batch;
+  int splits = 1;
+  if (a.batch == 1 && a.tri == TRI_NONE && tiles < 2 * 148 && a.K >= 512) {
+    splits = (int)ceil_div(2 * 148, tiles);
+    splits = std::min<int>(splits, (int)(a.K / 256));
+    splits = std::max(1, std::min(splits, 32));
+  }
+  const int kchunk = (int)ceil_div(ceil_div(a.K, splits), BK) * BK;
+  splits = (int)ceil_div(a.K, kchunk);
+  return splits > 1 ? sizeof(float) * (size_t)splits * a.M * a.N : 0;
+}
+
 }  // namespace slq

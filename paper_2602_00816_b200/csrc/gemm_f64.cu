@@ -60,7 +60,7 @@ struct Smem {
 };
 
 template <class TL, bool AK, bool BKm>
-__global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? 4 : (TL::THREADS == 256 && TL::BM * TL::BN <= 4096 ? 3 : 1)) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
+__global__ void __launch_bounds__(TL::THREADS, TL::THREADS == 128 ? (TL::BK >= 32 ? 2 : TL::BM * TL::BN >= 4096 ? 3 : 4) : (TL::THREADS == 256 && TL::BM * TL::BN <= 4096 ? 3 : 1)) gemm_dmma_kernel(GemmArgs<double> p, int splits, int kchunk,
                                                                 double* __restrict__ ws, unsigned* __restrict__ cnt) {
   using SM = Smem<TL, AK, BKm>;
   constexpr int BM = TL::BM, BN = TL::BN, BK = TL::BK, S = TL::STAGES;
@@ -271,15 +271,14 @@ double gemm_flops(const GemmArgs<double>& a) {
 }
 
 // auto split-K: fill ~2 waves of CTAs when the tile grid is small and K is long
-template <class TL>
-int choose_splits(const GemmArgs<double>& a, int tiles, int forced) {
+int choose_splits(const GemmArgs<double>& a, int tiles, int forced, int BK) {
   if (forced > 0) return forced;
   static const int min_k = getenv("SLQ_DMMA_SPLIT_MIN_K") ? atoi(getenv("SLQ_DMMA_SPLIT_MIN_K")) : 256;
   static const int waves = getenv("SLQ_DMMA_SPLIT_WAVES") ? atoi(getenv("SLQ_DMMA_SPLIT_WAVES")) : 2;
   // batched: only the long-K weight-gradient batches (attention batches keep their tuned plans)
   if ((a.batch != 1 && a.K < 2048) || a.tri != TRI_NONE || a.K < min_k || tiles >= waves * 148) return 1;
   int s = (int)ceil_div(waves * 148, tiles);
-  s = std::min<int>(s, (int)(a.K / (4 * TL::BK)));
+  s = std::min<int>(s, (int)(a.K / (4 * BK)));
   return std::max(1, std::min(s, 32));
 }
 
@@ -293,7 +292,7 @@ void launch(const Launch& L, const GemmArgs<double>& a, int forced_splits) {
     attr_set = true;
   }
   const int tiles_m = (int)ceil_div(a.M, TL::BM), tiles_n = (int)ceil_div(a.N, TL::BN);
-  int splits = choose_splits<TL>(a, tiles_m * tiles_n * a.batch, forced_splits);
+  int splits = choose_splits(a, tiles_m * tiles_n * a.batch, forced_splits, TL::BK);
   const int kchunk = (int)ceil_div(ceil_div(a.K, splits), TL::BK) * TL::BK;
   splits = std::max(1, (int)ceil_div(a.K, kchunk));
   double* ws = nullptr;
@@ -335,6 +334,9 @@ using V12 = Tile<32, 64, 16, 2, 4, 3>;
 using V13 = Tile<128, 64, 16, 8, 2, 2>;
 using V14 = Tile<64, 64, 32, 4, 4, 2>;
 constexpr int kVariants = 15;
+constexpr int kVarDims[kVariants][3] = {{64, 64, 16}, {64, 64, 16}, {64, 64, 32}, {128, 64, 16}, {64, 128, 16},
+                                        {128, 128, 16}, {32, 64, 16}, {64, 32, 16}, {128, 64, 32}, {64, 64, 16},
+                                        {64, 64, 16}, {64, 32, 16}, {32, 64, 16}, {128, 64, 16}, {64, 64, 32}};
 
 template <bool AK, bool BKm>
 void launch_variant(const Launch& L, const GemmArgs<double>& a, int v, int splits) {
@@ -414,6 +416,16 @@ void check(const GemmArgs<double>& a) {
   SLQ_CHECK_ARG((a.act != ACT_DGELU && a.act != ACT_DTANH) || a.aux, "derivative epilogue needs aux");
 }
 
+// split-K workspace bytes the DMMA launch of variant v takes (the same decisions as launch<>)
+size_t dmma_ws_bytes(const GemmArgs<double>& a, int v, int forced) {
+  const int BM = kVarDims[v][0], BN = kVarDims[v][1], BK = kVarDims[v][2];
+  const int tiles = (int)(ceil_div(a.M, BM) * ceil_div(a.N, BN)) * a.batch;
+  int splits = choose_splits(a, tiles, forced, BK);
+  const int kchunk = (int)ceil_div(ceil_div(a.K, splits), BK) * BK;
+  splits = std::max(1, (int)ceil_div(a.K, kchunk));
+  return splits > 1 ? sizeof(double) * (size_t)splits * a.M * a.N * a.batch : 0;
+}
+
 void run(const Launch& L, const GemmArgs<double>& a, int v, int splits) {
   const bool ak = a.sAk == 1 && !(a.sAm == 1 && a.K == 1);
   const bool bk = a.sBk == 1 && !(a.sBn == 1 && a.K == 1);
@@ -434,13 +446,79 @@ __global__ void k_fill(double* x, int64_t n, uint64_t seed) {
 
 }  // namespace
 
+// Ozaki GEMMs whose digit planes + split-K partials would exceed kOzWsCap are cut into blocks
+// computed one after the other in the same workspace (the c5 head GEMMs ask for up to 8 GB
+// otherwise): the output is split along M or N (independent blocks, any epilogue), or -- when the
+// output is small and K long, and the epilogue is a plain (scaled, optionally accumulating) store --
+// K is split and the blocks accumulate into C.
+constexpr size_t kOzWsCap = (size_t)1 << 30;
+struct OzBlocks {
+  int mb, nb, kb;  // block extents
+};
+bool oz_k_splittable(const GemmArgs<double>& a) {
+  return !a.bias && !a.resid && !a.aux && !a.C2 && a.act == ACT_NONE;
+}
+OzBlocks oz_blocks(const GemmArgs<double>& a, int S) {
+  OzBlocks b{a.M, a.N, a.K};
+  auto half = [](int x, int q) { return (int)(ceil_div(ceil_div(x, 2), q) * q); };
+  for (int it = 0; it < 64 && oz_ws_bytes(b.mb, b.nb, b.kb, S) > kOzWsCap; ++it) {
+    const bool m_big = b.mb >= b.nb;
+    const int big = m_big ? b.mb : b.nb, small = m_big ? b.nb : b.mb;
+    if (big > 4 * small || !oz_k_splittable(a) || b.kb < 256) {
+      if (big < 256) break;
+      if (m_big) b.mb = half(b.mb, 128);
+      else b.nb = half(b.nb, 128);
+    } else {
+      b.kb = half(b.kb, 64);
+    }
+  }
+  return b;
+}
+void gemm_oz_blocked(const Launch& L, const GemmArgs<double>& a) {
+  const OzBlocks b = oz_blocks(a, L.oz_S);
+  if (b.mb == a.M && b.nb == a.N && b.kb == a.K) {
+    gemm_oz(L, a, L.oz_S);
+    return;
+  }
+  for (int k0 = 0; k0 < a.K; k0 += b.kb)
+    for (int m0 = 0; m0 < a.M; m0 += b.mb)
+      for (int n0 = 0; n0 < a.N; n0 += b.nb) {
+        GemmArgs<double> c = a;
+        c.M = std::min(b.mb, a.M - m0);
+        c.N = std::min(b.nb, a.N - n0);
+        c.K = std::min(b.kb, a.K - k0);
+        c.A = a.A + (int64_t)m0 * a.sAm + (int64_t)k0 * a.sAk;
+        c.B = a.B + (int64_t)k0 * a.sBk + (int64_t)n0 * a.sBn;
+        c.C = a.C + (int64_t)m0 * a.ldc + n0;
+        if (a.bias) c.bias = a.bias + n0;
+        if (a.resid) c.resid = a.resid + (int64_t)m0 * a.ldr + n0;
+        if (a.aux) c.aux = a.aux + (int64_t)m0 * a.ldaux + n0;
+        if (a.C2) c.C2 = a.C2 + (int64_t)m0 * a.ldc2 + n0;
+        c.accumulate = a.accumulate || k0 > 0;
+        gemm_oz(L, c, L.oz_S);
+      }
+}
+
+template <>
+size_t gemm_ws_bytes<double>(const Launch& L, const GemmArgs<double>& a) {
+  if (a.M == 0 || a.N == 0) return 0;
+  if (L.gemm_mode == 2 && a.batch == 1 && a.tri == TRI_NONE && a.K > 0 &&
+      (double)a.M * a.N * (double)a.K >= L.oz_min_mnk) {
+    const OzBlocks b = oz_blocks(a, L.oz_S);
+    return oz_ws_bytes(b.mb, b.nb, b.kb, L.oz_S);
+  }
+  int splits = 0;
+  const int v = plan_variant(a, &splits);
+  return dmma_ws_bytes(a, v, splits);
+}
+
 template <>
 void gemm<double>(const Launch& L, const GemmArgs<double>& a) {
   check(a);
   if (a.M == 0 || a.N == 0) return;
   if (L.gemm_mode == 2 && a.batch == 1 && a.tri == TRI_NONE && a.K > 0 &&
-      (double)a.M * a.N * (double)a.K >= oz_min_mnk()) {
-    gemm_oz(L, a, oz_slices());
+      (double)a.M * a.N * (double)a.K >= L.oz_min_mnk) {
+    gemm_oz_blocked(L, a);
     return;
   }
   int splits = 0;

@@ -17,6 +17,7 @@ struct Workspace {
   size_t bytes = 0;
   std::vector<void*> retired;              // outgrown buffers (graphs may reference them)
   void* get(size_t need, cudaStream_t s);  // grows when too small; never frees a live buffer
+  void reserve(size_t need);               // exactly `need` bytes up front (the planned maximum)
   // zero-initialised arrival counters (fixed size, allocated on first use outside graph capture);
   // every kernel that uses them leaves them zero again.  nullptr when n exceeds the array.
   unsigned* cnt = nullptr;
@@ -33,6 +34,8 @@ struct Launch {
   int gemm_mode = 0;  // float GEMMs: 0 = SIMT fp32, 1 = tcgen05 bf16x3 split (fp32-faithful),
                       // 3 = tcgen05 single bf16 term (native bf16);
                       // double GEMMs: 0 = DMMA (mma.sync f64), 2 = tcgen05 int8 Ozaki (gemm_oz)
+  double oz_min_mnk = 1e9;  // gemm_mode 2: dense GEMMs with M N K below this stay on DMMA (desc.oz_min_mnk)
+  int oz_S = 7;             // gemm_mode 2: Ozaki digit planes (desc.oz_slices)
 };
 
 // batch addressing of one operand: offset(z) = (z / div) * outer + ((z % div) / rep) * inner
@@ -78,12 +81,16 @@ struct GemmArgs {
 
 template <class T>
 void gemm(const Launch& L, const GemmArgs<T>& a);
+// workspace bytes L.ws->get() is asked for by gemm(L, a) (split-K partials, Ozaki digit planes):
+// the memory plan and the up-front reservation of every pass workspace use it
+template <class T>
+size_t gemm_ws_bytes(const Launch& L, const GemmArgs<T>& a);
+size_t oz_ws_bytes(int M, int N, int K, int S);
+size_t tc_ws_bytes(int M, int N, int K, int terms);
 
 // fp64 GEMM as exact INT8 digit products on the tcgen05 tensor cores (Ozaki scheme, S digit
 // planes of 7 bits per operand; oz_gemm.cu).  batch == 1, dense (tri == TRI_NONE) only.
 void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S);
-int oz_slices();      // S for the pass path: SLQ_OZ_SLICES (4..7), default 7
-double oz_min_mnk();  // FP64_OZ: smaller GEMMs (M N K below this) stay on DMMA (SLQ_OZ_MIN_MNK)
 
 // fp32-faithful GEMM on the tcgen05 tensor cores: every fp32 operand is split into three bf16
 // terms (x = x0 + x1 + x2, 24 significant bits) and the six products with i + j <= 2 are

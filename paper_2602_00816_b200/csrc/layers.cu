@@ -38,6 +38,9 @@ __device__ __forceinline__ void online_add(T& m, T& s, T x) {
     m = x;
   } else if (x > T(-INFINITY)) {  // (x = m = -inf would give exp(nan))
     s += dexp(x - m);
+  } else if (x != x) {  // NaN: both comparisons are false; poison the row (the loss must be non-finite)
+    m = x;
+    s = x;
   }
 }
 template <class T>

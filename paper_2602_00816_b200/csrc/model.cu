@@ -27,11 +27,19 @@ int first_nonfinite_group(const double* dev, int n, int per, cudaStream_t s) {
 
 namespace {
 
+// Device allocations of one runner.  Every allocation is counted under the memory-plan category
+// set in `cat`; a dry arena (slq_plan_memory) only counts and returns nullptr.
+enum { AC_ACT = 0, AC_LOGITS, AC_SCRATCH, AC_COUNT };
 struct Arena {
   std::vector<void*> ptrs;
+  bool dry = false;
+  int cat = AC_ACT;
+  size_t bytes[AC_COUNT] = {};
   template <class T>
   T* alloc(int64_t n) {
     void* p = nullptr;
+    bytes[cat] += sizeof(T) * (size_t)std::max<int64_t>(n, 0);
+    if (dry) return nullptr;
     if (n > 0) SLQ_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)n));
     ptrs.push_back(p);
     return (T*)p;
@@ -41,6 +49,36 @@ struct Arena {
       if (p) cudaFree(p);
   }
 };
+
+// Upper bound of the embedding-backward chunk count (build_embed_csr): every vocabulary row that
+// occurs gets ceil(count / kEmbedChunk) chunks, so <= N / kEmbedChunk + min(V, N) over all rows
+inline int64_t embed_chunks_bound(int64_t N, int64_t V) { return N / kEmbedChunk + std::min(V, N) + 1; }
+
+// workspace of the column reductions (colreduce in layers.cu) for [rows x cols]
+template <class T>
+size_t colreduce_ws_bytes(int rows, int cols) {
+  const int cblocks = (int)ceil_div(cols, 32);
+  int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), ceil_div(2 * 148, cblocks)));
+  const int rpb = (int)ceil_div(std::max(rows, 1), rblocks);
+  rblocks = (int)ceil_div(std::max(rows, 1), rpb);
+  return sizeof(T) * 2 * (size_t)rblocks * cols;
+}
+
+// shape-only GEMM descriptors for workspace planning (the plans depend on M, N, K, batch, tri)
+template <class T>
+GemmArgs<T> shape(int M, int N, int K) {
+  GemmArgs<T> a;
+  a.M = M; a.N = N; a.K = K;
+  return a;
+}
+// the largest workspace the linear layer [out x in] over N rows asks for on the data-gradient
+// lane (forward + dgrad) and on the weight-gradient lane (wgrad)
+template <class T>
+void linear_ws(const Launch& L, int out, int in, int N, size_t& main, size_t& side) {
+  main = std::max(main, gemm_ws_bytes<T>(L, shape<T>(N, out, in)));
+  main = std::max(main, gemm_ws_bytes<T>(L, shape<T>(N, in, out)));
+  side = std::max(side, gemm_ws_bytes<T>(L, shape<T>(out, in, N)));
+}
 
 // y[N x out] = x[N x in] . W[out x in]^T (+ bias) (+ resid), optional activation
 template <class T>
@@ -250,7 +288,7 @@ struct SideStream {
 template <class T>
 T* upload(Arena& A, const void* host, int64_t n) {
   T* d = A.alloc<T>(n);
-  if (n > 0) SLQ_CUDA(cudaMemcpy(d, host, sizeof(T) * (size_t)n, cudaMemcpyHostToDevice));
+  if (n > 0 && !A.dry) SLQ_CUDA(cudaMemcpy(d, host, sizeof(T) * (size_t)n, cudaMemcpyHostToDevice));
   return d;
 }
 
@@ -265,17 +303,35 @@ struct MlpRunner : Runner<T> {
   int32_t* y;
   double* loss_rows;
 
-  MlpRunner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b, const Launch& L_) : L(L_) {
+  MlpRunner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b, const Launch& L_, bool dry = false)
+      : L(L_) {
+    A.dry = dry;
     u = &plan.units[0];
     n = b.n_rows; n_glob = b.n_rows_global; din = d.d_in; H = d.d_hidden; C = d.n_classes;
     float* xf = upload<float>(A, b.x.data(), (int64_t)n * din);
     x = A.alloc<T>((int64_t)n * din);
-    convert_f32<T>(L, xf, x, (int64_t)n * din);
+    if (!dry) convert_f32<T>(L, xf, x, (int64_t)n * din);
     y = upload<int32_t>(A, b.y.data(), n);
     h = A.alloc<T>((int64_t)n * H);
+    A.cat = AC_LOGITS;
     z2 = A.alloc<T>((int64_t)n * C);
+    A.cat = AC_SCRATCH;
     dh = A.alloc<T>((int64_t)n * H);
+    A.cat = AC_ACT;
     loss_rows = A.alloc<double>(std::max(n, 1));
+    if (!dry) {
+      size_t wm = 0, wsd = 0;
+      plan_ws(wm, wsd);
+      L.ws->reserve(wm);
+    }
+  }
+  size_t arena_bytes(int c) const override { return A.bytes[c]; }
+  void plan_ws(size_t& main, size_t& side) const override {  // no side stream: every GEMM on main
+    size_t s2 = 0;
+    linear_ws<T>(L, H, din, n, main, s2);
+    linear_ws<T>(L, C, H, n, main, s2);
+    main = std::max(main, s2);
+    main = std::max(main, colreduce_ws_bytes<T>(n, H));
   }
   double tokens_global() const override { return n_glob; }
   int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, n, 1, L.stream); }
@@ -308,13 +364,15 @@ struct GptRunner : Runner<T> {
   Launch L;
   const LayoutPlan* plan;
   int nseq, Tn, N, D, H, hd, F, V, Ly, nseq_glob;
-  bool tied;
+  bool tied, ckpt;
   double eps;
   int32_t* tok;
   EmbedCSR csr;
   double* loss_rows;
   std::vector<T*> xs;  // L+1 residual streams
   struct Layer { T *mean1, *rstd1, *h1, *qkv, *P, *o, *x1, *mean2, *rstd2, *h2, *u, *gu; };
+  // block activations: one set per layer, or (activation checkpointing) two sets that the
+  // forward fills alternately and the backward refills by recomputing the block forward
   std::vector<Layer> ly;
   T *meanf, *rstdf, *xf, *logits;
   // backward scratch: two sets (the side stream lags by up to one layer) and three residual-
@@ -322,19 +380,26 @@ struct GptRunner : Runner<T> {
   struct Bwd { T *dx1, *dh1, *dh2, *dqkv, *du; } bb[2];
   T *dxs[3], *dhf, *dP, *do_;
   SideStream ss;
-  // deferred weight gradients (SLQ_DEFER_WGRAD=1, fp64 DMMA passes, no collective): every layer's
-  // output gradients stay in per-layer slabs and the four weight-gradient contractions run as one
-  // batched launch each over the layers after the data-gradient chain
+  // deferred weight gradients (SLQ_DEFER_WGRAD=1, fp64 DMMA passes, no collective, no
+  // checkpointing): every layer's output gradients stay in per-layer slabs and the four weight-
+  // gradient contractions run as one batched launch each over the layers after the data-gradient
+  // chain
   bool defer_ok = false;
   T *s_h1 = nullptr, *s_o = nullptr, *s_h2 = nullptr, *s_gu = nullptr;
   T *s_dx = nullptr, *s_du = nullptr, *s_dx1 = nullptr, *s_dqkv = nullptr;
 
-  GptRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
-    ss.init(L);
+  GptRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_, bool dry = false)
+      : L(L_), plan(&p) {
+    A.dry = dry;
+    if (!dry) ss.init(L);
     nseq = b.n_seq; nseq_glob = b.n_seq_global; Tn = d.seq_len; N = nseq * Tn; D = d.d_model; H = d.n_heads;
     hd = D / H; F = d.d_ff; V = d.vocab; Ly = d.n_layers; tied = d.tie_embeddings != 0; eps = d.norm_eps;
+    ckpt = d.act_ckpt != 0 && Ly > 0;
     tok = upload<int32_t>(A, b.tokens.data(), (int64_t)nseq * (Tn + 1));
-    {
+    if (dry) {
+      A.alloc<int32_t>(V + 1); A.alloc<int32_t>(N); A.alloc<int32_t>(V + 1);
+      A.alloc<int32_t>(embed_chunks_bound(N, V) + 1);
+    } else {
       std::vector<int32_t> off, pos, coff, cbeg;
       build_embed_csr(b.tokens, nseq, Tn, V, off, pos, coff, cbeg);
       csr.off = upload<int32_t>(A, off.data(), V + 1);
@@ -346,34 +411,62 @@ struct GptRunner : Runner<T> {
     loss_rows = A.alloc<double>(std::max(N, 1));
     for (int l = 0; l <= Ly; ++l) xs.push_back(A.alloc<T>((int64_t)N * D));
     const int64_t PP = (int64_t)nseq * H * Tn * Tn;
-    // the weight-gradient operands of all layers in slabs (constant stride for batched launches)
-    s_h1 = A.alloc<T>((int64_t)Ly * N * D); s_o = A.alloc<T>((int64_t)Ly * N * D);
-    s_h2 = A.alloc<T>((int64_t)Ly * N * D); s_gu = A.alloc<T>((int64_t)Ly * N * F);
-    for (int l = 0; l < Ly; ++l) {
+    const int nsets = ckpt ? std::min(Ly, 2) : Ly;
+    if (!ckpt) {  // the weight-gradient operands of all layers in slabs (constant stride for batched launches)
+      s_h1 = A.alloc<T>((int64_t)Ly * N * D); s_o = A.alloc<T>((int64_t)Ly * N * D);
+      s_h2 = A.alloc<T>((int64_t)Ly * N * D); s_gu = A.alloc<T>((int64_t)Ly * N * F);
+    }
+    for (int l = 0; l < nsets; ++l) {
       Layer a;
-      a.mean1 = A.alloc<T>(N); a.rstd1 = A.alloc<T>(N); a.h1 = s_h1 + (int64_t)l * N * D;
-      a.qkv = A.alloc<T>((int64_t)N * 3 * D); a.P = A.alloc<T>(PP); a.o = s_o + (int64_t)l * N * D;
+      a.mean1 = A.alloc<T>(N); a.rstd1 = A.alloc<T>(N);
+      a.qkv = A.alloc<T>((int64_t)N * 3 * D); a.P = A.alloc<T>(PP);
       a.x1 = A.alloc<T>((int64_t)N * D); a.mean2 = A.alloc<T>(N); a.rstd2 = A.alloc<T>(N);
-      a.h2 = s_h2 + (int64_t)l * N * D; a.u = A.alloc<T>((int64_t)N * F); a.gu = s_gu + (int64_t)l * N * F;
+      a.u = A.alloc<T>((int64_t)N * F);
+      if (ckpt) {
+        a.h1 = A.alloc<T>((int64_t)N * D); a.o = A.alloc<T>((int64_t)N * D);
+        a.h2 = A.alloc<T>((int64_t)N * D); a.gu = A.alloc<T>((int64_t)N * F);
+      } else if (!dry) {
+        a.h1 = s_h1 + (int64_t)l * N * D; a.o = s_o + (int64_t)l * N * D;
+        a.h2 = s_h2 + (int64_t)l * N * D; a.gu = s_gu + (int64_t)l * N * F;
+      }
       ly.push_back(a);
     }
-    {
+    if (!dry) {
       const char* e = getenv("SLQ_DEFER_WGRAD");
       const double mnk = (double)std::max(F, 3 * D) * D * N;  // largest per-layer weight gradient
-      defer_ok = sizeof(T) == 8 && e && atoi(e) == 1 && Ly > 1 && (L.gemm_mode != 2 || mnk < oz_min_mnk());
+      defer_ok = sizeof(T) == 8 && e && atoi(e) == 1 && Ly > 1 && !ckpt && (L.gemm_mode != 2 || mnk < L.oz_min_mnk);
       if (defer_ok) {
         s_dx = A.alloc<T>((int64_t)Ly * N * D); s_du = A.alloc<T>((int64_t)Ly * N * F);
         s_dx1 = A.alloc<T>((int64_t)Ly * N * D); s_dqkv = A.alloc<T>((int64_t)Ly * N * 3 * D);
       }
     }
     meanf = A.alloc<T>(N); rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D);
+    A.cat = AC_LOGITS;
     logits = A.alloc<T>((int64_t)N * V);
+    A.cat = AC_SCRATCH;
     for (int i = 0; i < 3; ++i) dxs[i] = A.alloc<T>((int64_t)N * D);
     for (Bwd& b2 : bb) {
       b2.dx1 = A.alloc<T>((int64_t)N * D); b2.dh1 = A.alloc<T>((int64_t)N * D); b2.dh2 = A.alloc<T>((int64_t)N * D);
       b2.dqkv = A.alloc<T>((int64_t)N * 3 * D); b2.du = A.alloc<T>((int64_t)N * F);
     }
     dhf = A.alloc<T>((int64_t)N * D); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * D);
+    if (!dry) {  // every workspace at its planned size up front (no growth inside a pass)
+      size_t wm = 0, wsd = 0;
+      plan_ws(wm, wsd);
+      L.ws->reserve(wm);
+      ss.ws.reserve(wsd);
+    }
+  }
+  size_t arena_bytes(int c) const override { return A.bytes[c]; }
+  void plan_ws(size_t& main, size_t& side) const override {
+    linear_ws<T>(L, 3 * D, D, N, main, side);
+    linear_ws<T>(L, D, D, N, main, side);
+    linear_ws<T>(L, F, D, N, main, side);
+    linear_ws<T>(L, D, F, N, main, side);
+    linear_ws<T>(L, V, D, N, main, side);
+    main = std::max(main, sizeof(T) * (size_t)embed_chunks_bound(N, V) * D);
+    side = std::max(side, colreduce_ws_bytes<T>(N, F));
+    side = std::max(side, colreduce_ws_bytes<T>(N, 3 * D));
   }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
   int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, N, Tn, L.stream); }
@@ -387,6 +480,22 @@ struct GptRunner : Runner<T> {
     g.nseq = nseq; g.Tn = Tn; g.Hq = H; g.Hkv = H; g.hd = hd; g.W = 3 * D; g.qo = 0; g.ko = D; g.vo = 2 * D; g.ldo = D;
     return g;
   }
+  // block activations of layer l (checkpointing: the set shared with layer l +- 2)
+  Layer& act(int l) { return ckpt ? ly[(Ly - 1 - l) & 1] : ly[l]; }
+
+  // block l's forward from xs[l] into act(l); `out` = also the last GEMM, xs[l + 1] = x1 + mproj(gu)
+  // (the backward's recomputation does not need it)
+  void block_fwd(const T* Pl, const UnitPlan& ub, int l, bool out) {
+    auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
+    Layer& a = act(l);
+    layernorm_fwd<T>(L, xs[l], w("ln1.g"), w("ln1.b"), a.h1, a.mean1, a.rstd1, N, D, eps);
+    linear_fwd<T>(L, a.h1, D, w("qkv.w"), 3 * D, D, N, a.qkv, 3 * D, w("qkv.b"));
+    attention_fwd<T>(L, geom(), a.qkv, a.P, a.o);
+    linear_fwd<T>(L, a.o, D, w("proj.w"), D, D, N, a.x1, D, w("proj.b"), xs[l], D);
+    layernorm_fwd<T>(L, a.x1, w("ln2.g"), w("ln2.b"), a.h2, a.mean2, a.rstd2, N, D, eps);
+    linear_fwd<T>(L, a.h2, D, w("fc.w"), F, D, N, a.gu, F, w("fc.b"), nullptr, 0, ACT_GELU, a.u, F);
+    if (out) linear_fwd<T>(L, a.gu, F, w("mproj.w"), D, F, N, xs[l + 1], D, w("mproj.b"), a.x1, D);
+  }
 
   void fwd_bwd(PassIO<T>& io, double* loss_sum) override {
     const UnitPlan& u0 = plan->units[0];
@@ -399,18 +508,9 @@ struct GptRunner : Runner<T> {
       embed_fwd<T>(L, tok, Tn + 1, nseq, Tn, P0 + u0.t("wte").offset, P0 + u0.t("wpe").offset, xs[0], D);
     }
     for (int l = 0; l < Ly; ++l) {
-      const UnitPlan& ub = plan->units[1 + l];
       const T* Pl = io.params(1 + l);
       io.prefetch(l + 2);
-      auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
-      Layer& a = ly[l];
-      layernorm_fwd<T>(L, xs[l], w("ln1.g"), w("ln1.b"), a.h1, a.mean1, a.rstd1, N, D, eps);
-      linear_fwd<T>(L, a.h1, D, w("qkv.w"), 3 * D, D, N, a.qkv, 3 * D, w("qkv.b"));
-      attention_fwd<T>(L, g, a.qkv, a.P, a.o);
-      linear_fwd<T>(L, a.o, D, w("proj.w"), D, D, N, a.x1, D, w("proj.b"), xs[l], D);
-      layernorm_fwd<T>(L, a.x1, w("ln2.g"), w("ln2.b"), a.h2, a.mean2, a.rstd2, N, D, eps);
-      linear_fwd<T>(L, a.h2, D, w("fc.w"), F, D, N, a.gu, F, w("fc.b"), nullptr, 0, ACT_GELU, a.u, F);
-      linear_fwd<T>(L, a.gu, F, w("mproj.w"), D, F, N, xs[l + 1], D, w("mproj.b"), a.x1, D);
+      block_fwd(Pl, plan->units[1 + l], l, true);
     }
     const T* Pf = io.params(Ly + 1);
     io.prefetch(tied ? 0 : Ly);
@@ -453,9 +553,11 @@ struct GptRunner : Runner<T> {
       T* Gl = io.grads(1 + l);
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
-      Layer& a = ly[l];
       const int set = (Ly - 1 - l) & 1;
       ss.wait_mark(set);  // the side stream is done with this set (and with dxs[cur + 1]) from two layers up
+      // checkpointing: the two top blocks' activations are still in their sets from the forward
+      if (ckpt && l < Ly - 2) block_fwd(Pl, ub, l, false);
+      Layer& a = act(l);
       T *dx1 = bb[set].dx1, *dh1 = bb[set].dh1, *dh2 = bb[set].dh2, *dqkv = bb[set].dqkv, *du = bb[set].du;
       T* dx = dxs[cur];
       T* dxn = dxs[(cur + 1) % 3];
@@ -523,7 +625,7 @@ struct LlamaRunner : Runner<T> {
   const LayoutPlan* plan;
   int nseq, Tn, N, D, Hq, Hkv, hd, F, V, Ly, nseq_glob;
   int64_t Wq;  // width of the packed q|k|v projection
-  bool tied;
+  bool tied, ckpt;
   double eps;
   int32_t* tok;
   EmbedCSR csr;
@@ -531,21 +633,27 @@ struct LlamaRunner : Runner<T> {
   T *cos_t, *sin_t;
   std::vector<T*> xs;
   struct Layer { T *rstd1, *h1, *qkv, *P, *o, *x1, *rstd2, *h2, *ab, *f; };
-  std::vector<Layer> ly;
+  std::vector<Layer> ly;  // one set per layer, or two (activation checkpointing; see GptRunner)
   T *rstdf, *xf, *logits;
   // backward scratch: two sets for what the side stream reads (lag 1), three residual gradients
   struct Bwd { T *dx1, *dh1, *dh2, *dqkv, *dab; } bb[2];
   T *dxs[3], *dhf, *dP, *do_, *df;
   SideStream ss;
 
-  LlamaRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_) : L(L_), plan(&p) {
-    ss.init(L);
+  LlamaRunner(const slq_model_desc& d, const LayoutPlan& p, const HostBatch& b, const Launch& L_, bool dry = false)
+      : L(L_), plan(&p) {
+    A.dry = dry;
+    if (!dry) ss.init(L);
     nseq = b.n_seq; nseq_glob = b.n_seq_global; Tn = d.seq_len; N = nseq * Tn; D = d.d_model; Hq = d.n_heads;
     Hkv = d.n_kv_heads; hd = D / Hq; F = d.d_ff; V = d.vocab; Ly = d.n_layers; tied = d.tie_embeddings != 0;
     eps = d.norm_eps;
+    ckpt = d.act_ckpt != 0 && Ly > 0;
     Wq = (int64_t)(Hq + 2 * Hkv) * hd;
     tok = upload<int32_t>(A, b.tokens.data(), (int64_t)nseq * (Tn + 1));
-    {
+    if (dry) {
+      A.alloc<int32_t>(V + 1); A.alloc<int32_t>(N); A.alloc<int32_t>(V + 1);
+      A.alloc<int32_t>(embed_chunks_bound(N, V) + 1);
+    } else {
       std::vector<int32_t> off, pos, coff, cbeg;
       build_embed_csr(b.tokens, nseq, Tn, V, off, pos, coff, cbeg);
       csr.off = upload<int32_t>(A, off.data(), V + 1);
@@ -570,7 +678,8 @@ struct LlamaRunner : Runner<T> {
     }
     for (int l = 0; l <= Ly; ++l) xs.push_back(A.alloc<T>((int64_t)N * D));
     const int64_t PP = (int64_t)nseq * Hq * Tn * Tn;
-    for (int l = 0; l < Ly; ++l) {
+    const int nsets = ckpt ? std::min(Ly, 2) : Ly;
+    for (int l = 0; l < nsets; ++l) {
       Layer a;
       a.rstd1 = A.alloc<T>(N); a.h1 = A.alloc<T>((int64_t)N * D); a.qkv = A.alloc<T>((int64_t)N * Wq);
       a.P = A.alloc<T>(PP); a.o = A.alloc<T>((int64_t)N * Hq * hd); a.x1 = A.alloc<T>((int64_t)N * D);
@@ -578,7 +687,10 @@ struct LlamaRunner : Runner<T> {
       a.f = A.alloc<T>((int64_t)N * F);
       ly.push_back(a);
     }
-    rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D); logits = A.alloc<T>((int64_t)N * V);
+    rstdf = A.alloc<T>(N); xf = A.alloc<T>((int64_t)N * D);
+    A.cat = AC_LOGITS;
+    logits = A.alloc<T>((int64_t)N * V);
+    A.cat = AC_SCRATCH;
     for (int i = 0; i < 3; ++i) dxs[i] = A.alloc<T>((int64_t)N * D);
     for (Bwd& b2 : bb) {
       b2.dx1 = A.alloc<T>((int64_t)N * D); b2.dh1 = A.alloc<T>((int64_t)N * D); b2.dh2 = A.alloc<T>((int64_t)N * D);
@@ -586,6 +698,22 @@ struct LlamaRunner : Runner<T> {
     }
     dhf = A.alloc<T>((int64_t)N * D); dP = A.alloc<T>(PP); do_ = A.alloc<T>((int64_t)N * Hq * hd);
     df = A.alloc<T>((int64_t)N * F);
+    if (!dry) {
+      size_t wm = 0, wsd = 0;
+      plan_ws(wm, wsd);
+      L.ws->reserve(wm);
+      ss.ws.reserve(wsd);
+    }
+  }
+  size_t arena_bytes(int c) const override { return A.bytes[c]; }
+  void plan_ws(size_t& main, size_t& side) const override {
+    linear_ws<T>(L, (int)Wq, D, N, main, side);
+    linear_ws<T>(L, D, Hq * hd, N, main, side);
+    linear_ws<T>(L, 2 * F, D, N, main, side);
+    linear_ws<T>(L, D, F, N, main, side);
+    linear_ws<T>(L, V, D, N, main, side);
+    main = std::max(main, sizeof(T) * (size_t)embed_chunks_bound(N, V) * D);
+    side = std::max(side, colreduce_ws_bytes<T>(N, D));
   }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
   int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, N, Tn, L.stream); }
@@ -600,6 +728,27 @@ struct LlamaRunner : Runner<T> {
     g.qo = 0; g.ko = (int64_t)Hq * hd; g.vo = (int64_t)(Hq + Hkv) * hd; g.ldo = (int64_t)Hq * hd;
     return g;
   }
+  Layer& act(int l) { return ckpt ? ly[(Ly - 1 - l) & 1] : ly[l]; }
+
+  // block l's forward from xs[l] into act(l); `out`: also xs[l + 1] = x1 + wd(swiglu(...))
+  void block_fwd(const T* Pl, const UnitPlan& ub, int l, bool out) {
+    auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
+    const AttnGeom<T> g = geom();
+    const int64_t HD = (int64_t)Hq * hd;
+    Layer& a = act(l);
+    rmsnorm_fwd<T>(L, xs[l], w("attn_norm"), a.h1, a.rstd1, N, D, eps);
+    // wq, wk, wv are contiguous rows of one [Wq x D] matrix in the canonical order
+    linear_fwd<T>(L, a.h1, D, w("wq"), (int)Wq, D, N, a.qkv, Wq, (const T*)nullptr);
+    rope<T>(L, a.qkv + g.qo, Wq, N, Tn, Hq, hd, cos_t, sin_t, false);
+    rope<T>(L, a.qkv + g.ko, Wq, N, Tn, Hkv, hd, cos_t, sin_t, false);
+    attention_fwd<T>(L, g, a.qkv, a.P, a.o);
+    linear_fwd<T>(L, a.o, HD, w("wo"), D, (int)HD, N, a.x1, D, (const T*)nullptr, xs[l], D);
+    rmsnorm_fwd<T>(L, a.x1, w("mlp_norm"), a.h2, a.rstd2, N, D, eps);
+    // wg, wu contiguous: ab = h2 [wg; wu]^T
+    linear_fwd<T>(L, a.h2, D, w("wg"), 2 * F, D, N, a.ab, 2 * F, (const T*)nullptr);
+    swiglu_fwd<T>(L, a.ab, a.f, N, F);
+    if (out) linear_fwd<T>(L, a.f, F, w("wd"), D, F, N, xs[l + 1], D, (const T*)nullptr, a.x1, D);
+  }
 
   void fwd_bwd(PassIO<T>& io, double* loss_sum) override {
     const UnitPlan& u0 = plan->units[0];
@@ -612,23 +761,9 @@ struct LlamaRunner : Runner<T> {
       embed_fwd<T>(L, tok, Tn + 1, nseq, Tn, P0 + u0.t("tok").offset, (const T*)nullptr, xs[0], D);
     }
     for (int l = 0; l < Ly; ++l) {
-      const UnitPlan& ub = plan->units[1 + l];
       const T* Pl = io.params(1 + l);
       io.prefetch(l + 2);
-      auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
-      Layer& a = ly[l];
-      rmsnorm_fwd<T>(L, xs[l], w("attn_norm"), a.h1, a.rstd1, N, D, eps);
-      // wq, wk, wv are contiguous rows of one [Wq x D] matrix in the canonical order
-      linear_fwd<T>(L, a.h1, D, w("wq"), (int)Wq, D, N, a.qkv, Wq, (const T*)nullptr);
-      rope<T>(L, a.qkv + g.qo, Wq, N, Tn, Hq, hd, cos_t, sin_t, false);
-      rope<T>(L, a.qkv + g.ko, Wq, N, Tn, Hkv, hd, cos_t, sin_t, false);
-      attention_fwd<T>(L, g, a.qkv, a.P, a.o);
-      linear_fwd<T>(L, a.o, HD, w("wo"), D, (int)HD, N, a.x1, D, (const T*)nullptr, xs[l], D);
-      rmsnorm_fwd<T>(L, a.x1, w("mlp_norm"), a.h2, a.rstd2, N, D, eps);
-      // wg, wu contiguous: ab = h2 [wg; wu]^T
-      linear_fwd<T>(L, a.h2, D, w("wg"), 2 * F, D, N, a.ab, 2 * F, (const T*)nullptr);
-      swiglu_fwd<T>(L, a.ab, a.f, N, F);
-      linear_fwd<T>(L, a.f, F, w("wd"), D, F, N, xs[l + 1], D, (const T*)nullptr, a.x1, D);
+      block_fwd(Pl, plan->units[1 + l], l, true);
     }
     const T* Pf = io.params(Ly + 1);
     io.prefetch(tied ? 0 : Ly);
@@ -658,9 +793,10 @@ struct LlamaRunner : Runner<T> {
       T* Gl = io.grads(1 + l);
       auto w = [&](const char* n) { return Pl + ub.t(n).offset; };
       auto gw = [&](const char* n) { return Gl + ub.t(n).offset; };
-      Layer& a = ly[l];
       const int set = (Ly - 1 - l) & 1;
       ss.wait_mark(set);  // side stream done with this scratch set (two layers up)
+      if (ckpt && l < Ly - 2) block_fwd(Pl, ub, l, false);  // recompute (checkpointing)
+      Layer& a = act(l);
       T *dx1 = bb[set].dx1, *dh1 = bb[set].dh1, *dh2 = bb[set].dh2, *dqkv = bb[set].dqkv, *dab = bb[set].dab;
       T* dx = dxs[cur];
       T* dxn = dxs[(cur + 1) % 3];
@@ -703,15 +839,15 @@ struct LlamaRunner : Runner<T> {
 
 template <class T>
 std::unique_ptr<Runner<T>> make_runner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
-                                       const Launch& L) {
-  if (d.arch == SLQ_ARCH_MLP) return std::unique_ptr<Runner<T>>(new MlpRunner<T>(d, plan, b, L));
-  if (d.arch == SLQ_ARCH_GPT) return std::unique_ptr<Runner<T>>(new GptRunner<T>(d, plan, b, L));
-  return std::unique_ptr<Runner<T>>(new LlamaRunner<T>(d, plan, b, L));
+                                       const Launch& L, bool dry) {
+  if (d.arch == SLQ_ARCH_MLP) return std::unique_ptr<Runner<T>>(new MlpRunner<T>(d, plan, b, L, dry));
+  if (d.arch == SLQ_ARCH_GPT) return std::unique_ptr<Runner<T>>(new GptRunner<T>(d, plan, b, L, dry));
+  return std::unique_ptr<Runner<T>>(new LlamaRunner<T>(d, plan, b, L, dry));
 }
 
 template std::unique_ptr<Runner<double>> make_runner<double>(const slq_model_desc&, const LayoutPlan&,
-                                                             const HostBatch&, const Launch&);
+                                                             const HostBatch&, const Launch&, bool);
 template std::unique_ptr<Runner<float>> make_runner<float>(const slq_model_desc&, const LayoutPlan&,
-                                                           const HostBatch&, const Launch&);
+                                                           const HostBatch&, const Launch&, bool);
 
 }  // namespace slq

@@ -53,15 +53,22 @@ struct Runner {
   virtual void fwd_bwd_pair(PassIO<T>& mean, PassIO<T>& diff, double* loss_sum) {
     throw Error(SLQ_EUNSUPPORTED, "paired evaluation not available for this runner");
   }
+  // device bytes of the runner's own buffers by memory-plan category (0 activations + data, 1 logits,
+  // 2 backward scratch) -- exact for a real runner, the plan for a dry one
+  virtual size_t arena_bytes(int) const { return 0; }
+  // the largest GEMM / reduction workspace its pass asks for on the data-gradient lane (main) and
+  // on the side stream (side); reserved up front by real runners
+  virtual void plan_ws(size_t& main, size_t& side) const {}
 };
 
 // first group of `per` consecutive rows of dev[n] (device doubles) holding a non-finite value,
 // -1 if none (synchronous device -> host copy; error paths only)
 int first_nonfinite_group(const double* dev, int n, int per, cudaStream_t s);
 
+// dry: allocate nothing, launch nothing -- only count the bytes (slq_plan_memory)
 template <class T>
 std::unique_ptr<Runner<T>> make_runner(const slq_model_desc& d, const LayoutPlan& plan, const HostBatch& b,
-                                       const Launch& L);
+                                       const Launch& L, bool dry = false);
 // paired-evaluation runner (GPT); nullptr if the arch has none yet
 std::unique_ptr<Runner<float>> make_paired_runner(const slq_model_desc& d, const LayoutPlan& plan,
                                                   const HostBatch& b, const Launch& L);

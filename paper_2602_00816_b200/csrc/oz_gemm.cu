@@ -90,6 +90,13 @@ __device__ __forceinline__ double i2d(uint32_t x) {
 // 2^e as a double (e within the normal range), built from the exponent bits
 __device__ __forceinline__ double exp2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
 
+// exponent marker of a row / column holding a NaN or an infinity: the slicing cannot represent it,
+// so the epilogue scales that output row / column by NaN (non-finite inputs give non-finite
+// outputs, as in the DMMA path; the loss then fails the SLQ_ENUMERIC check).  It is the
+// largest int, so it survives the max over partial exponents.
+constexpr int kExNaN = 0x7fffffff;
+__device__ __forceinline__ double scale_of(int e) { return e == kExNaN ? __longlong_as_double(0x7ff8000000000000ll) : exp2i(e); }
+
 // Persistent kernel: grid <= #SMs, CTA c processes work units c, c + grid, ... (unit = output
 // tile x K split).  The TMA producer runs ahead across unit boundaries (ring of STAGES k-tiles);
 // the epilogue drains the S accumulators from TMEM into registers, releases TMEM (the next unit's
@@ -250,8 +257,8 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
       // scales first (their global-load latency overlaps the wait for the accumulators):
       // lane l holds 2^f for column n0 + c0 + l and 2^e for row m0 + lg + l
       const int n_l = n0 + c0 + lane, row_l = m0 + lg + lane;
-      const double sc_l = n_l < p.N ? exp2i(o.eb[n_l]) : 0.0;
-      const double sr = (nloc > 0 && row_l < p.M) ? exp2i(o.ea[row_l]) : 0.0;
+      const double sc_l = n_l < p.N ? scale_of(o.eb[n_l]) : 0.0;
+      const double sr = (nloc > 0 && row_l < p.M) ? scale_of(o.ea[row_l]) : 0.0;
       if (jb == 0) {
         mbar_wait(tmem_full, tl & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
@@ -493,12 +500,12 @@ __global__ void __launch_bounds__(320, 1)
       int m0, n0, sp, kt0, nloc;
       decode(w, m0, n0, sp, kt0, nloc);
       const int row_l = m0 + lg + lane;
-      const double sr = (nloc > 0 && row_l < p.M) ? exp2i(o.ea[row_l]) : 0.0;
+      const double sr = (nloc > 0 && row_l < p.M) ? scale_of(o.ea[row_l]) : 0.0;
       double sc_l[2];
 #pragma unroll
       for (int jb = 0; jb < 2; ++jb) {
         const int n_l = n0 + ch + 32 * jb + lane;
-        sc_l[jb] = n_l < p.N ? exp2i(o.eb[n_l]) : 0.0;
+        sc_l[jb] = n_l < p.N ? scale_of(o.eb[n_l]) : 0.0;
       }
       double v[64];
 #pragma unroll
@@ -608,7 +615,11 @@ __device__ __forceinline__ void digits(double x, int e, int8_t* d) {
   }
 }
 
-__device__ __forceinline__ int exp_of(double mx) {
+// !(|x| <= DBL_MAX): NaN or +-inf
+__device__ __forceinline__ bool nonfinite(double x) { return !(fabs(x) <= 1.7976931348623157e308); }
+
+__device__ __forceinline__ int exp_of(double mx, bool nf = false) {
+  if (nf) return kExNaN;
   if (!(mx > 0.0)) return 0;
   int e;
   frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)  ->  mx < 2^e
@@ -651,17 +662,26 @@ __global__ void __launch_bounds__(256) k_oz_colexp2(const __grid_constant__ Slic
   const int r = r0 + tx;
   const int k0 = kb * kColK, k1 = min(jb.K, k0 + kColK);
   double mx = 0.0;
+  bool nf = false;
   if (r < jb.rows) {
 #pragma unroll 4
-    for (int k = k0 + ty; k < k1; k += 8) mx = fmax(mx, fabs(jb.X[(int64_t)k * jb.ld + r]));
+    for (int k = k0 + ty; k < k1; k += 8) {
+      const double x = jb.X[(int64_t)k * jb.ld + r];
+      mx = fmax(mx, fabs(x));
+      nf |= nonfinite(x);
+    }
   }
-  red[ty][tx] = mx;
+  red[ty][tx] = nf ? __longlong_as_double(0x7ff8000000000000ll) : mx;
   __syncthreads();
   if (ty == 0 && r < jb.rows) {
-    double m = red[0][tx];
+    double m = 0.0;
+    bool bad = false;
 #pragma unroll
-    for (int i = 1; i < 8; ++i) m = fmax(m, red[i][tx]);
-    jb.xp[(int64_t)kb * jb.rows + r] = m > 0.0 ? exp_of(m) : kExNone;
+    for (int i = 0; i < 8; ++i) {
+      bad |= red[i][tx] != red[i][tx];
+      m = fmax(m, red[i][tx]);
+    }
+    jb.xp[(int64_t)kb * jb.rows + r] = bad ? kExNaN : (m > 0.0 ? exp_of(m) : kExNone);
   }
 }
 
@@ -679,17 +699,22 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
     const double* xr = jb.X + (int64_t)row * jb.ld;
     constexpr int V = 32;  // values per lane per sweep (1024-wide sweeps)
     double mx = 0.0;
+    bool nf = false;
     for (int k0 = 0; k0 < jb.K; k0 += 32 * V) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const int k = k0 + i * 32 + lane;
-        if (k < jb.K) mx = fmax(mx, fabs(xr[k]));
+        if (k < jb.K) {
+          mx = fmax(mx, fabs(xr[k]));
+          nf |= nonfinite(xr[k]);
+        }
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int e = exp_of(mx);
-    if (lane == 0) jb.ex[row] = e;
+    nf = __any_sync(0xffffffffu, nf);
+    if (lane == 0) jb.ex[row] = exp_of(mx, nf);
+    const int e = nf ? 0 : exp_of(mx);  // (digits of a non-finite row are never used)
     // 16-byte loads when the row base is 16-byte aligned (even pitch, aligned base)
     const bool v2 = (jb.ld % 2) == 0 && ((uintptr_t)jb.X & 15) == 0;
     for (int k4 = lane * 4; k4 < jb.Kp; k4 += 128) {
@@ -726,8 +751,8 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
       const int nkb = (jb.K + kColK - 1) / kColK;
       for (int kb = 0; kb < nkb; ++kb) e = max(e, jb.xp[(int64_t)kb * jb.rows + r]);
     }
-    es[threadIdx.x] = e == kExNone ? 0 : e;
-    if (kblk == 0 && r < jb.rows) jb.ex[r] = es[threadIdx.x];
+    if (kblk == 0 && r < jb.rows) jb.ex[r] = e == kExNone ? 0 : e;
+    es[threadIdx.x] = (e == kExNone || e == kExNaN) ? 0 : e;  // (digits of a non-finite row are never used)
   }
   const int wr = threadIdx.x / 8, kq = threadIdx.x % 8;
   const int kb0 = kblk * 128, kb1 = min(jb.Kp, kb0 + 128);
@@ -771,6 +796,16 @@ static CUtensorMap make_map_i8(const void* base, int64_t rows, int64_t cols, int
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// split-K: one CTA per SM (the stage ring fills the shared memory), so fill the 148 SMs with
+// tiles x splits <= 148; every split's K range keeps |acc| <= S * Ksplit * 127^2 < 2^31
+static void plan_splits(int S, int tiles, int nk, int KT, int& splits, int& ktps) {
+  const int kt_cap = (int)std::max<int64_t>(1, ((int64_t)2147483647 / ((int64_t)S * 127 * 127)) / KT);
+  splits = tiles < 148 ? std::max(1, std::min(148 / tiles, nk / 2)) : 1;
+  splits = std::max<int>(splits, (int)ceil_div(nk, kt_cap));
+  ktps = (int)ceil_div(nk, splits);
+  splits = (int)ceil_div(nk, ktps);
+}
+
 // W: the wide two-phase kernel (S = 7, BN = 128, 32-byte k-tiles)
 template <int S, int BN, bool W = false, int KTN = BK, int NI = 1>
 void run(const Launch& L, const GemmArgs<double>& a) {
@@ -787,14 +822,9 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   const int M = a.M, N = a.N, K = a.K;
   const int Kp = (int)ceil_div(K, 16) * 16;
   const int nk = (int)ceil_div(K, KT);
-  // split-K: one CTA per SM (the stage ring fills the shared memory), so fill the 148 SMs with
-  // tiles x splits <= 148; every split's K range keeps |acc| <= S * Ksplit * 127^2 < 2^31
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
-  const int kt_cap = (int)std::max<int64_t>(1, ((int64_t)2147483647 / ((int64_t)S * 127 * 127)) / KT);
-  int splits = tiles < 148 ? std::max(1, std::min(148 / tiles, nk / 2)) : 1;
-  splits = std::max<int>(splits, (int)ceil_div(nk, kt_cap));
-  const int ktps = (int)ceil_div(nk, splits);
-  splits = (int)ceil_div(nk, ktps);
+  int splits, ktps;
+  plan_splits(S, tiles, nk, KT, splits, ktps);
   const size_t a_bytes = align256((size_t)S * M * Kp), b_bytes = align256((size_t)S * N * Kp);
   const size_t e_bytes = align256(4 * (size_t)(M + N));
   const int nkb = (int)ceil_div(K, kColK);
@@ -870,23 +900,17 @@ void run(const Launch& L, const GemmArgs<double>& a) {
 
 }  // namespace oz
 
-int oz_slices() {
-  static int s = [] {
-    const char* e = getenv("SLQ_OZ_SLICES");
-    const int v = e ? atoi(e) : 7;
-    return (v >= 4 && v <= 7) ? v : 7;
-  }();
-  return s;
-}
-
-double oz_min_mnk() {
-  static double v = [] {
-    // measured on B200 (c2 step, tools/exp_oz.sh): the int8 path wins on the 2e9-MNK head GEMMs and
-    // breaks even below ~1e9, where slicing launches and the fp64 epilogue dominate
-    const char* e = getenv("SLQ_OZ_MIN_MNK");
-    return e ? atof(e) : 1e9;
-  }();
-  return v;
+// workspace of the production configuration (BN = 64, 64-byte k-tiles; the diagnostic wide / 32-byte
+// variants size their own)
+size_t oz_ws_bytes(int M, int N, int K, int S) {
+  using namespace oz;
+  const int Kp = (int)ceil_div(K, 16) * 16, nk = (int)ceil_div(K, BK);
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, 64));
+  int splits, ktps;
+  plan_splits(S, tiles, nk, BK, splits, ktps);
+  const int nkb = (int)ceil_div(K, kColK);
+  return align256((size_t)S * M * Kp) + align256((size_t)S * N * Kp) + align256(4 * (size_t)(M + N)) +
+         align256(4 * (size_t)(M + N) * nkb) + (splits > 1 ? align256(8 * (size_t)M * N * splits) : 0);
 }
 
 void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {

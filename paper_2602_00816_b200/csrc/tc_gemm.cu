@@ -389,6 +389,22 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace tc
 
+size_t tc_ws_bytes(int M, int N, int K, int terms) {
+  using namespace tc;
+  const int64_t ldk = (K + 7) / 8 * 8;
+  const size_t a_bytes = align256(2 * (size_t)M * ldk), b_bytes = align256(2 * (size_t)N * ldk);
+  const int npairs = terms == 1 ? 1 : 6, nk = (K + BK - 1) / BK;
+  const int64_t t128 = ceil_div(M, BM) * ceil_div(N, 128);
+  const int bn = t128 >= 148 ? 128 : 64;
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, bn));
+  const int total = npairs * nk;
+  int splits = 1;
+  if (tiles < 148) splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * 148, tiles), total / 4));
+  const int tps = (int)ceil_div(total, splits);
+  splits = (int)ceil_div(total, tps);
+  return terms * (a_bytes + b_bytes) + (splits > 1 ? align256(4 * (size_t)M * N * splits) : 0);
+}
+
 void gemm_tc_bf16x3(const Launch& L, const GemmArgs<float>& a, int terms) {
   using namespace tc;
   SLQ_CHECK_ARG(a.batch == 1 && a.M > 0 && a.N > 0 && a.K > 0, "tc gemm: batch 1, non-empty");

@@ -3,6 +3,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 from typing import Optional, Tuple
 
 import numpy as np
@@ -33,7 +34,8 @@ class ModelDescC(ctypes.Structure):
                 ("pass_numerics", ctypes.c_int32), ("reorth", ctypes.c_int32),
                 ("max_steps", ctypes.c_int32), ("eps_default", ctypes.c_double),
                 ("perturb", ctypes.c_int32), ("reorth_window", ctypes.c_int32),
-                ("basis_dtype", ctypes.c_int32)]
+                ("basis_dtype", ctypes.c_int32), ("oz_min_mnk", ctypes.c_double),
+                ("oz_slices", ctypes.c_int32), ("act_ckpt", ctypes.c_int32)]
 
 
 class BatchC(ctypes.Structure):
@@ -45,7 +47,13 @@ class BatchC(ctypes.Structure):
 
 class WorldC(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p),
+                ("comm_backend", ctypes.c_int32)]
+
+
+COMM = {"nccl": 0, "loopback": 1}
+MEM_NAMES = ["theta", "points", "grads", "lanczos", "fsdp", "activations", "logits", "scratch", "workspace",
+             "total"]
 
 
 _lib = None
@@ -94,6 +102,7 @@ def lib() -> ctypes.CDLL:
         "slq_nonfinite_seq": (I32, [P, P]),
         "slq_cg": (I32, [P, P, P, D, I32, D, P, P]),
         "slq_blockdiag": (I32, [P, U64, P, P]),
+        "slq_plan_memory": (I32, [ctypes.POINTER(ModelDescC), I32, I32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -111,7 +120,7 @@ def _check(st: int, ctx=None) -> None:
 
 def make_desc(cfg, pass_numerics: str = "fp64", reorth: Optional[str] = None, max_steps: Optional[int] = None,
               eps: Optional[float] = None, perturb: str = "exact", window: int = 0,
-              basis: str = "fp32") -> ModelDescC:
+              basis: str = "fp32", oz_min_mnk: float = 0.0, oz_slices: int = 0, act_ckpt: bool = False) -> ModelDescC:
     """slq_model_desc from a slq_inputs.ModelDesc-like object."""
     d = ModelDescC()
     d.arch = cfg.arch
@@ -129,7 +138,17 @@ def make_desc(cfg, pass_numerics: str = "fp64", reorth: Optional[str] = None, ma
     d.perturb = PERTURB[perturb]
     d.reorth_window = int(window)
     d.basis_dtype = BASIS[basis]
+    d.oz_min_mnk = float(oz_min_mnk)
+    d.oz_slices = int(oz_slices)
+    d.act_ckpt = int(bool(act_ckpt))
     return d
+
+
+def plan_memory(desc: ModelDescC, world_size: int, n_local: int) -> dict:
+    """Per-rank device-memory plan in bytes by category (slq_plan_memory; host only)."""
+    out = np.zeros(len(MEM_NAMES), dtype=np.int64)
+    _check(lib().slq_plan_memory(ctypes.byref(desc), int(world_size), int(n_local), out.ctypes.data))
+    return dict(zip(MEM_NAMES, (int(x) for x in out)))
 
 
 def plan_layout(desc: ModelDescC, world_size: int) -> dict:
@@ -231,6 +250,17 @@ def ghost_clusters(nodes, tol: float) -> Tuple[np.ndarray, int, float]:
     return ids, ng.value, ms.value
 
 
+def _torch_fence() -> None:
+    """The library orders its calls after the legacy default stream (slq.h, slq_world.cuda_stream);
+    if torch is writing shards on another current stream, wait for that stream first."""
+    t = sys.modules.get("torch")
+    if t is None or not t.cuda.is_available() or not t.cuda.is_initialized():
+        return
+    s = t.cuda.current_stream()
+    if s.cuda_stream != 0:
+        s.synchronize()
+
+
 def _ptr(x) -> int:
     """Raw pointer of a torch tensor (device or host) or numpy array."""
     if isinstance(x, np.ndarray):
@@ -246,10 +276,12 @@ class SlqContext:
     def __init__(self, cfg, theta0: np.ndarray, batch, *, n_global: Optional[int] = None, rank: int = 0,
                  world_size: int = 1, device: int = 0, stream: Optional[int] = None, unique_id: Optional[bytes] = None,
                  pass_numerics: str = "fp64", reorth: Optional[str] = None, max_steps: Optional[int] = None,
-                 eps: Optional[float] = None, perturb: str = "exact", window: int = 0, basis: str = "fp32"):
+                 eps: Optional[float] = None, perturb: str = "exact", window: int = 0, basis: str = "fp32",
+                 oz_min_mnk: float = 0.0, oz_slices: int = 0, act_ckpt: bool = False, comm: str = "nccl"):
         L = lib()
         self._keep = []
-        self.desc = make_desc(cfg, pass_numerics, reorth, max_steps, eps, perturb, window, basis)
+        self.desc = make_desc(cfg, pass_numerics, reorth, max_steps, eps, perturb, window, basis, oz_min_mnk,
+                              oz_slices, act_ckpt)
         th = np.ascontiguousarray(theta0, dtype=np.float32)
         b = BatchC()
         b.params_host = th.ctypes.data
@@ -276,6 +308,7 @@ class SlqContext:
             uid = ctypes.create_string_buffer(unique_id, 128)
             w.nccl_unique_id = ctypes.cast(uid, ctypes.c_void_p)
         w.cuda_stream = stream
+        w.comm_backend = COMM[comm]
         h = ctypes.c_void_p()
         _check(L.slq_init(ctypes.byref(self.desc), ctypes.byref(b), ctypes.byref(w), ctypes.byref(h)))
         self._h = h
@@ -319,10 +352,12 @@ class SlqContext:
 
     # -- the path
     def hvp(self, v, out, eps: float) -> None:
+        _torch_fence()
         _check(lib().slq_hvp(self._h, _ptr(v), _ptr(out), float(eps)), self._h)
 
     def grad(self, g=None) -> float:
         loss = ctypes.c_double()
+        _torch_fence()
         _check(lib().slq_grad(self._h, _ptr(g) if g is not None else None, ctypes.byref(loss)), self._h)
         return loss.value
 
@@ -349,6 +384,7 @@ class SlqContext:
 
     def cg(self, b, x, damping: float, max_iter: int, tol: float = 0.0):
         it, rr = ctypes.c_int32(), ctypes.c_double()
+        _torch_fence()
         _check(lib().slq_cg(self._h, _ptr(b), _ptr(x), float(damping), int(max_iter), float(tol), ctypes.byref(it),
                             ctypes.byref(rr)), self._h)
         return it.value, rr.value
@@ -360,6 +396,7 @@ class SlqContext:
         return rel, cos
 
     def probe(self, seed: int, q) -> None:
+        _torch_fence()
         _check(lib().slq_probe(self._h, ctypes.c_uint64(seed), _ptr(q)), self._h)
 
     # -- measurement

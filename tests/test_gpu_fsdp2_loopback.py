@@ -1,0 +1,121 @@
+"""libslq's FSDP engine at world_size 2 on ONE GPU (SLQ_COMM_LOOPBACK, slq.h): two ranks are two
+contexts of this process, one host thread each, whose collectives are host-synchronous (stream
+drain, host barrier, device copies / fixed rank-order sums) -- so no kernel ever waits on another
+rank's kernel.  This drives the real FsdpIO (rank chunks of every unit, padded shards, per-unit
+all-gather before forward and backward, reduce-scatter after backward, ping-pong buffers, the
+per-pass split communicators of the concurrent theta+ / theta- passes, scalar all-reduces)
+(SURVEY §8(e)).
+
+Checks: R = 2 equals R = 1 on the same global batch (sequence j is a pure function of (seed, j),
+R22) within reduction-order round-off; the shards reassemble to the R = 1 vectors; the collective
+audit per HVP: 2U reduce-scatters and <= 4U all-gathers (U = FSDP units; resident units are not
+re-gathered), and per full-reorth Lanczos step at most 3 scalar all-reduces ("(2+r)")."""
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import slq_inputs as si
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_00816_b200 import build
+    build.build()
+
+
+from paper_2602_00816_b200 import slq  # noqa: E402
+
+M = 8
+
+
+def _rank_run(cfg, th, numerics, rank, R, key, out, v_full):
+    try:
+        if cfg.arch == si.ARCH_MLP:
+            x, y = si.mlp_data(cfg)
+            sl = si.rank_slice(cfg.n_rows, rank, R)
+            batch, n_glob = (x[sl], y[sl]), cfg.n_rows
+        else:
+            tok = si.tokens(cfg)
+            batch, n_glob = tok[si.rank_slice(cfg.n_seq, rank, R)], cfg.n_seq
+        with slq.SlqContext(cfg, th, batch, n_global=n_glob, rank=rank, world_size=R, unique_id=key,
+                            comm="loopback" if R > 1 else "nccl", pass_numerics=numerics, reorth="full",
+                            max_steps=M) as c:
+            lay = c.layout()
+            v = torch.from_numpy(slq.shard_of(v_full, lay, rank, R)).cuda()
+            g = torch.empty_like(v)
+            loss = c.grad(g)
+            cc0 = c.collective_counts()
+            h = torch.empty_like(v)
+            c.hvp(v, h, cfg.eps)
+            cc1 = c.collective_counts()
+            a, b = c.lanczos(cfg.probe_seed0, M)
+            cc2 = c.collective_counts()
+            out[rank] = dict(loss=loss, g=g.cpu().numpy(), h=h.cpu().numpy(), a=a, b=b, lay=lay,
+                             cc=(cc0, cc1, cc2), units=len(lay["units"]))
+    except Exception as e:  # reported by the main thread
+        out[rank] = e
+
+
+def _world(cfg, numerics, R):
+    th = si.init_params(cfg)
+    v_full = si.random_vector(th.size, 5)
+    key = (b"slq-loopback-test-%s-%s-%d" % (cfg.name.encode(), numerics.encode(), R)).ljust(128, b"\0")
+    out = [None] * R
+    ts = [threading.Thread(target=_rank_run, args=(cfg, th, numerics, r, R, key, out, v_full)) for r in range(R)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for r in out:
+        if isinstance(r, Exception):
+            raise r
+    return out
+
+
+@pytest.mark.parametrize("name,numerics", [("gpt_tiny", "fp64"), ("gpt_tiny_tied", "fp64"), ("llama_tiny", "fp64"),
+                                           ("mlp_tiny", "fp64"), ("c2", "fp64_oz"), ("llama_tiny", "bf16x3")])
+def test_two_ranks_equal_one(name, numerics):
+    os.environ.setdefault("SLQ_TIMEOUT_S", "600")
+    cfg = si.CONFIGS[name]
+    r1 = _world(cfg, numerics, 1)[0]
+    r2 = _world(cfg, numerics, 2)
+    lay1 = r1["lay"]
+    g2 = slq.unshard([r["g"] for r in r2], r2[0]["lay"])
+    h2 = slq.unshard([r["h"] for r in r2], r2[0]["lay"])
+    g1 = slq.unshard([r1["g"]], lay1)
+    h1 = slq.unshard([r1["h"]], lay1)
+    eg = np.linalg.norm(g2 - g1) / np.linalg.norm(g1)
+    eh = np.linalg.norm(h2.astype(np.float64) - h1) / np.linalg.norm(h1)
+    ea = np.max(np.abs(r2[0]["a"] - r1["a"]) / np.abs(r1["a"]).max())
+    eb = np.max(np.abs(r2[0]["b"] - r1["b"]) / np.abs(r1["b"]))
+    U = r2[0]["units"]
+    cc0, cc1, cc2 = r2[0]["cc"]
+    ag_h, rs_h = cc1["allgather"] - cc0["allgather"], cc1["reduce_scatter"] - cc0["reduce_scatter"]
+    ar_l = cc2["allreduce"] - cc1["allreduce"]
+    ag_l = cc2["allgather"] - cc1["allgather"]
+    print(f"{name} [{numerics}] R=2 vs R=1: loss {r2[0]['loss']:.15f}/{r1['loss']:.15f} grad {eg:.1e} "
+          f"HVP {eh:.1e} alpha {ea:.1e} beta {eb:.1e}; U={U}: per HVP {ag_h} all-gathers, {rs_h} reduce-scatters; "
+          f"Lanczos {M} steps: {ar_l} all-reduces, {ag_l} all-gathers")
+    # both ranks agree on every scalar (all-reduced), bit for bit
+    assert r2[0]["loss"] == r2[1]["loss"]
+    assert np.array_equal(r2[0]["a"], r2[1]["a"]) and np.array_equal(r2[0]["b"], r2[1]["b"])
+    # fp64 passes: the R = 2 reduce-scatter sums two rank partials (round-off ~1e-16 of g), which the
+    # FD difference amplifies by ||g|| / (2 eta ||Hv||); fp32 (BF16X3) passes: the same at fp32
+    # round-off, i.e. Theorem 1's fp32 floor -- only agreement at that level is asserted
+    f32 = numerics == "bf16x3"
+    assert abs(r2[0]["loss"] - r1["loss"]) <= (1e-6 if f32 else 1e-13) * abs(r1["loss"])
+    assert eg <= (1e-5 if f32 else 1e-12)
+    tol = 5e-2 if f32 else 1e-7
+    assert eh <= tol and ea <= tol and eb <= tol
+    # collective audit
+    assert rs_h == 2 * U
+    assert 2 * U <= ag_h <= 4 * U
+    assert ag_l == M * ag_h
+    assert ar_l <= 3 * M + 1

@@ -1,17 +1,15 @@
 """The int8 Ozaki fp64 GEMM on tcgen05 (SLQ_PASS_FP64_OZ; oz_gemm.cu) against the DMMA fp64 GEMM,
 and the FP64_OZ pass mode against the fp64 oracle at the north star's fp32 gates (HVP rel-L2 <= 1e-4,
-alpha/beta <= 1e-5 over the first 32 Lanczos steps)."""
-import os
-
+alpha/beta <= 1e-5 over the first 32 Lanczos steps).  Two routes, each a per-context descriptor
+field (slq_model_desc.oz_min_mnk): "int8" = every dense GEMM on the int8 path (oz_min_mnk = 1), and
+"hybrid" = the production default the bench times (GEMMs below 1e9 M N K on DMMA)."""
 import numpy as np
 import pytest
 
 import slq_inputs as si
 from oracle import fdhvp, lanczos as OL, models, probe
 
-# every dense GEMM through the int8 path (the production default keeps GEMMs below 1e9 M N K on
-# DMMA); read by the library on first use, so set before any FP64_OZ context exists
-os.environ["SLQ_OZ_MIN_MNK"] = "0"
+ROUTES = {"int8": 1.0, "hybrid": 0.0}
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -46,12 +44,13 @@ def _batch(cfg):
     return si.mlp_data(cfg) if cfg.arch == si.ARCH_MLP else si.tokens(cfg)
 
 
+@pytest.mark.parametrize("route", ["int8", "hybrid"])
 @pytest.mark.parametrize("name", ["mlp_tiny", "c1", "gpt_tiny", "gpt_tiny_tied", "llama_tiny", "c2"])
-def test_fp64_oz_grad_and_hvp(name):
+def test_fp64_oz_grad_and_hvp(name, route):
     cfg = si.CONFIGS[name]
     th = si.init_params(cfg)
     v = si.random_vector(th.size, 5)
-    with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="fp64_oz") as c:
+    with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="fp64_oz", oz_min_mnk=ROUTES[route]) as c:
         lay = c.layout()
         g = torch.empty(c.P_loc, dtype=torch.float32, device="cuda")
         loss = c.grad(g)
@@ -64,16 +63,18 @@ def test_fp64_oz_grad_and_hvp(name):
     ref = fdhvp.hvp(fdhvp.make_grad_fn(cfg, _batch(cfg)), th, v, cfg.eps, "exact")
     eg = np.linalg.norm(gf - g_ref) / np.linalg.norm(g_ref)
     eh = np.linalg.norm(hv - ref) / np.linalg.norm(ref)
-    print(f"{name} [fp64_oz]: loss {abs(loss - l_ref) / abs(l_ref):.1e} grad {eg:.2e} HVP {eh:.2e}")
+    print(f"{name} [fp64_oz {route}]: loss {abs(loss - l_ref) / abs(l_ref):.1e} grad {eg:.2e} HVP {eh:.2e}")
     assert abs(loss - l_ref) <= 1e-9 * abs(l_ref)
     assert eg <= 1e-7 and eh <= 1e-4
 
 
-@pytest.mark.parametrize("name,m", [("gpt_tiny", 16), ("llama_tiny", 16), ("c1", 32), ("c2", 32)])
-def test_fp64_oz_lanczos_fp32_gates(name, m):
+@pytest.mark.parametrize("name,m,route", [("gpt_tiny", 16, "int8"), ("llama_tiny", 16, "int8"), ("c1", 32, "int8"),
+                                          ("c2", 32, "int8"), ("c2", 32, "hybrid")])
+def test_fp64_oz_lanczos_fp32_gates(name, m, route):
     cfg = si.CONFIGS[name]
     th = si.init_params(cfg)
-    with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="fp64_oz", reorth="full", max_steps=m) as c:
+    with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="fp64_oz", reorth="full", max_steps=m,
+                        oz_min_mnk=ROUTES[route]) as c:
         a, b = c.lanczos(cfg.probe_seed0, m)
     g = fdhvp.make_grad_fn(cfg, _batch(cfg))
     r = OL.lanczos(lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact"),
@@ -81,5 +82,25 @@ def test_fp64_oz_lanczos_fp32_gates(name, m):
     scale = np.abs(r.alpha).max()
     ea = np.abs(a - r.alpha) / np.maximum(np.abs(r.alpha), 1e-2 * scale)  # reading R14
     eb = np.abs(b - r.beta) / np.abs(r.beta)
-    print(f"{name} [fp64_oz]: max rel alpha {ea.max():.2e} beta {eb.max():.2e}")
+    print(f"{name} [fp64_oz {route}]: max rel alpha {ea.max():.2e} beta {eb.max():.2e}")
     assert ea.max() <= 1e-5 and eb.max() <= 1e-5
+
+
+def test_fp64_oz_nonfinite_propagates():
+    """A NaN weight (theta_0) on the int8 path: the operand slicing marks that column of the qkv
+    GEMM's B operand and the epilogue writes NaN (finite garbage before), so the loss is
+    non-finite and the HVP fails with SLQ_ENUMERIC naming a sequence."""
+    cfg = si.CONFIGS["c2"]
+    th = si.init_params(cfg).copy()
+    lay0 = slq.plan_layout(slq.make_desc(cfg, "fp64_oz"), 1)
+    g0 = int(lay0["units"][1][0])  # first transformer block: ln1.g, ln1.b, then attn.qkv.w
+    th[g0 + 2 * cfg.d_model + 7] = np.nan
+    with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="fp64_oz", oz_min_mnk=1.0) as c:
+        v = torch.from_numpy(slq.shard_of(si.random_vector(th.size, 5), c.layout(), 0, 1)).cuda()
+        out = torch.empty_like(v)
+        with pytest.raises(slq.SlqError) as e:
+            c.hvp(v, out, cfg.eps)
+        assert e.value.status == slq.SLQ_ENUMERIC
+        seq = c.nonfinite_seq()
+        print("nonfinite sequence", seq, e.value)
+        assert seq == 0  # the NaN column reaches every token's logits
