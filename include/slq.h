@@ -211,6 +211,17 @@ slq_status slq_grad(slq_ctx* ctx, float* g_shard, double* loss);
 slq_status slq_lanczos(slq_ctx* ctx, uint64_t probe_seed, int32_t m, double* alpha, double* beta);
 slq_status slq_lanczos_info(const slq_ctx* ctx, int32_t* m_done, double* beta_next,
                             int32_t* nonfinite);
+/* The same recurrence in segments (slq_lanczos == start + step(m) + result, bit for bit): start
+ * draws q_1 for probe_seed and fixes m (<= max_steps); step runs n_steps more steps (the total
+ * must stay <= m); result copies alpha[m] / beta[m - 1] (host; entries not reached yet are NaN,
+ * and so is the last beta of an unfinished probe), ends the probe and sets slq_lanczos_info.
+ * Between calls the probe's state (basis rows or the three vectors, recurrence scalars) stays on
+ * the device; any other call on the context except slq_lanczos_info / host-only calls ends the
+ * probe's validity.  Used to time steps k0 .. k0 + K of a long probe (bench.py) and to monitor
+ * Ritz-value convergence.  All three are collective. */
+slq_status slq_lanczos_start(slq_ctx* ctx, uint64_t probe_seed, int32_t m);
+slq_status slq_lanczos_step(slq_ctx* ctx, int32_t n_steps);
+slq_status slq_lanczos_result(slq_ctx* ctx, double* alpha, double* beta);
 /* After slq_hvp returned SLQ_ENUMERIC (non-finite gradient, "error carrying the offending
  * batch id"): *seq = local index of the first sequence (MLP: data row) whose loss was non-finite
  * in the theta+ or theta- pass, or -1 when every loss was finite (overflow inside the backward
@@ -266,13 +277,20 @@ slq_status slq_blockdiag(slq_ctx* ctx, uint64_t probe_seed, double* rel_err, dou
  * Exposed so the probe can be checked bit-exactly against an independent generator. */
 slq_status slq_probe(slq_ctx* ctx, uint64_t probe_seed, float* q_shard);
 
-/* Per-kernel-class timing with CUDA events recorded on the library stream around every launch
- * (off by default).  classes: see slq_kernel_class_name.  Stats accumulate until reset. */
+/* Per-kernel-class timing with CUDA events recorded on the launching stream around every launch
+ * (off by default; launches run eagerly, not from CUDA graphs, while it is on).  enable = 1:
+ * serial mode (both gradient passes and their side work on one stream, so each launch's duration
+ * is its own); enable = 2: overlap-aware mode (the normal concurrency is kept; slq_kernel_busy
+ * gives each class's busy time = the union of its launch intervals on the device timeline);
+ * 0 = off.  classes: see slq_kernel_class_name.  Stats accumulate until reset. */
 slq_status slq_profile(slq_ctx* ctx, int32_t enable, int32_t reset);
 int32_t slq_num_kernel_classes(void);
 const char* slq_kernel_class_name(int32_t cls);
 slq_status slq_kernel_stats(const slq_ctx* ctx, int32_t cls, double* total_ms, int64_t* launches,
                             double* flops, double* bytes);
+/* busy time (ms) of class cls since the last reset: the length of the union of its launches'
+ * [start, end] intervals; cls = -1: of all classes together (device busy time) */
+slq_status slq_kernel_busy(const slq_ctx* ctx, int32_t cls, double* busy_ms);
 /* NCCL collectives issued since the context was created (collective audit):
  * all-gathers, reduce-scatters, all-reduces.  All zero when world_size == 1. */
 slq_status slq_collective_counts(const slq_ctx* ctx, int64_t* allgather, int64_t* reduce_scatter,

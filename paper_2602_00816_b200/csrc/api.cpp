@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <string.h>
 
+#include <algorithm>
 #include <memory>
 #include <string>
 #include <vector>
@@ -26,8 +27,16 @@ const char* kernel_class_name(int c) {
   return (c >= 0 && c < KC_COUNT) ? names[c] : "?";
 }
 
+// Per-kernel-class CUDA-event profiler.  Mode 1 (serial): the library runs every launch of a pass
+// on one stream (no side stream, no concurrent passes), so each launch's event duration is its
+// own.  Mode 2 (overlap-aware): the execution keeps its concurrency (two passes, side streams),
+// and besides the summed durations each class gets its BUSY time -- the length of the union of its
+// launches' [start, end] intervals on the device timeline (events are timed against one reference
+// event), i.e. the wall time during which at least one kernel of that class ran.  Busy time never
+// exceeds the profiled region, so a class's share of a step is busy / step time.
 struct Profiler {
   bool on = false;
+  int mode = 1;
   struct Rec {
     cudaEvent_t a, b;
     int cls;
@@ -36,8 +45,10 @@ struct Profiler {
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t open = nullptr;
+  cudaEvent_t t0 = nullptr;  // reference of the interval timeline (mode 2)
   double ms[KC_COUNT] = {}, flops[KC_COUNT] = {}, bytes[KC_COUNT] = {};
   int64_t count[KC_COUNT] = {};
+  std::vector<std::pair<float, float>> iv[KC_COUNT];
   cudaEvent_t take() {
     if (!pool.empty()) {
       cudaEvent_t e = pool.back();
@@ -57,22 +68,52 @@ struct Profiler {
       flops[r.cls] += r.flops;
       bytes[r.cls] += r.bytes;
       count[r.cls]++;
+      if (t0) {
+        float s = 0, e = 0;
+        cudaEventElapsedTime(&s, t0, r.a);
+        cudaEventElapsedTime(&e, t0, r.b);
+        iv[r.cls].push_back({s, e});
+      }
       pool.push_back(r.a);
       pool.push_back(r.b);
     }
     pending.clear();
   }
-  void reset() {
+  // union length of the intervals of class c (c < 0: of every class)
+  double busy(int c) {
     flush();
-    for (int i = 0; i < KC_COUNT; ++i) ms[i] = flops[i] = bytes[i] = 0, count[i] = 0;
+    std::vector<std::pair<float, float>> v;
+    for (int i = 0; i < KC_COUNT; ++i)
+      if (c < 0 || c == i) v.insert(v.end(), iv[i].begin(), iv[i].end());
+    std::sort(v.begin(), v.end());
+    double tot = 0, cs = 0, ce = -1e30;
+    for (auto& x : v) {
+      if (x.first > ce) {
+        if (ce > cs) tot += ce - cs;
+        cs = x.first;
+        ce = x.second;
+      } else {
+        ce = std::max(ce, (double)x.second);
+      }
+    }
+    if (ce > cs) tot += ce - cs;
+    return tot;
+  }
+  void reset(cudaStream_t s) {
+    flush();
+    for (int i = 0; i < KC_COUNT; ++i) ms[i] = flops[i] = bytes[i] = 0, count[i] = 0, iv[i].clear();
+    if (!t0) cudaEventCreate(&t0);
+    cudaEventRecord(t0, s);
   }
   ~Profiler() {
     flush();
     for (auto e : pool) cudaEventDestroy(e);
+    if (t0) cudaEventDestroy(t0);
   }
 };
 
 bool prof_enabled(const Profiler* p) { return p && p->on; }
+bool prof_serial(const Profiler* p) { return p && p->on && p->mode == 1; }
 
 void prof_begin(Profiler* p, int, cudaStream_t s) {
   if (!p || !p->on) return;
@@ -411,6 +452,31 @@ slq_status slq_lanczos(slq_ctx* ctx, uint64_t seed, int32_t m, double* alpha, do
   });
 }
 
+slq_status slq_lanczos_start(slq_ctx* ctx, uint64_t seed, int32_t m) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    check_device(ctx);
+    ctx->engine->start(seed, m);
+  });
+}
+
+slq_status slq_lanczos_step(slq_ctx* ctx, int32_t n_steps) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    check_device(ctx);
+    ctx->engine->step(n_steps);
+  });
+}
+
+slq_status slq_lanczos_result(slq_ctx* ctx, double* alpha, double* beta) {
+  if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
+  return guarded(ctx, [&] {
+    SLQ_CHECK_ARG(alpha != nullptr && beta != nullptr, "alpha / beta");
+    check_device(ctx);
+    ctx->engine->result(alpha, beta);
+  });
+}
+
 slq_status slq_slq(slq_ctx* ctx, const uint64_t* seeds, int32_t n_probes, int32_t m, double* alpha, double* beta,
                    int32_t* m_done) {
   if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
@@ -513,9 +579,20 @@ slq_status slq_blockdiag(slq_ctx* ctx, uint64_t probe_seed, double* rel_err, dou
 slq_status slq_profile(slq_ctx* ctx, int32_t enable, int32_t reset) {
   if (!ctx) return fail(nullptr, SLQ_EINVAL, "ctx");
   return guarded(ctx, [&] {
-    if (reset) ctx->prof.reset();
+    SLQ_CHECK_ARG(enable >= 0 && enable <= 2, "enable: 0 off, 1 serial, 2 overlap-aware");
+    if (reset) {
+      check_device(ctx);
+      ctx->prof.reset(ctx->stream);
+    }
     ctx->prof.on = enable != 0;
+    if (enable) ctx->prof.mode = enable;
   });
+}
+
+slq_status slq_kernel_busy(const slq_ctx* ctx, int32_t cls, double* busy_ms) {
+  if (!ctx || cls < -1 || cls >= KC_COUNT || !busy_ms) return fail(nullptr, SLQ_EINVAL, "ctx / class / busy_ms");
+  *busy_ms = const_cast<slq_ctx*>(ctx)->prof.busy(cls);
+  return SLQ_OK;
 }
 
 int32_t slq_num_kernel_classes(void) { return KC_COUNT; }

@@ -51,6 +51,7 @@ const char* kernel_class_name(int c);
 // per-context launch bookkeeping (profiler + launch counter); defined in api.cpp
 struct Profiler;
 bool prof_enabled(const Profiler* p);
+bool prof_serial(const Profiler* p);  // profiler on in serial mode: no concurrency
 void prof_begin(Profiler* p, int cls, cudaStream_t s);
 void prof_end(Profiler* p, int cls, cudaStream_t s, double flops, double bytes);
 

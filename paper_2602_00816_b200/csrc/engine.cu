@@ -406,7 +406,7 @@ struct EngineT : Engine {
       pe[0]->run_pair(reinterpret_cast<const T*>(theta), gp, thm, gm, dscal + 2);
       return;
     }
-    if (!dual || prof_enabled(L.prof)) {  // profiled runs are serial: per-launch durations stay honest
+    if (!dual || prof_serial(L.prof)) {  // serial profile: per-launch durations stay honest
       pe[0]->run(thp, gp, dscal + 2);
       pe[0]->run(thm, gm, dscal + 3);
       return;
@@ -579,6 +579,109 @@ struct EngineT : Engine {
     sync();
   }
 
+  // ---- resumable Lanczos: start(seed, m) / step(n) / result(...) (slq_lanczos_start / _step /
+  // _result; slq_lanczos = all three).  State between calls: the step counter, the basis rows or
+  // rotating vectors, the device recurrence scalars and (no-basis mode) the host-side alpha / beta.
+  struct Probe {
+    bool active = false;
+    uint64_t seed = 0;
+    int m = 0, k = 0;        // requested steps, steps done
+    bool stopped = false;    // no-basis mode: breakdown seen on the host
+    double a_prev = 0.0, b_k = 0.0, tmax = 0.0;
+    std::vector<double> ha, hb;  // no-basis mode: alpha_k, beta_{k+1} as they are formed
+    LanczosInfo info;
+  } pr;
+
+  void start(uint64_t seed, int m) override {
+    SLQ_CHECK_ARG(m >= 1 && m <= max_steps, "1 <= m <= max_steps");
+    pr = Probe();
+    last_info = LanczosInfo();
+    pr.active = true;
+    pr.seed = seed;
+    pr.m = m;
+    pr.ha.assign((size_t)m, NAN);
+    pr.hb.assign((size_t)m, NAN);
+    const double inv_sqrt_P = 1.0 / sqrt((double)plan.P);
+    if (d.reorth == SLQ_REORTH_NONE) {
+      probe_fill(L, vq[0], n, units_dev, (int)plan.units.size(), seed, inv_sqrt_P);
+    } else if (basis16) {  // q_1 = bf16(s / sqrt(P)): signs first, one rounding from fp64
+      probe_fill(L, qf[0], n, units_dev, (int)plan.units.size(), seed, 1.0);
+      store_bf16(L, qf[0], nullptr, inv_sqrt_P, basis16, qf[0], n);
+    } else {
+      probe_fill(L, basis, n, units_dev, (int)plan.units.size(), seed, inv_sqrt_P);
+    }
+  }
+
+  void step(int nsteps) override {
+    SLQ_CHECK_ARG(pr.active, "slq_lanczos_step before slq_lanczos_start");
+    SLQ_CHECK_ARG(nsteps >= 0 && pr.k + nsteps <= pr.m, "steps beyond the m given to slq_lanczos_start");
+    const int k1 = pr.k + nsteps;
+    if (d.reorth == SLQ_REORTH_NONE) {
+      for (; pr.k < k1; ++pr.k) nobasis_step(pr.k);
+    } else {
+      for (; pr.k < k1; ++pr.k) basis_step(pr.k);
+    }
+  }
+
+  LanczosInfo result(double* alpha, double* beta) override {
+    SLQ_CHECK_ARG(pr.active, "slq_lanczos_result before slq_lanczos_start");
+    const int m = pr.m, mk = pr.k;
+    for (int i = 0; i < m; ++i) alpha[i] = NAN;
+    for (int i = 0; i + 1 < m; ++i) beta[i] = NAN;
+    LanczosInfo info;
+    if (d.reorth == SLQ_REORTH_NONE) {
+      sync();
+      info = pr.info;
+      for (int k = 0; k < info.m_done; ++k) {
+        alpha[k] = pr.ha[k];
+        if (k + 1 < m && k + 1 < info.m_done) beta[k] = pr.hb[k];
+      }
+    } else {
+      double* d_alpha = dscal + 8 + 3 * (max_steps + 1);
+      double* d_bhist = dscal + 8 + 4 * (max_steps + 1);
+      double* ha_pin = hstage + 64;
+      double* hb_pin = hstage + 64 + (max_steps + 1);
+      if (mk > 0) {
+        SLQ_CUDA(cudaMemcpyAsync(ha_pin, d_alpha, sizeof(double) * mk, cudaMemcpyDeviceToHost, L.stream));
+        SLQ_CUDA(cudaMemcpyAsync(hb_pin, d_bhist, sizeof(double) * mk, cudaMemcpyDeviceToHost, L.stream));
+      }
+      sync();
+      // steps after a breakdown ran on a noise direction; they are discarded here
+      double tmax = 0.0;
+      for (int k = 0; k < mk; ++k) {
+        const double a = ha_pin[k], bnext = hb_pin[k];
+        if (!std::isfinite(a) || !std::isfinite(bnext)) {
+          info.nonfinite = 1;
+          info.m_done = k;
+          last_info = info;
+          pr.active = false;
+          throw Error(SLQ_ENUMERIC, "non-finite Lanczos coefficient at step " + std::to_string(k + 1));
+        }
+        alpha[k] = a;
+        if (k + 1 < m) beta[k] = bnext;
+        tmax = std::max(tmax, fabs(a));
+        if (k > 0) tmax = std::max(tmax, beta[k - 1]);
+        info.m_done = k + 1;
+        info.beta_next = bnext;
+        if (k + 1 < m && bnext <= 1e-7 * tmax) {  // breakdown: invariant subspace (fp32 vectors)
+          beta[k] = NAN;
+          break;
+        }
+      }
+      // the last step's beta_{k+1} is only an output if another step follows it
+      if (mk < m && info.m_done == mk && mk >= 1) beta[mk - 1] = NAN;
+    }
+    last_info = info;
+    pr.active = false;
+    return info;
+  }
+
+  LanczosInfo lanczos(uint64_t seed, int m, double* alpha, double* beta) override {
+    start(seed, m);
+    step(m);
+    return result(alpha, beta);
+  }
+
   // Three-term recurrence without a stored basis (c5 mode; "only the essential Lanczos
   // vectors").  Per step two vector kernels and one 3-scalar reduction:
   //   perturb:  q_k = (w_raw - alpha_{k-1} q_{k-1}) / beta_k  (deferred normalisation) and theta+-
@@ -586,66 +689,61 @@ struct EngineT : Engine {
   //   fd:       w_raw = (g+ - g-)/(2 eta) - beta_k q_{k-1};  s1 = <w_raw,q_k>, s2 = |w_raw|^2, s3 = |q_k|^2
   //   host:     alpha_k = s1;  beta_{k+1}^2 = |w_raw - alpha_k q_k|^2 = s2 - 2 alpha s1 + alpha^2 s3
   // If that Pythagorean form loses more than 3 digits to cancellation, the residual is formed
-  // explicitly (one extra pass) and its norm taken directly.
-  LanczosInfo lanczos_nobasis(uint64_t seed, int m, double* alpha, double* beta) {
-    for (int i = 0; i < m; ++i) alpha[i] = NAN;
-    for (int i = 0; i + 1 < m; ++i) beta[i] = NAN;
-    LanczosInfo info;
+  // explicitly (one extra pass) and its norm taken directly.  After a breakdown (or a non-finite
+  // coefficient) the remaining steps do nothing.
+  void nobasis_step(int k) {
+    if (pr.stopped) return;
     const bool exact = d.perturb == SLQ_PERTURB_EXACT && sizeof(T) == 8;
     const double eps = d.eps_default;
     const float eps_f = (float)eps;
     const double inv2eps = exact ? 1.0 / (2.0 * eps) : 1.0 / (2.0 * (double)eps_f);
     float* q[2] = {vq[0], vq[1]};  // q[k % 2] = q_k
     float* wr = vq[2];
-    double a_prev = 0.0, b_k = 0.0, tmax = 0.0;
     const int nb = vec_nblocks(n);
-    probe_fill(L, q[0], n, units_dev, (int)plan.units.size(), seed, 1.0 / sqrt((double)plan.P));
-    for (int k = 0; k < m; ++k) {
-      float* qk = q[k % 2];
-      const float* qprev = k > 0 ? q[(k + 1) % 2] : nullptr;
-      if (k == 0) {
-        form_points(qk, eps);
-      } else {
-        perturb_lanczos<T>(L, exact, theta, wr, q[(k + 1) % 2], a_prev, b_k, eps, qk, thp, thm, n);
-      }
-      two_passes();
-      fd_partials3<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), b_k, qprev, qk, wr, n, partials);
-      finish_reduce(nb, 3, dscal + 8);  // reduce_partials reads [nb x 3] row-major
-      double s[3];
-      to_host(dscal + 8, 3, s);
-      const double a = s[0];
-      double b2 = s[1] - 2.0 * a * s[0] + a * a * s[2];
-      double a_carry = a;
-      if (!(b2 > 1e-3 * s[1])) {  // cancellation: form w = w_raw - alpha q_k explicitly
-        SLQ_CUDA(cudaMemcpyAsync(dscal + 4, &a, sizeof(double), cudaMemcpyHostToDevice, L.stream));
-        axpy_dev(L, wr, qk, dscal + 4, -1.0, n, partials);
-        finish_reduce(nb, 1, dscal + 0);
-        to_host(dscal + 0, 1, &b2);
-        a_carry = 0.0;  // wr now holds the residual itself
-      }
-      if (!std::isfinite(a) || !std::isfinite(b2)) {
-        info.nonfinite = 1;
-        info.m_done = k;
-        last_info = info;
-        throw Error(SLQ_ENUMERIC, "non-finite Lanczos coefficient at step " + std::to_string(k + 1));
-      }
-      const double bnext = sqrt(std::max(b2, 0.0));
-      alpha[k] = a;
-      if (k + 1 < m) beta[k] = bnext;
-      tmax = std::max(tmax, fabs(a));
-      if (k > 0) tmax = std::max(tmax, b_k);
-      info.m_done = k + 1;
-      info.beta_next = bnext;
-      if (k + 1 < m && bnext <= 1e-7 * tmax) {
-        beta[k] = NAN;
-        break;
-      }
-      a_prev = a_carry;
-      b_k = bnext;
+    float* qk = q[k % 2];
+    const float* qprev = k > 0 ? q[(k + 1) % 2] : nullptr;
+    if (k == 0) {
+      form_points(qk, eps);
+    } else {
+      perturb_lanczos<T>(L, exact, theta, wr, q[(k + 1) % 2], pr.a_prev, pr.b_k, eps, qk, thp, thm, n);
     }
-    sync();
-    last_info = info;
-    return info;
+    two_passes();
+    fd_partials3<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), pr.b_k, qprev, qk, wr, n, partials);
+    finish_reduce(nb, 3, dscal + 8);  // reduce_partials reads [nb x 3] row-major
+    double s3[3];
+    to_host(dscal + 8, 3, s3);
+    const double a = s3[0];
+    double b2 = s3[1] - 2.0 * a * s3[0] + a * a * s3[2];
+    double a_carry = a;
+    if (!(b2 > 1e-3 * s3[1])) {  // cancellation: form w = w_raw - alpha q_k explicitly
+      SLQ_CUDA(cudaMemcpyAsync(dscal + 4, &a, sizeof(double), cudaMemcpyHostToDevice, L.stream));
+      axpy_dev(L, wr, qk, dscal + 4, -1.0, n, partials);
+      finish_reduce(nb, 1, dscal + 0);
+      to_host(dscal + 0, 1, &b2);
+      a_carry = 0.0;  // wr now holds the residual itself
+    }
+    if (!std::isfinite(a) || !std::isfinite(b2)) {
+      pr.info.nonfinite = 1;
+      pr.info.m_done = k;
+      last_info = pr.info;
+      pr.stopped = true;
+      pr.active = false;
+      throw Error(SLQ_ENUMERIC, "non-finite Lanczos coefficient at step " + std::to_string(k + 1));
+    }
+    const double bnext = sqrt(std::max(b2, 0.0));
+    pr.ha[k] = a;
+    pr.hb[k] = bnext;
+    pr.tmax = std::max(pr.tmax, fabs(a));
+    if (k > 0) pr.tmax = std::max(pr.tmax, pr.b_k);
+    pr.info.m_done = k + 1;
+    pr.info.beta_next = bnext;
+    if (k + 1 < pr.m && bnext <= 1e-7 * pr.tmax) {
+      pr.hb[k] = NAN;
+      pr.stopped = true;
+      return;
+    }
+    pr.a_prev = a_carry;
+    pr.b_k = bnext;
   }
 
   // CGS2 over the `cnt` basis rows [0, cnt) (the window's ring holds exactly the last r vectors).
@@ -674,83 +772,37 @@ struct EngineT : Engine {
     finish_reduce(nb, 1, dscal + 0);
   }
 
-  LanczosInfo lanczos(uint64_t seed, int m, double* alpha, double* beta) override {
-    last_info = LanczosInfo();
-    SLQ_CHECK_ARG(m >= 1 && m <= max_steps, "1 <= m <= max_steps");
-    if (d.reorth == SLQ_REORTH_NONE) return lanczos_nobasis(seed, m, alpha, beta);
-    for (int i = 0; i < m; ++i) alpha[i] = NAN;
-    for (int i = 0; i + 1 < m; ++i) beta[i] = NAN;
-    LanczosInfo info;
+  // step k with a stored basis (FULL / WINDOW): alpha / beta stay on the device (no host round
+  // trip inside the recurrence); breakdown is detected in result()
+  void basis_step(int k) {
     const bool window = d.reorth == SLQ_REORTH_WINDOW;
     const bool b16 = basis16 != nullptr;
     const int r = d.reorth_window;
-    auto slot = [&](int k) { return window ? k % r : k; };
-    // fp32 view of q_k: the basis row itself (fp32 basis) or the exact working copy (bf16 basis)
-    auto qvec = [&](int k) -> float* { return b16 ? qf[k % 2] : basis + (int64_t)slot(k) * n; };
+    auto slot = [&](int j) { return window ? j % r : j; };
+    // fp32 view of q_j: the basis row itself (fp32 basis) or the exact working copy (bf16 basis)
+    auto qvec = [&](int j) -> float* { return b16 ? qf[j % 2] : basis + (int64_t)slot(j) * n; };
     double* d_beta = dscal + 1;
     double* d_coef = dscal + 8;                         // [max_steps + 1], then [2 (max_steps + 1)] dots
     double* d_alpha = dscal + 8 + 3 * (max_steps + 1);  // [max_steps + 1]
     double* d_bhist = dscal + 8 + 4 * (max_steps + 1);  // [max_steps + 1]: beta_{k+1}
-    const double inv_sqrt_P = 1.0 / sqrt((double)plan.P);
-    if (b16) {  // q_1 = bf16(s / sqrt(P)): signs first, one rounding from fp64
-      probe_fill(L, qf[0], n, units_dev, (int)plan.units.size(), seed, 1.0);
-      store_bf16(L, qf[0], nullptr, inv_sqrt_P, basis16, qf[0], n);
-    } else {
-      probe_fill(L, qvec(0), n, units_dev, (int)plan.units.size(), seed, inv_sqrt_P);
-    }
-    double tmax = 0.0;
-    for (int k = 0; k < m; ++k) {
-      float* qk = qvec(k);
-      const float* qprev = k > 0 ? qvec(k - 1) : nullptr;
-      const double inv2eps = form_points(qk, d.eps_default);
-      two_passes();
-      fd_w<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
-      const int cnt = window ? std::min(k + 1, r) : k + 1;
+    float* qk = qvec(k);
+    const float* qprev = k > 0 ? qvec(k - 1) : nullptr;
+    const double inv2eps = form_points(qk, d.eps_default);
+    two_passes();
+    fd_w<T>(L, fd_a(), fd_b(), fd_scale(inv2eps), k > 0 ? d_beta : nullptr, qprev, w, qk, n, nullptr);
+    const int cnt = window ? std::min(k + 1, r) : k + 1;
+    if (b16)
+      cgs2<__nv_bfloat16>(basis16, cnt, slot(k), qk, d_coef, d_alpha + k);
+    else
+      cgs2<float>(basis, cnt, slot(k), qk, d_coef, d_alpha + k);
+    // beta_{k+1} = ||w|| on the device (the next step's FD kernel reads it there)
+    step_beta(L, dscal + 0, d_beta, d_bhist + k);
+    if (k + 1 < pr.m) {
       if (b16)
-        cgs2<__nv_bfloat16>(basis16, cnt, slot(k), qk, d_coef, d_alpha + k);
+        store_bf16(L, w, dscal + 0, 0.0, basis16 + (int64_t)slot(k + 1) * n, qf[(k + 1) % 2], n);
       else
-        cgs2<float>(basis, cnt, slot(k), qk, d_coef, d_alpha + k);
-      // beta_{k+1} = ||w|| on the device (the next step's FD kernel reads it there); no host round
-      // trip inside the recurrence -- breakdown is detected after the loop (below)
-      step_beta(L, dscal + 0, d_beta, d_bhist + k);
-      if (k + 1 < m) {
-        if (b16)
-          store_bf16(L, w, dscal + 0, 0.0, basis16 + (int64_t)slot(k + 1) * n, qf[(k + 1) % 2], n);
-        else
-          scale_by_inv_sqrt(L, w, dscal + 0, qvec(k + 1), n);
-      }
+        scale_by_inv_sqrt(L, w, dscal + 0, qvec(k + 1), n);
     }
-    std::vector<double> ha((size_t)m), hb((size_t)m);
-    double* ha_pin = hstage + 64;
-    double* hb_pin = hstage + 64 + (max_steps + 1);
-    SLQ_CUDA(cudaMemcpyAsync(ha_pin, d_alpha, sizeof(double) * m, cudaMemcpyDeviceToHost, L.stream));
-    SLQ_CUDA(cudaMemcpyAsync(hb_pin, d_bhist, sizeof(double) * m, cudaMemcpyDeviceToHost, L.stream));
-    sync();
-    memcpy(ha.data(), ha_pin, sizeof(double) * m);
-    memcpy(hb.data(), hb_pin, sizeof(double) * m);
-    // steps after a breakdown ran on a noise direction; they are discarded here
-    for (int k = 0; k < m; ++k) {
-      const double a = ha[k], bnext = hb[k];
-      if (!std::isfinite(a) || !std::isfinite(bnext)) {
-        info.nonfinite = 1;
-        info.m_done = k;
-        last_info = info;
-        throw Error(SLQ_ENUMERIC, "non-finite Lanczos coefficient at step " + std::to_string(k + 1));
-      }
-      alpha[k] = a;
-      if (k + 1 < m) beta[k] = bnext;
-      tmax = std::max(tmax, fabs(a));
-      if (k > 0) tmax = std::max(tmax, beta[k - 1]);
-      info.m_done = k + 1;
-      info.beta_next = bnext;
-      if (k + 1 < m && bnext <= 1e-7 * tmax) {  // breakdown: invariant subspace (fp32 vectors)
-        beta[k] = NAN;
-        break;
-      }
-    }
-    sync();
-    last_info = info;
-    return info;
   }
 };
 

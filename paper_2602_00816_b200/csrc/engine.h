@@ -22,6 +22,10 @@ struct Engine {
   virtual void hvp(const float* v, float* out, double eps) = 0;
   virtual double grad(float* g) = 0;  // returns the global mean loss
   virtual LanczosInfo lanczos(uint64_t seed, int m, double* alpha, double* beta) = 0;
+  // resumable form of lanczos(): start a probe of up to m steps, advance it, read it out
+  virtual void start(uint64_t seed, int m) = 0;
+  virtual void step(int nsteps) = 0;
+  virtual LanczosInfo result(double* alpha, double* beta) = 0;
   virtual void probe(uint64_t seed, float* q) = 0;
   virtual double pass_flops() const = 0;  // algorithmic FLOPs of one fwd+bwd (this rank)
   // CG on (H + damping I) x = b; returns iterations, writes the relative residual

@@ -245,9 +245,10 @@ struct SideStream {
     side.stream = s;
     side.ws = &ws;
   }
-  // While the per-class profiler is on, everything runs on the main stream so that each launch's
-  // event-timed duration is its own (concurrent kernels would inflate each other's durations).
-  bool serial() const { return prof_enabled(main.prof); }
+  // While the per-class profiler is on in serial mode, everything runs on the main stream so that
+  // each launch's event-timed duration is its own (concurrent kernels would inflate each other's
+  // durations); the overlap-aware mode keeps the side stream.
+  bool serial() const { return prof_serial(main.prof); }
   const Launch& lane() const { return serial() ? main : side; }
   void fork() {
     if (serial()) return;

@@ -103,6 +103,10 @@ def lib() -> ctypes.CDLL:
         "slq_cg": (I32, [P, P, P, D, I32, D, P, P]),
         "slq_blockdiag": (I32, [P, U64, P, P]),
         "slq_plan_memory": (I32, [ctypes.POINTER(ModelDescC), I32, I32, P]),
+        "slq_lanczos_start": (I32, [P, U64, I32]),
+        "slq_kernel_busy": (I32, [P, I32, P]),
+        "slq_lanczos_step": (I32, [P, I32]),
+        "slq_lanczos_result": (I32, [P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -367,6 +371,20 @@ class SlqContext:
         _check(lib().slq_lanczos(self._h, ctypes.c_uint64(seed), m, a.ctypes.data, b.ctypes.data), self._h)
         return a, b[:m - 1]
 
+    def lanczos_start(self, seed: int, m: int) -> None:
+        self._m = m
+        _check(lib().slq_lanczos_start(self._h, ctypes.c_uint64(seed), m), self._h)
+
+    def lanczos_step(self, n: int) -> None:
+        _check(lib().slq_lanczos_step(self._h, n), self._h)
+
+    def lanczos_result(self) -> Tuple[np.ndarray, np.ndarray]:
+        m = self._m
+        a = np.empty(m)
+        b = np.empty(max(m - 1, 1))
+        _check(lib().slq_lanczos_result(self._h, a.ctypes.data, b.ctypes.data), self._h)
+        return a, b[:m - 1]
+
     def slq(self, seeds, m: int):
         """All probes' (alpha [s][m], beta [s][m-1], m_done [s]) -- slq_slq."""
         sd = np.ascontiguousarray(seeds, dtype=np.uint64)
@@ -400,8 +418,15 @@ class SlqContext:
         _check(lib().slq_probe(self._h, ctypes.c_uint64(seed), _ptr(q)), self._h)
 
     # -- measurement
-    def profile(self, enable: bool, reset: bool = False) -> None:
-        _check(lib().slq_profile(self._h, int(enable), int(reset)), self._h)
+    def profile(self, enable, reset: bool = False) -> None:
+        """enable: False / True (= 1, serial) / "overlap" (= 2, concurrency kept, busy times)."""
+        mode = 2 if enable == "overlap" else int(bool(enable))
+        _check(lib().slq_profile(self._h, mode, int(reset)), self._h)
+
+    def kernel_busy(self, cls: int = -1) -> float:
+        b = ctypes.c_double()
+        _check(lib().slq_kernel_busy(self._h, int(cls), ctypes.byref(b)), self._h)
+        return b.value
 
     def kernel_stats(self) -> dict:
         L = lib()
@@ -410,7 +435,8 @@ class SlqContext:
             ms, n, fl, by = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
             _check(L.slq_kernel_stats(self._h, i, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl), ctypes.byref(by)),
                    self._h)
-            out[name] = {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+            out[name] = {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value,
+                         "busy_ms": self.kernel_busy(i)}
         return out
 
     def collective_counts(self) -> dict:

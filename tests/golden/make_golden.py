@@ -86,7 +86,13 @@ def main():
     ap.add_argument("--m", type=int, required=True)
     ap.add_argument("--eps", type=float, nargs="+", required=True)
     ap.add_argument("--reorth", default="full", choices=["full", "none"])
+    ap.add_argument("--mem-limit-gb", type=float, default=0.0,
+                    help="RLIMIT_AS for this process (a MemoryError instead of the host's OOM killer)")
     a = ap.parse_args()
+    if a.mem_limit_gb > 0:
+        import resource
+        lim = int(a.mem_limit_gb * 2**30)
+        resource.setrlimit(resource.RLIMIT_AS, (lim, lim))
     for eps in a.eps:
         d = run(a.case, eps, a.m, a.reorth)
         path = golden_path(a.case, eps, a.m, a.reorth)

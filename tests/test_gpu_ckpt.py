@@ -62,21 +62,24 @@ def test_memory_plan_matches_allocation(name, numerics, ckpt):
     cfg = si.CONFIGS[name]
     th = si.init_params(cfg)
     tok = si.tokens(cfg)
+    desc = slq.make_desc(cfg, numerics, max_steps=cfg.m, act_ckpt=ckpt)
+    P_loc = slq.plan_layout(desc, 1)["P_loc"]
+    v = torch.zeros(P_loc, dtype=torch.float32, device="cuda")
+    v[0] = 1.0
+    out = torch.empty_like(v)
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # (torch's cached blocks would hide allocations from mem_get_info)
     free0, _ = torch.cuda.mem_get_info()
     with slq.SlqContext(cfg, th, tok, pass_numerics=numerics, max_steps=cfg.m, act_ckpt=ckpt) as c:
-        v = torch.zeros(c.P_loc, dtype=torch.float32, device="cuda")
-        v[0] = 1.0
-        out = torch.empty_like(v)
         torch.cuda.synchronize()
         free1, _ = torch.cuda.mem_get_info()
         c.hvp(v, out, cfg.eps)
         free2, _ = torch.cuda.mem_get_info()
         p = slq.plan_memory(c.desc, 1, cfg.n_seq)
-    used_init = free0 - free1 - 2 * 4 * c.P_loc  # (v, out are torch tensors)
-    used_hvp = free0 - free2 - 2 * 4 * c.P_loc
-    planned = p["total"] - 2 * 4 * c.P_loc       # minus the staging of host-pointer calls
+    used_init = free0 - free1
+    used_hvp = free0 - free2
+    planned = p["total"] - 2 * 4 * P_loc  # minus the staging of host-pointer calls (not used here)
     print(f"{name} ckpt={ckpt}: planned {planned / 2**30:.3f} GiB, after init {used_init / 2**30:.3f}, "
           f"after hvp {used_hvp / 2**30:.3f} GiB; plan {({k: round(x / 2**30, 3) for k, x in p.items()})}")
-    assert abs(used_init - planned) <= 0.03 * planned + (256 << 20)
+    assert abs(used_init - planned) <= 0.02 * planned + (256 << 20)
     assert used_hvp - used_init <= 0.03 * planned + (512 << 20)  # graphs, NCCL/cuBLAS-free: small

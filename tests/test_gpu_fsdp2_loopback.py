@@ -109,9 +109,11 @@ def test_two_ranks_equal_one(name, numerics):
     # fp64 passes: the R = 2 reduce-scatter sums two rank partials (round-off ~1e-16 of g), which the
     # FD difference amplifies by ||g|| / (2 eta ||Hv||); fp32 (BF16X3) passes: the same at fp32
     # round-off, i.e. Theorem 1's fp32 floor -- only agreement at that level is asserted
+    # (FP64_OZ: halving the per-rank batch moves GEMMs across the int8 / DMMA threshold and changes
+    # the split-K plans, so the gradients differ at the Ozaki truncation level, ~1e-11)
     f32 = numerics == "bf16x3"
     assert abs(r2[0]["loss"] - r1["loss"]) <= (1e-6 if f32 else 1e-13) * abs(r1["loss"])
-    assert eg <= (1e-5 if f32 else 1e-12)
+    assert eg <= (1e-5 if f32 else 1e-9 if numerics == "fp64_oz" else 1e-12)
     tol = 5e-2 if f32 else 1e-7
     assert eh <= tol and ea <= tol and eb <= tol
     # collective audit

@@ -1,14 +1,24 @@
-"""Parity of the larger configs (BASELINE configs[2..4]) at their parity batches.
+"""Parity of the larger configs (BASELINE configs[2..4]) at their parity batches
+against STORED oracle results (tests/golden/lanczos_*.json, written by the committed script
+tests/golden/make_golden.py, which calls only oracle/ -- the oracle costs 30-70 s per FD-HVP on
+these cases, too slow to recompute inside the GPU run).
 
-c3 (GPT-2-small shape, tied, bf16-representable weights) runs by default; the c4 (Llama-1B) and
-c5-twin (every Llama-3-8B layer shape, 2 blocks, vocab 128256) cases need ~60 GB of host RAM for
-the fp64 oracle and several minutes, so they run when SLQ_LARGE_TESTS=1 (their logs are kept
-under profiles/).  The GPU runs fp64 passes; gates are the north star's bf16 gates (moments
-<= 1e-2, extreme Ritz <= 2e-2) plus the fp32 ones the fp64 path also meets (HVP <= 1e-4,
-alpha/beta <= 1e-5).
+  * c3 (GPT-2-small shape, tied, bf16-representable weights; 2 x 1024 tokens): Lanczos m = 32
+    with full reorthogonalisation at eps in {1e-2, 1e-3, 1e-4} (BASELINE configs[2]'s sweep),
+    in the bench's own configuration (FP64_OZ hybrid: GEMMs >= 1e9 M N K on the int8 tensor
+    cores) and all-DMMA FP64;
+  * c4 (Llama-1B shape; 2 x 256 tokens) and the c5 twin (every Llama-3-8B layer shape, 2 blocks,
+    vocab 128256; 1 x 512 tokens, no stored basis as in configs[4]): Lanczos m = 16 (c4 with
+    full reorthogonalisation: m = 8).
+
+Gates: the north star's fp32 gates, which the fp64-faithful passes meet -- H q_1 relative error
+<= 1e-4 (on 8320 stored entries, its norm and four sign projections), alpha / beta <= 1e-5
+relative (alpha per reading R14) over every step -- and the bf16-model gates (density moments
+<= 1e-2, extreme Ritz values <= 2e-2).  One c3 case also compares the FULL H q_1 vector with a
+live oracle evaluation.
 """
+import json
 import os
-import time
 
 import numpy as np
 import pytest
@@ -19,6 +29,8 @@ from oracle import fdhvp, lanczos as OL, probe
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
 
 @pytest.fixture(scope="module", autouse=True)
 def built():
@@ -28,65 +40,98 @@ def built():
     build.build()
 
 
-def _case(name, numerics="fp64"):
-    from paper_2602_00816_b200 import slq
-    cfg = si.CONFIGS[name]
-    t0 = time.time()
+from paper_2602_00816_b200 import slq  # noqa: E402
+
+
+def golden(case, eps, m, reorth):
+    p = os.path.join(GOLD, f"lanczos_{case}_eps{eps:g}_m{m}_{reorth}.json")
+    with open(p) as f:
+        return json.load(f)
+
+
+def gpu_run(cfg, numerics, reorth, m, eps):
+    """GPU H q_1 (full canonical vector) and Lanczos alpha / beta for the config's probe."""
     th = si.init_params(cfg)
     tok = si.tokens(cfg)
-    P = th.size
-    q1 = probe.rademacher_probe(cfg.probe_seed0, P)
-    with slq.SlqContext(cfg, th, tok, reorth="full" if cfg.reorth_full else "none", max_steps=cfg.m,
-                        pass_numerics=numerics) as c:
+    q1 = probe.rademacher_probe(cfg.probe_seed0, th.size)
+    with slq.SlqContext(cfg, th, tok, reorth=reorth, max_steps=m, pass_numerics=numerics, eps=eps) as c:
         lay = c.layout()
         qd = torch.from_numpy(slq.shard_of(q1.astype(np.float32), lay, 0, 1)).cuda()
         out = torch.empty_like(qd)
-        c.hvp(qd, out, cfg.eps)
-        hv = slq.unshard([out.cpu().numpy()], lay)
-        a, b = c.lanczos(cfg.probe_seed0, cfg.m)
-    t_gpu = time.time() - t0
-    g = fdhvp.make_grad_fn(cfg, tok)
-    hq1 = fdhvp.fd_hvp_step(g, th, q1, cfg.eps, "exact")  # oracle H q1 (unit q1: hvp == step)
-    cache = {"first": hq1}
+        c.hvp(qd, out, eps)
+        hv = slq.unshard([out.cpu().numpy()], lay).astype(np.float64)
+        a, b = c.lanczos(cfg.probe_seed0, m)
+    # the GPU normalises its fp32 direction internally: H (q1_f32 / ||q1_f32||) ||q1_f32||, and q1 is
+    # unit, so rescale the oracle's H q1 by ||q1_f32|| (the fp32 rounding of 1/sqrt(P) is uniform)
+    return hv, a, b, float(np.linalg.norm(q1.astype(np.float32).astype(np.float64))), th.size
 
-    def op(q):
-        if "first" in cache:
-            return cache.pop("first")
-        return fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact")
 
-    r = OL.lanczos(op, q1, cfg.m, "full" if cfg.reorth_full else "none")
-    t_all = time.time() - t0
-    # GPU hvp normalises v internally; q1 is unit up to rounding, so compare directions' images
-    hv_ref = hq1 * np.linalg.norm(q1.astype(np.float32).astype(np.float64))
-    err = float(np.linalg.norm(hv - hv_ref) / np.linalg.norm(hv_ref))
-    mu_gpu = (a[0], a[0] ** 2 + b[0] ** 2)
-    mu_orc = (r.alpha[0], r.alpha[0] ** 2 + r.beta[0] ** 2)
-    n1, _ = OL.gauss_quadrature(a, b)
-    n2, _ = OL.gauss_quadrature(r.alpha, r.beta)
+def check(name, g, hv, a, b, nq, P, fp32_gates=True):
+    h = g["hvp_q1"]
+    idx = np.asarray(h["idx"], dtype=np.int64)
+    ref = np.asarray(h["val"]) * nq
+    e_samp = float(np.linalg.norm(hv[idx] - ref) / np.linalg.norm(ref))
+    e_norm = abs(np.linalg.norm(hv) - h["norm"] * nq) / (h["norm"] * nq)
+    e_proj = max(abs(float(np.dot(probe.signs(s, P), hv)) - p * nq) for s, p in zip(h["proj_seeds"], h["proj"]))
+    e_proj /= h["norm"] * nq
+    ra, rb = np.asarray(g["alpha"]), np.asarray(g["beta"])
+    ea = np.abs(a - ra) / np.maximum(np.abs(ra), 1e-2 * np.abs(ra).max())  # reading R14
+    eb = np.abs(b - rb) / np.abs(rb)
+    mu_g = (a[0], a[0] ** 2 + b[0] ** 2)
+    mu_o = (ra[0], ra[0] ** 2 + rb[0] ** 2)
+    n1, _ = slq.quadrature(a, b)
+    n2, _ = OL.gauss_quadrature(ra, rb)
     scale = max(abs(n2[0]), abs(n2[-1]))
-    print(f"{name} [{numerics}]: P={P} HVP rel {err:.2e}; alpha {a} vs {r.alpha}; beta {b} vs {r.beta}; "
-          f"mu1 {mu_gpu[0]:.6e}/{mu_orc[0]:.6e} mu2 {mu_gpu[1]:.6e}/{mu_orc[1]:.6e}; "
-          f"ritz {n1[0]:.6e},{n1[-1]:.6e} vs {n2[0]:.6e},{n2[-1]:.6e}; gpu {t_gpu:.0f}s total {t_all:.0f}s")
-    if numerics != "bf16x3":  # fp64-faithful passes also meet the fp32 gates
-        assert err <= 1e-4
-        assert np.all(np.abs(a - r.alpha) <= 1e-5 * np.maximum(np.abs(r.alpha), 1e-2 * np.abs(r.alpha).max()))
-        assert np.all(np.abs(b - r.beta) <= 1e-5 * np.abs(r.beta))
-    assert abs(mu_gpu[0] - mu_orc[0]) <= 1e-2 * np.sqrt(mu_orc[1])
-    assert abs(mu_gpu[1] - mu_orc[1]) <= 1e-2 * mu_orc[1]
-    assert abs(n1[0] - n2[0]) <= 2e-2 * scale and abs(n1[-1] - n2[-1]) <= 2e-2 * scale
+    er = max(abs(n1[0] - n2[0]), abs(n1[-1] - n2[-1])) / scale
+    print(f"{name}: H q1 sampled {e_samp:.2e} norm {e_norm:.2e} proj {e_proj:.2e}; alpha {ea.max():.2e} "
+          f"beta {eb.max():.2e} (m={len(a)}); mu1 {abs(mu_g[0] - mu_o[0]) / np.sqrt(mu_o[1]):.1e} "
+          f"mu2 {abs(mu_g[1] - mu_o[1]) / mu_o[1]:.1e}; extreme Ritz {n1[0]:.6e}, {n1[-1]:.6e} ({er:.1e})")
+    if fp32_gates:
+        assert e_samp <= 1e-4 and e_norm <= 1e-4 and e_proj <= 1e-3
+        assert ea.max() <= 1e-5 and eb.max() <= 1e-5
+    assert abs(mu_g[0] - mu_o[0]) <= 1e-2 * np.sqrt(mu_o[1])
+    assert abs(mu_g[1] - mu_o[1]) <= 1e-2 * mu_o[1]
+    assert er <= 2e-2
 
 
-@pytest.mark.parametrize("numerics", ["fp64", "fp64_oz"])
-def test_c3_parity_batch(numerics):
-    """fp64: DMMA; fp64_oz: the c3 GEMMs (>= 1e9 M N K) on the tcgen05 INT8 Ozaki path.  (The
-    fp32-faithful BF16X3 mode misses even the bf16 gates here -- HVP 7.1e-2, mu2 9%, extreme Ritz
-    2.6% on B200 -- because Theorem 1's round-off floor u ||g|| / (eps ||Hv||) is large on c3;
-    DESIGN.md "Numerics".)"""
-    _case("c3_parity", numerics)
+@pytest.mark.parametrize("numerics", ["fp64_oz", "fp64"])
+@pytest.mark.parametrize("eps", [1e-2, 1e-3, 1e-4])
+def test_c3_lanczos_m32(eps, numerics):
+    """fp64_oz = the bench configuration (hybrid route); fp64 = every GEMM on DMMA."""
+    g = golden("c3_parity", eps, 32, "full")
+    cfg = si.get_config("c3_parity", eps=eps, m=32)
+    hv, a, b, nq, P = gpu_run(cfg, numerics, "full", 32, eps)
+    check(f"c3_parity eps={eps:g} [{numerics}]", g, hv, a, b, nq, P)
 
 
-@pytest.mark.skipif(os.environ.get("SLQ_LARGE_TESTS") != "1", reason="set SLQ_LARGE_TESTS=1 (~60 GB host RAM)")
-@pytest.mark.parametrize("numerics", ["fp64", "fp64_oz"])
-@pytest.mark.parametrize("name", ["c4_parity", "c5_twin"])
-def test_large_parity(name, numerics):
-    _case(name, numerics)
+@pytest.mark.xfail(strict=True, raises=AssertionError,
+                   reason="BF16X3 (fp32-faithful passes) sits at Theorem 1's fp32 round-off floor u ||g|| / "
+                          "(eps ||Hv||), which is large on c3: B200 round 1 measured H q1 7.1e-2, mu2 9%, "
+                          "extreme Ritz 2.6% -- it misses the bf16 gates (DESIGN.md §5)")
+def test_c3_bf16x3_misses_the_bf16_gates():
+    g = golden("c3_parity", 1e-3, 32, "full")
+    cfg = si.get_config("c3_parity", eps=1e-3, m=32)
+    hv, a, b, nq, P = gpu_run(cfg, "bf16x3", "full", 32, 1e-3)
+    check("c3_parity eps=0.001 [bf16x3]", g, hv, a, b, nq, P, fp32_gates=False)
+
+
+def test_c3_full_vector_live_oracle():
+    """The whole 124M-entry H q_1 of the bench configuration against a live oracle evaluation."""
+    cfg = si.get_config("c3_parity", m=2)
+    hv, a, b, nq, P = gpu_run(cfg, "fp64_oz", "full", 2, cfg.eps)
+    th = si.init_params(cfg)
+    q1 = probe.rademacher_probe(cfg.probe_seed0, P)
+    ref = fdhvp.fd_hvp_step(fdhvp.make_grad_fn(cfg, si.tokens(cfg)), th, q1, cfg.eps, "exact") * nq
+    err = float(np.linalg.norm(hv - ref) / np.linalg.norm(ref))
+    print(f"c3_parity [fp64_oz] full H q1 vs live oracle: {err:.2e}")
+    assert err <= 1e-4
+
+
+@pytest.mark.parametrize("name,reorth,m", [("c4_parity", "none", 16), ("c4_parity", "full", 8), ("c5_twin", "none", 16)])
+def test_llama_large(name, reorth, m):
+    """c4: reorthogonalisation off (m = 16) and on (m = 8: the oracle's fp64 basis is 8.8 GB per
+    row) (configs[3]); c5 twin: no stored basis (configs[4]).  Bench configuration (FP64_OZ hybrid)."""
+    g = golden(name, 1e-3, m, reorth)
+    cfg = si.get_config(name, m=m)
+    hv, a, b, nq, P = gpu_run(cfg, "fp64_oz", reorth, m, cfg.eps)
+    check(f"{name} m={m} reorth={reorth} [fp64_oz]", g, hv, a, b, nq, P)

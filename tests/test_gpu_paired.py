@@ -54,9 +54,18 @@ def test_paired_grad_and_hvp(name, mode):
     assert eh <= 1e-4
 
 
-@pytest.mark.parametrize("mode", MODES)
+PAIRED_TC_XFAIL = pytest.mark.xfail(
+    strict=False, raises=AssertionError,
+    reason="SLQ_PASS_PAIRED (tcgen05 three-term bf16 splits, fp32 TMEM accumulation) misses the north star's "
+           "fp32 alpha/beta gate: B200 round 1, c2 m=32: alpha 8.8e-4 (reading R14), beta 2.1e-5 -- its HVP "
+           "(1.3e-5) meets the 1e-4 HVP gate and the bf16-model gates, not alpha/beta <= 1e-5 (DESIGN.md R14b)")
+
+
+@pytest.mark.parametrize("mode", [pytest.param(m, marks=PAIRED_TC_XFAIL) if m == "paired" else m for m in MODES])
 @pytest.mark.parametrize("name,m", [("gpt_tiny", 16), ("c2", 32)])
 def test_paired_lanczos_fp32_gates(name, m, mode):
+    """The north star's fp32 gates as every fp32-model mode is held to them: alpha per reading R14
+    and beta <= 1e-5 relative over the first 32 steps."""
     cfg = si.CONFIGS[name]
     th = si.init_params(cfg)
     tok = si.tokens(cfg)
@@ -66,15 +75,8 @@ def test_paired_lanczos_fp32_gates(name, m, mode):
     r = OL.lanczos(lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact"),
                    probe.rademacher_probe(cfg.probe_seed0, th.size), m, "full")
     scale = np.abs(r.alpha).max()
-    ea = np.abs(a - r.alpha) / np.maximum(np.abs(r.alpha), 1e-2 * scale)  # reading R14 (fp64 path gate)
+    ea = np.abs(a - r.alpha) / np.maximum(np.abs(r.alpha), 1e-2 * scale)  # reading R14
     es = np.abs(a - r.alpha) / scale                                       # relative to the spectral scale
     eb = np.abs(b - r.beta) / np.abs(r.beta)
     print(f"{name} [{mode}]: max rel alpha {ea.max():.2e} (vs spectral scale {es.max():.2e}) beta {eb.max():.2e}")
-    # The paired path's HVP error (1e-7 .. 1e-5) meets the 1e-4 HVP gate; alpha_k near zero
-    # amplifies it beyond R14's 1e-5 floor, so this mode is gated on alpha relative to the spectral
-    # scale (reading R14b).  The fp64 path meets R14 itself.  The tensor-core variant
-    # ("paired": three-term bf16 operand splits accumulated in fp32 TMEM) carries HVP 1.3e-5 on c2
-    # and drifts to 5e-5 of the spectral scale by step 32 (measured on B200): it meets the HVP
-    # gate and the bf16-model gates, not the fp32 alpha gate (R14b) -- gated at 1e-4.
-    tol_a = 1e-4 if mode == "paired" else 1e-5
-    assert es.max() <= tol_a and eb.max() <= 1e-4
+    assert ea.max() <= 1e-5 and eb.max() <= 1e-5
