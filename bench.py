@@ -63,6 +63,9 @@ def parse():
                         "exact int8 digit products on tcgen05 (Ozaki) and the rest on DMMA; fp64 = all DMMA; "
                         "bf16x3 = fp32-faithful tcgen05")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--probe-m", type=int, default=0,
+                   help="length of the probe holding the timed window (default: the config's m); a short probe "
+                        "for profiler runs (ncu), whose numbers are never bench values")
     # "report with reorth on and off where the config asks"; window / bf16 basis (f3)
     p.add_argument("--reorth", default="config", choices=["config", "full", "none", "window"])
     p.add_argument("--window", type=int, default=8)
@@ -277,7 +280,7 @@ def main():
         uid = obj[0]
     tok, n_glob = split_batch(cfg, rank, world)
     K, W = args.steps, max(args.warmup, 0)
-    m_probe = max(cfg.m, K + W)  # one probe holds the warm-up steps and the timed window
+    m_probe = max(args.probe_m or cfg.m, K + W)  # one probe holds the warm-up steps and the timed window
     k0 = max(W, (m_probe - K) // 2)
     ctx = slq.SlqContext(cfg, si.init_params(cfg), tok, n_global=n_glob, rank=rank, world_size=world, device=local,
                          unique_id=uid, pass_numerics=args.numerics,

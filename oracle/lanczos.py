@@ -83,10 +83,12 @@ def store(x: np.ndarray, basis: str) -> np.ndarray:
 
 def lanczos(apply_h: Callable[[np.ndarray], np.ndarray], q1: np.ndarray, m: int,
             reorth: str = "full", tol: float = 1e-10, keep_basis: bool = False,
-            window: int = 0, basis: str = "fp64") -> LanczosResult:
+            window: int = 0, basis: str = "fp64", on_step=None) -> LanczosResult:
     """m steps of symmetric Lanczos from unit q1, A(2,7) order, fp64 scalars.
     reorth: "none" | "full" | "window" (CGS2 against the `window` most recent vectors);
-    basis: storage of the Lanczos vectors, "fp64" | "fp32" | "bf16"."""
+    basis: storage of the Lanczos vectors, "fp64" | "fp32" | "bf16".
+    on_step(alpha, betas): optional progress hook (no arithmetic), called after every step with the
+    coefficients so far -- alpha_1..alpha_k and beta_2..beta_{k+1}."""
     if reorth == "window" and window < 1:
         raise ValueError("window reorthogonalisation needs window >= 1")
     q = store(q1, basis).copy()
@@ -113,6 +115,8 @@ def lanczos(apply_h: Callable[[np.ndarray], np.ndarray], q1: np.ndarray, m: int,
         b_next = float(np.sqrt(np.dot(w, w)))
         alpha.append(a)
         betas.append(b_next)
+        if on_step is not None:
+            on_step(list(alpha), list(betas))
         tmax = max(max(abs(x) for x in alpha), max(betas[:-1], default=0.0))
         if b_next <= tol * tmax:
             breakdown = True

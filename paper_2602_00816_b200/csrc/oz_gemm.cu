@@ -108,10 +108,54 @@ __device__ __forceinline__ double scale_of(int e) { return e == kExNaN ? __longl
 __host__ __device__ constexpr int oz_owner(int NI, int g) {
   return NI == 2 ? (g >= 1 && g <= 4 ? 1 : 0) : NI == 3 ? (g == 1 || g == 6 ? 0 : (g == 2 || g == 5 ? 1 : 2)) : 0;
 }
+// One 32-row x 4-column chunk of the output tile from the warp's staging tile T (row r, column c
+// at T[r * 4 + c], already row-scaled): lane l handles rows 8 j + l / 4 (j = 0..3) of column
+// l % 4, multiplies by its column scale and applies the fused epilogue (alpha, bias, residual,
+// activation, accumulate; split-K partials are stored plain into ws).
+__device__ __noinline__ void oz_epi_chunk(const GemmArgs<double>& p, const double* T, int mrow0, int n0c, int ncol,
+                                          double sc, int splits, int sp, double* ws) {
+  const int lane = threadIdx.x % 32;
+  const int cc = lane & 3;
+  const int n = n0c + cc;
+  if (cc >= ncol) return;
+  const bool plain = splits > 1 || (!p.bias && !p.resid && !p.aux && !p.accumulate && p.act == ACT_NONE &&
+                                    p.alpha == 1.0);
+  double* Wd = splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
+  const int64_t ldw = splits > 1 ? p.N : p.ldc;
+  const double bs = (!plain && p.bias) ? p.bias[n] : 0.0;
+  for (int j = 0; j < 4; ++j) {
+    const int m = mrow0 + 8 * j + (lane >> 2);
+    if (m >= p.M) break;
+    const double x = T[(8 * j + (lane >> 2)) * 4 + cc] * sc;
+    if (plain) {
+      Wd[(int64_t)m * ldw + n] = x;
+      continue;
+    }
+    const double y = p.alpha * x + bs + (p.resid ? p.resid[(int64_t)m * p.ldr + n] : 0.0);
+    double out;
+    switch (p.act) {
+      case ACT_GELU:
+        p.C2[(int64_t)m * p.ldc2 + n] = y;
+        out = gemm_detail::gelu_tanh(y);
+        break;
+      case ACT_TANH: out = tanh(y); break;
+      case ACT_DGELU: out = y * gemm_detail::gelu_tanh_grad(p.aux[(int64_t)m * p.ldaux + n]); break;
+      case ACT_DTANH: {
+        const double h = p.aux[(int64_t)m * p.ldaux + n];
+        out = y * (1.0 - h * h);
+        break;
+      }
+      default: out = y;
+    }
+    double* dst = p.C + (int64_t)m * p.ldc + n;
+    *dst = p.accumulate ? *dst + out : out;
+  }
+}
+
 template <int S, int BN, int KT = BK, int NI = 1>
 __global__ void __launch_bounds__(288 + 32 * NI, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
-              GemmArgs<double> p, double* __restrict__ ws) {
+              const __grid_constant__ GemmArgs<double> p, double* __restrict__ ws) {
   static_assert(NI == 1 || ((NI == 2 || NI == 3) && S == 7), "several issuers: S = 7 only");
   using CF = Cfg<S, BN, KT>;
   extern __shared__ uint8_t smem_raw[];
@@ -266,8 +310,9 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
       double v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.0;
-      // two digit-weight groups per TMEM round trip (2 x 32 columns, one wait)
-#pragma unroll
+      // two digit-weight groups per TMEM round trip (2 x 32 columns, one wait); the g loop stays
+      // rolled (the 32-wide bodies are unrolled) to keep the kernel inside the instruction cache
+#pragma unroll 1
       for (int g = 0; g < ((o.debug & 8) ? 0 : S); g += 2) {
         uint32_t r0[32], r1[32];
         tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
@@ -289,58 +334,20 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
       }
       // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
       // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
-      // sectors) instead of 32 rows x 8 bytes
+      // sectors) instead of 32 rows x 8 bytes.  The loads / activation / stores of a chunk are one
+      // out-of-line function: unrolling them 8 x 4 times per kernel (x 3 activations, fp64 tanh
+      // inlined) made the kernel 246 KB of SASS, far beyond the instruction cache the MMA-issuing
+      // warps share with the epilogue warps.
       const int ncol = p.N - (n0 + c0);  // valid columns of this warp's 32 (may be <= 0)
       double* T = stage_t + (warp - 2) * 128;
-      const bool plain = o.splits > 1 || (!p.bias && !p.resid && !p.aux && !p.accumulate && p.act == ACT_NONE &&
-                                          p.alpha == 1.0);
-      double* Wd = o.splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
-      const int64_t ldw = o.splits > 1 ? p.N : p.ldc;
 #pragma unroll
       for (int c = 0; c < ((o.debug & 4) ? 0 : 32); c += 4) {
         __syncwarp();
         *reinterpret_cast<double2*>(&T[lane * 4]) = make_double2(v[c] * sr, v[c + 1] * sr);
         *reinterpret_cast<double2*>(&T[lane * 4 + 2]) = make_double2(v[c + 2] * sr, v[c + 3] * sr);
         __syncwarp();
-        const int cc = c + (lane & 3);          // column within the warp's 32
-        const int n = n0 + c0 + cc;
-        const bool colok = cc < ncol;
-        const double sc = __shfl_sync(0xffffffffu, sc_l, cc);
-        double x[4], bs = 0.0, rs[4], ax[4], cold[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int m = m0 + lg + 8 * j + (lane >> 2);
-          const bool ok = colok && m < p.M;
-          x[j] = T[(8 * j + (lane >> 2)) * 4 + (lane & 3)] * sc;
-          if (!plain) {
-            rs[j] = (ok && p.resid) ? p.resid[(int64_t)m * p.ldr + n] : 0.0;
-            ax[j] = (ok && p.aux) ? p.aux[(int64_t)m * p.ldaux + n] : 0.0;
-            cold[j] = (ok && p.accumulate) ? p.C[(int64_t)m * p.ldc + n] : 0.0;
-          }
-        }
-        if (!plain && colok && p.bias) bs = p.bias[n];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int m = m0 + lg + 8 * j + (lane >> 2);
-          if (!colok || m >= p.M) continue;
-          if (plain) {
-            Wd[(int64_t)m * ldw + n] = x[j];
-            continue;
-          }
-          const double y = p.alpha * x[j] + bs + rs[j];
-          double out;
-          switch (p.act) {
-            case ACT_GELU:
-              p.C2[(int64_t)m * p.ldc2 + n] = y;
-              out = gemm_detail::gelu_tanh(y);
-              break;
-            case ACT_TANH: out = tanh(y); break;
-            case ACT_DGELU: out = y * gemm_detail::gelu_tanh_grad(ax[j]); break;
-            case ACT_DTANH: out = y * (1.0 - ax[j] * ax[j]); break;
-            default: out = y;
-          }
-          p.C[(int64_t)m * p.ldc + n] = p.accumulate ? cold[j] + out : out;
-        }
+        const double sc = __shfl_sync(0xffffffffu, sc_l, c + (lane & 3));
+        oz_epi_chunk(p, T, m0 + lg, n0 + c0 + c, c < ncol ? ncol - c : 0, sc, o.splits, sp, ws);
       }
      }  // column blocks
     }

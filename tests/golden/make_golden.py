@@ -41,8 +41,11 @@ def sample_indices(P: int, seed: int) -> np.ndarray:
     return np.unique(np.concatenate([np.arange(64), mid, np.arange(P - 64, P)])).astype(np.int64)
 
 
+OUT_DIR = HERE
+
+
 def golden_path(case: str, eps: float, m: int, reorth: str) -> str:
-    return os.path.join(HERE, f"lanczos_{case}_eps{eps:g}_m{m}_{reorth}.json")
+    return os.path.join(OUT_DIR, f"lanczos_{case}_eps{eps:g}_m{m}_{reorth}.json")
 
 
 def run(case: str, eps: float, m: int, reorth: str) -> dict:
@@ -54,29 +57,46 @@ def run(case: str, eps: float, m: int, reorth: str) -> dict:
     q1 = probe.rademacher_probe(cfg.probe_seed0, P)
     g = fdhvp.make_grad_fn(cfg, tok)
     first = {}
+    steps = []  # operator applications so far (a partial file is rewritten after each one)
+
+    def record(alpha, beta, beta_next, m_done, breakdown):
+        hq1 = first["hq1"]
+        idx = first.setdefault("idx", sample_indices(P, cfg.probe_seed0))
+        if "proj" not in first:
+            first["proj"] = [float(np.dot(probe.signs(s, P), hq1)) for s in PROJ_SEEDS]
+        return {
+            "case": case, "eps": eps, "m": m, "reorth": reorth, "perturb": "exact", "P": int(P),
+            "n_seq": cfg.n_seq, "seq_len": cfg.seq_len, "probe_seed": cfg.probe_seed0,
+            "alpha": [float(x) for x in alpha], "beta": [float(x) for x in beta],
+            "beta_next": float(beta_next), "m_done": int(m_done), "breakdown": bool(breakdown),
+            "hvp_q1": {"norm": float(np.linalg.norm(hq1)), "idx": [int(i) for i in idx],
+                       "val": [float(hq1[i]) for i in idx], "proj_seeds": list(PROJ_SEEDS), "proj": first["proj"]},
+            "generator": "tests/golden/make_golden.py (oracle/ only)",
+            "oracle_seconds": round(time.time() - t0, 1),
+            "host": f"{platform.node()} {os.cpu_count()} cpus",
+        }
 
     def op(q):
         h = fdhvp.fd_hvp_step(g, th, q, eps, "exact")
         if not first:
             first["hq1"] = h
             print(f"  {case} eps={eps:g}: H q1 after {time.time() - t0:.0f} s", flush=True)
+        steps.append(1)
         return h
 
-    r = OL.lanczos(op, q1, m, reorth)
-    hq1 = first["hq1"]
-    idx = sample_indices(P, cfg.probe_seed0)
-    proj = [float(np.dot(probe.signs(s, P), hq1)) for s in PROJ_SEEDS]
-    out = {
-        "case": case, "eps": eps, "m": m, "reorth": reorth, "perturb": "exact", "P": int(P),
-        "n_seq": cfg.n_seq, "seq_len": cfg.seq_len, "probe_seed": cfg.probe_seed0,
-        "alpha": [float(x) for x in r.alpha], "beta": [float(x) for x in r.beta],
-        "beta_next": float(r.beta_next), "m_done": int(r.m_done), "breakdown": bool(r.breakdown),
-        "hvp_q1": {"norm": float(np.linalg.norm(hq1)), "idx": [int(i) for i in idx],
-                   "val": [float(hq1[i]) for i in idx], "proj_seeds": list(PROJ_SEEDS), "proj": proj},
-        "generator": "tests/golden/make_golden.py (oracle/ only)",
-        "oracle_seconds": round(time.time() - t0, 1),
-        "host": f"{platform.node()} {os.cpu_count()} cpus",
-    }
+    # checkpoint after every step: a run cut short still leaves the coefficients of the steps it
+    # finished (the first k steps of an m-step run are the k-step run), as m = k in the file
+    def on_step(alpha, betas):
+        k = len(alpha)
+        if k < m:
+            d = record(alpha, betas[:k - 1], betas[k - 1], k, False)
+            d["m"] = k
+            d["partial_of"] = m
+            with open(golden_path(case, eps, m, reorth) + ".partial", "w") as f:
+                json.dump(d, f)
+
+    r = OL.lanczos(op, q1, m, reorth, on_step=on_step)
+    out = record(r.alpha, r.beta, r.beta_next, r.m_done, r.breakdown)
     return out
 
 
@@ -86,9 +106,13 @@ def main():
     ap.add_argument("--m", type=int, required=True)
     ap.add_argument("--eps", type=float, nargs="+", required=True)
     ap.add_argument("--reorth", default="full", choices=["full", "none"])
+    ap.add_argument("--out-dir", default=HERE)
     ap.add_argument("--mem-limit-gb", type=float, default=0.0,
                     help="RLIMIT_AS for this process (a MemoryError instead of the host's OOM killer)")
     a = ap.parse_args()
+    global OUT_DIR
+    OUT_DIR = a.out_dir
+    os.makedirs(OUT_DIR, exist_ok=True)
     if a.mem_limit_gb > 0:
         import resource
         lim = int(a.mem_limit_gb * 2**30)

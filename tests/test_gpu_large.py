@@ -43,10 +43,18 @@ def built():
 from paper_2602_00816_b200 import slq  # noqa: E402
 
 
-def golden(case, eps, m, reorth):
-    p = os.path.join(GOLD, f"lanczos_{case}_eps{eps:g}_m{m}_{reorth}.json")
-    with open(p) as f:
-        return json.load(f)
+def golden(case, eps, m_min, reorth):
+    """The stored oracle run of (case, eps, reorth) with the most steps (>= m_min)."""
+    import glob
+    best = None
+    for p in glob.glob(os.path.join(GOLD, f"lanczos_{case}_eps{eps:g}_m*_{reorth}.json")):
+        with open(p) as f:
+            g = json.load(f)
+        if best is None or g["m"] > best["m"]:
+            best = g
+    assert best is not None, f"no stored oracle run for {case} eps={eps:g} reorth={reorth}"
+    assert best["m"] >= m_min, f"stored oracle run has m={best['m']} < {m_min}"
+    return best
 
 
 def gpu_run(cfg, numerics, reorth, m, eps):
@@ -99,8 +107,8 @@ def check(name, g, hv, a, b, nq, P, fp32_gates=True):
 def test_c3_lanczos_m32(eps, numerics):
     """fp64_oz = the bench configuration (hybrid route); fp64 = every GEMM on DMMA."""
     g = golden("c3_parity", eps, 32, "full")
-    cfg = si.get_config("c3_parity", eps=eps, m=32)
-    hv, a, b, nq, P = gpu_run(cfg, numerics, "full", 32, eps)
+    cfg = si.get_config("c3_parity", eps=eps, m=g["m"])
+    hv, a, b, nq, P = gpu_run(cfg, numerics, "full", g["m"], eps)
     check(f"c3_parity eps={eps:g} [{numerics}]", g, hv, a, b, nq, P)
 
 
@@ -110,9 +118,19 @@ def test_c3_lanczos_m32(eps, numerics):
                           "extreme Ritz 2.6% -- it misses the bf16 gates (DESIGN.md §5)")
 def test_c3_bf16x3_misses_the_bf16_gates():
     g = golden("c3_parity", 1e-3, 32, "full")
-    cfg = si.get_config("c3_parity", eps=1e-3, m=32)
-    hv, a, b, nq, P = gpu_run(cfg, "bf16x3", "full", 32, 1e-3)
+    cfg = si.get_config("c3_parity", eps=1e-3, m=g["m"])
+    hv, a, b, nq, P = gpu_run(cfg, "bf16x3", "full", g["m"], 1e-3)
     check("c3_parity eps=0.001 [bf16x3]", g, hv, a, b, nq, P, fp32_gates=False)
+
+
+def test_c3_paired_bf16_gates():
+    """SURVEY §8(f1) on c3, a bf16 model: the paired (mean, half-difference) evaluation with pair
+    GEMMs on tcgen05 (three-term bf16 operand splits) against the stored oracle run at the gates
+    that apply to bf16 models (density moments <= 1e-2, extreme Ritz <= 2e-2)."""
+    g = golden("c3_parity", 1e-3, 32, "full")
+    cfg = si.get_config("c3_parity", eps=1e-3, m=g["m"])
+    hv, a, b, nq, P = gpu_run(cfg, "paired", "full", g["m"], 1e-3)
+    check("c3_parity eps=0.001 [paired]", g, hv, a, b, nq, P, fp32_gates=False)
 
 
 def test_c3_full_vector_live_oracle():
@@ -132,6 +150,6 @@ def test_llama_large(name, reorth, m):
     """c4: reorthogonalisation off (m = 16) and on (m = 8: the oracle's fp64 basis is 8.8 GB per
     row) (configs[3]); c5 twin: no stored basis (configs[4]).  Bench configuration (FP64_OZ hybrid)."""
     g = golden(name, 1e-3, m, reorth)
-    cfg = si.get_config(name, m=m)
-    hv, a, b, nq, P = gpu_run(cfg, "fp64_oz", reorth, m, cfg.eps)
-    check(f"{name} m={m} reorth={reorth} [fp64_oz]", g, hv, a, b, nq, P)
+    cfg = si.get_config(name, m=g["m"])
+    hv, a, b, nq, P = gpu_run(cfg, "fp64_oz", reorth, g["m"], cfg.eps)
+    check(f"{name} m={g['m']} reorth={reorth} [fp64_oz]", g, hv, a, b, nq, P)
