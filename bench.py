@@ -362,7 +362,7 @@ def main():
     dom = max(stats, key=lambda k: stats[k]["busy_ms"])
     st = stats[dom]
     t_dom = st["busy_ms"]
-    nS = 7
+    nS = 5 if cfg.param_bf16 else 7  # the library's default digit planes (slq.h oz_slices)
     if dom == "gemm_i8":
         # INT8 tensor-core products of the Ozaki fp64 GEMMs: peak = the measured bf16 SUSTAINED rate
         # (the timed region lasts seconds) x the nominal dense INT8 / BF16 ratio (4.5 / 2.25 POPS)
@@ -416,7 +416,10 @@ def main():
         "warmup": k0, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if cfg.name in WEAK else "strong",
         "vs_baseline": None, "dtype": {"fp64": "f64", "fp64_oz": "f64", "fp32": "f32", "bf16x3": "bf16x3", "bf16": "bf16", "paired": "paired-bf16x3", "paired_fp32": "paired-f32"}[args.numerics],
-        "dtype_note": {"fp64_oz": f"fp64 results; dense GEMMs with M*N*K >= {float(os.environ.get('SLQ_OZ_MIN_MNK', '1e9')):.0e} as exact int8 digit products on tcgen05 (Ozaki, S={os.environ.get('SLQ_OZ_SLICES', '7')}), the rest fp64 DMMA"}.get(args.numerics, ""),
+        "dtype_note": {"fp64_oz": f"fp64 activations and accumulation; dense GEMMs with M*N*K >= 1e9 as exact int8 "
+                                  f"digit products on tcgen05 (Ozaki, S={nS} digit planes of 7 bits per operand, "
+                                  f"{nS * (nS + 1) // 2} products; S=5 for the bf16 models, whose gates are the "
+                                  f"bf16 ones, S=7 for the fp32 models), the rest fp64 DMMA"}.get(args.numerics, ""),
         "data": "synthetic",
         "config": config_dict(args, cfg, world, n_glob),
         "s_per_lanczos_step": ms_step / 1000.0,

@@ -63,10 +63,11 @@ enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2, SLQ_PASS_PAIRE
  * (one product, fp32 accumulation).  The throughput mode of the bf16 models; its FD-HVP carries
  * Theorem 1's bf16 round-off floor and does not meet the parity gates. */
 /* SLQ_PASS_FP64_OZ: as FP64 (fp64 activations and nonlinearities), but every dense non-batched
- * GEMM runs on the tcgen05 INT8 tensor cores as exact digit products (Ozaki scheme: each operand
- * row/column scaled by a power of two and cut into S = 7 signed 7-bit digit planes; the
- * S(S+1)/2 leading products accumulate exactly in INT32 TMEM; error <~ 9 * 2^-49 K max|a| max|b|).
- * The batched causal attention GEMMs stay on the FP64 DMMA path. */
+ * GEMM with M N K >= oz_min_mnk runs on the tcgen05 INT8 tensor cores as exact digit products
+ * (Ozaki scheme: each operand row/column scaled by a power of two and cut into S signed 7-bit
+ * digit planes, S = oz_slices; the S(S+1)/2 leading products accumulate exactly in INT32 TMEM;
+ * error <~ (S + 2) 2^-7S K max|a| max|b|).  The batched causal attention GEMMs and the smaller
+ * dense GEMMs stay on the FP64 DMMA path.  Non-finite operand rows / columns give NaN outputs. */
 /* SLQ_PASS_PAIRED: the two gradient evaluations of Eq. (1) carried as (mean, half-difference)
  * pairs through ONE pass, so (g+ - g-) is never formed by subtracting rounded gradients
  * (SURVEY.md §8(f1)); non-batched pair GEMMs on tcgen05 (fp32-faithful three-term bf16 splits),
@@ -103,7 +104,9 @@ typedef struct {
    * rest run as int8 digit products.  0 = library default (1e9, the measured break-even on B200);
    * 1 puts every dense GEMM on the int8 path.  Per context (no process-global state). */
   double oz_min_mnk;
-  int32_t oz_slices;       /* SLQ_PASS_FP64_OZ digit planes S (4..7); 0 = default 7 (< 7 misses the fp32 gates) */
+  int32_t oz_slices;       /* SLQ_PASS_FP64_OZ digit planes S (4..7); 0 = default: 7 for fp32 models (param_dtype
+                            * FP32; S < 7 misses their fp32 alpha / beta gate), 5 for bf16 models (their
+                            * bf16 gates; R27) */
   /* 1: activation checkpointing (BASELINE configs[4]): each transformer block keeps only its input
    * residual stream from the forward and recomputes its forward inside its backward (bit-identical
    * gradients, +1 block forward per block, block activations for 2 blocks instead of n_layers) */

@@ -105,8 +105,14 @@ __device__ __forceinline__ double scale_of(int e) { return e == kExNaN ? __longl
 // 11), each a single issuing thread: NI = 2 -> {0, 5, 6} / {1..4} (14 + 14 products), NI = 3 ->
 // {1, 6} / {2, 5} / {0, 3, 4} (9 + 9 + 10).  One thread cannot issue 128 x 64 x 32 MMAs as fast as
 // the tensor pipe retires them; several threads can.
-__host__ __device__ constexpr int oz_owner(int NI, int g) {
-  return NI == 2 ? (g >= 1 && g <= 4 ? 1 : 0) : NI == 3 ? (g == 1 || g == 6 ? 0 : (g == 2 || g == 5 ? 1 : 2)) : 0;
+// Digit weight g has g + 1 products.  S = 7: NI = 2 -> {0, 5, 6} / {1..4} (14 + 14), NI = 3 ->
+// {1, 6} / {2, 5} / {0, 3, 4} (9 + 9 + 10); S = 6: NI = 2 -> {0, 1, 2, 5} / {3, 4} (12 + 9); S = 5:
+// NI = 2 -> {0, 1, 4} / {2, 3} (8 + 7).
+__host__ __device__ constexpr int oz_owner(int S, int NI, int g) {
+  return NI == 1   ? 0
+         : S == 7  ? (NI == 2 ? (g >= 1 && g <= 4 ? 1 : 0) : (g == 1 || g == 6 ? 0 : (g == 2 || g == 5 ? 1 : 2)))
+         : S == 6  ? (g == 3 || g == 4 ? 1 : 0)
+                   : (g == 2 || g == 3 ? 1 : 0);
 }
 // One 32-row x 4-column chunk of the output tile from the warp's staging tile T (row r, column c
 // at T[r * 4 + c], already row-scaled): lane l handles rows 8 j + l / 4 (j = 0..3) of column
@@ -156,7 +162,7 @@ template <int S, int BN, int KT = BK, int NI = 1>
 __global__ void __launch_bounds__(288 + 32 * NI, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
               const __grid_constant__ GemmArgs<double> p, double* __restrict__ ws) {
-  static_assert(NI == 1 || ((NI == 2 || NI == 3) && S == 7), "several issuers: S = 7 only");
+  static_assert(NI == 1 || (NI == 2 && S >= 5) || (NI == 3 && S == 7), "issuer split defined for S = 5..7");
   using CF = Cfg<S, BN, KT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
           if (!(o.debug & 1)) {
 #pragma unroll
             for (int g = 0; g < S; ++g) {
-              if (NI > 1 && oz_owner(NI, g) != iss) continue;
+              if (NI > 1 && oz_owner(S, NI, g) != iss) continue;
 #pragma unroll
               for (int pa = 0; pa <= g; ++pa) {
                 const int qb = g - pa;
@@ -928,8 +934,9 @@ void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
       if (wide) oz::run<4, 128>(L, a);
       else oz::run<4, 64>(L, a);
       break;
-    case 5: oz::run<5, 64>(L, a); break;
-    case 6: oz::run<6, 64>(L, a); break;
+    // S = 5 / 6 (the bf16 models' default is 5): two issuers as for S = 7
+    case 5: oz::run<5, 64, false, oz::BK, 2>(L, a); break;
+    case 6: oz::run<6, 64, false, oz::BK, 2>(L, a); break;
     default: {
       // the wide two-phase kernel when it has enough 128 x 128 tiles to fill the GPU
       static const int wide_env = getenv("SLQ_OZ_WIDE") ? atoi(getenv("SLQ_OZ_WIDE")) : 0;

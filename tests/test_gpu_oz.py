@@ -29,7 +29,7 @@ from paper_2602_00816_b200 import slq  # noqa: E402
 @pytest.mark.parametrize("M,N,K,ak,bk", [(128, 64, 64, 1, 1), (300, 70, 100, 1, 1), (2048, 768, 256, 1, 1),
                                          (2048, 256, 1024, 1, 0), (768, 256, 2048, 0, 0), (37, 203, 64, 0, 1),
                                          (1, 5, 3, 1, 1), (129, 65, 4000, 1, 1), (64, 4096, 20000, 1, 1)])
-@pytest.mark.parametrize("S", [4, 6, 7])
+@pytest.mark.parametrize("S", [4, 5, 6, 7])
 def test_oz_gemm_error_bound(M, N, K, ak, bk, S):
     """Truncated digits only: |C_oz - C| <= (S + 2) 2^-7S K 2^(e_i + f_j) (oz_gemm.cu header) and
     2^e_i < 2 max|A_i.|, so <= 4 (S + 2) 2^-7S K max|A_i.| max|B_.j|; covers ragged tiles, every
