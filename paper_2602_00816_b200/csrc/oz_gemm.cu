@@ -39,15 +39,18 @@ constexpr int BM = 128, BK = 64, UMMA_K = 32;
 
 // KT: k-tile width in bytes = int8 elements (64: SWIZZLE_64B, two MMAs per product per k-tile;
 // 32: SWIZZLE_32B, one MMA per product, twice the stages in the same shared memory)
+// NE = BN / 8 epilogue warps: four TMEM lane quadrants x BN / 32 groups of 32 columns
 template <int S, int BN, int KT = BK>
 struct Cfg {
+  static constexpr int NE = BN / 8;
+  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 128, "BN in {64, 96, 128}");
   static constexpr int A_PLANE = BM * KT, B_PLANE = BN * KT;  // bytes
   static constexpr int A_BYTES = S * A_PLANE, B_BYTES = S * B_PLANE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - 8 * 128 * 8) / STAGE_BYTES;
+  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - NE * 128 * 8) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
   static_assert(STAGES >= 2, "two stages at least");
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 8 * 128 * 8 /*epilogue*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + NE * 128 * 8 /*epilogue*/;
   static_assert(SMEM <= 232448, "dynamic shared memory per CTA");
   static constexpr int TMEM_COLS = S * BN <= 128 ? 128 : (S * BN <= 256 ? 256 : 512);
   static constexpr int NPROD = S * (S + 1) / 2;
@@ -158,8 +161,10 @@ __device__ __noinline__ void oz_epi_chunk(const GemmArgs<double>& p, const doubl
   }
 }
 
+// warps: 0 TMA producer, 1 MMA issuer 0 + TMEM allocator, 2 .. NE + 1 epilogue, NE + 2 .. NE + NI
+// the other MMA issuers
 template <int S, int BN, int KT = BK, int NI = 1>
-__global__ void __launch_bounds__(288 + 32 * NI, 1)
+__global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
               const __grid_constant__ GemmArgs<double> p, double* __restrict__ ws) {
   static_assert(NI == 1 || (NI == 2 && S >= 5) || (NI == 3 && S == 7), "issuer split defined for S = 5..7");
@@ -171,7 +176,8 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
   uint64_t* tmem_full = empty + CF::STAGES;
   uint64_t* tmem_empty = tmem_full + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-  double* stage_t = reinterpret_cast<double*>(smem + CF::STAGES * CF::STAGE_BYTES + 256);  // 8 x 32 x 4
+  double* stage_t = reinterpret_cast<double*>(smem + CF::STAGES * CF::STAGE_BYTES + 256);  // NE x 32 x 4
+  constexpr int NE = CF::NE;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + BM - 1) / BM;
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
       mbar_init(&empty[s], NI);  // one commit per issuing warp
     }
     mbar_init(tmem_full, NI);
-    mbar_init(tmem_empty, 8);  // one arrive per epilogue warp
+    mbar_init(tmem_empty, NE);  // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     asm volatile("fence.proxy.async.shared::cta;\n" ::);
   }
@@ -239,9 +245,9 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
         }
       }
     }
-  } else if (warp == 1 || warp >= 10) {
+  } else if (warp == 1 || warp >= NE + 2) {
     if (lane == 0) {  // ---- MMA issuer(s): S(S+1)/2 digit products per k-tile ----
-      const int iss = warp == 1 ? 0 : warp - 9;
+      const int iss = warp == 1 ? 0 : warp - (NE + 1);
       constexpr uint32_t idesc = make_idesc_i8(BM, BN);
       int it = 0, tl = 0;
       for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
@@ -294,50 +300,47 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
         }
       }
     }
-  } else if (warp < 10) {
-    // ---- epilogue (warps 2..9): warp w drains TMEM lanes 32 (w % 4) .. +31 (its quadrant), columns
-    // [32 h, 32 h + 32) with h = (w - 2) / 4, combining the S digit weights in fp64 ----
+  } else {
+    // ---- epilogue (warps 2 .. NE + 1): warp w drains TMEM lanes 32 (w % 4) .. +31 (its quadrant),
+    // columns [32 h, 32 h + 32) with h = (w - 2) / 4, combining the S digit weights in fp64 ----
     const int lg = (warp % 4) * 32;
+    const int c0 = ((warp - 2) / 4) * 32;
     int tl = 0;
     for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
       int m0, n0, sp, kt0, nloc;
       decode(w, m0, n0, sp, kt0, nloc);
-     for (int jb = 0; jb < BN / 64; ++jb) {  // 64-column blocks of the tile
-      const int c0 = ((warp - 2) / 4) * 32 + 64 * jb;
       // scales first (their global-load latency overlaps the wait for the accumulators):
       // lane l holds 2^f for column n0 + c0 + l and 2^e for row m0 + lg + l
       const int n_l = n0 + c0 + lane, row_l = m0 + lg + lane;
       const double sc_l = n_l < p.N ? scale_of(o.eb[n_l]) : 0.0;
       const double sr = (nloc > 0 && row_l < p.M) ? scale_of(o.ea[row_l]) : 0.0;
-      if (jb == 0) {
-        mbar_wait(tmem_full, tl & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      }
+      mbar_wait(tmem_full, tl & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       double v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.0;
       // two digit-weight groups per TMEM round trip (2 x 32 columns, one wait); the g loop stays
       // rolled (the 32-wide bodies are unrolled) to keep the kernel inside the instruction cache
+      // (more than 8 epilogue warps: one group per round trip, within the smaller register budget)
+      constexpr int GS = NE > 8 ? 1 : 2;
 #pragma unroll 1
-      for (int g = 0; g < ((o.debug & 8) ? 0 : S); g += 2) {
-        uint32_t r0[32], r1[32];
+      for (int g = 0; g < ((o.debug & 8) ? 0 : S); g += GS) {
+        uint32_t r0[32], r1[GS > 1 ? 32 : 1];
         tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
-        if (g + 1 < S) tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)((g + 1) * BN + c0), r1);
+        if (GS > 1 && g + 1 < S) tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)((g + 1) * BN + c0), r1);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
         const double w0 = exp2i(-7 * (g + 2)), w1 = exp2i(-7 * (g + 3));
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r0[i]), w0, v[i]);
-        if (g + 1 < S) {
+        if (GS > 1 && g + 1 < S) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r1[i]), w1, v[i]);
+          for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r1[GS > 1 ? i : 0]), w1, v[i]);
         }
       }
-      // accumulators drained (all column blocks): release TMEM to the next unit's MMAs
-      if (jb == BN / 64 - 1) {
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
-      }
+      // accumulators drained: release TMEM to the next unit's MMAs
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
       // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
       // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
       // sectors) instead of 32 rows x 8 bytes.  The loads / activation / stores of a chunk are one
@@ -355,7 +358,6 @@ __global__ void __launch_bounds__(288 + 32 * NI, 1)
         const double sc = __shfl_sync(0xffffffffu, sc_l, c + (lane & 3));
         oz_epi_chunk(p, T, m0 + lg, n0 + c0 + c, c < ncol ? ncol - c : 0, sc, o.splits, sp, ws);
       }
-     }  // column blocks
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -897,7 +899,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     if constexpr (W)
       k_oz_gemm_w<<<std::min(nwork, 148), 320, CfgW::SMEM, L.stream>>>(ta, tb, o, a, ws);
     else
-      k_oz_gemm<S, BN, KTN, NI><<<std::min(nwork, 148), 288 + 32 * NI, CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
+      k_oz_gemm<S, BN, KTN, NI><<<std::min(nwork, 148), 32 * (CF::NE + NI + 1), CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }
@@ -913,12 +915,16 @@ void run(const Launch& L, const GemmArgs<double>& a) {
 
 }  // namespace oz
 
-// workspace of the production configuration (BN = 64, 64-byte k-tiles; the diagnostic wide / 32-byte
-// variants size their own)
+// output tile width of the production kernel for S digit planes: the S accumulators of BN columns
+// share the 512 TMEM columns (S = 5: 5 x 96 = 480; S = 6, 7: 64)
+static int oz_bn(int S) { return S == 5 ? 96 : 64; }
+
+// workspace of the production configuration (BN = oz_bn(S), 64-byte k-tiles; the diagnostic wide /
+// 32-byte variants size their own)
 size_t oz_ws_bytes(int M, int N, int K, int S) {
   using namespace oz;
   const int Kp = (int)ceil_div(K, 16) * 16, nk = (int)ceil_div(K, BK);
-  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, 64));
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, oz_bn(S)));
   int splits, ktps;
   plan_splits(S, tiles, nk, BK, splits, ktps);
   const int nkb = (int)ceil_div(K, kColK);
@@ -934,8 +940,8 @@ void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
       if (wide) oz::run<4, 128>(L, a);
       else oz::run<4, 64>(L, a);
       break;
-    // S = 5 / 6 (the bf16 models' default is 5): two issuers as for S = 7
-    case 5: oz::run<5, 64, false, oz::BK, 2>(L, a); break;
+    // S = 5 / 6 (the bf16 models' default is 5): two issuers as for S = 7; S = 5 on 128 x 96 tiles
+    case 5: oz::run<5, 96, false, oz::BK, 2>(L, a); break;
     case 6: oz::run<6, 64, false, oz::BK, 2>(L, a); break;
     default: {
       // the wide two-phase kernel when it has enough 128 x 128 tiles to fill the GPU

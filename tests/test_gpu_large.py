@@ -139,6 +139,35 @@ def test_c3_paired_bf16_gates():
     check("c3_parity eps=0.001 [paired]", g, hv, a, b, nq, P, fp32_gates=False)
 
 
+@pytest.mark.parametrize("reorth,window,basis", [("full", 0, "bf16"), ("window", 8, "fp32"), ("window", 32, "bf16"),
+                                                 ("none", 0, "fp32")])
+def test_c3_basis_and_window_study(reorth, window, basis):
+    """SURVEY §8(f3) on c3 (the Lanczos basis stored in bf16; P:426-427 sliding-
+    window reorthogonalisation): each variant in the bench configuration against the stored
+    full-reorthogonalisation fp64-basis oracle run, at the bf16 gates, with the ghost count
+    (R18: single-linkage clusters at 2e-3 of the spectral scale)."""
+    g = golden("c3_parity", 1e-3, 32, "full")
+    m = g["m"]
+    cfg = si.get_config("c3_parity", eps=1e-3, m=m)
+    th = si.init_params(cfg)
+    with slq.SlqContext(cfg, th, si.tokens(cfg), reorth=reorth, window=window, basis=basis, max_steps=m,
+                        pass_numerics="fp64_oz") as c:
+        a, b = c.lanczos(cfg.probe_seed0, m)
+    nodes, _ = slq.quadrature(a, b)
+    ra, rb = np.asarray(g["alpha"]), np.asarray(g["beta"])
+    n2, _ = OL.gauss_quadrature(ra, rb)
+    scale = max(abs(n2[0]), abs(n2[-1]))
+    _, n_ghost, split = slq.ghost_clusters(nodes, 2e-3 * scale)
+    _, n_ghost_ref, _ = slq.ghost_clusters(n2, 2e-3 * scale)
+    er = max(abs(nodes[0] - n2[0]), abs(nodes[-1] - n2[-1])) / scale
+    mu2_g, mu2_o = a[0] ** 2 + b[0] ** 2, ra[0] ** 2 + rb[0] ** 2
+    e1 = abs(a[0] - ra[0]) / np.sqrt(mu2_o)
+    e2 = abs(mu2_g - mu2_o) / mu2_o
+    print(f"c3_parity m={m} reorth={reorth} window={window} basis={basis}: extreme Ritz {er:.2e} mu1 {e1:.2e} "
+          f"mu2 {e2:.2e}; ghost clusters {n_ghost} (oracle full fp64: {n_ghost_ref}), max split {split:.2e}")
+    assert er <= 2e-2 and e1 <= 1e-2 and e2 <= 1e-2
+
+
 def test_c3_full_vector_live_oracle():
     """The whole 124M-entry H q_1 (FP64_OZ hybrid at S = 7) against a live oracle evaluation."""
     cfg = si.get_config("c3_parity", m=2)
