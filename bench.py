@@ -62,6 +62,9 @@ def parse():
                    help="gradient-pass arithmetic: fp64_oz (default) = fp64 passes with the large GEMMs as "
                         "exact int8 digit products on tcgen05 (Ozaki) and the rest on DMMA; fp64 = all DMMA; "
                         "bf16x3 = fp32-faithful tcgen05")
+    p.add_argument("--oz-slices", type=int, default=0,
+                   help="FP64_OZ digit planes S (0: the library default, 5 for bf16 models, 7 for fp32 models)")
+    p.add_argument("--act-ckpt", action="store_true", help="activation checkpointing (BASELINE configs[4])")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--probe-m", type=int, default=0,
                    help="length of the probe holding the timed window (default: the config's m); a short probe "
@@ -211,6 +214,8 @@ def config_dict(args, cfg, world, n_glob):
                         + f", eps={cfg.eps}, Lanczos m={cfg.m} {reorth_label(args, cfg)}",
             "global_batch": n_glob, "seq_len": cfg.seq_len, "parallelism": f"fsdp{world}",
             "pass_numerics": args.numerics, "perturb": "exact",
+            "oz_slices": (args.oz_slices or (5 if cfg.param_bf16 else 7)) if args.numerics == "fp64_oz" else None,
+            "act_ckpt": bool(args.act_ckpt),
             "l2": "no flush: per-step working set (theta+-, g+- fp64, activations, basis) > 0.5 GB > 126 MB L2"}
 
 
@@ -285,7 +290,8 @@ def main():
     ctx = slq.SlqContext(cfg, si.init_params(cfg), tok, n_global=n_glob, rank=rank, world_size=world, device=local,
                          unique_id=uid, pass_numerics=args.numerics,
                          reorth=reorth_of(args, cfg), window=args.window if args.reorth == "window" else 0,
-                         basis=args.basis, max_steps=m_probe, perturb="exact")
+                         basis=args.basis, max_steps=m_probe, perturb="exact", oz_slices=args.oz_slices,
+                         act_ckpt=args.act_ckpt)
     stream = torch.cuda.ExternalStream(ctx.stream)
 
     def barrier():
@@ -362,7 +368,7 @@ def main():
     dom = max(stats, key=lambda k: stats[k]["busy_ms"])
     st = stats[dom]
     t_dom = st["busy_ms"]
-    nS = 5 if cfg.param_bf16 else 7  # the library's default digit planes (slq.h oz_slices)
+    nS = args.oz_slices or (5 if cfg.param_bf16 else 7)  # the library's default digit planes (slq.h oz_slices)
     if dom == "gemm_i8":
         # INT8 tensor-core products of the Ozaki fp64 GEMMs: peak = the measured bf16 SUSTAINED rate
         # (the timed region lasts seconds) x the nominal dense INT8 / BF16 ratio (4.5 / 2.25 POPS)

@@ -57,6 +57,42 @@ def test_quartic_closed_form():
         assert abs(bias - eps ** 2 / 6 * np.linalg.norm(6 * a * v ** 3)) <= 1e-12 * np.linalg.norm(ref)
 
 
+def test_theorem1_bound_pins():
+    """oracle.fdhvp.theorem1_bound (Theorem 1): with eps_mach = 0 it is exactly the FD
+    bias of the separable quartic (whose fourth derivative is constant, so the eps^2/6 term is the
+    whole truncation error); with fp32 gradient passes on c1 the bound's round-off term
+    eps_mach ||g|| / eps dominates at small eps and, with the measured bias constant, bounds the
+    measured FD error within a small factor."""
+    rng = np.random.default_rng(7)
+    n = 300
+    a = rng.uniform(0.5, 2.0, n)
+    th = rng.standard_normal(n)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    grad = lambda x: a * np.asarray(x, dtype=np.float64) ** 3
+    for eps in (3e-1, 1e-1, 3e-2):
+        hv = fdhvp.fd_hvp_step(grad, th, v, eps, mode="exact")
+        bias = np.linalg.norm(hv - 3 * a * th ** 2 * v)
+        bound = fdhvp.theorem1_bound(eps, 0.0, np.linalg.norm(grad(th)), np.linalg.norm(6 * a * v ** 3))
+        assert abs(bound - bias) <= 1e-11 * np.linalg.norm(hv)  # (bias is a difference of O(1) vectors)
+    # c1 with fp32 passes at fp32 perturbed points: error vs the fp64 FD-HVP at the same points
+    cfg = si.CONFIGS["c1"]
+    theta = si.init_params(cfg)
+    batch = si.mlp_data(cfg)
+    g64 = fdhvp.make_grad_fn(cfg, batch)
+    g32 = fdhvp.make_grad_fn(cfg, batch, dt=np.float32)
+    q = si.random_vector(theta.size, 11).astype(np.float64)
+    q /= np.linalg.norm(q)
+    gnorm = float(np.linalg.norm(g64(theta)))
+    u32 = float(np.finfo(np.float32).eps) / 2
+    for eps in (1e-3, 1e-4):
+        ref = fdhvp.fd_hvp_step(g64, theta, q, eps, "param_dtype")
+        err = float(np.linalg.norm(fdhvp.fd_hvp_step(g32, theta, q, eps, "param_dtype") - ref))
+        roundoff = fdhvp.theorem1_bound(eps, u32, gnorm, 0.0)  # the eps_mach ||g|| / eps term alone
+        print(f"c1 fp32 passes eps={eps:g}: FD error {err:.3e}, Theorem 1 round-off term {roundoff:.3e}")
+        assert 0.05 * roundoff <= err <= 20 * roundoff
+
+
 def _round_f32_exact(x: Fraction) -> np.float32:
     """Brute-force correct rounding of a rational to fp32 (ties to even)."""
     c = np.float32(float(x))
