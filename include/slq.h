@@ -72,7 +72,8 @@ enum { SLQ_PASS_FP64 = 0, SLQ_PASS_FP32 = 1, SLQ_PASS_BF16X3 = 2, SLQ_PASS_PAIRE
  * pairs through ONE pass, so (g+ - g-) is never formed by subtracting rounded gradients
  * (SURVEY.md §8(f1)); non-batched pair GEMMs on tcgen05 (fp32-faithful three-term bf16 splits),
  * nonlinear steps evaluated at both points in fp64.  SLQ_PASS_PAIRED_FP32: same with fp32 SIMT
- * GEMMs.  GPT arch, world_size 1. */
+ * GEMMs.  GPT and Llama archs, any world size (FSDP: the mean and the half-difference are gathered
+ * and reduce-scattered as two streams of per-unit collectives). */
 /* Lanczos reorthogonalisation: NONE = three-term recurrence with three
  * rotating vectors and no stored basis; FULL = CGS2 against every stored vector; WINDOW = CGS2
  * against the reorth_window most recent vectors q_{k-r+1} .. q_k (ring buffer of r rows;

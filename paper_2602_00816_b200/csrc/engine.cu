@@ -153,6 +153,7 @@ struct PassExec {
   std::unique_ptr<Runner<T>> runner;
   LocalIO<T> lio;
   FsdpIO<T>* fio = nullptr;
+  FsdpIO<T>* fio2 = nullptr;  // paired evaluation with FSDP: the half-difference (thetatil, gtil)
   struct Graph {
     const void* th;
     void* g;
@@ -185,8 +186,9 @@ struct PassExec {
   }
   // FSDP: this executor's collectives go through f (host-synchronous loopback collectives cannot
   // be captured, so such a pass stays eager)
-  void attach(FsdpIO<T>* f) {
+  void attach(FsdpIO<T>* f, FsdpIO<T>* f2 = nullptr) {
     fio = f;
+    fio2 = f2;
     if (f->comm->host_sync()) use_graphs = false;
   }
   ~PassExec() {
@@ -199,6 +201,18 @@ struct PassExec {
 
   void eager(const T* th, T* g, double* loss_dev) {
     if (runner->paired()) {
+      if (fio) {
+        fio->shard = th;
+        fio->gshard = g;
+        fio2->shard = lio2.shard;
+        fio2->gshard = lio2.gshard;
+        fio->begin_pass();
+        fio2->begin_pass();
+        runner->fwd_bwd_pair(*fio, *fio2, loss_dev);
+        fio->end_pass();
+        fio2->end_pass();
+        return;
+      }
       lio.shard = th;
       lio.gshard = g;
       runner->fwd_bwd_pair(lio, lio2, loss_dev);
@@ -362,17 +376,13 @@ struct EngineT : Engine {
     }
     SLQ_CUDA(cudaMallocHost(&hstage, (64 + 2 * (size_t)(max_steps + 1)) * sizeof(double)));
     paired_ = d.pass_numerics == SLQ_PASS_PAIRED || d.pass_numerics == SLQ_PASS_PAIRED_FP32;
-    if (paired_ && comm) throw Error(SLQ_EUNSUPPORTED, "paired evaluation with world_size > 1 is not implemented");
     // one pass evaluates both points in the paired modes: nothing to run concurrently
     dual = !paired_ && getenv("SLQ_SERIAL_PASSES") == nullptr;
     const int nexec = dual ? 2 : 1;
-    for (int i = 0; i < nexec; ++i) {
-      pe[i].reset(new PassExec<T>(d, plan, b, L, i > 0, paired_));
-      if (!comm) continue;
-      FsdpIO<T>& f = fio[i];
+    auto make_fio = [&](FsdpIO<T>& f, int color, cudaStream_t s) {
       f.plan = &plan;
-      f.comm = comm->split(i);
-      f.s = pe[i]->L.stream;
+      f.comm = comm->split(color);
+      f.s = s;
       int64_t mx = 0;
       for (const UnitPlan& u : plan.units) mx = std::max(mx, u.padded);
       f.pbuf0 = dalloc<T>(plan.units[0].padded);
@@ -382,7 +392,15 @@ struct EngineT : Engine {
         f.gb[k] = dalloc<T>(mx);
       }
       f.init();
-      pe[i]->attach(&f);
+    };
+    for (int i = 0; i < nexec; ++i) {
+      pe[i].reset(new PassExec<T>(d, plan, b, L, i > 0, paired_));
+      if (!comm) continue;
+      // paired: one executor, two FSDP streams of collectives -- the mean (theta, gbar) and the
+      // half-difference (thetatil = eta v, gtil), each with its own buffers and communicator
+      make_fio(fio[i], i, pe[i]->L.stream);
+      if (paired_) make_fio(fio[1], 1, pe[i]->L.stream);
+      pe[i]->attach(&fio[i], paired_ ? &fio[1] : nullptr);
     }
     if (dual) {
       SLQ_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
@@ -879,7 +897,7 @@ void plan_memory(const slq_model_desc& d, int world, int n_local, int64_t* out) 
   if (world > 1) {
     int64_t mx = 0;
     for (const UnitPlan& u : plan.units) mx = std::max(mx, u.padded);
-    out[SLQ_MEM_FSDP] = nexec * esz * (2 * plan.units[0].padded + 4 * mx);
+    out[SLQ_MEM_FSDP] = (paired ? 2 : nexec) * esz * (2 * plan.units[0].padded + 4 * mx);  // paired: mean + diff
   }
   HostBatch hb;
   if (d.arch == SLQ_ARCH_MLP) {

@@ -176,6 +176,117 @@ __global__ void k_pair_cols2(const double* __restrict__ part, int nparts, int nq
   }
 }
 
+// ---- RMSNorm (Llama): one warp per row; stats[row] = (r+, r-), y+- = x+- r+- g+- ----
+__global__ void k_prms_fwd(const float* __restrict__ xm, const float* __restrict__ xd, const float* __restrict__ gm,
+                           const float* __restrict__ gd, float* __restrict__ ym, float* __restrict__ yd,
+                           double2* __restrict__ stats, int rows, int D, double eps) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  if (row >= rows) return;
+  const int64_t o = (int64_t)row * D;
+  double sp = 0, sq = 0;
+  for (int c = lane; c < D; c += kWarp) {
+    const double xp = (double)xm[o + c] + xd[o + c], xq = (double)xm[o + c] - xd[o + c];
+    sp += xp * xp;
+    sq += xq * xq;
+  }
+  const double rp = 1.0 / sqrt(wsum(sp) / D + eps), rq = 1.0 / sqrt(wsum(sq) / D + eps);
+  for (int c = lane; c < D; c += kWarp) {
+    const double a = xm[o + c], b = xd[o + c], g0 = gm[c], g1 = gd[c];
+    store_pair(ym, yd, o + c, (a + b) * rp * (g0 + g1), (a - b) * rq * (g0 - g1));
+  }
+  if (lane == 0) stats[row] = make_double2(rp, rq);
+}
+
+// dx+- = r+- (h+- - x+- r+-^2 mean(h+- x+-)) (+ dres+-), h = dy g
+__global__ void k_prms_bwd(const float* __restrict__ dym, const float* __restrict__ dyd, const float* __restrict__ xm,
+                           const float* __restrict__ xd, const double2* __restrict__ stats, const float* __restrict__ gm,
+                           const float* __restrict__ gd, const float* __restrict__ rm_, const float* __restrict__ rd_,
+                           float* __restrict__ dxm, float* __restrict__ dxd, int rows, int D) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int lane = threadIdx.x % kWarp;
+  if (row >= rows) return;
+  const int64_t o = (int64_t)row * D;
+  const double2 s = stats[row];
+  double ap = 0, aq = 0;
+  for (int c = lane; c < D; c += kWarp) {
+    const double x0 = xm[o + c], x1 = xd[o + c], d0 = dym[o + c], d1 = dyd[o + c], g0 = gm[c], g1 = gd[c];
+    ap += (d0 + d1) * (g0 + g1) * (x0 + x1);
+    aq += (d0 - d1) * (g0 - g1) * (x0 - x1);
+  }
+  ap = wsum(ap) / D;
+  aq = wsum(aq) / D;
+  for (int c = lane; c < D; c += kWarp) {
+    const double x0 = xm[o + c], x1 = xd[o + c], d0 = dym[o + c], d1 = dyd[o + c], g0 = gm[c], g1 = gd[c];
+    double vp = s.x * ((d0 + d1) * (g0 + g1) - (x0 + x1) * s.x * s.x * ap);
+    double vq = s.y * ((d0 - d1) * (g0 - g1) - (x0 - x1) * s.y * s.y * aq);
+    if (rm_) {
+      const double r0 = rm_[o + c], r1 = rd_[o + c];
+      vp += r0 + r1;
+      vq += r0 - r1;
+    }
+    store_pair(dxm, dxd, o + c, vp, vq);
+  }
+}
+
+// RMSNorm gains: column sums over rows of dy+- x+- r+- (fp64), two stages
+__global__ void k_prms_param1(const float* __restrict__ dym, const float* __restrict__ dyd, const float* __restrict__ xm,
+                              const float* __restrict__ xd, const double2* __restrict__ stats, double* __restrict__ part,
+                              int rows, int cols, int rpb) {
+  __shared__ double s[2][8][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int c = blockIdx.x * 32 + tx;
+  const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
+  double gp = 0, gq = 0;
+  if (c < cols) {
+    for (int r = r0 + ty; r < r1; r += 8) {
+      const int64_t i = (int64_t)r * cols + c;
+      const double2 st = stats[r];
+      const double d0 = dym[i], d1 = dyd[i], x0 = xm[i], x1 = xd[i];
+      gp += (d0 + d1) * (x0 + x1) * st.x;
+      gq += (d0 - d1) * (x0 - x1) * st.y;
+    }
+  }
+  s[0][ty][tx] = gp;
+  s[1][ty][tx] = gq;
+  __syncthreads();
+  if (ty < 2 && c < cols) {
+    double acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += s[ty][i][tx];
+    part[((int64_t)blockIdx.y * 2 + ty) * cols + c] = acc;
+  }
+}
+
+// ---- SwiGLU (Llama): ab = [a | b] per row (gate | up, 2F wide), f = silu(a) b ----
+__device__ __forceinline__ double sigm_d(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+__global__ void k_pswiglu_fwd(const float* __restrict__ abm, const float* __restrict__ abd, float* __restrict__ fm,
+                              float* __restrict__ fd, int rows, int F) {
+  const int64_t n = (int64_t)rows * F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / F, j = i % F, ia = r * 2 * F + j, ib = ia + F;
+    const double ap = (double)abm[ia] + abd[ia], aq = (double)abm[ia] - abd[ia];
+    const double bp = (double)abm[ib] + abd[ib], bq = (double)abm[ib] - abd[ib];
+    store_pair(fm, fd, i, ap * sigm_d(ap) * bp, aq * sigm_d(aq) * bq);
+  }
+}
+
+__global__ void k_pswiglu_bwd(const float* __restrict__ dfm, const float* __restrict__ dfd, const float* __restrict__ abm,
+                              const float* __restrict__ abd, float* __restrict__ dabm, float* __restrict__ dabd, int rows,
+                              int F) {
+  const int64_t n = (int64_t)rows * F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / F, j = i % F, ia = r * 2 * F + j, ib = ia + F;
+    const double ap = (double)abm[ia] + abd[ia], aq = (double)abm[ia] - abd[ia];
+    const double bp = (double)abm[ib] + abd[ib], bq = (double)abm[ib] - abd[ib];
+    const double dp = (double)dfm[i] + dfd[i], dq = (double)dfm[i] - dfd[i];
+    const double sp = sigm_d(ap), sq = sigm_d(aq);
+    store_pair(dabm, dabd, ia, dp * bp * sp * (1.0 + ap * (1.0 - sp)), dq * bq * sq * (1.0 + aq * (1.0 - sq)));
+    store_pair(dabm, dabd, ib, dp * ap * sp, dq * aq * sq);
+  }
+}
+
 // ---- GELU (tanh form) ----
 __device__ __forceinline__ double gelu_d(double u) {
   const double c = 0.7978845608028654;
@@ -368,6 +479,38 @@ void pair_layernorm_params(const Launch& L, CPair dy, CPair x, const double4* st
   double* part = (double*)L.ws->get(sizeof(double) * 4 * (size_t)rblocks * cols, L.stream);
   PLAUNCH(KC_NORM, dim3(cblocks, rblocks), 256, k_pln_param1, dy.m, dy.d, x.m, x.d, stats, part, rows, cols, rpb);
   PLAUNCH(KC_NORM, (int)ceil_div(cols, 128), 128, k_pair_cols2, part, rblocks, 4, cols, dg.m, dg.d, db.m, db.d, false);
+}
+
+void pair_rmsnorm_fwd(const Launch& L, CPair x, CPair g, Pair y, double2* stats, int rows, int D, double eps) {
+  if (rows == 0) return;
+  PLAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_prms_fwd, x.m, x.d, g.m, g.d, y.m, y.d, stats, rows, D, eps);
+}
+void pair_rmsnorm_bwd(const Launch& L, CPair dy, CPair x, const double2* stats, CPair g, CPair dres, Pair dx, int rows,
+                      int D) {
+  if (rows == 0) return;
+  PLAUNCH(KC_NORM, (int)ceil_div(rows, 8), 256, k_prms_bwd, dy.m, dy.d, x.m, x.d, stats, g.m, g.d, dres.m, dres.d,
+          dx.m, dx.d, rows, D);
+}
+void pair_rmsnorm_params(const Launch& L, CPair dy, CPair x, const double2* stats, Pair dg, int rows, int cols) {
+  if (cols == 0) return;
+  const int cblocks = (int)ceil_div(cols, 32);
+  int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), ceil_div(2 * 148, cblocks)));
+  const int rpb = (int)ceil_div(std::max(rows, 1), rblocks);
+  rblocks = (int)ceil_div(std::max(rows, 1), rpb);
+  double* part = (double*)L.ws->get(sizeof(double) * 2 * (size_t)rblocks * cols, L.stream);
+  PLAUNCH(KC_NORM, dim3(cblocks, rblocks), 256, k_prms_param1, dy.m, dy.d, x.m, x.d, stats, part, rows, cols, rpb);
+  PLAUNCH(KC_NORM, (int)ceil_div(cols, 128), 128, k_pair_cols2, part, rblocks, 2, cols, dg.m, dg.d, (float*)nullptr,
+          (float*)nullptr, false);
+}
+void pair_swiglu_fwd(const Launch& L, CPair ab, Pair f, int rows, int F) {
+  const int64_t n = (int64_t)rows * F;
+  if (n == 0) return;
+  PLAUNCH(KC_ELEM, grid_for(n, 256), 256, k_pswiglu_fwd, ab.m, ab.d, f.m, f.d, rows, F);
+}
+void pair_swiglu_bwd(const Launch& L, CPair df, CPair ab, Pair dab, int rows, int F) {
+  const int64_t n = (int64_t)rows * F;
+  if (n == 0) return;
+  PLAUNCH(KC_ELEM, grid_for(n, 256), 256, k_pswiglu_bwd, df.m, df.d, ab.m, ab.d, dab.m, dab.d, rows, F);
 }
 
 void pair_gelu_fwd(const Launch& L, CPair u, Pair y, int64_t n) {

@@ -46,6 +46,12 @@ void pair_layernorm_bwd(const Launch& L, CPair dy, CPair x, const double4* stats
                         int rows, int D);
 void pair_layernorm_params(const Launch& L, CPair dy, CPair x, const double4* stats, Pair dg, Pair db, int rows,
                            int cols);
+void pair_rmsnorm_fwd(const Launch& L, CPair x, CPair g, Pair y, double2* stats, int rows, int D, double eps);
+void pair_rmsnorm_bwd(const Launch& L, CPair dy, CPair x, const double2* stats, CPair g, CPair dres, Pair dx, int rows,
+                      int D);
+void pair_rmsnorm_params(const Launch& L, CPair dy, CPair x, const double2* stats, Pair dg, int rows, int cols);
+void pair_swiglu_fwd(const Launch& L, CPair ab, Pair f, int rows, int F);
+void pair_swiglu_bwd(const Launch& L, CPair df, CPair ab, Pair dab, int rows, int F);
 void pair_gelu_fwd(const Launch& L, CPair u, Pair y, int64_t n);
 void pair_gelu_bwd(const Launch& L, CPair dy, CPair u, Pair du, int64_t n);
 void pair_softmax_causal_fwd(const Launch& L, Pair S, int64_t rows, int Tn);

@@ -1,6 +1,6 @@
 """Paired (mean, half-difference) evaluation of Eq. (1) on the GPU.
 
-One pass carries both gradient evaluations as pairs, so g+ - g- is never formed from rounded
+GPT and Llama.  One pass carries both gradient evaluations as pairs, so g+ - g- is never formed from rounded
 gradients; with fp32-faithful arithmetic (tcgen05 three-term splits, or fp32 SIMT) it must meet
 the FP32 gates of the north star against the fp64 oracle (exact perturbed points): HVP relative
 L2 <= 1e-4 and alpha/beta <= 1e-5 over the first 32 Lanczos steps.
@@ -29,7 +29,7 @@ MODES = ["paired", "paired_fp32"]
 
 
 @pytest.mark.parametrize("mode", MODES)
-@pytest.mark.parametrize("name", ["gpt_tiny", "gpt_tiny_tied", "c2"])
+@pytest.mark.parametrize("name", ["gpt_tiny", "gpt_tiny_tied", "llama_tiny", "c2"])
 def test_paired_grad_and_hvp(name, mode):
     cfg = si.CONFIGS[name]
     th = si.init_params(cfg)
@@ -62,7 +62,7 @@ PAIRED_TC_XFAIL = pytest.mark.xfail(
 
 
 @pytest.mark.parametrize("mode", [pytest.param(m, marks=PAIRED_TC_XFAIL) if m == "paired" else m for m in MODES])
-@pytest.mark.parametrize("name,m", [("gpt_tiny", 16), ("c2", 32)])
+@pytest.mark.parametrize("name,m", [("gpt_tiny", 16), ("llama_tiny", 16), ("c2", 32)])
 def test_paired_lanczos_fp32_gates(name, m, mode):
     """The north star's fp32 gates as every fp32-model mode is held to them: alpha per reading R14
     and beta <= 1e-5 relative over the first 32 steps."""
