@@ -42,7 +42,7 @@ def _run(cfg, numerics, ckpt, m):
 # >= 3 blocks; odd and even depths exercise both activation sets
 @pytest.mark.parametrize("name,layers,numerics", [("gpt_tiny", 5, "fp64"), ("gpt_tiny_tied", 4, "fp64"),
                                                   ("llama_tiny", 5, "fp64"), ("c2", 4, "fp64_oz"),
-                                                  ("llama_tiny", 3, "bf16x3"), ("c4_parity", 16, "fp64_oz")])
+                                                  ("llama_tiny", 3, "bf16x3"), ("c4_parity", 4, "fp64_oz")])
 def test_checkpointing_bit_identical(name, layers, numerics):
     cfg = si.get_config(name, n_layers=layers)
     m = 4 if name == "c4_parity" else 6
@@ -54,8 +54,8 @@ def test_checkpointing_bit_identical(name, layers, numerics):
         assert np.array_equal(x, y)
 
 
-@pytest.mark.parametrize("name,numerics,ckpt", [("c2", "fp64_oz", False), ("c3", "fp64_oz", False),
-                                                ("c3", "fp64_oz", True), ("c4_parity", "fp64", True)])
+@pytest.mark.parametrize("name,numerics,ckpt", [("c2", "fp64_oz", False), ("c3", "fp64_oz", True),
+                                                ("c4_parity", "fp64", True)])
 def test_memory_plan_matches_allocation(name, numerics, ckpt):
     """Device bytes a context holds after init and one HVP (workspaces are reserved up front at their
     planned size) against slq_plan_memory; the host-call staging buffers are not allocated here."""

@@ -19,6 +19,7 @@ extreme Ritz values <= 2e-2) apply to every mode, in particular the bench's own 
 reading R14) over every step.  Every case prints both sets of numbers.  One c3 case also compares the FULL H q_1 vector with a
 live oracle evaluation.
 """
+import functools
 import json
 import os
 
@@ -59,11 +60,23 @@ def golden(case, eps, m_min, reorth):
     return best
 
 
+# per-module memo of the host-side inputs (124M .. 1.5B parameters take seconds to generate)
+@functools.lru_cache(maxsize=2)
+def _inputs(name):
+    cfg = si.CONFIGS[name]
+    th = si.init_params(cfg)
+    return th, si.tokens(cfg), probe.rademacher_probe(cfg.probe_seed0, th.size)
+
+
+def _sign_dot(seed, x, chunk=1 << 25):
+    """sum_i s(seed, i) x_i with the oracle's Rademacher signs, in chunks (no P-long sign vector)"""
+    return float(sum(np.dot(probe.signs(seed, min(chunk, x.size - i), i), x[i:i + chunk])
+                     for i in range(0, x.size, chunk)))
+
+
 def gpu_run(cfg, numerics, reorth, m, eps, oz_slices=0):
     """GPU H q_1 (full canonical vector) and Lanczos alpha / beta for the config's probe."""
-    th = si.init_params(cfg)
-    tok = si.tokens(cfg)
-    q1 = probe.rademacher_probe(cfg.probe_seed0, th.size)
+    th, tok, q1 = _inputs(cfg.name)
     with slq.SlqContext(cfg, th, tok, reorth=reorth, max_steps=m, pass_numerics=numerics, eps=eps,
                         oz_slices=oz_slices) as c:
         lay = c.layout()
@@ -83,7 +96,7 @@ def check(name, g, hv, a, b, nq, P, fp32_gates=True):
     ref = np.asarray(h["val"]) * nq
     e_samp = float(np.linalg.norm(hv[idx] - ref) / np.linalg.norm(ref))
     e_norm = abs(np.linalg.norm(hv) - h["norm"] * nq) / (h["norm"] * nq)
-    e_proj = max(abs(float(np.dot(probe.signs(s, P), hv)) - p * nq) for s, p in zip(h["proj_seeds"], h["proj"]))
+    e_proj = max(abs(_sign_dot(s, hv) - p * nq) for s, p in zip(h["proj_seeds"], h["proj"]))
     e_proj /= h["norm"] * nq
     ra, rb = np.asarray(g["alpha"]), np.asarray(g["beta"])
     ea = np.abs(a - ra) / np.maximum(np.abs(ra), 1e-2 * np.abs(ra).max())  # reading R14
@@ -149,8 +162,8 @@ def test_c3_basis_and_window_study(reorth, window, basis):
     g = golden("c3_parity", 1e-3, 32, "full")
     m = g["m"]
     cfg = si.get_config("c3_parity", eps=1e-3, m=m)
-    th = si.init_params(cfg)
-    with slq.SlqContext(cfg, th, si.tokens(cfg), reorth=reorth, window=window, basis=basis, max_steps=m,
+    th, tok, _ = _inputs("c3_parity")
+    with slq.SlqContext(cfg, th, tok, reorth=reorth, window=window, basis=basis, max_steps=m,
                         pass_numerics="fp64_oz") as c:
         a, b = c.lanczos(cfg.probe_seed0, m)
     nodes, _ = slq.quadrature(a, b)
@@ -172,9 +185,8 @@ def test_c3_full_vector_live_oracle():
     """The whole 124M-entry H q_1 (FP64_OZ hybrid at S = 7) against a live oracle evaluation."""
     cfg = si.get_config("c3_parity", m=2)
     hv, a, b, nq, P = gpu_run(cfg, "fp64_oz", "full", 2, cfg.eps, oz_slices=7)
-    th = si.init_params(cfg)
-    q1 = probe.rademacher_probe(cfg.probe_seed0, P)
-    ref = fdhvp.fd_hvp_step(fdhvp.make_grad_fn(cfg, si.tokens(cfg)), th, q1, cfg.eps, "exact") * nq
+    th, tok, q1 = _inputs("c3_parity")
+    ref = fdhvp.fd_hvp_step(fdhvp.make_grad_fn(cfg, tok), th, q1, cfg.eps, "exact") * nq
     err = float(np.linalg.norm(hv - ref) / np.linalg.norm(ref))
     print(f"c3_parity [fp64_oz S=7] full H q1 vs live oracle: {err:.2e}")
     assert err <= 1e-4

@@ -9,6 +9,8 @@ import pytest
 import slq_inputs as si
 from oracle import fdhvp, lanczos as OL, models, probe
 
+from . import oracle_cache as OC
+
 ROUTES = {"int8": 1.0, "hybrid": 0.0}
 
 torch = pytest.importorskip("torch")
@@ -59,8 +61,8 @@ def test_fp64_oz_grad_and_hvp(name, route):
         c.hvp(vd, out, cfg.eps)
         hv = slq.unshard([out.cpu().numpy()], lay)
         gf = slq.unshard([g.cpu().numpy()], lay)
-    l_ref, g_ref = models.loss_grad(th, cfg, _batch(cfg))
-    ref = fdhvp.hvp(fdhvp.make_grad_fn(cfg, _batch(cfg)), th, v, cfg.eps, "exact")
+    l_ref, g_ref = OC.loss_grad(name)
+    ref = OC.hvp_exact(name, 5)
     eg = np.linalg.norm(gf - g_ref) / np.linalg.norm(g_ref)
     eh = np.linalg.norm(hv - ref) / np.linalg.norm(ref)
     print(f"{name} [fp64_oz {route}]: loss {abs(loss - l_ref) / abs(l_ref):.1e} grad {eg:.2e} HVP {eh:.2e}")
@@ -76,9 +78,7 @@ def test_fp64_oz_lanczos_fp32_gates(name, m, route):
     with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="fp64_oz", reorth="full", max_steps=m,
                         oz_min_mnk=ROUTES[route]) as c:
         a, b = c.lanczos(cfg.probe_seed0, m)
-    g = fdhvp.make_grad_fn(cfg, _batch(cfg))
-    r = OL.lanczos(lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact"),
-                   probe.rademacher_probe(cfg.probe_seed0, th.size), m, "full")
+    r = OC.lanczos_exact(name, m, "full")
     scale = np.abs(r.alpha).max()
     ea = np.abs(a - r.alpha) / np.maximum(np.abs(r.alpha), 1e-2 * scale)  # reading R14
     eb = np.abs(b - r.beta) / np.abs(r.beta)

@@ -11,6 +11,8 @@ import pytest
 import slq_inputs as si
 from oracle import fdhvp, lanczos as OL, models, probe
 
+from . import oracle_cache as OC
+
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
@@ -44,8 +46,8 @@ def test_paired_grad_and_hvp(name, mode):
         out = torch.empty_like(vd)
         c.hvp(vd, out, cfg.eps)
         hv = slq.unshard([out.cpu().numpy()], lay)
-    l_ref, g_ref = models.loss_grad(th, cfg, tok)
-    ref = fdhvp.hvp(fdhvp.make_grad_fn(cfg, tok), th, v, cfg.eps, "exact")
+    l_ref, g_ref = OC.loss_grad(name)
+    ref = OC.hvp_exact(name, 5)
     eg = np.linalg.norm(gfull - g_ref) / np.linalg.norm(g_ref)
     eh = np.linalg.norm(hv - ref) / np.linalg.norm(ref)
     print(f"{name} [{mode}]: loss {abs(loss - l_ref) / abs(l_ref):.1e} grad {eg:.2e} HVP {eh:.2e}")
@@ -71,9 +73,7 @@ def test_paired_lanczos_fp32_gates(name, m, mode):
     tok = si.tokens(cfg)
     with slq.SlqContext(cfg, th, tok, pass_numerics=mode, reorth="full", max_steps=m) as c:
         a, b = c.lanczos(cfg.probe_seed0, m)
-    g = fdhvp.make_grad_fn(cfg, tok)
-    r = OL.lanczos(lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact"),
-                   probe.rademacher_probe(cfg.probe_seed0, th.size), m, "full")
+    r = OC.lanczos_exact(name, m, "full")
     scale = np.abs(r.alpha).max()
     ea = np.abs(a - r.alpha) / np.maximum(np.abs(r.alpha), 1e-2 * scale)  # reading R14
     es = np.abs(a - r.alpha) / scale                                       # relative to the spectral scale

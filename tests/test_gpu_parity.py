@@ -10,6 +10,8 @@ import numpy as np
 import pytest
 
 import slq_inputs as si
+
+from . import oracle_cache as OC
 from oracle import fdhvp, lanczos as OL, models, probe
 
 torch = pytest.importorskip("torch")
@@ -128,6 +130,8 @@ def test_hvp_host_pointers_and_edge_cases():
 
 
 def _oracle_lanczos(cfg, m, reorth, mode="exact"):
+    if mode == "exact":
+        return OC.lanczos_exact(cfg.name, m, reorth)
     th = si.init_params(cfg)
     g = fdhvp.make_grad_fn(cfg, _batch(cfg))
     q1 = probe.rademacher_probe(cfg.probe_seed0, th.size)

@@ -5,6 +5,8 @@ import numpy as np
 import pytest
 
 import slq_inputs as si
+
+from . import oracle_cache as OC
 from oracle import fdhvp, lanczos as OL, probe
 
 torch = pytest.importorskip("torch")
@@ -34,6 +36,8 @@ def _gpu(cfg, m, **kw):
 
 
 def _oracle(cfg, m, reorth, window=0, basis="fp64"):
+    if cfg.name in si.CONFIGS and si.CONFIGS[cfg.name] == cfg:
+        return OC.lanczos_exact(cfg.name, m, reorth, window, basis)
     th = si.init_params(cfg)
     g = fdhvp.make_grad_fn(cfg, _batch(cfg))
     q1 = probe.rademacher_probe(cfg.probe_seed0, th.size)

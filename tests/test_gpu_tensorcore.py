@@ -11,6 +11,8 @@ import numpy as np
 import pytest
 
 import slq_inputs as si
+
+from . import oracle_cache as OC
 from oracle import fdhvp, lanczos as OL, probe
 
 torch = pytest.importorskip("torch")
@@ -67,9 +69,7 @@ def test_bf16x3_hvp_and_moments_within_bf16_gates(name):
     m = 4
     with slq.SlqContext(cfg, th, _batch(cfg), pass_numerics="bf16x3", reorth="full", max_steps=m) as c:
         a, b = c.lanczos(cfg.probe_seed0, m)
-    g = fdhvp.make_grad_fn(cfg, _batch(cfg))
-    r = OL.lanczos(lambda q: fdhvp.fd_hvp_step(g, th, q, cfg.eps, "exact"),
-                   probe.rademacher_probe(cfg.probe_seed0, th.size), m, "full")
+    r = OC.lanczos_exact(name, m, "full")
     mu = (a[0], a[0] ** 2 + b[0] ** 2)
     mu_ref = (r.alpha[0], r.alpha[0] ** 2 + r.beta[0] ** 2)
     n1, _ = OL.gauss_quadrature(a, b)
