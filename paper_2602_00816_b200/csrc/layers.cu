@@ -452,7 +452,11 @@ __global__ void k_softmax_causal(T* __restrict__ S, int64_t rows, int Tn) {
   for (int j = lane; j <= t; j += kWarp) online_add(mx, sum, s[j]);
   warp_online(mx, sum);
   const T inv = T(1) / sum;
-  for (int j = lane; j < Tn; j += kWarp) s[j] = (j <= t) ? dexp(s[j] - mx) * inv : T(0);
+  // entries j > t are zeroed only up to the end of t's 128-wide column block: the causal GEMMs that
+  // read P (TRI_K_LE_M / TRI_K_GE_M, tiles <= 128 aligned on 128) never go further, and the tiles
+  // entirely above the diagonal are neither computed nor read (TRI_SKIP_UPPER)
+  const int jend = min(Tn, (t / 128 + 1) * 128);
+  for (int j = lane; j < jend; j += kWarp) s[j] = (j <= t) ? dexp(s[j] - mx) * inv : T(0);
 }
 
 // register-resident variant for Tn <= 32 V: lane l holds s[l + 32 i]; one read of the causal part
@@ -501,7 +505,8 @@ __global__ void k_softmax_bwd(const T* __restrict__ P, T* __restrict__ dP, int64
   T s = T(0);
   for (int j = lane; j <= t; j += kWarp) s += p[j] * d[j];  // entries j > t were never computed
   s = warp_sum(s);
-  for (int j = lane; j < Tn; j += kWarp) d[j] = (j <= t) ? p[j] * (d[j] - s) : T(0);
+  const int jend = min(Tn, (t / 128 + 1) * 128);  // (see k_softmax_causal)
+  for (int j = lane; j < jend; j += kWarp) d[j] = (j <= t) ? p[j] * (d[j] - s) : T(0);
 }
 
 // one block per row: loss_row = lse - logit[tgt];  logits <- (softmax - onehot) * inv_ntok
