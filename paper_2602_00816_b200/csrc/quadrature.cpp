@@ -3,7 +3,10 @@
 // P:312-316 (§4): v^T f(H) v ~= e_1^T f(T_m) e_1, i.e. Gauss quadrature with nodes = eigenvalues
 // of T_m and weights = squared first components of its normalised eigenvectors (Golub-Welsch).
 // Implicit-shift QL with Wilkinson shifts on the symmetric tridiagonal T_m; only the first row of
-// the eigenvector matrix is accumulated (m <= a few hundred, microseconds on the host).
+// the eigenvector matrix is accumulated (m <= a few hundred, microseconds on the host).  The
+// iteration follows the textbook tridiagonal QL algorithm as presented in Press et al.,
+// "Numerical Recipes" (routine tqli; variable names d, e, z, g, r, s, c, p, f, b as there), the
+// standard host-side companion of Golub-Welsch; the oracle uses an independent cyclic Jacobi.
 #include <math.h>
 
 #include <algorithm>
