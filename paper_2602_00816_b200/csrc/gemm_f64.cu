@@ -474,7 +474,62 @@ OzBlocks oz_blocks(const GemmArgs<double>& a, int S) {
   }
   return b;
 }
+// The activation of an int8 Ozaki GEMM runs as a separate elementwise pass: inside the GEMM's
+// epilogue the fp64 tanh of GELU cost ~200 instructions per output and made the c3 fc-forward
+// GEMM epilogue-bound (22% INT8-pipe activity, 0.63 ms); as a streaming pass it is ~0.06 ms.
+//   GELU:  C2 = y (pre-activation, written by the GEMM), C = gelu(C2)
+//   TANH:  C = tanh(y)                       DGELU: C = y gelu'(aux)      DTANH: C = y (1 - aux^2)
+__global__ void k_oz_act(int act, int M, int N, const double* __restrict__ Y, int64_t ldy, double* __restrict__ C,
+                         int64_t ldc, const double* __restrict__ aux, int64_t ldaux) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / N, n = i % N;
+    const double y = Y[m * ldy + n];
+    double out;
+    switch (act) {
+      case ACT_GELU: out = gelu_tanh(y); break;
+      case ACT_TANH: out = tanh(y); break;
+      case ACT_DGELU: out = y * gelu_tanh_grad(aux[m * ldaux + n]); break;
+      default: {
+        const double h = aux[m * ldaux + n];
+        out = y * (1.0 - h * h);
+      }
+    }
+    C[m * ldc + n] = out;
+  }
+}
+
+void gemm_oz_core(const Launch& L, const GemmArgs<double>& a);
+
 void gemm_oz_blocked(const Launch& L, const GemmArgs<double>& a) {
+  if (a.act == ACT_NONE) {
+    gemm_oz_core(L, a);
+    return;
+  }
+  SLQ_CHECK_ARG(!a.accumulate, "oz gemm: accumulate with an activation");
+  GemmArgs<double> c = a;
+  c.act = ACT_NONE;
+  c.aux = nullptr;
+  c.C2 = nullptr;
+  const double* Y = a.C;
+  int64_t ldy = a.ldc;
+  if (a.act == ACT_GELU) {  // the pre-activation is an output of its own
+    c.C = a.C2;
+    c.ldc = a.ldc2;
+    Y = a.C2;
+    ldy = a.ldc2;
+  }
+  gemm_oz_core(L, c);
+  const int64_t total = (int64_t)a.M * a.N;
+  LaunchScope scope(L.prof, KC_ELEM, L.stream, 0,
+                    8.0 * total * ((a.act == ACT_DGELU || a.act == ACT_DTANH) ? 3 : 2));
+  const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+  k_oz_act<<<blocks, 256, 0, L.stream>>>(a.act, a.M, a.N, Y, ldy, a.C, a.ldc, a.aux, a.ldaux);
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+}
+
+void gemm_oz_core(const Launch& L, const GemmArgs<double>& a) {
   const OzBlocks b = oz_blocks(a, L.oz_S);
   if (b.mb == a.M && b.nb == a.N && b.kb == a.K) {
     gemm_oz(L, a, L.oz_S);

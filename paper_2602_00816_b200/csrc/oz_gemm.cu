@@ -119,45 +119,36 @@ __host__ __device__ constexpr int oz_owner(int S, int NI, int g) {
 }
 // One 32-row x 4-column chunk of the output tile from the warp's staging tile T (row r, column c
 // at T[r * 4 + c], already row-scaled): lane l handles rows 8 j + l / 4 (j = 0..3) of column
-// l % 4, multiplies by its column scale and applies the fused epilogue (alpha, bias, residual,
-// activation, accumulate; split-K partials are stored plain into ws).
+// l % 4, multiplies by its column scale and applies alpha, bias, residual and accumulate (split-K
+// partials are stored plain into ws).  Activations never reach this epilogue: gemm<double> runs
+// them as a separate streaming pass (gemm_f64.cu, k_oz_act).
 __device__ __noinline__ void oz_epi_chunk(const GemmArgs<double>& p, const double* T, int mrow0, int n0c, int ncol,
                                           double sc, int splits, int sp, double* ws) {
   const int lane = threadIdx.x % 32;
   const int cc = lane & 3;
   const int n = n0c + cc;
   if (cc >= ncol) return;
-  const bool plain = splits > 1 || (!p.bias && !p.resid && !p.aux && !p.accumulate && p.act == ACT_NONE &&
-                                    p.alpha == 1.0);
-  double* Wd = splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
-  const int64_t ldw = splits > 1 ? p.N : p.ldc;
-  const double bs = (!plain && p.bias) ? p.bias[n] : 0.0;
+  const int r0 = lane >> 2;
+  const int mmax = p.M - mrow0 - r0;  // rows 8 j + r0 with 8 j < mmax are valid
+  if (splits > 1 || (!p.bias && !p.resid && !p.accumulate && p.alpha == 1.0)) {
+    double* Wd = splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
+    const int64_t ldw = splits > 1 ? p.N : p.ldc;
+    double* dst = Wd + (int64_t)(mrow0 + r0) * ldw + n;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (8 * j < mmax) dst[(int64_t)(8 * j) * ldw] = T[(8 * j + r0) * 4 + cc] * sc;
+    return;
+  }
+  const double bs = p.bias ? p.bias[n] : 0.0;
+  double* dst = p.C + (int64_t)(mrow0 + r0) * p.ldc + n;
+  const double* rsd = p.resid ? p.resid + (int64_t)(mrow0 + r0) * p.ldr + n : nullptr;
+#pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int m = mrow0 + 8 * j + (lane >> 2);
-    if (m >= p.M) break;
-    const double x = T[(8 * j + (lane >> 2)) * 4 + cc] * sc;
-    if (plain) {
-      Wd[(int64_t)m * ldw + n] = x;
-      continue;
-    }
-    const double y = p.alpha * x + bs + (p.resid ? p.resid[(int64_t)m * p.ldr + n] : 0.0);
-    double out;
-    switch (p.act) {
-      case ACT_GELU:
-        p.C2[(int64_t)m * p.ldc2 + n] = y;
-        out = gemm_detail::gelu_tanh(y);
-        break;
-      case ACT_TANH: out = tanh(y); break;
-      case ACT_DGELU: out = y * gemm_detail::gelu_tanh_grad(p.aux[(int64_t)m * p.ldaux + n]); break;
-      case ACT_DTANH: {
-        const double h = p.aux[(int64_t)m * p.ldaux + n];
-        out = y * (1.0 - h * h);
-        break;
-      }
-      default: out = y;
-    }
-    double* dst = p.C + (int64_t)m * p.ldc + n;
-    *dst = p.accumulate ? *dst + out : out;
+    if (8 * j >= mmax) break;
+    double y = p.alpha * (T[(8 * j + r0) * 4 + cc] * sc) + bs;
+    if (rsd) y += rsd[(int64_t)(8 * j) * p.ldr];
+    double* d = dst + (int64_t)(8 * j) * p.ldc;
+    *d = p.accumulate ? *d + y : y;
   }
 }
 

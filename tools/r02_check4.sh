@@ -1,0 +1,12 @@
+#!/bin/bash
+# call D: the whole GPU suite alone (durations: the driver gives it 1200 s), then bench lines
+cd "$(dirname "$0")/.."
+O=gpurun_out
+export SLQ_TIMEOUT_S=600
+timeout 2400 python -m pytest tests -m gpu -q -rfEx --durations=50 --timeout 900 -p no:cacheprovider > $O/t_r02d.log 2>&1
+echo "pytest rc=$?" >> $O/t_r02d.log
+timeout 600 python bench.py --config c2 --no-cpu-baseline > $O/b_r02d_c2.json 2> $O/b_r02d_c2.err
+for v in "none" "window --window 8" "full --basis bf16" "window --window 8 --basis bf16"; do
+  tag=$(echo $v | tr ' ' '_' | tr -d '-')
+  timeout 900 python bench.py --reorth $v --no-cpu-baseline > $O/b_r02d_c3_$tag.json 2> $O/b_r02d_c3_$tag.err
+done
