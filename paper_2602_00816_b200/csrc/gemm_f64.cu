@@ -481,9 +481,8 @@ OzBlocks oz_blocks(const GemmArgs<double>& a, int S) {
 //   TANH:  C = tanh(y)                       DGELU: C = y gelu'(aux)      DTANH: C = y (1 - aux^2)
 __global__ void k_oz_act(int act, int M, int N, const double* __restrict__ Y, int64_t ldy, double* __restrict__ C,
                          int64_t ldc, const double* __restrict__ aux, int64_t ldaux) {
-  const int64_t total = (int64_t)M * N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / N, n = i % N;
+  for (int64_t m = blockIdx.y; m < M; m += gridDim.y)
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     const double y = Y[m * ldy + n];
     double out;
     switch (act) {
@@ -523,8 +522,8 @@ void gemm_oz_blocked(const Launch& L, const GemmArgs<double>& a) {
   const int64_t total = (int64_t)a.M * a.N;
   LaunchScope scope(L.prof, KC_ELEM, L.stream, 0,
                     8.0 * total * ((a.act == ACT_DGELU || a.act == ACT_DTANH) ? 3 : 2));
-  const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
-  k_oz_act<<<blocks, 256, 0, L.stream>>>(a.act, a.M, a.N, Y, ldy, a.C, a.ldc, a.aux, a.ldaux);
+  const dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.N, 256), 4), (unsigned)std::min(a.M, 65535));
+  k_oz_act<<<grid, 256, 0, L.stream>>>(a.act, a.M, a.N, Y, ldy, a.C, a.ldc, a.aux, a.ldaux);
   SLQ_CUDA(cudaGetLastError());
   ++*L.launches;
 }

@@ -461,6 +461,51 @@ __global__ void k_softmax_causal(T* __restrict__ S, int64_t rows, int Tn) {
 
 // register-resident variant for Tn <= 32 V: lane l holds s[l + 32 i]; one read of the causal part
 // and one write of the row (same per-lane summation order as k_softmax_causal)
+// One 128-thread block per row for long rows (Tn <= 128 V): the row is read once into registers
+// (V values per thread), one exp per element, block reductions for the max and the sum, one write
+// (up to the end of the diagonal 128-column block, as k_softmax_causal).  The warp-per-row kernels
+// either read the row twice with two exps per element (online form) or hold 32 fp64 values per
+// lane at low occupancy.
+template <class T, int V>
+__global__ void __launch_bounds__(128) k_softmax_causal_blk(T* __restrict__ S, int64_t rows, int Tn) {
+  __shared__ T red[4];
+  const int64_t row = blockIdx.x;
+  const int t = (int)(row % Tn);
+  T* s = S + row * Tn;
+  const int tid = threadIdx.x, lane = tid % kWarp, wid = tid / kWarp;
+  T v[V];
+  T mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = tid + 128 * i;
+    v[i] = j <= t ? s[j] : T(-INFINITY);
+    mx = max(mx, v[i]);
+  }
+  mx = warp_max(mx);
+  if (lane == 0) red[wid] = mx;
+  __syncthreads();
+  mx = max(max(red[0], red[1]), max(red[2], red[3]));
+  __syncthreads();
+  T sum = T(0);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    if (tid + 128 * i <= t) {
+      v[i] = dexp(v[i] - mx);
+      sum += v[i];
+    }
+  }
+  sum = warp_sum(sum);
+  if (lane == 0) red[wid] = sum;
+  __syncthreads();
+  const T inv = T(1) / ((red[0] + red[1]) + (red[2] + red[3]));
+  const int jend = min(Tn, (t / 128 + 1) * 128);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = tid + 128 * i;
+    if (j < jend) s[j] = j <= t ? v[i] * inv : T(0);
+  }
+}
+
 template <class T, int V>
 __global__ void k_softmax_causal_reg(T* __restrict__ S, int64_t rows, int Tn) {
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kWarp;
@@ -792,6 +837,10 @@ void softmax_causal_fwd(const Launch& L, T* S, int64_t rows, int Tn) {
   // per c3 launch -- its 107 registers halve the resident warps)
   if (Tn <= 256)
     LAUNCH(KC_ATTN, (int)ceil_div(rows, 8), 256, (k_softmax_causal_reg<T, 8>), S, rows, Tn);
+  else if (Tn <= 1024)
+    LAUNCH(KC_ATTN, (int)rows, 128, (k_softmax_causal_blk<T, 8>), S, rows, Tn);
+  else if (Tn <= 2048)
+    LAUNCH(KC_ATTN, (int)rows, 128, (k_softmax_causal_blk<T, 16>), S, rows, Tn);
   else
     LAUNCH(KC_ATTN, (int)ceil_div(rows, 8), 256, k_softmax_causal<T>, S, rows, Tn);
 }

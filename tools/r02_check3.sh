@@ -12,6 +12,5 @@ timeout 900 python bench.py --no-cpu-baseline > '$O'/b_r02c_c3.json 2> '$O'/b_r0
 timeout 900 python bench.py --oz-slices 7 --steps 10 --warmup 3 --no-cpu-baseline > '$O'/b_r02c_c3_s7.json 2> '$O'/b_r02c_c3_s7.err
 timeout 900 python bench.py --numerics paired --steps 10 --warmup 3 --no-cpu-baseline > '$O'/b_r02c_c3_paired.json 2> '$O'/b_r02c_c3_paired.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active --clock-control none -c 4000 --csv --log-file '$O'/ncu_r02c_c3_launches.csv python bench.py --steps 2 --warmup 1 --probe-m 3 --no-cpu-baseline > '$O'/ncu_r02c_c3_launches.log 2>&1
-timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize.py > '$O'/sanitize_r02_memcheck.log 2>&1; echo "rc=$?" >> '$O'/sanitize_r02_memcheck.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_oz_gemm -s 2 -c 1 -o '$O'/ncu_r02c_oz_fc --force-overwrite python bench.py --steps 1 --warmup 1 --probe-m 2 --no-cpu-baseline > '$O'/ncu_r02c_oz_fc.log 2>&1
 '
