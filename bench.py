@@ -339,6 +339,18 @@ def main():
     ctx.profile(False)
     ctx.lanczos_step(m_probe - k0 - K)
     ctx.lanczos_result()
+    # ... and once more in the serial mode (one stream, no concurrency): each launch's event-timed
+    # duration is its own -- the kernel's efficiency without the time it shares the GPU
+    Ks = min(K, 4)
+    ctx.lanczos_start(cfg.probe_seed0, m_probe)
+    ctx.lanczos_step(k0)
+    torch.cuda.synchronize()
+    ctx.profile(True, reset=True)
+    serial_ms = timed(lambda: ctx.lanczos_step(Ks), Ks)
+    stats_serial = ctx.kernel_stats()
+    ctx.profile(False)
+    ctx.lanczos_step(m_probe - k0 - Ks)
+    ctx.lanczos_result()
 
     # ---- standalone HVP, gradient step (same numerics), end-to-end HVP with host buffers ----
     P_loc = ctx.P_loc
@@ -408,6 +420,14 @@ def main():
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
     roof["busy_ms_per_step"] = t_dom / K
     roof["sum_launch_ms_per_step"] = st["ms"] / K
+    ss = stats_serial[dom]
+    if ss["ms"] > 0:
+        a_ser = (ss["flops"] if roof["unit"] != "GB/s" else ss["bytes"]) / (ss["ms"] * 1e-3) / (
+            1e12 if roof["unit"] != "GB/s" else 1e9)
+        roof["serial"] = {"achieved": a_ser, "frac": a_ser / roof["peak"], "ms_per_step": ss["ms"] / Ks,
+                          "share_of_serial_step": ss["ms"] / Ks / serial_ms, "serial_step_ms": serial_ms,
+                          "what": "the same window re-run with every kernel on one stream (profiler mode 1): "
+                                  "summed event-timed launch durations of the class, no co-running kernels"}
     roof["kernel"] = dom
     roof["share_of_step"] = t_dom / prof_ms / K
     roof["launches_per_step"] = st["launches"] / K
