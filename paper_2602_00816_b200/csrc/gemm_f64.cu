@@ -446,12 +446,14 @@ __global__ void k_fill(double* x, int64_t n, uint64_t seed) {
 
 }  // namespace
 
-// Ozaki GEMMs whose digit planes + split-K partials would exceed kOzWsCap are cut into blocks
-// computed one after the other in the same workspace (the c5 head GEMMs ask for up to 8 GB
-// otherwise): the output is split along M or N (independent blocks, any epilogue), or -- when the
-// output is small and K long, and the epilogue is a plain (scaled, optionally accumulating) store --
-// K is split and the blocks accumulate into C.
-constexpr size_t kOzWsCap = (size_t)1 << 30;
+// Ozaki GEMMs whose digit planes + split-K partials would exceed the workspace caps are cut into
+// blocks computed one after the other in the same workspace (the c5 head GEMMs ask for up to 8 GB
+// otherwise).  K blocks (plain, scaled or accumulating epilogue only: the blocks accumulate into C)
+// cost nothing extra -- every block slices its own K range -- so they are used above 1 GiB; M / N
+// blocks (any epilogue) re-slice the other operand for every block, so they are used only above
+// 4 GiB (on c3 the M blocks of the head's dgrad re-sliced its 50257 x 768 weight four times,
+// 4 ms per step).
+constexpr size_t kOzWsCapK = (size_t)1 << 30, kOzWsCapMN = (size_t)4 << 30;
 struct OzBlocks {
   int mb, nb, kb;  // block extents
 };
@@ -461,15 +463,17 @@ bool oz_k_splittable(const GemmArgs<double>& a) {
 OzBlocks oz_blocks(const GemmArgs<double>& a, int S) {
   OzBlocks b{a.M, a.N, a.K};
   auto half = [](int x, int q) { return (int)(ceil_div(ceil_div(x, 2), q) * q); };
-  for (int it = 0; it < 64 && oz_ws_bytes(b.mb, b.nb, b.kb, S) > kOzWsCap; ++it) {
-    const bool m_big = b.mb >= b.nb;
-    const int big = m_big ? b.mb : b.nb, small = m_big ? b.nb : b.mb;
-    if (big > 4 * small || !oz_k_splittable(a) || b.kb < 256) {
-      if (big < 256) break;
-      if (m_big) b.mb = half(b.mb, 128);
+  const bool ksplit = oz_k_splittable(a);
+  for (int it = 0; it < 64; ++it) {
+    const size_t ws = oz_ws_bytes(b.mb, b.nb, b.kb, S);
+    if (ws <= kOzWsCapK) break;
+    if (ksplit && b.kb >= 256) {
+      b.kb = half(b.kb, 64);
+    } else if (ws > kOzWsCapMN && std::max(b.mb, b.nb) >= 256) {
+      if (b.mb >= b.nb) b.mb = half(b.mb, 128);
       else b.nb = half(b.nb, 128);
     } else {
-      b.kb = half(b.kb, 64);
+      break;
     }
   }
   return b;
