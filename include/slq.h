@@ -106,8 +106,8 @@ typedef struct {
    * 1 puts every dense GEMM on the int8 path.  Per context (no process-global state). */
   double oz_min_mnk;
   int32_t oz_slices;       /* SLQ_PASS_FP64_OZ digit planes S (4..7); 0 = default: 7 for fp32 models (param_dtype
-                            * FP32; S < 7 misses their fp32 alpha / beta gate), 5 for bf16 models (their
-                            * bf16 gates; R27) */
+                            * FP32; S < 7 misses their fp32 alpha / beta gate), for bf16 models (their bf16
+                            * gates) 5 when eps_default >= 5e-4, else 6 (R27) */
   /* 1: activation checkpointing (BASELINE configs[4]): each transformer block keeps only its input
    * residual stream from the forward and recomputes its forward inside its backward (bit-identical
    * gradients, +1 block forward per block, block activations for 2 blocks instead of n_layers) */

@@ -836,8 +836,10 @@ Launch pass_launch(const slq_model_desc& d, const Launch& L) {
     Lp.oz_min_mnk = d.oz_min_mnk > 0 ? d.oz_min_mnk : 1e9;
     // digit planes: S = 7 for the fp32 models (their fp32 alpha / beta gate needs it: S = 6 drifts
     // to 1.9e-4 by step 32 on c2), S = 5 for the bf16 models, whose gates are the bf16 ones
-    // (moments <= 1e-2, extreme Ritz <= 2e-2; S = 5 leaves the FD-HVP at ~1e-5 .. 1e-4, R27)
-    Lp.oz_S = d.oz_slices > 0 ? d.oz_slices : (d.param_dtype == SLQ_PARAM_BF16 ? 5 : 7);
+    // (moments <= 1e-2, extreme Ritz <= 2e-2; R27)
+    // (eps < 5e-4 needs one more plane: the truncation enters the FD-HVP divided by 2 eps, and on c3
+    // at eps = 1e-4 S = 5 leaves the extreme Ritz values at 1.8e-2 of the 2e-2 gate)
+    Lp.oz_S = d.oz_slices > 0 ? d.oz_slices : (d.param_dtype == SLQ_PARAM_BF16 ? (d.eps_default >= 5e-4 ? 5 : 6) : 7);
     SLQ_CHECK_ARG(Lp.oz_S >= 4 && Lp.oz_S <= 7, "oz_slices must be 0 (default 7) or 4..7");
   } else {
     Lp.gemm_mode = (d.pass_numerics == SLQ_PASS_BF16X3 || d.pass_numerics == SLQ_PASS_PAIRED) ? 1
