@@ -466,6 +466,7 @@ def main():
                 "d2h_bytes_per_step": 4 * P_loc * world,
                 "what": "slq_hvp with pinned host v and host out (copies inside the call) per step"},
         "gpu_launches": launches,
+        "memory_plan_gib": {k: round(v / 2**30, 2) for k, v in slq.plan_memory(ctx.desc, world, tok.shape[0]).items()},
         "kernel_busy_ms_per_step": {k: s["busy_ms"] / K for k, s in stats.items() if s["launches"]},
         "kernel_serial_ms_per_step": {k: s["ms"] / Ks for k, s in stats_serial.items() if s["launches"]},
         "timed_window": {"probe_m": m_probe, "first_step": k0, "steps": K,

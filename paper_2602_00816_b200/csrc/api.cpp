@@ -1,6 +1,7 @@
 // C-ABI of libslq.so (include/slq.h): argument checking, context lifetime, host/device buffer
 // marshalling, the per-kernel-class CUDA-event profiler.  No torch types cross this boundary.
 #include <cuda_runtime.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
@@ -336,13 +337,17 @@ slq_status slq_init(const slq_model_desc* desc, const slq_batch* batch, const sl
                   desc->arch == SLQ_ARCH_MLP ? batch->n_rows_local : batch->n_seq_local, mem);
       size_t free_b = 0, total_b = 0;
       SLQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      if ((size_t)mem[SLQ_MEM_TOTAL] > free_b) {
-        static const char* names[SLQ_MEM_COUNT] = {"theta", "points", "grads", "lanczos", "fsdp", "activations",
-                                                   "logits", "scratch", "workspace", "total"};
-        std::string m = "device memory plan exceeds the free memory (" + std::to_string(free_b >> 20) + " MiB):";
-        for (int i = 0; i < SLQ_MEM_COUNT; ++i) m += std::string(" ") + names[i] + "=" + std::to_string(mem[i] >> 20) + "MiB";
-        throw Error(SLQ_ENOMEM, m + " (try act_ckpt = 1, a larger world_size or a smaller batch)");
-      }
+      static const char* names[SLQ_MEM_COUNT] = {"theta", "points", "grads", "lanczos", "fsdp", "activations",
+                                                 "logits", "scratch", "workspace", "total"};
+      std::string m;
+      for (int i = 0; i < SLQ_MEM_COUNT; ++i) m += std::string(" ") + names[i] + "=" + std::to_string(mem[i] >> 20) + "MiB";
+      // SLQ_VERBOSE=1: print the plan of every context (rank, world size, free memory)
+      if (getenv("SLQ_VERBOSE") && atoi(getenv("SLQ_VERBOSE")) > 0)
+        fprintf(stderr, "[slq] rank %d/%d device memory plan:%s (free %zu MiB)\n", world->rank, world->world_size,
+                m.c_str(), free_b >> 20);
+      if ((size_t)mem[SLQ_MEM_TOTAL] > free_b)
+        throw Error(SLQ_ENOMEM, "device memory plan exceeds the free memory (" + std::to_string(free_b >> 20) +
+                                    " MiB):" + m + " (try act_ckpt = 1, a larger world_size or a smaller batch)");
     }
     if (world->world_size > 1) {
       if (world->comm_backend == SLQ_COMM_LOOPBACK)

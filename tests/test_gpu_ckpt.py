@@ -42,10 +42,11 @@ def _run(cfg, numerics, ckpt, m):
 # >= 3 blocks; odd and even depths exercise both activation sets
 @pytest.mark.parametrize("name,layers,numerics", [("gpt_tiny", 5, "fp64"), ("gpt_tiny_tied", 4, "fp64"),
                                                   ("llama_tiny", 5, "fp64"), ("c2", 4, "fp64_oz"),
-                                                  ("llama_tiny", 3, "bf16x3"), ("c4_parity", 4, "fp64_oz")])
+                                                  ("llama_tiny", 3, "bf16x3"), ("c4_parity", 4, "fp64_oz"),
+                                                  ("c5_twin", 3, "fp64_oz")])
 def test_checkpointing_bit_identical(name, layers, numerics):
     cfg = si.get_config(name, n_layers=layers)
-    m = 4 if name == "c4_parity" else 6
+    m = 4 if name in ("c4_parity", "c5_twin") else 6
     r0 = _run(cfg, numerics, False, m)
     r1 = _run(cfg, numerics, True, m)
     print(f"{name} [{numerics}]: loss {r0[0]:.12f} alpha {r0[3]}")
