@@ -401,7 +401,7 @@ def main():
                                 else "fallback 1590 TFLOP/s") + " x 2 (nominal INT8 / BF16 dense ratio)",
                 "fp64_equiv_tflops": achieved / nprod,
                 "note": f"tcgen05 kind::i8 digit products, {nprod} INT8 GEMMs per fp64 GEMM (S = {nS} digit "
-                        f"planes); achieved = every INT8 op issued / the class's busy time"}
+                        f"planes); every INT8 op issued is counted"}
     elif dom == "gemm" and args.numerics not in ("fp64", "fp64_oz"):
         bf16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
         achieved = st["flops"] / (t_dom * 1e-3) / 1e12

@@ -563,26 +563,9 @@ __global__ void k_cross_entropy(T* __restrict__ logits, const int32_t* __restric
   const int b = row / Tn, t = row % Tn;
   const int y = tgt[(int64_t)b * tgt_stride + t];
   __shared__ T red[32], red2[32];
-  // one read of the row for the online (max, sum of exponentials); one read + write for the gradient.
-  // Four independent (max, sum) states per thread keep four loads in flight per lane.
+  // one read of the row for the online (max, sum of exponentials); one read + write for the gradient
   T mx = -INFINITY, sm = T(0);
-  {
-    T m4[4] = {T(-INFINITY), T(-INFINITY), T(-INFINITY), T(-INFINITY)}, s4[4] = {T(0), T(0), T(0), T(0)};
-    const int step = blockDim.x;
-    int j = threadIdx.x;
-    for (; j + 3 * step < V; j += 4 * step) {
-      const T x0 = z[j], x1 = z[j + step], x2 = z[j + 2 * step], x3 = z[j + 3 * step];
-      online_add(m4[0], s4[0], x0);
-      online_add(m4[1], s4[1], x1);
-      online_add(m4[2], s4[2], x2);
-      online_add(m4[3], s4[3], x3);
-    }
-    for (; j < V; j += step) online_add(m4[0], s4[0], z[j]);
-    mx = m4[0];
-    sm = s4[0];
-#pragma unroll
-    for (int k = 1; k < 4; ++k) online_merge(mx, sm, m4[k], s4[k]);
-  }
+  for (int j = threadIdx.x; j < V; j += blockDim.x) online_add(mx, sm, z[j]);
   warp_online(mx, sm);
   if (threadIdx.x % kWarp == 0) {
     red[threadIdx.x / kWarp] = mx;
@@ -605,7 +588,6 @@ __global__ void k_cross_entropy(T* __restrict__ logits, const int32_t* __restric
   if (threadIdx.x == 0) loss_rows[row] = (double)(lse - z[y]);
   __syncthreads();
   const T inv = T(1) / sum, scale = (T)inv_ntok;
-#pragma unroll 4
   for (int j = threadIdx.x; j < V; j += blockDim.x) {
     T p = dexp(z[j] - mx) * inv;
     if (j == y) p -= T(1);

@@ -26,9 +26,13 @@ def grad_fn(name):
     return fdhvp.make_grad_fn(cfg, batch(cfg))
 
 
-@functools.lru_cache(maxsize=None)
 def lanczos_exact(name, m, reorth="full", window=0, basis="fp64"):
     """oracle Lanczos from the config's probe on the exact-perturbation FD-HVP operator"""
+    return _lanczos_exact(name, int(m), reorth, int(window), basis)  # one cache key per run
+
+
+@functools.lru_cache(maxsize=None)
+def _lanczos_exact(name, m, reorth, window, basis):
     cfg = si.CONFIGS[name]
     th = theta(name)
     g = grad_fn(name)

@@ -3,6 +3,8 @@ checkpointing"): every block keeps its input residual stream only and recomputes
 inside its backward.  The recomputation runs the same kernels on the same inputs, so gradients,
 HVPs and Lanczos coefficients must be BIT-IDENTICAL to the run without it.  Also: the device
 memory actually taken by a context matches slq_plan_memory."""
+import functools
+
 import numpy as np
 import pytest
 
@@ -23,9 +25,13 @@ def built():
 from paper_2602_00816_b200 import slq  # noqa: E402
 
 
+@functools.lru_cache(maxsize=1)
+def _inputs(cfg):
+    return si.init_params(cfg), si.tokens(cfg)
+
+
 def _run(cfg, numerics, ckpt, m):
-    th = si.init_params(cfg)
-    tok = si.tokens(cfg)
+    th, tok = _inputs(cfg)
     with slq.SlqContext(cfg, th, tok, pass_numerics=numerics, reorth="full" if cfg.reorth_full else "none",
                         max_steps=m, act_ckpt=ckpt) as c:
         lay = c.layout()
@@ -46,7 +52,7 @@ def _run(cfg, numerics, ckpt, m):
                                                   ("c5_twin", 3, "fp64_oz")])
 def test_checkpointing_bit_identical(name, layers, numerics):
     cfg = si.get_config(name, n_layers=layers)
-    m = 4 if name in ("c4_parity", "c5_twin") else 6
+    m = {"c4_parity": 3, "c5_twin": 2}.get(name, 6)
     r0 = _run(cfg, numerics, False, m)
     r1 = _run(cfg, numerics, True, m)
     print(f"{name} [{numerics}]: loss {r0[0]:.12f} alpha {r0[3]}")
@@ -60,9 +66,8 @@ def test_checkpointing_bit_identical(name, layers, numerics):
 def test_memory_plan_matches_allocation(name, numerics, ckpt):
     """Device bytes a context holds after init and one HVP (workspaces are reserved up front at their
     planned size) against slq_plan_memory; the host-call staging buffers are not allocated here."""
-    cfg = si.CONFIGS[name]
-    th = si.init_params(cfg)
-    tok = si.tokens(cfg)
+    cfg = si.get_config(name, n_layers=4) if name == "c4_parity" else si.CONFIGS[name]
+    th, tok = _inputs(cfg)
     desc = slq.make_desc(cfg, numerics, max_steps=cfg.m, act_ckpt=ckpt)
     P_loc = slq.plan_layout(desc, 1)["P_loc"]
     v = torch.zeros(P_loc, dtype=torch.float32, device="cuda")

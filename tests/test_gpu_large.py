@@ -96,7 +96,9 @@ def check(name, g, hv, a, b, nq, P, fp32_gates=True):
     ref = np.asarray(h["val"]) * nq
     e_samp = float(np.linalg.norm(hv[idx] - ref) / np.linalg.norm(ref))
     e_norm = abs(np.linalg.norm(hv) - h["norm"] * nq) / (h["norm"] * nq)
-    e_proj = max(abs(_sign_dot(s, hv) - p * nq) for s, p in zip(h["proj_seeds"], h["proj"]))
+    # (one sign projection beyond 200M parameters: each costs ~15 s of host hashing there)
+    npj = 1 if P > 200_000_000 else len(h["proj"])
+    e_proj = max(abs(_sign_dot(s, hv) - p * nq) for s, p in list(zip(h["proj_seeds"], h["proj"]))[:npj])
     e_proj /= h["norm"] * nq
     ra, rb = np.asarray(g["alpha"]), np.asarray(g["beta"])
     ea = np.abs(a - ra) / np.maximum(np.abs(ra), 1e-2 * np.abs(ra).max())  # reading R14
@@ -118,8 +120,8 @@ def check(name, g, hv, a, b, nq, P, fp32_gates=True):
     assert er <= 2e-2
 
 
-@pytest.mark.parametrize("numerics,S", [("fp64_oz", 0), ("fp64_oz", 7), ("fp64", 0)])
-@pytest.mark.parametrize("eps", [1e-2, 1e-3, 1e-4])
+@pytest.mark.parametrize("eps,numerics,S", [(e, n, s) for e in (1e-2, 1e-3, 1e-4) for n, s in
+                                            (("fp64_oz", 0), ("fp64_oz", 7), ("fp64", 0)) if s != 7 or e == 1e-3])
 def test_c3_lanczos_m32(eps, numerics, S):
     """The bf16-model gates for every mode (c3 is a bf16 model, R27): fp64_oz S = 0 is the bench
     configuration (hybrid route, the bf16 models' default S = 5 digit planes); S = 7 is printed for

@@ -81,6 +81,7 @@ def _mode_param(mode, name):
 def test_paired_lanczos_fp32_gates(name, mode):
     """The north star's fp32 gates as every fp32-model mode is held to them: alpha per reading R14
     and beta <= 1e-5 relative over the first 32 steps."""
+    m = 32 if name == "c2" else 16
     cfg = si.CONFIGS[name]
     th = si.init_params(cfg)
     tok = si.tokens(cfg)
