@@ -30,12 +30,17 @@ def _inputs(cfg):
     return si.init_params(cfg), si.tokens(cfg)
 
 
+@functools.lru_cache(maxsize=1)
+def _direction(P):
+    return si.random_vector(P, 5)
+
+
 def _run(cfg, numerics, ckpt, m):
     th, tok = _inputs(cfg)
     with slq.SlqContext(cfg, th, tok, pass_numerics=numerics, reorth="full" if cfg.reorth_full else "none",
                         max_steps=m, act_ckpt=ckpt) as c:
         lay = c.layout()
-        v = torch.from_numpy(slq.shard_of(si.random_vector(th.size, 5), lay, 0, 1)).cuda()
+        v = torch.from_numpy(slq.shard_of(_direction(th.size), lay, 0, 1)).cuda()
         g = torch.empty_like(v)
         loss = c.grad(g)
         out = torch.empty_like(v)
