@@ -310,28 +310,58 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
       double v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.0;
-      // two digit-weight groups per TMEM round trip (2 x 32 columns, one wait); the g loop stays
-      // rolled (the 32-wide bodies are unrolled) to keep the kernel inside the instruction cache
-      // (more than 8 epilogue warps: one group per round trip, within the smaller register budget)
-      constexpr int GS = NE > 8 ? 1 : 2;
+      if constexpr (S <= 5) {
+        // Drain for S <= 5: the S accumulators are combined EXACTLY in int64 by Horner's rule in
+        // base 2^7, h = ((a_0 2^7 + a_1) 2^7 + ...) 2^7 + a_{S-1} (|a_g| < 2^31, so |h| < 2^60), and
+        // h is converted to fp64 only after TMEM is released -- the fp64 pipe work (the top stall of
+        // the short-K GEMMs) leaves the section in which the next tile's MMAs wait for the
+        // accumulators.  (S = 6, 7 would overflow int64 and keep the fp64 drain below.)
+        long long h[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) h[i] = 0;
 #pragma unroll 1
-      for (int g = 0; g < ((o.debug & 8) ? 0 : S); g += GS) {
-        uint32_t r0[32], r1[GS > 1 ? 32 : 1];
-        tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
-        if (GS > 1 && g + 1 < S) tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)((g + 1) * BN + c0), r1);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-        const double w0 = exp2i(-7 * (g + 2)), w1 = exp2i(-7 * (g + 3));
+        for (int g = 0; g < ((o.debug & 8) ? 0 : S); ++g) {
+          uint32_t r0[32];
+          tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r0[i]), w0, v[i]);
-        if (GS > 1 && g + 1 < S) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r1[GS > 1 ? i : 0]), w1, v[i]);
+          for (int i = 0; i < 32; ++i) h[i] = h[i] * 128 + (long long)(int)r0[i];
         }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
+        // v = h 2^(-7(S + 1)): hi 2^32 + lo exactly from two i2d conversions, one rounding in the fma
+        const double wl = exp2i(-7 * (S + 1));
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const double hi = i2d((uint32_t)(int)(h[i] >> 32));
+          const double lo = __hiloint2double(0x43300000, (int)(uint32_t)h[i]) - 4503599627370496.0;
+          v[i] = fma(hi, 4294967296.0, lo) * wl;
+        }
+      } else {
+        // two digit-weight groups per TMEM round trip (2 x 32 columns, one wait); the g loop stays
+        // rolled (the 32-wide bodies are unrolled) to keep the kernel inside the instruction cache
+        // (more than 8 epilogue warps: one group per round trip, within the smaller register budget)
+        constexpr int GS = NE > 8 ? 1 : 2;
+#pragma unroll 1
+        for (int g = 0; g < ((o.debug & 8) ? 0 : S); g += GS) {
+          uint32_t r0[32], r1[GS > 1 ? 32 : 1];
+          tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
+          if (GS > 1 && g + 1 < S) tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)((g + 1) * BN + c0), r1);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+          const double w0 = exp2i(-7 * (g + 2)), w1 = exp2i(-7 * (g + 3));
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r0[i]), w0, v[i]);
+          if (GS > 1 && g + 1 < S) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fma(i2d(r1[GS > 1 ? i : 0]), w1, v[i]);
+          }
+        }
+        // accumulators drained: release TMEM to the next unit's MMAs
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
       }
-      // accumulators drained: release TMEM to the next unit's MMAs
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
       // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
       // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
       // sectors) instead of 32 rows x 8 bytes.  The loads / activation / stores of a chunk are one
