@@ -117,38 +117,38 @@ __host__ __device__ constexpr int oz_owner(int S, int NI, int g) {
          : S == 6  ? (g == 3 || g == 4 ? 1 : 0)
                    : (g == 2 || g == 3 ? 1 : 0);
 }
-// One 32-row x 4-column chunk of the output tile from the warp's staging tile T (row r, column c
-// at T[r * 4 + c], already row-scaled): lane l handles rows 8 j + l / 4 (j = 0..3) of column
-// l % 4, multiplies by its column scale and applies alpha, bias, residual and accumulate (split-K
-// partials are stored plain into ws).  Activations never reach this epilogue: gemm<double> runs
-// them as a separate streaming pass (gemm_f64.cu, k_oz_act).
-__device__ __noinline__ void oz_epi_chunk(const GemmArgs<double>& p, const double* T, int mrow0, int n0c, int ncol,
-                                          double sc, int splits, int sp, double* ws) {
-  const int lane = threadIdx.x % 32;
-  const int cc = lane & 3;
-  const int n = n0c + cc;
-  if (cc >= ncol) return;
-  const int r0 = lane >> 2;
-  const int mmax = p.M - mrow0 - r0;  // rows 8 j + r0 with 8 j < mmax are valid
-  if (splits > 1 || (!p.bias && !p.resid && !p.accumulate && p.alpha == 1.0)) {
-    double* Wd = splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
-    const int64_t ldw = splits > 1 ? p.N : p.ldc;
-    double* dst = Wd + (int64_t)(mrow0 + r0) * ldw + n;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (8 * j < mmax) dst[(int64_t)(8 * j) * ldw] = T[(8 * j + r0) * 4 + cc] * sc;
+// Up to 4 consecutive outputs (row m, columns n .. n + nc - 1) of one lane: alpha, bias, residual,
+// accumulate (or plain stores of split-K partials / ragged columns).  Activations never reach this
+// epilogue: gemm<double> runs them as a separate streaming pass (gemm_f64.cu, k_oz_act).
+__device__ __noinline__ void oz_epi_row4(const GemmArgs<double>& p, int m, int n, int nc, const double* x, bool plain,
+                                         bool vec, double* Wd, int64_t ldw) {
+  double* d = Wd + (int64_t)m * ldw + n;
+  if (plain) {
+    for (int q = 0; q < nc; ++q) d[q] = x[q];
     return;
   }
-  const double bs = p.bias ? p.bias[n] : 0.0;
-  double* dst = p.C + (int64_t)(mrow0 + r0) * p.ldc + n;
-  const double* rsd = p.resid ? p.resid + (int64_t)(mrow0 + r0) * p.ldr + n : nullptr;
+  double y[4];
+  const double* rs = p.resid ? p.resid + (int64_t)m * p.ldr + n : nullptr;
+  if (nc == 4 && vec) {
+    double2 r01 = make_double2(0.0, 0.0), r23 = r01, c01 = r01, c23 = r01;
+    if (rs) {
+      r01 = *reinterpret_cast<const double2*>(rs);
+      r23 = *reinterpret_cast<const double2*>(rs + 2);
+    }
+    if (p.accumulate) {
+      c01 = *reinterpret_cast<const double2*>(d);
+      c23 = *reinterpret_cast<const double2*>(d + 2);
+    }
+    const double r[4] = {r01.x, r01.y, r23.x, r23.y}, co[4] = {c01.x, c01.y, c23.x, c23.y};
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (8 * j >= mmax) break;
-    double y = p.alpha * (T[(8 * j + r0) * 4 + cc] * sc) + bs;
-    if (rsd) y += rsd[(int64_t)(8 * j) * p.ldr];
-    double* d = dst + (int64_t)(8 * j) * p.ldc;
-    *d = p.accumulate ? *d + y : y;
+    for (int q = 0; q < 4; ++q) y[q] = p.alpha * x[q] + (p.bias ? p.bias[n + q] : 0.0) + r[q] + co[q];
+    *reinterpret_cast<double2*>(d) = make_double2(y[0], y[1]);
+    *reinterpret_cast<double2*>(d + 2) = make_double2(y[2], y[3]);
+    return;
+  }
+  for (int q = 0; q < nc; ++q) {
+    double v = p.alpha * x[q] + (p.bias ? p.bias[n + q] : 0.0) + (rs ? rs[q] : 0.0);
+    d[q] = p.accumulate ? d[q] + v : v;
   }
 }
 
@@ -362,22 +362,31 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
       }
-      // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
-      // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
-      // sectors) instead of 32 rows x 8 bytes.  The loads / activation / stores of a chunk are one
-      // out-of-line function: unrolling them 8 x 4 times per kernel (x 3 activations, fp64 tanh
-      // inlined) made the kernel 246 KB of SASS, far beyond the instruction cache the MMA-issuing
-      // warps share with the epilogue warps.
+      // Stores straight from registers: lane l owns output row m0 + lg + l and writes 4 consecutive
+      // columns per chunk as two 16-byte stores (one full 32-byte sector per lane).  (The previous
+      // shared-memory transpose + out-of-line per-chunk epilogue cost ~200 instructions per chunk and
+      // made the epilogue's store phase, not the MMAs, the per-tile period of the short-K GEMMs.)
       const int ncol = p.N - (n0 + c0);  // valid columns of this warp's 32 (may be <= 0)
-      double* T = stage_t + (warp - 2) * 128;
+      const int m = m0 + lg + lane;
+      const bool plain = o.splits > 1 || (!p.bias && !p.resid && !p.accumulate && p.alpha == 1.0);
+      double* Wd = o.splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
+      const int64_t ldw = o.splits > 1 ? p.N : p.ldc;
+      const bool vec = (ldw % 2) == 0 && (((uintptr_t)Wd) & 15) == 0 &&
+                       (plain || !p.resid || ((p.ldr % 2) == 0 && (((uintptr_t)p.resid) & 15) == 0));
+      double* dst = Wd + (int64_t)m * ldw + (n0 + c0);
 #pragma unroll
       for (int c = 0; c < ((o.debug & 4) ? 0 : 32); c += 4) {
-        __syncwarp();
-        *reinterpret_cast<double2*>(&T[lane * 4]) = make_double2(v[c] * sr, v[c + 1] * sr);
-        *reinterpret_cast<double2*>(&T[lane * 4 + 2]) = make_double2(v[c + 2] * sr, v[c + 3] * sr);
-        __syncwarp();
-        const double sc = __shfl_sync(0xffffffffu, sc_l, c + (lane & 3));
-        oz_epi_chunk(p, T, m0 + lg, n0 + c0 + c, c < ncol ? ncol - c : 0, sc, o.splits, sp, ws);
+        if (c >= ncol) break;  // (warp-uniform)
+        double x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = v[c + q] * sr * __shfl_sync(0xffffffffu, sc_l, c + q);
+        if (m >= p.M) continue;
+        if (plain && vec && c + 4 <= ncol) {
+          *reinterpret_cast<double2*>(dst + c) = make_double2(x[0], x[1]);
+          *reinterpret_cast<double2*>(dst + c + 2) = make_double2(x[2], x[3]);
+        } else {
+          oz_epi_row4(p, m, n0 + c0 + c, min(4, ncol - c), x, plain, vec, Wd, ldw);
+        }
       }
     }
   }
