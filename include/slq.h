@@ -319,6 +319,14 @@ slq_status slq_diag_fp64_peak(int32_t device, double* tflops);
  * (i, j); *tflops = fp64-equivalent rate of the Ozaki GEMM (2 M N K / time, slicing included). */
 slq_status slq_diag_oz_check(int32_t device, int32_t M, int32_t N, int32_t K, int32_t a_kmajor, int32_t b_kmajor,
                              int32_t S, int32_t iters, double* max_err, double* tflops);
+/* Diagnostic: causal multi-head attention forward + backward (nseq sequences of Tn tokens, Hq query
+ * heads sharing Hkv key/value heads of width hd) on random data through the FP64 DMMA path and
+ * through the FP64_OZ path (all six contractions as batched INT8 Ozaki GEMMs with S digit planes,
+ * oz_attn.cu).  err[4] = max |x_oz - x_dmma| / max |x_dmma| for O, dQ, dK, dV; ms[2] = time of one
+ * forward + backward of each path averaged over `iters` repetitions (0: not timed).  SLQ_EINVAL when
+ * the shape is not eligible for the Ozaki path (Tn % 128, hd % 32, hd <= 128). */
+slq_status slq_diag_attn_oz(int32_t device, int32_t nseq, int32_t Tn, int32_t Hq, int32_t Hkv, int32_t hd, int32_t S,
+                            int32_t iters, double* err, double* ms);
 /* Diagnostic: measured FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) throughput in TFLOP/s. */
 slq_status slq_diag_dmma_peak(int32_t device, double* tflops);
 /* Diagnostic: time the library's fp64 GEMM on one shape.  A [M x K] (K-contiguous if a_kmajor,

@@ -483,22 +483,34 @@ OzBlocks oz_blocks(const GemmArgs<double>& a, int S) {
 // GEMM epilogue-bound (22% INT8-pipe activity, 0.63 ms); as a streaming pass it is ~0.06 ms.
 //   GELU:  C2 = y (pre-activation, written by the GEMM), C = gelu(C2)
 //   TANH:  C = tanh(y)                       DGELU: C = y gelu'(aux)      DTANH: C = y (1 - aux^2)
-__global__ void k_oz_act(int act, int M, int N, const double* __restrict__ Y, int64_t ldy, double* __restrict__ C,
-                         int64_t ldc, const double* __restrict__ aux, int64_t ldaux) {
-  for (int64_t m = blockIdx.y; m < M; m += gridDim.y)
-    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    const double y = Y[m * ldy + n];
-    double out;
-    switch (act) {
-      case ACT_GELU: out = gelu_tanh(y); break;
-      case ACT_TANH: out = tanh(y); break;
-      case ACT_DGELU: out = y * gelu_tanh_grad(aux[m * ldaux + n]); break;
-      default: {
-        const double h = aux[m * ldaux + n];
-        out = y * (1.0 - h * h);
-      }
+// the activation pass of the Ozaki GEMMs: each thread owns 4 columns of a row, 256 apart
+// (coalesced), and issues all its loads before the first fp64 activation (four independent loads
+// in flight per thread: the pass is HBM-bound, and one load per thread left it at ~3.5 TB/s)
+template <int ACT>
+__global__ void __launch_bounds__(256) k_oz_act(int M, int N, const double* __restrict__ Y, int64_t ldy,
+                                                double* __restrict__ C, int64_t ldc, const double* __restrict__ aux,
+                                                int64_t ldaux) {
+  constexpr bool kAux = ACT == ACT_DGELU || ACT == ACT_DTANH;
+  for (int64_t m = blockIdx.y; m < M; m += gridDim.y) {
+    const int n0 = blockIdx.x * 1024 + threadIdx.x;
+    double y[4], x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int n = n0 + 256 * i;
+      y[i] = n < N ? Y[m * ldy + n] : 0.0;
+      x[i] = (kAux && n < N) ? aux[m * ldaux + n] : 0.0;
     }
-    C[m * ldc + n] = out;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int n = n0 + 256 * i;
+      if (n >= N) continue;
+      double out;
+      if constexpr (ACT == ACT_GELU) out = gelu_tanh(y[i]);
+      else if constexpr (ACT == ACT_TANH) out = tanh(y[i]);
+      else if constexpr (ACT == ACT_DGELU) out = y[i] * gelu_tanh_grad(x[i]);
+      else out = y[i] * (1.0 - x[i] * x[i]);
+      C[m * ldc + n] = out;
+    }
   }
 }
 
@@ -526,8 +538,13 @@ void gemm_oz_blocked(const Launch& L, const GemmArgs<double>& a) {
   const int64_t total = (int64_t)a.M * a.N;
   LaunchScope scope(L.prof, KC_ELEM, L.stream, 0,
                     8.0 * total * ((a.act == ACT_DGELU || a.act == ACT_DTANH) ? 3 : 2));
-  const dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.N, 256), 4), (unsigned)std::min(a.M, 65535));
-  k_oz_act<<<grid, 256, 0, L.stream>>>(a.act, a.M, a.N, Y, ldy, a.C, a.ldc, a.aux, a.ldaux);
+  const dim3 grid((unsigned)ceil_div(a.N, 1024), (unsigned)std::min(a.M, 65535));
+  switch (a.act) {
+    case ACT_GELU: k_oz_act<ACT_GELU><<<grid, 256, 0, L.stream>>>(a.M, a.N, Y, ldy, a.C, a.ldc, a.aux, a.ldaux); break;
+    case ACT_TANH: k_oz_act<ACT_TANH><<<grid, 256, 0, L.stream>>>(a.M, a.N, Y, ldy, a.C, a.ldc, a.aux, a.ldaux); break;
+    case ACT_DGELU: k_oz_act<ACT_DGELU><<<grid, 256, 0, L.stream>>>(a.M, a.N, Y, ldy, a.C, a.ldc, a.aux, a.ldaux); break;
+    default: k_oz_act<ACT_DTANH><<<grid, 256, 0, L.stream>>>(a.M, a.N, Y, ldy, a.C, a.ldc, a.aux, a.ldaux);
+  }
   SLQ_CUDA(cudaGetLastError());
   ++*L.launches;
 }

@@ -92,6 +92,34 @@ size_t tc_ws_bytes(int M, int N, int K, int terms);
 // planes of 7 bits per operand; oz_gemm.cu).  batch == 1, dense (tri == TRI_NONE) only.
 void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S);
 
+// S digit planes of one operand, already sliced: plane q of plane-batch zb, row r at
+// d + ((q * nb + zb) * rows + r) * Kp (rows = M for A, N for B); ex[zb * rows + r] the row
+// exponents (nullptr: 0).  GEMM batch z reads plane batch z0 + boff(z).
+struct OzPlanes {
+  const int8_t* d = nullptr;
+  const int* ex = nullptr;
+  int nb = 1, Kp = 0, z0 = 0;
+  BatchOff z;
+};
+// batched (optionally causal, a.tri) fp64 GEMM C[z] = alpha A[z] B[z] (+ C[z] with accumulate)
+// from pre-sliced planes (the attention path): a.M, a.N, a.K, a.batch, a.tri, a.C, a.ldc, a.offC,
+// a.alpha, a.accumulate are used; a.A / a.B are ignored
+void gemm_oz_planes(const Launch& L, int S, const OzPlanes& A, const OzPlanes& B, const GemmArgs<double>& a);
+
+// Causal multi-head attention with its six contractions as batched Ozaki GEMMs and the digit
+// planes of P and dS emitted by the softmax kernels (oz_attn.cu).  Geometry as model.cu's
+// AttnGeom: qkv rows r = b Tn + t (ld W), q head h at column qo + h hd, kv head g at ko / vo + g hd;
+// o / dO rows with ld ldo; P, dP [nseq Hq][Tn][Tn].
+struct AttnShape {
+  int nseq, Tn, Hq, Hkv, hd;
+  int64_t W, qo, ko, vo, ldo;
+};
+bool attn_oz_eligible(const Launch& L, const AttnShape& g);
+size_t attn_oz_ws_bytes(const Launch& L, const AttnShape& g);
+void attention_fwd_oz(const Launch& L, const AttnShape& g, const double* qkv, double* P, double* o);
+void attention_bwd_oz(const Launch& L, const AttnShape& g, const double* qkv, const double* P, const double* dO,
+                      double* dP, double* dqkv);
+
 // fp32-faithful GEMM on the tcgen05 tensor cores: every fp32 operand is split into three bf16
 // terms (x = x0 + x1 + x2, 24 significant bits) and the six products with i + j <= 2 are
 // accumulated in one fp32 TMEM accumulator (tc_gemm.cu).  batch == 1 only.  terms = 1: the

@@ -149,7 +149,24 @@ struct AttnGeom {
 };
 
 template <class T>
+AttnShape shape_of(const AttnGeom<T>& g) {
+  return AttnShape{g.nseq, g.Tn, g.Hq, g.Hkv, g.hd, g.W, g.qo, g.ko, g.vo, g.ldo};
+}
+// workspace of the Ozaki attention path (FP64_OZ passes, eligible shapes; 0 otherwise)
+template <class T>
+size_t attn_ws(const Launch& L, const AttnGeom<T>& g) {
+  if constexpr (sizeof(T) == 8) return attn_oz_ws_bytes(L, shape_of(g));
+  return 0;
+}
+
+template <class T>
 void attention_fwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, T* P, T* o) {
+  if constexpr (sizeof(T) == 8) {
+    if (attn_oz_eligible(L, shape_of(g))) {  // all six contractions on the INT8 tensor cores (oz_attn.cu)
+      attention_fwd_oz(L, shape_of(g), qkv, P, o);
+      return;
+    }
+  }
   const T scale = T(1.0 / sqrt((double)g.hd));
   {  // S = scale * Q K^T
     GemmArgs<T> a;
@@ -176,6 +193,12 @@ void attention_fwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, T* P, T*
 // gradients w.r.t. q, k, v (written into dqkv with the qkv geometry); dP is scratch [like P]
 template <class T>
 void attention_bwd(const Launch& L, const AttnGeom<T>& g, const T* qkv, const T* P, const T* dO, T* dP, T* dqkv) {
+  if constexpr (sizeof(T) == 8) {
+    if (attn_oz_eligible(L, shape_of(g))) {
+      attention_bwd_oz(L, shape_of(g), qkv, P, dO, dP, dqkv);
+      return;
+    }
+  }
   const T scale = T(1.0 / sqrt((double)g.hd));
   const int rep = g.rep();
   // dV[b, g] = sum_{r < rep} P[b, g*rep + r]^T dO[b, g*rep + r]
@@ -468,6 +491,7 @@ struct GptRunner : Runner<T> {
     main = std::max(main, sizeof(T) * (size_t)embed_chunks_bound(N, V) * D);
     side = std::max(side, colreduce_ws_bytes<T>(N, F));
     side = std::max(side, colreduce_ws_bytes<T>(N, 3 * D));
+    main = std::max(main, attn_ws<T>(L, geom()));
   }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
   int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, N, Tn, L.stream); }
@@ -715,6 +739,7 @@ struct LlamaRunner : Runner<T> {
     linear_ws<T>(L, V, D, N, main, side);
     main = std::max(main, sizeof(T) * (size_t)embed_chunks_bound(N, V) * D);
     side = std::max(side, colreduce_ws_bytes<T>(N, D));
+    main = std::max(main, attn_ws<T>(L, geom()));
   }
   double tokens_global() const override { return (double)nseq_glob * Tn; }
   int first_nonfinite_seq() override { return first_nonfinite_group(loss_rows, N, Tn, L.stream); }
@@ -852,3 +877,110 @@ template std::unique_ptr<Runner<float>> make_runner<float>(const slq_model_desc&
                                                            const HostBatch&, const Launch&, bool);
 
 }  // namespace slq
+
+namespace slq {
+namespace {
+__global__ void k_fill_unit(double* x, int64_t n, uint64_t seed, double amp) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    x[i] = amp * ((double)(int64_t)(z >> 11) / 4503599627370496.0 - 1.0);  // uniform [-amp, amp)
+  }
+}
+}  // namespace
+}  // namespace slq
+
+extern "C" slq_status slq_diag_attn_oz(int32_t device, int32_t nseq, int32_t Tn, int32_t Hq, int32_t Hkv, int32_t hd,
+                                       int32_t S, int32_t iters, double* err, double* ms) {
+  using namespace slq;
+  std::vector<double*> bufs;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  auto cleanup = [&] {
+    for (double* p : bufs) cudaFree(p);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  };
+  try {
+    SLQ_CHECK_ARG(nseq > 0 && Tn > 0 && Hq > 0 && Hkv > 0 && Hq % Hkv == 0 && hd > 0 && S >= 4 && S <= 7 &&
+                      iters >= 0 && err && ms, "arguments");
+    SLQ_CUDA(cudaSetDevice(device));
+    AttnGeom<double> g;
+    g.nseq = nseq; g.Tn = Tn; g.Hq = Hq; g.Hkv = Hkv; g.hd = hd;
+    g.W = (int64_t)(Hq + 2 * Hkv) * hd; g.qo = 0; g.ko = (int64_t)Hq * hd; g.vo = (int64_t)(Hq + Hkv) * hd;
+    g.ldo = (int64_t)Hq * hd;
+    const int64_t N = (int64_t)nseq * Tn, PP = (int64_t)nseq * Hq * Tn * Tn;
+    auto alloc = [&](int64_t n) {
+      double* p = nullptr;
+      SLQ_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)std::max<int64_t>(n, 1)));
+      bufs.push_back(p);
+      return p;
+    };
+    double* qkv = alloc(N * g.W);
+    double* dO = alloc(N * g.ldo);
+    double *P[2], *dP[2], *o[2], *dq[2];
+    for (int i = 0; i < 2; ++i) {
+      P[i] = alloc(PP); dP[i] = alloc(PP); o[i] = alloc(N * g.ldo); dq[i] = alloc(N * g.W);
+    }
+    k_fill_unit<<<1024, 256>>>(qkv, N * g.W, 21, 2.0);
+    k_fill_unit<<<1024, 256>>>(dO, N * g.ldo, 22, 1.0);
+    Workspace ws;
+    int64_t launches = 0;
+    Launch Ld{0, nullptr, &ws, &launches};
+    Launch Lo = Ld;
+    Lo.gemm_mode = 2; Lo.oz_S = S; Lo.oz_min_mnk = 0;
+    SLQ_CHECK_ARG(attn_oz_eligible(Lo, shape_of(g)), "shape not eligible for the Ozaki attention path");
+    const Launch* Ls[2] = {&Ld, &Lo};
+    for (int i = 0; i < 2; ++i) {
+      attention_fwd<double>(*Ls[i], g, qkv, P[i], o[i]);
+      attention_bwd<double>(*Ls[i], g, qkv, P[i], dO, dP[i], dq[i]);
+    }
+    SLQ_CUDA(cudaDeviceSynchronize());
+    // errors relative to each output's max norm: O, dQ, dK, dV
+    std::vector<double> h[2][2];
+    for (int i = 0; i < 2; ++i) {
+      h[i][0].resize((size_t)(N * g.ldo));
+      h[i][1].resize((size_t)(N * g.W));
+      SLQ_CUDA(cudaMemcpy(h[i][0].data(), o[i], sizeof(double) * h[i][0].size(), cudaMemcpyDeviceToHost));
+      SLQ_CUDA(cudaMemcpy(h[i][1].data(), dq[i], sizeof(double) * h[i][1].size(), cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < 4; ++k) {
+      const std::vector<double>& a = h[0][k == 0 ? 0 : 1];
+      const std::vector<double>& b = h[1][k == 0 ? 0 : 1];
+      const int64_t ld = k == 0 ? g.ldo : g.W;
+      const int64_t c0 = k == 0 ? 0 : (k == 1 ? g.qo : (k == 2 ? g.ko : g.vo));
+      const int64_t nc = k <= 1 ? (int64_t)Hq * hd : (int64_t)Hkv * hd;
+      double mx = 0.0, md = 0.0;
+      bool bad = false;
+      for (int64_t r = 0; r < N; ++r)
+        for (int64_t c = 0; c < nc; ++c) {
+          const double x = a[(size_t)(r * ld + c0 + c)], y = b[(size_t)(r * ld + c0 + c)];
+          if (!std::isfinite(y)) bad = true;
+          mx = std::max(mx, fabs(x));
+          md = std::max(md, fabs(x - y));
+        }
+      err[k] = bad ? INFINITY : (mx > 0 ? md / mx : md);
+    }
+    SLQ_CUDA(cudaEventCreate(&e0));
+    SLQ_CUDA(cudaEventCreate(&e1));
+    for (int i = 0; i < 2; ++i) {
+      float t = 0.f;
+      if (iters > 0) {
+        SLQ_CUDA(cudaEventRecord(e0));
+        for (int it = 0; it < iters; ++it) {
+          attention_fwd<double>(*Ls[i], g, qkv, P[i], o[i]);
+          attention_bwd<double>(*Ls[i], g, qkv, P[i], dO, dP[i], dq[i]);
+        }
+        SLQ_CUDA(cudaEventRecord(e1));
+        SLQ_CUDA(cudaEventSynchronize(e1));
+        SLQ_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      }
+      ms[i] = iters > 0 ? t / iters : 0.0;
+    }
+    cleanup();
+    return SLQ_OK;
+  } catch (const Error& e) {
+    cleanup();
+    return e.status;
+  }
+}

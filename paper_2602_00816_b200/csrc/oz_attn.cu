@@ -1,0 +1,621 @@
+// Causal multi-head attention of the FP64_OZ passes on the tcgen05 INT8 tensor cores.
+//
+// The six contractions of one attention layer (P:391-405 counts them in T_grad) -- S = Q K^T,
+// O = P V in the forward; dP = dO V^T, dV = P^T dO, dQ = dS K, dK = dS^T Q in the backward -- run
+// as batched Ozaki GEMMs (gemm_oz_planes: exact INT8 digit products, one launch per contraction,
+// causal tiles skipped or k-clipped) instead of FP64 DMMA.  Their operands are sliced here:
+//   * Q, K, V, dO rows (hd contiguous values per (head, position)): one warp per row;
+//   * K, V, dO', Q' columns (the B operands whose k index is the position): one CTA per head and
+//     32 columns, transposed through shared memory;
+//   * P and dS: emitted by the softmax kernels themselves -- the forward writes P (fp64, for the
+//     backward) and its row digits; the backward writes the digits of dS (row-major, for dQ) and,
+//     transposed, of P and dS (for dV and dK).  No fp64 dS is ever stored.
+// The transposed P / dS operands keep their row exponents: P^T's digits are those of P_qk 2^-r_q,
+// and the factor 2^r_q moves into the other operand, dV = sum_q (P_qk 2^-r_q) (2^r_q dO_q) (same for
+// dK with dS's exponents e_q and Q) -- an exact power-of-two rescaling, so the only error is the
+// dropped digits of the Ozaki scheme (oz_gemm.cu header), bounded relative to the rescaled operand.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.h"
+#include "kernels.h"
+#include "oz_common.cuh"
+
+namespace slq {
+namespace oz {
+
+__device__ __forceinline__ double nanmax(double a, double b) { return (b > a || b != b) ? b : a; }
+__device__ __forceinline__ double warp_nanmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_fmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_add(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- head rows: row (zb, t) = X[(b T + t) ld + col0 + h hd + 0 .. hd-1], zb = b heads + h ----
+struct RowJob {
+  const double* X;
+  int64_t ld, col0;
+  int heads, T, hd, nb;
+  int8_t* out;  // [S][nb][T][hd]
+  int* ex;      // [nb][T]
+  int blocks0;
+};
+struct RowJobs {
+  RowJob j[2];
+  int n;
+};
+
+constexpr int kRowsPerWarp = 4;
+
+template <int S>
+__global__ void __launch_bounds__(256) k_att_rows(const __grid_constant__ RowJobs js) {
+  const RowJob& jb = (js.n > 1 && (int)blockIdx.x >= js.j[1].blocks0) ? js.j[1] : js.j[0];
+  // 32-bit row arithmetic (nb T < 2^31; 64-bit divisions made this kernel integer-bound)
+  const int r0 = ((blockIdx.x - jb.blocks0) * 8 + threadIdx.x / 32) * kRowsPerWarp;
+  const int lane = threadIdx.x % 32;
+  const int nrows = jb.nb * jb.T;
+  if (r0 >= nrows) return;
+  const int vpl = jb.hd / 32;  // consecutive values per lane (hd = 32 .. 128)
+  // every row's loads first (kRowsPerWarp x vpl independent loads in flight per lane); the warp's
+  // rows are consecutive positions of one head (T % kRowsPerWarp == 0)
+  const int zb = r0 / jb.T, t0 = r0 - zb * jb.T;
+  const int b = zb / jb.heads, h = zb - b * jb.heads;
+  const double* xb = jb.X + ((int64_t)b * jb.T + t0) * jb.ld + jb.col0 + (int64_t)h * jb.hd + lane * vpl;
+  double v[kRowsPerWarp][4];
+#pragma unroll
+  for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+    const int r = r0 + rr;
+    const double* x = xb + (int64_t)rr * jb.ld - lane * vpl;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[rr][i] = (r < nrows && i < vpl) ? x[lane * vpl + i] : 0.0;
+  }
+  const int64_t plane = (int64_t)nrows * jb.hd;
+#pragma unroll
+  for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+    const int64_t r = r0 + rr;
+    if (r >= nrows) break;
+    double mx = 0.0;
+    bool nf = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mx = fmax(mx, fabs(v[rr][i]));
+      nf |= nonfinite(v[rr][i]);
+    }
+    mx = warp_fmax(mx);
+    nf = __any_sync(0xffffffffu, nf);
+    const int e = exp_of(mx, nf);
+    if (lane == 0) jb.ex[r] = e;
+    const int ed = nf ? 0 : e;
+    int8_t d[4][S];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) digits<S>(v[rr][i], ed, d[i]);
+    int8_t* o = jb.out + r * jb.hd + lane * vpl;
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      if (vpl == 2) {
+        *reinterpret_cast<uint16_t*>(o + q * plane) = (uint16_t)((uint8_t)d[0][q] | ((uint8_t)d[1][q] << 8));
+      } else if (vpl == 4) {
+        *reinterpret_cast<uint32_t*>(o + q * plane) = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
+                                                      ((uint32_t)(uint8_t)d[2][q] << 16) |
+                                                      ((uint32_t)(uint8_t)d[3][q] << 24);
+      } else {
+        for (int i = 0; i < vpl; ++i) o[q * plane + i] = d[i][q];
+      }
+    }
+  }
+}
+
+// ---- head columns, transposed: row (zb, dcol) of the output holds X[t][dcol] 2^pre[zb][t] over
+// t = 0 .. T-1 (the B operand of O = P V, dQ, dV, dK); exponent per (zb, dcol) over all t ----
+struct ColJob {
+  const double* X;
+  int64_t ld, col0;
+  int heads, T, hd, nb;
+  const int* pre;  // [nb][T] power-of-two row pre-scale (nullptr: none)
+  int8_t* out;     // [S][nb][hd][T]
+  int* ex;         // [nb][hd]
+};
+
+// 512 threads: pass 1 (column maxima) 16 t-lanes x 32 columns with 8 loads in flight per thread;
+// pass 2 128-deep t chunks through a shared tile, each thread 8 consecutive t of one column
+template <int S>
+__global__ void __launch_bounds__(512) k_att_cols(const __grid_constant__ ColJob jb) {
+  __shared__ double tile[128][33];
+  __shared__ double red[16][33];
+  __shared__ int es[32];
+  const int dblk = jb.hd / 32;
+  const int zb = blockIdx.x / dblk, d0 = (blockIdx.x % dblk) * 32;
+  const int b = zb / jb.heads, h = zb % jb.heads;
+  const double* x = jb.X + (int64_t)b * jb.T * jb.ld + jb.col0 + (int64_t)h * jb.hd + d0;
+  const int* pre = jb.pre ? jb.pre + (int64_t)zb * jb.T : nullptr;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  auto val = [&](int t) {
+    const double v = x[(int64_t)t * jb.ld + tx];
+    return pre ? v * scale_of(pre[t]) : v;
+  };
+  double mx = 0.0;
+  bool nf = false;
+  for (int t0 = 0; t0 < jb.T; t0 += 128) {  // T % 128 == 0
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = val(t0 + ty + 16 * i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      mx = fmax(mx, fabs(v[i]));
+      nf |= nonfinite(v[i]);
+    }
+  }
+  red[ty][tx] = nf ? __longlong_as_double(0x7ff8000000000000ll) : mx;
+  __syncthreads();
+  if (ty == 0) {
+    double m = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      bad |= red[i][tx] != red[i][tx];
+      m = fmax(m, red[i][tx]);
+    }
+    const int e = exp_of(m, bad);
+    es[tx] = e;
+    jb.ex[(int64_t)zb * jb.hd + d0 + tx] = e;
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)jb.nb * jb.hd * jb.T;
+  const int dd = threadIdx.x / 16, tq = (threadIdx.x % 16) * 8;
+  const int ed = es[dd] == kExNaN ? 0 : es[dd];
+  int8_t* orow = jb.out + ((int64_t)zb * jb.hd + d0 + dd) * jb.T + tq;
+  for (int t0 = 0; t0 < jb.T; t0 += 128) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = val(t0 + ty + 16 * i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tile[ty + 16 * i][tx] = v[i];
+    __syncthreads();
+    uint32_t w[S][2];
+#pragma unroll
+    for (int q = 0; q < S; ++q) w[q][0] = w[q][1] = 0u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int8_t dg[S];
+      digits<S>(tile[tq + j][dd], ed, dg);
+#pragma unroll
+      for (int q = 0; q < S; ++q) w[q][j / 4] |= (uint32_t)(uint8_t)dg[q] << (8 * (j % 4));
+    }
+#pragma unroll
+    for (int q = 0; q < S; ++q) *reinterpret_cast<uint2*>(orow + q * plane + t0) = make_uint2(w[q][0], w[q][1]);
+    __syncthreads();
+  }
+}
+
+// ---- forward softmax: S -> P in place (causal, zeros up to the end of the diagonal 128-column
+// block, as k_softmax_causal) and P's row digits (row exponent r_q of max_k P_qk = 1 / sum) ----
+// one 128-thread block per row (as k_softmax_causal_blk): the row is read once into registers
+// (V values per thread, j = tid + 128 i), block reductions for the max and the sum, one write of P
+// and of its S digit planes (each warp store covers 32 consecutive bytes of a plane)
+template <int S, int V>
+__global__ void __launch_bounds__(128) k_att_sm_fwd(double* __restrict__ P, int T, int8_t* __restrict__ out,
+                                                    int* __restrict__ ex, int64_t plane) {
+  __shared__ double red[4];
+  const int row = blockIdx.x;  // (32-bit: rows < 2^31)
+  const int q = row - (row / T) * T;
+  double* s = P + (int64_t)row * T;
+  int8_t* orow = out + (int64_t)row * T;
+  const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
+  double v[V];
+  double mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = tid + 128 * i;
+    v[i] = j <= q ? s[j] : -INFINITY;
+    mx = nanmax(mx, v[i]);
+  }
+  mx = warp_nanmax(mx);
+  if (lane == 0) red[wid] = mx;
+  __syncthreads();
+  mx = nanmax(nanmax(red[0], red[1]), nanmax(red[2], red[3]));
+  __syncthreads();
+  double sum = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    if (tid + 128 * i <= q) {
+      v[i] = exp(v[i] - mx);
+      sum += v[i];
+    }
+  }
+  sum = warp_add(sum);
+  if (lane == 0) red[wid] = sum;
+  __syncthreads();
+  const double inv = 1.0 / ((red[0] + red[1]) + (red[2] + red[3]));
+  const bool nf = !(inv > 0.0 && inv <= 1.7976931348623157e308);
+  const int e = exp_of(inv, nf), ed = nf ? 0 : e;  // max_k P_qk = exp(0) inv = inv < 2^e
+  if (tid == 0) ex[row] = e;
+  const int jend = min(T, (q / 128 + 1) * 128);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = tid + 128 * i;
+    if (j < jend) {
+      const double p = j <= q ? v[i] * inv : 0.0;
+      s[j] = p;
+      int8_t dg[S];
+      digits<S>(p, ed, dg);
+#pragma unroll
+      for (int qd = 0; qd < S; ++qd) orow[qd * plane + j] = dg[qd];
+    }
+  }
+}
+
+// ---- backward softmax: dS = P (dP - D), D_q = sum_k P_qk dP_qk, emitted only as digits: dS
+// row-major (exponent e_q of max_k |dS_qk|; A of dQ), and transposed [key][query] the digits of
+// dS_qk 2^-e_q (A of dK) and of P_qk 2^-r_q (A of dV), r_q the exponent of max_k P_qk ----
+// One 512-thread CTA per 32 query rows, two CTAs per SM (the CTAs in flight re-read their rows
+// from L2: 2 x 148 x 32 causal rows x 16 B stays below its capacity).  Phase 1: warp w owns rows
+// q0 + 2w, q0 + 2w + 1 (D and max P in one sweep, max |dS| in a second; eight loads in flight per
+// lane).  Phase 2: 64-key chunks, lane l keys 2l, 2l + 1 of the warp's two rows: P / dP loads and
+// dS row digits coalesced; the transposed digits go through [plane][query][key] shared tiles and
+// leave as 32-byte rows [key][q0 .. q0 + 31].
+template <int S>
+__global__ void __launch_bounds__(512, 2) k_att_sm_bwd(const double* __restrict__ P, const double* __restrict__ dP,
+                                                       int T, int8_t* __restrict__ pt, int8_t* __restrict__ dsa,
+                                                       int8_t* __restrict__ dst, int* __restrict__ exr,
+                                                       int* __restrict__ exe, int64_t plane) {
+  __shared__ __align__(16) uint8_t tp[S][32][64];
+  __shared__ __align__(16) uint8_t td[S][32][64];
+  const int cpr = T / 32;
+  const int64_t zq = blockIdx.x / cpr;
+  const int q0 = (blockIdx.x % cpr) * 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  double Dr[2];
+  int rd[2], ed[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int q = q0 + 2 * warp + u;
+    const double* p = P + (zq * T + q) * (int64_t)T;
+    const double* g = dP + (zq * T + q) * (int64_t)T;
+    double pm = 0.0, D = 0.0;
+    bool nf = false;
+    for (int j0 = 0; j0 <= q; j0 += 128) {
+      double a[4], c[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = j0 + lane + 32 * i;
+        a[i] = j <= q ? p[j] : 0.0;
+        c[i] = j <= q ? g[j] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        pm = fmax(pm, a[i]);
+        nf |= nonfinite(a[i]) || nonfinite(c[i]);
+        D += a[i] * c[i];
+      }
+    }
+    pm = warp_fmax(pm);
+    D = warp_add(D);
+    nf = __any_sync(0xffffffffu, nf);
+    double dm = 0.0;
+    for (int j0 = 0; j0 <= q; j0 += 128) {
+      double a[4], c[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = j0 + lane + 32 * i;
+        a[i] = j <= q ? p[j] : 0.0;
+        c[i] = j <= q ? g[j] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dm = fmax(dm, fabs(a[i] * (c[i] - D)));
+    }
+    dm = warp_fmax(dm);
+    const int r = exp_of(pm, nf), e = exp_of(dm, nf || nonfinite(D));
+    if (lane == 0) {
+      exr[zq * T + q] = r;
+      exe[zq * T + q] = e;
+    }
+    Dr[u] = D;
+    rd[u] = r == kExNaN ? 0 : r;
+    ed[u] = e == kExNaN ? 0 : e;
+  }
+  const int kend = min(T, (q0 / 128 + 1) * 128);
+  for (int c0 = 0; c0 < kend; c0 += 64) {
+    const int j = c0 + 2 * lane;
+    double2 a[2], c[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t ro = (zq * T + q0 + 2 * warp + u) * (int64_t)T;
+      a[u] = *reinterpret_cast<const double2*>(P + ro + j);
+      c[u] = *reinterpret_cast<const double2*>(dP + ro + j);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int q = q0 + 2 * warp + u;
+      const double pv[2] = {a[u].x, a[u].y}, gv[2] = {c[u].x, c[u].y};
+      uint16_t ws[S], wp[S];
+#pragma unroll
+      for (int qd = 0; qd < S; ++qd) ws[qd] = wp[qd] = 0;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const bool in = j + i <= q;
+        int8_t dgp[S], dgs[S];
+        digits<S>(in ? pv[i] : 0.0, rd[u], dgp);
+        digits<S>(in ? pv[i] * (gv[i] - Dr[u]) : 0.0, ed[u], dgs);
+#pragma unroll
+        for (int qd = 0; qd < S; ++qd) {
+          ws[qd] |= (uint16_t)((uint8_t)dgs[qd] << (8 * i));
+          wp[qd] |= (uint16_t)((uint8_t)dgp[qd] << (8 * i));
+        }
+      }
+      int8_t* arow = dsa + (zq * T + q) * (int64_t)T;
+#pragma unroll
+      for (int qd = 0; qd < S; ++qd) {
+        *reinterpret_cast<uint16_t*>(arow + qd * plane + j) = ws[qd];
+        *reinterpret_cast<uint16_t*>(&td[qd][2 * warp + u][2 * lane]) = ws[qd];
+        *reinterpret_cast<uint16_t*>(&tp[qd][2 * warp + u][2 * lane]) = wp[qd];
+      }
+    }
+    __syncthreads();
+    // transposed rows: thread (array, plane, key kk) gathers queries q0 .. q0 + 31 of key c0 + kk
+    for (int idx = threadIdx.x; idx < 2 * S * 64; idx += 512) {
+      const int kk = idx % 64, qd = (idx / 64) % S, arr = idx / (64 * S);
+      const uint8_t(*src)[64] = arr ? td[qd] : tp[qd];
+      uint32_t w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        w[u] = (uint32_t)src[4 * u][kk] | ((uint32_t)src[4 * u + 1][kk] << 8) | ((uint32_t)src[4 * u + 2][kk] << 16) |
+               ((uint32_t)src[4 * u + 3][kk] << 24);
+      int8_t* d = (arr ? dst : pt) + qd * plane + (zq * T + c0 + kk) * (int64_t)T + q0;
+      *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(d + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host side
+
+struct Carve {
+  uint8_t* p;
+  size_t off = 0;
+  template <class X>
+  X* take(size_t n) {
+    X* r = reinterpret_cast<X*>(p ? p + off : nullptr);
+    off += (sizeof(X) * n + 255) & ~(size_t)255;
+    return r;
+  }
+};
+
+struct Bufs {
+  // forward
+  int8_t *QA, *KB, *PA, *VB;
+  int *exQ, *exK, *exP, *exV;
+  // backward
+  int8_t *DOA, *VR, *PT, *DSA, *DST, *KT, *DOT, *QT;
+  int *exDO, *exVR, *exR, *exE, *exKT, *exDOT, *exQT;
+  size_t fwd_bytes, bwd_bytes;
+};
+
+static Bufs carve(const AttnShape& g, int S, uint8_t* base) {
+  const size_t zq = (size_t)g.nseq * g.Hq, zk = (size_t)g.nseq * g.Hkv, T = g.Tn, hd = g.hd;
+  Bufs b;
+  Carve f{base};
+  b.QA = f.take<int8_t>(S * zq * T * hd);
+  b.KB = f.take<int8_t>(S * zk * T * hd);
+  b.PA = f.take<int8_t>(S * zq * T * T);
+  b.VB = f.take<int8_t>(S * zk * hd * T);
+  b.exQ = f.take<int>(zq * T);
+  b.exK = f.take<int>(zk * T);
+  b.exP = f.take<int>(zq * T);
+  b.exV = f.take<int>(zk * hd);
+  b.fwd_bytes = f.off;
+  Carve w{base};
+  b.PT = w.take<int8_t>(S * zq * T * T);
+  b.DSA = w.take<int8_t>(S * zq * T * T);
+  b.DST = w.take<int8_t>(S * zq * T * T);
+  b.DOA = w.take<int8_t>(S * zq * T * hd);
+  b.VR = w.take<int8_t>(S * zk * T * hd);
+  b.KT = w.take<int8_t>(S * zk * hd * T);
+  b.DOT = w.take<int8_t>(S * zq * hd * T);
+  b.QT = w.take<int8_t>(S * zq * hd * T);
+  b.exDO = w.take<int>(zq * T);
+  b.exVR = w.take<int>(zk * T);
+  b.exR = w.take<int>(zq * T);
+  b.exE = w.take<int>(zq * T);
+  b.exKT = w.take<int>(zk * hd);
+  b.exDOT = w.take<int>(zq * hd);
+  b.exQT = w.take<int>(zq * hd);
+  b.bwd_bytes = w.off;
+  return b;
+}
+
+template <int S>
+static void launch_rows(const Launch& L, RowJobs js) {
+  int nb = 0;
+  for (int i = 0; i < js.n; ++i) {
+    js.j[i].blocks0 = nb;
+    nb += (int)ceil_div((int64_t)js.j[i].nb * js.j[i].T, 8 * kRowsPerWarp);
+  }
+  if (js.n == 1) js.j[1] = js.j[0];
+  double elems = 0;
+  for (int i = 0; i < js.n; ++i) elems += (double)js.j[i].nb * js.j[i].T * js.j[i].hd;
+  LaunchScope scope(L.prof, KC_OZ_SLICE, L.stream, 0, (8.0 + S) * elems);
+  k_att_rows<S><<<nb, 256, 0, L.stream>>>(js);
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+}
+
+template <int S>
+static void launch_cols(const Launch& L, const ColJob& j) {
+  LaunchScope scope(L.prof, KC_OZ_SLICE, L.stream, 0, (16.0 + S) * (double)j.nb * j.T * j.hd);
+  k_att_cols<S><<<j.nb * (j.hd / 32), 512, 0, L.stream>>>(j);
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+}
+
+static BatchOff ident() { return BatchOff{1, 0, 1, 1}; }
+
+template <int S>
+static void fwd(const Launch& L, const AttnShape& g, const double* qkv, double* P, double* o) {
+  const int zq = g.nseq * g.Hq, zk = g.nseq * g.Hkv, T = g.Tn, hd = g.hd, rep = g.Hq / g.Hkv;
+  Bufs b = carve(g, S, (uint8_t*)L.ws->get(attn_oz_ws_bytes(L, g), L.stream));
+  const BatchOff kv{g.Hkv, 1, g.Hq, rep};  // q head (b, h) -> kv head (b, h / rep)
+  {
+    RowJobs js;
+    js.n = 2;
+    js.j[0] = RowJob{qkv, g.W, g.qo, g.Hq, T, hd, zq, b.QA, b.exQ, 0};
+    js.j[1] = RowJob{qkv, g.W, g.ko, g.Hkv, T, hd, zk, b.KB, b.exK, 0};
+    launch_rows<S>(L, js);
+  }
+  {  // S = scale Q K^T (lower tiles only)
+    GemmArgs<double> a;
+    a.M = T; a.N = T; a.K = hd; a.batch = zq;
+    a.C = P; a.ldc = T; a.offC = BatchOff{(int64_t)T * T, 0, 1, 1};
+    a.alpha = 1.0 / std::sqrt((double)hd);
+    a.tri = TRI_SKIP_UPPER;
+    OzPlanes pa, pb;
+    pa.d = b.QA; pa.ex = b.exQ; pa.nb = zq; pa.Kp = hd; pa.z = ident();
+    pb.d = b.KB; pb.ex = b.exK; pb.nb = zk; pb.Kp = hd; pb.z = kv;
+    gemm_oz_planes(L, S, pa, pb, a);
+  }
+  {
+    LaunchScope scope(L.prof, KC_ATTN, L.stream, 0, (16.0 + 8.0 + S) * zq * (T * (T + 128.0) / 2));
+    const int64_t rows = (int64_t)zq * T, plane = rows * T;
+    if (T <= 256) k_att_sm_fwd<S, 2><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
+    else if (T <= 512) k_att_sm_fwd<S, 4><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
+    else if (T <= 1024) k_att_sm_fwd<S, 8><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
+    else k_att_sm_fwd<S, 16><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+  launch_cols<S>(L, ColJob{qkv, g.W, g.vo, g.Hkv, T, hd, zk, nullptr, b.VB, b.exV});
+  {  // O = P V (k clipped to the causal part)
+    GemmArgs<double> a;
+    a.M = T; a.N = hd; a.K = T; a.batch = zq;
+    a.C = o; a.ldc = g.ldo; a.offC = BatchOff{T * g.ldo, hd, g.Hq, 1};
+    a.tri = TRI_K_LE_M;
+    OzPlanes pa, pb;
+    pa.d = b.PA; pa.ex = b.exP; pa.nb = zq; pa.Kp = T; pa.z = ident();
+    pb.d = b.VB; pb.ex = b.exV; pb.nb = zk; pb.Kp = T; pb.z = kv;
+    gemm_oz_planes(L, S, pa, pb, a);
+  }
+}
+
+template <int S>
+static void bwd(const Launch& L, const AttnShape& g, const double* qkv, const double* P, const double* dO, double* dP,
+                double* dqkv) {
+  const int zq = g.nseq * g.Hq, zk = g.nseq * g.Hkv, T = g.Tn, hd = g.hd, rep = g.Hq / g.Hkv;
+  Bufs b = carve(g, S, (uint8_t*)L.ws->get(attn_oz_ws_bytes(L, g), L.stream));
+  const BatchOff kv{g.Hkv, 1, g.Hq, rep};
+  const BatchOff q_of_kv{g.Hq, rep, g.Hkv, 1};  // kv head (b, gk) -> q head (b, gk rep) (+ r via z0)
+  const double scale = 1.0 / std::sqrt((double)hd);
+  {
+    RowJobs js;
+    js.n = 2;
+    js.j[0] = RowJob{dO, g.ldo, 0, g.Hq, T, hd, zq, b.DOA, b.exDO, 0};
+    js.j[1] = RowJob{qkv, g.W, g.vo, g.Hkv, T, hd, zk, b.VR, b.exVR, 0};
+    launch_rows<S>(L, js);
+  }
+  {  // dP = dO V^T (lower tiles only)
+    GemmArgs<double> a;
+    a.M = T; a.N = T; a.K = hd; a.batch = zq;
+    a.C = dP; a.ldc = T; a.offC = BatchOff{(int64_t)T * T, 0, 1, 1};
+    a.tri = TRI_SKIP_UPPER;
+    OzPlanes pa, pb;
+    pa.d = b.DOA; pa.ex = b.exDO; pa.nb = zq; pa.Kp = hd; pa.z = ident();
+    pb.d = b.VR; pb.ex = b.exVR; pb.nb = zk; pb.Kp = hd; pb.z = kv;
+    gemm_oz_planes(L, S, pa, pb, a);
+  }
+  {
+    LaunchScope scope(L.prof, KC_ATTN, L.stream, 0, (32.0 + 3.0 * S) * zq * (T * (T + 128.0) / 2));
+    k_att_sm_bwd<S><<<zq * (T / 32), 512, 0, L.stream>>>(P, dP, T, b.PT, b.DSA, b.DST, b.exR, b.exE,
+                                                           (int64_t)zq * T * T);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+  }
+  launch_cols<S>(L, ColJob{qkv, g.W, g.ko, g.Hkv, T, hd, zk, nullptr, b.KT, b.exKT});
+  launch_cols<S>(L, ColJob{dO, g.ldo, 0, g.Hq, T, hd, zq, b.exR, b.DOT, b.exDOT});
+  launch_cols<S>(L, ColJob{qkv, g.W, g.qo, g.Hq, T, hd, zq, b.exE, b.QT, b.exQT});
+  // dV[b, gk] = sum_r (P~_h)^T dO'_h,  h = gk rep + r  (k = query >= the tile's first key)
+  for (int r = 0; r < rep; ++r) {
+    GemmArgs<double> a;
+    a.M = T; a.N = hd; a.K = T; a.batch = zk;
+    a.C = dqkv + g.vo; a.ldc = g.W; a.offC = BatchOff{T * g.W, hd, g.Hkv, 1};
+    a.accumulate = r > 0;
+    a.tri = TRI_K_GE_M;
+    OzPlanes pa, pb;
+    pa.d = b.PT; pa.ex = nullptr; pa.nb = zq; pa.Kp = T; pa.z0 = r; pa.z = q_of_kv;
+    pb.d = b.DOT; pb.ex = b.exDOT; pb.nb = zq; pb.Kp = T; pb.z0 = r; pb.z = q_of_kv;
+    gemm_oz_planes(L, S, pa, pb, a);
+  }
+  {  // dQ = scale dS K (k = key <= the tile's last query)
+    GemmArgs<double> a;
+    a.M = T; a.N = hd; a.K = T; a.batch = zq;
+    a.C = dqkv + g.qo; a.ldc = g.W; a.offC = BatchOff{T * g.W, hd, g.Hq, 1};
+    a.alpha = scale;
+    a.tri = TRI_K_LE_M;
+    OzPlanes pa, pb;
+    pa.d = b.DSA; pa.ex = b.exE; pa.nb = zq; pa.Kp = T; pa.z = ident();
+    pb.d = b.KT; pb.ex = b.exKT; pb.nb = zk; pb.Kp = T; pb.z = kv;
+    gemm_oz_planes(L, S, pa, pb, a);
+  }
+  // dK[b, gk] = scale sum_r (dS~_h)^T Q'_h
+  for (int r = 0; r < rep; ++r) {
+    GemmArgs<double> a;
+    a.M = T; a.N = hd; a.K = T; a.batch = zk;
+    a.C = dqkv + g.ko; a.ldc = g.W; a.offC = BatchOff{T * g.W, hd, g.Hkv, 1};
+    a.alpha = scale;
+    a.accumulate = r > 0;
+    a.tri = TRI_K_GE_M;
+    OzPlanes pa, pb;
+    pa.d = b.DST; pa.ex = nullptr; pa.nb = zq; pa.Kp = T; pa.z0 = r; pa.z = q_of_kv;
+    pb.d = b.QT; pb.ex = b.exQT; pb.nb = zq; pb.Kp = T; pb.z0 = r; pb.z = q_of_kv;
+    gemm_oz_planes(L, S, pa, pb, a);
+  }
+}
+
+}  // namespace oz
+
+bool attn_oz_eligible(const Launch& L, const AttnShape& g) {
+  static const bool off = getenv("SLQ_ATTN_DMMA") && atoi(getenv("SLQ_ATTN_DMMA")) != 0;  // A/B switch
+  return !off && L.gemm_mode == 2 && g.Tn % 128 == 0 && g.Tn <= 2048 && g.hd % 32 == 0 && g.hd <= 128 && g.Hkv > 0 &&
+         g.Hq % g.Hkv == 0 && (double)g.nseq * g.Hq * g.Tn * (double)g.Tn * g.hd >= L.oz_min_mnk;
+}
+
+size_t attn_oz_ws_bytes(const Launch& L, const AttnShape& g) {
+  if (!attn_oz_eligible(L, g)) return 0;
+  const oz::Bufs b = oz::carve(g, L.oz_S, nullptr);
+  return std::max(b.fwd_bytes, b.bwd_bytes);
+}
+
+void attention_fwd_oz(const Launch& L, const AttnShape& g, const double* qkv, double* P, double* o) {
+  switch (L.oz_S) {
+    case 4: oz::fwd<4>(L, g, qkv, P, o); break;
+    case 5: oz::fwd<5>(L, g, qkv, P, o); break;
+    case 6: oz::fwd<6>(L, g, qkv, P, o); break;
+    case 7: oz::fwd<7>(L, g, qkv, P, o); break;
+    default: throw Error(SLQ_EINVAL, "oz attention: S in 4..7");
+  }
+}
+
+void attention_bwd_oz(const Launch& L, const AttnShape& g, const double* qkv, const double* P, const double* dO,
+                      double* dP, double* dqkv) {
+  switch (L.oz_S) {
+    case 4: oz::bwd<4>(L, g, qkv, P, dO, dP, dqkv); break;
+    case 5: oz::bwd<5>(L, g, qkv, P, dO, dP, dqkv); break;
+    case 6: oz::bwd<6>(L, g, qkv, P, dO, dP, dqkv); break;
+    case 7: oz::bwd<7>(L, g, qkv, P, dO, dP, dqkv); break;
+    default: throw Error(SLQ_EINVAL, "oz attention: S in 4..7");
+  }
+}
+
+}  // namespace slq

@@ -29,6 +29,7 @@
 #include "gemm_common.cuh"
 #include "kernels.h"
 #include "tc_common.cuh"
+#include "oz_common.cuh"
 
 namespace slq {
 namespace oz {
@@ -65,12 +66,21 @@ __host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N) {
 struct OzArgs {
   int M, N, nk;          // nk: k-tiles of the whole K
   int kt_per_split, splits;
-  const int* ea;         // [M] row exponents of A
-  const int* eb;         // [N] column exponents of B
+  const int* ea;         // [nbA][M] row exponents of A (nullptr: 0)
+  const int* eb;         // [nbB][N] column exponents of B (nullptr: 0)
   int debug;  // diagnostic only (SLQ_OZ_DEBUG bits): 1 no MMAs, 2 no TMA loads, 4 no stores, 8 no TMEM drain
   int mfast;  // tile order: 1 = m fastest (the B tile is shared by the CTAs in flight and streamed
               // from DRAM once; the smaller A planes are re-read from L2), 0 = n fastest
+  // batched (attention) GEMMs over pre-sliced planes: GEMM z reads plane batch zA(z) of A (planes
+  // [S][nbA][M][Kp]) and zB(z) of B; tri: TRI_SKIP_UPPER tiles are not enumerated, TRI_K_LE_M /
+  // TRI_K_GE_M clip the tile's k range to the causal part (splits == 1 then)
+  int batch = 1, tri = 0, tiles_b = 0, nbA = 1, nbB = 1, z0A = 0, z0B = 0;
+  BatchOff zA, zB;
 };
+
+__device__ __forceinline__ int64_t boff(const BatchOff& b, int z) {
+  return (int64_t)(z / b.div) * b.outer + (int64_t)((z % b.div) / b.rep) * b.inner;
+}
 
 // 32 consecutive TMEM columns of the warp's 32 lanes (one 32-bit value per lane per column)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
@@ -83,22 +93,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
-
-// int32 (two's complement bits) -> double, exactly, with one integer op and one fp64 add (the
-// I2F.F64 conversion is a slow-path instruction): 2^52 + 2^31 + x has x + 2^31 in its low word
-__device__ __forceinline__ double i2d(uint32_t x) {
-  return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
-}
-
-// 2^e as a double (e within the normal range), built from the exponent bits
-__device__ __forceinline__ double exp2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
-
-// exponent marker of a row / column holding a NaN or an infinity: the slicing cannot represent it,
-// so the epilogue scales that output row / column by NaN (non-finite inputs give non-finite
-// outputs, as in the DMMA path; the loss then fails the SLQ_ENUMERIC check).  It is the
-// largest int, so it survives the max over partial exponents.
-constexpr int kExNaN = 0x7fffffff;
-__device__ __forceinline__ double scale_of(int e) { return e == kExNaN ? __longlong_as_double(0x7ff8000000000000ll) : exp2i(e); }
 
 // Persistent kernel: grid <= #SMs, CTA c processes work units c, c + grid, ... (unit = output
 // tile x K split).  The TMA producer runs ahead across unit boundaries (ring of STAGES k-tiles);
@@ -117,38 +111,29 @@ __host__ __device__ constexpr int oz_owner(int S, int NI, int g) {
          : S == 6  ? (g == 3 || g == 4 ? 1 : 0)
                    : (g == 2 || g == 3 ? 1 : 0);
 }
-// Up to 4 consecutive outputs (row m, columns n .. n + nc - 1) of one lane: alpha, bias, residual,
-// accumulate (or plain stores of split-K partials / ragged columns).  Activations never reach this
-// epilogue: gemm<double> runs them as a separate streaming pass (gemm_f64.cu, k_oz_act).
-__device__ __noinline__ void oz_epi_row4(const GemmArgs<double>& p, int m, int n, int nc, const double* x, bool plain,
-                                         bool vec, double* Wd, int64_t ldw) {
-  double* d = Wd + (int64_t)m * ldw + n;
-  if (plain) {
-    for (int q = 0; q < nc; ++q) d[q] = x[q];
-    return;
-  }
-  double y[4];
-  const double* rs = p.resid ? p.resid + (int64_t)m * p.ldr + n : nullptr;
-  if (nc == 4 && vec) {
-    double2 r01 = make_double2(0.0, 0.0), r23 = r01, c01 = r01, c23 = r01;
-    if (rs) {
-      r01 = *reinterpret_cast<const double2*>(rs);
-      r23 = *reinterpret_cast<const double2*>(rs + 2);
-    }
-    if (p.accumulate) {
-      c01 = *reinterpret_cast<const double2*>(d);
-      c23 = *reinterpret_cast<const double2*>(d + 2);
-    }
-    const double r[4] = {r01.x, r01.y, r23.x, r23.y}, co[4] = {c01.x, c01.y, c23.x, c23.y};
+// One 32-row x 4-column chunk of the output tile from the warp's staging tile T (row r, column c
+// at T[r * 4 + c], already row-scaled) for the epilogues that are not plain stores: lane l handles
+// rows 8 j + l / 4 (j = 0..3) of column l % 4, multiplies by its column scale and applies alpha,
+// bias, residual and accumulate.  Activations never reach this epilogue: gemm<double> runs them as
+// a separate streaming pass (gemm_f64.cu, k_oz_act).
+__device__ __noinline__ void oz_epi_chunk(const GemmArgs<double>& p, const double* T, int mrow0, int n0c, int ncol,
+                                          double sc, double* C) {
+  const int lane = threadIdx.x % 32;
+  const int cc = lane & 3;
+  const int n = n0c + cc;
+  if (cc >= ncol) return;
+  const int r0 = lane >> 2;
+  const int mmax = p.M - mrow0 - r0;  // rows 8 j + r0 with 8 j < mmax are valid
+  const double bs = p.bias ? p.bias[n] : 0.0;
+  double* dst = C + (int64_t)(mrow0 + r0) * p.ldc + n;
+  const double* rsd = p.resid ? p.resid + (int64_t)(mrow0 + r0) * p.ldr + n : nullptr;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) y[q] = p.alpha * x[q] + (p.bias ? p.bias[n + q] : 0.0) + r[q] + co[q];
-    *reinterpret_cast<double2*>(d) = make_double2(y[0], y[1]);
-    *reinterpret_cast<double2*>(d + 2) = make_double2(y[2], y[3]);
-    return;
-  }
-  for (int q = 0; q < nc; ++q) {
-    double v = p.alpha * x[q] + (p.bias ? p.bias[n + q] : 0.0) + (rs ? rs[q] : 0.0);
-    d[q] = p.accumulate ? d[q] + v : v;
+  for (int j = 0; j < 4; ++j) {
+    if (8 * j >= mmax) break;
+    double y = p.alpha * (T[(8 * j + r0) * 4 + cc] * sc) + bs;
+    if (rsd) y += rsd[(int64_t)(8 * j) * p.ldr];
+    double* d = dst + (int64_t)(8 * j) * p.ldc;
+    *d = p.accumulate ? *d + y : y;
   }
 }
 
@@ -172,22 +157,46 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + BM - 1) / BM;
-  const int nwork = tiles_n * tiles_m * o.splits;
-  // unit w -> (split, tile_m, tile_n): the larger operand's tile is the one the CTAs in flight
-  // share (o.mfast), so its digit planes stream from DRAM once and the smaller operand's planes are
-  // the ones re-read (from L2)
-  auto decode = [&](int w, int& m0, int& n0, int& sp, int& kt0, int& nloc) {
+  const int nwork = o.batch * o.tiles_b * o.splits;
+  // unit w -> (batch z, split, tile_m, tile_n): the larger operand's tile is the one the CTAs in
+  // flight share (o.mfast), so its digit planes stream from DRAM once and the smaller operand's
+  // planes are the ones re-read (from L2); TRI_SKIP_UPPER enumerates the lower tiles row by row
+  auto decode = [&](int w, int& z, int& m0, int& n0, int& sp, int& kt0, int& nloc) {
     sp = w % o.splits;
-    const int t = w / o.splits;
-    if (o.mfast) {
+    int t = w / o.splits;
+    z = t / o.tiles_b;
+    t -= z * o.tiles_b;
+    if (o.tri == TRI_K_LE_M || o.tri == TRI_K_GE_M) {
+      // k-clipped causal tiles differ in length (1 .. nk k-tiles): longest first across the whole
+      // batch, so the static round-robin hands every CTA a similar mix (largest-first balancing)
+      t = w / o.splits;
+      const int bn = o.batch * tiles_n;
+      const int rank = t / bn, rem = t - rank * bn;
+      z = rem / tiles_n;
+      n0 = (rem - z * tiles_n) * BN;
+      m0 = (o.tri == TRI_K_LE_M ? tiles_m - 1 - rank : rank) * BM;
+    } else if (o.tri == TRI_SKIP_UPPER) {
+      int mt = 0;
+      for (;;) {
+        const int c = min(tiles_n, (mt * BM + BM - 1) / BN + 1);
+        if (t < c) break;
+        t -= c;
+        ++mt;
+      }
+      m0 = mt * BM;
+      n0 = t * BN;
+    } else if (o.mfast) {
       m0 = (t % tiles_m) * BM;
       n0 = (t / tiles_m) * BN;
     } else {
       n0 = (t % tiles_n) * BN;
       m0 = (t / tiles_n) * BM;
     }
-    kt0 = sp * o.kt_per_split;
-    const int kt1 = min(o.nk, kt0 + o.kt_per_split);
+    int kb = 0, ke = o.nk;
+    if (o.tri == TRI_K_LE_M) ke = min(ke, (m0 + BM + KT - 1) / KT);
+    else if (o.tri == TRI_K_GE_M) kb = m0 / KT;
+    kt0 = kb + sp * o.kt_per_split;
+    const int kt1 = min(ke, kt0 + o.kt_per_split);
     nloc = kt1 > kt0 ? kt1 - kt0 : 0;
   };
 
@@ -215,8 +224,9 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
     if (lane == 0) {  // ---- TMA producer: all S digit planes of A and B for one k-tile per stage ----
       int it = 0;
       for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
-        int m0, n0, sp, kt0, nloc;
-        decode(w, m0, n0, sp, kt0, nloc);
+        int z, m0, n0, sp, kt0, nloc;
+        decode(w, z, m0, n0, sp, kt0, nloc);
+        const int ra = (o.z0A + (int)boff(o.zA, z)) * o.M + m0, rb = (o.z0B + (int)boff(o.zB, z)) * o.N + n0;
         for (int i = 0; i < nloc; ++i, ++it) {
           const int kt = kt0 + i, s = it % CF::STAGES;
           const uint32_t ph = (it / CF::STAGES) & 1;
@@ -230,8 +240,8 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
           mbar_expect_tx(&full[s], CF::STAGE_BYTES);
 #pragma unroll
           for (int q = 0; q < S; ++q) {
-            tma_load_2d(sa + q * CF::A_PLANE, &tmA, &full[s], kt * KT, q * o.M + m0);
-            tma_load_2d(sb + q * CF::B_PLANE, &tmB, &full[s], kt * KT, q * o.N + n0);
+            tma_load_2d(sa + q * CF::A_PLANE, &tmA, &full[s], kt * KT, q * o.nbA * o.M + ra);
+            tma_load_2d(sb + q * CF::B_PLANE, &tmB, &full[s], kt * KT, q * o.nbB * o.N + rb);
           }
         }
       }
@@ -242,8 +252,8 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
       constexpr uint32_t idesc = make_idesc_i8(BM, BN);
       int it = 0, tl = 0;
       for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
-        int m0, n0, sp, kt0, nloc;
-        decode(w, m0, n0, sp, kt0, nloc);
+        int z, m0, n0, sp, kt0, nloc;
+        decode(w, z, m0, n0, sp, kt0, nloc);
         mbar_wait(tmem_empty, (tl & 1) ^ 1);  // the previous unit's accumulators have been drained
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         uint32_t started = 0;  // the unit's accumulators have been initialised
@@ -298,13 +308,16 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
     const int c0 = ((warp - 2) / 4) * 32;
     int tl = 0;
     for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++tl) {
-      int m0, n0, sp, kt0, nloc;
-      decode(w, m0, n0, sp, kt0, nloc);
+      int z, m0, n0, sp, kt0, nloc;
+      decode(w, z, m0, n0, sp, kt0, nloc);
       // scales first (their global-load latency overlaps the wait for the accumulators):
-      // lane l holds 2^f for column n0 + c0 + l and 2^e for row m0 + lg + l
+      // lane l holds 2^f for column n0 + c0 + l and 2^e for row m0 + lg + l; alpha folds into the
+      // row scale (an exact power-of-two product, so alpha * (v 2^e 2^f) rounds identically)
       const int n_l = n0 + c0 + lane, row_l = m0 + lg + lane;
-      const double sc_l = n_l < p.N ? scale_of(o.eb[n_l]) : 0.0;
-      const double sr = (nloc > 0 && row_l < p.M) ? scale_of(o.ea[row_l]) : 0.0;
+      const double sc_l = n_l < p.N ? (o.eb ? scale_of(o.eb[(o.batch > 1 || o.z0B ? o.z0B + boff(o.zB, z) : 0) * p.N + n_l]) : 1.0) : 0.0;
+      const bool fold = o.splits == 1 && !p.bias && !p.resid && !p.accumulate;
+      double sr = (nloc > 0 && row_l < p.M) ? (o.ea ? scale_of(o.ea[(o.batch > 1 || o.z0A ? o.z0A + boff(o.zA, z) : 0) * p.M + row_l]) : 1.0) : 0.0;
+      if (fold) sr *= p.alpha;
       mbar_wait(tmem_full, tl & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       double v[32];
@@ -362,30 +375,37 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
       }
-      // Stores straight from registers: lane l owns output row m0 + lg + l and writes 4 consecutive
-      // columns per chunk as two 16-byte stores (one full 32-byte sector per lane).  (The previous
-      // shared-memory transpose + out-of-line per-chunk epilogue cost ~200 instructions per chunk and
-      // made the epilogue's store phase, not the MMAs, the per-tile period of the short-K GEMMs.)
+      // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
+      // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
+      // sectors) instead of 32 rows x 8-16 bytes (register-direct row stores measured 14% slower on
+      // the write-heavy c3 logits GEMM).  Plain stores (split-K partials, or no bias / residual /
+      // accumulate, alpha folded into the row scale) stay inline; the rest is one out-of-line
+      // function per chunk (the kernel must stay inside the instruction cache its MMA-issuing warps
+      // share with the epilogue warps).
       const int ncol = p.N - (n0 + c0);  // valid columns of this warp's 32 (may be <= 0)
-      const int m = m0 + lg + lane;
-      const bool plain = o.splits > 1 || (!p.bias && !p.resid && !p.accumulate && p.alpha == 1.0);
-      double* Wd = o.splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C;
+      const bool plain = o.splits > 1 || fold;
+      double* Wd = o.splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C + (o.batch > 1 ? boff(p.offC, z) : 0);
       const int64_t ldw = o.splits > 1 ? p.N : p.ldc;
-      const bool vec = (ldw % 2) == 0 && (((uintptr_t)Wd) & 15) == 0 &&
-                       (plain || !p.resid || ((p.ldr % 2) == 0 && (((uintptr_t)p.resid) & 15) == 0));
-      double* dst = Wd + (int64_t)m * ldw + (n0 + c0);
+      double* T = stage_t + (warp - 2) * 128;
+      const int cc = lane & 3, r0 = lane >> 2;
+      const int mmax = p.M - (m0 + lg) - r0;  // rows 8 j + r0 with 8 j < mmax are valid
+      double* dst = Wd + (int64_t)(m0 + lg + r0) * ldw + (n0 + c0 + cc);
 #pragma unroll
       for (int c = 0; c < ((o.debug & 4) ? 0 : 32); c += 4) {
         if (c >= ncol) break;  // (warp-uniform)
-        double x[4];
+        __syncwarp();
+        *reinterpret_cast<double2*>(&T[lane * 4]) = make_double2(v[c] * sr, v[c + 1] * sr);
+        *reinterpret_cast<double2*>(&T[lane * 4 + 2]) = make_double2(v[c + 2] * sr, v[c + 3] * sr);
+        __syncwarp();
+        const double sc = __shfl_sync(0xffffffffu, sc_l, c + cc);
+        if (plain) {
+          if (c + cc < ncol) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = v[c + q] * sr * __shfl_sync(0xffffffffu, sc_l, c + q);
-        if (m >= p.M) continue;
-        if (plain && vec && c + 4 <= ncol) {
-          *reinterpret_cast<double2*>(dst + c) = make_double2(x[0], x[1]);
-          *reinterpret_cast<double2*>(dst + c + 2) = make_double2(x[2], x[3]);
+            for (int j = 0; j < 4; ++j)
+              if (8 * j < mmax) dst[(int64_t)(8 * j) * ldw + c] = T[(8 * j + r0) * 4 + cc] * sc;
+          }
         } else {
-          oz_epi_row4(p, m, n0 + c0 + c, min(4, ncol - c), x, plain, vec, Wd, ldw);
+          oz_epi_chunk(p, T, m0 + lg, n0 + c0 + c, ncol - c, sc, Wd);
         }
       }
     }
@@ -645,34 +665,6 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-// The S digits of x for row exponent e (|x| < 2^e): the truncated base-128 expansion of x 2^-e,
-// d_p = trunc(128 r_p), r_{p+1} = 128 r_p - d_p.  Computed exactly in integers:
-// Q = trunc(x 2^(7S - e)) (an exact power-of-two scaling, |Q| < 2^(7S)), d_p = sign(x) *
-// ((|Q| >> 7 (S - 1 - p)) & 127) -- the same digits as the fp64 recurrence.
-template <int S>
-__device__ __forceinline__ void digits(double x, int e, int8_t* d) {
-  const long long q = __double2ll_rz(x * __longlong_as_double((long long)(7 * S - e + 1023) << 52));
-  const long long mag = q < 0 ? -q : q;
-#pragma unroll
-  for (int p = 0; p < S; ++p) {
-    const int v = (int)((mag >> (7 * (S - 1 - p))) & 127);
-    d[p] = (int8_t)(q < 0 ? -v : v);
-  }
-}
-
-// !(|x| <= DBL_MAX): NaN or +-inf
-__device__ __forceinline__ bool nonfinite(double x) { return !(fabs(x) <= 1.7976931348623157e308); }
-
-__device__ __forceinline__ int exp_of(double mx, bool nf = false) {
-  if (nf) return kExNaN;
-  if (!(mx > 0.0)) return 0;
-  int e;
-  frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)  ->  mx < 2^e
-  return e;
-}
-
-constexpr int kExNone = (int)0x80808080;  // "no nonzero element" marker of a partial exponent
-
 // ---- merged slicing of both GEMM operands (one or two launches per GEMM) ----
 // A job slices one operand into S digit planes [S][rows][Kp] and row exponents ex[rows].
 // kmajor: element (r, k) at X[r * ld + k]; else at X[k * ld + r] (the exponent pass then writes
@@ -683,14 +675,17 @@ struct SliceJob {
   int rows, K, Kp, kmajor;
   int8_t* out;
   int* ex;
-  int* xp;       // [ceil(K / 256)][rows] partial exponents (cols path)
+  int* xp;       // [ceil(K / kcol)][rows] partial exponents (cols path)
   int blocks0;   // first block of this job in the launch
+  int kcol;      // k extent of one exponent-pass block (cols path)
 };
 struct SliceJobs {
   SliceJob j[2];
   int n;
 };
-constexpr int kColK = 256;  // k extent of one exponent-pass block
+constexpr int kColK = 256;     // k extent of one exponent-pass block
+constexpr int kColKMin = 64;   // ... for operands whose exponent pass would not fill two waves of SMs
+static int col_kblk(int rows, int K) { return ceil_div(rows, 32) * ceil_div(K, kColK) >= 2 * 148 ? kColK : kColKMin; }
 
 __device__ __forceinline__ const SliceJob& job_of(const SliceJobs& js, int b) {
   return (js.n > 1 && b >= js.j[1].blocks0) ? js.j[1] : js.j[0];
@@ -705,7 +700,7 @@ __global__ void __launch_bounds__(256) k_oz_colexp2(const __grid_constant__ Slic
   __shared__ double red[8][33];
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   const int r = r0 + tx;
-  const int k0 = kb * kColK, k1 = min(jb.K, k0 + kColK);
+  const int k0 = kb * jb.kcol, k1 = min(jb.K, k0 + jb.kcol);
   double mx = 0.0;
   bool nf = false;
   if (r < jb.rows) {
@@ -793,7 +788,7 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
   if (threadIdx.x < 32) {
     int e = kExNone;
     if (r < jb.rows) {
-      const int nkb = (jb.K + kColK - 1) / kColK;
+      const int nkb = (jb.K + jb.kcol - 1) / jb.kcol;
       for (int kb = 0; kb < nkb; ++kb) e = max(e, jb.xp[(int64_t)kb * jb.rows + r]);
     }
     if (kblk == 0 && r < jb.rows) jb.ex[r] = e == kExNone ? 0 : e;
@@ -872,7 +867,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   plan_splits(S, tiles, nk, KT, splits, ktps);
   const size_t a_bytes = align256((size_t)S * M * Kp), b_bytes = align256((size_t)S * N * Kp);
   const size_t e_bytes = align256(4 * (size_t)(M + N));
-  const int nkb = (int)ceil_div(K, kColK);
+  const int nkb = (int)ceil_div(K, kColKMin);  // (sized for the finer exponent blocks)
   const size_t xp_bytes = align256(4 * (size_t)(M + N) * nkb);
   const size_t w_bytes = splits > 1 ? align256(8 * (size_t)M * N * splits) : 0;
   uint8_t* base = (uint8_t*)L.ws->get(a_bytes + b_bytes + e_bytes + xp_bytes + w_bytes, L.stream);
@@ -889,8 +884,8 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     // B(k, n) = B[k * sBk + n * sBn]: K-contiguous rows per n when sBk == 1 (pitch sBn)
     SliceJobs js;
     js.n = 2;
-    js.j[0] = SliceJob{a.A, a.sAk == 1 ? a.sAm : a.sAk, M, K, Kp, a.sAk == 1 ? 1 : 0, as, ea, xpa, 0};
-    js.j[1] = SliceJob{a.B, a.sBk == 1 ? a.sBn : a.sBk, N, K, Kp, a.sBk == 1 ? 1 : 0, bs, eb, xpb, 0};
+    js.j[0] = SliceJob{a.A, a.sAk == 1 ? a.sAm : a.sAk, M, K, Kp, a.sAk == 1 ? 1 : 0, as, ea, xpa, 0, col_kblk(M, K)};
+    js.j[1] = SliceJob{a.B, a.sBk == 1 ? a.sBn : a.sBk, N, K, Kp, a.sBk == 1 ? 1 : 0, bs, eb, xpb, 0, col_kblk(N, K)};
     // exponent pass (cols-path jobs only)
     int nexp = 0;
     SliceJobs je;
@@ -899,7 +894,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
       if (!js.j[i].kmajor) {
         SliceJob jj = js.j[i];
         jj.blocks0 = nexp;
-        nexp += (int)(ceil_div(jj.rows, 32) * ceil_div(K, kColK));
+        nexp += (int)(ceil_div(jj.rows, 32) * ceil_div(K, jj.kcol));
         je.j[je.n++] = jj;
       }
     if (je.n == 1) je.j[1] = je.j[0];
@@ -922,6 +917,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   static const int dbg = getenv("SLQ_OZ_DEBUG") ? atoi(getenv("SLQ_OZ_DEBUG")) : 0;
   static const int order = getenv("SLQ_OZ_ORDER") ? atoi(getenv("SLQ_OZ_ORDER")) : -1;  // 0 n-fast, 1 m-fast
   OzArgs o{M, N, nk, ktps, splits, ea, eb, dbg, order >= 0 ? order : (N > M ? 1 : 0)};
+  o.tiles_b = tiles;
   {
     LaunchScope scope(L.prof, KC_GEMM_I8, L.stream, 2.0 * M * N * (double)K * CF::NPROD,
                       (double)S * ((double)M * K + (double)N * K) + 8.0 * M * N);
@@ -943,6 +939,39 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   }
 }
 
+// batched / causal GEMM over pre-sliced digit planes (the attention path): no slicing, no split-K
+template <int S, int BN, int NI>
+void run_planes(const Launch& L, const OzPlanes& A, const OzPlanes& B, const GemmArgs<double>& a) {
+  using CF = Cfg<S, BN, BK>;
+  static bool attr = false;
+  if (!attr) {
+    SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN, BK, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    attr = true;
+  }
+  const int M = a.M, N = a.N, K = a.K;
+  const int nk = (int)ceil_div(K, BK);
+  const int tm = (int)ceil_div(M, BM), tn = (int)ceil_div(N, BN);
+  int tiles_b = tm * tn;
+  if (a.tri == TRI_SKIP_UPPER) {
+    tiles_b = 0;
+    for (int mt = 0; mt < tm; ++mt) tiles_b += std::min(tn, (mt * BM + BM - 1) / BN + 1);
+  }
+  const CUtensorMap ta = make_map_i8(A.d, (int64_t)S * A.nb * M, A.Kp, A.Kp, BM, BK);
+  const CUtensorMap tb = make_map_i8(B.d, (int64_t)S * B.nb * N, B.Kp, B.Kp, BN, BK);
+  OzArgs o{M, N, nk, nk, 1, A.ex, B.ex, 0, 0};
+  o.batch = a.batch; o.tri = a.tri; o.tiles_b = tiles_b;
+  o.nbA = A.nb; o.nbB = B.nb; o.z0A = A.z0; o.z0B = B.z0; o.zA = A.z; o.zB = B.z;
+  // algorithmic work: the causal half (T + 1) / 2T of the square for the triangular contractions
+  const double frac = a.tri == TRI_NONE ? 1.0 : (a.tri == TRI_SKIP_UPPER ? (M + 1.0) / (2.0 * M) : (K + 1.0) / (2.0 * K));
+  LaunchScope scope(L.prof, KC_GEMM_I8, L.stream, 2.0 * M * N * (double)K * a.batch * CF::NPROD * frac,
+                    (double)S * ((double)M * K + (double)N * K) * a.batch * frac + 8.0 * M * N * a.batch);
+  const int64_t nwork = (int64_t)a.batch * tiles_b;
+  k_oz_gemm<S, BN, BK, NI><<<(int)std::min<int64_t>(nwork, 148), 32 * (CF::NE + NI + 1), CF::SMEM, L.stream>>>(
+      ta, tb, o, a, nullptr);
+  SLQ_CUDA(cudaGetLastError());
+  ++*L.launches;
+}
+
 }  // namespace oz
 
 // output tile width of the production kernel for S digit planes: the S accumulators of BN columns
@@ -957,7 +986,7 @@ size_t oz_ws_bytes(int M, int N, int K, int S) {
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, oz_bn(S)));
   int splits, ktps;
   plan_splits(S, tiles, nk, BK, splits, ktps);
-  const int nkb = (int)ceil_div(K, kColK);
+  const int nkb = (int)ceil_div(K, kColKMin);
   return align256((size_t)S * M * Kp) + align256((size_t)S * N * Kp) + align256(4 * (size_t)(M + N)) +
          align256(4 * (size_t)(M + N) * nkb) + (splits > 1 ? align256(8 * (size_t)M * N * splits) : 0);
 }
@@ -991,6 +1020,23 @@ void gemm_oz(const Launch& L, const GemmArgs<double>& a, int S) {
         oz::run<7, 64, false, oz::BK, 2>(L, a);
       break;
     }
+  }
+}
+
+void gemm_oz_planes(const Launch& L, int S, const OzPlanes& A, const OzPlanes& B, const GemmArgs<double>& a) {
+  SLQ_CHECK_ARG(a.M > 0 && a.N > 0 && a.K > 0 && a.batch >= 1 && A.Kp == B.Kp && A.Kp % 16 == 0 && A.Kp >= a.K,
+                "oz planes gemm: shapes");
+  // head-dimension outputs (N <= 128): 128 x 64 tiles; S = 5 otherwise on 128 x 96
+  const bool narrow = a.N <= 128;
+  switch (S) {
+    case 4: oz::run_planes<4, 64, 1>(L, A, B, a); break;
+    case 5:
+      if (narrow) oz::run_planes<5, 64, 2>(L, A, B, a);
+      else oz::run_planes<5, 96, 2>(L, A, B, a);
+      break;
+    case 6: oz::run_planes<6, 64, 2>(L, A, B, a); break;
+    case 7: oz::run_planes<7, 64, 2>(L, A, B, a); break;
+    default: throw Error(SLQ_EINVAL, "oz planes gemm: S in 4..7");
   }
 }
 

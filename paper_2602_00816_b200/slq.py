@@ -4,7 +4,7 @@ from __future__ import annotations
 import ctypes
 import os
 import sys
-from typing import Optional, Tuple
+from typing import List, Optional, Tuple
 
 import numpy as np
 
@@ -98,6 +98,7 @@ def lib() -> ctypes.CDLL:
         "slq_diag_dmma_peak": (I32, [I32, P]),
         "slq_diag_gemm_f64": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
         "slq_diag_oz_check": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
+        "slq_diag_attn_oz": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
         "slq_diag_watchdog": (I32, [P, I32, D]),
         "slq_nonfinite_seq": (I32, [P, P]),
         "slq_cg": (I32, [P, P, P, D, I32, D, P, P]),
@@ -213,6 +214,16 @@ def oz_check(M: int, N: int, K: int, a_kmajor: bool = True, b_kmajor: bool = Tru
     _check(lib().slq_diag_oz_check(device, M, N, K, int(a_kmajor), int(b_kmajor), S, iters, ctypes.byref(e),
                                    ctypes.byref(t)))
     return e.value, t.value
+
+
+def attn_oz_check(nseq: int, Tn: int, Hq: int, Hkv: int, hd: int, S: int = 5, iters: int = 0,
+                  device: int = 0) -> Tuple[List[float], Tuple[float, float]]:
+    """Causal attention fwd + bwd on random data, FP64_OZ path (batched INT8 Ozaki GEMMs) vs the
+    FP64 DMMA path: ([max-norm relative error of O, dQ, dK, dV], (ms DMMA, ms Ozaki))."""
+    e = (ctypes.c_double * 4)()
+    t = (ctypes.c_double * 2)()
+    _check(lib().slq_diag_attn_oz(device, nseq, Tn, Hq, Hkv, hd, S, iters, e, t))
+    return list(e), (t[0], t[1])
 
 
 def kernel_class_names():
