@@ -24,7 +24,7 @@ void slq_average(const double* nodes, const double* weights, const int32_t* mc, 
 const char* kernel_class_name(int c) {
   static const char* names[KC_COUNT] = {"gemm", "attention", "norm", "cross_entropy", "embedding",
                                         "elementwise", "perturb", "fd_lanczos", "reorth", "vector", "gemm_i8",
-                                        "oz_slice"};
+                                        "oz_slice", "attn_i8"};
   return (c >= 0 && c < KC_COUNT) ? names[c] : "?";
 }
 

@@ -44,6 +44,7 @@ enum KernelClass {
   KC_VEC,          // other vector ops (probe, normalise, reductions)
   KC_GEMM_I8,      // fp64 GEMMs as tcgen05 INT8 digit products (Ozaki); flops = INT8 ops issued
   KC_OZ_SLICE,     // Ozaki operand scaling + digit slicing (HBM / L2 bound)
+  KC_ATTN_I8,      // the causal attention contractions as batched INT8 Ozaki GEMMs (oz_attn.cu)
   KC_COUNT
 };
 const char* kernel_class_name(int c);

@@ -563,38 +563,64 @@ __global__ void __launch_bounds__(1024, 1) k_cross_entropy(T* __restrict__ logit
   const int b = row / Tn, t = row % Tn;
   const int y = tgt[(int64_t)b * tgt_stride + t];
   __shared__ T red[32], red2[32];
-  // one read of the row for the online (max, sum of exponentials); one read + write for the gradient.
-  // 1024-thread blocks, one per SM (launch bounds): the rows in flight (148 x V x 8 B for V = 50257:
-  // 60 MB) stay in L2 for the second sweep, and eight loads per thread are in flight in each sweep
-  T mx = -INFINITY, sm = T(0);
-  const int bs = blockDim.x;
+  // Three sweeps over the row, one exp per element: the max; e_j = exp(z_j - max) stored in place
+  // with their sum; the gradient e_j / sum - [j == y] (scaled).  1024-thread blocks, one per SM
+  // (launch bounds): the rows in flight (148 x V x 8 B = 60 MB for V = 50257) stay in L2, so the
+  // second and third sweeps cost no DRAM traffic; the kernel is bound by the fp64 exp (the online
+  // (max, sum) form needed a second exp per element in the gradient sweep, serially dependent)
+  const int bs = blockDim.x, nw = bs / kWarp, lane = threadIdx.x % kWarp, wid = threadIdx.x / kWarp;
+  const T zy = z[y];  // (read before the second sweep overwrites the row)
+  T mx = -INFINITY;
+  bool bad = false;
   for (int j0 = threadIdx.x; j0 < V; j0 += 8 * bs) {
     T x[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = j0 + i * bs < V ? z[j0 + i * bs] : T(-INFINITY);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) online_add(mx, sm, x[i]);
+    for (int i = 0; i < 8; ++i) {
+      mx = max(mx, x[i]);
+      bad |= x[i] != x[i];
+    }
   }
-  warp_online(mx, sm);
-  if (threadIdx.x % kWarp == 0) {
-    red[threadIdx.x / kWarp] = mx;
-    red2[threadIdx.x / kWarp] = sm;
-  }
+  mx = warp_max(mx);
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) red[wid] = bad ? T(NAN) : mx;
   __syncthreads();
   if (threadIdx.x < kWarp) {
-    const bool ok = threadIdx.x < blockDim.x / kWarp;
-    T m = ok ? red[threadIdx.x] : T(-INFINITY), s2 = ok ? red2[threadIdx.x] : T(0);
-    warp_online(m, s2);
-    if (threadIdx.x == 0) {
-      red[0] = m;
-      red2[0] = s2;
-    }
+    T m = threadIdx.x < nw ? red[threadIdx.x] : T(-INFINITY);
+    const bool b2 = __any_sync(0xffffffffu, m != m);
+    m = warp_max(m);
+    if (threadIdx.x == 0) red[0] = b2 ? T(NAN) : m;
   }
   __syncthreads();
   mx = red[0];
+  __syncthreads();
+  T sm = T(0);
+  for (int j0 = threadIdx.x; j0 < V; j0 += 8 * bs) {
+    T x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = j0 + i * bs < V ? z[j0 + i * bs] : T(0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (j0 + i * bs < V) {
+        x[i] = dexp(x[i] - mx);
+        sm += x[i];
+        z[j0 + i * bs] = x[i];
+      }
+    }
+  }
+  sm = warp_sum(sm);
+  if (lane == 0) red2[wid] = sm;
+  __syncthreads();
+  if (threadIdx.x < kWarp) {
+    T s2 = threadIdx.x < nw ? red2[threadIdx.x] : T(0);
+    s2 = warp_sum(s2);
+    if (threadIdx.x == 0) red2[0] = s2;
+  }
+  __syncthreads();
   const T sum = red2[0];
   const T lse = mx + log(sum);
-  if (threadIdx.x == 0) loss_rows[row] = (double)(lse - z[y]);
+  if (threadIdx.x == 0) loss_rows[row] = (double)(lse - zy);
   __syncthreads();
   const T inv = T(1) / sum, scale = (T)inv_ntok;
   for (int j0 = threadIdx.x; j0 < V; j0 += 8 * bs) {
@@ -605,7 +631,7 @@ __global__ void __launch_bounds__(1024, 1) k_cross_entropy(T* __restrict__ logit
     for (int i = 0; i < 8; ++i) {
       const int j = j0 + i * bs;
       if (j < V) {
-        T p = dexp(x[i] - mx) * inv;
+        T p = x[i] * inv;
         if (j == y) p -= T(1);
         z[j] = p * scale;
       }

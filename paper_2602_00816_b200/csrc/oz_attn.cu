@@ -208,6 +208,11 @@ __global__ void __launch_bounds__(512) k_att_cols(const __grid_constant__ ColJob
 template <int S, int V>
 __global__ void __launch_bounds__(128) k_att_sm_fwd(double* __restrict__ P, int T, int8_t* __restrict__ out,
                                                     int* __restrict__ ex, int64_t plane) {
+  // V values per thread as V / 4 groups of 4 consecutive keys j = 4 (tid + 128 g) + k: 32-byte loads,
+  // one packed word per digit plane and group (the byte-per-element stores made this kernel
+  // issue-bound)
+  constexpr int G = V / 4;
+  static_assert(V % 4 == 0, "groups of 4");
   __shared__ double red[4];
   const int row = blockIdx.x;  // (32-bit: rows < 2^31)
   const int q = row - (row / T) * T;
@@ -217,10 +222,18 @@ __global__ void __launch_bounds__(128) k_att_sm_fwd(double* __restrict__ P, int 
   double v[V];
   double mx = -INFINITY;
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const int j = tid + 128 * i;
-    v[i] = j <= q ? s[j] : -INFINITY;
-    mx = nanmax(mx, v[i]);
+  for (int g = 0; g < G; ++g) {
+    const int j0 = 4 * (tid + 128 * g);
+    if (j0 <= q) {
+      const double2 a = *reinterpret_cast<const double2*>(s + j0);
+      const double2 b = *reinterpret_cast<const double2*>(s + j0 + 2);
+      v[4 * g] = a.x; v[4 * g + 1] = a.y; v[4 * g + 2] = b.x; v[4 * g + 3] = b.y;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (j0 + k > q) v[4 * g + k] = -INFINITY;
+      mx = nanmax(mx, v[4 * g + k]);
+    }
   }
   mx = warp_nanmax(mx);
   if (lane == 0) red[wid] = mx;
@@ -230,7 +243,7 @@ __global__ void __launch_bounds__(128) k_att_sm_fwd(double* __restrict__ P, int 
   double sum = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    if (tid + 128 * i <= q) {
+    if (4 * (tid + 128 * (i / 4)) + (i % 4) <= q) {
       v[i] = exp(v[i] - mx);
       sum += v[i];
     }
@@ -244,15 +257,18 @@ __global__ void __launch_bounds__(128) k_att_sm_fwd(double* __restrict__ P, int 
   if (tid == 0) ex[row] = e;
   const int jend = min(T, (q / 128 + 1) * 128);
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const int j = tid + 128 * i;
-    if (j < jend) {
-      const double p = j <= q ? v[i] * inv : 0.0;
-      s[j] = p;
-      int8_t dg[S];
-      digits<S>(p, ed, dg);
+  for (int g = 0; g < G; ++g) {
+    const int j0 = 4 * (tid + 128 * g);
+    if (j0 < jend) {
+      double p[4];
 #pragma unroll
-      for (int qd = 0; qd < S; ++qd) orow[qd * plane + j] = dg[qd];
+      for (int k = 0; k < 4; ++k) p[k] = j0 + k <= q ? v[4 * g + k] * inv : 0.0;
+      *reinterpret_cast<double2*>(s + j0) = make_double2(p[0], p[1]);
+      *reinterpret_cast<double2*>(s + j0 + 2) = make_double2(p[2], p[3]);
+      uint32_t w[S];
+      digits4<S>(p, ed, w);
+#pragma unroll
+      for (int qd = 0; qd < S; ++qd) *reinterpret_cast<uint32_t*>(orow + qd * plane + j0) = w[qd];
     }
   }
 }
@@ -271,8 +287,11 @@ __global__ void __launch_bounds__(512, 2) k_att_sm_bwd(const double* __restrict_
                                                        int T, int8_t* __restrict__ pt, int8_t* __restrict__ dsa,
                                                        int8_t* __restrict__ dst, int* __restrict__ exr,
                                                        int* __restrict__ exe, int64_t plane) {
-  __shared__ __align__(16) uint8_t tp[S][32][64];
-  __shared__ __align__(16) uint8_t td[S][32][64];
+  // chunk width: 128 keys (4 per lane, packed digit words) while the two [S][32][CW] tiles fit the
+  // 48 KB of static shared memory, else 64
+  constexpr int CW = S <= 5 ? 128 : 64, KPL = CW / 32;
+  __shared__ __align__(16) uint8_t tp[S][32][CW];
+  __shared__ __align__(16) uint8_t td[S][32][CW];
   const int cpr = T / 32;
   const int64_t zq = blockIdx.x / cpr;
   const int q0 = (blockIdx.x % cpr) * 32;
@@ -327,47 +346,69 @@ __global__ void __launch_bounds__(512, 2) k_att_sm_bwd(const double* __restrict_
     ed[u] = e == kExNaN ? 0 : e;
   }
   const int kend = min(T, (q0 / 128 + 1) * 128);
-  for (int c0 = 0; c0 < kend; c0 += 64) {
-    const int j = c0 + 2 * lane;
-    double2 a[2], c[2];
+  for (int c0 = 0; c0 < kend; c0 += CW) {
+    const int j = c0 + KPL * lane;
+    double pv[2][KPL], gv[2][KPL];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t ro = (zq * T + q0 + 2 * warp + u) * (int64_t)T;
-      a[u] = *reinterpret_cast<const double2*>(P + ro + j);
-      c[u] = *reinterpret_cast<const double2*>(dP + ro + j);
+#pragma unroll
+      for (int k = 0; k < KPL; k += 2) {
+        const double2 a = *reinterpret_cast<const double2*>(P + ro + j + k);
+        const double2 c = *reinterpret_cast<const double2*>(dP + ro + j + k);
+        pv[u][k] = a.x; pv[u][k + 1] = a.y;
+        gv[u][k] = c.x; gv[u][k + 1] = c.y;
+      }
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int q = q0 + 2 * warp + u;
-      const double pv[2] = {a[u].x, a[u].y}, gv[2] = {c[u].x, c[u].y};
-      uint16_t ws[S], wp[S];
+      double xp[KPL], xs[KPL];
 #pragma unroll
-      for (int qd = 0; qd < S; ++qd) ws[qd] = wp[qd] = 0;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const bool in = j + i <= q;
-        int8_t dgp[S], dgs[S];
-        digits<S>(in ? pv[i] : 0.0, rd[u], dgp);
-        digits<S>(in ? pv[i] * (gv[i] - Dr[u]) : 0.0, ed[u], dgs);
-#pragma unroll
-        for (int qd = 0; qd < S; ++qd) {
-          ws[qd] |= (uint16_t)((uint8_t)dgs[qd] << (8 * i));
-          wp[qd] |= (uint16_t)((uint8_t)dgp[qd] << (8 * i));
-        }
+      for (int k = 0; k < KPL; ++k) {
+        const bool in = j + k <= q;
+        xp[k] = in ? pv[u][k] : 0.0;
+        xs[k] = in ? pv[u][k] * (gv[u][k] - Dr[u]) : 0.0;
       }
       int8_t* arow = dsa + (zq * T + q) * (int64_t)T;
+      if constexpr (KPL == 4) {
+        uint32_t ws[S], wp[S];
+        digits4<S>(xs, ed[u], ws);
+        digits4<S>(xp, rd[u], wp);
 #pragma unroll
-      for (int qd = 0; qd < S; ++qd) {
-        *reinterpret_cast<uint16_t*>(arow + qd * plane + j) = ws[qd];
-        *reinterpret_cast<uint16_t*>(&td[qd][2 * warp + u][2 * lane]) = ws[qd];
-        *reinterpret_cast<uint16_t*>(&tp[qd][2 * warp + u][2 * lane]) = wp[qd];
+        for (int qd = 0; qd < S; ++qd) {
+          *reinterpret_cast<uint32_t*>(arow + qd * plane + j) = ws[qd];
+          *reinterpret_cast<uint32_t*>(&td[qd][2 * warp + u][KPL * lane]) = ws[qd];
+          *reinterpret_cast<uint32_t*>(&tp[qd][2 * warp + u][KPL * lane]) = wp[qd];
+        }
+      } else {
+        uint16_t ws[S], wp[S];
+#pragma unroll
+        for (int qd = 0; qd < S; ++qd) ws[qd] = wp[qd] = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          int8_t dgp[S], dgs[S];
+          digits<S>(xp[k], rd[u], dgp);
+          digits<S>(xs[k], ed[u], dgs);
+#pragma unroll
+          for (int qd = 0; qd < S; ++qd) {
+            ws[qd] |= (uint16_t)((uint8_t)dgs[qd] << (8 * k));
+            wp[qd] |= (uint16_t)((uint8_t)dgp[qd] << (8 * k));
+          }
+        }
+#pragma unroll
+        for (int qd = 0; qd < S; ++qd) {
+          *reinterpret_cast<uint16_t*>(arow + qd * plane + j) = ws[qd];
+          *reinterpret_cast<uint16_t*>(&td[qd][2 * warp + u][KPL * lane]) = ws[qd];
+          *reinterpret_cast<uint16_t*>(&tp[qd][2 * warp + u][KPL * lane]) = wp[qd];
+        }
       }
     }
     __syncthreads();
     // transposed rows: thread (array, plane, key kk) gathers queries q0 .. q0 + 31 of key c0 + kk
-    for (int idx = threadIdx.x; idx < 2 * S * 64; idx += 512) {
-      const int kk = idx % 64, qd = (idx / 64) % S, arr = idx / (64 * S);
-      const uint8_t(*src)[64] = arr ? td[qd] : tp[qd];
+    for (int idx = threadIdx.x; idx < 2 * S * CW; idx += 512) {
+      const int kk = idx % CW, qd = (idx / CW) % S, arr = idx / (CW * S);
+      const uint8_t(*src)[CW] = arr ? td[qd] : tp[qd];
       uint32_t w[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
@@ -490,8 +531,7 @@ static void fwd(const Launch& L, const AttnShape& g, const double* qkv, double* 
   {
     LaunchScope scope(L.prof, KC_ATTN, L.stream, 0, (16.0 + 8.0 + S) * zq * (T * (T + 128.0) / 2));
     const int64_t rows = (int64_t)zq * T, plane = rows * T;
-    if (T <= 256) k_att_sm_fwd<S, 2><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
-    else if (T <= 512) k_att_sm_fwd<S, 4><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
+    if (T <= 512) k_att_sm_fwd<S, 4><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
     else if (T <= 1024) k_att_sm_fwd<S, 8><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
     else k_att_sm_fwd<S, 16><<<rows, 128, 0, L.stream>>>(P, T, b.PA, b.exP, plane);
     SLQ_CUDA(cudaGetLastError());

@@ -51,5 +51,28 @@ __device__ __forceinline__ void digits(double x, int e, int8_t* d) {
   }
 }
 
+// The S digit planes of 4 consecutive values packed into S words (byte k of w[p] = digit p of x[k],
+// two's complement): the magnitudes' digits by shifts, the signs applied to all four bytes at once
+// (per-byte negation (b ^ 0xff) + 1 with __vadd4, no carries between bytes).  Same digits as digits<S>.
+template <int S>
+__device__ __forceinline__ void digits4(const double* x, int e, uint32_t* w) {
+  const double sc = __longlong_as_double((long long)(7 * S - e + 1023) << 52);
+  unsigned long long mag[4];
+  uint32_t neg = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const long long q = __double2ll_rz(x[k] * sc);
+    neg |= (q < 0 ? 0xffu : 0u) << (8 * k);
+    mag[k] = (unsigned long long)(q < 0 ? -q : q);
+  }
+#pragma unroll
+  for (int p = 0; p < S; ++p) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v |= (uint32_t)((mag[k] >> (7 * (S - 1 - p))) & 127u) << (8 * k);
+    w[p] = __vadd4(v ^ neg, neg & 0x01010101u);
+  }
+}
+
 }  // namespace oz
 }  // namespace slq

@@ -963,7 +963,7 @@ void run_planes(const Launch& L, const OzPlanes& A, const OzPlanes& B, const Gem
   o.nbA = A.nb; o.nbB = B.nb; o.z0A = A.z0; o.z0B = B.z0; o.zA = A.z; o.zB = B.z;
   // algorithmic work: the causal half (T + 1) / 2T of the square for the triangular contractions
   const double frac = a.tri == TRI_NONE ? 1.0 : (a.tri == TRI_SKIP_UPPER ? (M + 1.0) / (2.0 * M) : (K + 1.0) / (2.0 * K));
-  LaunchScope scope(L.prof, KC_GEMM_I8, L.stream, 2.0 * M * N * (double)K * a.batch * CF::NPROD * frac,
+  LaunchScope scope(L.prof, KC_ATTN_I8, L.stream, 2.0 * M * N * (double)K * a.batch * CF::NPROD * frac,
                     (double)S * ((double)M * K + (double)N * K) * a.batch * frac + 8.0 * M * N * a.batch);
   const int64_t nwork = (int64_t)a.batch * tiles_b;
   k_oz_gemm<S, BN, BK, NI><<<(int)std::min<int64_t>(nwork, 148), 32 * (CF::NE + NI + 1), CF::SMEM, L.stream>>>(

@@ -6,12 +6,12 @@ import collections
 import csv
 import sys
 
-CLASSES = [("gemm_i8", ("k_oz_gemm",)), ("oz_slice", ("k_oz_slice", "k_oz_colexp")),
+CLASSES = [("gemm_i8", ("k_oz_gemm",)), ("oz_slice", ("k_oz_slice", "k_oz_colexp", "k_att_rows", "k_att_cols")),
            ("gemm", ("gemm_dmma_kernel", "splitk_reduce", "gemm_kernel", "k_tc_")),
-           ("attention", ("softmax",)), ("norm", ("layernorm", "rmsnorm", "colreduce")),
+           ("attention", ("softmax", "k_att_sm")), ("norm", ("layernorm", "rmsnorm", "colreduce")),
            ("cross_entropy", ("cross_entropy",)), ("embedding", ("embed", "pos_bwd")),
            ("perturb", ("perturb",)), ("fd_lanczos", ("k_fd",)), ("reorth", ("reorth", "gram")),
-           ("elementwise", ("rope", "swiglu", "k_add", "convert", "gelu"))]
+           ("elementwise", ("rope", "swiglu", "k_add", "convert", "gelu", "k_oz_act"))]
 
 
 def cls_of(name):
