@@ -60,6 +60,10 @@ struct RowJobs {
 
 constexpr int kRowsPerWarp = 4;
 
+// hd in {32, 64, 128}: each lane owns 4 consecutive values (two 16-byte loads, one packed word per
+// digit plane), LPR = hd / 4 lanes per row, 32 / LPR rows per warp pass, kRowsPerWarp rows per warp
+// (all loads issued before the first reduction); other hd (multiples of 32): vpl = hd / 32 values
+// per lane, one row per warp pass
 template <int S>
 __global__ void __launch_bounds__(256) k_att_rows(const __grid_constant__ RowJobs js) {
   const RowJob& jb = (js.n > 1 && (int)blockIdx.x >= js.j[1].blocks0) ? js.j[1] : js.j[0];
@@ -68,12 +72,58 @@ __global__ void __launch_bounds__(256) k_att_rows(const __grid_constant__ RowJob
   const int lane = threadIdx.x % 32;
   const int nrows = jb.nb * jb.T;
   if (r0 >= nrows) return;
-  const int vpl = jb.hd / 32;  // consecutive values per lane (hd = 32 .. 128)
-  // every row's loads first (kRowsPerWarp x vpl independent loads in flight per lane); the warp's
-  // rows are consecutive positions of one head (T % kRowsPerWarp == 0)
+  // the warp's rows are consecutive positions of one head (T % kRowsPerWarp == 0)
   const int zb = r0 / jb.T, t0 = r0 - zb * jb.T;
   const int b = zb / jb.heads, h = zb - b * jb.heads;
-  const double* xb = jb.X + ((int64_t)b * jb.T + t0) * jb.ld + jb.col0 + (int64_t)h * jb.hd + lane * vpl;
+  const double* xb = jb.X + ((int64_t)b * jb.T + t0) * jb.ld + jb.col0 + (int64_t)h * jb.hd;
+  const int64_t plane = (int64_t)nrows * jb.hd;
+  if (jb.hd == 32 || jb.hd == 64 || jb.hd == 128) {
+    const int lpr = jb.hd / 4, rpp = 32 / lpr;  // lanes per row, rows per pass
+    const int sub = lane / lpr, col = 4 * (lane % lpr);
+    double v[kRowsPerWarp][4];
+#pragma unroll
+    for (int it = 0; it < kRowsPerWarp; ++it) {
+      const int rr = it * rpp + sub;  // (rows beyond kRowsPerWarp: idle lanes)
+      if (rr < kRowsPerWarp) {
+        const double* x = xb + (int64_t)rr * jb.ld + col;
+        const double2 a = *reinterpret_cast<const double2*>(x);
+        const double2 c = *reinterpret_cast<const double2*>(x + 2);
+        v[it][0] = a.x; v[it][1] = a.y; v[it][2] = c.x; v[it][3] = c.y;
+      } else {
+        v[it][0] = v[it][1] = v[it][2] = v[it][3] = 0.0;
+      }
+      if ((it + 1) * rpp >= kRowsPerWarp) break;
+    }
+#pragma unroll
+    for (int it = 0; it < kRowsPerWarp; ++it) {
+      const int rr = it * rpp + sub;
+      double mx = 0.0;
+      bool nf = false;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mx = fmax(mx, fabs(v[it][k]));
+        nf |= nonfinite(v[it][k]);
+      }
+      for (int o = lpr / 2; o > 0; o >>= 1) {  // reduce within the row's lpr lanes
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        nf |= __shfl_xor_sync(0xffffffffu, (int)nf, o) != 0;
+      }
+      if (rr < kRowsPerWarp) {
+        const int r = r0 + rr;
+        const int e = exp_of(mx, nf);
+        if (lane % lpr == 0) jb.ex[r] = e;
+        uint32_t w[S];
+        digits4<S>(v[it], nf ? 0 : e, w);
+        int8_t* o = jb.out + (int64_t)r * jb.hd + col;
+#pragma unroll
+        for (int q = 0; q < S; ++q) *reinterpret_cast<uint32_t*>(o + q * plane) = w[q];
+      }
+      if ((it + 1) * rpp >= kRowsPerWarp) break;
+    }
+    return;
+  }
+  const int vpl = jb.hd / 32;  // consecutive values per lane
+  xb += lane * vpl;
   double v[kRowsPerWarp][4];
 #pragma unroll
   for (int rr = 0; rr < kRowsPerWarp; ++rr) {
@@ -82,7 +132,6 @@ __global__ void __launch_bounds__(256) k_att_rows(const __grid_constant__ RowJob
 #pragma unroll
     for (int i = 0; i < 4; ++i) v[rr][i] = (r < nrows && i < vpl) ? x[lane * vpl + i] : 0.0;
   }
-  const int64_t plane = (int64_t)nrows * jb.hd;
 #pragma unroll
   for (int rr = 0; rr < kRowsPerWarp; ++rr) {
     const int64_t r = r0 + rr;
@@ -104,17 +153,8 @@ __global__ void __launch_bounds__(256) k_att_rows(const __grid_constant__ RowJob
     for (int i = 0; i < 4; ++i) digits<S>(v[rr][i], ed, d[i]);
     int8_t* o = jb.out + r * jb.hd + lane * vpl;
 #pragma unroll
-    for (int q = 0; q < S; ++q) {
-      if (vpl == 2) {
-        *reinterpret_cast<uint16_t*>(o + q * plane) = (uint16_t)((uint8_t)d[0][q] | ((uint8_t)d[1][q] << 8));
-      } else if (vpl == 4) {
-        *reinterpret_cast<uint32_t*>(o + q * plane) = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
-                                                      ((uint32_t)(uint8_t)d[2][q] << 16) |
-                                                      ((uint32_t)(uint8_t)d[3][q] << 24);
-      } else {
-        for (int i = 0; i < vpl; ++i) o[q * plane + i] = d[i][q];
-      }
-    }
+    for (int q = 0; q < S; ++q)
+      for (int i = 0; i < vpl; ++i) o[q * plane + i] = d[i][q];
   }
 }
 
@@ -129,29 +169,35 @@ struct ColJob {
   int* ex;         // [nb][hd]
 };
 
-// 512 threads: pass 1 (column maxima) 16 t-lanes x 32 columns with 8 loads in flight per thread;
-// pass 2 128-deep t chunks through a shared tile, each thread 8 consecutive t of one column
+// One 512-thread CTA per (head, 8 columns): 8 columns x 64 t-lanes (each warp reads 4 rows x 64 B);
+// pass 1 the column maxima (8 loads in flight per thread), pass 2 128-deep t chunks through a
+// shared tile, each thread 2 consecutive t of one column (64 threads write a column's 128 bytes)
+constexpr int kColW = 8;
+
 template <int S>
 __global__ void __launch_bounds__(512) k_att_cols(const __grid_constant__ ColJob jb) {
-  __shared__ double tile[128][33];
-  __shared__ double red[16][33];
-  __shared__ int es[32];
-  const int dblk = jb.hd / 32;
-  const int zb = blockIdx.x / dblk, d0 = (blockIdx.x % dblk) * 32;
+  __shared__ double tile[128][kColW + 1];
+  __shared__ double red[64][kColW + 1];
+  __shared__ int es[kColW];
+  const int dblk = jb.hd / kColW;
+  const int zb = blockIdx.x / dblk, d0 = (blockIdx.x % dblk) * kColW;
   const int b = zb / jb.heads, h = zb % jb.heads;
   const double* x = jb.X + (int64_t)b * jb.T * jb.ld + jb.col0 + (int64_t)h * jb.hd + d0;
   const int* pre = jb.pre ? jb.pre + (int64_t)zb * jb.T : nullptr;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int tx = threadIdx.x % kColW, ty = threadIdx.x / kColW;  // column, t-lane (64)
   auto val = [&](int t) {
     const double v = x[(int64_t)t * jb.ld + tx];
     return pre ? v * scale_of(pre[t]) : v;
   };
   double mx = 0.0;
   bool nf = false;
-  for (int t0 = 0; t0 < jb.T; t0 += 128) {  // T % 128 == 0
+  for (int t0 = 0; t0 < jb.T; t0 += 512) {
     double v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = val(t0 + ty + 16 * i);
+    for (int i = 0; i < 8; ++i) {
+      const int t = t0 + ty + 64 * i;
+      v[i] = t < jb.T ? val(t) : 0.0;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       mx = fmax(mx, fabs(v[i]));
@@ -160,42 +206,33 @@ __global__ void __launch_bounds__(512) k_att_cols(const __grid_constant__ ColJob
   }
   red[ty][tx] = nf ? __longlong_as_double(0x7ff8000000000000ll) : mx;
   __syncthreads();
-  if (ty == 0) {
+  if (threadIdx.x < kColW) {
     double m = 0.0;
     bool bad = false;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      bad |= red[i][tx] != red[i][tx];
-      m = fmax(m, red[i][tx]);
+    for (int i = 0; i < 64; ++i) {
+      bad |= red[i][threadIdx.x] != red[i][threadIdx.x];
+      m = fmax(m, red[i][threadIdx.x]);
     }
     const int e = exp_of(m, bad);
-    es[tx] = e;
-    jb.ex[(int64_t)zb * jb.hd + d0 + tx] = e;
+    es[threadIdx.x] = e;
+    jb.ex[(int64_t)zb * jb.hd + d0 + threadIdx.x] = e;
   }
   __syncthreads();
   const int64_t plane = (int64_t)jb.nb * jb.hd * jb.T;
-  const int dd = threadIdx.x / 16, tq = (threadIdx.x % 16) * 8;
+  const int dd = threadIdx.x / 64, tq = (threadIdx.x % 64) * 2;
   const int ed = es[dd] == kExNaN ? 0 : es[dd];
   int8_t* orow = jb.out + ((int64_t)zb * jb.hd + d0 + dd) * jb.T + tq;
-  for (int t0 = 0; t0 < jb.T; t0 += 128) {
-    double v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = val(t0 + ty + 16 * i);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) tile[ty + 16 * i][tx] = v[i];
+  for (int t0 = 0; t0 < jb.T; t0 += 128) {  // T % 128 == 0
+    const double v0 = val(t0 + ty), v1 = val(t0 + ty + 64);
+    tile[ty][tx] = v0;
+    tile[ty + 64][tx] = v1;
     __syncthreads();
-    uint32_t w[S][2];
+    int8_t d[2][S];
+    digits<S>(tile[tq][dd], ed, d[0]);
+    digits<S>(tile[tq + 1][dd], ed, d[1]);
 #pragma unroll
-    for (int q = 0; q < S; ++q) w[q][0] = w[q][1] = 0u;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int8_t dg[S];
-      digits<S>(tile[tq + j][dd], ed, dg);
-#pragma unroll
-      for (int q = 0; q < S; ++q) w[q][j / 4] |= (uint32_t)(uint8_t)dg[q] << (8 * (j % 4));
-    }
-#pragma unroll
-    for (int q = 0; q < S; ++q) *reinterpret_cast<uint2*>(orow + q * plane + t0) = make_uint2(w[q][0], w[q][1]);
+    for (int q = 0; q < S; ++q)
+      *reinterpret_cast<uint16_t*>(orow + q * plane + t0) = (uint16_t)((uint8_t)d[0][q] | ((uint8_t)d[1][q] << 8));
     __syncthreads();
   }
 }
@@ -296,52 +333,63 @@ __global__ void __launch_bounds__(512, 2) k_att_sm_bwd(const double* __restrict_
   const int64_t zq = blockIdx.x / cpr;
   const int q0 = (blockIdx.x % cpr) * 32;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  double Dr[2];
+  // phase 1, the warp's two rows interleaved (16 loads in flight per lane per sweep)
+  const int qa = q0 + 2 * warp, qb = qa + 1;  // qb = the longer row
+  const double* pr[2] = {P + (zq * T + qa) * (int64_t)T, P + (zq * T + qb) * (int64_t)T};
+  const double* gr[2] = {dP + (zq * T + qa) * (int64_t)T, dP + (zq * T + qb) * (int64_t)T};
+  // (a NaN / inf in P or dP reaches D or max P: both propagate NaN, so no per-element test)
+  double pm[2] = {0.0, 0.0}, Dr[2] = {0.0, 0.0};
+  for (int j0 = 0; j0 <= qb; j0 += 128) {
+    double a[2][4], c[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = j0 + lane + 32 * i;
+        const bool in = j <= qa + u;
+        a[u][i] = in ? pr[u][j] : 0.0;
+        c[u][i] = in ? gr[u][j] : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        pm[u] = nanmax(pm[u], a[u][i]);
+        Dr[u] += a[u][i] * c[u][i];
+      }
+  }
+  double dm[2] = {0.0, 0.0};
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    pm[u] = warp_nanmax(pm[u]);
+    Dr[u] = warp_add(Dr[u]);
+  }
+  for (int j0 = 0; j0 <= qb; j0 += 128) {
+    double a[2][4], c[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = j0 + lane + 32 * i;
+        const bool in = j <= qa + u;
+        a[u][i] = in ? pr[u][j] : 0.0;
+        c[u][i] = in ? gr[u][j] : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dm[u] = fmax(dm[u], fabs(a[u][i] * (c[u][i] - Dr[u])));
+  }
   int rd[2], ed[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const int q = q0 + 2 * warp + u;
-    const double* p = P + (zq * T + q) * (int64_t)T;
-    const double* g = dP + (zq * T + q) * (int64_t)T;
-    double pm = 0.0, D = 0.0;
-    bool nf = false;
-    for (int j0 = 0; j0 <= q; j0 += 128) {
-      double a[4], c[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int j = j0 + lane + 32 * i;
-        a[i] = j <= q ? p[j] : 0.0;
-        c[i] = j <= q ? g[j] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        pm = fmax(pm, a[i]);
-        nf |= nonfinite(a[i]) || nonfinite(c[i]);
-        D += a[i] * c[i];
-      }
-    }
-    pm = warp_fmax(pm);
-    D = warp_add(D);
-    nf = __any_sync(0xffffffffu, nf);
-    double dm = 0.0;
-    for (int j0 = 0; j0 <= q; j0 += 128) {
-      double a[4], c[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int j = j0 + lane + 32 * i;
-        a[i] = j <= q ? p[j] : 0.0;
-        c[i] = j <= q ? g[j] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dm = fmax(dm, fabs(a[i] * (c[i] - D)));
-    }
-    dm = warp_fmax(dm);
-    const int r = exp_of(pm, nf), e = exp_of(dm, nf || nonfinite(D));
+    dm[u] = warp_fmax(dm[u]);
+    const bool nf = nonfinite(pm[u]) || nonfinite(Dr[u]);
+    const int r = exp_of(pm[u], nf), e = exp_of(dm[u], nf);
     if (lane == 0) {
-      exr[zq * T + q] = r;
-      exe[zq * T + q] = e;
+      exr[zq * T + qa + u] = r;
+      exe[zq * T + qa + u] = e;
     }
-    Dr[u] = D;
     rd[u] = r == kExNaN ? 0 : r;
     ed[u] = e == kExNaN ? 0 : e;
   }
@@ -498,7 +546,7 @@ static void launch_rows(const Launch& L, RowJobs js) {
 template <int S>
 static void launch_cols(const Launch& L, const ColJob& j) {
   LaunchScope scope(L.prof, KC_OZ_SLICE, L.stream, 0, (16.0 + S) * (double)j.nb * j.T * j.hd);
-  k_att_cols<S><<<j.nb * (j.hd / 32), 512, 0, L.stream>>>(j);
+  k_att_cols<S><<<j.nb * (j.hd / kColW), 512, 0, L.stream>>>(j);
   SLQ_CUDA(cudaGetLastError());
   ++*L.launches;
 }

@@ -329,27 +329,51 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
         // h is converted to fp64 only after TMEM is released -- the fp64 pipe work (the top stall of
         // the short-K GEMMs) leaves the section in which the next tile's MMAs wait for the
         // accumulators.  (S = 6, 7 would overflow int64 and keep the fp64 drain below.)
-        long long h[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) h[i] = 0;
-#pragma unroll 1
-        for (int g = 0; g < ((o.debug & 8) ? 0 : S); ++g) {
-          uint32_t r0[32];
-          tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) h[i] = h[i] * 128 + (long long)(int)r0[i];
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
-        // v = h 2^(-7(S + 1)): hi 2^32 + lo exactly from two i2d conversions, one rounding in the fma
+        // Short units (K of the unit < kLim): |h| <= K 127^2 2^(7(S-1)) sum_g (g+1) 2^(-7g) < 2^53, so
+        // the same Horner combination is exact in fp64 (one i2d + one DFMA per accumulator value,
+        // about half the int64 instruction count -- the drain is the per-tile period of the
+        // K = 64 attention GEMMs); both branches give the identical integer h.
+        constexpr double kLim = 9007199254740992.0 / (16129.0 * 1.0158 * (double)(1ll << (7 * (S - 1))));
         const double wl = exp2i(-7 * (S + 1));
+        if ((double)nloc * KT < kLim) {
+          double hd[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const double hi = i2d((uint32_t)(int)(h[i] >> 32));
-          const double lo = __hiloint2double(0x43300000, (int)(uint32_t)h[i]) - 4503599627370496.0;
-          v[i] = fma(hi, 4294967296.0, lo) * wl;
+          for (int i = 0; i < 32; ++i) hd[i] = 0.0;
+#pragma unroll 1
+          for (int g = 0; g < ((o.debug & 8) ? 0 : S); ++g) {
+            uint32_t r0[32];
+            tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) hd[i] = fma(hd[i], 128.0, i2d(r0[i]));
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = hd[i] * wl;
+        } else {
+          long long h[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) h[i] = 0;
+#pragma unroll 1
+          for (int g = 0; g < ((o.debug & 8) ? 0 : S); ++g) {
+            uint32_t r0[32];
+            tmem_ld32(tmem + ((uint32_t)lg << 16) + (uint32_t)(g * BN + c0), r0);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) h[i] = h[i] * 128 + (long long)(int)r0[i];
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
+          // v = h 2^(-7(S + 1)): hi 2^32 + lo exactly from two i2d conversions, one rounding in the fma
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const double hi = i2d((uint32_t)(int)(h[i] >> 32));
+            const double lo = __hiloint2double(0x43300000, (int)(uint32_t)h[i]) - 4503599627370496.0;
+            v[i] = fma(hi, 4294967296.0, lo) * wl;
+          }
         }
       } else {
         // two digit-weight groups per TMEM round trip (2 x 32 columns, one wait); the g loop stays
