@@ -982,7 +982,8 @@ void run_planes(const Launch& L, const OzPlanes& A, const OzPlanes& B, const Gem
   }
   const CUtensorMap ta = make_map_i8(A.d, (int64_t)S * A.nb * M, A.Kp, A.Kp, BM, BK);
   const CUtensorMap tb = make_map_i8(B.d, (int64_t)S * B.nb * N, B.Kp, B.Kp, BN, BK);
-  OzArgs o{M, N, nk, nk, 1, A.ex, B.ex, 0, 0};
+  static const int dbg = getenv("SLQ_OZ_DEBUG") ? atoi(getenv("SLQ_OZ_DEBUG")) : 0;  // diagnostic only
+  OzArgs o{M, N, nk, nk, 1, A.ex, B.ex, dbg, 0};
   o.batch = a.batch; o.tri = a.tri; o.tiles_b = tiles_b;
   o.nbA = A.nb; o.nbB = B.nb; o.z0A = A.z0; o.z0B = B.z0; o.zA = A.z; o.zB = B.z;
   // algorithmic work: the causal half (T + 1) / 2T of the square for the triangular contractions
