@@ -111,32 +111,6 @@ __host__ __device__ constexpr int oz_owner(int S, int NI, int g) {
          : S == 6  ? (g == 3 || g == 4 ? 1 : 0)
                    : (g == 2 || g == 3 ? 1 : 0);
 }
-// One 32-row x 4-column chunk of the output tile from the warp's staging tile T (row r, column c
-// at T[r * 4 + c], already row-scaled) for the epilogues that are not plain stores: lane l handles
-// rows 8 j + l / 4 (j = 0..3) of column l % 4, multiplies by its column scale and applies alpha,
-// bias, residual and accumulate.  Activations never reach this epilogue: gemm<double> runs them as
-// a separate streaming pass (gemm_f64.cu, k_oz_act).
-__device__ __noinline__ void oz_epi_chunk(const GemmArgs<double>& p, const double* T, int mrow0, int n0c, int ncol,
-                                          double sc, double* C) {
-  const int lane = threadIdx.x % 32;
-  const int cc = lane & 3;
-  const int n = n0c + cc;
-  if (cc >= ncol) return;
-  const int r0 = lane >> 2;
-  const int mmax = p.M - mrow0 - r0;  // rows 8 j + r0 with 8 j < mmax are valid
-  const double bs = p.bias ? p.bias[n] : 0.0;
-  double* dst = C + (int64_t)(mrow0 + r0) * p.ldc + n;
-  const double* rsd = p.resid ? p.resid + (int64_t)(mrow0 + r0) * p.ldr + n : nullptr;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (8 * j >= mmax) break;
-    double y = p.alpha * (T[(8 * j + r0) * 4 + cc] * sc) + bs;
-    if (rsd) y += rsd[(int64_t)(8 * j) * p.ldr];
-    double* d = dst + (int64_t)(8 * j) * p.ldc;
-    *d = p.accumulate ? *d + y : y;
-  }
-}
-
 // warps: 0 TMA producer, 1 MMA issuer 0 + TMEM allocator, 2 .. NE + 1 epilogue, NE + 2 .. NE + NI
 // the other MMA issuers
 template <int S, int BN, int KT = BK, int NI = 1>
@@ -402,10 +376,12 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
       // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
       // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
       // sectors) instead of 32 rows x 8-16 bytes (register-direct row stores measured 14% slower on
-      // the write-heavy c3 logits GEMM).  Plain stores (split-K partials, or no bias / residual /
-      // accumulate, alpha folded into the row scale) stay inline; the rest is one out-of-line
-      // function per chunk (the kernel must stay inside the instruction cache its MMA-issuing warps
-      // share with the epilogue warps).
+      // the write-heavy c3 logits GEMM).  Lane l stores rows 8 j + l / 4 of column l % 4.  Plain
+      // stores: split-K partials, or no bias / residual / accumulate (alpha folded into the row
+      // scale).  Otherwise y = alpha (x sc) + bias (+ residual) (+ old C): the bias comes from a
+      // register loaded with the scales, and each chunk's residual / old-C values are loaded one
+      // chunk ahead (the out-of-line per-chunk function this replaces serialised 8 dependent global
+      // round trips per tile, which made the bias / residual forward GEMMs epilogue-bound).
       const int ncol = p.N - (n0 + c0);  // valid columns of this warp's 32 (may be <= 0)
       const bool plain = o.splits > 1 || fold;
       double* Wd = o.splits > 1 ? ws + (int64_t)sp * p.M * p.N : p.C + (o.batch > 1 ? boff(p.offC, z) : 0);
@@ -414,6 +390,16 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
       const int cc = lane & 3, r0 = lane >> 2;
       const int mmax = p.M - (m0 + lg) - r0;  // rows 8 j + r0 with 8 j < mmax are valid
       double* dst = Wd + (int64_t)(m0 + lg + r0) * ldw + (n0 + c0 + cc);
+      const double* rsd = (!plain && p.resid) ? p.resid + (int64_t)(m0 + lg + r0) * p.ldr + (n0 + c0 + cc) : nullptr;
+      const double* bsp = (!plain && p.bias) ? p.bias + (n0 + c0 + cc) : nullptr;
+      double rn[4], bn = 0.0;
+      auto fetch = [&](int c) {
+        const bool okc = c + cc < ncol;
+        bn = (bsp && okc) ? bsp[c] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rn[j] = (rsd && okc && 8 * j < mmax) ? rsd[(int64_t)(8 * j) * p.ldr + c] : 0.0;
+      };
+      if (!plain) fetch(0);
 #pragma unroll
       for (int c = 0; c < ((o.debug & 4) ? 0 : 32); c += 4) {
         if (c >= ncol) break;  // (warp-uniform)
@@ -429,7 +415,22 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
               if (8 * j < mmax) dst[(int64_t)(8 * j) * ldw + c] = T[(8 * j + r0) * 4 + cc] * sc;
           }
         } else {
-          oz_epi_chunk(p, T, m0 + lg, n0 + c0 + c, ncol - c, sc, Wd);
+          double y[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            y[j] = p.alpha * (T[(8 * j + r0) * 4 + cc] * sc) + bn;
+            if (rsd) y[j] += rn[j];
+          }
+          if (c + 4 < 32 && c + 4 < ncol) fetch(c + 4);  // next chunk's loads in flight during these stores
+          if (c + cc < ncol) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (8 * j < mmax) {
+                double* d = dst + (int64_t)(8 * j) * ldw + c;
+                *d = p.accumulate ? *d + y[j] : y[j];
+              }
+            }
+          }
         }
       }
     }
