@@ -41,22 +41,32 @@ constexpr int BM = 128, BK = 64, UMMA_K = 32;
 // KT: k-tile width in bytes = int8 elements (64: SWIZZLE_64B, two MMAs per product per k-tile;
 // 32: SWIZZLE_32B, one MMA per product, twice the stages in the same shared memory)
 // NE = BN / 8 epilogue warps: four TMEM lane quadrants x BN / 32 groups of 32 columns
-template <int S, int BN, int KT = BK>
+// TS: plain-epilogue output through per-warp 128B-swizzled shared tiles and TMA stores (8 KB per
+// epilogue warp; the single-k-tile attention GEMMs, whose fp64 stores otherwise bound them)
+template <int S, int BN, int KT = BK, bool TS = false>
 struct Cfg {
   static constexpr int NE = BN / 8;
   static_assert(BN % 32 == 0 && BN >= 64 && BN <= 128, "BN in {64, 96, 128}");
   static constexpr int A_PLANE = BM * KT, B_PLANE = BN * KT;  // bytes
   static constexpr int A_BYTES = S * A_PLANE, B_BYTES = S * B_PLANE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - NE * 128 * 8) / STAGE_BYTES;
+  static constexpr int OUTB = TS ? 8192 : 128 * 8;  // epilogue staging bytes per warp
+  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - NE * OUTB) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
-  static_assert(STAGES >= 2, "two stages at least");
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + NE * 128 * 8 /*epilogue*/;
+  static_assert(STAGES >= (TS ? 1 : 2), "pipeline stages");
+  static constexpr int BAR_BYTES = TS ? 1024 : 256;  // (TS: keeps the staging tiles 1024-byte aligned)
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + BAR_BYTES + NE * OUTB;
   static_assert(SMEM <= 232448, "dynamic shared memory per CTA");
   static constexpr int TMEM_COLS = S * BN <= 128 ? 128 : (S * BN <= 256 ? 256 : 512);
   static constexpr int NPROD = S * (S + 1) / 2;
   static_assert(S * BN <= 512, "S accumulators of BN columns must fit TMEM");
 };
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(map),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
 
 // instruction descriptor, kind::i8: D s32, A and B signed 8-bit, both K-major, M x N
 __host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N) {
@@ -113,12 +123,13 @@ __host__ __device__ constexpr int oz_owner(int S, int NI, int g) {
 }
 // warps: 0 TMA producer, 1 MMA issuer 0 + TMEM allocator, 2 .. NE + 1 epilogue, NE + 2 .. NE + NI
 // the other MMA issuers
-template <int S, int BN, int KT = BK, int NI = 1>
-__global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
+template <int S, int BN, int KT = BK, int NI = 1, bool TS = false>
+__global__ void __launch_bounds__(32 * (Cfg<S, BN, KT, TS>::NE + NI + 1), 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs o,
-              const __grid_constant__ GemmArgs<double> p, double* __restrict__ ws) {
+              const __grid_constant__ GemmArgs<double> p, double* __restrict__ ws,
+              const __grid_constant__ CUtensorMap tmC) {
   static_assert(NI == 1 || (NI == 2 && S >= 5) || (NI == 3 && S == 7), "issuer split defined for S = 5..7");
-  using CF = Cfg<S, BN, KT>;
+  using CF = Cfg<S, BN, KT, TS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES);
@@ -126,7 +137,7 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
   uint64_t* tmem_full = empty + CF::STAGES;
   uint64_t* tmem_empty = tmem_full + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-  double* stage_t = reinterpret_cast<double*>(smem + CF::STAGES * CF::STAGE_BYTES + 256);  // NE x 32 x 4
+  double* stage_t = reinterpret_cast<double*>(smem + CF::STAGES * CF::STAGE_BYTES + CF::BAR_BYTES);  // NE x OUTB
   constexpr int NE = CF::NE;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -373,6 +384,33 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)));
       }
+      if constexpr (TS) {
+        // plain epilogue through TMA stores (host-checked: one split, no bias / residual /
+        // accumulate, the C rows of batch z contiguous at z M): the warp's 32 x 32 block goes to
+        // two [32 rows][16 columns] 128B-swizzled shared tiles (16-byte chunk j of row r at
+        // r 128 + (j ^ (r % 8)) 16), one lane issues the two bulk tensor stores; the tiles are reused
+        // once the previous unit's stores have read them
+        uint8_t* stg = reinterpret_cast<uint8_t*>(stage_t) + (warp - 2) * CF::OUTB;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const double s0 = __shfl_sync(0xffffffffu, sc_l, c), s1 = __shfl_sync(0xffffffffu, sc_l, c + 1);
+          const int box = c >> 4, ch = (c & 15) >> 1;
+          *reinterpret_cast<double2*>(stg + box * 4096 + lane * 128 + ((ch ^ (lane & 7)) << 4)) =
+              make_double2(v[c] * sr * s0, v[c + 1] * sr * s1);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && !(o.debug & 4)) {
+          const int rowg = (o.batch > 1 ? z * p.M : 0) + m0 + lg;
+#pragma unroll
+          for (int box = 0; box < 2; ++box)
+            if (n0 + c0 + 16 * box < p.N) tma_store_2d(&tmC, stg + box * 4096, n0 + c0 + 16 * box, rowg);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+        continue;
+      }
       // Row scale in registers (lane = row); then 4-column chunks go through a per-warp 32 x 4
       // shared tile so that each store instruction writes 8 rows x 32 contiguous bytes (full
       // sectors) instead of 32 rows x 8-16 bytes (register-direct row stores measured 14% slower on
@@ -433,6 +471,9 @@ __global__ void __launch_bounds__(32 * (Cfg<S, BN, KT>::NE + NI + 1), 1)
           }
         }
       }
+    }
+    if constexpr (TS) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -729,7 +770,7 @@ __global__ void __launch_bounds__(256) k_oz_colexp2(const __grid_constant__ Slic
   double mx = 0.0;
   bool nf = false;
   if (r < jb.rows) {
-#pragma unroll 4
+#pragma unroll 8
     for (int k = k0 + ty; k < k1; k += 8) {
       const double x = jb.X[(int64_t)k * jb.ld + r];
       mx = fmax(mx, fabs(x));
@@ -792,24 +833,32 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
 #pragma unroll
         for (int j = 0; j < 4; ++j) x[j] = (k4 + j < jb.K) ? xr[k4 + j] : 0.0;
       }
-      int8_t d[4][S];
+      uint32_t w[S];
+      digits4<S>(x, e, w);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) digits<S>(x[j], e, d[j]);
-#pragma unroll
-      for (int q = 0; q < S; ++q) {
-        const uint32_t w = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
-                           ((uint32_t)(uint8_t)d[2][q] << 16) | ((uint32_t)(uint8_t)d[3][q] << 24);
-        *reinterpret_cast<uint32_t*>(jb.out + q * plane + (int64_t)row * jb.Kp + k4) = w;
-      }
+      for (int q = 0; q < S; ++q) *reinterpret_cast<uint32_t*>(jb.out + q * plane + (int64_t)row * jb.Kp + k4) = w[q];
     }
     return;
   }
-  __shared__ double tile[32][33];
+  // the block's whole 32-row x 128-k tile in one sweep (16 loads in flight per thread), then the
+  // digits of 4 x 4 consecutive k per thread
+  __shared__ double tile[128][33];
   __shared__ int es[32];
   const int rb = (jb.rows + 31) / 32;
   const int r0 = (b % rb) * 32, kblk = b / rb;
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   const int r = r0 + tx;
+  const int kb0 = kblk * 128, kb1 = min(jb.Kp, kb0 + 128);
+  {
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int k = kb0 + ty + 8 * i;
+      x[i] = (r < jb.rows && k < jb.K) ? jb.X[(int64_t)k * jb.ld + r] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) tile[ty + 8 * i][tx] = x[i];
+  }
   if (threadIdx.x < 32) {
     int e = kExNone;
     if (r < jb.rows) {
@@ -819,27 +868,20 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
     if (kblk == 0 && r < jb.rows) jb.ex[r] = e == kExNone ? 0 : e;
     es[threadIdx.x] = (e == kExNone || e == kExNaN) ? 0 : e;  // (digits of a non-finite row are never used)
   }
+  __syncthreads();
   const int wr = threadIdx.x / 8, kq = threadIdx.x % 8;
-  const int kb0 = kblk * 128, kb1 = min(jb.Kp, kb0 + 128);
-  for (int k0 = kb0; k0 < kb1; k0 += 32) {
-    __syncthreads();
+  if (r0 + wr >= jb.rows) return;
+  const int ew = es[wr];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int k = k0 + ty + 8 * i;
-      tile[ty + 8 * i][tx] = (r < jb.rows && k < jb.K) ? jb.X[(int64_t)k * jb.ld + r] : 0.0;
-    }
-    __syncthreads();
-    if (r0 + wr < jb.rows && k0 + 4 * kq < jb.Kp) {
-      int8_t d[4][S];
+  for (int g = 0; g < 4; ++g) {
+    const int kl = 32 * g + 4 * kq;
+    if (kb0 + kl >= kb1) break;
+    const double x[4] = {tile[kl][wr], tile[kl + 1][wr], tile[kl + 2][wr], tile[kl + 3][wr]};
+    uint32_t w[S];
+    digits4<S>(x, ew, w);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) digits<S>(tile[4 * kq + j][wr], es[wr], d[j]);
-#pragma unroll
-      for (int q = 0; q < S; ++q) {
-        const uint32_t w = (uint32_t)(uint8_t)d[0][q] | ((uint32_t)(uint8_t)d[1][q] << 8) |
-                           ((uint32_t)(uint8_t)d[2][q] << 16) | ((uint32_t)(uint8_t)d[3][q] << 24);
-        *reinterpret_cast<uint32_t*>(jb.out + q * plane + (int64_t)(r0 + wr) * jb.Kp + k0 + 4 * kq) = w;
-      }
-    }
+    for (int q = 0; q < S; ++q)
+      *reinterpret_cast<uint32_t*>(jb.out + q * plane + (int64_t)(r0 + wr) * jb.Kp + kb0 + kl) = w[q];
   }
 }
 
@@ -950,7 +992,8 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     if constexpr (W)
       k_oz_gemm_w<<<std::min(nwork, 148), 320, CfgW::SMEM, L.stream>>>(ta, tb, o, a, ws);
     else
-      k_oz_gemm<S, BN, KTN, NI><<<std::min(nwork, 148), 32 * (CF::NE + NI + 1), CF::SMEM, L.stream>>>(ta, tb, o, a, ws);
+      k_oz_gemm<S, BN, KTN, NI><<<std::min(nwork, 148), 32 * (CF::NE + NI + 1), CF::SMEM, L.stream>>>(ta, tb, o, a, ws,
+                                                                                                   ta);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
   }
@@ -964,13 +1007,29 @@ void run(const Launch& L, const GemmArgs<double>& a) {
   }
 }
 
-// batched / causal GEMM over pre-sliced digit planes (the attention path): no slicing, no split-K
-template <int S, int BN, int NI>
+// 2-D fp64 tensor [rows x cols] (row pitch ld elements), box {16, 32}, 128-byte swizzle: the TS
+// epilogue's store map
+static CUtensorMap make_map_f64_store(const double* base, int64_t rows, int64_t cols, int64_t ld) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {16, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(SLQ_ECUDA, "cuTensorMapEncodeTiled (fp64 store) failed: " + std::to_string((int)r));
+  return m;
+}
+
+// batched / causal GEMM over pre-sliced digit planes (the attention path): no slicing, no split-K.
+// TS: the TMA-store epilogue (one pipeline stage; only for plain outputs with contiguous batches)
+template <int S, int BN, int NI, bool TS>
 void run_planes(const Launch& L, const OzPlanes& A, const OzPlanes& B, const GemmArgs<double>& a) {
-  using CF = Cfg<S, BN, BK>;
+  using CF = Cfg<S, BN, BK, TS>;
   static bool attr = false;
   if (!attr) {
-    SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN, BK, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    SLQ_CUDA(cudaFuncSetAttribute(k_oz_gemm<S, BN, BK, NI, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr = true;
   }
   const int M = a.M, N = a.N, K = a.K;
@@ -983,6 +1042,7 @@ void run_planes(const Launch& L, const OzPlanes& A, const OzPlanes& B, const Gem
   }
   const CUtensorMap ta = make_map_i8(A.d, (int64_t)S * A.nb * M, A.Kp, A.Kp, BM, BK);
   const CUtensorMap tb = make_map_i8(B.d, (int64_t)S * B.nb * N, B.Kp, B.Kp, BN, BK);
+  const CUtensorMap tc = TS ? make_map_f64_store(a.C, (int64_t)a.batch * M, N, a.ldc) : ta;
   static const int dbg = getenv("SLQ_OZ_DEBUG") ? atoi(getenv("SLQ_OZ_DEBUG")) : 0;  // diagnostic only
   OzArgs o{M, N, nk, nk, 1, A.ex, B.ex, dbg, 0};
   o.batch = a.batch; o.tri = a.tri; o.tiles_b = tiles_b;
@@ -992,10 +1052,20 @@ void run_planes(const Launch& L, const OzPlanes& A, const OzPlanes& B, const Gem
   LaunchScope scope(L.prof, KC_ATTN_I8, L.stream, 2.0 * M * N * (double)K * a.batch * CF::NPROD * frac,
                     (double)S * ((double)M * K + (double)N * K) * a.batch * frac + 8.0 * M * N * a.batch);
   const int64_t nwork = (int64_t)a.batch * tiles_b;
-  k_oz_gemm<S, BN, BK, NI><<<(int)std::min<int64_t>(nwork, 148), 32 * (CF::NE + NI + 1), CF::SMEM, L.stream>>>(
-      ta, tb, o, a, nullptr);
+  k_oz_gemm<S, BN, BK, NI, TS><<<(int)std::min<int64_t>(nwork, 148), 32 * (CF::NE + NI + 1), CF::SMEM, L.stream>>>(
+      ta, tb, o, a, nullptr, tc);
   SLQ_CUDA(cudaGetLastError());
   ++*L.launches;
+}
+
+template <int S, int BN, int NI>
+void run_planes_sel(const Launch& L, const OzPlanes& A, const OzPlanes& B, const GemmArgs<double>& a) {
+  static const bool ts_off = getenv("SLQ_OZ_NO_TMA_STORE") && atoi(getenv("SLQ_OZ_NO_TMA_STORE")) != 0;  // A/B
+  const bool ts = !ts_off && a.K <= 2 * BK && !a.accumulate && !a.bias && !a.resid && a.offC.inner == 0 &&
+                  a.offC.div == 1 && (a.batch == 1 || (a.offC.outer == (int64_t)a.M * a.ldc && a.M % BM == 0)) &&
+                  (a.ldc % 2) == 0 && (((uintptr_t)a.C) & 15) == 0;
+  if (ts) run_planes<S, BN, NI, true>(L, A, B, a);
+  else run_planes<S, BN, NI, false>(L, A, B, a);
 }
 
 }  // namespace oz
@@ -1055,13 +1125,13 @@ void gemm_oz_planes(const Launch& L, int S, const OzPlanes& A, const OzPlanes& B
   // head-dimension outputs (N <= 128): 128 x 64 tiles; S = 5 otherwise on 128 x 96
   const bool narrow = a.N <= 128;
   switch (S) {
-    case 4: oz::run_planes<4, 64, 1>(L, A, B, a); break;
+    case 4: oz::run_planes_sel<4, 64, 1>(L, A, B, a); break;
     case 5:
-      if (narrow) oz::run_planes<5, 64, 2>(L, A, B, a);
-      else oz::run_planes<5, 96, 2>(L, A, B, a);
+      if (narrow) oz::run_planes_sel<5, 64, 2>(L, A, B, a);
+      else oz::run_planes_sel<5, 96, 2>(L, A, B, a);
       break;
-    case 6: oz::run_planes<6, 64, 2>(L, A, B, a); break;
-    case 7: oz::run_planes<7, 64, 2>(L, A, B, a); break;
+    case 6: oz::run_planes_sel<6, 64, 2>(L, A, B, a); break;
+    case 7: oz::run_planes_sel<7, 64, 2>(L, A, B, a); break;
     default: throw Error(SLQ_EINVAL, "oz planes gemm: S in 4..7");
   }
 }
