@@ -748,6 +748,7 @@ struct SliceJob {
 struct SliceJobs {
   SliceJob j[2];
   int n;
+  int regrow = 1;  // rows path with Kp <= 1024: the row held in registers (0: re-read through L1, A/B)
 };
 constexpr int kColK = 256;     // k extent of one exponent-pass block
 constexpr int kColKMin = 64;   // ... for operands whose exponent pass would not fill two waves of SMs
@@ -803,6 +804,46 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
     const int row = b * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= jb.rows) return;
     const double* xr = jb.X + (int64_t)row * jb.ld;
+    // 16-byte loads when the row base is 16-byte aligned (even pitch, aligned base)
+    const bool v2 = (jb.ld % 2) == 0 && ((uintptr_t)jb.X & 15) == 0;
+    if (v2 && jb.Kp <= 1024 && js.regrow) {
+      // the whole row in registers (4 consecutive k per lane per 128-wide sweep): one read of X
+      double x[8][4];
+      double mx = 0.0;
+      bool nf = false;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k4 = 128 * i + 4 * lane;
+        if (k4 + 3 < jb.K) {
+          const double2 p0 = *reinterpret_cast<const double2*>(xr + k4);
+          const double2 p1 = *reinterpret_cast<const double2*>(xr + k4 + 2);
+          x[i][0] = p0.x; x[i][1] = p0.y; x[i][2] = p1.x; x[i][3] = p1.y;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) x[i][j] = (k4 + j < jb.K) ? xr[k4 + j] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          mx = fmax(mx, fabs(x[i][j]));
+          nf |= nonfinite(x[i][j]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      nf = __any_sync(0xffffffffu, nf);
+      if (lane == 0) jb.ex[row] = exp_of(mx, nf);
+      const int e = nf ? 0 : exp_of(mx);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k4 = 128 * i + 4 * lane;
+        if (k4 >= jb.Kp) break;
+        uint32_t w[S];
+        digits4<S>(x[i], e, w);
+#pragma unroll
+        for (int q = 0; q < S; ++q) *reinterpret_cast<uint32_t*>(jb.out + q * plane + (int64_t)row * jb.Kp + k4) = w[q];
+      }
+      return;
+    }
     constexpr int V = 32;  // values per lane per sweep (1024-wide sweeps)
     double mx = 0.0;
     bool nf = false;
@@ -821,8 +862,6 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
     nf = __any_sync(0xffffffffu, nf);
     if (lane == 0) jb.ex[row] = exp_of(mx, nf);
     const int e = nf ? 0 : exp_of(mx);  // (digits of a non-finite row are never used)
-    // 16-byte loads when the row base is 16-byte aligned (even pitch, aligned base)
-    const bool v2 = (jb.ld % 2) == 0 && ((uintptr_t)jb.X & 15) == 0;
     for (int k4 = lane * 4; k4 < jb.Kp; k4 += 128) {
       double x[4];
       if (v2 && k4 + 3 < jb.K) {
@@ -883,6 +922,95 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
     for (int q = 0; q < S; ++q)
       *reinterpret_cast<uint32_t*>(jb.out + q * plane + (int64_t)(r0 + wr) * jb.Kp + kb0 + kl) = w[q];
   }
+}
+
+// cols-path jobs in ONE pass (exponent and digits together; X read from HBM once instead of twice):
+// a cluster of kSlCS CTAs covers 16 rows x all of K.  CTA c stages k in [c kc, (c + 1) kc) of its 16
+// rows in shared memory with 8-byte cp.async (each 16-row k line is a 128-byte coalesced read), the
+// cluster combines the per-CTA row maxima through distributed shared memory, and every CTA emits the
+// digits of its staged slab, 32 lanes x 4 consecutive k = 128 contiguous bytes of one row per plane.
+// Shared tile [kc][16] with the row slot XOR-swizzled by (k >> 2) & 15, so neither the per-row max
+// sweep nor the 4-consecutive-k digit reads conflict.  Exponents and digits are those of
+// k_oz_colexp2 + k_oz_slice2 (max of |x| over the row, frexp exponent, kExNaN for non-finite rows).
+constexpr int kSlCS = 8, kSlRows = 16, kSlKcMax = 1024;
+static int slcl_kc(int Kp) { return (int)ceil_div(ceil_div(Kp, kSlCS), 16) * 16; }
+
+template <int S>
+__global__ void __cluster_dims__(kSlCS, 1, 1) __launch_bounds__(256)
+    k_oz_slicecl(const __grid_constant__ SliceJobs js, int kc) {
+  extern __shared__ double tile[];  // [kc][16]
+  __shared__ double red[16][17];
+  __shared__ double pm[kSlRows];
+  __shared__ int es[kSlRows];
+  const SliceJob& jb = job_of(js, blockIdx.x);
+  const int b = blockIdx.x - jb.blocks0;  // (blocks0 is a multiple of kSlCS: c is the cluster rank)
+  const int c = b % kSlCS, r0 = (b / kSlCS) * kSlRows, k0 = c * kc;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int r = r0 + tx;
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(tile);
+  for (int k = ty; k < kc; k += 16) {
+    const int kg = k0 + k;
+    const bool ok = r < jb.rows && kg < jb.K;
+    const double* src = ok ? jb.X + (int64_t)kg * jb.ld + r : jb.X;
+    const uint32_t dst = sb + 8u * (uint32_t)(k * 16 + (tx ^ ((k >> 2) & 15)));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  double mx = 0.0;
+  bool nf = false;
+  for (int k = ty; k < kc; k += 16) {  // (this thread's own copies)
+    const double x = tile[k * 16 + (tx ^ ((k >> 2) & 15))];
+    mx = fmax(mx, fabs(x));
+    nf |= nonfinite(x);
+  }
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  red[ty][tx] = nf ? qnan : mx;
+  __syncthreads();
+  if (threadIdx.x < kSlRows) {
+    double m = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      bad |= red[i][threadIdx.x] != red[i][threadIdx.x];
+      m = fmax(m, red[i][threadIdx.x]);
+    }
+    pm[threadIdx.x] = bad ? qnan : m;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (threadIdx.x < kSlRows) {
+    double m = 0.0;
+    bool bad = false;
+    const uint32_t la = (uint32_t)__cvta_generic_to_shared(&pm[threadIdx.x]);
+#pragma unroll
+    for (int q = 0; q < kSlCS; ++q) {
+      uint32_t ra;
+      double v;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(q));
+      asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(ra) : "memory");
+      bad |= v != v;
+      m = fmax(m, v);
+    }
+    const int e = exp_of(m, bad);
+    if (c == 0 && r0 + (int)threadIdx.x < jb.rows) jb.ex[r0 + threadIdx.x] = e;
+    es[threadIdx.x] = bad ? 0 : e;  // (digits of a non-finite row are never used)
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)jb.rows * jb.Kp;
+  const int nq = min(kc, jb.Kp - k0) / 4;  // quads of this CTA's slab inside Kp (Kp, kc multiples of 16)
+  for (int idx = threadIdx.x; idx < kSlRows * nq; idx += 256) {
+    const int rr = idx / nq, q = idx - rr * nq;
+    if (r0 + rr >= jb.rows) break;
+    const int sw = rr ^ (q & 15);
+    const double x[4] = {tile[(4 * q) * 16 + sw], tile[(4 * q + 1) * 16 + sw], tile[(4 * q + 2) * 16 + sw],
+                         tile[(4 * q + 3) * 16 + sw]};
+    uint32_t w[S];
+    digits4<S>(x, es[rr], w);
+#pragma unroll
+    for (int p = 0; p < S; ++p)
+      *reinterpret_cast<uint32_t*>(jb.out + p * plane + (int64_t)(r0 + rr) * jb.Kp + k0 + 4 * q) = w[p];
+  }
+  // no CTA exits while a peer may still read its pm
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 // 2-D int8 tensor [rows x cols] (row pitch ld bytes), box {64, box_rows}, 64-byte swizzle
@@ -949,10 +1077,51 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     LaunchScope scope(L.prof, KC_OZ_SLICE, L.stream, 0, (8.0 + S) * ((double)M * K + (double)N * K));
     // A(m, k): K-contiguous when sAk == 1 (rows = M, pitch sAm), else stored [K x M] with pitch sAk;
     // B(k, n) = B[k * sBk + n * sBn]: K-contiguous rows per n when sBk == 1 (pitch sBn)
+    static const int regrow = getenv("SLQ_OZ_SLICE_L1") ? 0 : 1;  // A/B switch
     SliceJobs js;
     js.n = 2;
+    js.regrow = regrow;
     js.j[0] = SliceJob{a.A, a.sAk == 1 ? a.sAm : a.sAk, M, K, Kp, a.sAk == 1 ? 1 : 0, as, ea, xpa, 0, col_kblk(M, K)};
     js.j[1] = SliceJob{a.B, a.sBk == 1 ? a.sBn : a.sBk, N, K, Kp, a.sBk == 1 ? 1 : 0, bs, eb, xpb, 0, col_kblk(N, K)};
+    static const bool twopass = getenv("SLQ_OZ_SLICE_TWOPASS") != nullptr;  // A/B switch
+    const int kc = slcl_kc(Kp);
+    if (!twopass && kc <= kSlKcMax) {
+      // cols-path jobs: one fused cluster launch; rows-path jobs: k_oz_slice2
+      static bool cl_attr = false;
+      if (!cl_attr) {
+        SLQ_CUDA(cudaFuncSetAttribute(k_oz_slicecl<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSlKcMax * kSlRows * 8));
+        cl_attr = true;
+      }
+      SliceJobs jc, jr;
+      jc.n = jr.n = 0;
+      jr.regrow = regrow;
+      int ncl = 0, nr = 0;
+      for (int i = 0; i < 2; ++i) {
+        SliceJob jj = js.j[i];
+        if (jj.kmajor) {
+          jj.blocks0 = nr;
+          nr += (int)ceil_div(jj.rows, 8);
+          jr.j[jr.n++] = jj;
+        } else {
+          jj.blocks0 = ncl;
+          ncl += (int)ceil_div(jj.rows, kSlRows) * kSlCS;
+          jc.j[jc.n++] = jj;
+        }
+      }
+      if (ncl > 0) {
+        if (jc.n == 1) jc.j[1] = jc.j[0];
+        k_oz_slicecl<S><<<ncl, 256, (size_t)kc * kSlRows * 8, L.stream>>>(jc, kc);
+        SLQ_CUDA(cudaGetLastError());
+        ++*L.launches;
+      }
+      if (nr > 0) {
+        if (jr.n == 1) jr.j[1] = jr.j[0];
+        k_oz_slice2<S><<<nr, 256, 0, L.stream>>>(jr);
+        SLQ_CUDA(cudaGetLastError());
+        ++*L.launches;
+      }
+    } else {
     // exponent pass (cols-path jobs only)
     int nexp = 0;
     SliceJobs je;
@@ -978,6 +1147,7 @@ void run(const Launch& L, const GemmArgs<double>& a) {
     k_oz_slice2<S><<<nsl, 256, 0, L.stream>>>(js);
     SLQ_CUDA(cudaGetLastError());
     ++*L.launches;
+    }
   }
   const CUtensorMap ta = make_map_i8(as, (int64_t)S * M, Kp, Kp, BM, KT);
   const CUtensorMap tb = make_map_i8(bs, (int64_t)S * N, Kp, Kp, BN, KT);

@@ -30,12 +30,14 @@ from paper_2602_00816_b200 import slq  # noqa: E402
 
 @pytest.mark.parametrize("M,N,K,ak,bk", [(128, 64, 64, 1, 1), (300, 70, 100, 1, 1), (2048, 768, 256, 1, 1),
                                          (2048, 256, 1024, 1, 0), (768, 256, 2048, 0, 0), (37, 203, 64, 0, 1),
-                                         (1, 5, 3, 1, 1), (129, 65, 4000, 1, 1), (64, 4096, 20000, 1, 1)])
+                                         (1, 5, 3, 1, 1), (129, 65, 4000, 1, 1), (64, 4096, 20000, 1, 1),
+                                         (100, 50, 8192, 0, 0), (130, 70, 8200, 0, 0), (33, 17, 900, 0, 1)])
 @pytest.mark.parametrize("S", [4, 5, 6, 7])
 def test_oz_gemm_error_bound(M, N, K, ak, bk, S):
     """Truncated digits only: |C_oz - C| <= (S + 2) 2^-7S K 2^(e_i + f_j) (oz_gemm.cu header) and
     2^e_i < 2 max|A_i.|, so <= 4 (S + 2) 2^-7S K max|A_i.| max|B_.j|; covers ragged tiles, every
-    operand layout, split-K and the K cap that keeps INT32 exact."""
+    operand layout, split-K and the K cap that keeps INT32 exact; the cols-path operands (ak / bk = 0)
+    go through the fused cluster slicing up to K = 8192 (8 CTAs x 1024 k) and the two-pass slicing above."""
     err, tf = slq.oz_check(M, N, K, bool(ak), bool(bk), S, iters=1)
     bound = 4 * (S + 2) * 2.0 ** (-7 * S)
     print(f"oz S={S} {M}x{N}x{K} ak={ak} bk={bk}: err {err:.2e} (bound {bound:.1e}), {tf:.1f} TFLOP/s")
