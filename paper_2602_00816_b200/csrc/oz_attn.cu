@@ -237,6 +237,67 @@ __global__ void __launch_bounds__(512) k_att_cols(const __grid_constant__ ColJob
   }
 }
 
+// The same output with ONE read of X: the CTA's whole 8-column x T strip is staged in shared memory
+// by 8-byte cp.async (16 loads in flight per thread at T = 1024), then the column maxima and the
+// digits come from shared memory.  Strip [T][kColW + 1] (padded rows).  T <= 2048.
+template <int S>
+__global__ void __launch_bounds__(512) k_att_cols1(const __grid_constant__ ColJob jb) {
+  extern __shared__ double strip[];  // [T][kColW + 1]
+  __shared__ double red[64][kColW + 1];
+  __shared__ int es[kColW];
+  constexpr int LDS = kColW + 1;
+  const int dblk = jb.hd / kColW;
+  const int zb = blockIdx.x / dblk, d0 = (blockIdx.x % dblk) * kColW;
+  const int b = zb / jb.heads, h = zb % jb.heads;
+  const double* x = jb.X + (int64_t)b * jb.T * jb.ld + jb.col0 + (int64_t)h * jb.hd + d0;
+  const int* pre = jb.pre ? jb.pre + (int64_t)zb * jb.T : nullptr;
+  const int tx = threadIdx.x % kColW, ty = threadIdx.x / kColW;  // column, t-lane (64)
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(strip);
+  for (int t = ty; t < jb.T; t += 64)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + 8u * (uint32_t)(t * LDS + tx)),
+                 "l"(x + (int64_t)t * jb.ld + tx)
+                 : "memory");
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  auto val = [&](int t, int c) {
+    const double v = strip[t * LDS + c];
+    return pre ? v * scale_of(pre[t]) : v;
+  };
+  double mx = 0.0;
+  bool nf = false;
+  for (int t = ty; t < jb.T; t += 64) {
+    const double v = val(t, tx);
+    mx = fmax(mx, fabs(v));
+    nf |= nonfinite(v);
+  }
+  red[ty][tx] = nf ? __longlong_as_double(0x7ff8000000000000ll) : mx;
+  __syncthreads();
+  if (threadIdx.x < kColW) {
+    double m = 0.0;
+    bool bad = false;
+    for (int i = 0; i < 64; ++i) {
+      bad |= red[i][threadIdx.x] != red[i][threadIdx.x];
+      m = fmax(m, red[i][threadIdx.x]);
+    }
+    const int e = exp_of(m, bad);
+    es[threadIdx.x] = e;
+    jb.ex[(int64_t)zb * jb.hd + d0 + threadIdx.x] = e;
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)jb.nb * jb.hd * jb.T;
+  const int dd = threadIdx.x / 64, tq = (threadIdx.x % 64) * 2;
+  const int ed = es[dd] == kExNaN ? 0 : es[dd];
+  int8_t* orow = jb.out + ((int64_t)zb * jb.hd + d0 + dd) * jb.T + tq;
+  for (int t0 = 0; t0 < jb.T; t0 += 128) {  // T % 128 == 0
+    int8_t d[2][S];
+    digits<S>(val(t0 + tq, dd), ed, d[0]);
+    digits<S>(val(t0 + tq + 1, dd), ed, d[1]);
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      *reinterpret_cast<uint16_t*>(orow + q * plane + t0) = (uint16_t)((uint8_t)d[0][q] | ((uint8_t)d[1][q] << 8));
+  }
+}
+
 // ---- forward softmax: S -> P in place (causal, zeros up to the end of the diagonal 128-column
 // block, as k_softmax_causal) and P's row digits (row exponent r_q of max_k P_qk = 1 / sum) ----
 // one 128-thread block per row (as k_softmax_causal_blk): the row is read once into registers
@@ -545,6 +606,21 @@ static void launch_rows(const Launch& L, RowJobs js) {
 
 template <int S>
 static void launch_cols(const Launch& L, const ColJob& j) {
+  static const bool twopass = getenv("SLQ_OZ_SLICE_TWOPASS") != nullptr;  // A/B switch
+  if (!twopass && j.T <= 2048) {
+    LaunchScope scope(L.prof, KC_OZ_SLICE, L.stream, 0, (8.0 + S) * (double)j.nb * j.T * j.hd);
+    const size_t smem = (size_t)j.T * (kColW + 1) * 8;
+    static bool attr = false;
+    if (!attr) {
+      SLQ_CUDA(cudaFuncSetAttribute(k_att_cols1<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2048 * (kColW + 1) * 8));
+      attr = true;
+    }
+    k_att_cols1<S><<<j.nb * (j.hd / kColW), 512, smem, L.stream>>>(j);
+    SLQ_CUDA(cudaGetLastError());
+    ++*L.launches;
+    return;
+  }
   LaunchScope scope(L.prof, KC_OZ_SLICE, L.stream, 0, (16.0 + S) * (double)j.nb * j.T * j.hd);
   k_att_cols<S><<<j.nb * (j.hd / kColW), 512, 0, L.stream>>>(j);
   SLQ_CUDA(cudaGetLastError());
