@@ -925,41 +925,43 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
 }
 
 // cols-path jobs in ONE pass (exponent and digits together; X read from HBM once instead of twice):
-// a cluster of kSlCS CTAs covers 16 rows x all of K.  CTA c stages k in [c kc, (c + 1) kc) of its 16
-// rows in shared memory with 8-byte cp.async (each 16-row k line is a 128-byte coalesced read), the
+// a cluster of kSlCS CTAs covers 8 rows x all of K.  CTA c stages k in [c kc, (c + 1) kc) of its 8
+// rows in shared memory with 8-byte cp.async (each 8-row k line is a 64-byte coalesced read), the
 // cluster combines the per-CTA row maxima through distributed shared memory, and every CTA emits the
 // digits of its staged slab, 32 lanes x 4 consecutive k = 128 contiguous bytes of one row per plane.
-// Shared tile [kc][16] with the row slot XOR-swizzled by (k >> 2) & 15, so neither the per-row max
-// sweep nor the 4-consecutive-k digit reads conflict.  Exponents and digits are those of
-// k_oz_colexp2 + k_oz_slice2 (max of |x| over the row, frexp exponent, kExNaN for non-finite rows).
-constexpr int kSlCS = 8, kSlRows = 16, kSlKcMax = 1024;
+// Shared tile [kc][8] with the row slot XOR-swizzled by (k >> 2) & 7 (the digit reads of 16 lanes
+// then hit 8 distinct slots: at most 2-way conflicts).  8 rows (64 KB at kc = 1024) keep three CTAs
+// per SM, so one CTA's digit phase overlaps the others' loads (16 rows / 128 KB ran at 1.7 TB/s).
+// Exponents and digits are those of k_oz_colexp2 + k_oz_slice2 (max of |x| over the row, frexp exponent, kExNaN for non-finite rows).
+constexpr int kSlCS = 8, kSlRows = 8, kSlKcMax = 1024;
 static int slcl_kc(int Kp) { return (int)ceil_div(ceil_div(Kp, kSlCS), 16) * 16; }
 
 template <int S>
 __global__ void __cluster_dims__(kSlCS, 1, 1) __launch_bounds__(256)
     k_oz_slicecl(const __grid_constant__ SliceJobs js, int kc) {
-  extern __shared__ double tile[];  // [kc][16]
-  __shared__ double red[16][17];
+  extern __shared__ double tile[];  // [kc][kSlRows]
+  __shared__ double red[256 / kSlRows][kSlRows + 1];
   __shared__ double pm[kSlRows];
   __shared__ int es[kSlRows];
   const SliceJob& jb = job_of(js, blockIdx.x);
   const int b = blockIdx.x - jb.blocks0;  // (blocks0 is a multiple of kSlCS: c is the cluster rank)
   const int c = b % kSlCS, r0 = (b / kSlCS) * kSlRows, k0 = c * kc;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  constexpr int NY = 256 / kSlRows;  // k lines per sweep
+  const int tx = threadIdx.x % kSlRows, ty = threadIdx.x / kSlRows;
   const int r = r0 + tx;
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(tile);
-  for (int k = ty; k < kc; k += 16) {
+  for (int k = ty; k < kc; k += NY) {
     const int kg = k0 + k;
     const bool ok = r < jb.rows && kg < jb.K;
     const double* src = ok ? jb.X + (int64_t)kg * jb.ld + r : jb.X;
-    const uint32_t dst = sb + 8u * (uint32_t)(k * 16 + (tx ^ ((k >> 2) & 15)));
+    const uint32_t dst = sb + 8u * (uint32_t)(k * kSlRows + (tx ^ ((k >> 2) & (kSlRows - 1))));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   double mx = 0.0;
   bool nf = false;
-  for (int k = ty; k < kc; k += 16) {  // (this thread's own copies)
-    const double x = tile[k * 16 + (tx ^ ((k >> 2) & 15))];
+  for (int k = ty; k < kc; k += NY) {  // (this thread's own copies)
+    const double x = tile[k * kSlRows + (tx ^ ((k >> 2) & (kSlRows - 1)))];
     mx = fmax(mx, fabs(x));
     nf |= nonfinite(x);
   }
@@ -970,7 +972,7 @@ __global__ void __cluster_dims__(kSlCS, 1, 1) __launch_bounds__(256)
     double m = 0.0;
     bool bad = false;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < NY; ++i) {
       bad |= red[i][threadIdx.x] != red[i][threadIdx.x];
       m = fmax(m, red[i][threadIdx.x]);
     }
@@ -1000,9 +1002,9 @@ __global__ void __cluster_dims__(kSlCS, 1, 1) __launch_bounds__(256)
   for (int idx = threadIdx.x; idx < kSlRows * nq; idx += 256) {
     const int rr = idx / nq, q = idx - rr * nq;
     if (r0 + rr >= jb.rows) break;
-    const int sw = rr ^ (q & 15);
-    const double x[4] = {tile[(4 * q) * 16 + sw], tile[(4 * q + 1) * 16 + sw], tile[(4 * q + 2) * 16 + sw],
-                         tile[(4 * q + 3) * 16 + sw]};
+    const int sw = rr ^ (q & (kSlRows - 1));
+    const double x[4] = {tile[(4 * q) * kSlRows + sw], tile[(4 * q + 1) * kSlRows + sw],
+                         tile[(4 * q + 2) * kSlRows + sw], tile[(4 * q + 3) * kSlRows + sw]};
     uint32_t w[S];
     digits4<S>(x, es[rr], w);
 #pragma unroll
