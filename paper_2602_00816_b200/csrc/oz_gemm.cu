@@ -936,9 +936,8 @@ __global__ void __launch_bounds__(256) k_oz_slice2(const __grid_constant__ Slice
 constexpr int kSlCS = 8, kSlRows = 8, kSlKcMax = 1024;
 static int slcl_kc(int Kp) { return (int)ceil_div(ceil_div(Kp, kSlCS), 16) * 16; }
 
-template <int S>
-__global__ void __cluster_dims__(kSlCS, 1, 1) __launch_bounds__(256)
-    k_oz_slicecl(const __grid_constant__ SliceJobs js, int kc) {
+template <int S, int kSlRows, int kSlCS>
+__device__ __forceinline__ void slicecl_body(const SliceJobs& js, int kc) {
   extern __shared__ double tile[];  // [kc][kSlRows]
   __shared__ double red[256 / kSlRows][kSlRows + 1];
   __shared__ double pm[kSlRows];
@@ -1013,6 +1012,20 @@ __global__ void __cluster_dims__(kSlCS, 1, 1) __launch_bounds__(256)
   }
   // no CTA exits while a peer may still read its pm
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int S>
+__global__ void __cluster_dims__(kSlCS, 1, 1) __launch_bounds__(256)
+    k_oz_slicecl(const __grid_constant__ SliceJobs js, int kc) {
+  slicecl_body<S, kSlRows, kSlCS>(js, kc);
+}
+
+// opt-in form (SLQ_OZ_SLICE_CS16=1): 16 rows (128-byte k-line segments) over a non-portable cluster of
+// 16 CTAs, 64 KB slabs at K = 8192; cluster dimension given at launch
+constexpr int kSl16Rows = 16, kSl16CS = 16, kSl16KcMax = 512;
+template <int S>
+__global__ void __launch_bounds__(256) k_oz_slicecl16(const __grid_constant__ SliceJobs js, int kc) {
+  slicecl_body<S, kSl16Rows, kSl16CS>(js, kc);
 }
 
 // 2-D int8 tensor [rows x cols] (row pitch ld bytes), box {64, box_rows}, 64-byte swizzle
@@ -1113,7 +1126,46 @@ void run(const Launch& L, const GemmArgs<double>& a) {
       }
       if (ncl > 0) {
         if (jc.n == 1) jc.j[1] = jc.j[0];
-        k_oz_slicecl<S><<<ncl, 256, (size_t)kc * kSlRows * 8, L.stream>>>(jc, kc);
+        static const bool cs16 = getenv("SLQ_OZ_SLICE_CS16") && atoi(getenv("SLQ_OZ_SLICE_CS16")) != 0;
+        static int cs16_ok = -1;  // the 16-CTA cluster of 64 KB slabs fits (cudaOccupancyMaxActiveClusters)
+        const int kc16 = (int)ceil_div(ceil_div(Kp, kSl16CS), 16) * 16;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        if (cs16 && kc16 <= kSl16KcMax) {
+          cfg.blockDim = dim3(256);
+          cfg.dynamicSmemBytes = (size_t)kc16 * kSl16Rows * 8;
+          cfg.stream = L.stream;
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = kSl16CS;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          if (cs16_ok < 0) {
+            SLQ_CUDA(cudaFuncSetAttribute(k_oz_slicecl16<S>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            SLQ_CUDA(cudaFuncSetAttribute(k_oz_slicecl16<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kSl16KcMax * kSl16Rows * 8));
+            cfg.gridDim = dim3(kSl16CS);
+            cfg.dynamicSmemBytes = (size_t)kSl16KcMax * kSl16Rows * 8;
+            int nclu = 0;
+            cs16_ok = cudaOccupancyMaxActiveClusters(&nclu, k_oz_slicecl16<S>, &cfg) == cudaSuccess && nclu > 0;
+            (void)cudaGetLastError();
+            cfg.dynamicSmemBytes = (size_t)kc16 * kSl16Rows * 8;
+          }
+        }
+        if (cs16 && kc16 <= kSl16KcMax && cs16_ok == 1) {
+          SliceJobs j16 = jc;
+          int n16 = 0;
+          for (int i = 0; i < j16.n; ++i) {
+            j16.j[i].blocks0 = n16;
+            n16 += (int)ceil_div(j16.j[i].rows, kSl16Rows) * kSl16CS;
+          }
+          if (j16.n == 1) j16.j[1] = j16.j[0];
+          cfg.gridDim = dim3(n16);
+          SLQ_CUDA(cudaLaunchKernelEx(&cfg, k_oz_slicecl16<S>, j16, kc16));
+        } else {
+          k_oz_slicecl<S><<<ncl, 256, (size_t)kc * kSlRows * 8, L.stream>>>(jc, kc);
+        }
         SLQ_CUDA(cudaGetLastError());
         ++*L.launches;
       }
